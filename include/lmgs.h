@@ -1,0 +1,159 @@
+/*
+ * lmgs — B200-native (sm_100a) 3D Gaussian splatting forward rasterizer.
+ * C ABI: plain pointers and sizes, no torch types.  All Gaussian / frame
+ * pointers are DEVICE pointers unless the entry point says "host".
+ *
+ * Reference interfaces each entry point replaces (paths under
+ * /root/reference/pkg/src/landmark/):
+ *
+ *   lmgs_render            gaussian_core.py:582-597  render_image(model, camera,
+ *                          tile_size, background, with_record, subset)
+ *                          = project_splats (187-230) + rasterize (340-403);
+ *                          also the engine runtime switch
+ *                          engine_api.py:291-299 Engine._render_gaussian
+ *   lmgs_project           gaussian_core.py:187-230  project_splats (+ eval_sh_colors 129-142)
+ *   lmgs_copy_instances    gaussian_core.py:256-263  TileRecord.order for every tile
+ *                          (the per-tile lists the reference builds at 362-392)
+ *   lmgs_render_batch      render_runtime.py:250-308 run_session's per-pose loop,
+ *                          batched over camera views on one device
+ *   lmgs_composite_blocks  (new) front-to-back "over" of per-block premultiplied
+ *                          images; replaces render_runtime.py:189-191 (BlockSession
+ *                          concatenating resident cells into one model)
+ *
+ * Error behaviour: every entry point returns an lmgs_status; on failure
+ * lmgs_last_error(ctx) holds a message.  Bad arguments map to the reference's
+ * InvalidInputError / ShapeError in the Python wrapper (common.py:14-31).
+ *
+ * Threading: a context is bound to one device; calls on one context must be
+ * serialised (use one context per concurrently-rendering stream).
+ */
+#ifndef LMGS_H_
+#define LMGS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LMGS_ABI_VERSION 1
+
+typedef enum lmgs_status {
+  LMGS_OK = 0,
+  LMGS_ERR_INVALID = 1,     /* bad argument (shape, size, null pointer)   */
+  LMGS_ERR_CUDA = 2,        /* CUDA runtime error                         */
+  LMGS_ERR_OOM = 3,         /* device allocation failed                   */
+  LMGS_ERR_UNSUPPORTED = 4  /* e.g. tile_size > 64                        */
+} lmgs_status;
+
+typedef struct lmgs_context lmgs_context;
+
+/* One pinhole view.  r_wc rows = (right, down, forward); center = -r_wc^T t_wc
+ * and lim_x/lim_y = 1.3*max(cx, W-cx)/fx (gaussian_core.py:208-209) are
+ * computed on the host in fp64 exactly as the reference does, and reach the
+ * kernels as launch arguments (constant bank). */
+typedef struct lmgs_camera {
+  double r_wc[9];
+  double t_wc[3];
+  double center[3];
+  double fx, fy, cx, cy;
+  double lim_x, lim_y;
+  int32_t width, height;
+} lmgs_camera;
+
+/* Structure-of-arrays Gaussian set, fp32, contiguous (GaussianModel,
+ * gaussian_core.py:34-61).  sh: [count, sh_coeffs, 3]. */
+typedef struct lmgs_gaussians {
+  const float* means;           /* [count,3]                       */
+  const float* quats;           /* [count,4] (w,x,y,z), unit       */
+  const float* scales;          /* [count,3] > 0, linear           */
+  const float* opacity_logits;  /* [count]                         */
+  const float* sh;              /* [count, sh_coeffs, 3]           */
+  const int64_t* prim_ids;      /* [count] ascending original ids (render_image's
+                                   `subset`, 593-595) or NULL = row index        */
+  int64_t count;
+  int32_t sh_degree;            /* model degree, sh_coeffs == (sh_degree+1)^2 */
+  int32_t sh_coeffs;
+} lmgs_gaussians;
+
+typedef struct lmgs_settings {
+  int32_t tile_size;       /* >= 1, <= 64 (reference default 16)             */
+  int32_t sh_eval_degree;  /* 1 = reference eval_sh_colors; 3 = full degree 3 */
+  float background[3];
+  uint32_t flags;          /* LMGS_FLAG_*                                    */
+} lmgs_settings;
+
+#define LMGS_FLAG_STAGE_TIMES 1u  /* record per-stage CUDA events (lmgs_get_stats) */
+
+/* Per-view outputs (device).  rgb is required; the rest may be NULL. */
+typedef struct lmgs_frame {
+  float* rgb;             /* [H,W,3] image incl. T_final * background          */
+  float* alpha;           /* [H,W]   1 - T_final                               */
+  float* depth;           /* [H,W]   sum_i w_i z_i (not in the reference)      */
+  float* transmittance;   /* [H,W]   T_final (for block compositing)           */
+  int32_t* touched;       /* [count] pixels with w > 0 per Gaussian (0 if culled) */
+  uint8_t* kept;          /* [count] 1 if z > 0.01 (near cull, 196-198)        */
+  int32_t* tile_ranges;   /* [T,2]   [start,end) of each tile's instance list  */
+  int32_t* n_processed;   /* [T]     blend break index per tile (324-325)      */
+} lmgs_frame;
+
+#define LMGS_MAX_STAGES 8
+
+typedef struct lmgs_stats {
+  int64_t n_gaussians;
+  int64_t n_kept;            /* M */
+  int64_t n_instances;       /* K */
+  int32_t n_tiles;           /* T */
+  int32_t tiles_x, tiles_y;
+  int32_t n_stages;
+  float stage_ms[LMGS_MAX_STAGES];  /* valid with LMGS_FLAG_STAGE_TIMES */
+  const char* stage_names[LMGS_MAX_STAGES];
+} lmgs_stats;
+
+int lmgs_abi_version(void);
+int lmgs_context_create(int device, lmgs_context** out);
+void lmgs_context_destroy(lmgs_context* ctx);
+const char* lmgs_last_error(const lmgs_context* ctx);
+
+/* Render one view; stream is a cudaStream_t (NULL = legacy default stream).
+ * Returns after the instance count is known (one device->host read of K);
+ * the image kernels are enqueued on `stream` and not waited for. */
+int lmgs_render(lmgs_context* ctx, const lmgs_gaussians* g, const lmgs_camera* cam,
+                const lmgs_settings* s, const lmgs_frame* out, void* stream);
+
+/* Render n_views views of the same Gaussians; out[v] receives view v. */
+int lmgs_render_batch(lmgs_context* ctx, const lmgs_gaussians* g, const lmgs_camera* cams,
+                      int32_t n_views, const lmgs_settings* s, const lmgs_frame* out,
+                      void* stream);
+
+/* Statistics of the last lmgs_render on this context (stage times require the
+ * stream to have completed: call after synchronising). */
+int lmgs_get_stats(lmgs_context* ctx, lmgs_stats* out);
+
+/* Copy the last render's sorted tile instances: keys[K] = tile << 32 | depth
+ * rank, prim_ids[K] = original Gaussian id (TileRecord.order mapped through
+ * splats.prim_id).  Either pointer may be NULL.  Device buffers, K entries. */
+int lmgs_copy_instances(lmgs_context* ctx, uint64_t* keys, int64_t* prim_ids, void* stream);
+
+/* Stage K1 alone (project_splats): per input Gaussian, fp64 geometry.
+ * mean2d [count,2], cov2d [count,3] = (c00,c01,c11) incl. the 0.3 floor,
+ * depth [count], radius [count], colors [count,3] (fp32), opacity [count]
+ * (fp32), kept [count]; values of culled Gaussians are unspecified. */
+int lmgs_project(lmgs_context* ctx, const lmgs_gaussians* g, const lmgs_camera* cam,
+                 const lmgs_settings* s, double* mean2d, double* cov2d, double* depth,
+                 double* radius, float* colors, float* opacity, uint8_t* kept, void* stream);
+
+/* Front-to-back composite of n_blocks per-block renders (background 0):
+ * rgb_b premultiplied [H*W*3], trans_b [H*W] (T_final), depth_b [H*W]
+ * (nullable), stacked block-major: rgb[b*H*W*3 ...].  order[n_blocks] lists
+ * block indices front to back.  out_rgb = sum_b (prod_{b'<b} T_b') C_b +
+ * (prod T) bg; out_alpha = 1 - prod T; out_depth likewise (nullable). */
+int lmgs_composite_blocks(const float* rgb, const float* trans, const float* depth,
+                          int32_t n_blocks, const int32_t* order_host, int64_t n_pixels,
+                          const float* background_host, float* out_rgb, float* out_alpha,
+                          float* out_depth, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LMGS_H_ */

@@ -1,0 +1,178 @@
+"""Camera-batch renderer: many views of one device-resident scene.
+
+The per-pose loop of the reference's render sessions (render_runtime.py:250-308,
+``run_session``) batched on one device.  Each view needs one device->host read
+of its instance count K; two contexts on two streams alternate views so that
+while the host waits for view v's K the GPU is still sorting / blending view
+v-1, keeping the device busy.  The batch joins back onto the caller's stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+
+import numpy as np
+import torch
+
+from . import _lib
+from .raster import GaussianModel, _ptr, abi_camera, abi_settings
+
+KERNELS_PER_VIEW = 19  # preprocess 1, depth sort 10, scan 1, duplicate 1, tile sort 4, ranges 1, blend 1
+
+
+class BatchRenderer:
+    def __init__(self, model: GaussianModel, width: int, height: int, max_views: int,
+                 tile_size: int = 16, sh_eval_degree: int = 3, background=(0.0, 0.0, 0.0),
+                 with_touched: bool = True, n_streams: int = 2):
+        self.model = model
+        self.dev = model.device
+        self.w, self.h, self.ts = int(width), int(height), int(tile_size)
+        self.tx, self.ty = -(-self.w // self.ts), -(-self.h // self.ts)
+        self.max_views = int(max_views)
+        self.sh_eval_degree = int(sh_eval_degree)
+        self.background = background
+        dev = self.dev
+        v = self.max_views
+        self.rgb = torch.empty((v, self.h, self.w, 3), dtype=torch.float32, device=dev)
+        self.alpha = torch.empty((v, self.h, self.w), dtype=torch.float32, device=dev)
+        self.depth = torch.empty((v, self.h, self.w), dtype=torch.float32, device=dev)
+        self.ranges = torch.empty((v, self.tx * self.ty, 2), dtype=torch.int32, device=dev)
+        self.nproc = torch.empty((v, self.tx * self.ty), dtype=torch.int32, device=dev)
+        n = model.count
+        self.touched = torch.empty((v, n), dtype=torch.int32, device=dev) if with_touched else None
+        self.kept = torch.empty((v, n), dtype=torch.uint8, device=dev)
+        self.ctxs = [_lib.Context(dev.index) for _ in range(n_streams)]
+        self.streams = [torch.cuda.Stream(device=dev) for _ in range(n_streams)]
+        self.done = [torch.cuda.Event() for _ in range(n_streams)]
+        self.view_done = [torch.cuda.Event() for _ in range(v)]
+        self.stats = []
+        self._g = model._abi()
+
+    def kernels_per_step(self, n_views: int | None = None) -> int:
+        return KERNELS_PER_VIEW * (self.max_views if n_views is None else n_views)
+
+    def _frame(self, i) -> _lib.Frame:
+        return _lib.Frame(_ptr(self.rgb[i]), _ptr(self.alpha[i]), _ptr(self.depth[i]), None,
+                          _ptr(self.touched[i]) if self.touched is not None else None,
+                          _ptr(self.kept[i]), _ptr(self.ranges[i]), _ptr(self.nproc[i]))
+
+    def render(self, cams, stage_times: bool = False):
+        """Render len(cams) views into the batch buffers (async w.r.t. the host
+        except for the per-view K read).  With ``stage_times`` the views run
+        serially on one stream and per-stage CUDA-event times are summed."""
+        assert len(cams) <= self.max_views
+        L = _lib.lib()
+        caller = torch.cuda.current_stream(self.dev)
+        flags = _lib.LMGS_FLAG_STAGE_TIMES if stage_times else 0
+        st = abi_settings(self.ts, self.sh_eval_degree, self.background, flags)
+        g = self._g
+        if stage_times:
+            tot = {}
+            inst = pairs = 0
+            ctx = self.ctxs[0]
+            for i, cam in enumerate(cams):
+                c = abi_camera(cam)
+                fr = self._frame(i)
+                _lib.check(ctx.handle, L.lmgs_render(ctx.handle, ctypes.byref(g), ctypes.byref(c),
+                                                     ctypes.byref(st), ctypes.byref(fr),
+                                                     caller.cuda_stream), "lmgs_render")
+                s = ctx.stats()
+                for k, v in s["stage_ms"].items():
+                    tot[k] = tot.get(k, 0.0) + v
+                inst += s["n_instances"]
+                pairs += self._pairs(i)
+            nv = len(cams)
+            n = self.model.count
+            s_read = int(self.model.sh.shape[1]) * 12
+            k_avg = inst / nv
+            pix = self.w * self.h
+            t = self.tx * self.ty
+            proc = self._processed_total(len(cams)) / nv
+            alg = {  # algorithmic bytes per frame
+                "preprocess": n * (44 + s_read + 89),
+                "depth_sort": n * (8 + 7 * 24),
+                "scan": n * 16,
+                "duplicate": n * 24 + 8 * k_avg,
+                "tile_sort": 40 * k_avg,
+                "tile_ranges": 8 * k_avg + 8 * t,
+                "blend": 76 * proc + 8 * t + 20 * pix + 4 * n,
+            }
+            return {"stage_ms": tot, "alg_bytes": alg,
+                    "per_frame": {"instances": k_avg, "pairs": pairs / nv, "processed": proc}}
+        ns = len(self.streams)
+        for s in self.streams:
+            s.wait_stream(caller)
+        for i, cam in enumerate(cams):
+            j = i % ns
+            ctx, s = self.ctxs[j], self.streams[j]
+            c = abi_camera(cam)
+            fr = self._frame(i)
+            _lib.check(ctx.handle, L.lmgs_render(ctx.handle, ctypes.byref(g), ctypes.byref(c),
+                                                 ctypes.byref(st), ctypes.byref(fr),
+                                                 s.cuda_stream), "lmgs_render")
+            self.view_done[i].record(s)
+        for s in self.streams:
+            caller.wait_stream(s)
+        return None
+
+    def _pairs(self, i) -> float:
+        """Pixel-instance pairs evaluated by the blend of view i: sum_t P_t n_t."""
+        n = self.nproc[i].double()
+        ts = self.ts
+        # pixels per tile incl. partial edge tiles
+        wx = torch.full((self.tx,), ts, dtype=torch.float64, device=self.dev)
+        wx[-1] = self.w - (self.tx - 1) * ts
+        wy = torch.full((self.ty,), ts, dtype=torch.float64, device=self.dev)
+        wy[-1] = self.h - (self.ty - 1) * ts
+        p = (wy[:, None] * wx[None, :]).reshape(-1)
+        return float((n * p).sum().item())
+
+    def _processed_total(self, nv) -> float:
+        return float(self.nproc[:nv].double().sum().item())
+
+    def bench_e2e(self, cams, steps: int, barrier=None, world: int = 1, device=None) -> dict:
+        """Frames/s through the public API with host buffers: per step the
+        camera poses travel H2D (kernel parameters, from pinned host structs)
+        and every RGB frame is copied D2H into pinned host memory on a copy
+        stream overlapped with the next views' rendering."""
+        nv = len(cams)
+        host = torch.empty((nv, self.h, self.w, 3), dtype=torch.float32, pin_memory=True)
+        copy = torch.cuda.Stream(device=self.dev)
+        caller = torch.cuda.current_stream(self.dev)
+
+        def step():
+            self.render(cams)
+            for i in range(nv):
+                copy.wait_event(self.view_done[i])
+                with torch.cuda.stream(copy):
+                    host[i].copy_(self.rgb[i], non_blocking=True)
+            caller.wait_stream(copy)
+
+        step()  # warm
+        torch.cuda.synchronize()
+        if barrier:
+            barrier()
+        t0 = time.perf_counter()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(caller)
+        for _ in range(steps):
+            step()
+        b.record(caller)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        ms = a.elapsed_time(b)
+        t = torch.tensor([ms], dtype=torch.float64, device=self.dev)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        h2d = nv * ctypes.sizeof(_lib.Camera)
+        d2h = nv * self.h * self.w * 3 * 4
+        return {"value": nv * world * steps / (ms / 1e3), "unit": "frames/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
+                "wall_s": wall,
+                "path": "BatchRenderer.render (lmgs_render C-ABI) with cameras from host, "
+                        "RGB frames D2H to pinned host memory each step; scene resident "
+                        "(uploaded once, as the reference Engine holds its model)"}

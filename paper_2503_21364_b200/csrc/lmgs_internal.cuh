@@ -1,0 +1,179 @@
+// Internal declarations shared by the lmgs CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/lmgs.h"
+
+namespace lmgs {
+
+// Reference constants, gaussian_core.py:21-27.
+constexpr double kTermEps = 1e-4;     // TERM_EPS
+constexpr double kSigmaMax = 0.9999;  // SIGMA_MAX
+constexpr double kCov2dReg = 0.3;     // COV2D_REG
+constexpr double kNearCullZ = 0.01;   // NEAR_CULL_Z
+constexpr double kShC0 = 0.28209479177387814;
+constexpr double kShC1 = 0.4886025119029199;
+constexpr double kLog2e = 1.4426950408889634;
+
+constexpr uint64_t kCulledKey = ~0ull;
+
+// Per-Gaussian blend record written by K1, read by K7 once per (instance,
+// tile).  64 B = two 32-B sectors.  fp64 fields feed the exact per-pixel
+// circle test; the fp32 fields feed the per-pixel exponent.
+struct __align__(16) BlendRec {
+  double mx, my;   // mean2d (px), fp64 — rasterize lo/hi and _blend d (311)
+  double r2;       // radius^2, fp64 (314)
+  float qa, qb, qc;  // -0.5*log2(e)*(ca, 2cb, cc): power = qa dx^2 + qb dx dy + qc dy^2
+  float log2_alpha;  // log2(sigmoid(logit))
+  float cr, cg, cb;  // view colour
+  float z;           // camera-space depth
+};
+static_assert(sizeof(BlendRec) == 64, "BlendRec must be 64 B");
+
+// Tile rectangle, inclusive: x0 | y0 << 16 | x1 << 32 | y1 << 48 (empty -> count 0).
+__host__ __device__ inline uint64_t pack_rect(uint32_t x0, uint32_t y0, uint32_t x1, uint32_t y1) {
+  return (uint64_t)x0 | ((uint64_t)y0 << 16) | ((uint64_t)x1 << 32) | ((uint64_t)y1 << 48);
+}
+
+struct CamArgs {
+  double r[9], t[3], center[3];
+  double fx, fy, cx, cy, lim_x, lim_y;
+  int32_t width, height, tile_size, tiles_x, tiles_y;
+};
+
+struct PreprocessArgs {
+  const float* means;
+  const float* quats;
+  const float* scales;
+  const float* logits;
+  const float* sh;
+  int64_t n;
+  int32_t sh_coeffs;
+  int32_t eval_degree;
+  CamArgs cam;
+  // outputs
+  uint64_t* depth_keys;  // [n] fp64 depth bits, kCulledKey if culled
+  uint32_t* ids;         // [n] iota (radix payload)
+  uint64_t* rects;       // [n]
+  uint32_t* tile_counts; // [n]
+  BlendRec* recs;        // [n]
+  uint8_t* kept;         // [n] nullable
+  unsigned long long* n_kept;  // scalar (atomic)
+  // optional fp64 dump for lmgs_project
+  double* dbg_mean2d;
+  double* dbg_cov2d;
+  double* dbg_depth;
+  double* dbg_radius;
+  float* dbg_colors;
+  float* dbg_opacity;
+};
+
+void launch_preprocess(const PreprocessArgs& a, cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// LSD radix sort (onesweep: one histogram pass + one scatter pass per digit
+// with decoupled look-back), 8-bit digits, u64 keys, optional u32 values.
+// The plan kernel detects trivial digits (all keys share it) and skips those
+// passes on the device; the result lands in buffer index plan->result.
+
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 1 << kRadixBits;
+constexpr int kMaxPasses = 8;
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;
+
+struct RadixPlan {
+  int32_t n_passes;
+  int32_t active[kMaxPasses];
+  int32_t src[kMaxPasses];
+  int32_t result;
+  int32_t pad[7];
+  uint32_t digit_start[kMaxPasses][kRadix];
+};
+
+struct RadixSortBuffers {
+  uint64_t* keys[2];
+  uint32_t* vals[2];   // vals[0] == nullptr -> keys only
+  RadixPlan* plan;     // device
+  uint32_t* hist;      // [kMaxPasses * kRadix]
+  uint32_t* lookback;  // [kMaxPasses * max_blocks * kRadix]
+  uint32_t* counters;  // [kMaxPasses]
+  int64_t max_blocks;
+};
+
+size_t radix_lookback_words(int64_t capacity);
+// n <= capacity; sorts bits [begin_bit, begin_bit + 8*n_passes).
+void radix_sort(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_passes,
+                cudaStream_t s);
+
+// Exclusive scan of counts gathered through a permutation:
+//   offsets[r] = sum_{r' < r} counts[perm[r']],  *total = sum over all r.
+// perm == nullptr -> identity.  Decoupled look-back, one pass.
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+size_t scan_status_words(int64_t n);
+void scan_counts(const uint32_t* counts, const uint32_t* perm_a, const uint32_t* perm_b,
+                 const RadixPlan* plan, int64_t n, uint64_t* offsets, uint64_t* total,
+                 unsigned long long* status, uint32_t* counter, cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// raster stages
+
+struct DuplicateArgs {
+  const uint32_t* ids[2];  // depth-sorted ids (ping-pong, selected by plan)
+  const RadixPlan* plan;
+  const uint64_t* rects;
+  const uint32_t* tile_counts;
+  const uint64_t* offsets;  // rank-order exclusive offsets
+  int64_t n;
+  int32_t tiles_x;
+  uint64_t* keys_out;      // [K] tile << 32 | rank
+};
+void launch_duplicate(const DuplicateArgs& a, cudaStream_t s);
+
+void launch_tile_ranges(const uint64_t* keys_a, const uint64_t* keys_b, const RadixPlan* plan,
+                        int64_t k, int2* ranges, cudaStream_t s);
+
+struct BlendArgs {
+  const uint64_t* keys[2];
+  const RadixPlan* key_plan;
+  const uint32_t* ids[2];
+  const RadixPlan* id_plan;
+  const int2* ranges;
+  const BlendRec* recs;
+  int32_t width, height, tile_size, tiles_x, tiles_y;
+  float bg[3];
+  float* rgb;
+  float* alpha;
+  float* depth;
+  float* trans;
+  int32_t* touched;
+  int32_t* n_processed;
+};
+int launch_blend(const BlendArgs& a, cudaStream_t s);  // returns 0 or LMGS_ERR_UNSUPPORTED
+
+void launch_fill_background(float* rgb, float* alpha, float* depth, float* trans, int64_t n_pix,
+                            const float bg[3], cudaStream_t s);
+
+struct InstanceExportArgs {
+  const uint64_t* keys[2];
+  const RadixPlan* key_plan;
+  const uint32_t* ids[2];
+  const RadixPlan* id_plan;
+  const int64_t* prim_ids;  // nullable: original ids
+  int64_t k;
+  uint64_t* keys_out;
+  int64_t* prims_out;
+};
+void launch_export_instances(const InstanceExportArgs& a, cudaStream_t s);
+
+constexpr int kMaxCompositeBlocks = 64;
+// `order` is a host array (n_blocks <= kMaxCompositeBlocks), passed by value.
+void launch_composite(const float* rgb, const float* trans, const float* depth, int n_blocks,
+                      const int32_t* order, int64_t n_pix, const float bg[3], float* out_rgb,
+                      float* out_alpha, float* out_depth, cudaStream_t s);
+
+}  // namespace lmgs

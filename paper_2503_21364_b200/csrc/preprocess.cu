@@ -1,0 +1,248 @@
+// K1 preprocess: near cull, fp64 EWA projection, tile rectangle + count,
+// SH colour, blend record.  One thread per Gaussian.
+//
+// Reference: project_splats (gaussian_core.py:187-230), quat_to_rotmat
+// (93-102), covariance_3d (105-117), eval_sh_colors (129-142), and the tile
+// overlap predicate of rasterize (362-373) restated as an inclusive tile
+// rectangle.
+//
+// This file is compiled with -fmad=false: every fp64 operation rounds exactly
+// where torch's does.  The products torch hands to MKL dgemm (means @ r_wc.T,
+// j @ r_wc) are written as the explicit FMA chain MKL evaluates; the bmm
+// products (covariance, jw @ cov3d @ jw^T) as plain sequential sums.  The
+// only deviation: sqrt here is IEEE-rounded while torch.sqrt (MKL VML) is
+// <= 1 ulp low on ~0.7% of inputs.
+#include "lmgs_internal.cuh"
+
+namespace lmgs {
+namespace {
+
+__device__ __forceinline__ double mkl_dot3(double a0, double b0, double a1, double b1, double a2,
+                                           double b2) {
+  return fma(a2, b2, fma(a1, b1, a0 * b0));
+}
+__device__ __forceinline__ double bmm_dot3(double a0, double b0, double a1, double b1, double a2,
+                                           double b2) {
+  return (a0 * b0 + a1 * b1) + a2 * b2;
+}
+
+// Inclusive tile index range [a, b] along one axis for lo/hi of a splat's
+// bbox, identical to the reference comparisons hi >= t0 and lo <= t0 + tw
+// with tw = min(ts, size - t0).  Empty when a > b.
+__device__ __forceinline__ void axis_range(double lo, double hi, int size, int ts, int nt,
+                                           int* a, int* b) {
+  int j;
+  if (!(lo > -2.0 * ts)) j = 0;
+  else if (lo > (double)size + 2.0 * ts) j = nt;
+  else j = max((int)floor(lo / (double)ts) - 2, 0);
+  while (j < nt) {
+    int end = min((j + 1) * ts, size);
+    if (lo <= (double)end) break;
+    ++j;
+  }
+  int k;
+  if (!(hi < (double)size + 2.0 * ts)) k = nt - 1;
+  else if (hi < -2.0 * ts) k = -1;
+  else k = min((int)floor(hi / (double)ts) + 2, nt - 1);
+  while (k >= 0 && !((double)(k * ts) <= hi)) --k;
+  *a = j;
+  *b = k;
+}
+
+// Colour along centre->mean; degree <= 1 is eval_sh_colors (129-142),
+// degrees 2-3 extend it with the standard real SH basis, clamp(0,1), no +0.5.
+__device__ __forceinline__ void sh_color(const float* __restrict__ sh, int ncoef, int deg,
+                                         float x, float y, float z, float out[3]) {
+  const float C0 = (float)kShC0, C1 = (float)kShC1;
+  float c[3];
+  const float4* sh4 = reinterpret_cast<const float4*>(sh);
+  // coefficients 0..3 (12 floats = 3 float4)
+  float v[48];
+  int nload = ncoef * 3;
+  if ((reinterpret_cast<uintptr_t>(sh) & 15) == 0 && (nload & 3) == 0) {
+#pragma unroll
+    for (int q = 0; q < 12; ++q) {
+      if (4 * q < nload) {
+        float4 f = __ldg(sh4 + q);
+        v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 48; ++q)
+      if (q < nload) v[q] = __ldg(sh + q);
+  }
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) c[ch] = C0 * v[ch];
+  if (deg >= 1 && ncoef >= 4) {
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch)
+      c[ch] = ((c[ch] - (C1 * y) * v[3 + ch]) + (C1 * z) * v[6 + ch]) - (C1 * x) * v[9 + ch];
+  }
+  if (deg >= 2 && ncoef >= 9) {
+    float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    const float C20 = 1.0925484305920792f, C21 = -1.0925484305920792f,
+                C22 = 0.31539156525252005f, C23 = -1.0925484305920792f,
+                C24 = 0.5462742152960396f;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch)
+      c[ch] = c[ch] + C20 * xy * v[12 + ch] + C21 * yz * v[15 + ch] +
+              C22 * (2.0f * zz - xx - yy) * v[18 + ch] + C23 * xz * v[21 + ch] +
+              C24 * (xx - yy) * v[24 + ch];
+    if (deg >= 3 && ncoef >= 16) {
+      const float C30 = -0.5900435899266435f, C31 = 2.890611442640554f,
+                  C32 = -0.4570457994644658f, C33 = 0.3731763325901154f,
+                  C34 = -0.4570457994644658f, C35 = 1.445305721320277f,
+                  C36 = -0.5900435899266435f;
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch)
+        c[ch] = c[ch] + C30 * y * (3.0f * xx - yy) * v[27 + ch] + C31 * xy * z * v[30 + ch] +
+                C32 * y * (4.0f * zz - xx - yy) * v[33 + ch] +
+                C33 * z * (2.0f * zz - 3.0f * xx - 3.0f * yy) * v[36 + ch] +
+                C34 * x * (4.0f * zz - xx - yy) * v[39 + ch] + C35 * z * (xx - yy) * v[42 + ch] +
+                C36 * x * (xx - 3.0f * yy) * v[45 + ch];
+    }
+  }
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) out[ch] = fminf(fmaxf(c[ch], 0.0f), 1.0f);
+}
+
+__global__ void __launch_bounds__(256) k_preprocess(PreprocessArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool keep = false;
+  if (i < a.n) {
+    const CamArgs& cam = a.cam;
+    const double m0 = a.means[3 * i], m1 = a.means[3 * i + 1], m2 = a.means[3 * i + 2];
+    // p = means @ r_wc.T + t_wc (195): MKL FMA chain, then + t
+    const double x = mkl_dot3(m0, cam.r[0], m1, cam.r[1], m2, cam.r[2]) + cam.t[0];
+    const double y = mkl_dot3(m0, cam.r[3], m1, cam.r[4], m2, cam.r[5]) + cam.t[1];
+    const double z = mkl_dot3(m0, cam.r[6], m1, cam.r[7], m2, cam.r[8]) + cam.t[2];
+    keep = z > kNearCullZ;  // 196
+    a.ids[i] = (uint32_t)i;
+    if (a.kept) a.kept[i] = keep;
+    if (!keep) {
+      a.depth_keys[i] = kCulledKey;
+      a.tile_counts[i] = 0;
+      a.rects[i] = 0;
+    } else {
+      const double mx = cam.fx * x / z + cam.cx;  // 201
+      const double my = cam.fy * y / z + cam.cy;
+      // quat_to_rotmat (93-102)
+      const float4 q = __ldg(reinterpret_cast<const float4*>(a.quats) + i);
+      const double qw = q.x, qx = q.y, qy = q.z, qz = q.w;
+      const double nr = sqrt(((qw * qw + qx * qx) + qy * qy) + qz * qz);
+      const double w = qw / nr, X = qx / nr, Y = qy / nr, Z = qz / nr;
+      const double r00 = 1 - 2 * (Y * Y + Z * Z), r01 = 2 * (X * Y - w * Z),
+                   r02 = 2 * (X * Z + w * Y);
+      const double r10 = 2 * (X * Y + w * Z), r11 = 1 - 2 * (X * X + Z * Z),
+                   r12 = 2 * (Y * Z - w * X);
+      const double r20 = 2 * (X * Z - w * Y), r21 = 2 * (Y * Z + w * X),
+                   r22 = 1 - 2 * (X * X + Y * Y);
+      // covariance_3d (105-117): M = R * s[None,:], Sigma = M M^T
+      const double s0 = a.scales[3 * i], s1 = a.scales[3 * i + 1], s2 = a.scales[3 * i + 2];
+      const double M00 = r00 * s0, M01 = r01 * s1, M02 = r02 * s2;
+      const double M10 = r10 * s0, M11 = r11 * s1, M12 = r12 * s2;
+      const double M20 = r20 * s0, M21 = r21 * s1, M22 = r22 * s2;
+      const double S00 = bmm_dot3(M00, M00, M01, M01, M02, M02);
+      const double S01 = bmm_dot3(M00, M10, M01, M11, M02, M12);
+      const double S02 = bmm_dot3(M00, M20, M01, M21, M02, M22);
+      const double S10 = bmm_dot3(M10, M00, M11, M01, M12, M02);
+      const double S11 = bmm_dot3(M10, M10, M11, M11, M12, M12);
+      const double S12 = bmm_dot3(M10, M20, M11, M21, M12, M22);
+      const double S20 = bmm_dot3(M20, M00, M21, M01, M22, M02);
+      const double S21 = bmm_dot3(M20, M10, M21, M11, M22, M12);
+      const double S22 = bmm_dot3(M20, M20, M21, M21, M22, M22);
+      // clamped Jacobian (205-218); `fx / z` is torch's reciprocal(z) * fx
+      const double tx = fmin(fmax(x / z, -cam.lim_x), cam.lim_x) * z;
+      const double ty = fmin(fmax(y / z, -cam.lim_y), cam.lim_y) * z;
+      const double rz = 1.0 / z;
+      const double zz = z * z;
+      const double J00 = rz * cam.fx, J02 = -cam.fx * tx / zz;
+      const double J11 = rz * cam.fy, J12 = -cam.fy * ty / zz;
+      // jw = j @ r_wc (219): MKL FMA chain over (J0k, 0, J2k) rows incl. the zeros
+      const double W00 = mkl_dot3(J00, cam.r[0], 0.0, cam.r[3], J02, cam.r[6]);
+      const double W01 = mkl_dot3(J00, cam.r[1], 0.0, cam.r[4], J02, cam.r[7]);
+      const double W02 = mkl_dot3(J00, cam.r[2], 0.0, cam.r[5], J02, cam.r[8]);
+      const double W10 = mkl_dot3(0.0, cam.r[0], J11, cam.r[3], J12, cam.r[6]);
+      const double W11 = mkl_dot3(0.0, cam.r[1], J11, cam.r[4], J12, cam.r[7]);
+      const double W12 = mkl_dot3(0.0, cam.r[2], J11, cam.r[5], J12, cam.r[8]);
+      // cov2d = (jw @ cov3d) @ jw^T + 0.3 I (220-221)
+      const double T00 = bmm_dot3(W00, S00, W01, S10, W02, S20);
+      const double T01 = bmm_dot3(W00, S01, W01, S11, W02, S21);
+      const double T02 = bmm_dot3(W00, S02, W01, S12, W02, S22);
+      const double T10 = bmm_dot3(W10, S00, W11, S10, W12, S20);
+      const double T11 = bmm_dot3(W10, S01, W11, S11, W12, S21);
+      const double T12 = bmm_dot3(W10, S02, W11, S12, W12, S22);
+      const double ca = bmm_dot3(T00, W00, T01, W01, T02, W02) + kCov2dReg;
+      const double cb = bmm_dot3(T00, W10, T01, W11, T02, W12);  // cov2d[0,1]
+      const double cc = bmm_dot3(T10, W10, T11, W11, T12, W12) + kCov2dReg;
+      // lam_max / radius (223-225)
+      const double h = 0.5 * (ca - cc);
+      const double lam = 0.5 * (ca + cc) + sqrt(h * h + cb * cb);
+      const double radius = 3.0 * sqrt(lam);
+      // tile rectangle (362-373)
+      int x0, x1, y0, y1;
+      axis_range(mx - radius, mx + radius, cam.width, cam.tile_size, cam.tiles_x, &x0, &x1);
+      axis_range(my - radius, my + radius, cam.height, cam.tile_size, cam.tiles_y, &y0, &y1);
+      uint32_t cnt = 0;
+      if (x0 <= x1 && y0 <= y1) cnt = (uint32_t)(x1 - x0 + 1) * (uint32_t)(y1 - y0 + 1);
+      a.tile_counts[i] = cnt;
+      a.rects[i] = cnt ? pack_rect(x0, y0, x1, y1) : 0;
+      a.depth_keys[i] = (uint64_t)__double_as_longlong(z);
+      // conic (_blend 309-310), fp64 then pre-scaled to the exp2 domain in fp32
+      const double det = ca * cc - cb * cb;
+      const double ica = cc / det, icb = -cb / det, icc = ca / det;
+      const float logit = a.logits[i];
+      const float log2_alpha =
+          logit < -15.0f ? logit * (float)kLog2e : -log2f(1.0f + expf(-logit));
+      float col[3] = {0.f, 0.f, 0.f};
+      if (cnt || a.dbg_colors) {
+        const double dx = m0 - cam.center[0], dy = m1 - cam.center[1], dz = m2 - cam.center[2];
+        double nrm = sqrt((dx * dx + dy * dy) + dz * dz);
+        nrm = fmax(nrm, 1e-12);
+        sh_color(a.sh + (int64_t)i * a.sh_coeffs * 3, a.sh_coeffs, a.eval_degree,
+                 (float)(dx / nrm), (float)(dy / nrm), (float)(dz / nrm), col);
+      }
+      BlendRec rec;
+      rec.mx = mx;
+      rec.my = my;
+      rec.r2 = radius * radius;
+      rec.qa = (float)(-0.5 * kLog2e * ica);
+      rec.qb = (float)(-kLog2e * icb);
+      rec.qc = (float)(-0.5 * kLog2e * icc);
+      rec.log2_alpha = log2_alpha;
+      rec.cr = col[0];
+      rec.cg = col[1];
+      rec.cb = col[2];
+      rec.z = (float)z;
+      a.recs[i] = rec;
+      if (a.dbg_mean2d) {
+        a.dbg_mean2d[2 * i] = mx;
+        a.dbg_mean2d[2 * i + 1] = my;
+        a.dbg_cov2d[3 * i] = ca;
+        a.dbg_cov2d[3 * i + 1] = cb;
+        a.dbg_cov2d[3 * i + 2] = cc;
+        a.dbg_depth[i] = z;
+        a.dbg_radius[i] = radius;
+        a.dbg_colors[3 * i] = col[0];
+        a.dbg_colors[3 * i + 1] = col[1];
+        a.dbg_colors[3 * i + 2] = col[2];
+        a.dbg_opacity[i] = (float)(1.0 / (1.0 + exp(-(double)logit)));
+      }
+    }
+  }
+  // kept count: warp ballot + one atomic per warp
+  const unsigned ballot = __ballot_sync(0xffffffffu, keep);
+  if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(a.n_kept, (unsigned long long)__popc(ballot));
+}
+
+}  // namespace
+
+void launch_preprocess(const PreprocessArgs& a, cudaStream_t s) {
+  if (a.n <= 0) return;
+  const int threads = 256;
+  const int64_t blocks = (a.n + threads - 1) / threads;
+  k_preprocess<<<(unsigned)blocks, threads, 0, s>>>(a);
+}
+
+}  // namespace lmgs

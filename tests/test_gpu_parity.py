@@ -1,0 +1,182 @@
+"""CUDA path (liblmgs.so via the C-ABI) vs the reference's golden outputs and the CPU oracle.
+
+Bar (BASELINE.json north_star): tile lists and tile ranges bit-exact, touched
+exact, image max-abs <= 1e-4 per channel (fp32 blend vs the fp64 reference),
+alpha = 1 - T_final <= 1e-4.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import GOLDEN_CASES
+from paper_2503_21364_b200 import GaussianModel, project, render, render_image, scenes
+from paper_2503_21364_b200.errors import InvalidInputError, ShapeError
+
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = 1e-4  # max-abs per channel, written in the north star
+
+
+def _lists_from_record(rec):
+    r = rec.tile_ranges.numpy().astype(np.int64)
+    offsets = np.concatenate([[0], np.cumsum(r[:, 1] - r[:, 0])])
+    return offsets, rec.inst_prim_ids.numpy()
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_render_image_matches_reference_golden(golden_case, name):
+    c = golden_case(name)
+    img, touched, rec = render_image(c.gaussians, c.camera, c.tile_size, c.background,
+                                     with_record=True, subset=c.subset)
+    torch.cuda.synchronize()
+    offsets, lists = _lists_from_record(rec)
+    # ranges are contiguous [start, end) in tile order
+    r = rec.tile_ranges.numpy()
+    nonempty = r[:, 1] > r[:, 0]
+    assert np.all(r[nonempty, 0] == offsets[:-1][nonempty])
+    np.testing.assert_array_equal(offsets, c.offsets)
+    np.testing.assert_array_equal(lists, c.lists)
+    np.testing.assert_array_equal(rec.prim_id.numpy(), c.splat_prim_id)
+    np.testing.assert_array_equal(touched.cpu().numpy(), c.touched)
+    err = np.abs(img.cpu().double().numpy() - c.image).max()
+    assert err <= IMG_TOL, err
+    assert np.abs(rec.t_final.numpy() - c.t_final).max() <= IMG_TOL
+
+
+def test_record_tiles_view(golden_case):
+    c = golden_case("ragged_100x70_ts16")
+    _, _, rec = render_image(c.gaussians, c.camera, c.tile_size, c.background, with_record=True)
+    k = 0
+    for tile in rec.tiles:
+        ids = rec.prim_id[tile.order].numpy()
+        np.testing.assert_array_equal(ids, c.lists[k:k + len(ids)])
+        k += len(ids)
+    assert k == len(c.lists)
+
+
+def test_project_bit_exact_vs_oracle():
+    """K1's fp64 geometry equals the oracle's bit for bit (same op order)."""
+    g = scenes.synthetic_gaussians(200_000, seed=4)
+    cam = scenes.orbit_cameras(2, 1920, 1080, seed=4)[1]
+    model = GaussianModel.from_host(g)
+    p = project(cam, model, sh_eval_degree=1)
+    o = oracle.project(g, cam, sh_eval_degree=1)
+    kept = p["kept"].cpu().numpy()
+    ids = np.nonzero(kept)[0]
+    np.testing.assert_array_equal(ids, o["prim_id"])
+    np.testing.assert_array_equal(p["mean2d"].cpu().numpy()[ids], o["mean2d"])
+    np.testing.assert_array_equal(p["depth"].cpu().numpy()[ids], o["depth"])
+    np.testing.assert_array_equal(p["cov2d"].cpu().numpy()[ids], o["cov2d"])
+    np.testing.assert_array_equal(p["radius"].cpu().numpy()[ids], o["radius"])
+    assert np.abs(p["colors"].cpu().numpy()[ids] - o["colors"]).max() <= 1e-6
+    assert np.abs(p["opacity"].cpu().numpy()[ids] - o["opac"]).max() <= 1e-6
+
+
+@pytest.mark.parametrize("deg", [0, 1, 2, 3])
+def test_sh_degrees_vs_oracle(deg):
+    g = scenes.synthetic_gaussians(3000, seed=deg, sh_degree=3)
+    cam = scenes.orbit_cameras(1, 128, 96, seed=deg)[0]
+    o = oracle.render(g, cam, 16, sh_eval_degree=deg)
+    out = render(cam, GaussianModel.from_host(g), 16, sh_eval_degree=deg, with_instances=True)
+    assert np.abs(out.rgb.cpu().double().numpy() - o["image"]).max() <= IMG_TOL
+    np.testing.assert_array_equal(out.inst_prim_ids.cpu().numpy(), o["inst_prim"])
+
+
+def _full_frame_check(g, cam, ts=16, bg=(0.0, 0.0, 0.0), deg=3):
+    model = GaussianModel.from_host(g, validate=False)
+    out = render(cam, model, ts, bg, sh_eval_degree=deg, with_instances=True,
+                 out={"transmittance": None})
+    torch.cuda.synchronize()
+    o = oracle.render(g, cam, ts, bg, sh_eval_degree=deg)
+    assert out.n_instances == o["K"]
+    r = out.tile_ranges.cpu().numpy().astype(np.int64)
+    counts = r[:, 1] - r[:, 0]
+    np.testing.assert_array_equal(counts, o["tile_counts"])
+    np.testing.assert_array_equal(r[counts > 0, 0], o["offsets"][:-1][counts > 0])
+    np.testing.assert_array_equal(out.inst_prim_ids.cpu().numpy(), o["inst_prim"])
+    kept = out.kept.cpu().numpy().astype(bool)
+    touched = out.touched.cpu().numpy()[kept]
+    mism = int((touched != o["touched"]).sum())
+    img = out.rgb.cpu().double().numpy()
+    err = float(np.abs(img - o["image"]).max())
+    aerr = float(np.abs(out.alpha.cpu().double().numpy() - o["alpha"]).max())
+    derr = float(np.abs(out.depth.cpu().double().numpy() - o["depth"]).max())
+    nproc = out.n_processed.cpu().numpy()
+    return dict(err=err, aerr=aerr, derr=derr, touched_mismatch=mism,
+                nproc_mismatch=int((nproc != o["n_processed"]).sum()), K=o["K"], oracle=o)
+
+
+def test_c1_full_frame_vs_oracle():
+    g = scenes.synthetic_gaussians(10_000, seed=0)
+    cam = scenes.orbit_cameras(1, 256, 256, seed=0)[0]
+    r = _full_frame_check(g, cam)
+    assert r["err"] <= IMG_TOL and r["aerr"] <= IMG_TOL
+    assert r["touched_mismatch"] == 0 and r["nproc_mismatch"] == 0
+
+
+@pytest.mark.slow
+def test_c2_full_frame_vs_oracle():
+    """Config 2: 1M Gaussians, 1920x1080, full frame, every tile list exact."""
+    g = scenes.synthetic_gaussians(1_000_000, seed=0)
+    cam = scenes.orbit_cameras(1, 1920, 1080, seed=0)[0]
+    r = _full_frame_check(g, cam)
+    print(f"c2: K={r['K']} max|rgb|={r['err']:.2e} max|alpha|={r['aerr']:.2e} "
+          f"depth={r['derr']:.2e} touched_mism={r['touched_mismatch']} "
+          f"nproc_mism={r['nproc_mismatch']}")
+    assert r["err"] <= IMG_TOL and r["aerr"] <= IMG_TOL
+    assert r["touched_mismatch"] == 0
+
+
+@pytest.mark.slow
+def test_c3_view_full_frame_vs_oracle():
+    """Config 3 scene (6M Gaussians, 1080p): one orbit view, full frame."""
+    g = scenes.synthetic_gaussians(6_000_000, seed=0)
+    cam = scenes.orbit_cameras(64, 1920, 1080, seed=0)[5]
+    r = _full_frame_check(g, cam)
+    print(f"c3 view: K={r['K']} max|rgb|={r['err']:.2e} touched_mism={r['touched_mismatch']}")
+    assert r["err"] <= IMG_TOL and r["aerr"] <= IMG_TOL
+    assert r["touched_mismatch"] == 0
+
+
+@pytest.mark.parametrize("ts", [1, 5, 8, 16, 24, 32, 48, 64])
+def test_tile_sizes_vs_oracle(ts):
+    g = scenes.synthetic_gaussians(2000, seed=11)
+    cam = scenes.orbit_cameras(1, 100, 70, seed=11)[0]
+    r = _full_frame_check(g, cam, ts=ts, bg=(0.1, 0.2, 0.3))
+    assert r["err"] <= IMG_TOL and r["touched_mismatch"] == 0 and r["nproc_mismatch"] == 0
+
+
+def test_empty_model_is_background():
+    g = scenes.synthetic_gaussians(0, seed=0)
+    cam = scenes.orbit_cameras(1, 40, 30)[0]
+    out = render(cam, GaussianModel.from_host(g), 16, (0.2, 0.4, 0.6))
+    torch.cuda.synchronize()
+    assert out.n_instances == 0
+    np.testing.assert_allclose(out.rgb.cpu().numpy(), np.broadcast_to([0.2, 0.4, 0.6], (30, 40, 3)),
+                               atol=1e-7)
+    assert float(out.alpha.abs().max()) == 0.0
+
+
+def test_permutation_invariance():
+    """test_gaussian_core.py:254-260: reordering the model leaves the image unchanged."""
+    g = scenes.synthetic_gaussians(5000, seed=2)
+    cam = scenes.orbit_cameras(1, 160, 120, seed=2)[0]
+    a = render(cam, GaussianModel.from_host(g)).rgb
+    perm = scenes.make_rng(0, "perm").permutation(g.count)
+    b = render(cam, GaussianModel.from_host(g.subset(perm))).rgb
+    assert float((a - b).abs().max()) <= 1e-6
+
+
+def test_errors_match_reference_types():
+    g = scenes.synthetic_gaussians(10, seed=0, sh_degree=1)
+    cam = scenes.orbit_cameras(1, 32, 32)[0]
+    with pytest.raises(ShapeError):
+        GaussianModel(g.means, g.quats, g.scales, g.opacity_logits, g.sh, sh_degree=3)
+    with pytest.raises(InvalidInputError):
+        GaussianModel(g.means, g.quats * 2, g.scales, g.opacity_logits, g.sh, sh_degree=1)
+    with pytest.raises(InvalidInputError):
+        GaussianModel(g.means, g.quats, -g.scales, g.opacity_logits, g.sh, sh_degree=1)
+    with pytest.raises(InvalidInputError):
+        render(cam, GaussianModel.from_host(g), tile_size=0)
