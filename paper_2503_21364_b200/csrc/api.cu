@@ -61,8 +61,9 @@ struct Carver {
 // sizes of the per-Gaussian arena for capacity n
 size_t gaussian_bytes(int64_t n) {
   size_t b = 0;
-  b += 2 * align_up(sizeof(uint64_t) * n);  // depth keys x2
-  b += 2 * align_up(sizeof(uint32_t) * n);  // ids x2
+  b += 2 * align_up(sizeof(uint32_t) * n);  // fp32 depth keys x2
+  b += 2 * align_up(sizeof(uint64_t) * n);  // fp64 depth keys x2
+  b += 3 * align_up(sizeof(uint32_t) * n);  // ids x3
   b += align_up(sizeof(uint64_t) * n);      // rects
   b += align_up(sizeof(uint32_t) * n);      // tile counts
   b += align_up(sizeof(BlendRec) * n);      // records
@@ -80,13 +81,15 @@ size_t instance_bytes(int64_t k) {
 
 struct Scalars {  // device-side small state
   RadixPlan depth_plan;
+  RadixPlan fallback_plan;
   RadixPlan tile_plan;
-  uint32_t hist[2][kMaxPasses * kRadix];
-  uint32_t counters[2][kMaxPasses];
+  uint32_t hist[3][kMaxPasses * kRadix];
+  uint32_t counters[3][kMaxPasses];
   uint32_t scan_counter;
   uint32_t pad;
   unsigned long long n_kept;
   uint64_t total;
+  DevSlots slots;
 };
 
 }  // namespace
@@ -96,13 +99,15 @@ struct lmgs_context {
   std::string err;
   DevBuf gbuf, ibuf, fbuf;
   Scalars* d_scal = nullptr;
-  uint64_t* h_pinned = nullptr;  // [0] = K, [1] = kept
+  uint64_t* h_pinned = nullptr;  // [0] = K, [1] = kept, [2] = fallback flag
   cudaEvent_t ev[kNumStages + 1] = {};
   bool events_ok = false;
   // views into the arenas for the current / last render
   int64_t cap_n = -1, cap_k = -1;
-  uint64_t* depth_keys[2] = {nullptr, nullptr};
-  uint32_t* ids[2] = {nullptr, nullptr};
+  uint32_t* keys32[2] = {nullptr, nullptr};
+  uint64_t* keys64[2] = {nullptr, nullptr};
+  uint32_t* ids[3] = {nullptr, nullptr, nullptr};
+  int64_t fallbacks = 0;  // views that needed the 64-bit depth sort
   uint64_t* rects = nullptr;
   uint32_t* tile_counts = nullptr;
   BlendRec* recs = nullptr;
@@ -154,10 +159,13 @@ int ensure_gaussians(lmgs_context* c, int64_t n, cudaStream_t s) {
   LMGS_CUDA(c, c->gbuf.reserve(gaussian_bytes(n)));
   const int64_t cap = (int64_t)(c->gbuf.bytes >= gaussian_bytes(n + n / 4) ? n + n / 4 : n);
   Carver cv{static_cast<char*>(c->gbuf.ptr)};
-  c->depth_keys[0] = cv.take<uint64_t>(cap);
-  c->depth_keys[1] = cv.take<uint64_t>(cap);
+  c->keys32[0] = cv.take<uint32_t>(cap);
+  c->keys32[1] = cv.take<uint32_t>(cap);
+  c->keys64[0] = cv.take<uint64_t>(cap);
+  c->keys64[1] = cv.take<uint64_t>(cap);
   c->ids[0] = cv.take<uint32_t>(cap);
   c->ids[1] = cv.take<uint32_t>(cap);
+  c->ids[2] = cv.take<uint32_t>(cap);
   c->rects = cv.take<uint64_t>(cap);
   c->tile_counts = cv.take<uint32_t>(cap);
   c->recs = cv.take<BlendRec>(cap);
@@ -261,6 +269,7 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
   int2* ranges = out->tile_ranges ? reinterpret_cast<int2*>(out->tile_ranges) : c->ranges;
   LMGS_CUDA(c, cudaMemsetAsync(ranges, 0, sizeof(int2) * tiles, s));
   LMGS_CUDA(c, cudaMemsetAsync(&c->d_scal->n_kept, 0, sizeof(unsigned long long), s));
+  LMGS_CUDA(c, cudaMemsetAsync(&c->d_scal->slots.fallback, 0, sizeof(int), s));
   if (out->touched && n > 0) LMGS_CUDA(c, cudaMemsetAsync(out->touched, 0, sizeof(int32_t) * n, s));
 
   if (timed) LMGS_CUDA(c, cudaEventRecord(c->ev[0], s));
@@ -274,8 +283,10 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
   pa.sh_coeffs = g->sh_coeffs;
   pa.eval_degree = st->sh_eval_degree < g->sh_degree ? st->sh_eval_degree : g->sh_degree;
   pa.cam = ca;
-  pa.depth_keys = c->depth_keys[0];
+  pa.depth_keys32 = c->keys32[0];
+  pa.depth_keys = c->keys64[0];
   pa.ids = c->ids[0];
+  pa.ids_fb = c->ids[2];
   pa.rects = c->rects;
   pa.tile_counts = c->tile_counts;
   pa.recs = c->recs;
@@ -284,39 +295,64 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
   launch_preprocess(pa, s);
   if (timed) LMGS_CUDA(c, cudaEventRecord(c->ev[1], s));
 
+  // K2: depth order = fp32-key radix sort + exact fp64 fix-up of equal-key runs
+  DevSlots* slots = &c->d_scal->slots;
   RadixSortBuffers db{};
-  db.keys[0] = c->depth_keys[0];
-  db.keys[1] = c->depth_keys[1];
+  db.keys[0] = c->keys32[0];
+  db.keys[1] = c->keys32[1];
+  db.key_bytes = 4;
   db.vals[0] = c->ids[0];
   db.vals[1] = c->ids[1];
   db.plan = &c->d_scal->depth_plan;
   db.hist = c->d_scal->hist[0];
   db.lookback = c->depth_lookback;
   db.counters = c->d_scal->counters[0];
-  db.max_blocks = (c->cap_n + kSortTile - 1) / kSortTile;
-  radix_sort(db, n, 0, 8, s);
+  db.keys_result = &slots->depth_keys32;
+  db.vals_result = &slots->sorted_ids;
+  radix_sort(db, n, 0, 4, s);
+  depth_fixup(&slots->depth_keys32, &slots->sorted_ids, n, c->keys64[0], &slots->fallback, s);
   if (timed) LMGS_CUDA(c, cudaEventRecord(c->ev[2], s));
 
-  scan_counts(c->tile_counts, c->ids[0], c->ids[1], &c->d_scal->depth_plan, n, c->offsets,
-              &c->d_scal->total, c->scan_status, &c->d_scal->scan_counter, s);
+  // K3: tiles_touched in depth order -> exclusive offsets and K
+  scan_counts(c->tile_counts, &slots->sorted_ids, n, c->offsets, &c->d_scal->total,
+              c->scan_status, &c->d_scal->scan_counter, s);
   LMGS_CUDA(c, cudaMemcpyAsync(c->h_pinned, &c->d_scal->total, sizeof(uint64_t),
                                cudaMemcpyDeviceToHost, s));
   LMGS_CUDA(c, cudaMemcpyAsync(c->h_pinned + 1, &c->d_scal->n_kept, sizeof(uint64_t),
+                               cudaMemcpyDeviceToHost, s));
+  LMGS_CUDA(c, cudaMemcpyAsync(c->h_pinned + 2, &slots->fallback, sizeof(int),
                                cudaMemcpyDeviceToHost, s));
   LMGS_CUDA(c, cudaGetLastError());
   LMGS_CUDA(c, cudaStreamSynchronize(s));
   const int64_t k = (int64_t)c->h_pinned[0];
   c->stats.n_instances = k;
   c->stats.n_kept = (int64_t)c->h_pinned[1];
+  if (*reinterpret_cast<int*>(c->h_pinned + 2)) {
+    // a run of > kFixupRun equal fp32 depths: exact 64-bit (depth, id) sort
+    ++c->fallbacks;
+    RadixSortBuffers fb{};
+    fb.keys[0] = c->keys64[0];
+    fb.keys[1] = c->keys64[1];
+    fb.key_bytes = 8;
+    fb.vals[0] = c->ids[2];
+    fb.vals[1] = c->ids[0];
+    fb.plan = &c->d_scal->fallback_plan;
+    fb.hist = c->d_scal->hist[1];
+    fb.lookback = c->depth_lookback;
+    fb.counters = c->d_scal->counters[1];
+    fb.keys_result = &slots->fb_keys;
+    fb.vals_result = &slots->sorted_ids;
+    radix_sort(fb, n, 0, 8, s);
+    scan_counts(c->tile_counts, &slots->sorted_ids, n, c->offsets, &c->d_scal->total,
+                c->scan_status, &c->d_scal->scan_counter, s);
+  }
   if (k >= ((int64_t)1 << 30) - 1)
     return fail(c, LMGS_ERR_UNSUPPORTED, "more than 2^30 tile instances in one view");
   if (timed) LMGS_CUDA(c, cudaEventRecord(c->ev[3], s));
 
   if (int r = ensure_instances(c, k > 0 ? k : 1, s)) return r;
   DuplicateArgs da{};
-  da.ids[0] = c->ids[0];
-  da.ids[1] = c->ids[1];
-  da.plan = &c->d_scal->depth_plan;
+  da.slots = slots;
   da.rects = c->rects;
   da.tile_counts = c->tile_counts;
   da.offsets = c->offsets;
@@ -329,25 +365,21 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
   RadixSortBuffers kb{};
   kb.keys[0] = c->inst_keys[0];
   kb.keys[1] = c->inst_keys[1];
+  kb.key_bytes = 8;
   kb.plan = &c->d_scal->tile_plan;
-  kb.hist = c->d_scal->hist[1];
+  kb.hist = c->d_scal->hist[2];
   kb.lookback = c->inst_lookback;
-  kb.counters = c->d_scal->counters[1];
-  kb.max_blocks = (c->cap_k + kSortTile - 1) / kSortTile;
+  kb.counters = c->d_scal->counters[2];
+  kb.keys_result = &slots->inst_keys;
   const int tile_bits = bits_for(tiles);
   radix_sort(kb, k, 32, (tile_bits + 7) / 8, s);
   if (timed) LMGS_CUDA(c, cudaEventRecord(c->ev[5], s));
 
-  launch_tile_ranges(c->inst_keys[0], c->inst_keys[1], &c->d_scal->tile_plan, k, ranges, s);
+  launch_tile_ranges(slots, k, ranges, s);
   if (timed) LMGS_CUDA(c, cudaEventRecord(c->ev[6], s));
 
   BlendArgs ba{};
-  ba.keys[0] = c->inst_keys[0];
-  ba.keys[1] = c->inst_keys[1];
-  ba.key_plan = &c->d_scal->tile_plan;
-  ba.ids[0] = c->ids[0];
-  ba.ids[1] = c->ids[1];
-  ba.id_plan = &c->d_scal->depth_plan;
+  ba.slots = slots;
   ba.ranges = ranges;
   ba.recs = c->recs;
   ba.width = cam->width;
@@ -453,12 +485,7 @@ int lmgs_copy_instances(lmgs_context* c, uint64_t* keys, int64_t* prim_ids, void
   if (!c) return LMGS_ERR_INVALID;
   DeviceGuard guard(c->device);
   InstanceExportArgs a{};
-  a.keys[0] = c->inst_keys[0];
-  a.keys[1] = c->inst_keys[1];
-  a.key_plan = &c->d_scal->tile_plan;
-  a.ids[0] = c->ids[0];
-  a.ids[1] = c->ids[1];
-  a.id_plan = &c->d_scal->depth_plan;
+  a.slots = &c->d_scal->slots;
   a.prim_ids = c->last_prim_ids;
   a.k = c->stats.n_instances;
   a.keys_out = keys;
@@ -488,8 +515,10 @@ int lmgs_project(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* ca
   pa.sh_coeffs = g->sh_coeffs;
   pa.eval_degree = s->sh_eval_degree < g->sh_degree ? s->sh_eval_degree : g->sh_degree;
   pa.cam = make_cam(cam, s->tile_size);
-  pa.depth_keys = c->depth_keys[0];
+  pa.depth_keys32 = c->keys32[0];
+  pa.depth_keys = c->keys64[0];
   pa.ids = c->ids[0];
+  pa.ids_fb = c->ids[2];
   pa.rects = c->rects;
   pa.tile_counts = c->tile_counts;
   pa.recs = c->recs;

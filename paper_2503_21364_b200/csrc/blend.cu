@@ -1,0 +1,263 @@
+// K7 blend_tiles: per-tile front-to-back alpha blending.
+//
+// Reference: _blend (gaussian_core.py:286-332), background term (326),
+// scatter into the image (396-397).
+//
+// One CTA per tile.  Per batch of up to 256 splats (in list order):
+//   1. each thread stages one splat record into shared memory (fp32 conic and
+//      colour, tile-local fp32 mean, guard-banded r^2 bounds, fp64 mean and
+//      r^2 for the exact fallback, a conservative bbox);
+//   2. each warp culls the batch against the bbox of its own pixels (8x4
+//      pixel blocks for 16x16 tiles) — 32 splats per ballot — and keeps an
+//      ordered list of the splats that can touch it;
+//   3. each warp walks its list: per pixel the exact circle test, exponent,
+//      MUFU ex2, front-to-back update; touched is counted with one ballot
+//      per (warp, splat);
+//   4. the CTA stops at the first batch boundary after which no pixel is
+//      active; n_processed is the exact break index of the reference loop.
+//
+// Exactness: inside = d.d <= r^2 (314) is
+// decided in fp32 with a certified guard band and re-done in fp64 inside the
+// band; active = T >= TERM_EPS before each splat (315); touched counts w > 0
+// (323) judged from the exponent (an fp32 ex2 underflows where fp64 exp
+// does not).  The continuous part runs in fp32.
+#include "lmgs_internal.cuh"
+
+namespace lmgs {
+namespace {
+
+// smallest float >= 1e-4: (double)T >= 1e-4  <=>  T >= kTermEpsF for fp32 T
+constexpr float kTermEpsF = 1.00000005e-4f;
+constexpr float kSigmaMaxF = 0.9999f;
+constexpr int kBatch = 256;
+constexpr int kMaxWarps = 8;
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// PPT pixels per thread; SWZ: 16x16 tile on 256 threads with each warp owning
+// an 8x4 pixel block (tighter warp bboxes than 16x2 rows).
+template <int PPT, bool SWZ>
+__global__ void __launch_bounds__(256) k_blend(BlendArgs a) {
+  __shared__ float4 s_geo[kBatch];   // mx_local, my_local, qa, qb
+  __shared__ float4 s_geo2[kBatch];  // qc, log2_alpha, r2_lo, r2_hi
+  __shared__ float4 s_col[kBatch];   // r, g, b, z
+  __shared__ float4 s_box[kBatch];   // conservative bbox: xmin, xmax, ymin, ymax (tile-local)
+  __shared__ double s_mx[kBatch], s_my[kBatch], s_r2[kBatch];
+  __shared__ uint32_t s_id[kBatch];
+  __shared__ uint8_t s_list[kMaxWarps][kBatch];
+  __shared__ uint16_t s_cnt[kMaxWarps][kBatch];
+  __shared__ int s_last[kMaxWarps];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nthreads = blockDim.x;
+  const int nwarps = (nthreads + 31) >> 5;
+  const int tile = blockIdx.x;
+  const int ts = a.tile_size;
+  const int tile_x = tile % a.tiles_x, tile_y = tile / a.tiles_x;
+  const int x0 = tile_x * ts, y0 = tile_y * ts;
+  const int2 range = a.ranges[tile];
+  const uint64_t* __restrict__ keys = static_cast<const uint64_t*>(a.slots->inst_keys);
+  const uint32_t* __restrict__ ids = static_cast<const uint32_t*>(a.slots->sorted_ids);
+
+  float T[PPT], C0[PPT], C1[PPT], C2[PPT], D[PPT], px[PPT], py[PPT];
+  int lxs[PPT], lys[PPT], last[PPT];
+  bool valid[PPT];
+  float bx0 = 3.0e38f, bx1 = -3.0e38f, by0 = 3.0e38f, by1 = -3.0e38f;
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    int lx, ly, pix;
+    if (SWZ) {
+      lx = (warp & 1) * 8 + (lane & 7);
+      ly = (warp >> 1) * 4 + (lane >> 3);
+      pix = ly * 16 + lx;
+    } else {
+      pix = tid + p * nthreads;
+      lx = pix % ts;
+      ly = pix / ts;
+    }
+    lxs[p] = lx;
+    lys[p] = ly;
+    valid[p] = pix < ts * ts && x0 + lx < a.width && y0 + ly < a.height;
+    T[p] = valid[p] ? 1.0f : 0.0f;  // invalid pixels never go active
+    C0[p] = C1[p] = C2[p] = D[p] = 0.0f;
+    px[p] = (float)lx + 0.5f;  // _pixel_centers (335-337), tile-local
+    py[p] = (float)ly + 0.5f;
+    last[p] = -1;
+    if (valid[p]) {
+      bx0 = fminf(bx0, px[p]);
+      bx1 = fmaxf(bx1, px[p]);
+      by0 = fminf(by0, py[p]);
+      by1 = fmaxf(by1, py[p]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    bx0 = fminf(bx0, __shfl_xor_sync(0xffffffffu, bx0, o));
+    bx1 = fmaxf(bx1, __shfl_xor_sync(0xffffffffu, bx1, o));
+    by0 = fminf(by0, __shfl_xor_sync(0xffffffffu, by0, o));
+    by1 = fmaxf(by1, __shfl_xor_sync(0xffffffffu, by1, o));
+  }
+  const uint32_t lt = lanemask_lt();
+
+  for (int b0 = range.x; b0 < range.y; b0 += kBatch) {
+    bool mine_active = false;
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) mine_active |= T[p] >= kTermEpsF;
+    if (__syncthreads_count(mine_active) == 0) break;
+    const int nb = min(kBatch, range.y - b0);
+    for (int j = tid; j < nb; j += nthreads) {
+      const uint64_t key = keys[b0 + j];
+      const uint32_t id = ids[(uint32_t)key];
+      const BlendRec rec = a.recs[id];
+      const double mxl = rec.mx - (double)x0, myl = rec.my - (double)y0;
+      const double ax = fabs(mxl) + ts, ay = fabs(myl) + ts;
+      const double band = (rec.r2 + ax * ax + ay * ay) * 0x1p-18;
+      const float fx = (float)mxl, fy = (float)myl;
+      const float r = sqrtf((float)rec.r2) * 1.0001f + 1e-3f;
+      s_geo[j] = make_float4(fx, fy, rec.qa, rec.qb);
+      s_geo2[j] = make_float4(rec.qc, rec.log2_alpha, __double2float_rd(rec.r2 - band),
+                              __double2float_ru(rec.r2 + band));
+      s_col[j] = make_float4(rec.cr, rec.cg, rec.cb, rec.z);
+      s_box[j] = make_float4(fx - r, fx + r, fy - r, fy + r);
+      s_mx[j] = rec.mx;
+      s_my[j] = rec.my;
+      s_r2[j] = rec.r2;
+      s_id[j] = id;
+#pragma unroll
+      for (int w = 0; w < kMaxWarps; ++w) s_cnt[w][j] = 0;
+    }
+    __syncthreads();
+    // per-warp cull: ordered list of the batch's splats whose bbox meets ours
+    int cnt = 0;
+    if (__any_sync(0xffffffffu, mine_active)) {
+      for (int j0 = 0; j0 < nb; j0 += 32) {
+        const int j = j0 + lane;
+        bool hit = false;
+        if (j < nb) {
+          const float4 bb = s_box[j];
+          hit = bb.y >= bx0 && bb.x <= bx1 && bb.w >= by0 && bb.z <= by1;
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, hit);
+        if (hit) s_list[warp][cnt + __popc(m & lt)] = (uint8_t)j;
+        cnt += __popc(m);
+      }
+    }
+    __syncwarp();
+    for (int q = 0; q < cnt; ++q) {
+      const int k = s_list[warp][q];
+      const float4 g = s_geo[k];
+      const float4 h = s_geo2[k];
+      const float4 c = s_col[k];
+      int contrib_n = 0;
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) {
+        if (T[p] >= kTermEpsF) {
+          const float dx = px[p] - g.x, dy = py[p] - g.y;
+          const float d2 = fmaf(dx, dx, dy * dy);
+          bool inside = d2 <= h.z;
+          if (!inside && d2 <= h.w) {
+            // guard band: the reference's fp64 test, bit for bit
+            const double ddx = ((double)(x0 + lxs[p]) + 0.5) - s_mx[k];
+            const double ddy = ((double)(y0 + lys[p]) + 0.5) - s_my[k];
+            inside = __dadd_rn(__dmul_rn(ddx, ddx), __dmul_rn(ddy, ddy)) <= s_r2[k];
+          }
+          if (inside) {
+            const float power = fmaf(fmaf(g.z, dx, g.w * dy), dx, fmaf(h.x * dy, dy, h.y));
+            bool contrib = power > -1060.0f;
+            if (!contrib && power >= -1080.0f)
+              contrib = exp2((double)power) * (double)T[p] > 0.0;
+            const float sig = fminf(ex2_approx(power), kSigmaMaxF);
+            const float w = T[p] * sig;
+            C0[p] = fmaf(w, c.x, C0[p]);
+            C1[p] = fmaf(w, c.y, C1[p]);
+            C2[p] = fmaf(w, c.z, C2[p]);
+            D[p] = fmaf(w, c.w, D[p]);
+            T[p] = T[p] * (1.0f - sig);
+            contrib_n += contrib;
+            if (T[p] < kTermEpsF) last[p] = b0 - range.x + k;
+          }
+        }
+      }
+      int wsum;
+      if (PPT == 1) wsum = __popc(__ballot_sync(0xffffffffu, contrib_n));
+      else wsum = __reduce_add_sync(0xffffffffu, contrib_n);
+      if (lane == 0) s_cnt[warp][k] = (uint16_t)wsum;
+    }
+    __syncthreads();
+    if (a.touched) {
+      for (int j = tid; j < nb; j += nthreads) {
+        int s = 0;
+#pragma unroll
+        for (int w = 0; w < kMaxWarps; ++w) s += w < nwarps ? s_cnt[w][j] : 0;
+        if (s) atomicAdd(a.touched + s_id[j], s);
+      }
+    }
+  }
+
+  // n_processed: the break index of _blend's loop (324-325)
+  int my_last = -1;
+  bool my_live = false;
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    my_last = max(my_last, last[p]);
+    my_live |= valid[p] && T[p] >= kTermEpsF;
+  }
+  const int any_live = __syncthreads_or(my_live);
+  if (a.n_processed) {
+    int v = my_last;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if (lane == 0) s_last[warp] = v;
+    __syncthreads();
+    if (tid == 0) {
+      int m = -1;
+      for (int w = 0; w < nwarps; ++w) m = max(m, s_last[w]);
+      a.n_processed[tile] = any_live ? (range.y - range.x) : (m + 1);
+    }
+  }
+  // outputs: C + T * bg (326), alpha = 1 - T_final, depth, T_final
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    if (!valid[p]) continue;
+    const int64_t o = (int64_t)(y0 + lys[p]) * a.width + (x0 + lxs[p]);
+    a.rgb[3 * o + 0] = fmaf(T[p], a.bg[0], C0[p]);
+    a.rgb[3 * o + 1] = fmaf(T[p], a.bg[1], C1[p]);
+    a.rgb[3 * o + 2] = fmaf(T[p], a.bg[2], C2[p]);
+    if (a.alpha) a.alpha[o] = 1.0f - T[p];
+    if (a.depth) a.depth[o] = D[p];
+    if (a.trans) a.trans[o] = T[p];
+  }
+}
+
+}  // namespace
+
+int launch_blend(const BlendArgs& a, cudaStream_t s) {
+  const int ts = a.tile_size;
+  const int tiles = a.tiles_x * a.tiles_y;
+  if (tiles <= 0) return 0;
+  if (ts == 16) {
+    k_blend<1, true><<<tiles, 256, 0, s>>>(a);
+  } else if (ts < 16) {
+    const int threads = ((ts * ts + 31) / 32) * 32;
+    k_blend<1, false><<<tiles, threads, 0, s>>>(a);
+  } else if (ts <= 32) {
+    k_blend<4, false><<<tiles, 256, 0, s>>>(a);
+  } else if (ts <= 64) {
+    k_blend<16, false><<<tiles, 256, 0, s>>>(a);
+  } else {
+    return LMGS_ERR_UNSUPPORTED;
+  }
+  return 0;
+}
+
+}  // namespace lmgs

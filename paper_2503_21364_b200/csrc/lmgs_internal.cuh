@@ -54,8 +54,10 @@ struct PreprocessArgs {
   int32_t eval_degree;
   CamArgs cam;
   // outputs
-  uint64_t* depth_keys;  // [n] fp64 depth bits, kCulledKey if culled
-  uint32_t* ids;         // [n] iota (radix payload)
+  uint32_t* depth_keys32;  // [n] bits(fp32 rd(depth)), 0xffffffff if culled
+  uint64_t* depth_keys;    // [n] fp64 depth bits, kCulledKey if culled
+  uint32_t* ids;           // [n] iota (radix payload)
+  uint32_t* ids_fb;        // [n] iota (payload of the gated 64-bit fallback sort)
   uint64_t* rects;       // [n]
   uint32_t* tile_counts; // [n]
   BlendRec* recs;        // [n]
@@ -95,36 +97,54 @@ struct RadixPlan {
 };
 
 struct RadixSortBuffers {
-  uint64_t* keys[2];
+  void* keys[2];       // uint32_t or uint64_t keys, ping-pong
+  int key_bytes;       // 4 or 8
   uint32_t* vals[2];   // vals[0] == nullptr -> keys only
   RadixPlan* plan;     // device
   uint32_t* hist;      // [kMaxPasses * kRadix]
-  uint32_t* lookback;  // [kMaxPasses * max_blocks * kRadix]
+  uint32_t* lookback;  // [kMaxPasses * blocks * kRadix]
   uint32_t* counters;  // [kMaxPasses]
-  int64_t max_blocks;
+  const int* gate;     // nullable: device flag, 0 -> the whole sort is a no-op
+  void** keys_result;  // nullable: device slot receiving the result key buffer
+  void** vals_result;  // nullable: device slot receiving the result value buffer
 };
 
 size_t radix_lookback_words(int64_t capacity);
-// n <= capacity; sorts bits [begin_bit, begin_bit + 8*n_passes).
+// sorts bits [begin_bit, begin_bit + 8*n_passes) of n keys (stable).
 void radix_sort(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_passes,
                 cudaStream_t s);
 
+// Runs of equal fp32 depth keys (length <= kFixupRun) re-ordered by the exact
+// (fp64 depth bits, id); a longer run sets *fallback = 1.
+constexpr int kFixupRun = 32;
+void depth_fixup(void* const* keys_ptr, void* const* ids_ptr, int64_t n,
+                 const uint64_t* depth64, int* fallback, cudaStream_t s);
+
 // Exclusive scan of counts gathered through a permutation:
 //   offsets[r] = sum_{r' < r} counts[perm[r']],  *total = sum over all r.
-// perm == nullptr -> identity.  Decoupled look-back, one pass.
+// perm_ptr == nullptr -> identity, else *perm_ptr (device slot) is the perm.
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
 size_t scan_status_words(int64_t n);
-void scan_counts(const uint32_t* counts, const uint32_t* perm_a, const uint32_t* perm_b,
-                 const RadixPlan* plan, int64_t n, uint64_t* offsets, uint64_t* total,
-                 unsigned long long* status, uint32_t* counter, cudaStream_t s);
+void scan_counts(const uint32_t* counts, void* const* perm_ptr, int64_t n, uint64_t* offsets,
+                 uint64_t* total, unsigned long long* status, uint32_t* counter, cudaStream_t s);
+
+// Device-side slots naming where each sort's result landed (written by the
+// plan kernels, read by the consumers) so the pipeline never syncs on them.
+struct DevSlots {
+  void* sorted_ids;   // uint32_t[n]: ids in (depth, id) order
+  void* depth_keys32; // uint32_t[n]: fp32 depth keys in sorted order
+  void* fb_keys;      // fallback 64-bit sort keys (unused downstream)
+  void* inst_keys;    // uint64_t[K]: tile-sorted instance keys
+  int fallback;       // depth fix-up found a run > kFixupRun
+  int pad;
+};
 
 // ---------------------------------------------------------------------------
 // raster stages
 
 struct DuplicateArgs {
-  const uint32_t* ids[2];  // depth-sorted ids (ping-pong, selected by plan)
-  const RadixPlan* plan;
+  const DevSlots* slots;
   const uint64_t* rects;
   const uint32_t* tile_counts;
   const uint64_t* offsets;  // rank-order exclusive offsets
@@ -134,14 +154,10 @@ struct DuplicateArgs {
 };
 void launch_duplicate(const DuplicateArgs& a, cudaStream_t s);
 
-void launch_tile_ranges(const uint64_t* keys_a, const uint64_t* keys_b, const RadixPlan* plan,
-                        int64_t k, int2* ranges, cudaStream_t s);
+void launch_tile_ranges(const DevSlots* slots, int64_t k, int2* ranges, cudaStream_t s);
 
 struct BlendArgs {
-  const uint64_t* keys[2];
-  const RadixPlan* key_plan;
-  const uint32_t* ids[2];
-  const RadixPlan* id_plan;
+  const DevSlots* slots;
   const int2* ranges;
   const BlendRec* recs;
   int32_t width, height, tile_size, tiles_x, tiles_y;
@@ -159,10 +175,7 @@ void launch_fill_background(float* rgb, float* alpha, float* depth, float* trans
                             const float bg[3], cudaStream_t s);
 
 struct InstanceExportArgs {
-  const uint64_t* keys[2];
-  const RadixPlan* key_plan;
-  const uint32_t* ids[2];
-  const RadixPlan* id_plan;
+  const DevSlots* slots;
   const int64_t* prim_ids;  // nullable: original ids
   int64_t k;
   uint64_t* keys_out;

@@ -119,9 +119,11 @@ __global__ void __launch_bounds__(256) k_preprocess(PreprocessArgs a) {
     const double z = mkl_dot3(m0, cam.r[6], m1, cam.r[7], m2, cam.r[8]) + cam.t[2];
     keep = z > kNearCullZ;  // 196
     a.ids[i] = (uint32_t)i;
+    a.ids_fb[i] = (uint32_t)i;
     if (a.kept) a.kept[i] = keep;
     if (!keep) {
       a.depth_keys[i] = kCulledKey;
+      a.depth_keys32[i] = 0xffffffffu;
       a.tile_counts[i] = 0;
       a.rects[i] = 0;
     } else {
@@ -189,6 +191,7 @@ __global__ void __launch_bounds__(256) k_preprocess(PreprocessArgs a) {
       a.tile_counts[i] = cnt;
       a.rects[i] = cnt ? pack_rect(x0, y0, x1, y1) : 0;
       a.depth_keys[i] = (uint64_t)__double_as_longlong(z);
+      a.depth_keys32[i] = __float_as_uint(__double2float_rd(z));
       // conic (_blend 309-310), fp64 then pre-scaled to the exp2 domain in fp32
       const double det = ca * cc - cb * cb;
       const double ica = cc / det, icb = -cb / det, icc = ca / det;

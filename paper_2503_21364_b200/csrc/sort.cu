@@ -1,19 +1,25 @@
 // Device-wide LSD radix sort (onesweep) and a single-pass exclusive scan.
 //
-// Used twice per view:
-//   K2  depth_rank_sort: (fp64 depth bits, id) pairs, all 64 bits, so equal
-//       depths keep ascending id order — np.lexsort((prim_id, depth)) of
-//       _sort_order (gaussian_core.py:277-283) over all near-kept splats;
-//   K5  tile sort: keys (tile << 32 | rank) stably by the tile bits only,
-//       which turns the rank-ordered instance stream into per-tile lists in
-//       (depth, id) order — the per-tile _sort_order call of rasterize (392).
+// Used per view for
+//   K2  depth order: _sort_order's np.lexsort((prim_id, depth)) over all
+//       near-kept splats (gaussian_core.py:277-283).  Primary pass set on a
+//       32-bit key = bits(fp32 round-down(depth)) (monotone in the fp64
+//       depth), stable on the id payload; then k_depth_fixup re-orders every
+//       run of equal fp32 keys by the exact (fp64 depth, id) pair.  A run longer
+//       than kFixupRun sets a device flag that enables a full 64-bit-key sort
+//       (launched unconditionally, gated on the device) — exact order always,
+//       fast path for real scenes.
+//   K5  tile sort: keys (tile << 32 | rank) stably on the tile bits only,
+//       turning the rank-ordered instance stream into per-tile lists in
+//       (depth, id) order (rasterize's per-tile _sort_order, 392).
 //
-// Structure per sort: one histogram kernel computes every digit's global
-// histogram in a single read of the keys; a 1-block plan kernel scans them,
-// marks digits that all keys share as trivial, and routes the ping-pong
-// buffers; then one scatter kernel per digit ranks a 4096-key tile in shared
-// memory (warp match + per-warp counters, stable) and finds its global
-// offsets with decoupled look-back over the preceding tiles.
+// Per sort: one histogram kernel computes every digit's global histogram in a
+// single read; a 1-block plan kernel scans them, marks digits all keys share
+// as trivial (skipped on the device) and routes the ping-pong buffers; then
+// one onesweep kernel per digit: a tile of kSortTile keys is ranked in shared
+// memory (warp match + per-warp counters, stable), staged in shared memory in
+// digit order, its global digit offsets found by decoupled look-back over the
+// preceding tiles, and written out in coalesced per-digit runs.
 #include "lmgs_internal.cuh"
 
 namespace lmgs {
@@ -24,21 +30,24 @@ constexpr uint32_t kFlagIncl = 2u << 30;
 constexpr uint32_t kValueMask = (1u << 30) - 1;
 constexpr int kWarps = kSortThreads / 32;
 
+// Look-back status words carry their payload (flag | value) in one atomic
+// word and publish nothing else, so relaxed gpu-scope accesses suffice; an
+// acquire load would invalidate L1 (CCTL.IVALL) on every poll.
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long* p) {
   unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_release64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
@@ -46,18 +55,28 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
+template <typename K>
+__device__ __forceinline__ uint32_t digit_of(K key, int shift) {
+  return (uint32_t)((uint64_t)key >> shift) & 0xffu;
+}
+
+__device__ __forceinline__ bool gated_off(const int* gate) { return gate && *gate == 0; }
+
 // ---------------------------------------------------------------------------
 // histogram of every digit in one pass over the keys
 
-__global__ void __launch_bounds__(kSortThreads) k_radix_hist(const uint64_t* __restrict__ keys,
+template <typename K>
+__global__ void __launch_bounds__(kSortThreads) k_radix_hist(const K* __restrict__ keys,
                                                              int64_t n, int begin_bit,
-                                                             int n_passes, uint32_t* hist) {
+                                                             int n_passes, uint32_t* hist,
+                                                             const int* gate) {
+  if (gated_off(gate)) return;
   __shared__ uint32_t s_hist[kMaxPasses][kRadix];
   for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += blockDim.x) (&s_hist[0][0])[i] = 0;
   __syncthreads();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint64_t k = keys[i] >> begin_bit;
+    const uint64_t k = (uint64_t)keys[i] >> begin_bit;
     for (int p = 0; p < n_passes; ++p) atomicAdd(&s_hist[p][(k >> (8 * p)) & 0xff], 1u);
   }
   __syncthreads();
@@ -67,105 +86,161 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_hist(const uint64_t* __r
   }
 }
 
-// one block of kRadix threads: scan each digit histogram, detect trivial passes
+// one block of kRadix threads: scan each digit histogram, detect trivial
+// passes, route buffers, publish where the result will land.
 __global__ void __launch_bounds__(kRadix) k_radix_plan(const uint32_t* __restrict__ hist,
-                                                       int64_t n, int n_passes, RadixPlan* plan) {
+                                                       int64_t n, int n_passes, RadixPlan* plan,
+                                                       const int* gate, void* keys0,
+                                                       void* keys1, void* vals0, void* vals1,
+                                                       void** keys_result, void** vals_result) {
+  const bool off = gated_off(gate);
   __shared__ uint32_t s_scan[kRadix];
   __shared__ int s_trivial[kMaxPasses];
   const int d = threadIdx.x;
-  for (int p = 0; p < n_passes; ++p) {
-    const uint32_t c = hist[p * kRadix + d];
-    if (d == 0) s_trivial[p] = 0;
-    __syncthreads();
-    if ((int64_t)c == n) s_trivial[p] = 1;
-    s_scan[d] = c;
-    __syncthreads();
-    for (int off = 1; off < kRadix; off <<= 1) {
-      const uint32_t v = d >= off ? s_scan[d - off] : 0;
+  if (!off) {
+    for (int p = 0; p < n_passes; ++p) {
+      const uint32_t c = hist[p * kRadix + d];
+      if (d == 0) s_trivial[p] = 0;
       __syncthreads();
-      s_scan[d] += v;
+      if ((int64_t)c == n) s_trivial[p] = 1;
+      s_scan[d] = c;
+      __syncthreads();
+      for (int o = 1; o < kRadix; o <<= 1) {
+        const uint32_t v = d >= o ? s_scan[d - o] : 0;
+        __syncthreads();
+        s_scan[d] += v;
+        __syncthreads();
+      }
+      plan->digit_start[p][d] = s_scan[d] - c;
       __syncthreads();
     }
-    plan->digit_start[p][d] = s_scan[d] - c;
-    __syncthreads();
   }
   if (d == 0) {
     int cur = 0;
     for (int p = 0; p < kMaxPasses; ++p) {
-      const int act = p < n_passes && !s_trivial[p] && n > 1;
+      const int act = !off && p < n_passes && !s_trivial[p] && n > 1;
       plan->active[p] = act;
       plan->src[p] = cur;
       if (act) cur ^= 1;
     }
     plan->result = cur;
     plan->n_passes = n_passes;
+    if (!off) {
+      if (keys_result) *keys_result = cur ? keys1 : keys0;
+      if (vals_result) *vals_result = cur ? vals1 : vals0;
+    }
   }
 }
 
-// one scatter pass (digit p)
-__global__ void __launch_bounds__(kSortThreads) k_radix_pass(
-    uint64_t* keys0, uint64_t* keys1, uint32_t* vals0, uint32_t* vals1, int64_t n, int begin_bit,
-    int pass, const RadixPlan* __restrict__ plan, uint32_t* lookback, uint32_t* counter,
-    int64_t lb_stride) {
+// one onesweep scatter pass (digit `pass`)
+template <typename K>
+__global__ void __launch_bounds__(kSortThreads, 2) k_onesweep(
+    K* keys0, K* keys1, uint32_t* vals0, uint32_t* vals1, int64_t n, int begin_bit, int pass,
+    const RadixPlan* __restrict__ plan, uint32_t* lookback, uint32_t* counter, int64_t lb_stride) {
   if (!plan->active[pass]) return;
-  __shared__ uint32_t s_warp_cnt[kWarps][kRadix];
-  __shared__ uint32_t s_base[kRadix];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // layout: [warp counters | exchange keys | exchange vals] + small arrays
+  uint32_t* s_warp = reinterpret_cast<uint32_t*>(smem_raw);  // [kWarps][kRadix]
+  K* s_keys = reinterpret_cast<K*>(smem_raw);                 // [kSortTile] (after ranking)
+  uint32_t* s_vals = reinterpret_cast<uint32_t*>(smem_raw + sizeof(K) * kSortTile);
+  __shared__ uint32_t s_local_start[kRadix];
+  __shared__ uint32_t s_global[kRadix];
   __shared__ uint32_t s_bid;
+  __shared__ uint32_t s_wsum[kWarps];
+
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_bid = atomicAdd(counter + pass, 1u);
-  for (int i = tid; i < kWarps * kRadix; i += kSortThreads) (&s_warp_cnt[0][0])[i] = 0;
+  for (int i = tid; i < kWarps * kRadix; i += kSortThreads) s_warp[i] = 0;
   __syncthreads();
   const uint32_t bid = s_bid;
   const int64_t base = (int64_t)bid * kSortTile;
   if (base >= n) return;
+  const int count = (int)min((int64_t)kSortTile, n - base);
   const int src = plan->src[pass];
-  const uint64_t* __restrict__ kin = src ? keys1 : keys0;
-  uint64_t* __restrict__ kout = src ? keys0 : keys1;
+  const K* __restrict__ kin = src ? keys1 : keys0;
+  K* __restrict__ kout = src ? keys0 : keys1;
   const uint32_t* __restrict__ vin = src ? vals1 : vals0;
   uint32_t* __restrict__ vout = src ? vals0 : vals1;
   const bool has_vals = vals0 != nullptr;
   const int shift = begin_bit + 8 * pass;
 
-  uint64_t key[kSortItems];
+  K key[kSortItems];
   uint32_t val[kSortItems];
-  uint32_t rank[kSortItems];
-  const int64_t wbase = base + (int64_t)warp * 32 * kSortItems;
+  uint32_t pos[kSortItems];
+  const int wbase = warp * 32 * kSortItems;
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
-    const int64_t idx = wbase + j * 32 + lane;
-    key[j] = idx < n ? kin[idx] : ~0ull;
-    if (has_vals) val[j] = idx < n ? vin[idx] : 0u;
+    const int i = wbase + j * 32 + lane;
+    key[j] = i < count ? kin[base + i] : (K)~(K)0;
+    if (has_vals) val[j] = i < count ? vin[base + i] : 0u;
   }
+  // stable rank within the warp: items in (j, lane) order
   const uint32_t lt = lanemask_lt();
+  uint32_t* my_cnt = s_warp + warp * kRadix;
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
-    const int64_t idx = wbase + j * 32 + lane;
-    const bool valid = idx < n;
-    const uint32_t d = (uint32_t)(key[j] >> shift) & 0xffu;
+    const int i = wbase + j * 32 + lane;
+    const bool valid = i < count;
+    const uint32_t d = digit_of(key[j], shift);
     const uint32_t peers = __match_any_sync(0xffffffffu, valid ? d : 256u + lane);
-    const uint32_t before = s_warp_cnt[warp][d];
-    rank[j] = before + __popc(peers & lt);
+    const uint32_t before = my_cnt[d];
+    pos[j] = before + __popc(peers & lt);
     __syncwarp();
-    if (valid && (peers & lt) == 0) s_warp_cnt[warp][d] = before + __popc(peers);
+    if (valid && (peers & lt) == 0) my_cnt[d] = before + __popc(peers);
     __syncwarp();
   }
   __syncthreads();
-  // per digit: exclusive prefix over warps, block total, look-back
+  // per digit (thread d): warp-exclusive offsets, block total, block-local start
+  uint32_t total;
   {
-    const int d = tid;  // kSortThreads == kRadix
+    const int d = tid;
     uint32_t run = 0;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
-      const uint32_t c = s_warp_cnt[w][d];
-      s_warp_cnt[w][d] = run;
+      const uint32_t c = s_warp[w * kRadix + d];
+      s_warp[w * kRadix + d] = run;
       run += c;
     }
+    total = run;
+    // publish the aggregate early so successors can proceed
+    uint32_t* lb = lookback + ((int64_t)pass * lb_stride) * kRadix;
+    if (bid == 0) st_release(lb + d, kFlagIncl | total);
+    else st_release(lb + (int64_t)bid * kRadix + d, kFlagAgg | total);
+    // block-wide exclusive scan over digits
+    uint32_t incl = total;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    uint32_t wpre = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) wpre += w < warp ? s_wsum[w] : 0;
+    s_local_start[d] = wpre + incl - total;
+  }
+  __syncthreads();
+  // local positions, then stage keys (and values) in digit order
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const uint32_t d = digit_of(key[j], shift);
+    pos[j] += s_local_start[d] + s_warp[warp * kRadix + d];
+  }
+  __syncthreads();  // s_warp is reused as exchange space
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    if (wbase + j * 32 + lane < count) {
+      s_keys[pos[j]] = key[j];
+      if (has_vals) s_vals[pos[j]] = val[j];
+    }
+  }
+  // decoupled look-back for this tile's global digit offsets
+  {
+    const int d = tid;
     uint32_t* lb = lookback + ((int64_t)pass * lb_stride) * kRadix;
     uint32_t excl = 0;
-    if (bid == 0) {
-      st_release(lb + d, kFlagIncl | run);
-    } else {
-      st_release(lb + (int64_t)bid * kRadix + d, kFlagAgg | run);
+    if (bid != 0) {
       int64_t look = (int64_t)bid - 1;
       while (true) {
         uint32_t v;
@@ -176,21 +251,65 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_pass(
         if ((v & ~kValueMask) == kFlagIncl) break;
         --look;
       }
-      st_release(lb + (int64_t)bid * kRadix + d, kFlagIncl | (excl + run));
+      st_release(lb + (int64_t)bid * kRadix + d, kFlagIncl | (excl + total));
     }
-    s_base[d] = plan->digit_start[pass][d] + excl;
+    s_global[d] = plan->digit_start[pass][d] + excl - s_local_start[d];
   }
   __syncthreads();
-#pragma unroll
-  for (int j = 0; j < kSortItems; ++j) {
-    const int64_t idx = wbase + j * 32 + lane;
-    if (idx < n) {
-      const uint32_t d = (uint32_t)(key[j] >> shift) & 0xffu;
-      const uint32_t pos = s_base[d] + s_warp_cnt[warp][d] + rank[j];
-      kout[pos] = key[j];
-      if (has_vals) vout[pos] = val[j];
-    }
+  // coalesced write-out: consecutive threads, consecutive staged positions
+  for (int i = tid; i < count; i += kSortThreads) {
+    const K k = s_keys[i];
+    const uint32_t o = s_global[digit_of(k, shift)] + i;
+    kout[o] = k;
+    if (has_vals) vout[o] = s_vals[i];
   }
+}
+
+template <typename K>
+constexpr size_t onesweep_smem() {
+  return sizeof(K) * kSortTile + sizeof(uint32_t) * kSortTile;
+}
+
+// ---------------------------------------------------------------------------
+// depth fix-up: order each run of equal fp32 keys by (fp64 depth, id)
+
+__global__ void __launch_bounds__(256) k_depth_fixup(void* const* keys_ptr,
+                                                     void* const* ids_ptr, int64_t n,
+                                                     const uint64_t* __restrict__ depth64,
+                                                     int* fallback) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t* keys = static_cast<const uint32_t*>(*keys_ptr);
+  uint32_t* ids = static_cast<uint32_t*>(*ids_ptr);
+  const uint32_t k = keys[i];
+  if (k == 0xffffffffu) return;                    // culled tail
+  if (i > 0 && keys[i - 1] == k) return;           // not a run start
+  if (i + 1 >= n || keys[i + 1] != k) return;      // run of length 1
+  int len = 2;
+  while (i + len < n && keys[i + len] == k && len <= kFixupRun) ++len;
+  if (len > kFixupRun) {
+    atomicExch(fallback, 1);
+    return;
+  }
+  uint64_t dk[kFixupRun];
+  uint32_t id[kFixupRun];
+  for (int a = 0; a < len; ++a) {
+    id[a] = ids[i + a];
+    dk[a] = depth64[id[a]];
+  }
+  for (int a = 1; a < len; ++a) {  // insertion sort by (depth bits, id)
+    const uint64_t kd = dk[a];
+    const uint32_t ki = id[a];
+    int b = a - 1;
+    while (b >= 0 && (dk[b] > kd || (dk[b] == kd && id[b] > ki))) {
+      dk[b + 1] = dk[b];
+      id[b + 1] = id[b];
+      --b;
+    }
+    dk[b + 1] = kd;
+    id[b + 1] = ki;
+  }
+  for (int a = 0; a < len; ++a) ids[i + a] = id[a];
 }
 
 // ---------------------------------------------------------------------------
@@ -202,9 +321,7 @@ constexpr unsigned long long kScanMask = (1ull << 62) - 1;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
 __global__ void __launch_bounds__(kScanThreads) k_scan(const uint32_t* __restrict__ counts,
-                                                       const uint32_t* perm_a,
-                                                       const uint32_t* perm_b,
-                                                       const RadixPlan* plan, int64_t n,
+                                                       void* const* perm_ptr, int64_t n,
                                                        uint64_t* __restrict__ offsets,
                                                        uint64_t* total,
                                                        unsigned long long* status,
@@ -217,7 +334,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const uint32_t* __restric
   __syncthreads();
   const uint32_t bid = s_bid;
   const int64_t base = (int64_t)bid * kScanTile + (int64_t)tid * kScanItems;
-  const uint32_t* perm = perm_a ? ((plan && plan->result) ? perm_b : perm_a) : nullptr;
+  const uint32_t* perm = perm_ptr ? static_cast<const uint32_t*>(*perm_ptr) : nullptr;
   uint32_t v[kScanItems];
   unsigned long long local = 0;
 #pragma unroll
@@ -228,7 +345,6 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const uint32_t* __restric
     v[j] = c;
     local += c;
   }
-  // block exclusive scan of per-thread sums
   unsigned long long incl = local;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
@@ -245,7 +361,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const uint32_t* __restric
       const unsigned long long o = __shfl_up_sync(0xffffffffu, wi, off);
       if (lane >= off) wi += o;
     }
-    if (lane < kScanThreads / 32) s_warp[lane] = wi - wv;  // exclusive warp prefix
+    if (lane < kScanThreads / 32) s_warp[lane] = wi - wv;
     const unsigned long long block_total = __shfl_sync(0xffffffffu, wi, kScanThreads / 32 - 1);
     if (lane == 0) {
       unsigned long long excl = 0;
@@ -280,6 +396,37 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const uint32_t* __restric
   }
 }
 
+template <typename K>
+void radix_sort_impl(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_passes,
+                     cudaStream_t s) {
+  if (n_passes > kMaxPasses) n_passes = kMaxPasses;
+  const int64_t blocks = (n + kSortTile - 1) / kSortTile;
+  cudaMemsetAsync(b.hist, 0, sizeof(uint32_t) * kMaxPasses * kRadix, s);
+  cudaMemsetAsync(b.counters, 0, sizeof(uint32_t) * kMaxPasses, s);
+  if (blocks > 0 && n_passes > 0)
+    cudaMemsetAsync(b.lookback, 0, sizeof(uint32_t) * (size_t)n_passes * blocks * kRadix, s);
+  K* k0 = static_cast<K*>(b.keys[0]);
+  K* k1 = static_cast<K*>(b.keys[1]);
+  if (n > 0 && n_passes > 0) {
+    int hist_blocks = (int)((n + kSortThreads * 16 - 1) / (kSortThreads * 16));
+    if (hist_blocks > 148 * 4) hist_blocks = 148 * 4;
+    k_radix_hist<K><<<hist_blocks, kSortThreads, 0, s>>>(k0, n, begin_bit, n_passes, b.hist,
+                                                         b.gate);
+  }
+  k_radix_plan<<<1, kRadix, 0, s>>>(b.hist, n, n_passes, b.plan, b.gate, k0, k1, b.vals[0],
+                                    b.vals[1], b.keys_result, b.vals_result);
+  if (blocks == 0) return;
+  const size_t smem = onesweep_smem<K>();
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_onesweep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
+  for (int p = 0; p < n_passes; ++p)
+    k_onesweep<K><<<(unsigned)blocks, kSortThreads, smem, s>>>(
+        k0, k1, b.vals[0], b.vals[1], n, begin_bit, p, b.plan, b.lookback, b.counters, blocks);
+}
+
 }  // namespace
 
 size_t radix_lookback_words(int64_t capacity) {
@@ -289,23 +436,15 @@ size_t radix_lookback_words(int64_t capacity) {
 
 void radix_sort(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_passes,
                 cudaStream_t s) {
-  if (n_passes > kMaxPasses) n_passes = kMaxPasses;
-  const int64_t blocks = (n + kSortTile - 1) / kSortTile;
-  cudaMemsetAsync(b.hist, 0, sizeof(uint32_t) * kMaxPasses * kRadix, s);
-  cudaMemsetAsync(b.counters, 0, sizeof(uint32_t) * kMaxPasses, s);
-  if (blocks > 0 && n_passes > 0)
-    cudaMemsetAsync(b.lookback, 0, sizeof(uint32_t) * (size_t)n_passes * blocks * kRadix, s);
-  if (n > 0) {
-    int hist_blocks = (int)((n + kSortThreads * 8 - 1) / (kSortThreads * 8));
-    if (hist_blocks > 148 * 8) hist_blocks = 148 * 8;
-    k_radix_hist<<<hist_blocks, kSortThreads, 0, s>>>(b.keys[0], n, begin_bit, n_passes, b.hist);
-  }
-  k_radix_plan<<<1, kRadix, 0, s>>>(b.hist, n, n_passes, b.plan);
-  if (blocks == 0) return;
-  for (int p = 0; p < n_passes; ++p)
-    k_radix_pass<<<(unsigned)blocks, kSortThreads, 0, s>>>(b.keys[0], b.keys[1], b.vals[0],
-                                                           b.vals[1], n, begin_bit, p, b.plan,
-                                                           b.lookback, b.counters, blocks);
+  if (b.key_bytes == 4) radix_sort_impl<uint32_t>(b, n, begin_bit, n_passes, s);
+  else radix_sort_impl<uint64_t>(b, n, begin_bit, n_passes, s);
+}
+
+void depth_fixup(void* const* keys_ptr, void* const* ids_ptr, int64_t n,
+                 const uint64_t* depth64, int* fallback, cudaStream_t s) {
+  if (n <= 0) return;
+  k_depth_fixup<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(keys_ptr, ids_ptr, n, depth64,
+                                                            fallback);
 }
 
 size_t scan_status_words(int64_t n) {
@@ -313,9 +452,9 @@ size_t scan_status_words(int64_t n) {
   return (size_t)(blocks > 0 ? blocks : 1);
 }
 
-void scan_counts(const uint32_t* counts, const uint32_t* perm_a, const uint32_t* perm_b,
-                 const RadixPlan* plan, int64_t n, uint64_t* offsets, uint64_t* total,
-                 unsigned long long* status, uint32_t* counter, cudaStream_t s) {
+void scan_counts(const uint32_t* counts, void* const* perm_ptr, int64_t n, uint64_t* offsets,
+                 uint64_t* total, unsigned long long* status, uint32_t* counter,
+                 cudaStream_t s) {
   const int64_t blocks = (n + kScanTile - 1) / kScanTile;
   cudaMemsetAsync(counter, 0, sizeof(uint32_t), s);
   if (blocks == 0) {
@@ -323,8 +462,8 @@ void scan_counts(const uint32_t* counts, const uint32_t* perm_a, const uint32_t*
     return;
   }
   cudaMemsetAsync(status, 0, sizeof(unsigned long long) * blocks, s);
-  k_scan<<<(unsigned)blocks, kScanThreads, 0, s>>>(counts, perm_a, perm_b, plan, n, offsets,
-                                                   total, status, counter);
+  k_scan<<<(unsigned)blocks, kScanThreads, 0, s>>>(counts, perm_ptr, n, offsets, total, status,
+                                                   counter);
 }
 
 }  // namespace lmgs
