@@ -130,9 +130,11 @@ int lmgs_render_batch(lmgs_context* ctx, const lmgs_gaussians* g, const lmgs_cam
  * stream to have completed: call after synchronising). */
 int lmgs_get_stats(lmgs_context* ctx, lmgs_stats* out);
 
-/* Copy the last render's sorted tile instances: keys[K] = tile << 32 | depth
- * rank, prim_ids[K] = original Gaussian id (TileRecord.order mapped through
- * splats.prim_id).  Either pointer may be NULL.  Device buffers, K entries. */
+/* Copy the last render's sorted tile instances: keys[K] = tile << 32 | row
+ * (the Gaussian's row in the input arrays), prim_ids[K] = original Gaussian id
+ * (TileRecord.order mapped through splats.prim_id).  Lists are sorted by tile,
+ * then by (fp64 depth, prim id).  Either pointer may be NULL.  Device buffers,
+ * K entries. */
 int lmgs_copy_instances(lmgs_context* ctx, uint64_t* keys, int64_t* prim_ids, void* stream);
 
 /* Stage K1 alone (project_splats): per input Gaussian, fp64 geometry.

@@ -86,7 +86,7 @@ struct Scalars {  // device-side small state
   uint32_t hist[3][kMaxPasses * kRadix];
   uint32_t counters[3][kMaxPasses];
   uint32_t scan_counter;
-  uint32_t pad;
+  int blend_counter;
   unsigned long long n_kept;
   uint64_t total;
   DevSlots slots;
@@ -380,6 +380,7 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
 
   BlendArgs ba{};
   ba.slots = slots;
+  ba.work_counter = &c->d_scal->blend_counter;
   ba.ranges = ranges;
   ba.recs = c->recs;
   ba.width = cam->width;

@@ -67,7 +67,6 @@ __global__ void __launch_bounds__(256) k_blend(BlendArgs a) {
   const int x0 = tile_x * ts, y0 = tile_y * ts;
   const int2 range = a.ranges[tile];
   const uint64_t* __restrict__ keys = static_cast<const uint64_t*>(a.slots->inst_keys);
-  const uint32_t* __restrict__ ids = static_cast<const uint32_t*>(a.slots->sorted_ids);
 
   float T[PPT], C0[PPT], C1[PPT], C2[PPT], D[PPT], px[PPT], py[PPT];
   int lxs[PPT], lys[PPT], last[PPT];
@@ -116,8 +115,7 @@ __global__ void __launch_bounds__(256) k_blend(BlendArgs a) {
     if (__syncthreads_count(mine_active) == 0) break;
     const int nb = min(kBatch, range.y - b0);
     for (int j = tid; j < nb; j += nthreads) {
-      const uint64_t key = keys[b0 + j];
-      const uint32_t id = ids[(uint32_t)key];
+      const uint32_t id = (uint32_t)keys[b0 + j];
       const BlendRec rec = a.recs[id];
       const double mxl = rec.mx - (double)x0, myl = rec.my - (double)y0;
       const double ax = fabs(mxl) + ts, ay = fabs(myl) + ts;
@@ -239,13 +237,167 @@ __global__ void __launch_bounds__(256) k_blend(BlendArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// 16x16 tiles: persistent warps over warp-granular work items.
+//
+// Item = (tile, 8x4 pixel block); 8 items per tile.  A warp takes items from
+// a global counter, walks its tile's list 32 splats at a time (each lane
+// loads one record's geometry sector, culls it against the warp's pixel box,
+// and loads the colour sector only on a hit), blends the hits in list order,
+// and stops as soon as its own 32 pixels are done — no CTA barriers, and a
+// finished warp immediately starts the next item.  n_processed is the max of
+// the warps' break indices (atomicMax); touched is one red.add per
+// (warp, splat) with contributions.
+
+constexpr int kWarpsPerBlock16 = 8;
+
+__global__ void __launch_bounds__(256, 4) k_blend16w(BlendArgs a, int n_items) {
+  __shared__ float4 s_geo[kWarpsPerBlock16][32];   // mx_local, my_local, qa, qb
+  __shared__ float4 s_geo2[kWarpsPerBlock16][32];  // qc, log2_alpha, r2_lo, r2_hi
+  __shared__ float4 s_col[kWarpsPerBlock16][32];   // r, g, b, z
+  __shared__ double s_mx[kWarpsPerBlock16][32], s_my[kWarpsPerBlock16][32],
+      s_r2[kWarpsPerBlock16][32];
+  __shared__ uint32_t s_id[kWarpsPerBlock16][32];
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t* __restrict__ keys = static_cast<const uint64_t*>(a.slots->inst_keys);
+  const float4* __restrict__ rec4 = reinterpret_cast<const float4*>(a.recs);
+
+  while (true) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(a.work_counter, 1);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= n_items) break;
+    const int tile = item >> 3, sub = item & 7;
+    const int tile_x = tile % a.tiles_x, tile_y = tile / a.tiles_x;
+    const int x0 = tile_x * 16, y0 = tile_y * 16;
+    const int lx = (sub & 1) * 8 + (lane & 7), ly = (sub >> 1) * 4 + (lane >> 3);
+    const bool valid = x0 + lx < a.width && y0 + ly < a.height;
+    const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+    if (!vmask) continue;
+    // warp pixel box (pixel centres, tile-local), valid pixels only
+    const float px = (float)lx + 0.5f, py = (float)ly + 0.5f;
+    float bx0 = valid ? px : 3.0e38f, bx1 = valid ? px : -3.0e38f;
+    float by0 = valid ? py : 3.0e38f, by1 = valid ? py : -3.0e38f;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      bx0 = fminf(bx0, __shfl_xor_sync(0xffffffffu, bx0, o));
+      bx1 = fmaxf(bx1, __shfl_xor_sync(0xffffffffu, bx1, o));
+      by0 = fminf(by0, __shfl_xor_sync(0xffffffffu, by0, o));
+      by1 = fmaxf(by1, __shfl_xor_sync(0xffffffffu, by1, o));
+    }
+    const int2 range = a.ranges[tile];
+    float T = valid ? 1.0f : 0.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, D = 0.f;
+    int last = -1;
+    for (int b = range.x; b < range.y; b += 32) {
+      if (!__any_sync(0xffffffffu, T >= kTermEpsF)) break;
+      const int j = b + lane;
+      bool hit = false;
+      if (j < range.y) {
+        const uint32_t id = (uint32_t)keys[j];
+        const float4 g0 = __ldg(rec4 + 4 * (size_t)id);      // mx, my (fp64)
+        const float4 g1 = __ldg(rec4 + 4 * (size_t)id + 1);  // r2 (fp64), qa, qb
+        const double mx = __hiloint2double(__float_as_int(g0.y), __float_as_int(g0.x));
+        const double my = __hiloint2double(__float_as_int(g0.w), __float_as_int(g0.z));
+        const double r2 = __hiloint2double(__float_as_int(g1.y), __float_as_int(g1.x));
+        const double mxl = mx - (double)x0, myl = my - (double)y0;
+        const float fx = (float)mxl, fy = (float)myl;
+        const float r = sqrtf((float)r2) * 1.0001f + 1e-3f;
+        hit = fx + r >= bx0 && fx - r <= bx1 && fy + r >= by0 && fy - r <= by1;
+        if (hit) {
+          const float4 g2 = __ldg(rec4 + 4 * (size_t)id + 2);  // qc, log2a, r, g
+          const float4 g3 = __ldg(rec4 + 4 * (size_t)id + 3);  // b, z
+          const double ax = fabs(mxl) + 16.0, ay = fabs(myl) + 16.0;
+          const double band = (r2 + ax * ax + ay * ay) * 0x1p-18;
+          s_geo[warp][lane] = make_float4(fx, fy, g1.z, g1.w);
+          s_geo2[warp][lane] = make_float4(g2.x, g2.y, __double2float_rd(r2 - band),
+                                           __double2float_ru(r2 + band));
+          s_col[warp][lane] = make_float4(g2.z, g2.w, g3.x, g3.y);
+          s_mx[warp][lane] = mx;
+          s_my[warp][lane] = my;
+          s_r2[warp][lane] = r2;
+          s_id[warp][lane] = id;
+        }
+      }
+      uint32_t m = __ballot_sync(0xffffffffu, hit);
+      __syncwarp();
+      while (m) {
+        const int k = __ffs(m) - 1;
+        m &= m - 1;
+        const float4 g = s_geo[warp][k];
+        const float4 h = s_geo2[warp][k];
+        const float4 c = s_col[warp][k];
+        bool contrib = false;
+        if (T >= kTermEpsF) {
+          const float dx = px - g.x, dy = py - g.y;
+          const float d2 = fmaf(dx, dx, dy * dy);
+          bool inside = d2 <= h.z;
+          if (!inside && d2 <= h.w) {
+            const double ddx = ((double)(x0 + lx) + 0.5) - s_mx[warp][k];
+            const double ddy = ((double)(y0 + ly) + 0.5) - s_my[warp][k];
+            inside = __dadd_rn(__dmul_rn(ddx, ddx), __dmul_rn(ddy, ddy)) <= s_r2[warp][k];
+          }
+          if (inside) {
+            const float power = fmaf(fmaf(g.z, dx, g.w * dy), dx, fmaf(h.x * dy, dy, h.y));
+            contrib = power > -1060.0f;
+            if (!contrib && power >= -1080.0f) contrib = exp2((double)power) * (double)T > 0.0;
+            const float sig = fminf(ex2_approx(power), kSigmaMaxF);
+            const float w = T * sig;
+            C0 = fmaf(w, c.x, C0);
+            C1 = fmaf(w, c.y, C1);
+            C2 = fmaf(w, c.z, C2);
+            D = fmaf(w, c.w, D);
+            T = T * (1.0f - sig);
+            if (T < kTermEpsF) last = b - range.x + k;
+          }
+        }
+        const uint32_t cm = __ballot_sync(0xffffffffu, contrib);
+        if (lane == 0 && cm && a.touched) atomicAdd(a.touched + s_id[warp][k], __popc(cm));
+      }
+      __syncwarp();
+    }
+    if (a.n_processed) {
+      int v = last;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+      const bool live = __any_sync(0xffffffffu, valid && T >= kTermEpsF);
+      if (lane == 0) atomicMax(a.n_processed + tile, live ? (range.y - range.x) : v + 1);
+    }
+    if (valid) {
+      const int64_t o = (int64_t)(y0 + ly) * a.width + (x0 + lx);
+      a.rgb[3 * o + 0] = fmaf(T, a.bg[0], C0);
+      a.rgb[3 * o + 1] = fmaf(T, a.bg[1], C1);
+      a.rgb[3 * o + 2] = fmaf(T, a.bg[2], C2);
+      if (a.alpha) a.alpha[o] = 1.0f - T;
+      if (a.depth) a.depth[o] = D;
+      if (a.trans) a.trans[o] = T;
+    }
+  }
+}
+
 }  // namespace
 
 int launch_blend(const BlendArgs& a, cudaStream_t s) {
   const int ts = a.tile_size;
   const int tiles = a.tiles_x * a.tiles_y;
   if (tiles <= 0) return 0;
-  if (ts == 16) {
+  if (ts == 16 && a.work_counter) {
+    cudaMemsetAsync(a.work_counter, 0, sizeof(int), s);
+    if (a.n_processed) cudaMemsetAsync(a.n_processed, 0, sizeof(int) * tiles, s);
+    const int items = tiles * 8;
+    static int blocks_per_sm = 0, sms = 0;
+    if (!blocks_per_sm) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_blend16w, 256, 0);
+      if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    int grid = sms * blocks_per_sm;
+    const int need = (items + kWarpsPerBlock16 - 1) / kWarpsPerBlock16;
+    if (grid > need) grid = need;
+    k_blend16w<<<grid, 256, 0, s>>>(a, items);
+  } else if (ts == 16) {
     k_blend<1, true><<<tiles, 256, 0, s>>>(a);
   } else if (ts < 16) {
     const int threads = ((ts * ts + 31) / 32) * 32;

@@ -168,6 +168,7 @@ struct BlendArgs {
   float* trans;
   int32_t* touched;
   int32_t* n_processed;
+  int* work_counter;  // device scalar for the persistent 16x16 kernel (nullable)
 };
 int launch_blend(const BlendArgs& a, cudaStream_t s);  // returns 0 or LMGS_ERR_UNSUPPORTED
 

@@ -9,8 +9,11 @@
 namespace lmgs {
 namespace {
 
-// One thread per depth rank r: emit (tile << 32 | r) for every tile in the
-// splat's rectangle, row-major, at its rank-order offset.
+// One thread per depth rank r: emit (tile << 32 | id) for every tile in the
+// splat's rectangle, row-major, at its rank-order offset.  The stream is in
+// depth order, so a stable sort on the tile bits alone yields per-tile lists
+// in (depth, id) order; the low word carries the Gaussian row id so the blend
+// reads its record without a rank -> id gather.
 __global__ void __launch_bounds__(256) k_duplicate(DuplicateArgs a) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= a.n) return;
@@ -24,7 +27,7 @@ __global__ void __launch_bounds__(256) k_duplicate(DuplicateArgs a) {
   uint64_t off = a.offsets[r];
   for (int y = y0; y <= y1; ++y)
     for (int x = x0; x <= x1; ++x)
-      a.keys_out[off++] = ((uint64_t)(uint32_t)(y * a.tiles_x + x) << 32) | (uint64_t)r;
+      a.keys_out[off++] = ((uint64_t)(uint32_t)(y * a.tiles_x + x) << 32) | (uint64_t)id;
 }
 
 __global__ void __launch_bounds__(256) k_tile_ranges(const DevSlots* slots, int64_t k,
@@ -55,7 +58,7 @@ __global__ void k_export(InstanceExportArgs a) {
   const uint64_t key = static_cast<const uint64_t*>(a.slots->inst_keys)[i];
   if (a.keys_out) a.keys_out[i] = key;
   if (a.prims_out) {
-    const uint32_t id = static_cast<const uint32_t*>(a.slots->sorted_ids)[(uint32_t)key];
+    const uint32_t id = (uint32_t)key;
     a.prims_out[i] = a.prim_ids ? a.prim_ids[id] : (int64_t)id;
   }
 }

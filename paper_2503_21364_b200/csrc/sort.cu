@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kRadix) k_radix_plan(const uint32_t* __restric
 
 // one onesweep scatter pass (digit `pass`)
 template <typename K>
-__global__ void __launch_bounds__(kSortThreads, 2) k_onesweep(
+__global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(
     K* keys0, K* keys1, uint32_t* vals0, uint32_t* vals1, int64_t n, int begin_bit, int pass,
     const RadixPlan* __restrict__ plan, uint32_t* lookback, uint32_t* counter, int64_t lb_stride) {
   if (!plan->active[pass]) return;
@@ -183,11 +183,14 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_onesweep(
     const bool valid = i < count;
     const uint32_t d = digit_of(key[j], shift);
     const uint32_t peers = __match_any_sync(0xffffffffu, valid ? d : 256u + lane);
-    const uint32_t before = my_cnt[d];
-    pos[j] = before + __popc(peers & lt);
-    __syncwarp();
-    if (valid && (peers & lt) == 0) my_cnt[d] = before + __popc(peers);
-    __syncwarp();
+    // the lowest peer bumps the warp counter; the returned old count is this
+    // round's base.  Shared-memory atomics of one warp retire in issue order,
+    // so successive rounds need no read-modify-write chain through registers.
+    const int leader = __ffs(peers) - 1;
+    uint32_t old = 0;
+    if (valid && lane == leader) old = atomicAdd(my_cnt + d, (uint32_t)__popc(peers));
+    old = __shfl_sync(0xffffffffu, old, leader);
+    pos[j] = old + __popc(peers & lt);
   }
   __syncthreads();
   // per digit (thread d): warp-exclusive offsets, block total, block-local start

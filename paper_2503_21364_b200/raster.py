@@ -174,7 +174,7 @@ class RenderRecord:
     prim_id: torch.Tensor         # (M,) original id of each kept splat
     tile_ranges: torch.Tensor     # (T,2)
     inst_prim_ids: torch.Tensor   # (K,) prim id per tile instance, per-tile lists concatenated
-    inst_keys: torch.Tensor       # (K,) tile << 32 | depth rank
+    inst_keys: torch.Tensor       # (K,) tile << 32 | input row
     t_final: torch.Tensor         # (H,W)
     n_processed: torch.Tensor     # (T,)
     _tiles: list = field(default=None, repr=False)
@@ -222,7 +222,7 @@ class RenderOutput:
     n_processed: torch.Tensor     # (T,)  i32
     n_instances: int
     n_kept: int
-    inst_keys: torch.Tensor | None = None      # (K,) i64 (tile << 32 | rank)
+    inst_keys: torch.Tensor | None = None      # (K,) i64 (tile << 32 | input row)
     inst_prim_ids: torch.Tensor | None = None  # (K,) i64
     stats: dict | None = None
 
