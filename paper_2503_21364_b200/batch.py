@@ -18,7 +18,7 @@ import torch
 from . import _lib
 from .raster import GaussianModel, _ptr, abi_camera, abi_settings
 
-KERNELS_PER_VIEW = 19  # preprocess 1, depth sort 10, scan 1, duplicate 1, tile sort 4, ranges 1, blend 1
+KERNELS_PER_VIEW = 7  # preprocess, tile hist, column scan, tile scan, place, tile sort x2 (small/medium), blend -> see DESIGN.md
 
 
 class BatchRenderer:
@@ -90,13 +90,11 @@ class BatchRenderer:
             t = self.tx * self.ty
             proc = self._processed_total(len(cams)) / nv
             alg = {  # algorithmic bytes per frame
-                "preprocess": n * (44 + s_read + 89),
-                "depth_sort": n * (8 + 7 * 24),
-                "scan": n * 16,
-                "duplicate": n * 24 + 8 * k_avg,
-                "tile_sort": 40 * k_avg,
-                "tile_ranges": 8 * k_avg + 8 * t,
-                "blend": 76 * proc + 8 * t + 20 * pix + 4 * n,
+                "preprocess": n * (44 + s_read + 89) + 4 * k_avg,
+                "tile_scan": 20 * t,
+                "place": 16 * n + 12 * k_avg,
+                "tile_sort": 12 * k_avg,
+                "blend": 68 * proc + 8 * t + 20 * pix + 4 * n,
             }
             return {"stage_ms": tot, "alg_bytes": alg,
                     "per_frame": {"instances": k_avg, "pairs": pairs / nv, "processed": proc}}

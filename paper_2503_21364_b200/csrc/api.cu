@@ -1,11 +1,17 @@
 // C-ABI entry points (include/lmgs.h): context, device arena, stage pipeline.
 //
-// One view = K1 preprocess -> K2 depth-rank radix sort -> K3 rank-order scan
-// of tiles_touched -> (one 8-byte device->host read of K) -> K4 duplicate ->
-// K5 tile radix sort -> K6 tile ranges -> K7 blend.
+// One view:
+//   K1 preprocess  (fp64 geometry, tile rect, blend record)
+//   K3 tile counts (per-SM shared-memory histograms + column scan) and tile
+//      scan (one CTA: ranges, size classes, K) -> one 8-byte D2H read of K
+//   K4 place       (shared-memory cursors: each instance into its tile bucket)
+//   K5 tile sort   (per-tile smem LSD radix on the fp32 depth + exact fp64 fix-up;
+//                   oversized buckets: onesweep radix + the same fix-up)
+//   K7 blend       (persistent warps over (tile, 8x4 block) items)
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "lmgs_internal.cuh"
 
@@ -16,9 +22,8 @@ namespace {
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
-const char* kStageNames[] = {"preprocess", "depth_sort", "scan", "duplicate",
-                             "tile_sort",  "tile_ranges", "blend"};
-constexpr int kNumStages = 7;
+const char* kStageNames[] = {"preprocess", "tile_scan", "place", "tile_sort", "blend"};
+constexpr int kNumStages = 5;
 
 // grow-only device buffer
 struct DevBuf {
@@ -29,7 +34,7 @@ struct DevBuf {
     if (ptr) cudaFree(ptr);
     ptr = nullptr;
     bytes = 0;
-    size_t want = need + need / 4;  // headroom against per-view K jitter
+    size_t want = need + need / 4;  // headroom against per-view jitter
     cudaError_t e = cudaMalloc(&ptr, want);
     if (e != cudaSuccess) {
       cudaGetLastError();
@@ -58,37 +63,37 @@ struct Carver {
   }
 };
 
-// sizes of the per-Gaussian arena for capacity n
 size_t gaussian_bytes(int64_t n) {
   size_t b = 0;
-  b += 2 * align_up(sizeof(uint32_t) * n);  // fp32 depth keys x2
-  b += 2 * align_up(sizeof(uint64_t) * n);  // fp64 depth keys x2
-  b += 3 * align_up(sizeof(uint32_t) * n);  // ids x3
-  b += align_up(sizeof(uint64_t) * n);      // rects
-  b += align_up(sizeof(uint32_t) * n);      // tile counts
-  b += align_up(sizeof(BlendRec) * n);      // records
-  b += align_up(sizeof(uint64_t) * n);      // offsets
-  b += align_up(sizeof(uint32_t) * radix_lookback_words(n));
-  b += align_up(sizeof(unsigned long long) * scan_status_words(n));
-  return b + 16 * kAlign;
+  b += align_up(sizeof(uint32_t) * n);  // fp32 depth keys
+  b += align_up(sizeof(uint64_t) * n);  // fp64 depth keys
+  b += align_up(sizeof(uint64_t) * n);  // rects
+  b += align_up(sizeof(uint32_t) * n);  // tile counts
+  b += align_up(sizeof(BlendRec) * n);  // records
+  return b + 8 * kAlign;
+}
+size_t tile_bytes(int64_t t, int ctas) {
+  return align_up(sizeof(uint32_t) * t * ctas) + 5 * align_up(sizeof(uint32_t) * t) +
+         align_up(sizeof(int2) * t) + 8 * kAlign;
 }
 size_t instance_bytes(int64_t k) {
-  size_t b = 0;
-  b += 2 * align_up(sizeof(uint64_t) * k);
-  b += align_up(sizeof(uint32_t) * radix_lookback_words(k));
-  return b + 8 * kAlign;
+  return 2 * align_up(sizeof(uint32_t) * k) + 4 * kAlign;
+}
+size_t big_bytes(int64_t k) {
+  return 2 * align_up(sizeof(uint64_t) * k) + 2 * align_up(sizeof(uint32_t) * k) +
+         align_up(sizeof(uint32_t) * radix_lookback_words(k)) + 8 * kAlign;
 }
 
 struct Scalars {  // device-side small state
-  RadixPlan depth_plan;
-  RadixPlan fallback_plan;
-  RadixPlan tile_plan;
-  uint32_t hist[3][kMaxPasses * kRadix];
-  uint32_t counters[3][kMaxPasses];
-  uint32_t scan_counter;
-  int blend_counter;
+  RadixPlan big_plan;
+  uint32_t hist[kMaxPasses * kRadix];
+  uint32_t counters[kMaxPasses];
+  uint32_t class_counts[4];
   unsigned long long n_kept;
   uint64_t total;
+  unsigned long long big_total;
+  int blend_counter;
+  int pad;
   DevSlots slots;
 };
 
@@ -96,30 +101,36 @@ struct Scalars {  // device-side small state
 
 struct lmgs_context {
   int device = 0;
+  int sms = 148;  // K3a / K4 CTA slices (one per SM)
   std::string err;
-  DevBuf gbuf, ibuf, fbuf;
+  DevBuf gbuf, tbuf, ibuf, bbuf;
   Scalars* d_scal = nullptr;
-  uint64_t* h_pinned = nullptr;  // [0] = K, [1] = kept, [2] = fallback flag
+  uint64_t* h_pinned = nullptr;  // [0]=K [1]=kept [2]=class counts (3 x u32 packed)
   cudaEvent_t ev[kNumStages + 1] = {};
   bool events_ok = false;
-  // views into the arenas for the current / last render
-  int64_t cap_n = -1, cap_k = -1;
-  uint32_t* keys32[2] = {nullptr, nullptr};
-  uint64_t* keys64[2] = {nullptr, nullptr};
-  uint32_t* ids[3] = {nullptr, nullptr, nullptr};
-  int64_t fallbacks = 0;  // views that needed the 64-bit depth sort
+  int64_t cap_n = -1, cap_t = -1, cap_k = -1, cap_big = -1;
+  // per-Gaussian arena
+  uint32_t* key32 = nullptr;
+  uint64_t* key64 = nullptr;
   uint64_t* rects = nullptr;
   uint32_t* tile_counts = nullptr;
   BlendRec* recs = nullptr;
-  uint64_t* offsets = nullptr;
-  uint32_t* depth_lookback = nullptr;
-  unsigned long long* scan_status = nullptr;
-  uint64_t* inst_keys[2] = {nullptr, nullptr};
-  uint32_t* inst_lookback = nullptr;
+  // per-tile arena
+  uint32_t* bin_hist = nullptr;   // [sms][tiles]
+  uint32_t* tile_count = nullptr;
+  uint32_t* lists[3] = {nullptr, nullptr, nullptr};
+  uint32_t* big_off = nullptr;
   int2* ranges = nullptr;
-  int64_t ranges_cap = -1;
+  // per-instance arena
+  uint32_t* bucket = nullptr;
+  uint32_t* sorted_ids = nullptr;
+  // oversized-bucket arena
+  uint64_t* big_keys[2] = {nullptr, nullptr};
+  uint32_t* big_vals[2] = {nullptr, nullptr};
+  uint32_t* big_lookback = nullptr;
   const int64_t* last_prim_ids = nullptr;
-  // stats of the last render
+  const int2* last_ranges = nullptr;
+  int64_t big_views = 0;  // views that needed the oversized-bucket path
   lmgs_stats stats{};
   bool last_timed = false;
 };
@@ -159,42 +170,52 @@ int ensure_gaussians(lmgs_context* c, int64_t n, cudaStream_t s) {
   LMGS_CUDA(c, c->gbuf.reserve(gaussian_bytes(n)));
   const int64_t cap = (int64_t)(c->gbuf.bytes >= gaussian_bytes(n + n / 4) ? n + n / 4 : n);
   Carver cv{static_cast<char*>(c->gbuf.ptr)};
-  c->keys32[0] = cv.take<uint32_t>(cap);
-  c->keys32[1] = cv.take<uint32_t>(cap);
-  c->keys64[0] = cv.take<uint64_t>(cap);
-  c->keys64[1] = cv.take<uint64_t>(cap);
-  c->ids[0] = cv.take<uint32_t>(cap);
-  c->ids[1] = cv.take<uint32_t>(cap);
-  c->ids[2] = cv.take<uint32_t>(cap);
+  c->key32 = cv.take<uint32_t>(cap);
+  c->key64 = cv.take<uint64_t>(cap);
   c->rects = cv.take<uint64_t>(cap);
   c->tile_counts = cv.take<uint32_t>(cap);
   c->recs = cv.take<BlendRec>(cap);
-  c->offsets = cv.take<uint64_t>(cap);
-  c->depth_lookback = cv.take<uint32_t>(radix_lookback_words(cap));
-  c->scan_status = cv.take<unsigned long long>(scan_status_words(cap));
   c->cap_n = cap;
   return LMGS_OK;
 }
 
+int ensure_tiles(lmgs_context* c, int64_t t, cudaStream_t s) {
+  if (t <= c->cap_t && c->ranges) return LMGS_OK;
+  LMGS_CUDA(c, cudaStreamSynchronize(s));
+  LMGS_CUDA(c, c->tbuf.reserve(tile_bytes(t, c->sms)));
+  Carver cv{static_cast<char*>(c->tbuf.ptr)};
+  c->bin_hist = cv.take<uint32_t>(t * c->sms);
+  c->tile_count = cv.take<uint32_t>(t);
+  for (int i = 0; i < 3; ++i) c->lists[i] = cv.take<uint32_t>(t);
+  c->big_off = cv.take<uint32_t>(t);
+  c->ranges = cv.take<int2>(t);
+  c->cap_t = t;
+  return LMGS_OK;
+}
+
 int ensure_instances(lmgs_context* c, int64_t k, cudaStream_t s) {
-  if (k <= c->cap_k && c->inst_keys[0]) return LMGS_OK;
+  if (k <= c->cap_k && c->bucket) return LMGS_OK;
   LMGS_CUDA(c, cudaStreamSynchronize(s));
   LMGS_CUDA(c, c->ibuf.reserve(instance_bytes(k)));
   const int64_t cap = (int64_t)(c->ibuf.bytes >= instance_bytes(k + k / 4) ? k + k / 4 : k);
   Carver cv{static_cast<char*>(c->ibuf.ptr)};
-  c->inst_keys[0] = cv.take<uint64_t>(cap);
-  c->inst_keys[1] = cv.take<uint64_t>(cap);
-  c->inst_lookback = cv.take<uint32_t>(radix_lookback_words(cap));
+  c->bucket = cv.take<uint32_t>(cap);
+  c->sorted_ids = cv.take<uint32_t>(cap);
   c->cap_k = cap;
   return LMGS_OK;
 }
 
-int ensure_ranges(lmgs_context* c, int64_t tiles, cudaStream_t s) {
-  if (tiles <= c->ranges_cap && c->ranges) return LMGS_OK;
+int ensure_big(lmgs_context* c, int64_t k, cudaStream_t s) {
+  if (k <= c->cap_big && c->big_keys[0]) return LMGS_OK;
   LMGS_CUDA(c, cudaStreamSynchronize(s));
-  LMGS_CUDA(c, c->fbuf.reserve(align_up(sizeof(int2) * tiles)));
-  c->ranges = static_cast<int2*>(c->fbuf.ptr);
-  c->ranges_cap = (int64_t)(c->fbuf.bytes / sizeof(int2));
+  LMGS_CUDA(c, c->bbuf.reserve(big_bytes(k)));
+  Carver cv{static_cast<char*>(c->bbuf.ptr)};
+  c->big_keys[0] = cv.take<uint64_t>(k);
+  c->big_keys[1] = cv.take<uint64_t>(k);
+  c->big_vals[0] = cv.take<uint32_t>(k);
+  c->big_vals[1] = cv.take<uint32_t>(k);
+  c->big_lookback = cv.take<uint32_t>(radix_lookback_words(k));
+  c->cap_big = k;
   return LMGS_OK;
 }
 
@@ -247,13 +268,73 @@ int bits_for(int64_t v) {  // bits needed to represent values in [0, v)
   return b;
 }
 
+PreprocessArgs make_pre(lmgs_context* c, const lmgs_gaussians* g, const CamArgs& ca,
+                        const lmgs_settings* st, uint8_t* kept) {
+  PreprocessArgs pa{};
+  pa.means = g->means;
+  pa.quats = g->quats;
+  pa.scales = g->scales;
+  pa.logits = g->opacity_logits;
+  pa.sh = g->sh;
+  pa.n = g->count;
+  pa.sh_coeffs = g->sh_coeffs;
+  pa.eval_degree = st->sh_eval_degree < g->sh_degree ? st->sh_eval_degree : g->sh_degree;
+  pa.cam = ca;
+  pa.depth_keys32 = c->key32;
+  pa.depth_keys = c->key64;
+  pa.rects = c->rects;
+  pa.tile_counts = c->tile_counts;
+  pa.recs = c->recs;
+  pa.kept = kept;
+  pa.n_kept = &c->d_scal->n_kept;
+  return pa;
+}
+
+// oversized buckets: gather, onesweep on (bucket index << 32 | fp32 key), fix-up, scatter
+int sort_big_tiles(lmgs_context* c, const TileSortArgs& ta, int n_big, cudaStream_t s) {
+  // big list + ranges to host (rare path), offsets on host
+  std::vector<uint32_t> tiles(n_big);
+  std::vector<int2> rg(c->cap_t);
+  LMGS_CUDA(c, cudaMemcpyAsync(tiles.data(), c->lists[2], sizeof(uint32_t) * n_big,
+                               cudaMemcpyDeviceToHost, s));
+  LMGS_CUDA(c, cudaMemcpyAsync(rg.data(), ta.ranges, sizeof(int2) * c->stats.n_tiles,
+                               cudaMemcpyDeviceToHost, s));
+  LMGS_CUDA(c, cudaStreamSynchronize(s));
+  std::vector<uint32_t> off(n_big);
+  int64_t total = 0;
+  for (int b = 0; b < n_big; ++b) {
+    off[b] = (uint32_t)total;
+    total += rg[tiles[b]].y - rg[tiles[b]].x;
+  }
+  if (int r = ensure_big(c, total, s)) return r;
+  LMGS_CUDA(c, cudaMemcpyAsync(c->big_off, off.data(), sizeof(uint32_t) * n_big,
+                               cudaMemcpyHostToDevice, s));
+  launch_big_gather(ta, c->lists[2], n_big, c->big_off, c->big_keys[0], c->big_vals[0], s);
+  RadixSortBuffers rb{};
+  rb.keys[0] = c->big_keys[0];
+  rb.keys[1] = c->big_keys[1];
+  rb.key_bytes = 8;
+  rb.vals[0] = c->big_vals[0];
+  rb.vals[1] = c->big_vals[1];
+  rb.plan = &c->d_scal->big_plan;
+  rb.hist = c->d_scal->hist;
+  rb.lookback = c->big_lookback;
+  rb.counters = c->d_scal->counters;
+  rb.keys_result = &c->d_scal->slots.big_keys;
+  rb.vals_result = &c->d_scal->slots.big_vals;
+  radix_sort(rb, total, 0, (32 + bits_for(n_big) + 7) / 8, s);
+  launch_big_fixup(&c->d_scal->slots.big_keys, &c->d_scal->slots.big_vals, total, ta.key64, s);
+  launch_big_scatter(ta, c->lists[2], n_big, c->big_off, &c->d_scal->slots.big_vals, s);
+  ++c->big_views;
+  return LMGS_OK;
+}
+
 int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
                const lmgs_settings* st, const lmgs_frame* out, cudaStream_t s) {
   const bool timed = (st->flags & LMGS_FLAG_STAGE_TIMES) && c->events_ok;
   const CamArgs ca = make_cam(cam, st->tile_size);
   const int64_t n = g->count;
   const int64_t tiles = (int64_t)ca.tiles_x * ca.tiles_y;
-  const int64_t npix = (int64_t)cam->width * cam->height;
   c->stats = lmgs_stats{};
   c->stats.n_gaussians = n;
   c->stats.n_tiles = (int32_t)tiles;
@@ -265,122 +346,76 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
   c->last_prim_ids = g->prim_ids;
 
   if (int r = ensure_gaussians(c, n > 0 ? n : 1, s)) return r;
-  if (int r = ensure_ranges(c, tiles, s)) return r;
+  if (int r = ensure_tiles(c, tiles, s)) return r;
   int2* ranges = out->tile_ranges ? reinterpret_cast<int2*>(out->tile_ranges) : c->ranges;
-  LMGS_CUDA(c, cudaMemsetAsync(ranges, 0, sizeof(int2) * tiles, s));
+  c->last_ranges = ranges;
   LMGS_CUDA(c, cudaMemsetAsync(&c->d_scal->n_kept, 0, sizeof(unsigned long long), s));
-  LMGS_CUDA(c, cudaMemsetAsync(&c->d_scal->slots.fallback, 0, sizeof(int), s));
   if (out->touched && n > 0) LMGS_CUDA(c, cudaMemsetAsync(out->touched, 0, sizeof(int32_t) * n, s));
 
   if (timed) LMGS_CUDA(c, cudaEventRecord(c->ev[0], s));
-  PreprocessArgs pa{};
-  pa.means = g->means;
-  pa.quats = g->quats;
-  pa.scales = g->scales;
-  pa.logits = g->opacity_logits;
-  pa.sh = g->sh;
-  pa.n = n;
-  pa.sh_coeffs = g->sh_coeffs;
-  pa.eval_degree = st->sh_eval_degree < g->sh_degree ? st->sh_eval_degree : g->sh_degree;
-  pa.cam = ca;
-  pa.depth_keys32 = c->keys32[0];
-  pa.depth_keys = c->keys64[0];
-  pa.ids = c->ids[0];
-  pa.ids_fb = c->ids[2];
-  pa.rects = c->rects;
-  pa.tile_counts = c->tile_counts;
-  pa.recs = c->recs;
-  pa.kept = out->kept;
-  pa.n_kept = &c->d_scal->n_kept;
-  launch_preprocess(pa, s);
+  launch_preprocess(make_pre(c, g, ca, st, out->kept), s);
   if (timed) LMGS_CUDA(c, cudaEventRecord(c->ev[1], s));
 
-  // K2: depth order = fp32-key radix sort + exact fp64 fix-up of equal-key runs
-  DevSlots* slots = &c->d_scal->slots;
-  RadixSortBuffers db{};
-  db.keys[0] = c->keys32[0];
-  db.keys[1] = c->keys32[1];
-  db.key_bytes = 4;
-  db.vals[0] = c->ids[0];
-  db.vals[1] = c->ids[1];
-  db.plan = &c->d_scal->depth_plan;
-  db.hist = c->d_scal->hist[0];
-  db.lookback = c->depth_lookback;
-  db.counters = c->d_scal->counters[0];
-  db.keys_result = &slots->depth_keys32;
-  db.vals_result = &slots->sorted_ids;
-  radix_sort(db, n, 0, 4, s);
-  depth_fixup(&slots->depth_keys32, &slots->sorted_ids, n, c->keys64[0], &slots->fallback, s);
-  if (timed) LMGS_CUDA(c, cudaEventRecord(c->ev[2], s));
+  BinArgs bin{};
+  bin.rects = c->rects;
+  bin.counts = c->tile_counts;
+  bin.key32 = c->key32;
+  bin.n = n;
+  bin.tiles_x = ca.tiles_x;
+  bin.tiles = (int)tiles;
+  bin.ctas = c->sms;
+  bin.hist = c->bin_hist;
+  bin.tile_count = c->tile_count;
+  bin.ranges = ranges;
+  launch_bin_hist(bin, s);
 
-  // K3: tiles_touched in depth order -> exclusive offsets and K
-  scan_counts(c->tile_counts, &slots->sorted_ids, n, c->offsets, &c->d_scal->total,
-              c->scan_status, &c->d_scal->scan_counter, s);
+  TileScanArgs sa{};
+  sa.tile_count = c->tile_count;
+  sa.tiles = (int)tiles;
+  sa.small_cap = kSmallTileCap;
+  sa.medium_cap = kMediumTileCap;
+  sa.ranges = ranges;
+  for (int i = 0; i < 3; ++i) sa.lists[i] = c->lists[i];
+  sa.class_counts = c->d_scal->class_counts;
+  sa.total = &c->d_scal->total;
+  launch_scan_tiles(sa, s);
   LMGS_CUDA(c, cudaMemcpyAsync(c->h_pinned, &c->d_scal->total, sizeof(uint64_t),
                                cudaMemcpyDeviceToHost, s));
   LMGS_CUDA(c, cudaMemcpyAsync(c->h_pinned + 1, &c->d_scal->n_kept, sizeof(uint64_t),
                                cudaMemcpyDeviceToHost, s));
-  LMGS_CUDA(c, cudaMemcpyAsync(c->h_pinned + 2, &slots->fallback, sizeof(int),
+  LMGS_CUDA(c, cudaMemcpyAsync(c->h_pinned + 2, c->d_scal->class_counts, 4 * sizeof(uint32_t),
                                cudaMemcpyDeviceToHost, s));
   LMGS_CUDA(c, cudaGetLastError());
   LMGS_CUDA(c, cudaStreamSynchronize(s));
   const int64_t k = (int64_t)c->h_pinned[0];
   c->stats.n_instances = k;
   c->stats.n_kept = (int64_t)c->h_pinned[1];
-  if (*reinterpret_cast<int*>(c->h_pinned + 2)) {
-    // a run of > kFixupRun equal fp32 depths: exact 64-bit (depth, id) sort
-    ++c->fallbacks;
-    RadixSortBuffers fb{};
-    fb.keys[0] = c->keys64[0];
-    fb.keys[1] = c->keys64[1];
-    fb.key_bytes = 8;
-    fb.vals[0] = c->ids[2];
-    fb.vals[1] = c->ids[0];
-    fb.plan = &c->d_scal->fallback_plan;
-    fb.hist = c->d_scal->hist[1];
-    fb.lookback = c->depth_lookback;
-    fb.counters = c->d_scal->counters[1];
-    fb.keys_result = &slots->fb_keys;
-    fb.vals_result = &slots->sorted_ids;
-    radix_sort(fb, n, 0, 8, s);
-    scan_counts(c->tile_counts, &slots->sorted_ids, n, c->offsets, &c->d_scal->total,
-                c->scan_status, &c->d_scal->scan_counter, s);
-  }
-  if (k >= ((int64_t)1 << 30) - 1)
-    return fail(c, LMGS_ERR_UNSUPPORTED, "more than 2^30 tile instances in one view");
-  if (timed) LMGS_CUDA(c, cudaEventRecord(c->ev[3], s));
+  const uint32_t* cls = reinterpret_cast<const uint32_t*>(c->h_pinned + 2);
+  const int n_small = (int)cls[0], n_medium = (int)cls[1], n_big = (int)cls[2];
+  if (k >= ((int64_t)1 << 31) - 1)
+    return fail(c, LMGS_ERR_UNSUPPORTED, "more than 2^31 tile instances in one view");
+  if (timed) LMGS_CUDA(c, cudaEventRecord(c->ev[2], s));
 
   if (int r = ensure_instances(c, k > 0 ? k : 1, s)) return r;
-  DuplicateArgs da{};
-  da.slots = slots;
-  da.rects = c->rects;
-  da.tile_counts = c->tile_counts;
-  da.offsets = c->offsets;
-  da.n = n;
-  da.tiles_x = ca.tiles_x;
-  da.keys_out = c->inst_keys[0];
-  if (k > 0) launch_duplicate(da, s);
+  bin.bucket = c->bucket;
+  if (k > 0) launch_bin_place(bin, s);
+  if (timed) LMGS_CUDA(c, cudaEventRecord(c->ev[3], s));
+
+  TileSortArgs ta{};
+  ta.bucket = c->bucket;
+  ta.key32 = c->key32;
+  ta.ranges = ranges;
+  ta.key64 = c->key64;
+  ta.sorted_ids = c->sorted_ids;
+  launch_tile_sort(ta, c->lists[0], c->d_scal->class_counts + 0, n_small, 0, s);
+  launch_tile_sort(ta, c->lists[1], c->d_scal->class_counts + 1, n_medium, 1, s);
+  if (n_big > 0) {
+    if (int r = sort_big_tiles(c, ta, n_big, s)) return r;
+  }
   if (timed) LMGS_CUDA(c, cudaEventRecord(c->ev[4], s));
 
-  RadixSortBuffers kb{};
-  kb.keys[0] = c->inst_keys[0];
-  kb.keys[1] = c->inst_keys[1];
-  kb.key_bytes = 8;
-  kb.plan = &c->d_scal->tile_plan;
-  kb.hist = c->d_scal->hist[2];
-  kb.lookback = c->inst_lookback;
-  kb.counters = c->d_scal->counters[2];
-  kb.keys_result = &slots->inst_keys;
-  const int tile_bits = bits_for(tiles);
-  radix_sort(kb, k, 32, (tile_bits + 7) / 8, s);
-  if (timed) LMGS_CUDA(c, cudaEventRecord(c->ev[5], s));
-
-  launch_tile_ranges(slots, k, ranges, s);
-  if (timed) LMGS_CUDA(c, cudaEventRecord(c->ev[6], s));
-
   BlendArgs ba{};
-  ba.slots = slots;
-  ba.work_counter = &c->d_scal->blend_counter;
+  ba.sorted_ids = c->sorted_ids;
   ba.ranges = ranges;
   ba.recs = c->recs;
   ba.width = cam->width;
@@ -395,12 +430,12 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
   ba.trans = out->transmittance;
   ba.touched = out->touched;
   ba.n_processed = out->n_processed;
+  ba.work_counter = &c->d_scal->blend_counter;
   if (int r = launch_blend(ba, s)) return fail(c, r, "unsupported tile size");
   if (timed) {
-    LMGS_CUDA(c, cudaEventRecord(c->ev[7], s));
+    LMGS_CUDA(c, cudaEventRecord(c->ev[5], s));
     c->last_timed = true;
   }
-  (void)npix;
   LMGS_CUDA(c, cudaGetLastError());
   return LMGS_OK;
 }
@@ -417,9 +452,11 @@ int lmgs_context_create(int device, lmgs_context** out) {
   lmgs_context* c = new lmgs_context();
   c->device = device;
   DeviceGuard guard(device);
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  if (c->sms < 1) c->sms = 1;
   cudaError_t e = cudaMalloc(&c->d_scal, sizeof(Scalars));
   if (e == cudaSuccess) e = cudaMemset(c->d_scal, 0, sizeof(Scalars));
-  if (e == cudaSuccess) e = cudaHostAlloc(&c->h_pinned, 4 * sizeof(uint64_t), cudaHostAllocDefault);
+  if (e == cudaSuccess) e = cudaHostAlloc(&c->h_pinned, 8 * sizeof(uint64_t), cudaHostAllocDefault);
   if (e != cudaSuccess) {
     cudaGetLastError();
     lmgs_context_destroy(c);
@@ -437,8 +474,9 @@ void lmgs_context_destroy(lmgs_context* c) {
   DeviceGuard guard(c->device);
   cudaDeviceSynchronize();
   c->gbuf.release();
+  c->tbuf.release();
   c->ibuf.release();
-  c->fbuf.release();
+  c->bbuf.release();
   if (c->d_scal) cudaFree(c->d_scal);
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   for (int i = 0; i <= kNumStages; ++i)
@@ -486,12 +524,13 @@ int lmgs_copy_instances(lmgs_context* c, uint64_t* keys, int64_t* prim_ids, void
   if (!c) return LMGS_ERR_INVALID;
   DeviceGuard guard(c->device);
   InstanceExportArgs a{};
-  a.slots = &c->d_scal->slots;
+  a.ranges = c->last_ranges;
+  a.sorted_ids = c->sorted_ids;
   a.prim_ids = c->last_prim_ids;
-  a.k = c->stats.n_instances;
   a.keys_out = keys;
   a.prims_out = prim_ids;
-  launch_export_instances(a, static_cast<cudaStream_t>(stream));
+  if (c->stats.n_instances > 0)
+    launch_export_instances(a, c->stats.n_tiles, static_cast<cudaStream_t>(stream));
   LMGS_CUDA(c, cudaGetLastError());
   return LMGS_OK;
 }
@@ -506,25 +545,7 @@ int lmgs_project(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* ca
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t n = g->count;
   if (int r = ensure_gaussians(c, n > 0 ? n : 1, st)) return r;
-  PreprocessArgs pa{};
-  pa.means = g->means;
-  pa.quats = g->quats;
-  pa.scales = g->scales;
-  pa.logits = g->opacity_logits;
-  pa.sh = g->sh;
-  pa.n = n;
-  pa.sh_coeffs = g->sh_coeffs;
-  pa.eval_degree = s->sh_eval_degree < g->sh_degree ? s->sh_eval_degree : g->sh_degree;
-  pa.cam = make_cam(cam, s->tile_size);
-  pa.depth_keys32 = c->keys32[0];
-  pa.depth_keys = c->keys64[0];
-  pa.ids = c->ids[0];
-  pa.ids_fb = c->ids[2];
-  pa.rects = c->rects;
-  pa.tile_counts = c->tile_counts;
-  pa.recs = c->recs;
-  pa.kept = kept;
-  pa.n_kept = &c->d_scal->n_kept;
+  PreprocessArgs pa = make_pre(c, g, make_cam(cam, s->tile_size), s, kept);
   pa.dbg_mean2d = mean2d;
   pa.dbg_cov2d = cov2d;
   pa.dbg_depth = depth;

@@ -56,13 +56,12 @@ struct PreprocessArgs {
   // outputs
   uint32_t* depth_keys32;  // [n] bits(fp32 rd(depth)), 0xffffffff if culled
   uint64_t* depth_keys;    // [n] fp64 depth bits, kCulledKey if culled
-  uint32_t* ids;           // [n] iota (radix payload)
-  uint32_t* ids_fb;        // [n] iota (payload of the gated 64-bit fallback sort)
-  uint64_t* rects;       // [n]
-  uint32_t* tile_counts; // [n]
-  BlendRec* recs;        // [n]
-  uint8_t* kept;         // [n] nullable
+  uint64_t* rects;         // [n]
+  uint32_t* tile_counts;   // [n] tiles touched per Gaussian
+  BlendRec* recs;          // [n]
+  uint8_t* kept;           // [n] nullable
   unsigned long long* n_kept;  // scalar (atomic)
+  uint64_t* sh_wait;           // set in-kernel: mbarrier guarding staged SH (TMA path)
   // optional fp64 dump for lmgs_project
   double* dbg_mean2d;
   double* dbg_cov2d;
@@ -76,9 +75,9 @@ void launch_preprocess(const PreprocessArgs& a, cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // LSD radix sort (onesweep: one histogram pass + one scatter pass per digit
-// with decoupled look-back), 8-bit digits, u64 keys, optional u32 values.
+// with decoupled look-back), 8-bit digits, u32/u64 keys, optional u32 values.
 // The plan kernel detects trivial digits (all keys share it) and skips those
-// passes on the device; the result lands in buffer index plan->result.
+// passes on the device; the result buffers are published in device slots.
 
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
@@ -114,50 +113,83 @@ size_t radix_lookback_words(int64_t capacity);
 void radix_sort(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_passes,
                 cudaStream_t s);
 
-// Runs of equal fp32 depth keys (length <= kFixupRun) re-ordered by the exact
-// (fp64 depth bits, id); a longer run sets *fallback = 1.
-constexpr int kFixupRun = 32;
-void depth_fixup(void* const* keys_ptr, void* const* ids_ptr, int64_t n,
-                 const uint64_t* depth64, int* fallback, cudaStream_t s);
-
-// Exclusive scan of counts gathered through a permutation:
-//   offsets[r] = sum_{r' < r} counts[perm[r']],  *total = sum over all r.
-// perm_ptr == nullptr -> identity, else *perm_ptr (device slot) is the perm.
-constexpr int kScanThreads = 256;
-constexpr int kScanItems = 16;
-size_t scan_status_words(int64_t n);
-void scan_counts(const uint32_t* counts, void* const* perm_ptr, int64_t n, uint64_t* offsets,
-                 uint64_t* total, unsigned long long* status, uint32_t* counter, cudaStream_t s);
-
-// Device-side slots naming where each sort's result landed (written by the
-// plan kernels, read by the consumers) so the pipeline never syncs on them.
+// Device-side slots naming where a sort's result landed (written by the plan
+// kernel, read by consumers) so the pipeline never syncs on it.
 struct DevSlots {
-  void* sorted_ids;   // uint32_t[n]: ids in (depth, id) order
-  void* depth_keys32; // uint32_t[n]: fp32 depth keys in sorted order
-  void* fb_keys;      // fallback 64-bit sort keys (unused downstream)
-  void* inst_keys;    // uint64_t[K]: tile-sorted instance keys
-  int fallback;       // depth fix-up found a run > kFixupRun
-  int pad;
+  void* big_keys;  // oversized-bucket sort result keys
+  void* big_vals;  // oversized-bucket sort result ids
 };
 
 // ---------------------------------------------------------------------------
-// raster stages
+// tile binning (tiles.cu)
 
-struct DuplicateArgs {
-  const DevSlots* slots;
+// runs of equal fp32 depth keys up to this length are fixed up in registers
+constexpr int kFixupRun = 32;
+constexpr int kSmallTileCap = 2048;    // bucket sorted by a 256-thread CTA, 32 KB smem
+constexpr int kMediumTileCap = 16384;  // bucket sorted by a 512-thread CTA, 208 KB smem
+
+// K3a/K3b/K4: per-CTA (one per SM) tile histograms and placement
+constexpr int kBinThreads = 1024;
+constexpr int kSlabTiles = 49152;  // tile counters per shared-memory slab (192 KB)
+
+struct BinArgs {
   const uint64_t* rects;
-  const uint32_t* tile_counts;
-  const uint64_t* offsets;  // rank-order exclusive offsets
+  const uint32_t* counts;   // tiles touched per Gaussian
+  const uint32_t* key32;
   int64_t n;
   int32_t tiles_x;
-  uint64_t* keys_out;      // [K] tile << 32 | rank
+  int32_t tiles;
+  int32_t ctas;             // Gaussian slices (CTAs) of K3a / K4
+  uint32_t* hist;           // [ctas][tiles] counts, then per-(cta, tile) offsets
+  uint32_t* tile_count;     // [tiles] out of K3b
+  const int2* ranges;       // K4 input
+  uint32_t* bucket;         // [K] out of K4: Gaussian ids, arbitrary order within a tile
 };
-void launch_duplicate(const DuplicateArgs& a, cudaStream_t s);
+size_t bin_smem_bytes(int tiles);
+void launch_bin_hist(const BinArgs& a, cudaStream_t s);   // K3a + K3b
+void launch_bin_place(const BinArgs& a, cudaStream_t s);  // K4
 
-void launch_tile_ranges(const DevSlots* slots, int64_t k, int2* ranges, cudaStream_t s);
+struct TileScanArgs {
+  const uint32_t* tile_count;  // [tiles]
+  int tiles;
+  int small_cap, medium_cap;
+  int2* ranges;                // [tiles] out: [start, end)
+  uint32_t* lists[3];          // [tiles] each: tile ids of class small/medium/big
+  uint32_t* class_counts;      // [3]
+  uint64_t* total;             // K
+};
+void launch_scan_tiles(const TileScanArgs& a, cudaStream_t s);
+
+struct TileSortArgs {
+  const uint32_t* bucket;
+  const uint32_t* key32;  // [n] fp32 depth keys (L2-resident gather)
+  const int2* ranges;
+  const uint64_t* key64;  // [n] fp64 depth bits (exact tie order)
+  uint32_t* sorted_ids;   // [K] out: per-tile lists in (depth, id) order
+};
+void launch_tile_sort(const TileSortArgs& a, const uint32_t* tile_list,
+                      const uint32_t* list_count, int n_list, int cls, cudaStream_t s);
+void launch_big_gather(const TileSortArgs& a, const uint32_t* big_list, int n_big,
+                       const uint32_t* big_off, uint64_t* keys, uint32_t* vals, cudaStream_t s);
+void launch_big_fixup(void* const* keys_ptr, void* const* vals_ptr, int64_t n,
+                      const uint64_t* key64, cudaStream_t s);
+void launch_big_scatter(const TileSortArgs& a, const uint32_t* big_list, int n_big,
+                        const uint32_t* big_off, void* const* vals_ptr, cudaStream_t s);
+
+struct InstanceExportArgs {
+  const int2* ranges;
+  const uint32_t* sorted_ids;
+  const int64_t* prim_ids;  // nullable: original ids
+  uint64_t* keys_out;
+  int64_t* prims_out;
+};
+void launch_export_instances(const InstanceExportArgs& a, int tiles, cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// blend (blend.cu) and compositing (raster.cu)
 
 struct BlendArgs {
-  const DevSlots* slots;
+  const uint32_t* sorted_ids;
   const int2* ranges;
   const BlendRec* recs;
   int32_t width, height, tile_size, tiles_x, tiles_y;
@@ -174,15 +206,6 @@ int launch_blend(const BlendArgs& a, cudaStream_t s);  // returns 0 or LMGS_ERR_
 
 void launch_fill_background(float* rgb, float* alpha, float* depth, float* trans, int64_t n_pix,
                             const float bg[3], cudaStream_t s);
-
-struct InstanceExportArgs {
-  const DevSlots* slots;
-  const int64_t* prim_ids;  // nullable: original ids
-  int64_t k;
-  uint64_t* keys_out;
-  int64_t* prims_out;
-};
-void launch_export_instances(const InstanceExportArgs& a, cudaStream_t s);
 
 constexpr int kMaxCompositeBlocks = 64;
 // `order` is a host array (n_blocks <= kMaxCompositeBlocks), passed by value.

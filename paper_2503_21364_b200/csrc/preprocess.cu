@@ -51,6 +51,7 @@ __device__ __forceinline__ void axis_range(double lo, double hi, int size, int t
 
 // Colour along centre->mean; degree <= 1 is eval_sh_colors (129-142),
 // degrees 2-3 extend it with the standard real SH basis, clamp(0,1), no +0.5.
+template <bool SMEM>
 __device__ __forceinline__ void sh_color(const float* __restrict__ sh, int ncoef, int deg,
                                          float x, float y, float z, float out[3]) {
   const float C0 = (float)kShC0, C1 = (float)kShC1;
@@ -63,14 +64,14 @@ __device__ __forceinline__ void sh_color(const float* __restrict__ sh, int ncoef
 #pragma unroll
     for (int q = 0; q < 12; ++q) {
       if (4 * q < nload) {
-        float4 f = __ldg(sh4 + q);
+        const float4 f = SMEM ? sh4[q] : __ldg(sh4 + q);
         v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
       }
     }
   } else {
 #pragma unroll
     for (int q = 0; q < 48; ++q)
-      if (q < nload) v[q] = __ldg(sh + q);
+      if (q < nload) v[q] = SMEM ? sh[q] : __ldg(sh + q);
   }
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) c[ch] = C0 * v[ch];
@@ -107,19 +108,49 @@ __device__ __forceinline__ void sh_color(const float* __restrict__ sh, int ncoef
   for (int ch = 0; ch < 3; ++ch) out[ch] = fminf(fmaxf(c[ch], 0.0f), 1.0f);
 }
 
-__global__ void __launch_bounds__(256) k_preprocess(PreprocessArgs a) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+constexpr int kPreThreads = 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// One Gaussian.  Inputs arrive as values (from shared memory staged by TMA or
+// straight from global memory); `sh` points at its coefficients.
+template <bool SMEM>
+__device__ __forceinline__ bool process_one(const PreprocessArgs& a, int64_t i, double m0, double m1,
+                                            double m2, float4 q, double s0, double s1, double s2,
+                                            float logit, const float* sh) {
   bool keep = false;
-  if (i < a.n) {
+  {
     const CamArgs& cam = a.cam;
-    const double m0 = a.means[3 * i], m1 = a.means[3 * i + 1], m2 = a.means[3 * i + 2];
     // p = means @ r_wc.T + t_wc (195): MKL FMA chain, then + t
     const double x = mkl_dot3(m0, cam.r[0], m1, cam.r[1], m2, cam.r[2]) + cam.t[0];
     const double y = mkl_dot3(m0, cam.r[3], m1, cam.r[4], m2, cam.r[5]) + cam.t[1];
     const double z = mkl_dot3(m0, cam.r[6], m1, cam.r[7], m2, cam.r[8]) + cam.t[2];
     keep = z > kNearCullZ;  // 196
-    a.ids[i] = (uint32_t)i;
-    a.ids_fb[i] = (uint32_t)i;
     if (a.kept) a.kept[i] = keep;
     if (!keep) {
       a.depth_keys[i] = kCulledKey;
@@ -130,7 +161,6 @@ __global__ void __launch_bounds__(256) k_preprocess(PreprocessArgs a) {
       const double mx = cam.fx * x / z + cam.cx;  // 201
       const double my = cam.fy * y / z + cam.cy;
       // quat_to_rotmat (93-102)
-      const float4 q = __ldg(reinterpret_cast<const float4*>(a.quats) + i);
       const double qw = q.x, qx = q.y, qy = q.z, qz = q.w;
       const double nr = sqrt(((qw * qw + qx * qx) + qy * qy) + qz * qz);
       const double w = qw / nr, X = qx / nr, Y = qy / nr, Z = qz / nr;
@@ -141,7 +171,6 @@ __global__ void __launch_bounds__(256) k_preprocess(PreprocessArgs a) {
       const double r20 = 2 * (X * Z - w * Y), r21 = 2 * (Y * Z + w * X),
                    r22 = 1 - 2 * (X * X + Y * Y);
       // covariance_3d (105-117): M = R * s[None,:], Sigma = M M^T
-      const double s0 = a.scales[3 * i], s1 = a.scales[3 * i + 1], s2 = a.scales[3 * i + 2];
       const double M00 = r00 * s0, M01 = r01 * s1, M02 = r02 * s2;
       const double M10 = r10 * s0, M11 = r11 * s1, M12 = r12 * s2;
       const double M20 = r20 * s0, M21 = r21 * s1, M22 = r22 * s2;
@@ -195,15 +224,15 @@ __global__ void __launch_bounds__(256) k_preprocess(PreprocessArgs a) {
       // conic (_blend 309-310), fp64 then pre-scaled to the exp2 domain in fp32
       const double det = ca * cc - cb * cb;
       const double ica = cc / det, icb = -cb / det, icc = ca / det;
-      const float logit = a.logits[i];
       const float log2_alpha =
           logit < -15.0f ? logit * (float)kLog2e : -log2f(1.0f + expf(-logit));
       float col[3] = {0.f, 0.f, 0.f};
+      if (SMEM) mbar_wait(a.sh_wait, 0);
       if (cnt || a.dbg_colors) {
         const double dx = m0 - cam.center[0], dy = m1 - cam.center[1], dz = m2 - cam.center[2];
         double nrm = sqrt((dx * dx + dy * dy) + dz * dz);
         nrm = fmax(nrm, 1e-12);
-        sh_color(a.sh + (int64_t)i * a.sh_coeffs * 3, a.sh_coeffs, a.eval_degree,
+        sh_color<SMEM>(sh, a.sh_coeffs, a.eval_degree,
                  (float)(dx / nrm), (float)(dy / nrm), (float)(dz / nrm), col);
       }
       BlendRec rec;
@@ -234,18 +263,98 @@ __global__ void __launch_bounds__(256) k_preprocess(PreprocessArgs a) {
       }
     }
   }
-  // kept count: warp ballot + one atomic per warp
+  return keep;
+}
+
+__device__ __forceinline__ void count_kept(const PreprocessArgs& a, bool keep) {
   const unsigned ballot = __ballot_sync(0xffffffffu, keep);
   if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(a.n_kept, (unsigned long long)__popc(ballot));
 }
+
+// direct loads (tail block, unaligned inputs)
+__global__ void __launch_bounds__(256) k_preprocess_direct(PreprocessArgs a, int64_t first) {
+  const int64_t i = first + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool keep = false;
+  if (i < a.n) {
+    const float4 q = __ldg(reinterpret_cast<const float4*>(a.quats) + i);
+    keep = process_one<false>(a, i, a.means[3 * i], a.means[3 * i + 1], a.means[3 * i + 2], q,
+                              a.scales[3 * i], a.scales[3 * i + 1], a.scales[3 * i + 2],
+                              a.logits[i], a.sh + i * a.sh_coeffs * 3);
+  }
+  count_kept(a, keep);
+}
+
+// ---------------------------------------------------------------------------
+// TMA-staged path: one thread issues cp.async.bulk copies of the block's
+// means / quats / scales / logits (one mbarrier) and of its SH coefficients
+// (a second mbarrier); the SH bytes stream into shared memory while the fp64
+// geometry of the block is being computed.
+
+__global__ void __launch_bounds__(kPreThreads, 2) k_preprocess_tma(PreprocessArgs a) {
+  extern __shared__ __align__(128) float smem_f[];
+  float* s_means = smem_f;                       // [256*3]
+  float* s_quats = s_means + kPreThreads * 3;    // [256*4]
+  float* s_scales = s_quats + kPreThreads * 4;   // [256*3]
+  float* s_logits = s_scales + kPreThreads * 3;  // [256]
+  float* s_sh = s_logits + kPreThreads;          // [256*ncoef*3]
+  __shared__ __align__(8) uint64_t s_bar[2];
+  const int tid = threadIdx.x;
+  const int64_t i0 = (int64_t)blockIdx.x * kPreThreads;
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t sh_bytes = (uint32_t)(kPreThreads * a.sh_coeffs * 3 * 4);
+  if (tid == 0) {
+    mbar_expect_tx(&s_bar[0], kPreThreads * (12 + 16 + 12 + 4));
+    bulk_g2s(s_means, a.means + i0 * 3, kPreThreads * 12, &s_bar[0]);
+    bulk_g2s(s_quats, a.quats + i0 * 4, kPreThreads * 16, &s_bar[0]);
+    bulk_g2s(s_scales, a.scales + i0 * 3, kPreThreads * 12, &s_bar[0]);
+    bulk_g2s(s_logits, a.logits + i0, kPreThreads * 4, &s_bar[0]);
+    mbar_expect_tx(&s_bar[1], sh_bytes);
+    bulk_g2s(s_sh, a.sh + i0 * a.sh_coeffs * 3, sh_bytes, &s_bar[1]);
+  }
+  mbar_wait(&s_bar[0], 0);
+  const int64_t i = i0 + tid;
+  const float4 q = reinterpret_cast<const float4*>(s_quats)[tid];
+  // the SH wait happens inside process_one just before the colour is needed
+  a.sh_wait = &s_bar[1];
+  const bool keep =
+      process_one<true>(a, i, s_means[3 * tid], s_means[3 * tid + 1], s_means[3 * tid + 2], q,
+                        s_scales[3 * tid], s_scales[3 * tid + 1], s_scales[3 * tid + 2],
+                        s_logits[tid], s_sh + tid * a.sh_coeffs * 3);
+  count_kept(a, keep);
+  // every thread must observe the SH barrier before the block may exit
+  mbar_wait(&s_bar[1], 0);
+}
+
 
 }  // namespace
 
 void launch_preprocess(const PreprocessArgs& a, cudaStream_t s) {
   if (a.n <= 0) return;
-  const int threads = 256;
-  const int64_t blocks = (a.n + threads - 1) / threads;
-  k_preprocess<<<(unsigned)blocks, threads, 0, s>>>(a);
+  // full blocks through TMA when every chunk is 16-byte aligned and sized
+  const bool aligned =
+      ((reinterpret_cast<uintptr_t>(a.means) | reinterpret_cast<uintptr_t>(a.quats) |
+        reinterpret_cast<uintptr_t>(a.scales) | reinterpret_cast<uintptr_t>(a.logits) |
+        reinterpret_cast<uintptr_t>(a.sh)) & 15) == 0;
+  const int64_t full = aligned ? a.n / kPreThreads : 0;
+  if (full > 0) {
+    const size_t smem = sizeof(float) * kPreThreads * (3 + 4 + 3 + 1 + 3 * a.sh_coeffs);
+    static size_t set = 0;
+    if (smem > set) {
+      cudaFuncSetAttribute(k_preprocess_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      set = smem;
+    }
+    k_preprocess_tma<<<(unsigned)full, kPreThreads, smem, s>>>(a);
+  }
+  const int64_t first = full * kPreThreads;
+  const int64_t rest = a.n - first;
+  if (rest > 0)
+    k_preprocess_direct<<<(unsigned)((rest + 255) / 256), 256, 0, s>>>(a, first);
 }
 
 }  // namespace lmgs

@@ -1,17 +1,9 @@
-// Device-wide LSD radix sort (onesweep) and a single-pass exclusive scan.
+// Device-wide LSD radix sort (onesweep).
 //
-// Used per view for
-//   K2  depth order: _sort_order's np.lexsort((prim_id, depth)) over all
-//       near-kept splats (gaussian_core.py:277-283).  Primary pass set on a
-//       32-bit key = bits(fp32 round-down(depth)) (monotone in the fp64
-//       depth), stable on the id payload; then k_depth_fixup re-orders every
-//       run of equal fp32 keys by the exact (fp64 depth, id) pair.  A run longer
-//       than kFixupRun sets a device flag that enables a full 64-bit-key sort
-//       (launched unconditionally, gated on the device) — exact order always,
-//       fast path for real scenes.
-//   K5  tile sort: keys (tile << 32 | rank) stably on the tile bits only,
-//       turning the rank-ordered instance stream into per-tile lists in
-//       (depth, id) order (rasterize's per-tile _sort_order, 392).
+// Used for tile buckets too large for one CTA's shared memory (tiles.cu):
+// keys (bucket index << 32 | fp32 depth bits), id payload; equal-key runs are
+// then fixed up by the exact (fp64 depth, id) pair — rasterize's per-tile
+// _sort_order (gaussian_core.py:392 -> 277-283).
 //
 // Per sort: one histogram kernel computes every digit's global histogram in a
 // single read; a 1-block plan kernel scans them, marks digits all keys share
@@ -40,14 +32,6 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
 }
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
@@ -273,132 +257,6 @@ constexpr size_t onesweep_smem() {
   return sizeof(K) * kSortTile + sizeof(uint32_t) * kSortTile;
 }
 
-// ---------------------------------------------------------------------------
-// depth fix-up: order each run of equal fp32 keys by (fp64 depth, id)
-
-__global__ void __launch_bounds__(256) k_depth_fixup(void* const* keys_ptr,
-                                                     void* const* ids_ptr, int64_t n,
-                                                     const uint64_t* __restrict__ depth64,
-                                                     int* fallback) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint32_t* keys = static_cast<const uint32_t*>(*keys_ptr);
-  uint32_t* ids = static_cast<uint32_t*>(*ids_ptr);
-  const uint32_t k = keys[i];
-  if (k == 0xffffffffu) return;                    // culled tail
-  if (i > 0 && keys[i - 1] == k) return;           // not a run start
-  if (i + 1 >= n || keys[i + 1] != k) return;      // run of length 1
-  int len = 2;
-  while (i + len < n && keys[i + len] == k && len <= kFixupRun) ++len;
-  if (len > kFixupRun) {
-    atomicExch(fallback, 1);
-    return;
-  }
-  uint64_t dk[kFixupRun];
-  uint32_t id[kFixupRun];
-  for (int a = 0; a < len; ++a) {
-    id[a] = ids[i + a];
-    dk[a] = depth64[id[a]];
-  }
-  for (int a = 1; a < len; ++a) {  // insertion sort by (depth bits, id)
-    const uint64_t kd = dk[a];
-    const uint32_t ki = id[a];
-    int b = a - 1;
-    while (b >= 0 && (dk[b] > kd || (dk[b] == kd && id[b] > ki))) {
-      dk[b + 1] = dk[b];
-      id[b + 1] = id[b];
-      --b;
-    }
-    dk[b + 1] = kd;
-    id[b + 1] = ki;
-  }
-  for (int a = 0; a < len; ++a) ids[i + a] = id[a];
-}
-
-// ---------------------------------------------------------------------------
-// exclusive scan of counts[perm[r]] (decoupled look-back, u64 status words)
-
-constexpr unsigned long long kScanAgg = 1ull << 62;
-constexpr unsigned long long kScanIncl = 2ull << 62;
-constexpr unsigned long long kScanMask = (1ull << 62) - 1;
-constexpr int kScanTile = kScanThreads * kScanItems;
-
-__global__ void __launch_bounds__(kScanThreads) k_scan(const uint32_t* __restrict__ counts,
-                                                       void* const* perm_ptr, int64_t n,
-                                                       uint64_t* __restrict__ offsets,
-                                                       uint64_t* total,
-                                                       unsigned long long* status,
-                                                       uint32_t* counter) {
-  __shared__ uint32_t s_bid;
-  __shared__ unsigned long long s_warp[kScanThreads / 32];
-  __shared__ unsigned long long s_excl;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_bid = atomicAdd(counter, 1u);
-  __syncthreads();
-  const uint32_t bid = s_bid;
-  const int64_t base = (int64_t)bid * kScanTile + (int64_t)tid * kScanItems;
-  const uint32_t* perm = perm_ptr ? static_cast<const uint32_t*>(*perm_ptr) : nullptr;
-  uint32_t v[kScanItems];
-  unsigned long long local = 0;
-#pragma unroll
-  for (int j = 0; j < kScanItems; ++j) {
-    const int64_t r = base + j;
-    uint32_t c = 0;
-    if (r < n) c = counts[perm ? perm[r] : r];
-    v[j] = c;
-    local += c;
-  }
-  unsigned long long incl = local;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, off);
-    if (lane >= off) incl += o;
-  }
-  if (lane == 31) s_warp[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    unsigned long long wv = lane < kScanThreads / 32 ? s_warp[lane] : 0;
-    unsigned long long wi = wv;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const unsigned long long o = __shfl_up_sync(0xffffffffu, wi, off);
-      if (lane >= off) wi += o;
-    }
-    if (lane < kScanThreads / 32) s_warp[lane] = wi - wv;
-    const unsigned long long block_total = __shfl_sync(0xffffffffu, wi, kScanThreads / 32 - 1);
-    if (lane == 0) {
-      unsigned long long excl = 0;
-      if (bid == 0) {
-        st_release64(status, kScanIncl | block_total);
-      } else {
-        st_release64(status + bid, kScanAgg | block_total);
-        int64_t look = (int64_t)bid - 1;
-        while (true) {
-          unsigned long long s;
-          do {
-            s = ld_acquire64(status + look);
-          } while ((s & ~kScanMask) == 0);
-          excl += s & kScanMask;
-          if ((s & ~kScanMask) == kScanIncl) break;
-          --look;
-        }
-        st_release64(status + bid, kScanIncl | (excl + block_total));
-      }
-      s_excl = excl;
-      const int64_t nblocks = (n + kScanTile - 1) / kScanTile;
-      if ((int64_t)bid == nblocks - 1) *total = excl + block_total;
-    }
-  }
-  __syncthreads();
-  unsigned long long run = s_excl + s_warp[warp] + (incl - local);
-#pragma unroll
-  for (int j = 0; j < kScanItems; ++j) {
-    const int64_t r = base + j;
-    if (r < n) offsets[r] = run;
-    run += v[j];
-  }
-}
-
 template <typename K>
 void radix_sort_impl(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_passes,
                      cudaStream_t s) {
@@ -441,32 +299,6 @@ void radix_sort(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_passe
                 cudaStream_t s) {
   if (b.key_bytes == 4) radix_sort_impl<uint32_t>(b, n, begin_bit, n_passes, s);
   else radix_sort_impl<uint64_t>(b, n, begin_bit, n_passes, s);
-}
-
-void depth_fixup(void* const* keys_ptr, void* const* ids_ptr, int64_t n,
-                 const uint64_t* depth64, int* fallback, cudaStream_t s) {
-  if (n <= 0) return;
-  k_depth_fixup<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(keys_ptr, ids_ptr, n, depth64,
-                                                            fallback);
-}
-
-size_t scan_status_words(int64_t n) {
-  const int64_t blocks = (n + kScanTile - 1) / kScanTile;
-  return (size_t)(blocks > 0 ? blocks : 1);
-}
-
-void scan_counts(const uint32_t* counts, void* const* perm_ptr, int64_t n, uint64_t* offsets,
-                 uint64_t* total, unsigned long long* status, uint32_t* counter,
-                 cudaStream_t s) {
-  const int64_t blocks = (n + kScanTile - 1) / kScanTile;
-  cudaMemsetAsync(counter, 0, sizeof(uint32_t), s);
-  if (blocks == 0) {
-    cudaMemsetAsync(total, 0, sizeof(uint64_t), s);
-    return;
-  }
-  cudaMemsetAsync(status, 0, sizeof(unsigned long long) * blocks, s);
-  k_scan<<<(unsigned)blocks, kScanThreads, 0, s>>>(counts, perm_ptr, n, offsets, total, status,
-                                                   counter);
 }
 
 }  // namespace lmgs
