@@ -73,7 +73,7 @@ size_t gaussian_bytes(int64_t n) {
   return b + 8 * kAlign;
 }
 size_t tile_bytes(int64_t t, int ctas) {
-  return align_up(sizeof(uint32_t) * t * ctas) + 6 * align_up(sizeof(uint32_t) * t) +
+  return align_up(sizeof(uint32_t) * t * ctas) + 5 * align_up(sizeof(uint32_t) * t) +
          align_up(sizeof(int2) * t) + 8 * kAlign;
 }
 size_t instance_bytes(int64_t k) {
@@ -118,7 +118,7 @@ struct lmgs_context {
   // per-tile arena
   uint32_t* bin_hist = nullptr;   // [sms][tiles]
   uint32_t* tile_count = nullptr;
-  uint32_t* lists[4] = {nullptr, nullptr, nullptr, nullptr};
+  uint32_t* lists[3] = {nullptr, nullptr, nullptr};
   uint32_t* big_off = nullptr;
   int2* ranges = nullptr;
   // per-instance arena
@@ -186,7 +186,7 @@ int ensure_tiles(lmgs_context* c, int64_t t, cudaStream_t s) {
   Carver cv{static_cast<char*>(c->tbuf.ptr)};
   c->bin_hist = cv.take<uint32_t>(t * c->sms);
   c->tile_count = cv.take<uint32_t>(t);
-  for (int i = 0; i < 4; ++i) c->lists[i] = cv.take<uint32_t>(t);
+  for (int i = 0; i < 3; ++i) c->lists[i] = cv.take<uint32_t>(t);
   c->big_off = cv.take<uint32_t>(t);
   c->ranges = cv.take<int2>(t);
   c->cap_t = t;
@@ -295,7 +295,7 @@ int sort_big_tiles(lmgs_context* c, const TileSortArgs& ta, int n_big, cudaStrea
   // big list + ranges to host (rare path), offsets on host
   std::vector<uint32_t> tiles(n_big);
   std::vector<int2> rg(c->cap_t);
-  LMGS_CUDA(c, cudaMemcpyAsync(tiles.data(), c->lists[3], sizeof(uint32_t) * n_big,
+  LMGS_CUDA(c, cudaMemcpyAsync(tiles.data(), c->lists[2], sizeof(uint32_t) * n_big,
                                cudaMemcpyDeviceToHost, s));
   LMGS_CUDA(c, cudaMemcpyAsync(rg.data(), ta.ranges, sizeof(int2) * c->stats.n_tiles,
                                cudaMemcpyDeviceToHost, s));
@@ -309,7 +309,7 @@ int sort_big_tiles(lmgs_context* c, const TileSortArgs& ta, int n_big, cudaStrea
   if (int r = ensure_big(c, total, s)) return r;
   LMGS_CUDA(c, cudaMemcpyAsync(c->big_off, off.data(), sizeof(uint32_t) * n_big,
                                cudaMemcpyHostToDevice, s));
-  launch_big_gather(ta, c->lists[3], n_big, c->big_off, c->big_keys[0], c->big_vals[0], s);
+  launch_big_gather(ta, c->lists[2], n_big, c->big_off, c->big_keys[0], c->big_vals[0], s);
   RadixSortBuffers rb{};
   rb.keys[0] = c->big_keys[0];
   rb.keys[1] = c->big_keys[1];
@@ -324,7 +324,7 @@ int sort_big_tiles(lmgs_context* c, const TileSortArgs& ta, int n_big, cudaStrea
   rb.vals_result = &c->d_scal->slots.big_vals;
   radix_sort(rb, total, 0, (32 + bits_for(n_big) + 7) / 8, s);
   launch_big_fixup(&c->d_scal->slots.big_keys, &c->d_scal->slots.big_vals, total, ta.key64, s);
-  launch_big_scatter(ta, c->lists[3], n_big, c->big_off, &c->d_scal->slots.big_vals, s);
+  launch_big_scatter(ta, c->lists[2], n_big, c->big_off, &c->d_scal->slots.big_vals, s);
   ++c->big_views;
   return LMGS_OK;
 }
@@ -372,8 +372,10 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
   TileScanArgs sa{};
   sa.tile_count = c->tile_count;
   sa.tiles = (int)tiles;
+  sa.small_cap = kSmallTileCap;
+  sa.medium_cap = kMediumTileCap;
   sa.ranges = ranges;
-  for (int i = 0; i < 4; ++i) sa.lists[i] = c->lists[i];
+  for (int i = 0; i < 3; ++i) sa.lists[i] = c->lists[i];
   sa.class_counts = c->d_scal->class_counts;
   sa.total = &c->d_scal->total;
   launch_scan_tiles(sa, s);
@@ -389,8 +391,7 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
   c->stats.n_instances = k;
   c->stats.n_kept = (int64_t)c->h_pinned[1];
   const uint32_t* cls = reinterpret_cast<const uint32_t*>(c->h_pinned + 2);
-  const int n_small = (int)cls[0], n_mid = (int)cls[1], n_medium = (int)cls[2];
-  const int n_big = (int)cls[3];
+  const int n_small = (int)cls[0], n_medium = (int)cls[1], n_big = (int)cls[2];
   if (k >= ((int64_t)1 << 31) - 1)
     return fail(c, LMGS_ERR_UNSUPPORTED, "more than 2^31 tile instances in one view");
   if (timed) LMGS_CUDA(c, cudaEventRecord(c->ev[2], s));
@@ -407,8 +408,7 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
   ta.key64 = c->key64;
   ta.sorted_ids = c->sorted_ids;
   launch_tile_sort(ta, c->lists[0], c->d_scal->class_counts + 0, n_small, 0, s);
-  launch_tile_sort(ta, c->lists[1], c->d_scal->class_counts + 1, n_mid, 1, s);
-  launch_tile_sort(ta, c->lists[2], c->d_scal->class_counts + 2, n_medium, 2, s);
+  launch_tile_sort(ta, c->lists[1], c->d_scal->class_counts + 1, n_medium, 1, s);
   if (n_big > 0) {
     if (int r = sort_big_tiles(c, ta, n_big, s)) return r;
   }

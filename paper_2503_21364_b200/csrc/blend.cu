@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(256) k_blend(BlendArgs a) {
 
 constexpr int kWarpsPerBlock16 = 8;
 
-__global__ void __launch_bounds__(256, 3) k_blend16w(BlendArgs a, int n_items) {
+__global__ void __launch_bounds__(256, 4) k_blend16w(BlendArgs a, int n_items) {
   __shared__ float4 s_geo[kWarpsPerBlock16][32];   // mx_local, my_local, qa, qb
   __shared__ float4 s_geo2[kWarpsPerBlock16][32];  // qc, log2_alpha, r2_lo, r2_hi
   __shared__ float4 s_col[kWarpsPerBlock16][32];   // r, g, b, z
@@ -289,27 +289,14 @@ __global__ void __launch_bounds__(256, 3) k_blend16w(BlendArgs a, int n_items) {
     const int2 range = a.ranges[tile];
     float T = valid ? 1.0f : 0.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, D = 0.f;
     int last = -1;
-    // software pipeline: the geometry sector of chunk c+1 is in flight while
-    // chunk c is blended
-    uint32_t nid = 0;
-    float4 ng0 = make_float4(0.f, 0.f, 0.f, 0.f), ng1 = ng0;
-    if (range.x + lane < range.y) {
-      nid = list[range.x + lane];
-      ng0 = __ldg(rec4 + 4 * (size_t)nid);
-      ng1 = __ldg(rec4 + 4 * (size_t)nid + 1);
-    }
     for (int b = range.x; b < range.y; b += 32) {
       if (!__any_sync(0xffffffffu, T >= kTermEpsF)) break;
       const int j = b + lane;
-      const uint32_t id = nid;
-      const float4 g0 = ng0, g1 = ng1;
-      if (j + 32 < range.y) {
-        nid = list[j + 32];
-        ng0 = __ldg(rec4 + 4 * (size_t)nid);
-        ng1 = __ldg(rec4 + 4 * (size_t)nid + 1);
-      }
       bool hit = false;
       if (j < range.y) {
+        const uint32_t id = list[j];
+        const float4 g0 = __ldg(rec4 + 4 * (size_t)id);      // mx, my (fp64)
+        const float4 g1 = __ldg(rec4 + 4 * (size_t)id + 1);  // r2 (fp64), qa, qb
         const double mx = __hiloint2double(__float_as_int(g0.y), __float_as_int(g0.x));
         const double my = __hiloint2double(__float_as_int(g0.w), __float_as_int(g0.z));
         const double r2 = __hiloint2double(__float_as_int(g1.y), __float_as_int(g1.x));
@@ -340,32 +327,30 @@ __global__ void __launch_bounds__(256, 3) k_blend16w(BlendArgs a, int n_items) {
         const float4 g = s_geo[warp][k];
         const float4 h = s_geo2[warp][k];
         const float4 c = s_col[warp][k];
-        // predicated body: no divergent branches on the common path
-        const float dx = px - g.x, dy = py - g.y;
-        const float d2 = fmaf(dx, dx, dy * dy);
-        const bool active = T >= kTermEpsF;
-        bool inside = d2 <= h.z;
-        const bool band = active && !inside && d2 <= h.w;
-        if (__any_sync(0xffffffffu, band) && band) {
-          // guard band: the reference's fp64 test, bit for bit
-          const double ddx = ((double)(x0 + lx) + 0.5) - s_mx[warp][k];
-          const double ddy = ((double)(y0 + ly) + 0.5) - s_my[warp][k];
-          inside = __dadd_rn(__dmul_rn(ddx, ddx), __dmul_rn(ddy, ddy)) <= s_r2[warp][k];
+        bool contrib = false;
+        if (T >= kTermEpsF) {
+          const float dx = px - g.x, dy = py - g.y;
+          const float d2 = fmaf(dx, dx, dy * dy);
+          bool inside = d2 <= h.z;
+          if (!inside && d2 <= h.w) {
+            const double ddx = ((double)(x0 + lx) + 0.5) - s_mx[warp][k];
+            const double ddy = ((double)(y0 + ly) + 0.5) - s_my[warp][k];
+            inside = __dadd_rn(__dmul_rn(ddx, ddx), __dmul_rn(ddy, ddy)) <= s_r2[warp][k];
+          }
+          if (inside) {
+            const float power = fmaf(fmaf(g.z, dx, g.w * dy), dx, fmaf(h.x * dy, dy, h.y));
+            contrib = power > -1060.0f;
+            if (!contrib && power >= -1080.0f) contrib = exp2((double)power) * (double)T > 0.0;
+            const float sig = fminf(ex2_approx(power), kSigmaMaxF);
+            const float w = T * sig;
+            C0 = fmaf(w, c.x, C0);
+            C1 = fmaf(w, c.y, C1);
+            C2 = fmaf(w, c.z, C2);
+            D = fmaf(w, c.w, D);
+            T = T * (1.0f - sig);
+            if (T < kTermEpsF) last = b - range.x + k;
+          }
         }
-        const bool on = active && inside;
-        const float power = fmaf(fmaf(g.z, dx, g.w * dy), dx, fmaf(h.x * dy, dy, h.y));
-        bool contrib = on && power > -1060.0f;
-        const bool deep = on && !contrib && power >= -1080.0f;
-        if (__any_sync(0xffffffffu, deep) && deep)
-          contrib = exp2((double)power) * (double)T > 0.0;
-        const float sig = on ? fminf(ex2_approx(power), kSigmaMaxF) : 0.0f;
-        const float w = T * sig;
-        C0 = fmaf(w, c.x, C0);
-        C1 = fmaf(w, c.y, C1);
-        C2 = fmaf(w, c.z, C2);
-        D = fmaf(w, c.w, D);
-        T = T * (1.0f - sig);
-        last = (on && T < kTermEpsF) ? b - range.x + k : last;
         const uint32_t cm = __ballot_sync(0xffffffffu, contrib);
         if (lane == 0 && cm && a.touched) atomicAdd(a.touched + s_id[warp][k], __popc(cm));
       }

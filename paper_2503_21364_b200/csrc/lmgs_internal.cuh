@@ -125,9 +125,8 @@ struct DevSlots {
 
 // runs of equal fp32 depth keys up to this length are fixed up in registers
 constexpr int kFixupRun = 32;
-constexpr int kSmallTileCap = 2048;    // bucket sorted by a 256-thread CTA
-constexpr int kMidTileCap = 8192;      // bucket sorted by a 512-thread CTA
-constexpr int kMediumTileCap = 16384;  // bucket sorted by a 1024-thread CTA; larger: global path
+constexpr int kSmallTileCap = 2048;    // bucket sorted by a 256-thread CTA, 32 KB smem
+constexpr int kMediumTileCap = 16384;  // bucket sorted by a 512-thread CTA, 208 KB smem
 
 // K3a/K3b/K4: per-CTA (one per SM) tile histograms and placement
 constexpr int kBinThreads = 1024;
@@ -153,9 +152,10 @@ void launch_bin_place(const BinArgs& a, cudaStream_t s);  // K4
 struct TileScanArgs {
   const uint32_t* tile_count;  // [tiles]
   int tiles;
+  int small_cap, medium_cap;
   int2* ranges;                // [tiles] out: [start, end)
-  uint32_t* lists[4];          // [tiles] each: tile ids of class small/mid/medium/big
-  uint32_t* class_counts;      // [4]
+  uint32_t* lists[3];          // [tiles] each: tile ids of class small/medium/big
+  uint32_t* class_counts;      // [3]
   uint64_t* total;             // K
 };
 void launch_scan_tiles(const TileScanArgs& a, cudaStream_t s);

@@ -16,8 +16,8 @@
 //        tile buckets through shared-memory cursors (order inside a bucket
 //        is arbitrary);
 //   K5   one CTA per bucket sorts it in shared memory: one counting pass into
-//        as many bins as the bucket's capacity, spanning its fp32-key range,
-//        then per-bin sorts by (fp32 key, fp64 depth, id) — the exact order;
+//        4096 bins over the bucket's fp32-key range, then per-bin insertion
+//        sorts by (fp32 key, fp64 depth, id) — the exact order;
 //   big  buckets above kMediumTileCap: onesweep radix on
 //        (bucket index << 32 | fp32 key) + the same fix-up (sort.cu).
 #include "lmgs_internal.cuh"
@@ -101,11 +101,11 @@ constexpr int kScanTilesThreads = 1024;
 __global__ void __launch_bounds__(kScanTilesThreads) k_scan_tiles(TileScanArgs a) {
   __shared__ uint32_t s_warp[kScanTilesThreads / 32];
   __shared__ unsigned long long s_carry;
-  __shared__ uint32_t s_cls[4];
+  __shared__ uint32_t s_cls[3];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
     s_carry = 0;
-    s_cls[0] = s_cls[1] = s_cls[2] = s_cls[3] = 0;
+    s_cls[0] = s_cls[1] = s_cls[2] = 0;
   }
   __syncthreads();
   for (int base = 0; base < a.tiles; base += kScanTilesThreads) {
@@ -134,10 +134,7 @@ __global__ void __launch_bounds__(kScanTilesThreads) k_scan_tiles(TileScanArgs a
     if (t < a.tiles) {
       a.ranges[t] = make_int2((int)excl, (int)(excl + c));
       if (c > 0) {
-        const int cls = c <= (uint32_t)kSmallTileCap    ? 0
-                        : c <= (uint32_t)kMidTileCap    ? 1
-                        : c <= (uint32_t)kMediumTileCap ? 2
-                                                        : 3;
+        const int cls = c <= (uint32_t)a.small_cap ? 0 : (c <= (uint32_t)a.medium_cap ? 1 : 2);
         const uint32_t slot = atomicAdd(&s_cls[cls], 1u);
         a.lists[cls][slot] = (uint32_t)t;
       }
@@ -151,7 +148,6 @@ __global__ void __launch_bounds__(kScanTilesThreads) k_scan_tiles(TileScanArgs a
     a.class_counts[0] = s_cls[0];
     a.class_counts[1] = s_cls[1];
     a.class_counts[2] = s_cls[2];
-    a.class_counts[3] = s_cls[3];
   }
 }
 
@@ -245,7 +241,6 @@ __device__ void fix_run(uint32_t* ids, int len, const uint64_t* __restrict__ key
 // long-bin list.  Entries of the first pass are held in registers.
 
 constexpr int kBinSortMax = 64;
-constexpr int kBinThread = 16;
 
 __device__ __forceinline__ bool entry_less(uint32_t ka, uint32_t ia, uint32_t kb, uint32_t ib,
                                            const uint64_t* __restrict__ key64) {
@@ -261,12 +256,13 @@ __device__ void sort_small_bin(uint32_t* key, uint16_t* idx, int lo, int hi,
   for (int a = lo + 1; a < hi; ++a) {
     const uint32_t ka = key[a];
     const uint16_t xa = idx[a];
+    const uint32_t ia = (uint32_t)bucket[xa];
     int b = a - 1;
     while (b >= lo) {
       const uint32_t kb = key[b];
       if (kb < ka) break;
-      if (kb == ka) {  // fp32 tie: ids and fp64 depths decide (rare)
-        const uint32_t ia = bucket[xa], ib = bucket[idx[b]];
+      if (kb == ka) {
+        const uint32_t ib = (uint32_t)bucket[idx[b]];
         if (!entry_less(ka, ia, kb, ib, key64)) break;
       }
       key[b + 1] = kb;
@@ -276,55 +272,6 @@ __device__ void sort_small_bin(uint32_t* key, uint16_t* idx, int lo, int hi,
     key[b + 1] = ka;
     idx[b + 1] = xa;
   }
-}
-
-// One warp sorts buf[lo, hi) (hi - lo <= 64): bitonic over 64 slots of
-// (key << 32 | local index), two per lane, partners via shuffles; then runs of
-// equal fp32 keys (rare) are ordered by (fp64 depth, id) by lane 0.
-__device__ void warp_sort_bin(uint32_t* key, uint16_t* idx, int lo, int hi,
-                              const uint32_t* __restrict__ bucket,
-                              const uint64_t* __restrict__ key64) {
-  const int lane = threadIdx.x & 31;
-  const int len = hi - lo;
-  uint64_t e0 = lane < len ? ((uint64_t)key[lo + lane] << 32) | idx[lo + lane] : ~0ull;
-  uint64_t e1 = lane + 32 < len ? ((uint64_t)key[lo + lane + 32] << 32) | idx[lo + lane + 32]
-                                : ~0ull;
-#pragma unroll
-  for (int k = 2; k <= 64; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      if (j == 32) {  // slots lane and lane + 32; k == 64 -> ascending
-        const uint64_t lo_v = e0 < e1 ? e0 : e1, hi_v = e0 < e1 ? e1 : e0;
-        e0 = lo_v;
-        e1 = hi_v;
-      } else {
-        const uint64_t p0 = __shfl_xor_sync(0xffffffffu, e0, j);
-        const uint64_t p1 = __shfl_xor_sync(0xffffffffu, e1, j);
-        const bool keep_min0 = ((lane & j) == 0) == ((lane & k) == 0);
-        const bool keep_min1 = (((lane + 32) & j) == 0) == (((lane + 32) & k) == 0);
-        e0 = keep_min0 ? (e0 < p0 ? e0 : p0) : (e0 < p0 ? p0 : e0);
-        e1 = keep_min1 ? (e1 < p1 ? e1 : p1) : (e1 < p1 ? p1 : e1);
-      }
-    }
-  }
-  if (lane < len) {
-    key[lo + lane] = (uint32_t)(e0 >> 32);
-    idx[lo + lane] = (uint16_t)e0;
-  }
-  if (lane + 32 < len) {
-    key[lo + lane + 32] = (uint32_t)(e1 >> 32);
-    idx[lo + lane + 32] = (uint16_t)e1;
-  }
-  __syncwarp();
-  if (lane == 0) {  // exact order inside runs of equal fp32 keys
-    for (int i = lo; i < hi;) {
-      int e = i + 1;
-      while (e < hi && key[e] == key[i]) ++e;
-      if (e - i > 1) sort_small_bin(key, idx, i, e, bucket, key64);
-      i = e;
-    }
-  }
-  __syncwarp();
 }
 
 template <int THREADS, int NBINS>
@@ -365,15 +312,13 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort(TileSortArgs a, const uin
                                                       const uint32_t* list_count) {
   constexpr int PER = (CAP + THREADS - 1) / THREADS;
   constexpr int NW = THREADS / 32;
-  constexpr int kMaxLong = 1024;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint32_t* s_key = reinterpret_cast<uint32_t*>(smem_raw);            // [CAP]
-  uint16_t* s_idx = reinterpret_cast<uint16_t*>(smem_raw + 4 * CAP);  // [CAP]
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem_raw + 6 * CAP);  // [NBINS]
-  int2* s_long = reinterpret_cast<int2*>(s_cnt + NBINS);              // [kMaxLong]
-  uint16_t* s_mid = reinterpret_cast<uint16_t*>(s_long + kMaxLong);   // [NBINS]
-  __shared__ uint32_t s_kmin, s_kmax, s_nlong, s_nmid;
-  __shared__ unsigned long long s_kmin64, s_kmax64;
+  uint32_t* s_key = reinterpret_cast<uint32_t*>(smem_raw);                 // [CAP]
+  uint16_t* s_idx = reinterpret_cast<uint16_t*>(smem_raw + 4 * CAP);       // [CAP]
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem_raw + 6 * CAP);       // [NBINS + 1]
+  uint32_t* s_start = s_cnt + (NBINS + 1);                                 // [NBINS + 1]
+  uint16_t* s_long = reinterpret_cast<uint16_t*>(s_start + (NBINS + 1));   // [NBINS]
+  __shared__ uint32_t s_kmin, s_kmax, s_nlong;
   __shared__ uint32_t s_wsum[NW];
   const int tid = threadIdx.x, lane = tid & 31;
   const uint32_t nlist = *list_count;
@@ -383,113 +328,79 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort(TileSortArgs a, const uin
     const int n = r.y - r.x;
     const uint32_t* __restrict__ bucket = a.bucket + r.x;
     if (tid == 0) {
-      s_kmin64 = ~0ull;
-      s_kmax64 = 0ull;
+      s_kmin = 0xffffffffu;
+      s_kmax = 0u;
       s_nlong = 0u;
-      s_nmid = 0u;
     }
-    for (int i = tid; i < NBINS; i += THREADS) s_cnt[i] = 0u;
+    for (int i = tid; i <= NBINS; i += THREADS) s_cnt[i] = 0u;
     __syncthreads();
-    // level 1: ids, then their fp64 depth keys (all gathers issued before use),
-    // then a tile-local 32-bit key: (key64 - kmin64) >> lshift, monotone in the
-    // fp64 depth with span/2^32 resolution — ties are exact fp64 ties or rare
+    // level 1: entries into registers, key range
     uint32_t rk[PER];
-    {
-      uint32_t rid[PER];
+    uint32_t kmin = 0xffffffffu, kmax = 0u;
 #pragma unroll
-      for (int j = 0; j < PER; ++j) {
-        const int i = tid + j * THREADS;
-        rid[j] = i < n ? bucket[i] : 0u;
+    for (int j = 0; j < PER; ++j) {
+      const int i = tid + j * THREADS;
+      rk[j] = i < n ? a.key32[bucket[i]] : 0u;
+      if (i < n) {
+        kmin = min(kmin, rk[j]);
+        kmax = max(kmax, rk[j]);
       }
-      uint64_t k64[PER];
+    }
 #pragma unroll
-      for (int j = 0; j < PER; ++j) {
-        const int i = tid + j * THREADS;
-        k64[j] = i < n ? a.key64[rid[j]] : 0ull;
-      }
-      unsigned long long kmin = ~0ull, kmax = 0ull;
-#pragma unroll
-      for (int j = 0; j < PER; ++j) {
-        const int i = tid + j * THREADS;
-        if (i < n) {
-          kmin = min(kmin, (unsigned long long)k64[j]);
-          kmax = max(kmax, (unsigned long long)k64[j]);
-        }
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
-        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
-      }
-      if (lane == 0) {
-        atomicMin(&s_kmin64, kmin);
-        atomicMax(&s_kmax64, kmax);
-      }
-      __syncthreads();
-      const unsigned long long kspan = s_kmax64 - s_kmin64;
-      const int lshift = kspan ? max(0, 64 - __clzll((long long)kspan) - 32) : 0;
-#pragma unroll
-      for (int j = 0; j < PER; ++j) rk[j] = (uint32_t)((k64[j] - s_kmin64) >> lshift);
-      if (tid == 0) {
-        s_kmin = 0u;
-        s_kmax = (uint32_t)(kspan >> lshift);
-      }
+    for (int o = 16; o; o >>= 1) {
+      kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+      kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    if (lane == 0) {
+      atomicMin(&s_kmin, kmin);
+      atomicMax(&s_kmax, kmax);
     }
     __syncthreads();
     const uint32_t k0 = s_kmin;
     const uint32_t span = s_kmax - k0;
     int shift = 0;
     while ((span >> shift) >= (uint32_t)NBINS) ++shift;
+    uint32_t rbin[PER];
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
       const int i = tid + j * THREADS;
-      if (i < n) atomicAdd(s_cnt + ((rk[j] - k0) >> shift), 1u);
+      rbin[j] = (rk[j] - k0) >> shift;
+      if (i < n) atomicAdd(s_cnt + rbin[j], 1u);
     }
     __syncthreads();
     block_exclusive_scan<THREADS, NBINS>(s_cnt, s_wsum, NBINS);
+    for (int i = tid; i <= NBINS; i += THREADS) s_start[i] = s_cnt[i];
+    __syncthreads();
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
       const int i = tid + j * THREADS;
       if (i < n) {
-        const uint32_t p = atomicAdd(s_cnt + ((rk[j] - k0) >> shift), 1u);
+        const uint32_t p = atomicAdd(s_cnt + rbin[j], 1u);
         s_key[p] = rk[j];
         s_idx[p] = (uint16_t)i;
       }
     }
     __syncthreads();
-    // after the scatter s_cnt[d] = end of bin d; bin d = [end(d-1), end(d))
+    // per-bin ordering
     for (int d = tid; d < NBINS; d += THREADS) {
-      const int lo = d ? (int)s_cnt[d - 1] : 0, hi = (int)s_cnt[d];
-      const int len = hi - lo;
-      if (len > kBinSortMax) {
-        const uint32_t q = atomicAdd(&s_nlong, 1u);
-        if (q < kMaxLong) s_long[q] = make_int2(lo, hi);
-        else sort_small_bin(s_key, s_idx, lo, hi, bucket, a.key64);  // overflow: slow but exact
-      } else if (len > kBinThread) {
-        s_mid[atomicAdd(&s_nmid, 1u)] = (uint16_t)d;
-      } else if (len > 1) {
-        sort_small_bin(s_key, s_idx, lo, hi, bucket, a.key64);
-      }
+      const int lo = (int)s_start[d], hi = (int)s_start[d + 1];
+      if (hi - lo > kBinSortMax) s_long[atomicAdd(&s_nlong, 1u)] = (uint16_t)d;
+      else if (hi - lo > 1) sort_small_bin(s_key, s_idx, lo, hi, bucket, a.key64);
     }
     __syncthreads();
-    for (int q = tid >> 5; q < (int)s_nmid; q += NW) {
-      const int d = s_mid[q];
-      warp_sort_bin(s_key, s_idx, d ? (int)s_cnt[d - 1] : 0, (int)s_cnt[d], bucket, a.key64);
-    }
-    __syncthreads();
-    // level 2 for long bins, one bin at a time, CTA-wide (s_cnt is free now)
-    const int nlong = (int)min(s_nlong, (uint32_t)kMaxLong);
+    // level 2 for long bins, one bin at a time, CTA-wide
+    const int nlong = (int)s_nlong;
     for (int q = 0; q < nlong; ++q) {
-      const int lo = s_long[q].x, hi = s_long[q].y;
+      const int d = s_long[q];
+      const int lo = (int)s_start[d], hi = (int)s_start[d + 1];
       const int len = hi - lo;
+      // into registers (len <= CAP)
       uint32_t lk[PER];
       uint16_t lx[PER];
       uint32_t lmin = 0xffffffffu, lmax = 0u;
 #pragma unroll
       for (int j = 0; j < PER; ++j) {
         const int i = tid + j * THREADS;
-        lk[j] = 0u;
-        lx[j] = 0;
         if (i < len) {
           lk[j] = s_key[lo + i];
           lx[j] = s_idx[lo + i];
@@ -507,7 +418,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort(TileSortArgs a, const uin
         s_kmin = 0xffffffffu;
         s_kmax = 0u;
       }
-      for (int i = tid; i < NBINS; i += THREADS) s_cnt[i] = 0u;
+      for (int i = tid; i <= NBINS; i += THREADS) s_cnt[i] = 0u;
       __syncthreads();
       if (lane == 0) {
         atomicMin(&s_kmin, lmin);
@@ -516,29 +427,36 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort(TileSortArgs a, const uin
       __syncthreads();
       const uint32_t l0 = s_kmin, lspan = s_kmax - l0;
       if (lspan == 0) {  // all fp32 keys equal: order by (fp64 depth, id) only
+        __syncthreads();
         if (tid == 0) sort_small_bin(s_key, s_idx, lo, hi, bucket, a.key64);
         __syncthreads();
         continue;
       }
       int sh = 0;
       while ((lspan >> sh) >= (uint32_t)NBINS) ++sh;
+      uint32_t lb[PER];
 #pragma unroll
       for (int j = 0; j < PER; ++j) {
         const int i = tid + j * THREADS;
-        if (i < len) atomicAdd(s_cnt + ((lk[j] - l0) >> sh), 1u);
+        lb[j] = (lk[j] - l0) >> sh;
+        if (i < len) atomicAdd(s_cnt + lb[j], 1u);
       }
       __syncthreads();
       block_exclusive_scan<THREADS, NBINS>(s_cnt, s_wsum, NBINS);
+      // s_start is still needed for the outer bins: keep the level-2 starts in
+      // s_cnt (cursor) and a copy in the tail of s_long's space is not
+      // available, so sub-bins are re-derived from the cursor after scatter.
 #pragma unroll
       for (int j = 0; j < PER; ++j) {
         const int i = tid + j * THREADS;
         if (i < len) {
-          const uint32_t p = lo + atomicAdd(s_cnt + ((lk[j] - l0) >> sh), 1u);
+          const uint32_t p = lo + atomicAdd(s_cnt + lb[j], 1u);
           s_key[p] = lk[j];
           s_idx[p] = lx[j];
         }
       }
       __syncthreads();
+      // after the scatter s_cnt[b] = end of sub-bin b; sub-bin b = [end[b-1], end[b])
       for (int b = tid; b < NBINS; b += THREADS) {
         const int e = (int)s_cnt[b];
         const int st = b ? (int)s_cnt[b - 1] : 0;
@@ -546,27 +464,15 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort(TileSortArgs a, const uin
       }
       __syncthreads();
     }
-    // write ids in order (gathers batched 8 deep)
-    for (int base = 0; base < n; base += 8 * THREADS) {
-      uint32_t v[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int i = base + tid + j * THREADS;
-        v[j] = i < n ? bucket[s_idx[i]] : 0u;
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int i = base + tid + j * THREADS;
-        if (i < n) a.sorted_ids[r.x + i] = v[j];
-      }
-    }
+    // write ids in order
+    for (int i = tid; i < n; i += THREADS) a.sorted_ids[r.x + i] = bucket[s_idx[i]];
     __syncthreads();
   }
 }
 
 template <int THREADS, int CAP, int NBINS>
 constexpr size_t tile_sort_smem() {
-  return 6 * (size_t)CAP + 4 * (size_t)NBINS + 8 * 1024 + 2 * (size_t)NBINS + 16;
+  return 6 * (size_t)CAP + 8 * (size_t)(NBINS + 1) + 2 * (size_t)NBINS + 16;
 }
 
 // ---------------------------------------------------------------------------
@@ -580,8 +486,7 @@ __global__ void k_big_gather(TileSortArgs a, const uint32_t* big_list, int n_big
     const uint32_t o = big_off[b];
     for (int i = threadIdx.x; i < r.y - r.x; i += blockDim.x) {
       const uint32_t id = a.bucket[r.x + i];
-      const uint32_t k32 = __float_as_uint(__double2float_rd(__longlong_as_double(a.key64[id])));
-      keys[o + i] = ((uint64_t)b << 32) | k32;
+      keys[o + i] = ((uint64_t)b << 32) | a.key32[id];
       vals[o + i] = id;
     }
   }
@@ -655,25 +560,19 @@ void launch_bin_place(const BinArgs& a, cudaStream_t s) {
 void launch_tile_sort(const TileSortArgs& a, const uint32_t* tile_list,
                       const uint32_t* list_count, int n_list, int cls, cudaStream_t s) {
   if (n_list <= 0) return;
-  // class 0: <= 2048 entries, 1: <= 8192, 2: <= 16384 (class 3 takes the global path)
-  constexpr int kT0 = 256, kT1 = 512, kT2 = 1024;
-  constexpr int kB0 = kSmallTileCap, kB1 = kMidTileCap, kB2 = kMediumTileCap;  // one bin per entry
+  constexpr int kST = 256, kMT = 1024, kSB = 1024, kMB = 4096;
   static bool attr = false;
   if (!attr) {
-    set_smem(k_tile_sort<kT0, kSmallTileCap, kB0>, tile_sort_smem<kT0, kSmallTileCap, kB0>());
-    set_smem(k_tile_sort<kT1, kMidTileCap, kB1>, tile_sort_smem<kT1, kMidTileCap, kB1>());
-    set_smem(k_tile_sort<kT2, kMediumTileCap, kB2>, tile_sort_smem<kT2, kMediumTileCap, kB2>());
+    set_smem(k_tile_sort<kST, kSmallTileCap, kSB>, tile_sort_smem<kST, kSmallTileCap, kSB>());
+    set_smem(k_tile_sort<kMT, kMediumTileCap, kMB>, tile_sort_smem<kMT, kMediumTileCap, kMB>());
     attr = true;
   }
   if (cls == 0)
-    k_tile_sort<kT0, kSmallTileCap, kB0>
-        <<<n_list, kT0, tile_sort_smem<kT0, kSmallTileCap, kB0>(), s>>>(a, tile_list, list_count);
-  else if (cls == 1)
-    k_tile_sort<kT1, kMidTileCap, kB1>
-        <<<n_list, kT1, tile_sort_smem<kT1, kMidTileCap, kB1>(), s>>>(a, tile_list, list_count);
+    k_tile_sort<kST, kSmallTileCap, kSB>
+        <<<n_list, kST, tile_sort_smem<kST, kSmallTileCap, kSB>(), s>>>(a, tile_list, list_count);
   else
-    k_tile_sort<kT2, kMediumTileCap, kB2>
-        <<<n_list, kT2, tile_sort_smem<kT2, kMediumTileCap, kB2>(), s>>>(a, tile_list, list_count);
+    k_tile_sort<kMT, kMediumTileCap, kMB>
+        <<<n_list, kMT, tile_sort_smem<kMT, kMediumTileCap, kMB>(), s>>>(a, tile_list, list_count);
 }
 
 void launch_big_gather(const TileSortArgs& a, const uint32_t* big_list, int n_big,
