@@ -270,7 +270,7 @@ def run_ours(args, rank, world, local):
                        "parallelism": f"camera-batch dp{world}",
                        "l2": "no flush: scene 1.42 GB and per-view buffers > 126 MB L2",
                        "geometry": "fp64 (bit-exact tile lists)", "blend": "fp32"},
-            "gpu_launches": renderer.kernels_per_step() * args.steps,
+            "gpu_launches": renderer.launches_per_step * args.steps,
             "e2e": e2e,
             "roofline": roof,
             "cpu_baseline": cpu,

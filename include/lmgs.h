@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define LMGS_ABI_VERSION 1
+#define LMGS_ABI_VERSION 2
 
 typedef enum lmgs_status {
   LMGS_OK = 0,
@@ -103,9 +103,11 @@ typedef struct lmgs_stats {
   int64_t n_gaussians;
   int64_t n_kept;            /* M */
   int64_t n_instances;       /* K */
+  int64_t n_visible;         /* splats touching >= 1 tile */
   int32_t n_tiles;           /* T */
   int32_t tiles_x, tiles_y;
   int32_t n_stages;
+  int32_t n_launches;        /* liblmgs kernels launched by the last render */
   float stage_ms[LMGS_MAX_STAGES];  /* valid with LMGS_FLAG_STAGE_TIMES */
   const char* stage_names[LMGS_MAX_STAGES];
 } lmgs_stats;

@@ -13,7 +13,7 @@ from pathlib import Path
 from .errors import InvalidInputError, LmgsError, ShapeError
 
 LIB_PATH = Path(__file__).resolve().parent / "liblmgs.so"
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 P = ctypes.c_void_p
 D = ctypes.c_double
@@ -54,8 +54,9 @@ class Frame(ctypes.Structure):
 
 
 class Stats(ctypes.Structure):
-    _fields_ = [("n_gaussians", I64), ("n_kept", I64), ("n_instances", I64), ("n_tiles", I32),
-                ("tiles_x", I32), ("tiles_y", I32), ("n_stages", I32),
+    _fields_ = [("n_gaussians", I64), ("n_kept", I64), ("n_instances", I64),
+                ("n_visible", I64), ("n_tiles", I32), ("tiles_x", I32), ("tiles_y", I32),
+                ("n_stages", I32), ("n_launches", I32),
                 ("stage_ms", F * MAX_STAGES), ("stage_names", ctypes.c_char_p * MAX_STAGES)]
 
 
@@ -132,5 +133,6 @@ class Context:
         check(self.handle, lib().lmgs_get_stats(self.handle, ctypes.byref(s)), "lmgs_get_stats")
         names = [s.stage_names[i].decode() if s.stage_names[i] else "" for i in range(s.n_stages)]
         return dict(n_gaussians=s.n_gaussians, n_kept=s.n_kept, n_instances=s.n_instances,
-                    n_tiles=s.n_tiles, tiles_x=s.tiles_x, tiles_y=s.tiles_y,
+                    n_visible=s.n_visible, n_launches=s.n_launches, n_tiles=s.n_tiles,
+                    tiles_x=s.tiles_x, tiles_y=s.tiles_y,
                     stage_ms={names[i]: float(s.stage_ms[i]) for i in range(s.n_stages)})

@@ -18,7 +18,11 @@ import torch
 from . import _lib
 from .raster import GaussianModel, _ptr, abi_camera, abi_settings
 
-KERNELS_PER_VIEW = 7  # preprocess, tile hist, column scan, tile scan, place, tile sort x2 (small/medium), blend -> see DESIGN.md
+
+def tile_passes(tiles: int) -> int:
+    """8-bit LSD passes of the K5 tile sort (tile ids < tiles)."""
+    bits = max(int(tiles - 1).bit_length(), 1)
+    return (bits + 7) // 8
 
 
 class BatchRenderer:
@@ -47,10 +51,8 @@ class BatchRenderer:
         self.done = [torch.cuda.Event() for _ in range(n_streams)]
         self.view_done = [torch.cuda.Event() for _ in range(v)]
         self.stats = []
+        self.launches_per_step = None  # liblmgs kernels per render() call (set by stage_times)
         self._g = model._abi()
-
-    def kernels_per_step(self, n_views: int | None = None) -> int:
-        return KERNELS_PER_VIEW * (self.max_views if n_views is None else n_views)
 
     def _frame(self, i) -> _lib.Frame:
         return _lib.Frame(_ptr(self.rgb[i]), _ptr(self.alpha[i]), _ptr(self.depth[i]), None,
@@ -69,7 +71,7 @@ class BatchRenderer:
         g = self._g
         if stage_times:
             tot = {}
-            inst = pairs = 0
+            inst = pairs = vis = launches = 0
             ctx = self.ctxs[0]
             for i, cam in enumerate(cams):
                 c = abi_camera(cam)
@@ -81,23 +83,29 @@ class BatchRenderer:
                 for k, v in s["stage_ms"].items():
                     tot[k] = tot.get(k, 0.0) + v
                 inst += s["n_instances"]
+                vis += s["n_visible"]
+                launches += s["n_launches"]
                 pairs += self._pairs(i)
+            self.launches_per_step = launches
             nv = len(cams)
             n = self.model.count
             s_read = int(self.model.sh.shape[1]) * 12
             k_avg = inst / nv
+            v_avg = vis / nv
             pix = self.w * self.h
             t = self.tx * self.ty
+            p = tile_passes(t)
             proc = self._processed_total(len(cams)) / nv
             alg = {  # algorithmic bytes per frame
-                "preprocess": n * (44 + s_read + 89) + 4 * k_avg,
-                "tile_scan": 20 * t,
-                "place": 16 * n + 12 * k_avg,
-                "tile_sort": 12 * k_avg,
-                "blend": 68 * proc + 8 * t + 20 * pix + 4 * n,
+                "preprocess": n * (44 + s_read + 89),
+                "depth_sort": n * (4 + 4 * 16 - 4 + 4),
+                "emit": 16 * v_avg + 8 * k_avg,
+                "tile_sort": 16 * p * k_avg + 8 * k_avg + 8 * t,
+                "blend": 72 * proc + 8 * t + 20 * pix + 4 * n,
             }
             return {"stage_ms": tot, "alg_bytes": alg,
-                    "per_frame": {"instances": k_avg, "pairs": pairs / nv, "processed": proc}}
+                    "per_frame": {"instances": k_avg, "visible": v_avg, "pairs": pairs / nv,
+                                  "processed": proc, "tile_passes": p}}
         ns = len(self.streams)
         for s in self.streams:
             s.wait_stream(caller)

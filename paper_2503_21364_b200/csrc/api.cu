@@ -1,13 +1,15 @@
 // C-ABI entry points (include/lmgs.h): context, device arena, stage pipeline.
 //
-// One view:
-//   K1 preprocess  (fp64 geometry, tile rect, blend record)
-//   K3 tile counts (per-SM shared-memory histograms + column scan) and tile
-//      scan (one CTA: ranges, size classes, K) -> one 8-byte D2H read of K
-//   K4 place       (shared-memory cursors: each instance into its tile bucket)
-//   K5 tile sort   (per-tile smem LSD radix on the fp32 depth + exact fp64 fix-up;
-//                   oversized buckets: onesweep radix + the same fix-up)
-//   K7 blend       (persistent warps over (tile, 8x4 block) items)
+// One view (stream-ordered, one 24-byte D2H read of the counters):
+//   K1 preprocess  fp64 geometry, tile rect + count, blend record, fp32 depth
+//                  key; counts M (near-kept), visible splats and K
+//   K2 depth sort  onesweep LSD radix of the fp32 depth keys (implicit id
+//                  payload), then the exact fp64 fix-up of equal-key runs
+//   K4 emit        splats in depth-rank order -> keys tile << 32 | id (scan by
+//                  decoupled look-back) + tile-digit histograms
+//   K5 tile sort   stable onesweep LSD radix on the tile bits (2 passes at 1080p)
+//   K6 ranges      per-tile [start, end) from the sorted keys
+//   K7 blend       persistent warps over (tile, 8x4 block) items
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -22,7 +24,7 @@ namespace {
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
-const char* kStageNames[] = {"preprocess", "tile_scan", "place", "tile_sort", "blend"};
+const char* kStageNames[] = {"preprocess", "depth_sort", "emit", "tile_sort", "blend"};
 constexpr int kNumStages = 5;
 
 // grow-only device buffer
@@ -65,35 +67,30 @@ struct Carver {
 
 size_t gaussian_bytes(int64_t n) {
   size_t b = 0;
-  b += align_up(sizeof(uint32_t) * n);  // fp32 depth keys
-  b += align_up(sizeof(uint64_t) * n);  // fp64 depth keys
-  b += align_up(sizeof(uint64_t) * n);  // rects
-  b += align_up(sizeof(uint32_t) * n);  // tile counts
-  b += align_up(sizeof(BlendRec) * n);  // records
-  return b + 8 * kAlign;
-}
-size_t tile_bytes(int64_t t, int ctas) {
-  return align_up(sizeof(uint32_t) * t * ctas) + 5 * align_up(sizeof(uint32_t) * t) +
-         align_up(sizeof(int2) * t) + 8 * kAlign;
+  b += 2 * align_up(sizeof(uint32_t) * n);  // fp32 depth keys (ping-pong)
+  b += 2 * align_up(sizeof(uint32_t) * n);  // ids (ping-pong)
+  b += align_up(sizeof(uint64_t) * n);      // fp64 depth keys
+  b += align_up(sizeof(uint64_t) * n);      // rects
+  b += align_up(sizeof(BlendRec) * n);      // records
+  b += align_up(sizeof(uint32_t) * radix_lookback_words(n));  // K2 look-back
+  b += align_up(sizeof(uint64_t) * emit_chunks(n));            // K4 look-back
+  return b + 10 * kAlign;
 }
 size_t instance_bytes(int64_t k) {
-  return 2 * align_up(sizeof(uint32_t) * k) + 4 * kAlign;
-}
-size_t big_bytes(int64_t k) {
-  return 2 * align_up(sizeof(uint64_t) * k) + 2 * align_up(sizeof(uint32_t) * k) +
-         align_up(sizeof(uint32_t) * radix_lookback_words(k)) + 8 * kAlign;
+  return 2 * align_up(sizeof(uint64_t) * k) + align_up(sizeof(uint32_t) * radix_lookback_words(k)) +
+         4 * kAlign;
 }
 
 struct Scalars {  // device-side small state
-  RadixPlan big_plan;
-  uint32_t hist[kMaxPasses * kRadix];
-  uint32_t counters[kMaxPasses];
-  uint32_t class_counts[4];
-  unsigned long long n_kept;
-  uint64_t total;
-  unsigned long long big_total;
+  RadixPlan depth_plan, tile_plan;
+  uint32_t depth_hist[kMaxPasses * kRadix];
+  uint32_t tile_hist[kMaxPasses * kRadix];
+  uint32_t depth_counters[kMaxPasses];
+  uint32_t tile_counters[kMaxPasses];
+  unsigned long long counts[3];  // n_kept, n_vis, n_inst (one D2H copy)
+  unsigned long long zrange[2];  // min / max visible fp64 depth bits
+  uint32_t emit_ticket;
   int blend_counter;
-  int pad;
   DevSlots slots;
 };
 
@@ -101,36 +98,30 @@ struct Scalars {  // device-side small state
 
 struct lmgs_context {
   int device = 0;
-  int sms = 148;  // K3a / K4 CTA slices (one per SM)
+  int sms = 148;
   std::string err;
-  DevBuf gbuf, tbuf, ibuf, bbuf;
+  DevBuf gbuf, tbuf, ibuf;
   Scalars* d_scal = nullptr;
-  uint64_t* h_pinned = nullptr;  // [0]=K [1]=kept [2]=class counts (3 x u32 packed)
-  cudaEvent_t ev[kNumStages + 1] = {};
+  uint64_t* h_pinned = nullptr;  // [0..2] = n_kept, n_vis, K
+  cudaEvent_t ev[2 * kNumStages] = {};
+  cudaEvent_t counts_ready = nullptr;
   bool events_ok = false;
-  int64_t cap_n = -1, cap_t = -1, cap_k = -1, cap_big = -1;
+  int64_t cap_n = -1, cap_t = -1, cap_k = -1;
   // per-Gaussian arena
-  uint32_t* key32 = nullptr;
+  uint32_t* key32[2] = {nullptr, nullptr};
+  uint32_t* ids[2] = {nullptr, nullptr};
   uint64_t* key64 = nullptr;
   uint64_t* rects = nullptr;
-  uint32_t* tile_counts = nullptr;
   BlendRec* recs = nullptr;
+  uint32_t* depth_lookback = nullptr;
+  uint64_t* emit_lookback = nullptr;
   // per-tile arena
-  uint32_t* bin_hist = nullptr;   // [sms][tiles]
-  uint32_t* tile_count = nullptr;
-  uint32_t* lists[3] = {nullptr, nullptr, nullptr};
-  uint32_t* big_off = nullptr;
   int2* ranges = nullptr;
   // per-instance arena
-  uint32_t* bucket = nullptr;
-  uint32_t* sorted_ids = nullptr;
-  // oversized-bucket arena
-  uint64_t* big_keys[2] = {nullptr, nullptr};
-  uint32_t* big_vals[2] = {nullptr, nullptr};
-  uint32_t* big_lookback = nullptr;
+  uint64_t* inst_keys[2] = {nullptr, nullptr};
+  uint32_t* tile_lookback = nullptr;
   const int64_t* last_prim_ids = nullptr;
   const int2* last_ranges = nullptr;
-  int64_t big_views = 0;  // views that needed the oversized-bucket path
   lmgs_stats stats{};
   bool last_timed = false;
 };
@@ -170,11 +161,13 @@ int ensure_gaussians(lmgs_context* c, int64_t n, cudaStream_t s) {
   LMGS_CUDA(c, c->gbuf.reserve(gaussian_bytes(n)));
   const int64_t cap = (int64_t)(c->gbuf.bytes >= gaussian_bytes(n + n / 4) ? n + n / 4 : n);
   Carver cv{static_cast<char*>(c->gbuf.ptr)};
-  c->key32 = cv.take<uint32_t>(cap);
+  for (int i = 0; i < 2; ++i) c->key32[i] = cv.take<uint32_t>(cap);
+  for (int i = 0; i < 2; ++i) c->ids[i] = cv.take<uint32_t>(cap);
   c->key64 = cv.take<uint64_t>(cap);
   c->rects = cv.take<uint64_t>(cap);
-  c->tile_counts = cv.take<uint32_t>(cap);
   c->recs = cv.take<BlendRec>(cap);
+  c->depth_lookback = cv.take<uint32_t>(radix_lookback_words(cap));
+  c->emit_lookback = cv.take<uint64_t>(emit_chunks(cap));
   c->cap_n = cap;
   return LMGS_OK;
 }
@@ -182,40 +175,22 @@ int ensure_gaussians(lmgs_context* c, int64_t n, cudaStream_t s) {
 int ensure_tiles(lmgs_context* c, int64_t t, cudaStream_t s) {
   if (t <= c->cap_t && c->ranges) return LMGS_OK;
   LMGS_CUDA(c, cudaStreamSynchronize(s));
-  LMGS_CUDA(c, c->tbuf.reserve(tile_bytes(t, c->sms)));
-  Carver cv{static_cast<char*>(c->tbuf.ptr)};
-  c->bin_hist = cv.take<uint32_t>(t * c->sms);
-  c->tile_count = cv.take<uint32_t>(t);
-  for (int i = 0; i < 3; ++i) c->lists[i] = cv.take<uint32_t>(t);
-  c->big_off = cv.take<uint32_t>(t);
-  c->ranges = cv.take<int2>(t);
+  LMGS_CUDA(c, c->tbuf.reserve(align_up(sizeof(int2) * t) + kAlign));
+  c->ranges = static_cast<int2*>(c->tbuf.ptr);
   c->cap_t = t;
   return LMGS_OK;
 }
 
 int ensure_instances(lmgs_context* c, int64_t k, cudaStream_t s) {
-  if (k <= c->cap_k && c->bucket) return LMGS_OK;
+  if (k <= c->cap_k && c->inst_keys[0]) return LMGS_OK;
   LMGS_CUDA(c, cudaStreamSynchronize(s));
   LMGS_CUDA(c, c->ibuf.reserve(instance_bytes(k)));
   const int64_t cap = (int64_t)(c->ibuf.bytes >= instance_bytes(k + k / 4) ? k + k / 4 : k);
   Carver cv{static_cast<char*>(c->ibuf.ptr)};
-  c->bucket = cv.take<uint32_t>(cap);
-  c->sorted_ids = cv.take<uint32_t>(cap);
+  c->inst_keys[0] = cv.take<uint64_t>(cap);
+  c->inst_keys[1] = cv.take<uint64_t>(cap);
+  c->tile_lookback = cv.take<uint32_t>(radix_lookback_words(cap));
   c->cap_k = cap;
-  return LMGS_OK;
-}
-
-int ensure_big(lmgs_context* c, int64_t k, cudaStream_t s) {
-  if (k <= c->cap_big && c->big_keys[0]) return LMGS_OK;
-  LMGS_CUDA(c, cudaStreamSynchronize(s));
-  LMGS_CUDA(c, c->bbuf.reserve(big_bytes(k)));
-  Carver cv{static_cast<char*>(c->bbuf.ptr)};
-  c->big_keys[0] = cv.take<uint64_t>(k);
-  c->big_keys[1] = cv.take<uint64_t>(k);
-  c->big_vals[0] = cv.take<uint32_t>(k);
-  c->big_vals[1] = cv.take<uint32_t>(k);
-  c->big_lookback = cv.take<uint32_t>(radix_lookback_words(k));
-  c->cap_big = k;
   return LMGS_OK;
 }
 
@@ -280,58 +255,33 @@ PreprocessArgs make_pre(lmgs_context* c, const lmgs_gaussians* g, const CamArgs&
   pa.sh_coeffs = g->sh_coeffs;
   pa.eval_degree = st->sh_eval_degree < g->sh_degree ? st->sh_eval_degree : g->sh_degree;
   pa.cam = ca;
-  pa.depth_keys32 = c->key32;
   pa.depth_keys = c->key64;
   pa.rects = c->rects;
-  pa.tile_counts = c->tile_counts;
   pa.recs = c->recs;
   pa.kept = kept;
-  pa.n_kept = &c->d_scal->n_kept;
+  pa.n_kept = &c->d_scal->counts[0];
+  pa.n_vis = &c->d_scal->counts[1];
+  pa.n_inst = &c->d_scal->counts[2];
+  pa.zrange = c->d_scal->zrange;
   return pa;
 }
 
-// oversized buckets: gather, onesweep on (bucket index << 32 | fp32 key), fix-up, scatter
-int sort_big_tiles(lmgs_context* c, const TileSortArgs& ta, int n_big, cudaStream_t s) {
-  // big list + ranges to host (rare path), offsets on host
-  std::vector<uint32_t> tiles(n_big);
-  std::vector<int2> rg(c->cap_t);
-  LMGS_CUDA(c, cudaMemcpyAsync(tiles.data(), c->lists[2], sizeof(uint32_t) * n_big,
-                               cudaMemcpyDeviceToHost, s));
-  LMGS_CUDA(c, cudaMemcpyAsync(rg.data(), ta.ranges, sizeof(int2) * c->stats.n_tiles,
-                               cudaMemcpyDeviceToHost, s));
-  LMGS_CUDA(c, cudaStreamSynchronize(s));
-  std::vector<uint32_t> off(n_big);
-  int64_t total = 0;
-  for (int b = 0; b < n_big; ++b) {
-    off[b] = (uint32_t)total;
-    total += rg[tiles[b]].y - rg[tiles[b]].x;
+struct StageTimer {
+  lmgs_context* c;
+  cudaStream_t s;
+  bool on;
+  void begin(int i) {
+    if (on) cudaEventRecord(c->ev[2 * i], s);
   }
-  if (int r = ensure_big(c, total, s)) return r;
-  LMGS_CUDA(c, cudaMemcpyAsync(c->big_off, off.data(), sizeof(uint32_t) * n_big,
-                               cudaMemcpyHostToDevice, s));
-  launch_big_gather(ta, c->lists[2], n_big, c->big_off, c->big_keys[0], c->big_vals[0], s);
-  RadixSortBuffers rb{};
-  rb.keys[0] = c->big_keys[0];
-  rb.keys[1] = c->big_keys[1];
-  rb.key_bytes = 8;
-  rb.vals[0] = c->big_vals[0];
-  rb.vals[1] = c->big_vals[1];
-  rb.plan = &c->d_scal->big_plan;
-  rb.hist = c->d_scal->hist;
-  rb.lookback = c->big_lookback;
-  rb.counters = c->d_scal->counters;
-  rb.keys_result = &c->d_scal->slots.big_keys;
-  rb.vals_result = &c->d_scal->slots.big_vals;
-  radix_sort(rb, total, 0, (32 + bits_for(n_big) + 7) / 8, s);
-  launch_big_fixup(&c->d_scal->slots.big_keys, &c->d_scal->slots.big_vals, total, ta.key64, s);
-  launch_big_scatter(ta, c->lists[2], n_big, c->big_off, &c->d_scal->slots.big_vals, s);
-  ++c->big_views;
-  return LMGS_OK;
-}
+  void end(int i) {
+    if (on) cudaEventRecord(c->ev[2 * i + 1], s);
+  }
+};
 
 int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
                const lmgs_settings* st, const lmgs_frame* out, cudaStream_t s) {
   const bool timed = (st->flags & LMGS_FLAG_STAGE_TIMES) && c->events_ok;
+  StageTimer tm{c, s, timed};
   const CamArgs ca = make_cam(cam, st->tile_size);
   const int64_t n = g->count;
   const int64_t tiles = (int64_t)ca.tiles_x * ca.tiles_y;
@@ -344,78 +294,110 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
   for (int i = 0; i < kNumStages; ++i) c->stats.stage_names[i] = kStageNames[i];
   c->last_timed = false;
   c->last_prim_ids = g->prim_ids;
+  const int tile_bits = bits_for(tiles);
+  if (tile_bits > 8 * kMaxTilePasses)
+    return fail(c, LMGS_ERR_UNSUPPORTED, "more than 2^24 tiles in one view");
+  const int tile_passes = tile_bits ? (tile_bits + 7) / 8 : 1;
 
   if (int r = ensure_gaussians(c, n > 0 ? n : 1, s)) return r;
   if (int r = ensure_tiles(c, tiles, s)) return r;
   int2* ranges = out->tile_ranges ? reinterpret_cast<int2*>(out->tile_ranges) : c->ranges;
   c->last_ranges = ranges;
-  LMGS_CUDA(c, cudaMemsetAsync(&c->d_scal->n_kept, 0, sizeof(unsigned long long), s));
+  Scalars* sc = c->d_scal;
+  LMGS_CUDA(c, cudaMemsetAsync(sc->counts, 0, sizeof(sc->counts), s));
+  LMGS_CUDA(c, cudaMemsetAsync(&sc->zrange[0], 0xff, sizeof(sc->zrange[0]), s));
+  LMGS_CUDA(c, cudaMemsetAsync(&sc->zrange[1], 0, sizeof(sc->zrange[1]), s));
   if (out->touched && n > 0) LMGS_CUDA(c, cudaMemsetAsync(out->touched, 0, sizeof(int32_t) * n, s));
 
-  if (timed) LMGS_CUDA(c, cudaEventRecord(c->ev[0], s));
-  launch_preprocess(make_pre(c, g, ca, st, out->kept), s);
-  if (timed) LMGS_CUDA(c, cudaEventRecord(c->ev[1], s));
-
-  BinArgs bin{};
-  bin.rects = c->rects;
-  bin.counts = c->tile_counts;
-  bin.key32 = c->key32;
-  bin.n = n;
-  bin.tiles_x = ca.tiles_x;
-  bin.tiles = (int)tiles;
-  bin.ctas = c->sms;
-  bin.hist = c->bin_hist;
-  bin.tile_count = c->tile_count;
-  bin.ranges = ranges;
-  launch_bin_hist(bin, s);
-
-  TileScanArgs sa{};
-  sa.tile_count = c->tile_count;
-  sa.tiles = (int)tiles;
-  sa.small_cap = kSmallTileCap;
-  sa.medium_cap = kMediumTileCap;
-  sa.ranges = ranges;
-  for (int i = 0; i < 3; ++i) sa.lists[i] = c->lists[i];
-  sa.class_counts = c->d_scal->class_counts;
-  sa.total = &c->d_scal->total;
-  launch_scan_tiles(sa, s);
-  LMGS_CUDA(c, cudaMemcpyAsync(c->h_pinned, &c->d_scal->total, sizeof(uint64_t),
+  // K1
+  int launched = 0;
+  tm.begin(0);
+  launched += launch_preprocess(make_pre(c, g, ca, st, out->kept), s);
+  tm.end(0);
+  LMGS_CUDA(c, cudaMemcpyAsync(c->h_pinned, sc->counts, sizeof(sc->counts),
                                cudaMemcpyDeviceToHost, s));
-  LMGS_CUDA(c, cudaMemcpyAsync(c->h_pinned + 1, &c->d_scal->n_kept, sizeof(uint64_t),
-                               cudaMemcpyDeviceToHost, s));
-  LMGS_CUDA(c, cudaMemcpyAsync(c->h_pinned + 2, c->d_scal->class_counts, 4 * sizeof(uint32_t),
-                               cudaMemcpyDeviceToHost, s));
-  LMGS_CUDA(c, cudaGetLastError());
-  LMGS_CUDA(c, cudaStreamSynchronize(s));
-  const int64_t k = (int64_t)c->h_pinned[0];
-  c->stats.n_instances = k;
-  c->stats.n_kept = (int64_t)c->h_pinned[1];
-  const uint32_t* cls = reinterpret_cast<const uint32_t*>(c->h_pinned + 2);
-  const int n_small = (int)cls[0], n_medium = (int)cls[1], n_big = (int)cls[2];
-  if (k >= ((int64_t)1 << 31) - 1)
-    return fail(c, LMGS_ERR_UNSUPPORTED, "more than 2^31 tile instances in one view");
-  if (timed) LMGS_CUDA(c, cudaEventRecord(c->ev[2], s));
+  LMGS_CUDA(c, cudaEventRecord(c->counts_ready, s));
 
-  if (int r = ensure_instances(c, k > 0 ? k : 1, s)) return r;
-  bin.bucket = c->bucket;
-  if (k > 0) launch_bin_place(bin, s);
-  if (timed) LMGS_CUDA(c, cudaEventRecord(c->ev[3], s));
-
-  TileSortArgs ta{};
-  ta.bucket = c->bucket;
-  ta.key32 = c->key32;
-  ta.ranges = ranges;
-  ta.key64 = c->key64;
-  ta.sorted_ids = c->sorted_ids;
-  launch_tile_sort(ta, c->lists[0], c->d_scal->class_counts + 0, n_small, 0, s);
-  launch_tile_sort(ta, c->lists[1], c->d_scal->class_counts + 1, n_medium, 1, s);
-  if (n_big > 0) {
-    if (int r = sort_big_tiles(c, ta, n_big, s)) return r;
+  // K2: 32-bit depth keys + histograms, (key, id) radix sort of all splats,
+  // then the fp64 fix-up of equal-key runs
+  tm.begin(1);
+  {
+    LMGS_CUDA(c, cudaMemsetAsync(sc->depth_hist, 0, sizeof(sc->depth_hist), s));
+    launched += launch_depth_keys(c->key64, sc->zrange, n, c->key32[0], sc->depth_hist, s);
+    RadixSortBuffers rb{};
+    rb.keys[0] = c->key32[0];
+    rb.keys[1] = c->key32[1];
+    rb.key_bytes = 4;
+    rb.vals[0] = c->ids[0];
+    rb.vals[1] = c->ids[1];
+    rb.plan = &sc->depth_plan;
+    rb.hist = sc->depth_hist;
+    rb.lookback = c->depth_lookback;
+    rb.counters = sc->depth_counters;
+    rb.keys_result = &sc->slots.depth_keys;
+    rb.vals_result = &sc->slots.depth_ids;
+    rb.iota_vals = true;
+    rb.hist_ready = true;
+    launched += radix_sort(rb, n, 0, 4, s);
+    launched += launch_depth_fixup(&sc->slots.depth_keys, &sc->slots.depth_ids, n, c->key64, s);
   }
-  if (timed) LMGS_CUDA(c, cudaEventRecord(c->ev[4], s));
+  tm.end(1);
 
+  // the only host wait of the view: M, visible splats, K (the depth sort keeps
+  // the device busy meanwhile)
+  LMGS_CUDA(c, cudaGetLastError());
+  LMGS_CUDA(c, cudaEventSynchronize(c->counts_ready));
+  c->stats.n_kept = (int64_t)c->h_pinned[0];
+  const int64_t n_vis = (int64_t)c->h_pinned[1];
+  c->stats.n_visible = n_vis;
+  const int64_t k = (int64_t)c->h_pinned[2];
+  c->stats.n_instances = k;
+  if (k >= ((int64_t)1 << 30))
+    return fail(c, LMGS_ERR_UNSUPPORTED, "more than 2^30 tile instances in one view");
+  if (int r = ensure_instances(c, k > 0 ? k : 1, s)) return r;
+
+  // K4
+  tm.begin(2);
+  LMGS_CUDA(c, cudaMemsetAsync(sc->tile_hist, 0, sizeof(sc->tile_hist), s));
+  LMGS_CUDA(c, cudaMemsetAsync(&sc->emit_ticket, 0, sizeof(uint32_t), s));
+  if (n_vis > 0) {
+    LMGS_CUDA(c, cudaMemsetAsync(c->emit_lookback, 0, sizeof(uint64_t) * emit_chunks(n_vis), s));
+    EmitArgs ea{};
+    ea.order_slot = &sc->slots.depth_ids;
+    ea.rects = c->rects;
+    ea.n_vis = n_vis;
+    ea.tiles_x = ca.tiles_x;
+    ea.n_tile_passes = tile_passes;
+    ea.keys = c->inst_keys[0];
+    ea.lookback = c->emit_lookback;
+    ea.ticket = &sc->emit_ticket;
+    ea.hist = sc->tile_hist;
+    launched += launch_emit(ea, s);
+  }
+  tm.end(2);
+
+  // K5 + K6
+  tm.begin(3);
+  {
+    RadixSortBuffers rb{};
+    rb.keys[0] = c->inst_keys[0];
+    rb.keys[1] = c->inst_keys[1];
+    rb.key_bytes = 8;
+    rb.plan = &sc->tile_plan;
+    rb.hist = sc->tile_hist;
+    rb.lookback = c->tile_lookback;
+    rb.counters = sc->tile_counters;
+    rb.keys_result = &sc->slots.inst_keys;
+    rb.hist_ready = true;
+    launched += radix_sort(rb, k, 32, tile_passes, s);
+    launched += launch_tile_ranges(&sc->slots.inst_keys, k, (int)tiles, ranges, s);
+  }
+  tm.end(3);
+
+  // K7
+  tm.begin(4);
   BlendArgs ba{};
-  ba.sorted_ids = c->sorted_ids;
+  ba.keys_slot = &sc->slots.inst_keys;
   ba.ranges = ranges;
   ba.recs = c->recs;
   ba.width = cam->width;
@@ -430,12 +412,12 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
   ba.trans = out->transmittance;
   ba.touched = out->touched;
   ba.n_processed = out->n_processed;
-  ba.work_counter = &c->d_scal->blend_counter;
+  ba.work_counter = &sc->blend_counter;
   if (int r = launch_blend(ba, s)) return fail(c, r, "unsupported tile size");
-  if (timed) {
-    LMGS_CUDA(c, cudaEventRecord(c->ev[5], s));
-    c->last_timed = true;
-  }
+  launched += tiles > 0 ? 1 : 0;
+  tm.end(4);
+  c->stats.n_launches = launched;
+  c->last_timed = timed;
   LMGS_CUDA(c, cudaGetLastError());
   return LMGS_OK;
 }
@@ -462,8 +444,13 @@ int lmgs_context_create(int device, lmgs_context** out) {
     lmgs_context_destroy(c);
     return e == cudaErrorMemoryAllocation ? LMGS_ERR_OOM : LMGS_ERR_CUDA;
   }
+  if (cudaEventCreateWithFlags(&c->counts_ready, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    lmgs_context_destroy(c);
+    return LMGS_ERR_CUDA;
+  }
   c->events_ok = true;
-  for (int i = 0; i <= kNumStages; ++i)
+  for (int i = 0; i < 2 * kNumStages; ++i)
     if (cudaEventCreate(&c->ev[i]) != cudaSuccess) c->events_ok = false;
   *out = c;
   return LMGS_OK;
@@ -476,11 +463,11 @@ void lmgs_context_destroy(lmgs_context* c) {
   c->gbuf.release();
   c->tbuf.release();
   c->ibuf.release();
-  c->bbuf.release();
   if (c->d_scal) cudaFree(c->d_scal);
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
-  for (int i = 0; i <= kNumStages; ++i)
+  for (int i = 0; i < 2 * kNumStages; ++i)
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+  if (c->counts_ready) cudaEventDestroy(c->counts_ready);
   delete c;
 }
 
@@ -509,10 +496,10 @@ int lmgs_get_stats(lmgs_context* c, lmgs_stats* out) {
   if (!c || !out) return LMGS_ERR_INVALID;
   DeviceGuard guard(c->device);
   if (c->last_timed) {
-    LMGS_CUDA(c, cudaEventSynchronize(c->ev[kNumStages]));
+    LMGS_CUDA(c, cudaEventSynchronize(c->ev[2 * kNumStages - 1]));
     for (int i = 0; i < kNumStages; ++i) {
       float ms = 0.f;
-      LMGS_CUDA(c, cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]));
+      LMGS_CUDA(c, cudaEventElapsedTime(&ms, c->ev[2 * i], c->ev[2 * i + 1]));
       c->stats.stage_ms[i] = ms;
     }
   }
@@ -525,12 +512,12 @@ int lmgs_copy_instances(lmgs_context* c, uint64_t* keys, int64_t* prim_ids, void
   DeviceGuard guard(c->device);
   InstanceExportArgs a{};
   a.ranges = c->last_ranges;
-  a.sorted_ids = c->sorted_ids;
+  a.keys_slot = &c->d_scal->slots.inst_keys;
   a.prim_ids = c->last_prim_ids;
   a.keys_out = keys;
   a.prims_out = prim_ids;
-  if (c->stats.n_instances > 0)
-    launch_export_instances(a, c->stats.n_tiles, static_cast<cudaStream_t>(stream));
+  a.k = c->stats.n_instances;
+  launch_export_instances(a, static_cast<cudaStream_t>(stream));
   LMGS_CUDA(c, cudaGetLastError());
   return LMGS_OK;
 }

@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(256) k_blend(BlendArgs a) {
   const int tile_x = tile % a.tiles_x, tile_y = tile / a.tiles_x;
   const int x0 = tile_x * ts, y0 = tile_y * ts;
   const int2 range = a.ranges[tile];
-  const uint32_t* __restrict__ list = a.sorted_ids;
+  const uint64_t* __restrict__ list = static_cast<const uint64_t*>(*a.keys_slot);
 
   float T[PPT], C0[PPT], C1[PPT], C2[PPT], D[PPT], px[PPT], py[PPT];
   int lxs[PPT], lys[PPT], last[PPT];
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(256) k_blend(BlendArgs a) {
     if (__syncthreads_count(mine_active) == 0) break;
     const int nb = min(kBatch, range.y - b0);
     for (int j = tid; j < nb; j += nthreads) {
-      const uint32_t id = list[b0 + j];
+      const uint32_t id = (uint32_t)list[b0 + j];
       const BlendRec rec = a.recs[id];
       const double mxl = rec.mx - (double)x0, myl = rec.my - (double)y0;
       const double ax = fabs(mxl) + ts, ay = fabs(myl) + ts;
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(256, 4) k_blend16w(BlendArgs a, int n_items) {
   __shared__ uint32_t s_id[kWarpsPerBlock16][32];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t* __restrict__ list = a.sorted_ids;
+  const uint64_t* __restrict__ list = static_cast<const uint64_t*>(*a.keys_slot);
   const float4* __restrict__ rec4 = reinterpret_cast<const float4*>(a.recs);
 
   while (true) {
@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(256, 4) k_blend16w(BlendArgs a, int n_items) {
       const int j = b + lane;
       bool hit = false;
       if (j < range.y) {
-        const uint32_t id = list[j];
+        const uint32_t id = (uint32_t)list[j];
         const float4 g0 = __ldg(rec4 + 4 * (size_t)id);      // mx, my (fp64)
         const float4 g1 = __ldg(rec4 + 4 * (size_t)id + 1);  // r2 (fp64), qa, qb
         const double mx = __hiloint2double(__float_as_int(g0.y), __float_as_int(g0.x));

@@ -54,13 +54,14 @@ struct PreprocessArgs {
   int32_t eval_degree;
   CamArgs cam;
   // outputs
-  uint32_t* depth_keys32;  // [n] bits(fp32 rd(depth)), 0xffffffff if culled
-  uint64_t* depth_keys;    // [n] fp64 depth bits, kCulledKey if culled
-  uint64_t* rects;         // [n]
-  uint32_t* tile_counts;   // [n] tiles touched per Gaussian
+  uint64_t* depth_keys;    // [n] fp64 depth bits; kCulledKey if culled or off-screen
+  uint64_t* rects;         // [n] inclusive tile rect (visible splats; count = its area)
   BlendRec* recs;          // [n]
   uint8_t* kept;           // [n] nullable
-  unsigned long long* n_kept;  // scalar (atomic)
+  unsigned long long* n_kept;  // scalar (atomic): z > near
+  unsigned long long* n_vis;   // scalar (atomic): tiles touched > 0
+  unsigned long long* n_inst;  // scalar (atomic): sum of tile counts = K
+  unsigned long long* zrange;  // [2] fp64 bits of min / max visible depth (atomic)
   uint64_t* sh_wait;           // set in-kernel: mbarrier guarding staged SH (TMA path)
   // optional fp64 dump for lmgs_project
   double* dbg_mean2d;
@@ -71,7 +72,7 @@ struct PreprocessArgs {
   float* dbg_opacity;
 };
 
-void launch_preprocess(const PreprocessArgs& a, cudaStream_t s);
+int launch_preprocess(const PreprocessArgs& a, cudaStream_t s);  // returns kernels launched
 
 // ---------------------------------------------------------------------------
 // LSD radix sort (onesweep: one histogram pass + one scatter pass per digit
@@ -79,19 +80,26 @@ void launch_preprocess(const PreprocessArgs& a, cudaStream_t s);
 // The plan kernel detects trivial digits (all keys share it) and skips those
 // passes on the device; the result buffers are published in device slots.
 
+#ifndef LMGS_SORT_ITEMS
+#define LMGS_SORT_ITEMS 16
+#endif
+#ifndef LMGS_SORT_MIN_CTAS
+#define LMGS_SORT_MIN_CTAS 3
+#endif
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
 constexpr int kMaxPasses = 8;
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
+constexpr int kSortItems = LMGS_SORT_ITEMS;  // keys per thread per onesweep tile
 constexpr int kSortTile = kSortThreads * kSortItems;
 
 struct RadixPlan {
   int32_t n_passes;
+  int32_t first_active;  // first non-trivial pass (-1: none)
   int32_t active[kMaxPasses];
   int32_t src[kMaxPasses];
   int32_t result;
-  int32_t pad[7];
+  int32_t pad[6];
   uint32_t digit_start[kMaxPasses][kRadix];
 };
 
@@ -106,90 +114,80 @@ struct RadixSortBuffers {
   const int* gate;     // nullable: device flag, 0 -> the whole sort is a no-op
   void** keys_result;  // nullable: device slot receiving the result key buffer
   void** vals_result;  // nullable: device slot receiving the result value buffer
+  bool hist_ready;     // hist already holds every digit histogram (the producer built it)
+  bool iota_vals;      // vals[0] is implicit: value = input index (never read)
 };
 
 size_t radix_lookback_words(int64_t capacity);
 // sorts bits [begin_bit, begin_bit + 8*n_passes) of n keys (stable).
-void radix_sort(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_passes,
-                cudaStream_t s);
+int radix_sort(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_passes,
+               cudaStream_t s);  // returns kernels launched
 
 // Device-side slots naming where a sort's result landed (written by the plan
 // kernel, read by consumers) so the pipeline never syncs on it.
 struct DevSlots {
-  void* big_keys;  // oversized-bucket sort result keys
-  void* big_vals;  // oversized-bucket sort result ids
+  void* depth_keys;  // K2 result: fp32 depth keys in (depth, id) order
+  void* depth_ids;   // K2 result: Gaussian ids in (depth, id) order
+  void* inst_keys;   // K5 result: tile << 32 | id, sorted by tile then depth rank
+  void* unused;
 };
 
 // ---------------------------------------------------------------------------
-// tile binning (tiles.cu)
+// depth order + instance emission + tile ranges (tiles.cu)
 
-// runs of equal fp32 depth keys up to this length are fixed up in registers
-constexpr int kFixupRun = 32;
-constexpr int kSmallTileCap = 2048;    // bucket sorted by a 256-thread CTA, 32 KB smem
-constexpr int kMediumTileCap = 16384;  // bucket sorted by a 512-thread CTA, 208 KB smem
+constexpr int kMaxTilePasses = 3;  // tile ids < 2^24
 
-// K3a/K3b/K4: per-CTA (one per SM) tile histograms and placement
-constexpr int kBinThreads = 1024;
-constexpr int kSlabTiles = 49152;  // tile counters per shared-memory slab (192 KB)
+// K2a: 32-bit depth keys quantised over the view's visible depth range
+// (monotone in the fp64 depth; 0xffffffff = invisible) + their 4 digit
+// histograms for the radix sort
+int launch_depth_keys(const uint64_t* key64, const unsigned long long* zrange, int64_t n,
+                      uint32_t* key32, uint32_t* hist, cudaStream_t s);
 
-struct BinArgs {
-  const uint64_t* rects;
-  const uint32_t* counts;   // tiles touched per Gaussian
-  const uint32_t* key32;
-  int64_t n;
+// K2b: order runs of equal 32-bit keys by (fp64 depth, id) — _sort_order's exact key
+int launch_depth_fixup(void* const* keys_slot, void* const* ids_slot, int64_t n,
+                        const uint64_t* key64, cudaStream_t s);
+
+// K4: walk Gaussians in depth order, scan their tile counts (decoupled
+// look-back) and emit one key (tile << 32 | id) per overlapped tile — the
+// instance array comes out sorted by depth rank, so a stable sort by tile
+// alone yields rasterize's per-tile (depth, id) lists.  Also builds the tile
+// digit histograms of the K5 radix passes.
+constexpr int kEmitThreads = 256;
+constexpr int kEmitItems = 8;
+constexpr int kEmitChunk = kEmitThreads * kEmitItems;
+struct EmitArgs {
+  void* const* order_slot;  // -> uint32_t[n_vis] Gaussian ids in depth order
+  const uint64_t* rects;    // count = rect area (every splat in rank order is visible)
+  int64_t n_vis;
   int32_t tiles_x;
-  int32_t tiles;
-  int32_t ctas;             // Gaussian slices (CTAs) of K3a / K4
-  uint32_t* hist;           // [ctas][tiles] counts, then per-(cta, tile) offsets
-  uint32_t* tile_count;     // [tiles] out of K3b
-  const int2* ranges;       // K4 input
-  uint32_t* bucket;         // [K] out of K4: Gaussian ids, arbitrary order within a tile
+  int32_t n_tile_passes;
+  uint64_t* keys;           // [K] out
+  uint64_t* lookback;       // [chunks] status words
+  uint32_t* ticket;         // chunk ticket counter (zeroed)
+  uint32_t* hist;           // [kMaxTilePasses][256] digit histograms (zeroed)
 };
-size_t bin_smem_bytes(int tiles);
-void launch_bin_hist(const BinArgs& a, cudaStream_t s);   // K3a + K3b
-void launch_bin_place(const BinArgs& a, cudaStream_t s);  // K4
+inline int64_t emit_chunks(int64_t n_vis) { return (n_vis + kEmitChunk - 1) / kEmitChunk; }
+int launch_emit(const EmitArgs& a, cudaStream_t s);
 
-struct TileScanArgs {
-  const uint32_t* tile_count;  // [tiles]
-  int tiles;
-  int small_cap, medium_cap;
-  int2* ranges;                // [tiles] out: [start, end)
-  uint32_t* lists[3];          // [tiles] each: tile ids of class small/medium/big
-  uint32_t* class_counts;      // [3]
-  uint64_t* total;             // K
-};
-void launch_scan_tiles(const TileScanArgs& a, cudaStream_t s);
-
-struct TileSortArgs {
-  const uint32_t* bucket;
-  const uint32_t* key32;  // [n] fp32 depth keys (L2-resident gather)
-  const int2* ranges;
-  const uint64_t* key64;  // [n] fp64 depth bits (exact tie order)
-  uint32_t* sorted_ids;   // [K] out: per-tile lists in (depth, id) order
-};
-void launch_tile_sort(const TileSortArgs& a, const uint32_t* tile_list,
-                      const uint32_t* list_count, int n_list, int cls, cudaStream_t s);
-void launch_big_gather(const TileSortArgs& a, const uint32_t* big_list, int n_big,
-                       const uint32_t* big_off, uint64_t* keys, uint32_t* vals, cudaStream_t s);
-void launch_big_fixup(void* const* keys_ptr, void* const* vals_ptr, int64_t n,
-                      const uint64_t* key64, cudaStream_t s);
-void launch_big_scatter(const TileSortArgs& a, const uint32_t* big_list, int n_big,
-                        const uint32_t* big_off, void* const* vals_ptr, cudaStream_t s);
+// K6: tile ranges from the sorted keys ([start, end), empty tiles included)
+int launch_tile_ranges(void* const* keys_slot, int64_t k, int tiles, int2* ranges,
+                        cudaStream_t s);
 
 struct InstanceExportArgs {
   const int2* ranges;
-  const uint32_t* sorted_ids;
+  void* const* keys_slot;
   const int64_t* prim_ids;  // nullable: original ids
   uint64_t* keys_out;
   int64_t* prims_out;
+  int64_t k;
 };
-void launch_export_instances(const InstanceExportArgs& a, int tiles, cudaStream_t s);
+void launch_export_instances(const InstanceExportArgs& a, cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // blend (blend.cu) and compositing (raster.cu)
 
 struct BlendArgs {
-  const uint32_t* sorted_ids;
+  void* const* keys_slot;  // -> uint64_t[K] tile << 32 | id
   const int2* ranges;
   const BlendRec* recs;
   int32_t width, height, tile_size, tiles_x, tiles_y;

@@ -108,7 +108,6 @@ __device__ __forceinline__ void sh_color(const float* __restrict__ sh, int ncoef
   for (int ch = 0; ch < 3; ++ch) out[ch] = fminf(fmaxf(c[ch], 0.0f), 1.0f);
 }
 
-constexpr int kPreThreads = 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -139,11 +138,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 
 // One Gaussian.  Inputs arrive as values (from shared memory staged by TMA or
 // straight from global memory); `sh` points at its coefficients.
+constexpr int kPreThreads = 256;  // both kernels (count_kept reduces over 8 warps)
+
+// Returns the splat's tile count (0: culled or off-screen); *keep = near-kept.
 template <bool SMEM>
-__device__ __forceinline__ bool process_one(const PreprocessArgs& a, int64_t i, double m0, double m1,
+__device__ __forceinline__ uint32_t process_one(const PreprocessArgs& a, int64_t i, double m0, double m1,
                                             double m2, float4 q, double s0, double s1, double s2,
-                                            float logit, const float* sh) {
+                                            float logit, const float* sh, bool* keep_out) {
   bool keep = false;
+  uint32_t cnt = 0;
   {
     const CamArgs& cam = a.cam;
     // p = means @ r_wc.T + t_wc (195): MKL FMA chain, then + t
@@ -154,8 +157,6 @@ __device__ __forceinline__ bool process_one(const PreprocessArgs& a, int64_t i, 
     if (a.kept) a.kept[i] = keep;
     if (!keep) {
       a.depth_keys[i] = kCulledKey;
-      a.depth_keys32[i] = 0xffffffffu;
-      a.tile_counts[i] = 0;
       a.rects[i] = 0;
     } else {
       const double mx = cam.fx * x / z + cam.cx;  // 201
@@ -215,12 +216,11 @@ __device__ __forceinline__ bool process_one(const PreprocessArgs& a, int64_t i, 
       int x0, x1, y0, y1;
       axis_range(mx - radius, mx + radius, cam.width, cam.tile_size, cam.tiles_x, &x0, &x1);
       axis_range(my - radius, my + radius, cam.height, cam.tile_size, cam.tiles_y, &y0, &y1);
-      uint32_t cnt = 0;
       if (x0 <= x1 && y0 <= y1) cnt = (uint32_t)(x1 - x0 + 1) * (uint32_t)(y1 - y0 + 1);
-      a.tile_counts[i] = cnt;
-      a.rects[i] = cnt ? pack_rect(x0, y0, x1, y1) : 0;
-      a.depth_keys[i] = (uint64_t)__double_as_longlong(z);
-      a.depth_keys32[i] = __float_as_uint(__double2float_rd(z));
+      a.rects[i] = cnt ? pack_rect(x0, y0, x1, y1) : 0;  // read only for visible splats
+      // off-screen splats sort behind every visible one (K2 orders only the
+      // n_vis visible splats)
+      a.depth_keys[i] = cnt ? (uint64_t)__double_as_longlong(z) : kCulledKey;
       // conic (_blend 309-310), fp64 then pre-scaled to the exp2 domain in fp32
       const double det = ca * cc - cb * cb;
       const double ica = cc / det, icb = -cb / det, icc = ca / det;
@@ -263,25 +263,68 @@ __device__ __forceinline__ bool process_one(const PreprocessArgs& a, int64_t i, 
       }
     }
   }
-  return keep;
+  *keep_out = keep;
+  return cnt;
 }
 
-__device__ __forceinline__ void count_kept(const PreprocessArgs& a, bool keep) {
+// block-aggregated counters: near-kept splats (M), visible splats, instances
+// (K), and the visible depth range (positive fp64 bits order like integers).
+// One atomic per counter per CTA: per-warp atomics on these five addresses
+// serialised in L2 and doubled the kernel's time.
+__device__ __forceinline__ void count_kept(const PreprocessArgs& a, bool keep, uint32_t cnt,
+                                           int64_t i) {
+  __shared__ unsigned long long s_acc[kPreThreads / 32][5];
   const unsigned ballot = __ballot_sync(0xffffffffu, keep);
-  if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(a.n_kept, (unsigned long long)__popc(ballot));
+  const unsigned vis = __ballot_sync(0xffffffffu, cnt > 0);
+  unsigned long long k = cnt;
+  unsigned long long zlo = ~0ull, zhi = 0ull;
+  if (cnt) zlo = zhi = a.depth_keys[i];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    k += __shfl_xor_sync(0xffffffffu, k, o);
+    zlo = min(zlo, __shfl_xor_sync(0xffffffffu, zlo, o));
+    zhi = max(zhi, __shfl_xor_sync(0xffffffffu, zhi, o));
+  }
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s_acc[warp][0] = __popc(ballot);
+    s_acc[warp][1] = __popc(vis);
+    s_acc[warp][2] = k;
+    s_acc[warp][3] = zlo;
+    s_acc[warp][4] = zhi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long kept = 0, nv = 0, inst = 0, lo = ~0ull, hi = 0ull;
+    for (int w = 0; w < kPreThreads / 32; ++w) {
+      kept += s_acc[w][0];
+      nv += s_acc[w][1];
+      inst += s_acc[w][2];
+      lo = min(lo, s_acc[w][3]);
+      hi = max(hi, s_acc[w][4]);
+    }
+    if (kept) atomicAdd(a.n_kept, kept);
+    if (nv) {
+      atomicAdd(a.n_vis, nv);
+      atomicMin(a.zrange, lo);
+      atomicMax(a.zrange + 1, hi);
+    }
+    if (inst) atomicAdd(a.n_inst, inst);
+  }
 }
 
 // direct loads (tail block, unaligned inputs)
 __global__ void __launch_bounds__(256) k_preprocess_direct(PreprocessArgs a, int64_t first) {
   const int64_t i = first + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool keep = false;
+  uint32_t cnt = 0;
   if (i < a.n) {
     const float4 q = __ldg(reinterpret_cast<const float4*>(a.quats) + i);
-    keep = process_one<false>(a, i, a.means[3 * i], a.means[3 * i + 1], a.means[3 * i + 2], q,
-                              a.scales[3 * i], a.scales[3 * i + 1], a.scales[3 * i + 2],
-                              a.logits[i], a.sh + i * a.sh_coeffs * 3);
+    cnt = process_one<false>(a, i, a.means[3 * i], a.means[3 * i + 1], a.means[3 * i + 2], q,
+                             a.scales[3 * i], a.scales[3 * i + 1], a.scales[3 * i + 2],
+                             a.logits[i], a.sh + i * a.sh_coeffs * 3, &keep);
   }
-  count_kept(a, keep);
+  count_kept(a, keep, cnt, i);
 }
 
 // ---------------------------------------------------------------------------
@@ -321,11 +364,12 @@ __global__ void __launch_bounds__(kPreThreads, 2) k_preprocess_tma(PreprocessArg
   const float4 q = reinterpret_cast<const float4*>(s_quats)[tid];
   // the SH wait happens inside process_one just before the colour is needed
   a.sh_wait = &s_bar[1];
-  const bool keep =
+  bool keep = false;
+  const uint32_t cnt =
       process_one<true>(a, i, s_means[3 * tid], s_means[3 * tid + 1], s_means[3 * tid + 2], q,
                         s_scales[3 * tid], s_scales[3 * tid + 1], s_scales[3 * tid + 2],
-                        s_logits[tid], s_sh + tid * a.sh_coeffs * 3);
-  count_kept(a, keep);
+                        s_logits[tid], s_sh + tid * a.sh_coeffs * 3, &keep);
+  count_kept(a, keep, cnt, i);
   // every thread must observe the SH barrier before the block may exit
   mbar_wait(&s_bar[1], 0);
 }
@@ -333,8 +377,9 @@ __global__ void __launch_bounds__(kPreThreads, 2) k_preprocess_tma(PreprocessArg
 
 }  // namespace
 
-void launch_preprocess(const PreprocessArgs& a, cudaStream_t s) {
-  if (a.n <= 0) return;
+int launch_preprocess(const PreprocessArgs& a, cudaStream_t s) {
+  if (a.n <= 0) return 0;
+  int launched = 0;
   // full blocks through TMA when every chunk is 16-byte aligned and sized
   const bool aligned =
       ((reinterpret_cast<uintptr_t>(a.means) | reinterpret_cast<uintptr_t>(a.quats) |
@@ -350,11 +395,15 @@ void launch_preprocess(const PreprocessArgs& a, cudaStream_t s) {
       set = smem;
     }
     k_preprocess_tma<<<(unsigned)full, kPreThreads, smem, s>>>(a);
+    ++launched;
   }
   const int64_t first = full * kPreThreads;
   const int64_t rest = a.n - first;
-  if (rest > 0)
+  if (rest > 0) {
     k_preprocess_direct<<<(unsigned)((rest + 255) / 256), 256, 0, s>>>(a, first);
+    ++launched;
+  }
+  return launched;
 }
 
 }  // namespace lmgs

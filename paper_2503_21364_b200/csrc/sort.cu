@@ -1,9 +1,11 @@
 // Device-wide LSD radix sort (onesweep).
 //
-// Used for tile buckets too large for one CTA's shared memory (tiles.cu):
-// keys (bucket index << 32 | fp32 depth bits), id payload; equal-key runs are
-// then fixed up by the exact (fp64 depth, id) pair — rasterize's per-tile
-// _sort_order (gaussian_core.py:392 -> 277-283).
+// Two sorts per view:
+//   K2  fp32 depth keys of all Gaussians with an implicit id payload (stable,
+//       so equal keys stay in id order; runs of equal fp32 keys are then fixed
+//       up by the exact fp64 depth — _sort_order, gaussian_core.py:277-283);
+//   K5  the instance keys tile << 32 | id, sorted on the tile bits only
+//       (stable: the emitted array is already in depth-rank order).
 //
 // Per sort: one histogram kernel computes every digit's global histogram in a
 // single read; a 1-block plan kernel scans them, marks digits all keys share
@@ -21,6 +23,10 @@ constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagIncl = 2u << 30;
 constexpr uint32_t kValueMask = (1u << 30) - 1;
 constexpr int kWarps = kSortThreads / 32;
+#ifndef LMGS_LOOK_WINDOW
+#define LMGS_LOOK_WINDOW 8
+#endif
+constexpr int kLookWindow = LMGS_LOOK_WINDOW;
 
 // Look-back status words carry their payload (flag | value) in one atomic
 // word and publish nothing else, so relaxed gpu-scope accesses suffice; an
@@ -100,13 +106,17 @@ __global__ void __launch_bounds__(kRadix) k_radix_plan(const uint32_t* __restric
     }
   }
   if (d == 0) {
-    int cur = 0;
+    int cur = 0, first = -1;
     for (int p = 0; p < kMaxPasses; ++p) {
       const int act = !off && p < n_passes && !s_trivial[p] && n > 1;
       plan->active[p] = act;
       plan->src[p] = cur;
-      if (act) cur ^= 1;
+      if (act) {
+        cur ^= 1;
+        if (first < 0) first = p;
+      }
     }
+    plan->first_active = first;
     plan->result = cur;
     plan->n_passes = n_passes;
     if (!off) {
@@ -117,16 +127,28 @@ __global__ void __launch_bounds__(kRadix) k_radix_plan(const uint32_t* __restric
 }
 
 // one onesweep scatter pass (digit `pass`)
-template <typename K>
-__global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(
+//
+// 1. load kSortTile keys (warp-striped, coalesced);
+// 2. early counts: the CTA's digit histogram by shared atomics, published at
+//    once to the look-back array so successors never wait on our ranking;
+// 3. stable rank inside each warp: lanes holding the same digit find each other
+//    through a per-warp shared "match" word (atomicOr of their lane bits, read
+//    back, cleared by the lowest lane) — MATCH.ANY serialises on this part;
+// 4. per-digit prefix over warps, staging in shared memory in digit order;
+// 5. decoupled look-back (windowed) for the global digit offsets;
+// 6. coalesced write-out in per-digit runs.
+template <typename K, bool VALS>
+__global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
     K* keys0, K* keys1, uint32_t* vals0, uint32_t* vals1, int64_t n, int begin_bit, int pass,
-    const RadixPlan* __restrict__ plan, uint32_t* lookback, uint32_t* counter, int64_t lb_stride) {
+    const RadixPlan* __restrict__ plan, uint32_t* lookback, uint32_t* counter, int64_t lb_stride,
+    bool iota_vals) {
   if (!plan->active[pass]) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  // layout: [warp counters | exchange keys | exchange vals] + small arrays
-  uint32_t* s_warp = reinterpret_cast<uint32_t*>(smem_raw);  // [kWarps][kRadix]
-  K* s_keys = reinterpret_cast<K*>(smem_raw);                 // [kSortTile] (after ranking)
+  K* s_keys = reinterpret_cast<K*>(smem_raw);  // [kSortTile] staging
   uint32_t* s_vals = reinterpret_cast<uint32_t*>(smem_raw + sizeof(K) * kSortTile);
+  __shared__ uint32_t s_match[kWarps][kRadix];
+  __shared__ uint32_t s_wcnt[kWarps][kRadix];
+  __shared__ uint32_t s_hist[kRadix];
   __shared__ uint32_t s_local_start[kRadix];
   __shared__ uint32_t s_global[kRadix];
   __shared__ uint32_t s_bid;
@@ -134,7 +156,11 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_bid = atomicAdd(counter + pass, 1u);
-  for (int i = tid; i < kWarps * kRadix; i += kSortThreads) s_warp[i] = 0;
+  for (int i = tid; i < kWarps * kRadix; i += kSortThreads) {
+    (&s_match[0][0])[i] = 0;
+    (&s_wcnt[0][0])[i] = 0;
+  }
+  s_hist[tid] = 0;  // kSortThreads == kRadix
   __syncthreads();
   const uint32_t bid = s_bid;
   const int64_t base = (int64_t)bid * kSortTile;
@@ -145,56 +171,43 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(
   K* __restrict__ kout = src ? keys0 : keys1;
   const uint32_t* __restrict__ vin = src ? vals1 : vals0;
   uint32_t* __restrict__ vout = src ? vals0 : vals1;
-  const bool has_vals = vals0 != nullptr;
+  // implicit payload on the first pass that moves data: value = input index
+  const bool iota = iota_vals && pass == plan->first_active;
   const int shift = begin_bit + 8 * pass;
 
   K key[kSortItems];
-  uint32_t val[kSortItems];
+  uint32_t val[VALS ? kSortItems : 1];
   uint32_t pos[kSortItems];
   const int wbase = warp * 32 * kSortItems;
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const int i = wbase + j * 32 + lane;
     key[j] = i < count ? kin[base + i] : (K)~(K)0;
-    if (has_vals) val[j] = i < count ? vin[base + i] : 0u;
+    if (VALS) val[j] = iota ? (uint32_t)(base + i) : (i < count ? vin[base + i] : 0u);
   }
-  // stable rank within the warp: items in (j, lane) order
-  const uint32_t lt = lanemask_lt();
-  uint32_t* my_cnt = s_warp + warp * kRadix;
+#ifdef LMGS_DBG_COPY
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const int i = wbase + j * 32 + lane;
-    const bool valid = i < count;
-    const uint32_t d = digit_of(key[j], shift);
-    const uint32_t peers = __match_any_sync(0xffffffffu, valid ? d : 256u + lane);
-    // the lowest peer bumps the warp counter; the returned old count is this
-    // round's base.  Shared-memory atomics of one warp retire in issue order,
-    // so successive rounds need no read-modify-write chain through registers.
-    const int leader = __ffs(peers) - 1;
-    uint32_t old = 0;
-    if (valid && lane == leader) old = atomicAdd(my_cnt + d, (uint32_t)__popc(peers));
-    old = __shfl_sync(0xffffffffu, old, leader);
-    pos[j] = old + __popc(peers & lt);
+    if (i < count) {
+      kout[base + i] = key[j];
+      if (VALS) vout[base + i] = val[j];
+    }
   }
+  return;
+#endif
+  // 2. early counts, published with the look-back before ranking
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j)
+    if (wbase + j * 32 + lane < count) atomicAdd(&s_hist[digit_of(key[j], shift)], 1u);
   __syncthreads();
-  // per digit (thread d): warp-exclusive offsets, block total, block-local start
-  uint32_t total;
+  uint32_t* lb = lookback + ((int64_t)pass * lb_stride) * kRadix;
+  const uint32_t total = s_hist[tid];  // thread d == digit d
   {
     const int d = tid;
-    uint32_t run = 0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      const uint32_t c = s_warp[w * kRadix + d];
-      s_warp[w * kRadix + d] = run;
-      run += c;
-    }
-    total = run;
-    // publish the aggregate early so successors can proceed
-    uint32_t* lb = lookback + ((int64_t)pass * lb_stride) * kRadix;
     if (bid == 0) st_release(lb + d, kFlagIncl | total);
     else st_release(lb + (int64_t)bid * kRadix + d, kFlagAgg | total);
-    // block-wide exclusive scan over digits
-    uint32_t incl = total;
+    uint32_t incl = total;  // block-wide exclusive scan over digits
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
@@ -206,86 +219,153 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) wpre += w < warp ? s_wsum[w] : 0;
     s_local_start[d] = wpre + incl - total;
-  }
-  __syncthreads();
-  // local positions, then stage keys (and values) in digit order
-#pragma unroll
-  for (int j = 0; j < kSortItems; ++j) {
-    const uint32_t d = digit_of(key[j], shift);
-    pos[j] += s_local_start[d] + s_warp[warp * kRadix + d];
-  }
-  __syncthreads();  // s_warp is reused as exchange space
-#pragma unroll
-  for (int j = 0; j < kSortItems; ++j) {
-    if (wbase + j * 32 + lane < count) {
-      s_keys[pos[j]] = key[j];
-      if (has_vals) s_vals[pos[j]] = val[j];
-    }
-  }
-  // decoupled look-back for this tile's global digit offsets
-  {
-    const int d = tid;
-    uint32_t* lb = lookback + ((int64_t)pass * lb_stride) * kRadix;
+    // decoupled look-back for this tile's global digit offsets, right after
+    // the early counts so the inclusive prefix is published before ranking.
+    // Each digit's thread reads a window of kLookWindow predecessors with
+    // independent loads (one L2 round trip per window, not per predecessor),
+    // then walks it from the nearest one, re-polling only unpublished entries.
     uint32_t excl = 0;
+#ifdef LMGS_DBG_NO_LOOKBACK
+    if (false) {
+#else
     if (bid != 0) {
+#endif
       int64_t look = (int64_t)bid - 1;
-      while (true) {
-        uint32_t v;
-        do {
-          v = ld_acquire(lb + look * kRadix + d);
-        } while ((v & ~kValueMask) == 0);
-        excl += v & kValueMask;
-        if ((v & ~kValueMask) == kFlagIncl) break;
-        --look;
+      bool done = false;
+      while (!done) {
+        uint32_t v[kLookWindow];
+#pragma unroll
+        for (int w = 0; w < kLookWindow; ++w)
+          v[w] = look - w >= 0 ? ld_acquire(lb + (look - w) * kRadix + d) : kFlagIncl;
+#pragma unroll
+        for (int w = 0; w < kLookWindow; ++w) {
+          if (done) break;
+          while ((v[w] & ~kValueMask) == 0) v[w] = ld_acquire(lb + (look - w) * kRadix + d);
+          excl += v[w] & kValueMask;
+          done = (v[w] & ~kValueMask) == kFlagIncl;
+        }
+        look -= kLookWindow;
       }
       st_release(lb + (int64_t)bid * kRadix + d, kFlagIncl | (excl + total));
     }
-    s_global[d] = plan->digit_start[pass][d] + excl - s_local_start[d];
+    s_global[d] = plan->digit_start[pass][d] + excl - (wpre + incl - total);
+  }
+  // 3. stable in-warp ranking, items in (j, lane) order
+  const uint32_t lt = lanemask_lt();
+  uint32_t* my_match = s_match[warp];
+  uint32_t* my_cnt = s_wcnt[warp];
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const bool valid = wbase + j * 32 + lane < count;
+    const uint32_t d = digit_of(key[j], shift);
+    if (valid) atomicOr(my_match + d, 1u << lane);
+    __syncwarp();
+    const uint32_t peers = valid ? my_match[d] : (1u << lane);
+    __syncwarp();
+    const int leader = __ffs(peers) - 1;
+    uint32_t before = 0;
+    if (valid && lane == leader) {
+      before = my_cnt[d];
+      my_cnt[d] = before + (uint32_t)__popc(peers);
+      my_match[d] = 0;
+    }
+    before = __shfl_sync(0xffffffffu, before, leader);
+    pos[j] = before + __popc(peers & lt);
+    __syncwarp();
   }
   __syncthreads();
-  // coalesced write-out: consecutive threads, consecutive staged positions
+  // 4. per digit: exclusive prefix over warps
+  {
+    const int d = tid;
+    uint32_t run = s_local_start[d];
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t c = s_wcnt[w][d];
+      s_wcnt[w][d] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    if (wbase + j * 32 + lane < count) {
+      const uint32_t p = pos[j] + my_cnt[digit_of(key[j], shift)];
+      s_keys[p] = key[j];
+      if (VALS) s_vals[p] = val[j];
+    }
+  }
+  __syncthreads();
+  // 6. coalesced write-out: consecutive threads, consecutive staged positions
   for (int i = tid; i < count; i += kSortThreads) {
     const K k = s_keys[i];
     const uint32_t o = s_global[digit_of(k, shift)] + i;
     kout[o] = k;
-    if (has_vals) vout[o] = s_vals[i];
+    if (VALS) vout[o] = s_vals[i];
   }
 }
 
-template <typename K>
+// implicit payload with no data-moving pass (every digit trivial): the result
+// buffer vals[0] still has to hold the identity permutation
+__global__ void k_iota_if_idle(const RadixPlan* __restrict__ plan, uint32_t* vals, int64_t n) {
+  if (plan->first_active >= 0) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    vals[i] = (uint32_t)i;
+}
+
+template <typename K, bool VALS>
 constexpr size_t onesweep_smem() {
-  return sizeof(K) * kSortTile + sizeof(uint32_t) * kSortTile;
+  return sizeof(K) * kSortTile + (VALS ? sizeof(uint32_t) * kSortTile : 0);
+}
+
+template <typename K, bool VALS>
+void launch_onesweep(const RadixSortBuffers& b, int64_t n, int begin_bit, int p, int64_t blocks,
+                     cudaStream_t s) {
+  constexpr size_t smem = onesweep_smem<K, VALS>();
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_onesweep<K, VALS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr_set = true;
+  }
+  k_onesweep<K, VALS><<<(unsigned)blocks, kSortThreads, smem, s>>>(
+      static_cast<K*>(b.keys[0]), static_cast<K*>(b.keys[1]), b.vals[0], b.vals[1], n, begin_bit,
+      p, b.plan, b.lookback, b.counters, blocks, b.iota_vals);
 }
 
 template <typename K>
-void radix_sort_impl(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_passes,
-                     cudaStream_t s) {
+int radix_sort_impl(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_passes,
+                    cudaStream_t s) {
+  int launched = 0;
   if (n_passes > kMaxPasses) n_passes = kMaxPasses;
   const int64_t blocks = (n + kSortTile - 1) / kSortTile;
-  cudaMemsetAsync(b.hist, 0, sizeof(uint32_t) * kMaxPasses * kRadix, s);
+  if (!b.hist_ready) cudaMemsetAsync(b.hist, 0, sizeof(uint32_t) * kMaxPasses * kRadix, s);
   cudaMemsetAsync(b.counters, 0, sizeof(uint32_t) * kMaxPasses, s);
   if (blocks > 0 && n_passes > 0)
     cudaMemsetAsync(b.lookback, 0, sizeof(uint32_t) * (size_t)n_passes * blocks * kRadix, s);
   K* k0 = static_cast<K*>(b.keys[0]);
   K* k1 = static_cast<K*>(b.keys[1]);
-  if (n > 0 && n_passes > 0) {
+  if (n > 0 && n_passes > 0 && !b.hist_ready) {
     int hist_blocks = (int)((n + kSortThreads * 16 - 1) / (kSortThreads * 16));
     if (hist_blocks > 148 * 4) hist_blocks = 148 * 4;
     k_radix_hist<K><<<hist_blocks, kSortThreads, 0, s>>>(k0, n, begin_bit, n_passes, b.hist,
                                                          b.gate);
+    ++launched;
   }
   k_radix_plan<<<1, kRadix, 0, s>>>(b.hist, n, n_passes, b.plan, b.gate, k0, k1, b.vals[0],
                                     b.vals[1], b.keys_result, b.vals_result);
-  if (blocks == 0) return;
-  const size_t smem = onesweep_smem<K>();
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_onesweep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set = true;
+  ++launched;
+  if (b.iota_vals && n > 0) {
+    const int64_t g = (n + 255) / 256;
+    k_iota_if_idle<<<(unsigned)(g < 148 * 8 ? g : 148 * 8), 256, 0, s>>>(b.plan, b.vals[0], n);
+    ++launched;
   }
-  for (int p = 0; p < n_passes; ++p)
-    k_onesweep<K><<<(unsigned)blocks, kSortThreads, smem, s>>>(
-        k0, k1, b.vals[0], b.vals[1], n, begin_bit, p, b.plan, b.lookback, b.counters, blocks);
+  if (blocks == 0) return launched;
+  for (int p = 0; p < n_passes; ++p) {
+    if (b.vals[1]) launch_onesweep<K, true>(b, n, begin_bit, p, blocks, s);
+    else launch_onesweep<K, false>(b, n, begin_bit, p, blocks, s);
+  }
+  return launched + n_passes;
 }
 
 }  // namespace
@@ -295,10 +375,10 @@ size_t radix_lookback_words(int64_t capacity) {
   return (size_t)kMaxPasses * (size_t)(blocks > 0 ? blocks : 1) * kRadix;
 }
 
-void radix_sort(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_passes,
-                cudaStream_t s) {
-  if (b.key_bytes == 4) radix_sort_impl<uint32_t>(b, n, begin_bit, n_passes, s);
-  else radix_sort_impl<uint64_t>(b, n, begin_bit, n_passes, s);
+int radix_sort(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_passes,
+               cudaStream_t s) {
+  if (b.key_bytes == 4) return radix_sort_impl<uint32_t>(b, n, begin_bit, n_passes, s);
+  return radix_sort_impl<uint64_t>(b, n, begin_bit, n_passes, s);
 }
 
 }  // namespace lmgs

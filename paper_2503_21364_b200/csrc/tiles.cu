@@ -1,35 +1,28 @@
-// Tile binning: K3 tile counts + scan, K4 placement, K5 per-tile sort, export.
+// Tile instance lists: K2b depth-order fix-up, K4 emission, K6 tile ranges,
+// instance export.
 //
 // Reference: rasterize (gaussian_core.py:340-403) builds, for every tile, the
 // list of splats whose bbox overlaps it (367-373) in _sort_order's
 // (depth, prim_id) order (277-283, 392).
 //
-// B200 design — per-tile lists are built tile-locally, with no global sort
-// and no hot global atomics:
-//   K3a  one CTA per SM owns a contiguous slice of Gaussians and builds the
-//        per-tile instance histogram of its slice in shared memory (8K-32K
-//        counters), writing one row H[cta][tile];
-//   K3b  a column scan turns H into per-(cta, tile) offsets and tile totals;
-//   K3c  one CTA scans the tile totals: tile_ranges (an output), K, and the
-//        size class of every tile;
-//   K4   the same CTAs place their instances (Gaussian ids, 4 B) into the
-//        tile buckets through shared-memory cursors (order inside a bucket
-//        is arbitrary);
-//   K5   one CTA per bucket sorts it in shared memory: one counting pass into
-//        4096 bins over the bucket's fp32-key range, then per-bin insertion
-//        sorts by (fp32 key, fp64 depth, id) — the exact order;
-//   big  buckets above kMediumTileCap: onesweep radix on
-//        (bucket index << 32 | fp32 key) + the same fix-up (sort.cu).
+// B200 design — sort each splat once, not each (splat, tile) pair:
+//   K2   one device-wide radix sort of 32-bit depth keys of all N splats
+//        (K2a quantises the fp64 depth over the view's depth range; sort.cu,
+//        stable, payload = id), then K2b fixes the order inside runs of equal
+//        keys by the exact fp64 depth: the result is the global rank order
+//        (depth, id) of the visible splats;
+//   K4   walks the splats in rank order, scans their tile counts (one pass,
+//        decoupled look-back) and emits one 8-byte key tile << 32 | id per
+//        overlapped tile, so the instance array comes out already ordered by
+//        depth rank; it also builds the tile-digit histograms of K5;
+//   K5   a stable LSD radix sort of those keys on the tile bits only (sort.cu,
+//        2 passes of 8 bits at 1080p) — every tile's list is then exactly the
+//        reference's per-tile (depth, id) order, with no per-tile sort;
+//   K6   tile ranges [start, end) from the boundaries of the sorted keys.
 #include "lmgs_internal.cuh"
 
 namespace lmgs {
 namespace {
-
-__device__ __forceinline__ uint32_t lanemask_lt() {
-  uint32_t m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
 
 __device__ __forceinline__ void unpack_rect(uint64_t rect, int& x0, int& y0, int& x1, int& y1) {
   x0 = (int)(rect & 0xffff);
@@ -39,178 +32,53 @@ __device__ __forceinline__ void unpack_rect(uint64_t rect, int& x0, int& y0, int
 }
 
 // ---------------------------------------------------------------------------
-// K3a: per-CTA shared-memory tile histograms
+// K2a: 32-bit depth keys.  key = trunc((z - zmin) * (2^32 - 2) / (zmax - zmin))
+// is monotone non-decreasing in z (each rounded fp64 step is), so sorting by
+// it and then by the exact fp64 depth inside equal-key runs gives _sort_order's
+// (depth, id) order; over the view's own depth range it separates far more
+// depths than an fp32 rounding of z would (runs become rare).
 
-__global__ void __launch_bounds__(kBinThreads) k_bin_hist(BinArgs a) {
-  extern __shared__ __align__(16) uint32_t s_cnt[];
-  const int c = blockIdx.x;
-  const int64_t lo = a.n * c / a.ctas, hi = a.n * (c + 1) / a.ctas;
-  for (int slab = 0; slab < a.tiles; slab += kSlabTiles) {
-    const int sw = min(kSlabTiles, a.tiles - slab);
-    for (int t = threadIdx.x; t < sw; t += blockDim.x) s_cnt[t] = 0;
-    __syncthreads();
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-      if (!a.counts[i]) continue;
-      int x0, y0, x1, y1;
-      unpack_rect(a.rects[i], x0, y0, x1, y1);
-      for (int y = y0; y <= y1; ++y)
-        for (int x = x0; x <= x1; ++x) {
-          const unsigned t = (unsigned)(y * a.tiles_x + x - slab);
-          if (t < (unsigned)sw) atomicAdd(s_cnt + t, 1u);
-        }
+__global__ void __launch_bounds__(256) k_depth_keys(const uint64_t* __restrict__ key64,
+                                                    const unsigned long long* zrange, int64_t n,
+                                                    uint32_t* __restrict__ key32,
+                                                    uint32_t* hist) {
+  __shared__ uint32_t s_hist[4][256];
+  for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&s_hist[0][0])[i] = 0;
+  __syncthreads();
+  const double zmin = __longlong_as_double((long long)zrange[0]);
+  const double zmax = __longlong_as_double((long long)zrange[1]);
+  const double span = zmax - zmin;
+  const double scale = span > 0.0 ? 4294967294.0 / span : 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t kb = key64[i];
+    uint32_t k = 0xffffffffu;
+    if (kb != kCulledKey) {
+      const double q = (__longlong_as_double((long long)kb) - zmin) * scale;
+      k = q >= 4294967294.0 ? 4294967294u : (uint32_t)q;
     }
-    __syncthreads();
-    uint32_t* row = a.hist + (int64_t)c * a.tiles + slab;
-    for (int t = threadIdx.x; t < sw; t += blockDim.x) row[t] = s_cnt[t];
-    __syncthreads();
-  }
-}
-
-// K3b: exclusive scan down each tile column of H; totals per tile.  Loads
-// are batched 16 deep so the column walk is not a chain of dependent misses.
-__global__ void k_bin_colscan(BinArgs a) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= a.tiles) return;
-  uint32_t* __restrict__ col = a.hist + t;
-  const int64_t stride = a.tiles;
-  uint32_t run = 0;
-  int c = 0;
-  for (; c + 16 <= a.ctas; c += 16) {
-    uint32_t v[16];
+    key32[i] = k;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = col[(c + j) * stride];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      col[(c + j) * stride] = run;
-      run += v[j];
-    }
-  }
-  for (; c < a.ctas; ++c) {
-    const uint32_t v = col[c * stride];
-    col[c * stride] = run;
-    run += v;
-  }
-  a.tile_count[t] = run;
-}
-
-// ---------------------------------------------------------------------------
-// K3c: exclusive scan of tile counts (one CTA), classification by size
-
-constexpr int kScanTilesThreads = 1024;
-
-__global__ void __launch_bounds__(kScanTilesThreads) k_scan_tiles(TileScanArgs a) {
-  __shared__ uint32_t s_warp[kScanTilesThreads / 32];
-  __shared__ unsigned long long s_carry;
-  __shared__ uint32_t s_cls[3];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    s_carry = 0;
-    s_cls[0] = s_cls[1] = s_cls[2] = 0;
+    for (int d = 0; d < 4; ++d) atomicAdd(&s_hist[d][(k >> (8 * d)) & 0xffu], 1u);
   }
   __syncthreads();
-  for (int base = 0; base < a.tiles; base += kScanTilesThreads) {
-    const int t = base + tid;
-    const uint32_t c = t < a.tiles ? a.tile_count[t] : 0u;
-    uint32_t incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t w = s_warp[lane];
-      uint32_t wi = w;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xffffffffu, wi, o);
-        if (lane >= o) wi += v;
-      }
-      s_warp[lane] = wi - w;
-    }
-    __syncthreads();
-    const unsigned long long excl = s_carry + s_warp[warp] + (incl - c);
-    if (t < a.tiles) {
-      a.ranges[t] = make_int2((int)excl, (int)(excl + c));
-      if (c > 0) {
-        const int cls = c <= (uint32_t)a.small_cap ? 0 : (c <= (uint32_t)a.medium_cap ? 1 : 2);
-        const uint32_t slot = atomicAdd(&s_cls[cls], 1u);
-        a.lists[cls][slot] = (uint32_t)t;
-      }
-    }
-    __syncthreads();
-    if (tid == kScanTilesThreads - 1) s_carry = excl + c;
-    __syncthreads();
-  }
-  if (tid == 0) {
-    *a.total = s_carry;
-    a.class_counts[0] = s_cls[0];
-    a.class_counts[1] = s_cls[1];
-    a.class_counts[2] = s_cls[2];
+  for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) {
+    const uint32_t v = (&s_hist[0][0])[i];
+    if (v) atomicAdd(hist + i, v);
   }
 }
 
 // ---------------------------------------------------------------------------
-// K4: placement through shared-memory cursors (same CTA slices as K3a)
-
-__global__ void __launch_bounds__(kBinThreads) k_bin_place(BinArgs a) {
-  extern __shared__ __align__(16) uint32_t s_pos[];
-  const int c = blockIdx.x;
-  const int64_t lo = a.n * c / a.ctas, hi = a.n * (c + 1) / a.ctas;
-  for (int slab = 0; slab < a.tiles; slab += kSlabTiles) {
-    const int sw = min(kSlabTiles, a.tiles - slab);
-    const uint32_t* row = a.hist + (int64_t)c * a.tiles + slab;
-    for (int t = threadIdx.x; t < sw; t += blockDim.x)
-      s_pos[t] = (uint32_t)a.ranges[slab + t].x + row[t];
-    __syncthreads();
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-      if (!a.counts[i]) continue;
-      int x0, y0, x1, y1;
-      unpack_rect(a.rects[i], x0, y0, x1, y1);
-      for (int y = y0; y <= y1; ++y)
-        for (int x = x0; x <= x1; ++x) {
-          const unsigned t = (unsigned)(y * a.tiles_x + x - slab);
-          if (t < (unsigned)sw) a.bucket[atomicAdd(s_pos + t, 1u)] = (uint32_t)i;
-        }
-    }
-    __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------------------
-// exact fix-up of a run of equal fp32 keys: order by (fp64 depth bits, id)
+// K2b: exact fix-up of a run of equal keys: order by (fp64 depth bits, id).
+// The radix sort is stable and its payload is the input index, so a run is
+// already in id order; an in-place insertion sort is linear on the common
+// run (exact duplicates) and runs are short.
 
 __device__ __forceinline__ bool less64(uint64_t ka, uint32_t ia, uint64_t kb, uint32_t ib) {
   return ka < kb || (ka == kb && ia < ib);
 }
 
-// ids[0..len) hold one run; reorder by (key64[id], id).  Short runs are sorted
-// in registers; longer ones in place (insertion sort is linear on the common
-// long run — exact duplicates, already in id order).
 __device__ void fix_run(uint32_t* ids, int len, const uint64_t* __restrict__ key64) {
-  if (len <= kFixupRun) {
-    uint64_t dk[kFixupRun];
-    uint32_t id[kFixupRun];
-    for (int a = 0; a < len; ++a) {
-      id[a] = ids[a];
-      dk[a] = key64[id[a]];
-    }
-    for (int a = 1; a < len; ++a) {
-      const uint64_t kd = dk[a];
-      const uint32_t ki = id[a];
-      int b = a - 1;
-      while (b >= 0 && less64(kd, ki, dk[b], id[b])) {
-        dk[b + 1] = dk[b];
-        id[b + 1] = id[b];
-        --b;
-      }
-      dk[b + 1] = kd;
-      id[b + 1] = ki;
-    }
-    for (int a = 0; a < len; ++a) ids[a] = id[a];
-    return;
-  }
   for (int a = 1; a < len; ++a) {
     const uint32_t ki = ids[a];
     const uint64_t kd = key64[ki];
@@ -225,377 +93,253 @@ __device__ void fix_run(uint32_t* ids, int len, const uint64_t* __restrict__ key
   }
 }
 
-// ---------------------------------------------------------------------------
-// K5: per-tile sort in shared memory — one unstable MSD counting pass
-//
-// The exact order is (fp64 depth, id); the fp32 key is a monotone summary of
-// the fp64 depth, so any order that is sorted by fp32 key and then by
-// (fp64 depth, id) inside equal fp32 keys is exact.  Stability is therefore
-// never needed: entries are scattered by shared-memory atomics into NBINS
-// bins spanning the bucket's own [kmin, kmax] fp32-key range, then each bin
-// (a few entries) is insertion-sorted by (fp32 key, fp64 depth, id).  Bins
-// with more than kBinSortMax entries get a second counting pass over their
-// own key range (CTA-wide), then the same insertion sort.
-//
-// smem: buf (key u32 + bucket-local index u16) x CAP, cnt/start NBINS+1 each,
-// long-bin list.  Entries of the first pass are held in registers.
-
-constexpr int kBinSortMax = 64;
-
-__device__ __forceinline__ bool entry_less(uint32_t ka, uint32_t ia, uint32_t kb, uint32_t ib,
-                                           const uint64_t* __restrict__ key64) {
-  if (ka != kb) return ka < kb;
-  const uint64_t da = key64[ia], db = key64[ib];
-  return da < db || (da == db && ia < ib);
-}
-
-// insertion sort of buf[lo, hi) by (key, fp64 depth, id); ids resolved via the bucket
-__device__ void sort_small_bin(uint32_t* key, uint16_t* idx, int lo, int hi,
-                               const uint32_t* __restrict__ bucket,
-                               const uint64_t* __restrict__ key64) {
-  for (int a = lo + 1; a < hi; ++a) {
-    const uint32_t ka = key[a];
-    const uint16_t xa = idx[a];
-    const uint32_t ia = (uint32_t)bucket[xa];
-    int b = a - 1;
-    while (b >= lo) {
-      const uint32_t kb = key[b];
-      if (kb < ka) break;
-      if (kb == ka) {
-        const uint32_t ib = (uint32_t)bucket[idx[b]];
-        if (!entry_less(ka, ia, kb, ib, key64)) break;
-      }
-      key[b + 1] = kb;
-      idx[b + 1] = idx[b];
-      --b;
-    }
-    key[b + 1] = ka;
-    idx[b + 1] = xa;
-  }
-}
-
-template <int THREADS, int NBINS>
-__device__ __forceinline__ void block_exclusive_scan(uint32_t* v, uint32_t* s_wsum, int count) {
-  // v[0..count) -> exclusive prefix in place; v[count] = total.  count % THREADS == 0.
-  constexpr int PER = NBINS / THREADS;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint32_t loc[PER];
-  uint32_t sum = 0;
-#pragma unroll
-  for (int j = 0; j < PER; ++j) {
-    loc[j] = v[tid * PER + j];
-    sum += loc[j];
-  }
-  uint32_t incl = sum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += x;
-  }
-  if (lane == 31) s_wsum[warp] = incl;
-  __syncthreads();
-  uint32_t pre = 0;
-  for (int w = 0; w < warp; ++w) pre += s_wsum[w];
-  uint32_t run = pre + incl - sum;
-#pragma unroll
-  for (int j = 0; j < PER; ++j) {
-    v[tid * PER + j] = run;
-    run += loc[j];
-  }
-  if (tid == THREADS - 1) v[count] = run;
-  __syncthreads();
-  (void)count;
-}
-
-template <int THREADS, int CAP, int NBINS>
-__global__ void __launch_bounds__(THREADS) k_tile_sort(TileSortArgs a, const uint32_t* tile_list,
-                                                      const uint32_t* list_count) {
-  constexpr int PER = (CAP + THREADS - 1) / THREADS;
-  constexpr int NW = THREADS / 32;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint32_t* s_key = reinterpret_cast<uint32_t*>(smem_raw);                 // [CAP]
-  uint16_t* s_idx = reinterpret_cast<uint16_t*>(smem_raw + 4 * CAP);       // [CAP]
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem_raw + 6 * CAP);       // [NBINS + 1]
-  uint32_t* s_start = s_cnt + (NBINS + 1);                                 // [NBINS + 1]
-  uint16_t* s_long = reinterpret_cast<uint16_t*>(s_start + (NBINS + 1));   // [NBINS]
-  __shared__ uint32_t s_kmin, s_kmax, s_nlong;
-  __shared__ uint32_t s_wsum[NW];
-  const int tid = threadIdx.x, lane = tid & 31;
-  const uint32_t nlist = *list_count;
-  for (uint32_t li = blockIdx.x; li < nlist; li += gridDim.x) {
-    const int t = (int)tile_list[li];
-    const int2 r = a.ranges[t];
-    const int n = r.y - r.x;
-    const uint32_t* __restrict__ bucket = a.bucket + r.x;
-    if (tid == 0) {
-      s_kmin = 0xffffffffu;
-      s_kmax = 0u;
-      s_nlong = 0u;
-    }
-    for (int i = tid; i <= NBINS; i += THREADS) s_cnt[i] = 0u;
-    __syncthreads();
-    // level 1: entries into registers, key range
-    uint32_t rk[PER];
-    uint32_t kmin = 0xffffffffu, kmax = 0u;
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      const int i = tid + j * THREADS;
-      rk[j] = i < n ? a.key32[bucket[i]] : 0u;
-      if (i < n) {
-        kmin = min(kmin, rk[j]);
-        kmax = max(kmax, rk[j]);
-      }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
-      kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
-    }
-    if (lane == 0) {
-      atomicMin(&s_kmin, kmin);
-      atomicMax(&s_kmax, kmax);
-    }
-    __syncthreads();
-    const uint32_t k0 = s_kmin;
-    const uint32_t span = s_kmax - k0;
-    int shift = 0;
-    while ((span >> shift) >= (uint32_t)NBINS) ++shift;
-    uint32_t rbin[PER];
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      const int i = tid + j * THREADS;
-      rbin[j] = (rk[j] - k0) >> shift;
-      if (i < n) atomicAdd(s_cnt + rbin[j], 1u);
-    }
-    __syncthreads();
-    block_exclusive_scan<THREADS, NBINS>(s_cnt, s_wsum, NBINS);
-    for (int i = tid; i <= NBINS; i += THREADS) s_start[i] = s_cnt[i];
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      const int i = tid + j * THREADS;
-      if (i < n) {
-        const uint32_t p = atomicAdd(s_cnt + rbin[j], 1u);
-        s_key[p] = rk[j];
-        s_idx[p] = (uint16_t)i;
-      }
-    }
-    __syncthreads();
-    // per-bin ordering
-    for (int d = tid; d < NBINS; d += THREADS) {
-      const int lo = (int)s_start[d], hi = (int)s_start[d + 1];
-      if (hi - lo > kBinSortMax) s_long[atomicAdd(&s_nlong, 1u)] = (uint16_t)d;
-      else if (hi - lo > 1) sort_small_bin(s_key, s_idx, lo, hi, bucket, a.key64);
-    }
-    __syncthreads();
-    // level 2 for long bins, one bin at a time, CTA-wide
-    const int nlong = (int)s_nlong;
-    for (int q = 0; q < nlong; ++q) {
-      const int d = s_long[q];
-      const int lo = (int)s_start[d], hi = (int)s_start[d + 1];
-      const int len = hi - lo;
-      // into registers (len <= CAP)
-      uint32_t lk[PER];
-      uint16_t lx[PER];
-      uint32_t lmin = 0xffffffffu, lmax = 0u;
-#pragma unroll
-      for (int j = 0; j < PER; ++j) {
-        const int i = tid + j * THREADS;
-        if (i < len) {
-          lk[j] = s_key[lo + i];
-          lx[j] = s_idx[lo + i];
-          lmin = min(lmin, lk[j]);
-          lmax = max(lmax, lk[j]);
-        }
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        lmin = min(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
-        lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
-      }
-      __syncthreads();
-      if (tid == 0) {
-        s_kmin = 0xffffffffu;
-        s_kmax = 0u;
-      }
-      for (int i = tid; i <= NBINS; i += THREADS) s_cnt[i] = 0u;
-      __syncthreads();
-      if (lane == 0) {
-        atomicMin(&s_kmin, lmin);
-        atomicMax(&s_kmax, lmax);
-      }
-      __syncthreads();
-      const uint32_t l0 = s_kmin, lspan = s_kmax - l0;
-      if (lspan == 0) {  // all fp32 keys equal: order by (fp64 depth, id) only
-        __syncthreads();
-        if (tid == 0) sort_small_bin(s_key, s_idx, lo, hi, bucket, a.key64);
-        __syncthreads();
-        continue;
-      }
-      int sh = 0;
-      while ((lspan >> sh) >= (uint32_t)NBINS) ++sh;
-      uint32_t lb[PER];
-#pragma unroll
-      for (int j = 0; j < PER; ++j) {
-        const int i = tid + j * THREADS;
-        lb[j] = (lk[j] - l0) >> sh;
-        if (i < len) atomicAdd(s_cnt + lb[j], 1u);
-      }
-      __syncthreads();
-      block_exclusive_scan<THREADS, NBINS>(s_cnt, s_wsum, NBINS);
-      // s_start is still needed for the outer bins: keep the level-2 starts in
-      // s_cnt (cursor) and a copy in the tail of s_long's space is not
-      // available, so sub-bins are re-derived from the cursor after scatter.
-#pragma unroll
-      for (int j = 0; j < PER; ++j) {
-        const int i = tid + j * THREADS;
-        if (i < len) {
-          const uint32_t p = lo + atomicAdd(s_cnt + lb[j], 1u);
-          s_key[p] = lk[j];
-          s_idx[p] = lx[j];
-        }
-      }
-      __syncthreads();
-      // after the scatter s_cnt[b] = end of sub-bin b; sub-bin b = [end[b-1], end[b])
-      for (int b = tid; b < NBINS; b += THREADS) {
-        const int e = (int)s_cnt[b];
-        const int st = b ? (int)s_cnt[b - 1] : 0;
-        if (e - st > 1) sort_small_bin(s_key, s_idx, lo + st, lo + e, bucket, a.key64);
-      }
-      __syncthreads();
-    }
-    // write ids in order
-    for (int i = tid; i < n; i += THREADS) a.sorted_ids[r.x + i] = bucket[s_idx[i]];
-    __syncthreads();
-  }
-}
-
-template <int THREADS, int CAP, int NBINS>
-constexpr size_t tile_sort_smem() {
-  return 6 * (size_t)CAP + 8 * (size_t)(NBINS + 1) + 2 * (size_t)NBINS + 16;
-}
-
-// ---------------------------------------------------------------------------
-// global path for oversized buckets
-
-__global__ void k_big_gather(TileSortArgs a, const uint32_t* big_list, int n_big,
-                             const uint32_t* big_off, uint64_t* keys, uint32_t* vals) {
-  for (int b = blockIdx.x; b < n_big; b += gridDim.x) {
-    const int t = (int)big_list[b];
-    const int2 r = a.ranges[t];
-    const uint32_t o = big_off[b];
-    for (int i = threadIdx.x; i < r.y - r.x; i += blockDim.x) {
-      const uint32_t id = a.bucket[r.x + i];
-      keys[o + i] = ((uint64_t)b << 32) | a.key32[id];
-      vals[o + i] = id;
-    }
-  }
-}
-
-__global__ void k_big_fixup(void* const* keys_ptr, void* const* vals_ptr, int64_t n,
-                            const uint64_t* __restrict__ key64) {
+__global__ void k_depth_fixup(void* const* keys_slot, void* const* ids_slot, int64_t n,
+                              const uint64_t* __restrict__ key64) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const uint64_t* keys = static_cast<const uint64_t*>(*keys_ptr);
-  uint32_t* vals = static_cast<uint32_t*>(*vals_ptr);
-  const uint64_t k = keys[i];
+  const uint32_t* keys = static_cast<const uint32_t*>(*keys_slot);
+  const uint32_t k = keys[i];
+  if (k == 0xffffffffu) return;  // invisible tail
   if (i > 0 && keys[i - 1] == k) return;
   if (i + 1 >= n || keys[i + 1] != k) return;
   int64_t len = 2;
   while (i + len < n && keys[i + len] == k) ++len;
-  fix_run(vals + i, (int)len, key64);
+  fix_run(static_cast<uint32_t*>(*ids_slot) + i, (int)len, key64);
 }
 
-__global__ void k_big_scatter(TileSortArgs a, const uint32_t* big_list, int n_big,
-                              const uint32_t* big_off, void* const* vals_ptr) {
-  const uint32_t* vals = static_cast<const uint32_t*>(*vals_ptr);
-  for (int b = blockIdx.x; b < n_big; b += gridDim.x) {
-    const int t = (int)big_list[b];
-    const int2 r = a.ranges[t];
-    const uint32_t o = big_off[b];
-    for (int i = threadIdx.x; i < r.y - r.x; i += blockDim.x) a.sorted_ids[r.x + i] = vals[o + i];
+// ---------------------------------------------------------------------------
+// K4: rank-ordered emission with a single-pass scan (decoupled look-back)
+//
+// A CTA takes the next chunk of kEmitChunk ranks (ticket order).  Warp w owns
+// 256 consecutive ranks; it scans their tile counts in rank order, the CTA
+// learns the chunk's global offset by look-back, and then every warp writes
+// its instances with consecutive lanes on consecutive output slots (a binary
+// search over the warp's running counts maps a slot to its splat).
+
+constexpr uint64_t kLbAgg = 1ull << 62;
+constexpr uint64_t kLbIncl = 2ull << 62;
+constexpr uint64_t kLbMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ uint64_t ld_relaxed64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kEmitThreads) k_emit(EmitArgs a) {
+  constexpr int NW = kEmitThreads / 32;
+  constexpr int PW = 32 * kEmitItems;  // ranks per warp
+  __shared__ uint32_t s_end[NW][PW];   // running (inclusive) tile count within the warp
+  __shared__ uint32_t s_id[NW][PW];
+  __shared__ uint64_t s_rect[NW][PW];
+  __shared__ uint32_t s_hist[kMaxTilePasses][256];
+  __shared__ uint32_t s_wtot[NW];
+  __shared__ uint32_t s_ticket;
+  __shared__ unsigned long long s_excl;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_ticket = atomicAdd(a.ticket, 1u);
+  for (int i = tid; i < kMaxTilePasses * 256; i += kEmitThreads) (&s_hist[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t chunk = s_ticket;
+  const int64_t base = chunk * kEmitChunk + (int64_t)warp * PW;
+  const uint32_t* __restrict__ order = static_cast<const uint32_t*>(*a.order_slot);
+
+  uint32_t id[kEmitItems];
+#pragma unroll
+  for (int j = 0; j < kEmitItems; ++j) {
+    const int64_t r = base + j * 32 + lane;
+    id[j] = r < a.n_vis ? order[r] : 0xffffffffu;
+  }
+  uint32_t cnt[kEmitItems];
+  uint64_t rect[kEmitItems];
+#pragma unroll
+  for (int j = 0; j < kEmitItems; ++j) rect[j] = id[j] != 0xffffffffu ? __ldg(a.rects + id[j]) : 0ull;
+#pragma unroll
+  for (int j = 0; j < kEmitItems; ++j) {
+    int x0, y0, x1, y1;
+    unpack_rect(rect[j], x0, y0, x1, y1);
+    cnt[j] = id[j] != 0xffffffffu ? (uint32_t)(x1 - x0 + 1) * (uint32_t)(y1 - y0 + 1) : 0u;
+  }
+  uint32_t run = 0;
+#pragma unroll
+  for (int j = 0; j < kEmitItems; ++j) {
+    uint32_t incl = cnt[j];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    incl += run;
+    s_end[warp][j * 32 + lane] = incl;
+    s_id[warp][j * 32 + lane] = id[j];
+    s_rect[warp][j * 32 + lane] = rect[j];
+    run = __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (lane == 0) s_wtot[warp] = run;
+  __syncthreads();
+  uint64_t wofs = 0, total = 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const uint32_t v = s_wtot[w];
+    wofs += w < warp ? v : 0;
+    total += v;
+  }
+  if (warp == 0) {
+    // warp-cooperative look-back: 32 predecessors per L2 round trip
+    uint64_t* lb = a.lookback;
+    if (chunk == 0) {
+      if (lane == 0) {
+        st_relaxed64(lb, kLbIncl | total);
+        s_excl = 0;
+      }
+    } else {
+      if (lane == 0) st_relaxed64(lb + chunk, kLbAgg | total);
+      uint64_t excl = 0;
+      int64_t end = chunk;  // predecessors [end - 32, end) in this window
+      while (true) {
+        const int64_t idx = end - 1 - lane;
+        uint64_t v = kLbIncl;  // before chunk 0: inclusive zero (never reached)
+        if (idx >= 0) {
+          do {
+            v = ld_relaxed64(lb + idx);
+          } while ((v & ~kLbMask) == 0);
+        }
+        const uint32_t incl = __ballot_sync(0xffffffffu, (v & ~kLbMask) == kLbIncl);
+        const int stop = incl ? __ffs(incl) - 1 : 31;  // nearest inclusive predecessor
+        unsigned long long part = lane <= stop ? (v & kLbMask) : 0ull;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        excl += part;
+        if (incl) break;
+        end -= 32;
+      }
+      if (lane == 0) {
+        st_relaxed64(lb + chunk, kLbIncl | (excl + total));
+        s_excl = excl;
+      }
+    }
+  }
+  __syncthreads();
+  const uint64_t out0 = s_excl + wofs;
+  const uint32_t wtot = s_wtot[warp];
+  const uint32_t* ends = s_end[warp];
+  const int passes = a.n_tile_passes;
+  for (uint32_t p0 = 0; p0 < wtot; p0 += 32) {  // warp-uniform trip count
+    const uint32_t p = p0 + lane;
+    const bool on = p < wtot;
+    int lo = 0, hi = PW - 1;  // first item whose running count exceeds p
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {  // PW = 256: exactly 8 halvings
+      const int mid = (lo + hi) >> 1;
+      if (ends[mid] > p) hi = mid;
+      else lo = mid + 1;
+    }
+    uint32_t tile = 0;
+    if (on) {
+      const uint32_t q = p - (lo ? ends[lo - 1] : 0u);
+      int x0, y0, x1, y1;
+      unpack_rect(s_rect[warp][lo], x0, y0, x1, y1);
+      const uint32_t w = (uint32_t)(x1 - x0 + 1);
+      const uint32_t dy = q / w;
+      tile = (uint32_t)(y0 + (int)dy) * (uint32_t)a.tiles_x + (uint32_t)x0 + (q - dy * w);
+      a.keys[out0 + p] = ((uint64_t)tile << 32) | s_id[warp][lo];
+      // the low digit differs across lanes (consecutive tiles of a row)
+      atomicAdd(&s_hist[0][tile & 0xffu], 1u);
+    }
+    // higher digits are almost always warp-uniform: one aggregated add
+    const uint32_t act = __ballot_sync(0xffffffffu, on);
+    const int first = __ffs(act) - 1;
+    for (int ps = 1; ps < passes; ++ps) {
+      const uint32_t dg = (tile >> (8 * ps)) & 0xffu;
+      const uint32_t d0 = __shfl_sync(0xffffffffu, dg, first);
+      if (__all_sync(0xffffffffu, !on || dg == d0)) {
+        if (lane == first) atomicAdd(&s_hist[ps][d0], (uint32_t)__popc(act));
+      } else if (on) {
+        atomicAdd(&s_hist[ps][dg], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < passes * 256; i += kEmitThreads) {
+    const uint32_t v = (&s_hist[0][0])[i];
+    if (v) atomicAdd(a.hist + i, v);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K6: ranges from tile boundaries of the sorted keys.  Position i sits between
+// tiles a = tile(i-1) and b = tile(i): tile a ends at i, b starts at i, and
+// every tile strictly between them is empty at i.
+
+__global__ void k_tile_ranges(void* const* keys_slot, int64_t k, int tiles, int2* ranges) {
+  const uint64_t* __restrict__ keys = static_cast<const uint64_t*>(*keys_slot);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= k; i += stride) {
+    const int ta = i > 0 ? (int)(keys[i - 1] >> 32) : -1;
+    const int tb = i < k ? (int)(keys[i] >> 32) : tiles;
+    if (ta == tb) continue;
+    const int pos = (int)i;
+    if (ta >= 0) ranges[ta].y = pos;
+    for (int t = ta + 1; t < tb; ++t) ranges[t] = make_int2(pos, pos);
+    if (tb < tiles) ranges[tb].x = pos;
   }
 }
 
 // instance export: keys = tile << 32 | row, prims = original id
 __global__ void k_export(InstanceExportArgs a) {
-  const int t = blockIdx.x;
-  const int2 r = a.ranges[t];
-  for (int i = r.x + threadIdx.x; i < r.y; i += blockDim.x) {
-    const uint32_t id = a.sorted_ids[i];
-    if (a.keys_out) a.keys_out[i] = ((uint64_t)(uint32_t)t << 32) | id;
+  const uint64_t* __restrict__ keys = static_cast<const uint64_t*>(*a.keys_slot);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.k; i += stride) {
+    const uint64_t key = keys[i];
+    const uint32_t id = (uint32_t)key;
+    if (a.keys_out) a.keys_out[i] = key;
     if (a.prims_out) a.prims_out[i] = a.prim_ids ? a.prim_ids[id] : (int64_t)id;
   }
 }
 
-template <typename Kern>
-void set_smem(Kern k, size_t bytes) {
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+inline unsigned grid_for(int64_t n, int threads, int64_t cap = 148 * 16) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g > cap) g = cap;
+  return (unsigned)(g > 0 ? g : 1);
 }
 
 }  // namespace
 
-size_t bin_smem_bytes(int tiles) { return sizeof(uint32_t) * (size_t)min(tiles, kSlabTiles); }
-
-void launch_bin_hist(const BinArgs& a, cudaStream_t s) {
-  const size_t smem = bin_smem_bytes(a.tiles);
-  static size_t set = 0;
-  if (smem > set) {
-    set_smem(k_bin_hist, bin_smem_bytes(kSlabTiles));
-    set_smem(k_bin_place, bin_smem_bytes(kSlabTiles));
-    set = bin_smem_bytes(kSlabTiles);
-  }
-  k_bin_hist<<<a.ctas, kBinThreads, smem, s>>>(a);
-  k_bin_colscan<<<(a.tiles + 127) / 128, 128, 0, s>>>(a);
+int launch_depth_keys(const uint64_t* key64, const unsigned long long* zrange, int64_t n,
+                      uint32_t* key32, uint32_t* hist, cudaStream_t s) {
+  if (n <= 0) return 0;
+  k_depth_keys<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(key64, zrange, n, key32, hist);
+  return 1;
 }
 
-void launch_scan_tiles(const TileScanArgs& a, cudaStream_t s) {
-  k_scan_tiles<<<1, kScanTilesThreads, 0, s>>>(a);
+int launch_depth_fixup(void* const* keys_slot, void* const* ids_slot, int64_t n,
+                       const uint64_t* key64, cudaStream_t s) {
+  if (n <= 1) return 0;
+  k_depth_fixup<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(keys_slot, ids_slot, n, key64);
+  return 1;
 }
 
-void launch_bin_place(const BinArgs& a, cudaStream_t s) {
-  k_bin_place<<<a.ctas, kBinThreads, bin_smem_bytes(a.tiles), s>>>(a);
+int launch_emit(const EmitArgs& a, cudaStream_t s) {
+  const int64_t chunks = emit_chunks(a.n_vis);
+  if (chunks <= 0) return 0;
+  k_emit<<<(unsigned)chunks, kEmitThreads, 0, s>>>(a);
+  return 1;
 }
 
-void launch_tile_sort(const TileSortArgs& a, const uint32_t* tile_list,
-                      const uint32_t* list_count, int n_list, int cls, cudaStream_t s) {
-  if (n_list <= 0) return;
-  constexpr int kST = 256, kMT = 1024, kSB = 1024, kMB = 4096;
-  static bool attr = false;
-  if (!attr) {
-    set_smem(k_tile_sort<kST, kSmallTileCap, kSB>, tile_sort_smem<kST, kSmallTileCap, kSB>());
-    set_smem(k_tile_sort<kMT, kMediumTileCap, kMB>, tile_sort_smem<kMT, kMediumTileCap, kMB>());
-    attr = true;
-  }
-  if (cls == 0)
-    k_tile_sort<kST, kSmallTileCap, kSB>
-        <<<n_list, kST, tile_sort_smem<kST, kSmallTileCap, kSB>(), s>>>(a, tile_list, list_count);
-  else
-    k_tile_sort<kMT, kMediumTileCap, kMB>
-        <<<n_list, kMT, tile_sort_smem<kMT, kMediumTileCap, kMB>(), s>>>(a, tile_list, list_count);
+int launch_tile_ranges(void* const* keys_slot, int64_t k, int tiles, int2* ranges,
+                       cudaStream_t s) {
+  if (tiles <= 0) return 0;
+  k_tile_ranges<<<grid_for(k + 1, 256), 256, 0, s>>>(keys_slot, k, tiles, ranges);
+  return 1;
 }
 
-void launch_big_gather(const TileSortArgs& a, const uint32_t* big_list, int n_big,
-                       const uint32_t* big_off, uint64_t* keys, uint32_t* vals, cudaStream_t s) {
-  if (n_big <= 0) return;
-  k_big_gather<<<n_big, 256, 0, s>>>(a, big_list, n_big, big_off, keys, vals);
-}
-
-void launch_big_fixup(void* const* keys_ptr, void* const* vals_ptr, int64_t n,
-                      const uint64_t* key64, cudaStream_t s) {
-  if (n <= 0) return;
-  k_big_fixup<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(keys_ptr, vals_ptr, n, key64);
-}
-
-void launch_big_scatter(const TileSortArgs& a, const uint32_t* big_list, int n_big,
-                        const uint32_t* big_off, void* const* vals_ptr, cudaStream_t s) {
-  if (n_big <= 0) return;
-  k_big_scatter<<<n_big, 256, 0, s>>>(a, big_list, n_big, big_off, vals_ptr);
-}
-
-void launch_export_instances(const InstanceExportArgs& a, int tiles, cudaStream_t s) {
-  if (tiles <= 0) return;
-  k_export<<<tiles, 256, 0, s>>>(a);
+void launch_export_instances(const InstanceExportArgs& a, cudaStream_t s) {
+  if (a.k <= 0) return;
+  k_export<<<grid_for(a.k, 256), 256, 0, s>>>(a);
 }
 
 }  // namespace lmgs
