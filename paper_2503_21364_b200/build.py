@@ -29,6 +29,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
           f"-I{INCLUDE}", "--expt-relaxed-constexpr"]
 PER_FILE = {"preprocess.cu": ["-fmad=false"]}
+# extra nvcc flags for tuning experiments (e.g. "-DLMGS_PRE_MIN_CTAS=6")
+EXTRA = os.environ.get("LMGS_NVCC_FLAGS", "").split()
 
 
 def nvcc() -> str:
@@ -56,7 +58,7 @@ def _stale(target: Path, inputs) -> bool:
 def _compile(src: Path, force: bool, log: list) -> Path:
     obj = BUILD / (src.stem + ".o")
     if force or _stale(obj, [src, *_deps(), Path(__file__)]):
-        cmd = [nvcc(), *ARCH, *COMMON, *PER_FILE.get(src.name, []), "-c", str(src), "-o",
+        cmd = [nvcc(), *ARCH, *COMMON, *PER_FILE.get(src.name, []), *EXTRA, "-c", str(src), "-o",
                str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log.append((src.name, r.stderr))

@@ -12,6 +12,7 @@
 // products (covariance, jw @ cov3d @ jw^T) as plain sequential sums.  The
 // only deviation: sqrt here is IEEE-rounded while torch.sqrt (MKL VML) is
 // <= 1 ulp low on ~0.7% of inputs.
+#include "device_util.cuh"
 #include "lmgs_internal.cuh"
 
 namespace lmgs {
@@ -109,36 +110,18 @@ __device__ __forceinline__ void sh_color(const float* __restrict__ sh, int ncoef
 }
 
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n.reg .pred p;\nWAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-
 // One Gaussian.  Inputs arrive as values (from shared memory staged by TMA or
 // straight from global memory); `sh` points at its coefficients.
-constexpr int kPreThreads = 256;  // both kernels (count_kept reduces over 8 warps)
+#ifndef LMGS_PRE_THREADS
+#define LMGS_PRE_THREADS 128
+#endif
+#ifndef LMGS_PRE_MIN_CTAS
+#define LMGS_PRE_MIN_CTAS 7
+#endif
+// Gaussians (threads) per CTA in both kernels; count_kept reduces over its warps.
+// 128 x 7 CTAs per SM: 28 warps to hide the fp64 dependency chains, 7 x 30 KB
+// of TMA-staged inputs in flight per SM.
+constexpr int kPreThreads = LMGS_PRE_THREADS;
 
 // Returns the splat's tile count (0: culled or off-screen); *keep = near-kept.
 template <bool SMEM>
@@ -314,7 +297,7 @@ __device__ __forceinline__ void count_kept(const PreprocessArgs& a, bool keep, u
 }
 
 // direct loads (tail block, unaligned inputs)
-__global__ void __launch_bounds__(256) k_preprocess_direct(PreprocessArgs a, int64_t first) {
+__global__ void __launch_bounds__(kPreThreads) k_preprocess_direct(PreprocessArgs a, int64_t first) {
   const int64_t i = first + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool keep = false;
   uint32_t cnt = 0;
@@ -333,7 +316,7 @@ __global__ void __launch_bounds__(256) k_preprocess_direct(PreprocessArgs a, int
 // (a second mbarrier); the SH bytes stream into shared memory while the fp64
 // geometry of the block is being computed.
 
-__global__ void __launch_bounds__(kPreThreads, 2) k_preprocess_tma(PreprocessArgs a) {
+__global__ void __launch_bounds__(kPreThreads, LMGS_PRE_MIN_CTAS) k_preprocess_tma(PreprocessArgs a) {
   extern __shared__ __align__(128) float smem_f[];
   float* s_means = smem_f;                       // [256*3]
   float* s_quats = s_means + kPreThreads * 3;    // [256*4]
@@ -346,7 +329,7 @@ __global__ void __launch_bounds__(kPreThreads, 2) k_preprocess_tma(PreprocessArg
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_init_fence();
   }
   __syncthreads();
   const uint32_t sh_bytes = (uint32_t)(kPreThreads * a.sh_coeffs * 3 * 4);
@@ -400,7 +383,8 @@ int launch_preprocess(const PreprocessArgs& a, cudaStream_t s) {
   const int64_t first = full * kPreThreads;
   const int64_t rest = a.n - first;
   if (rest > 0) {
-    k_preprocess_direct<<<(unsigned)((rest + 255) / 256), 256, 0, s>>>(a, first);
+    k_preprocess_direct<<<(unsigned)((rest + kPreThreads - 1) / kPreThreads), kPreThreads, 0, s>>>(
+        a, first);
     ++launched;
   }
   return launched;

@@ -19,6 +19,7 @@
 //        2 passes of 8 bits at 1080p) — every tile's list is then exactly the
 //        reference's per-tile (depth, id) order, with no per-tile sort;
 //   K6   tile ranges [start, end) from the boundaries of the sorted keys.
+#include "device_util.cuh"
 #include "lmgs_internal.cuh"
 
 namespace lmgs {
@@ -113,21 +114,12 @@ __global__ void k_depth_fixup(void* const* keys_slot, void* const* ids_slot, int
 // A CTA takes the next chunk of kEmitChunk ranks (ticket order).  Warp w owns
 // 256 consecutive ranks; it scans their tile counts in rank order, the CTA
 // learns the chunk's global offset by look-back, and then every warp writes
-// its instances with consecutive lanes on consecutive output slots (a binary
-// search over the warp's running counts maps a slot to its splat).
+// its instances with consecutive lanes on consecutive output slots (a 32-slot
+// window maps slots to splats with one OR-reduction and a few shuffles).
 
 constexpr uint64_t kLbAgg = 1ull << 62;
 constexpr uint64_t kLbIncl = 2ull << 62;
 constexpr uint64_t kLbMask = (1ull << 62) - 1;
-
-__device__ __forceinline__ uint64_t ld_relaxed64(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed64(uint64_t* p, uint64_t v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 
 __global__ void __launch_bounds__(kEmitThreads) k_emit(EmitArgs a) {
   constexpr int NW = kEmitThreads / 32;
@@ -148,36 +140,41 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(EmitArgs a) {
   const int64_t base = chunk * kEmitChunk + (int64_t)warp * PW;
   const uint32_t* __restrict__ order = static_cast<const uint32_t*>(*a.order_slot);
 
+  // blocked layout: lane l owns ranks base + l*kEmitItems + j (item index
+  // l*kEmitItems + j within the warp), so the warp's scan is one shuffle scan
+  // of per-lane sums
   uint32_t id[kEmitItems];
 #pragma unroll
   for (int j = 0; j < kEmitItems; ++j) {
-    const int64_t r = base + j * 32 + lane;
+    const int64_t r = base + lane * kEmitItems + j;
     id[j] = r < a.n_vis ? order[r] : 0xffffffffu;
   }
-  uint32_t cnt[kEmitItems];
   uint64_t rect[kEmitItems];
 #pragma unroll
   for (int j = 0; j < kEmitItems; ++j) rect[j] = id[j] != 0xffffffffu ? __ldg(a.rects + id[j]) : 0ull;
+  uint32_t incl_local[kEmitItems];
+  uint32_t sum = 0;
 #pragma unroll
   for (int j = 0; j < kEmitItems; ++j) {
     int x0, y0, x1, y1;
     unpack_rect(rect[j], x0, y0, x1, y1);
-    cnt[j] = id[j] != 0xffffffffu ? (uint32_t)(x1 - x0 + 1) * (uint32_t)(y1 - y0 + 1) : 0u;
+    sum += id[j] != 0xffffffffu ? (uint32_t)(x1 - x0 + 1) * (uint32_t)(y1 - y0 + 1) : 0u;
+    incl_local[j] = sum;
   }
-  uint32_t run = 0;
+  uint32_t scan = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, scan, o);
+    if (lane >= o) scan += v;
+  }
+  const uint32_t lane_excl = scan - sum;
+  const uint32_t run = __shfl_sync(0xffffffffu, scan, 31);
 #pragma unroll
   for (int j = 0; j < kEmitItems; ++j) {
-    uint32_t incl = cnt[j];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    incl += run;
-    s_end[warp][j * 32 + lane] = incl;
-    s_id[warp][j * 32 + lane] = id[j];
-    s_rect[warp][j * 32 + lane] = rect[j];
-    run = __shfl_sync(0xffffffffu, incl, 31);
+    const int k = lane * kEmitItems + j;
+    s_end[warp][k] = lane_excl + incl_local[j];
+    s_id[warp][k] = id[j];
+    s_rect[warp][k] = rect[j];
   }
   if (lane == 0) s_wtot[warp] = run;
   __syncthreads();
@@ -193,11 +190,11 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(EmitArgs a) {
     uint64_t* lb = a.lookback;
     if (chunk == 0) {
       if (lane == 0) {
-        st_relaxed64(lb, kLbIncl | total);
+        st_relaxed_gpu(lb, kLbIncl | total);
         s_excl = 0;
       }
     } else {
-      if (lane == 0) st_relaxed64(lb + chunk, kLbAgg | total);
+      if (lane == 0) st_relaxed_gpu(lb + chunk, kLbAgg | total);
       uint64_t excl = 0;
       int64_t end = chunk;  // predecessors [end - 32, end) in this window
       while (true) {
@@ -205,7 +202,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(EmitArgs a) {
         uint64_t v = kLbIncl;  // before chunk 0: inclusive zero (never reached)
         if (idx >= 0) {
           do {
-            v = ld_relaxed64(lb + idx);
+            v = ld_relaxed_gpu(lb + idx);
           } while ((v & ~kLbMask) == 0);
         }
         const uint32_t incl = __ballot_sync(0xffffffffu, (v & ~kLbMask) == kLbIncl);
@@ -218,7 +215,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(EmitArgs a) {
         end -= 32;
       }
       if (lane == 0) {
-        st_relaxed64(lb + chunk, kLbIncl | (excl + total));
+        st_relaxed_gpu(lb + chunk, kLbIncl | (excl + total));
         s_excl = excl;
       }
     }
@@ -226,27 +223,37 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(EmitArgs a) {
   __syncthreads();
   const uint64_t out0 = s_excl + wofs;
   const uint32_t wtot = s_wtot[warp];
-  const uint32_t* ends = s_end[warp];
+  const uint32_t* ends = s_end[warp];  // item k covers slots [ends[k-1], ends[k])
   const int passes = a.n_tile_passes;
+  // Slots are written 32 at a time, lane l -> slot p0 + l.  k0 is the item
+  // holding slot p0; lane j looks at item k0 + j, items starting inside the
+  // window mark their offset in a 32-bit mask, and slot l's item is k0 plus
+  // the number of marks at offsets <= l.
+  __syncwarp();
+  int k0 = 0;
   for (uint32_t p0 = 0; p0 < wtot; p0 += 32) {  // warp-uniform trip count
+    const int kj = k0 + lane;
+    const bool have = kj < PW;
+    const uint32_t st = have ? (kj ? ends[kj - 1] : 0u) : 0xffffffffu;
+    const bool mark = lane > 0 && st < p0 + 32u;
+    const uint32_t smask = __reduce_or_sync(0xffffffffu, mark ? 1u << (st - p0) : 0u);
+    const int idx = __popc(smask & (0xffffffffu >> (31 - lane)));
+    const uint64_t my_rect = have ? s_rect[warp][kj] : 0ull;
+    const uint32_t my_id = have ? s_id[warp][kj] : 0u;
+    const uint32_t st_i = __shfl_sync(0xffffffffu, st, idx);
+    const uint32_t r_lo = __shfl_sync(0xffffffffu, (uint32_t)my_rect, idx);
+    const uint32_t r_hi = __shfl_sync(0xffffffffu, (uint32_t)(my_rect >> 32), idx);
+    const uint32_t id_i = __shfl_sync(0xffffffffu, my_id, idx);
     const uint32_t p = p0 + lane;
     const bool on = p < wtot;
-    int lo = 0, hi = PW - 1;  // first item whose running count exceeds p
-#pragma unroll
-    for (int it = 0; it < 8; ++it) {  // PW = 256: exactly 8 halvings
-      const int mid = (lo + hi) >> 1;
-      if (ends[mid] > p) hi = mid;
-      else lo = mid + 1;
-    }
     uint32_t tile = 0;
     if (on) {
-      const uint32_t q = p - (lo ? ends[lo - 1] : 0u);
-      int x0, y0, x1, y1;
-      unpack_rect(s_rect[warp][lo], x0, y0, x1, y1);
+      const uint32_t q = p - st_i;
+      const int x0 = (int)(r_lo & 0xffff), y0 = (int)(r_lo >> 16), x1 = (int)(r_hi & 0xffff);
       const uint32_t w = (uint32_t)(x1 - x0 + 1);
       const uint32_t dy = q / w;
       tile = (uint32_t)(y0 + (int)dy) * (uint32_t)a.tiles_x + (uint32_t)x0 + (q - dy * w);
-      a.keys[out0 + p] = ((uint64_t)tile << 32) | s_id[warp][lo];
+      a.keys[out0 + p] = ((uint64_t)tile << 32) | id_i;
       // the low digit differs across lanes (consecutive tiles of a row)
       atomicAdd(&s_hist[0][tile & 0xffu], 1u);
     }
@@ -262,6 +269,9 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(EmitArgs a) {
         atomicAdd(&s_hist[ps][dg], 1u);
       }
     }
+    // next window starts in the item holding slot p0 + 32
+    const int idx31 = __shfl_sync(0xffffffffu, idx, 31);
+    k0 += idx31 + (ends[k0 + idx31] == p0 + 32u ? 1 : 0);
   }
   __syncthreads();
   for (int i = tid; i < passes * 256; i += kEmitThreads) {
