@@ -76,6 +76,9 @@ size_t gaussian_bytes(int64_t n) {
   b += align_up(sizeof(uint64_t) * emit_chunks(n));            // K4 look-back
   return b + 10 * kAlign;
 }
+size_t tile_bytes(int64_t t) {
+  return align_up(sizeof(int2) * t) + align_up(sizeof(uint32_t) * t) + 2 * kAlign;
+}
 size_t instance_bytes(int64_t k) {
   return 2 * align_up(sizeof(uint64_t) * k) + align_up(sizeof(uint32_t) * radix_lookback_words(k)) +
          4 * kAlign;
@@ -117,6 +120,7 @@ struct lmgs_context {
   uint64_t* emit_lookback = nullptr;
   // per-tile arena
   int2* ranges = nullptr;
+  uint32_t* tile_count = nullptr;
   // per-instance arena
   uint64_t* inst_keys[2] = {nullptr, nullptr};
   uint32_t* tile_lookback = nullptr;
@@ -175,8 +179,10 @@ int ensure_gaussians(lmgs_context* c, int64_t n, cudaStream_t s) {
 int ensure_tiles(lmgs_context* c, int64_t t, cudaStream_t s) {
   if (t <= c->cap_t && c->ranges) return LMGS_OK;
   LMGS_CUDA(c, cudaStreamSynchronize(s));
-  LMGS_CUDA(c, c->tbuf.reserve(align_up(sizeof(int2) * t) + kAlign));
-  c->ranges = static_cast<int2*>(c->tbuf.ptr);
+  LMGS_CUDA(c, c->tbuf.reserve(tile_bytes(t)));
+  Carver cv{static_cast<char*>(c->tbuf.ptr)};
+  c->ranges = cv.take<int2>(t);
+  c->tile_count = cv.take<uint32_t>(t);
   c->cap_t = t;
   return LMGS_OK;
 }
@@ -389,8 +395,11 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
     rb.counters = sc->tile_counters;
     rb.keys_result = &sc->slots.inst_keys;
     rb.hist_ready = true;
+    rb.seg_counts = c->tile_count;
+    rb.seg_shift = 32;
+    LMGS_CUDA(c, cudaMemsetAsync(c->tile_count, 0, sizeof(uint32_t) * tiles, s));
     launched += radix_sort(rb, k, 32, tile_passes, s);
-    launched += launch_tile_ranges(&sc->slots.inst_keys, k, (int)tiles, ranges, s);
+    launched += launch_ranges_from_counts(c->tile_count, (int)tiles, ranges, s);
   }
   tm.end(3);
 

@@ -96,10 +96,11 @@ constexpr int kSortTile = kSortThreads * kSortItems;
 struct RadixPlan {
   int32_t n_passes;
   int32_t first_active;  // first non-trivial pass (-1: none)
+  int32_t last_active;   // last non-trivial pass (-1: none)
   int32_t active[kMaxPasses];
   int32_t src[kMaxPasses];
   int32_t result;
-  int32_t pad[6];
+  int32_t pad[5];
   uint32_t digit_start[kMaxPasses][kRadix];
 };
 
@@ -116,6 +117,11 @@ struct RadixSortBuffers {
   void** vals_result;  // nullable: device slot receiving the result value buffer
   bool hist_ready;     // hist already holds every digit histogram (the producer built it)
   bool iota_vals;      // vals[0] is implicit: value = input index (never read)
+  // nullable: the last data-moving pass adds the length of every run of equal
+  // (key >> seg_shift) to seg_counts[key >> seg_shift] (zeroed by the caller);
+  // the sorted key bits must cover the segment bits (tile sort: ranges)
+  uint32_t* seg_counts;
+  int seg_shift;
 };
 
 size_t radix_lookback_words(int64_t capacity);
@@ -169,9 +175,9 @@ struct EmitArgs {
 inline int64_t emit_chunks(int64_t n_vis) { return (n_vis + kEmitChunk - 1) / kEmitChunk; }
 int launch_emit(const EmitArgs& a, cudaStream_t s);
 
-// K6: tile ranges from the sorted keys ([start, end), empty tiles included)
-int launch_tile_ranges(void* const* keys_slot, int64_t k, int tiles, int2* ranges,
-                        cudaStream_t s);
+// K6: tile ranges [start, end) = exclusive scan of the per-tile counts the
+// tile sort's last pass accumulated (empty tiles included)
+int launch_ranges_from_counts(const uint32_t* counts, int tiles, int2* ranges, cudaStream_t s);
 
 struct InstanceExportArgs {
   const int2* ranges;

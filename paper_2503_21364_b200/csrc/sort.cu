@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kRadix) k_radix_plan(const uint32_t* __restric
     }
   }
   if (d == 0) {
-    int cur = 0, first = -1;
+    int cur = 0, first = -1, last = -1;
     for (int p = 0; p < kMaxPasses; ++p) {
       const int act = !off && p < n_passes && !s_trivial[p] && n > 1;
       plan->active[p] = act;
@@ -114,9 +114,11 @@ __global__ void __launch_bounds__(kRadix) k_radix_plan(const uint32_t* __restric
       if (act) {
         cur ^= 1;
         if (first < 0) first = p;
+        last = p;
       }
     }
     plan->first_active = first;
+    plan->last_active = last;
     plan->result = cur;
     plan->n_passes = n_passes;
     if (!off) {
@@ -141,7 +143,7 @@ template <typename K, bool VALS>
 __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
     K* keys0, K* keys1, uint32_t* vals0, uint32_t* vals1, int64_t n, int begin_bit, int pass,
     const RadixPlan* __restrict__ plan, uint32_t* lookback, uint32_t* counter, int64_t lb_stride,
-    bool iota_vals) {
+    bool iota_vals, uint32_t* seg_counts, int seg_shift) {
   if (!plan->active[pass]) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K* s_keys = reinterpret_cast<K*>(smem_raw);  // [kSortTile] staging
@@ -296,11 +298,21 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
   }
   __syncthreads();
   // 6. coalesced write-out: consecutive threads, consecutive staged positions
+  const bool segs = seg_counts && pass == plan->last_active;
   for (int i = tid; i < count; i += kSortThreads) {
     const K k = s_keys[i];
     const uint32_t o = s_global[digit_of(k, shift)] + i;
     kout[o] = k;
     if (VALS) vout[o] = s_vals[i];
+    if (segs) {
+      // the staged tile is sorted on every key bit sorted so far: runs of one
+      // segment are contiguous; a run [i0, i1] adds (i1 + 1) - i0
+      const uint64_t sg = (uint64_t)k >> seg_shift;
+      if (i == 0 || ((uint64_t)s_keys[i - 1] >> seg_shift) != sg)
+        atomicAdd(seg_counts + sg, (uint32_t)(-i));
+      if (i + 1 == count || ((uint64_t)s_keys[i + 1] >> seg_shift) != sg)
+        atomicAdd(seg_counts + sg, (uint32_t)(i + 1));
+    }
   }
 }
 
@@ -311,6 +323,15 @@ __global__ void k_iota_if_idle(const RadixPlan* __restrict__ plan, uint32_t* val
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     vals[i] = (uint32_t)i;
+}
+
+// segment counts with no data-moving pass: every key is equal on the sorted
+// bits, so there is a single segment holding all n keys
+template <typename K>
+__global__ void k_segments_if_idle(const RadixPlan* __restrict__ plan, const K* keys, int64_t n,
+                                   uint32_t* seg_counts, int seg_shift) {
+  if (plan->last_active >= 0 || n <= 0) return;
+  seg_counts[(uint64_t)keys[0] >> seg_shift] = (uint32_t)n;
 }
 
 template <typename K, bool VALS>
@@ -330,7 +351,7 @@ void launch_onesweep(const RadixSortBuffers& b, int64_t n, int begin_bit, int p,
   }
   k_onesweep<K, VALS><<<(unsigned)blocks, kSortThreads, smem, s>>>(
       static_cast<K*>(b.keys[0]), static_cast<K*>(b.keys[1]), b.vals[0], b.vals[1], n, begin_bit,
-      p, b.plan, b.lookback, b.counters, blocks, b.iota_vals);
+      p, b.plan, b.lookback, b.counters, blocks, b.iota_vals, b.seg_counts, b.seg_shift);
 }
 
 template <typename K>
@@ -358,6 +379,10 @@ int radix_sort_impl(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_p
   if (b.iota_vals && n > 0) {
     const int64_t g = (n + 255) / 256;
     k_iota_if_idle<<<(unsigned)(g < 148 * 8 ? g : 148 * 8), 256, 0, s>>>(b.plan, b.vals[0], n);
+    ++launched;
+  }
+  if (b.seg_counts && n > 0) {
+    k_segments_if_idle<K><<<1, 1, 0, s>>>(b.plan, k0, n, b.seg_counts, b.seg_shift);
     ++launched;
   }
   if (blocks == 0) return launched;

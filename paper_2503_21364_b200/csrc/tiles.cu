@@ -18,7 +18,8 @@
 //   K5   a stable LSD radix sort of those keys on the tile bits only (sort.cu,
 //        2 passes of 8 bits at 1080p) — every tile's list is then exactly the
 //        reference's per-tile (depth, id) order, with no per-tile sort;
-//   K6   tile ranges [start, end) from the boundaries of the sorted keys.
+//   K6   tile ranges [start, end): the last K5 pass adds each CTA's per-tile
+//        run lengths to a tile-count array, and one CTA scans it.
 #include "device_util.cuh"
 #include "lmgs_internal.cuh"
 
@@ -281,21 +282,44 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(EmitArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// K6: ranges from tile boundaries of the sorted keys.  Position i sits between
-// tiles a = tile(i-1) and b = tile(i): tile a ends at i, b starts at i, and
-// every tile strictly between them is empty at i.
+// K6: tile ranges = exclusive scan of the per-tile counts (one CTA)
 
-__global__ void k_tile_ranges(void* const* keys_slot, int64_t k, int tiles, int2* ranges) {
-  const uint64_t* __restrict__ keys = static_cast<const uint64_t*>(*keys_slot);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= k; i += stride) {
-    const int ta = i > 0 ? (int)(keys[i - 1] >> 32) : -1;
-    const int tb = i < k ? (int)(keys[i] >> 32) : tiles;
-    if (ta == tb) continue;
-    const int pos = (int)i;
-    if (ta >= 0) ranges[ta].y = pos;
-    for (int t = ta + 1; t < tb; ++t) ranges[t] = make_int2(pos, pos);
-    if (tb < tiles) ranges[tb].x = pos;
+constexpr int kScanThreads = 1024;
+
+__global__ void __launch_bounds__(kScanThreads) k_ranges_from_counts(const uint32_t* counts,
+                                                                     int tiles, int2* ranges) {
+  __shared__ uint32_t s_warp[kScanThreads / 32];
+  __shared__ uint32_t s_carry;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_carry = 0;
+  __syncthreads();
+  for (int base = 0; base < tiles; base += kScanThreads) {
+    const int t = base + tid;
+    const uint32_t c = t < tiles ? counts[t] : 0u;
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t w = s_warp[lane];
+      uint32_t wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += v;
+      }
+      s_warp[lane] = wi - w;
+    }
+    __syncthreads();
+    const uint32_t excl = s_carry + s_warp[warp] + (incl - c);
+    if (t < tiles) ranges[t] = make_int2((int)excl, (int)(excl + c));
+    __syncthreads();
+    if (tid == kScanThreads - 1) s_carry = excl + c;
+    __syncthreads();
   }
 }
 
@@ -340,10 +364,9 @@ int launch_emit(const EmitArgs& a, cudaStream_t s) {
   return 1;
 }
 
-int launch_tile_ranges(void* const* keys_slot, int64_t k, int tiles, int2* ranges,
-                       cudaStream_t s) {
+int launch_ranges_from_counts(const uint32_t* counts, int tiles, int2* ranges, cudaStream_t s) {
   if (tiles <= 0) return 0;
-  k_tile_ranges<<<grid_for(k + 1, 256), 256, 0, s>>>(keys_slot, k, tiles, ranges);
+  k_ranges_from_counts<<<1, kScanThreads, 0, s>>>(counts, tiles, ranges);
   return 1;
 }
 
