@@ -251,6 +251,12 @@ __global__ void __launch_bounds__(256) k_blend(BlendArgs a) {
 
 constexpr int kWarpsPerBlock16 = 8;
 
+// NP pixels per lane: the warp owns an 8 x (4*NP) block of its 16x16 tile
+// (16 / (4*NP) * 2 items per tile); lane l holds pixels (l & 7, (l >> 3) + 4p).
+// With NP = 2 the per-splat work (shared loads, ballots, the touched atomic,
+// loop control) is shared by two pixels and the two pixels' dependency chains
+// interleave.
+template <int NP>
 __global__ void __launch_bounds__(256, 4) k_blend16w(BlendArgs a, int n_items) {
   __shared__ float4 s_geo[kWarpsPerBlock16][32];   // mx_local, my_local, qa, qb
   __shared__ float4 s_geo2[kWarpsPerBlock16][32];  // qc, log2_alpha, r2_lo, r2_hi
@@ -258,6 +264,8 @@ __global__ void __launch_bounds__(256, 4) k_blend16w(BlendArgs a, int n_items) {
   __shared__ double s_mx[kWarpsPerBlock16][32], s_my[kWarpsPerBlock16][32],
       s_r2[kWarpsPerBlock16][32];
   __shared__ uint32_t s_id[kWarpsPerBlock16][32];
+  constexpr int kItemsPerTile = 8 / NP;
+  constexpr int kRows = 4 * NP;  // block height
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t* __restrict__ list = static_cast<const uint64_t*>(*a.keys_slot);
@@ -268,17 +276,32 @@ __global__ void __launch_bounds__(256, 4) k_blend16w(BlendArgs a, int n_items) {
     if (lane == 0) item = atomicAdd(a.work_counter, 1);
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= n_items) break;
-    const int tile = item >> 3, sub = item & 7;
+    const int tile = item / kItemsPerTile, sub = item % kItemsPerTile;
     const int tile_x = tile % a.tiles_x, tile_y = tile / a.tiles_x;
     const int x0 = tile_x * 16, y0 = tile_y * 16;
-    const int lx = (sub & 1) * 8 + (lane & 7), ly = (sub >> 1) * 4 + (lane >> 3);
-    const bool valid = x0 + lx < a.width && y0 + ly < a.height;
-    const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
-    if (!vmask) continue;
-    // warp pixel box (pixel centres, tile-local), valid pixels only
-    const float px = (float)lx + 0.5f, py = (float)ly + 0.5f;
-    float bx0 = valid ? px : 3.0e38f, bx1 = valid ? px : -3.0e38f;
-    float by0 = valid ? py : 3.0e38f, by1 = valid ? py : -3.0e38f;
+    const int lx = (sub & 1) * 8 + (lane & 7);
+    int ly[NP];
+    bool valid[NP];
+    float T[NP], C0[NP], C1[NP], C2[NP], D[NP];
+    bool any_valid = false;
+    float bx0 = 3.0e38f, bx1 = -3.0e38f, by0 = 3.0e38f, by1 = -3.0e38f;
+    const float px = (float)lx + 0.5f;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      ly[q] = (sub >> 1) * kRows + (lane >> 3) + 4 * q;
+      valid[q] = x0 + lx < a.width && y0 + ly[q] < a.height;
+      T[q] = valid[q] ? 1.0f : 0.0f;  // invalid pixels never go active
+      C0[q] = C1[q] = C2[q] = D[q] = 0.0f;
+      any_valid |= valid[q];
+      if (valid[q]) {  // warp pixel box (pixel centres, tile-local)
+        const float py = (float)ly[q] + 0.5f;
+        bx0 = fminf(bx0, px);
+        bx1 = fmaxf(bx1, px);
+        by0 = fminf(by0, py);
+        by1 = fmaxf(by1, py);
+      }
+    }
+    if (!__any_sync(0xffffffffu, any_valid)) continue;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       bx0 = fminf(bx0, __shfl_xor_sync(0xffffffffu, bx0, o));
@@ -287,93 +310,127 @@ __global__ void __launch_bounds__(256, 4) k_blend16w(BlendArgs a, int n_items) {
       by1 = fmaxf(by1, __shfl_xor_sync(0xffffffffu, by1, o));
     }
     const int2 range = a.ranges[tile];
-    float T = valid ? 1.0f : 0.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, D = 0.f;
-    int last = -1;
-    for (int b = range.x; b < range.y; b += 32) {
-      if (!__any_sync(0xffffffffu, T >= kTermEpsF)) break;
+    int last = -1;     // list index after which no pixel of this warp is active
+    bool live = true;  // some valid pixel still has T >= TERM_EPS
+    // software pipeline: batch b's id and geometry sectors were loaded while
+    // batch b - 32 was being blended
+    uint32_t id = 0;
+    float4 g0 = make_float4(0.f, 0.f, 0.f, 0.f), g1 = g0;
+    if (range.x + lane < range.y) {
+      id = (uint32_t)list[range.x + lane];
+      g0 = __ldg(rec4 + 4 * (size_t)id);
+      g1 = __ldg(rec4 + 4 * (size_t)id + 1);
+    }
+    for (int b = range.x; b < range.y && live; b += 32) {
       const int j = b + lane;
+      const bool have = j < range.y;
+      const uint32_t cid = id;
+      const float4 c0 = g0, c1 = g1;
+      if (j + 32 < range.y) {  // prefetch the next batch
+        id = (uint32_t)list[j + 32];
+        g0 = __ldg(rec4 + 4 * (size_t)id);
+        g1 = __ldg(rec4 + 4 * (size_t)id + 1);
+      }
       bool hit = false;
-      if (j < range.y) {
-        const uint32_t id = (uint32_t)list[j];
-        const float4 g0 = __ldg(rec4 + 4 * (size_t)id);      // mx, my (fp64)
-        const float4 g1 = __ldg(rec4 + 4 * (size_t)id + 1);  // r2 (fp64), qa, qb
-        const double mx = __hiloint2double(__float_as_int(g0.y), __float_as_int(g0.x));
-        const double my = __hiloint2double(__float_as_int(g0.w), __float_as_int(g0.z));
-        const double r2 = __hiloint2double(__float_as_int(g1.y), __float_as_int(g1.x));
+      if (have) {
+        const double mx = __hiloint2double(__float_as_int(c0.y), __float_as_int(c0.x));
+        const double my = __hiloint2double(__float_as_int(c0.w), __float_as_int(c0.z));
+        const double r2 = __hiloint2double(__float_as_int(c1.y), __float_as_int(c1.x));
         const double mxl = mx - (double)x0, myl = my - (double)y0;
         const float fx = (float)mxl, fy = (float)myl;
         const float r = sqrtf((float)r2) * 1.0001f + 1e-3f;
         hit = fx + r >= bx0 && fx - r <= bx1 && fy + r >= by0 && fy - r <= by1;
         if (hit) {
-          const float4 g2 = __ldg(rec4 + 4 * (size_t)id + 2);  // qc, log2a, r, g
-          const float4 g3 = __ldg(rec4 + 4 * (size_t)id + 3);  // b, z
+          const float4 g2 = __ldg(rec4 + 4 * (size_t)cid + 2);  // qc, log2a, r, g
+          const float4 g3 = __ldg(rec4 + 4 * (size_t)cid + 3);  // b, z
           const double ax = fabs(mxl) + 16.0, ay = fabs(myl) + 16.0;
           const double band = (r2 + ax * ax + ay * ay) * 0x1p-18;
-          s_geo[warp][lane] = make_float4(fx, fy, g1.z, g1.w);
+          s_geo[warp][lane] = make_float4(fx, fy, c1.z, c1.w);
           s_geo2[warp][lane] = make_float4(g2.x, g2.y, __double2float_rd(r2 - band),
                                            __double2float_ru(r2 + band));
           s_col[warp][lane] = make_float4(g2.z, g2.w, g3.x, g3.y);
           s_mx[warp][lane] = mx;
           s_my[warp][lane] = my;
           s_r2[warp][lane] = r2;
-          s_id[warp][lane] = id;
+          s_id[warp][lane] = cid;
         }
       }
       uint32_t m = __ballot_sync(0xffffffffu, hit);
       __syncwarp();
+      uint32_t my_touch = 0;  // pixels with w > 0 for this lane's splat (cid)
       while (m) {
         const int k = __ffs(m) - 1;
         m &= m - 1;
         const float4 g = s_geo[warp][k];
         const float4 h = s_geo2[warp][k];
         const float4 c = s_col[warp][k];
-        bool contrib = false;
-        if (T >= kTermEpsF) {
-          const float dx = px - g.x, dy = py - g.y;
+        const float dx = px - g.x;
+        uint32_t contrib_bits = 0;
+        bool active = false;
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          // branch-free common path: sigma is computed for every pixel and
+          // forced to 0 when the pixel is outside the circle or already
+          // inactive, which leaves C and T bit-identical (fmaf(0, c, C) = C,
+          // T * (1 - 0) = T); only the rare fp64 decisions branch
+          const bool on = T[q] >= kTermEpsF;
+          const float dy = ((float)ly[q] + 0.5f) - g.y;
           const float d2 = fmaf(dx, dx, dy * dy);
           bool inside = d2 <= h.z;
-          if (!inside && d2 <= h.w) {
+          if (on && !inside && d2 <= h.w) {  // guard band: the reference's fp64 test
             const double ddx = ((double)(x0 + lx) + 0.5) - s_mx[warp][k];
-            const double ddy = ((double)(y0 + ly) + 0.5) - s_my[warp][k];
+            const double ddy = ((double)(y0 + ly[q]) + 0.5) - s_my[warp][k];
             inside = __dadd_rn(__dmul_rn(ddx, ddx), __dmul_rn(ddy, ddy)) <= s_r2[warp][k];
           }
-          if (inside) {
-            const float power = fmaf(fmaf(g.z, dx, g.w * dy), dx, fmaf(h.x * dy, dy, h.y));
-            contrib = power > -1060.0f;
-            if (!contrib && power >= -1080.0f) contrib = exp2((double)power) * (double)T > 0.0;
-            const float sig = fminf(ex2_approx(power), kSigmaMaxF);
-            const float w = T * sig;
-            C0 = fmaf(w, c.x, C0);
-            C1 = fmaf(w, c.y, C1);
-            C2 = fmaf(w, c.z, C2);
-            D = fmaf(w, c.w, D);
-            T = T * (1.0f - sig);
-            if (T < kTermEpsF) last = b - range.x + k;
-          }
+          const float power = fmaf(fmaf(g.z, dx, g.w * dy), dx, fmaf(h.x * dy, dy, h.y));
+          const bool take = on && inside;
+          bool contrib = take && power > -1060.0f;
+          if (take && !contrib && power >= -1080.0f)  // fp32 ex2 underflows first
+            contrib = exp2((double)power) * (double)T[q] > 0.0;
+          const float sig = take ? fminf(ex2_approx(power), kSigmaMaxF) : 0.0f;
+          const float w = T[q] * sig;
+          C0[q] = fmaf(w, c.x, C0[q]);
+          C1[q] = fmaf(w, c.y, C1[q]);
+          C2[q] = fmaf(w, c.z, C2[q]);
+          D[q] = fmaf(w, c.w, D[q]);
+          T[q] = T[q] * (1.0f - sig);
+          contrib_bits += contrib;
+          active |= T[q] >= kTermEpsF;
         }
-        const uint32_t cm = __ballot_sync(0xffffffffu, contrib);
-        if (lane == 0 && cm && a.touched) atomicAdd(a.touched + s_id[warp][k], __popc(cm));
+        const int wsum = NP == 1 ? __popc(__ballot_sync(0xffffffffu, contrib_bits))
+                                 : __reduce_add_sync(0xffffffffu, contrib_bits);
+        if (lane == k) my_touch += wsum;
+        // pixels only go inactive on a splat they are inside: the warp's break
+        // index is the first splat after which none of its pixels is active
+        if (!__any_sync(0xffffffffu, active)) {
+          last = b - range.x + k;
+          live = false;
+          break;
+        }
       }
+      if (my_touch && a.touched) atomicAdd(a.touched + cid, (int)my_touch);
       __syncwarp();
     }
-    if (a.n_processed) {
-      int v = last;
+    if (a.n_processed && lane == 0)
+      atomicMax(a.n_processed + tile, live ? (range.y - range.x) : last + 1);
 #pragma unroll
-      for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-      const bool live = __any_sync(0xffffffffu, valid && T >= kTermEpsF);
-      if (lane == 0) atomicMax(a.n_processed + tile, live ? (range.y - range.x) : v + 1);
-    }
-    if (valid) {
-      const int64_t o = (int64_t)(y0 + ly) * a.width + (x0 + lx);
-      a.rgb[3 * o + 0] = fmaf(T, a.bg[0], C0);
-      a.rgb[3 * o + 1] = fmaf(T, a.bg[1], C1);
-      a.rgb[3 * o + 2] = fmaf(T, a.bg[2], C2);
-      if (a.alpha) a.alpha[o] = 1.0f - T;
-      if (a.depth) a.depth[o] = D;
-      if (a.trans) a.trans[o] = T;
+    for (int q = 0; q < NP; ++q) {
+      if (!valid[q]) continue;
+      const int64_t o = (int64_t)(y0 + ly[q]) * a.width + (x0 + lx);
+      a.rgb[3 * o + 0] = fmaf(T[q], a.bg[0], C0[q]);
+      a.rgb[3 * o + 1] = fmaf(T[q], a.bg[1], C1[q]);
+      a.rgb[3 * o + 2] = fmaf(T[q], a.bg[2], C2[q]);
+      if (a.alpha) a.alpha[o] = 1.0f - T[q];
+      if (a.depth) a.depth[o] = D[q];
+      if (a.trans) a.trans[o] = T[q];
     }
   }
 }
+
+#ifndef LMGS_BLEND_NP
+#define LMGS_BLEND_NP 1
+#endif
+constexpr int kBlendNP = LMGS_BLEND_NP;
 
 }  // namespace
 
@@ -384,19 +441,19 @@ int launch_blend(const BlendArgs& a, cudaStream_t s) {
   if (ts == 16 && a.work_counter) {
     cudaMemsetAsync(a.work_counter, 0, sizeof(int), s);
     if (a.n_processed) cudaMemsetAsync(a.n_processed, 0, sizeof(int) * tiles, s);
-    const int items = tiles * 8;
+    const int items = tiles * (8 / kBlendNP);
     static int blocks_per_sm = 0, sms = 0;
     if (!blocks_per_sm) {
       int dev = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_blend16w, 256, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_blend16w<kBlendNP>, 256, 0);
       if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
     int grid = sms * blocks_per_sm;
     const int need = (items + kWarpsPerBlock16 - 1) / kWarpsPerBlock16;
     if (grid > need) grid = need;
-    k_blend16w<<<grid, 256, 0, s>>>(a, items);
+    k_blend16w<kBlendNP><<<grid, 256, 0, s>>>(a, items);
   } else if (ts == 16) {
     k_blend<1, true><<<tiles, 256, 0, s>>>(a);
   } else if (ts < 16) {
