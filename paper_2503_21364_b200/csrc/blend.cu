@@ -256,8 +256,11 @@ constexpr int kWarpsPerBlock16 = 8;
 // With NP = 2 the per-splat work (shared loads, ballots, the touched atomic,
 // loop control) is shared by two pixels and the two pixels' dependency chains
 // interleave.
+#ifndef LMGS_BLEND_MINB
+#define LMGS_BLEND_MINB 4  // 4 x 256 threads per SM (64 registers): measured best
+#endif
 template <int NP>
-__global__ void __launch_bounds__(256, 4) k_blend16w(BlendArgs a, int n_items) {
+__global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, int n_items) {
   __shared__ float4 s_geo[kWarpsPerBlock16][32];   // mx_local, my_local, qa, qb
   __shared__ float4 s_geo2[kWarpsPerBlock16][32];  // qc, log2_alpha, r2_lo, r2_hi
   __shared__ float4 s_col[kWarpsPerBlock16][32];   // r, g, b, z

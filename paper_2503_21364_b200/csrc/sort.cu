@@ -144,7 +144,20 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
     K* keys0, K* keys1, uint32_t* vals0, uint32_t* vals1, int64_t n, int begin_bit, int pass,
     const RadixPlan* __restrict__ plan, uint32_t* lookback, uint32_t* counter, int64_t lb_stride,
     bool iota_vals, uint32_t* seg_counts, int seg_shift) {
-  if (!plan->active[pass]) return;
+  if (!plan->active[pass]) {
+    // no pass moves data (every digit trivial): the result buffers are the
+    // inputs, so pass 0 materialises the implicit payload and the single
+    // segment instead of separate launches
+    if (pass == 0 && plan->first_active < 0) {
+      if (VALS && iota_vals)
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+             i += (int64_t)gridDim.x * blockDim.x)
+          vals0[i] = (uint32_t)i;
+      if (seg_counts && blockIdx.x == 0 && threadIdx.x == 0 && n > 0)
+        seg_counts[(uint64_t)keys0[0] >> seg_shift] = (uint32_t)n;
+    }
+    return;
+  }
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K* s_keys = reinterpret_cast<K*>(smem_raw);  // [kSortTile] staging
   uint32_t* s_vals = reinterpret_cast<uint32_t*>(smem_raw + sizeof(K) * kSortTile);
@@ -316,24 +329,6 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
   }
 }
 
-// implicit payload with no data-moving pass (every digit trivial): the result
-// buffer vals[0] still has to hold the identity permutation
-__global__ void k_iota_if_idle(const RadixPlan* __restrict__ plan, uint32_t* vals, int64_t n) {
-  if (plan->first_active >= 0) return;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    vals[i] = (uint32_t)i;
-}
-
-// segment counts with no data-moving pass: every key is equal on the sorted
-// bits, so there is a single segment holding all n keys
-template <typename K>
-__global__ void k_segments_if_idle(const RadixPlan* __restrict__ plan, const K* keys, int64_t n,
-                                   uint32_t* seg_counts, int seg_shift) {
-  if (plan->last_active >= 0 || n <= 0) return;
-  seg_counts[(uint64_t)keys[0] >> seg_shift] = (uint32_t)n;
-}
-
 template <typename K, bool VALS>
 constexpr size_t onesweep_smem() {
   return sizeof(K) * kSortTile + (VALS ? sizeof(uint32_t) * kSortTile : 0);
@@ -376,15 +371,6 @@ int radix_sort_impl(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_p
   k_radix_plan<<<1, kRadix, 0, s>>>(b.hist, n, n_passes, b.plan, b.gate, k0, k1, b.vals[0],
                                     b.vals[1], b.keys_result, b.vals_result);
   ++launched;
-  if (b.iota_vals && n > 0) {
-    const int64_t g = (n + 255) / 256;
-    k_iota_if_idle<<<(unsigned)(g < 148 * 8 ? g : 148 * 8), 256, 0, s>>>(b.plan, b.vals[0], n);
-    ++launched;
-  }
-  if (b.seg_counts && n > 0) {
-    k_segments_if_idle<K><<<1, 1, 0, s>>>(b.plan, k0, n, b.seg_counts, b.seg_shift);
-    ++launched;
-  }
   if (blocks == 0) return launched;
   for (int p = 0; p < n_passes; ++p) {
     if (b.vals[1]) launch_onesweep<K, true>(b, n, begin_bit, p, blocks, s);

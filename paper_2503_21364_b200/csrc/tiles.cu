@@ -252,7 +252,11 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(EmitArgs a) {
       const uint32_t q = p - st_i;
       const int x0 = (int)(r_lo & 0xffff), y0 = (int)(r_lo >> 16), x1 = (int)(r_hi & 0xffff);
       const uint32_t w = (uint32_t)(x1 - x0 + 1);
-      const uint32_t dy = q / w;
+      // q / w without the integer-division sequence: q < 2^24, w < 2^16, so
+      // the float quotient is within one of the truth; fix it up exactly
+      uint32_t dy = (uint32_t)__fdividef((float)q, (float)w);
+      if (dy * w > q) --dy;
+      else if ((dy + 1) * w <= q) ++dy;
       tile = (uint32_t)(y0 + (int)dy) * (uint32_t)a.tiles_x + (uint32_t)x0 + (q - dy * w);
       a.keys[out0 + p] = ((uint64_t)tile << 32) | id_i;
       // the low digit differs across lanes (consecutive tiles of a row)
@@ -285,6 +289,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(EmitArgs a) {
 // K6: tile ranges = exclusive scan of the per-tile counts (one CTA)
 
 constexpr int kScanThreads = 1024;
+constexpr int kScanPer = 8;  // counts per thread per step
 
 __global__ void __launch_bounds__(kScanThreads) k_ranges_from_counts(const uint32_t* counts,
                                                                      int tiles, int2* ranges) {
@@ -293,10 +298,16 @@ __global__ void __launch_bounds__(kScanThreads) k_ranges_from_counts(const uint3
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_carry = 0;
   __syncthreads();
-  for (int base = 0; base < tiles; base += kScanThreads) {
-    const int t = base + tid;
-    const uint32_t c = t < tiles ? counts[t] : 0u;
-    uint32_t incl = c;
+  for (int base = 0; base < tiles; base += kScanThreads * kScanPer) {
+    const int t0 = base + tid * kScanPer;
+    uint32_t c[kScanPer];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int j = 0; j < kScanPer; ++j) {
+      c[j] = t0 + j < tiles ? counts[t0 + j] : 0u;
+      sum += c[j];
+    }
+    uint32_t incl = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
@@ -315,10 +326,14 @@ __global__ void __launch_bounds__(kScanThreads) k_ranges_from_counts(const uint3
       s_warp[lane] = wi - w;
     }
     __syncthreads();
-    const uint32_t excl = s_carry + s_warp[warp] + (incl - c);
-    if (t < tiles) ranges[t] = make_int2((int)excl, (int)(excl + c));
+    uint32_t run = s_carry + s_warp[warp] + (incl - sum);
+#pragma unroll
+    for (int j = 0; j < kScanPer; ++j) {
+      if (t0 + j < tiles) ranges[t0 + j] = make_int2((int)run, (int)(run + c[j]));
+      run += c[j];
+    }
     __syncthreads();
-    if (tid == kScanThreads - 1) s_carry = excl + c;
+    if (tid == kScanThreads - 1) s_carry = run;
     __syncthreads();
   }
 }
