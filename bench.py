@@ -191,7 +191,8 @@ def run_ours(args, rank, world, local):
     views = args.views
     all_cams = scenes.orbit_cameras(views * world, W, H, seed=0)
     cams = all_cams[rank * views:(rank + 1) * views]
-    renderer = BatchRenderer(model, W, H, views, tile_size=16, sh_eval_degree=3)
+    renderer = BatchRenderer(model, W, H, views, tile_size=16, sh_eval_degree=3,
+                             n_streams=args.streams)
 
     # warm-up (also sizes every arena)
     for _ in range(args.warmup):
@@ -295,6 +296,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", type=int, default=3,
+                    help="contexts/streams the view batch alternates over")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":

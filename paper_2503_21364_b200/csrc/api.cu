@@ -344,7 +344,7 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
     rb.vals_result = &sc->slots.depth_ids;
     rb.iota_vals = true;
     rb.hist_ready = true;
-    launched += radix_sort(rb, n, 0, 4, s);
+    launched += radix_sort(rb, n, 0, kDepthPasses, s);
     launched += launch_depth_fixup(&sc->slots.depth_keys, &sc->slots.depth_ids, n, c->key64, s);
   }
   tm.end(1);

@@ -143,9 +143,11 @@ struct DevSlots {
 
 constexpr int kMaxTilePasses = 3;  // tile ids < 2^24
 
-// K2a: 32-bit depth keys quantised over the view's visible depth range
-// (monotone in the fp64 depth; 0xffffffff = invisible) + their 4 digit
-// histograms for the radix sort
+// K2a: 24-bit depth keys quantised over the view's visible depth range
+// (monotone in the fp64 depth; kDepthKeyNone = invisible) + their digit
+// histograms for the radix sort (kDepthPasses passes of 8 bits)
+constexpr int kDepthPasses = 3;
+constexpr uint32_t kDepthKeyNone = (1u << (8 * kDepthPasses)) - 1;
 int launch_depth_keys(const uint64_t* key64, const unsigned long long* zrange, int64_t n,
                       uint32_t* key32, uint32_t* hist, cudaStream_t s);
 
