@@ -39,6 +39,18 @@ N_GAUSS = 6_000_000
 W, H = 1920, 1080
 
 
+# dram__bytes_read.sum + dram__bytes_write.sum per launch of each stage's kernels
+# on a c3 view, from the committed full ncu captures (profiles/r02/*_summary.txt;
+# stage = sum of its kernels).  Reported as `traffic` beside the algorithmic bytes.
+NCU_TRAFFIC_R02 = {
+    "preprocess": 1603.5e6 + 465.2e6,
+    "depth_sort": (48.0e6 + 0.1e6) + (25.3e6 + 1.0e6) + 2 * (49.3e6 + 2.5e6) + (100.6e6 + 5.9e6),
+    "emit": 135.6e6 + 122.6e6,
+    "tile_sort": 2 * (168.4e6 + 124.0e6),
+    "blend": 141.2e6 + 32.3e6,
+}
+
+
 def peaks():
     try:
         return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -243,11 +255,20 @@ def run_ours(args, rank, world, local):
         dom_ms = st[dom] / frames
         achieved = alg[dom] / (dom_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
-                "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": NCU_TRAFFIC_R02.get(dom),
+                "traffic_source": "profiles/r02 ncu --set full (dram bytes per launch, c3 view)",
+                "stage_traffic": NCU_TRAFFIC_R02,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"
                 if "hbm_gbs" in pk else "fallback 6650 GB/s (B200_PROFILING.md)",
                 "stage_ms_per_frame": {k: v / frames for k, v in st.items()},
-                "stage_gbs": {k: alg[k] / (st[k] / frames / 1e3) / 1e9 for k in st if st[k] > 0}}
+                "stage_gbs": {k: alg[k] / (st[k] / frames / 1e3) / 1e9 for k in st if st[k] > 0},
+                "stage_alg_bytes": alg}
+        roof["stage_frac"] = {k: v / hbm for k, v in roof["stage_gbs"].items()}
+        if dom == "blend":
+            roof["note"] = ("the dominant stage (blend) is FP32/MUFU-issue bound, not HBM "
+                            "bound: its HBM fraction is informational; blend_pairs is its "
+                            "roofline")
         blend_pairs = per.get("pairs", 0)
         if blend_pairs:
             sm_clk = (clocks.get("sm_mhz") or 1965.0) * 1e6
