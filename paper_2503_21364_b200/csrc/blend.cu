@@ -324,10 +324,38 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
       g0 = __ldg(rec4 + 4 * (size_t)id);
       g1 = __ldg(rec4 + 4 * (size_t)id + 1);
     }
+    uint32_t box_mask = __ballot_sync(0xffffffffu, any_valid);  // lanes the box covers
     for (int b = range.x; b < range.y && live; b += 32) {
       const int j = b + lane;
       const bool have = j < range.y;
       const uint32_t cid = id;
+      // shrink the cull box to the pixels still active (finished pixels need
+      // no more splats); recomputed only when some lane has finished
+      bool act_any = false;
+#pragma unroll
+      for (int q = 0; q < NP; ++q) act_any |= T[q] >= kTermEpsF;
+      const uint32_t act_mask = __ballot_sync(0xffffffffu, act_any);
+      if (act_mask != box_mask) {
+        box_mask = act_mask;
+        bx0 = 3.0e38f, bx1 = -3.0e38f, by0 = 3.0e38f, by1 = -3.0e38f;
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          if (T[q] >= kTermEpsF) {
+            const float py = (float)ly[q] + 0.5f;
+            bx0 = fminf(bx0, px);
+            bx1 = fmaxf(bx1, px);
+            by0 = fminf(by0, py);
+            by1 = fmaxf(by1, py);
+          }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          bx0 = fminf(bx0, __shfl_xor_sync(0xffffffffu, bx0, o));
+          bx1 = fmaxf(bx1, __shfl_xor_sync(0xffffffffu, bx1, o));
+          by0 = fminf(by0, __shfl_xor_sync(0xffffffffu, by0, o));
+          by1 = fmaxf(by1, __shfl_xor_sync(0xffffffffu, by1, o));
+        }
+      }
       const float4 c0 = g0, c1 = g1;
       if (j + 32 < range.y) {  // prefetch the next batch
         id = (uint32_t)list[j + 32];
@@ -341,8 +369,12 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
         const double r2 = __hiloint2double(__float_as_int(c1.y), __float_as_int(c1.x));
         const double mxl = mx - (double)x0, myl = my - (double)y0;
         const float fx = (float)mxl, fy = (float)myl;
+        // exact circle-vs-box cull (the reference's support is the circle
+        // d.d <= r^2 around the mean) with a conservative radius margin
         const float r = sqrtf((float)r2) * 1.0001f + 1e-3f;
-        hit = fx + r >= bx0 && fx - r <= bx1 && fy + r >= by0 && fy - r <= by1;
+        const float ex = fx - fminf(fmaxf(fx, bx0), bx1);
+        const float ey = fy - fminf(fmaxf(fy, by0), by1);
+        hit = fmaf(ex, ex, ey * ey) <= r * r;
         if (hit) {
           const float4 g2 = __ldg(rec4 + 4 * (size_t)cid + 2);  // qc, log2a, r, g
           const float4 g3 = __ldg(rec4 + 4 * (size_t)cid + 3);  // b, z
@@ -375,7 +407,8 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
           // branch-free common path: sigma is computed for every pixel and
           // forced to 0 when the pixel is outside the circle or already
           // inactive, which leaves C and T bit-identical (fmaf(0, c, C) = C,
-          // T * (1 - 0) = T); only the rare fp64 decisions branch
+          // T * (1 - 0) = T); only the rare fp64 decisions branch.  (Skipping
+          // splats that cover no active pixel with an extra vote measured slower.)
           const bool on = T[q] >= kTermEpsF;
           const float dy = ((float)ly[q] + 0.5f) - g.y;
           const float d2 = fmaf(dx, dx, dy * dy);
