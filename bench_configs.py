@@ -1,0 +1,156 @@
+"""Per-configuration measurements on one B200, beside bench.py's headline (c3).
+
+    python bench_configs.py [--configs c2,c4,c5] [--out FILE]
+
+One JSON line per configuration (BASELINE.json `configs`):
+  c2  1M Gaussians, 1920x1080, single view (16 orbit views timed back to back)
+  c4  6M Gaussians, 3840x2160, single view (8 orbit views timed back to back)
+  c5  50M-Gaussian city in 8 spatial blocks (6.25M each), 1080p: every block
+      rendered with background 0 into (premultiplied RGB, T, depth) layers and
+      composited front to back in block order (the single-GPU run of the block
+      algorithm the 8-GPU run distributes); the monolithic render of all 50M
+      Gaussians is timed too and the block composite's deviation from it is
+      reported (not gated: SURVEY §7 item 9).
+
+Timing: CUDA events on the launching stream after warm-up; inputs resident in
+HBM.  Stage times come from one extra run with per-stage events.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import time
+
+import numpy as np
+import torch
+
+from paper_2503_21364_b200 import GaussianModel, render, scenes
+from paper_2503_21364_b200.batch import BatchRenderer
+from paper_2503_21364_b200.distributed import block_order
+from paper_2503_21364_b200.raster import composite_blocks
+
+
+def _events_ms(fn, iters: int, warm: int) -> float:
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / iters
+
+
+def batch_config(name: str, n: int, w: int, h: int, views: int, steps: int) -> dict:
+    t0 = time.perf_counter()
+    g = scenes.synthetic_gaussians(n, seed=0)
+    gen_s = time.perf_counter() - t0
+    model = GaussianModel.from_host(g, validate=False)
+    cams = scenes.orbit_cameras(views, w, h, seed=0)
+    r = BatchRenderer(model, w, h, views, tile_size=16, sh_eval_degree=3, n_streams=3)
+    ms = _events_ms(lambda: r.render(cams), steps, 2)
+    st = r.render(cams, stage_times=True)
+    torch.cuda.synchronize()
+    per = {k: v / views for k, v in st["stage_ms"].items()}
+    return {"config": name, "gaussians": n, "width": w, "height": h, "views": views,
+            "frames_per_s": views / (ms / 1e3), "ms_per_frame": ms / views,
+            "stage_ms_per_frame": per, "instances_per_frame": st["per_frame"]["instances"],
+            "processed_per_frame": st["per_frame"]["processed"],
+            "stage_gbs": {k: st["alg_bytes"][k] / (per[k] / 1e3) / 1e9 for k in per if per[k]},
+            "host_generate_s": gen_s}
+
+
+def city_config(per_block: int, steps: int) -> dict:
+    t0 = time.perf_counter()
+    city = scenes.city_scene(per_block=per_block)
+    gen_s = time.perf_counter() - t0
+    cam = city.camera
+    h, w = cam.height, cam.width
+    models = [GaussianModel.from_host(b, validate=False) for b in city.blocks]
+    nb = len(models)
+    order = block_order(np.asarray(cam.center), city.block_bboxes)
+    # planar per-block layers, rendered into in place (no copies)
+    lrgb = torch.empty((nb, h, w, 3), dtype=torch.float32, device="cuda")
+    ltrans = torch.empty((nb, h, w), dtype=torch.float32, device="cuda")
+    ldepth = torch.empty((nb, h, w), dtype=torch.float32, device="cuda")
+
+    def render_block(b):
+        render(cam, models[b], 16, (0.0, 0.0, 0.0), 3,
+               out={"rgb": lrgb[b], "transmittance": ltrans[b], "depth": ldepth[b]})
+
+    def blocks():
+        for b in range(nb):
+            render_block(b)
+
+    def composite():
+        return composite_blocks(lrgb, ltrans, order, (0.0, 0.0, 0.0), ldepth)
+
+    def frame():
+        blocks()
+        return composite()
+
+    ms_frame = _events_ms(frame, steps, 1)
+    ms_comp = _events_ms(composite, steps, 1)
+    block_ms = [_events_ms(lambda b=b: render_block(b), 2, 1) for b in range(nb)]
+    rgb_blk, alpha_blk, _ = frame()
+    torch.cuda.synchronize()
+    # monolithic render of all 50M (the deviation of the block composite from it)
+    mono = None
+    try:
+        cat = scenes.HostGaussians(*(np.concatenate([getattr(b, f) for b in city.blocks])
+                                     for f in ("means", "quats", "scales", "opacity_logits", "sh")),
+                                   city.blocks[0].sh_degree)
+        big = GaussianModel.from_host(cat, validate=False)
+        del cat
+        out = {}
+        ms_mono = _events_ms(lambda: out.update(o=render(cam, big, 16, (0.0, 0.0, 0.0), 3)), 2, 1)
+        d = (out["o"].rgb - rgb_blk).abs().amax(dim=-1).flatten()
+        mono = {"ms_per_frame": ms_mono, "instances": out["o"].n_instances,
+                "block_vs_monolithic_rgb": {
+                    "max_abs": float(d.max()), "mean_abs": float(d.mean()),
+                    "p99_abs": float(torch.quantile(d[::7].float(), 0.99)),
+                    "frac_pixels_over_1e-3": float((d > 1e-3).float().mean()),
+                    "frac_pixels_over_1e-2": float((d > 1e-2).float().mean())}}
+        del big
+    except torch.cuda.OutOfMemoryError as e:  # pragma: no cover - reported, not fatal
+        mono = {"error": str(e)[:200]}
+    return {"config": "c5", "gaussians": per_block * nb, "blocks": nb, "width": w, "height": h,
+            "ms_per_frame_serial_blocks": ms_frame, "frames_per_s_serial": 1e3 / ms_frame,
+            "ms_composite": ms_comp, "ms_per_block": block_ms,
+            "critical_path_8gpu_ms": max(block_ms) + ms_comp,
+            "note": "one GPU renders all 8 blocks serially; with one block per GPU the frame "
+                    "is bounded by the slowest block + exchange + composite (critical_path "
+                    "excludes the NVLink exchange)",
+            "block_order": order, "monolithic": mono, "host_generate_s": gen_s}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="c2,c4,c5")
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    lines = []
+    for c in a.configs.split(","):
+        if c == "c2":
+            line = batch_config("c2", 1_000_000, 1920, 1080, 16, a.steps)
+        elif c == "c4":
+            line = batch_config("c4", 6_000_000, 3840, 2160, 8, a.steps)
+        elif c == "c5":
+            line = city_config(6_250_000, a.steps)
+        else:
+            raise SystemExit(f"unknown config {c}")
+        print(json.dumps(line), flush=True)
+        lines.append(line)
+        torch.cuda.empty_cache()
+    if a.out:
+        with open(a.out, "w") as f:
+            for line in lines:
+                f.write(json.dumps(line) + "\n")
+
+
+if __name__ == "__main__":
+    main()

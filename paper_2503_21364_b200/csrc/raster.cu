@@ -22,7 +22,10 @@ struct BlockOrder {
 };
 
 // Front-to-back "over" of per-block premultiplied renders (background 0):
-// C = sum_b (prod_{b'<b} T_b') C_b + (prod_b T_b) bg.
+// C = sum_b (prod_{b'<b} T_b') C_b + (prod_b T_b) bg.  Blocks are read four
+// at a time (independent loads in flight) before the dependent "over" chain.
+constexpr int kCompUnroll = 4;
+
 __global__ void k_composite(const float* __restrict__ rgb, const float* __restrict__ trans,
                             const float* __restrict__ depth, int n_blocks, const BlockOrder order,
                             int64_t n_pix, float b0, float b1, float b2, float* out_rgb,
@@ -30,13 +33,26 @@ __global__ void k_composite(const float* __restrict__ rgb, const float* __restri
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_pix) return;
   float T = 1.0f, r = 0.f, g = 0.f, b = 0.f, d = 0.f;
-  for (int k = 0; k < n_blocks; ++k) {
-    const int64_t o = (int64_t)order.v[k] * n_pix + i;
-    r = fmaf(T, rgb[3 * o + 0], r);
-    g = fmaf(T, rgb[3 * o + 1], g);
-    b = fmaf(T, rgb[3 * o + 2], b);
-    if (depth) d = fmaf(T, depth[o], d);
-    T *= trans[o];
+  for (int k0 = 0; k0 < n_blocks; k0 += kCompUnroll) {
+    float cr[kCompUnroll], cg[kCompUnroll], cb[kCompUnroll], ct[kCompUnroll], cd[kCompUnroll];
+#pragma unroll
+    for (int u = 0; u < kCompUnroll; ++u) {
+      const bool on = k0 + u < n_blocks;
+      const int64_t o = on ? (int64_t)order.v[k0 + u] * n_pix + i : i;
+      cr[u] = on ? __ldg(rgb + 3 * o + 0) : 0.f;
+      cg[u] = on ? __ldg(rgb + 3 * o + 1) : 0.f;
+      cb[u] = on ? __ldg(rgb + 3 * o + 2) : 0.f;
+      ct[u] = on ? __ldg(trans + o) : 1.f;
+      cd[u] = (on && depth) ? __ldg(depth + o) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < kCompUnroll; ++u) {
+      r = fmaf(T, cr[u], r);
+      g = fmaf(T, cg[u], g);
+      b = fmaf(T, cb[u], b);
+      d = fmaf(T, cd[u], d);
+      T *= ct[u];
+    }
   }
   out_rgb[3 * i + 0] = fmaf(T, b0, r);
   out_rgb[3 * i + 1] = fmaf(T, b1, g);
