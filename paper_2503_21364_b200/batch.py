@@ -59,10 +59,15 @@ class BatchRenderer:
                           _ptr(self.touched[i]) if self.touched is not None else None,
                           _ptr(self.kept[i]), _ptr(self.ranges[i]), _ptr(self.nproc[i]))
 
-    def render(self, cams, stage_times: bool = False):
+    def render(self, cams, stage_times: bool = False, host_rgb: torch.Tensor | None = None,
+               copy_stream: torch.cuda.Stream | None = None):
         """Render len(cams) views into the batch buffers (async w.r.t. the host
         except for the per-view K read).  With ``stage_times`` the views run
-        serially on one stream and per-stage CUDA-event times are summed."""
+        serially on one stream and per-stage CUDA-event times are summed.
+
+        ``host_rgb`` (pinned, (V,H,W,3) fp32): each frame's D2H copy is queued on
+        ``copy_stream`` right after its view is launched, so the copies overlap
+        the following views' rendering instead of trailing the batch."""
         assert len(cams) <= self.max_views
         L = _lib.lib()
         caller = torch.cuda.current_stream(self.dev)
@@ -118,8 +123,14 @@ class BatchRenderer:
                                                  ctypes.byref(st), ctypes.byref(fr),
                                                  s.cuda_stream), "lmgs_render")
             self.view_done[i].record(s)
+            if host_rgb is not None:
+                copy_stream.wait_event(self.view_done[i])
+                with torch.cuda.stream(copy_stream):
+                    host_rgb[i].copy_(self.rgb[i], non_blocking=True)
         for s in self.streams:
             caller.wait_stream(s)
+        if host_rgb is not None:
+            caller.wait_stream(copy_stream)
         return None
 
     def _pairs(self, i) -> float:
@@ -141,19 +152,15 @@ class BatchRenderer:
         """Frames/s through the public API with host buffers: per step the
         camera poses travel H2D (kernel parameters, from pinned host structs)
         and every RGB frame is copied D2H into pinned host memory on a copy
-        stream overlapped with the next views' rendering."""
+        stream, queued as soon as its view is launched so it overlaps the next
+        views' rendering."""
         nv = len(cams)
         host = torch.empty((nv, self.h, self.w, 3), dtype=torch.float32, pin_memory=True)
         copy = torch.cuda.Stream(device=self.dev)
         caller = torch.cuda.current_stream(self.dev)
 
         def step():
-            self.render(cams)
-            for i in range(nv):
-                copy.wait_event(self.view_done[i])
-                with torch.cuda.stream(copy):
-                    host[i].copy_(self.rgb[i], non_blocking=True)
-            caller.wait_stream(copy)
+            self.render(cams, host_rgb=host, copy_stream=copy)
 
         step()  # warm
         torch.cuda.synchronize()
