@@ -19,6 +19,12 @@
  *   lmgs_composite_blocks  (new) front-to-back "over" of per-block premultiplied
  *                          images; replaces render_runtime.py:189-191 (BlockSession
  *                          concatenating resident cells into one model)
+ *   lmgs_checkpoint_info_read / lmgs_checkpoint_load / lmgs_checkpoint_save
+ *                          data_io.py:256-316 load_gaussian_checkpoint /
+ *                          save_gaussian_checkpoint (LMGS format), into / from
+ *                          device SoA arrays
+ *   lmgs_encode_rgb8       render_runtime.py:397-401 encode_frame's pixels
+ *                          (round(clip(rgb, 0, 1) * 255), half to even)
  *
  * Error behaviour: every entry point returns an lmgs_status; on failure
  * lmgs_last_error(ctx) holds a message.  Bad arguments map to the reference's
@@ -43,7 +49,9 @@ typedef enum lmgs_status {
   LMGS_ERR_INVALID = 1,     /* bad argument (shape, size, null pointer)   */
   LMGS_ERR_CUDA = 2,        /* CUDA runtime error                         */
   LMGS_ERR_OOM = 3,         /* device allocation failed                   */
-  LMGS_ERR_UNSUPPORTED = 4  /* e.g. tile_size > 64                        */
+  LMGS_ERR_UNSUPPORTED = 4, /* e.g. tile_size > 64                        */
+  LMGS_ERR_FORMAT = 5,      /* malformed checkpoint (reference FormatError) */
+  LMGS_ERR_IO = 6           /* file open / read / write failed             */
 } lmgs_status;
 
 typedef struct lmgs_context lmgs_context;
@@ -156,6 +164,43 @@ int lmgs_composite_blocks(const float* rgb, const float* trans, const float* dep
                           int32_t n_blocks, const int32_t* order_host, int64_t n_pixels,
                           const float* background_host, float* out_rgb, float* out_alpha,
                           float* out_depth, void* stream);
+
+/* LMGS checkpoint header (data_io.py:3-9): "<4sIIQ" then count rows of
+ * row_floats f32, a grid flag byte and the optional grid block. */
+typedef struct lmgs_checkpoint_info {
+  uint32_t version;
+  uint32_t sh_degree;
+  int64_t count;
+  int32_t row_floats;          /* 11 + 3 * (sh_degree + 1)^2               */
+  int32_t has_grid;
+  int64_t data_offset;         /* byte offset of the first row             */
+  float grid_bbox[6];          /* (min xyz, max xyz) when has_grid         */
+  uint32_t grid_nx, grid_ny;
+  int64_t grid_table_offset;   /* byte offset of the nx*ny u32 table       */
+} lmgs_checkpoint_info;
+
+/* Parse and validate a checkpoint header (host only, no device work).  err
+ * (nullable, err_len bytes) receives the message on failure. */
+int lmgs_checkpoint_info_read(const char* path, lmgs_checkpoint_info* info, char* err,
+                              int err_len);
+
+/* Stream the rows into device SoA arrays sized from the header (means
+ * [count,3], quats [count,4], scales [count,3], logits [count], sh
+ * [count,(d+1)^2,3]); grid_table_host (nullable) receives the nx*ny submodel
+ * ids.  Returns after the data is on the device. */
+int lmgs_checkpoint_load(const char* path, float* means, float* quats, float* scales,
+                         float* logits, float* sh, uint32_t* grid_table_host, void* stream,
+                         char* err, int err_len);
+
+/* Write device SoA Gaussians as an LMGS file (temp file, then rename);
+ * grid (nullable or has_grid = 0: no grid block) with its host table. */
+int lmgs_checkpoint_save(const char* path, const lmgs_gaussians* g,
+                         const lmgs_checkpoint_info* grid, const uint32_t* grid_table_host,
+                         void* stream, char* err, int err_len);
+
+/* out[i] = round_half_even(clip(rgb[i], 0, 1) * 255) for n_values floats
+ * (device pointers; the wire frame's pixel bytes). */
+int lmgs_encode_rgb8(const float* rgb, int64_t n_values, uint8_t* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -22,14 +22,16 @@ I32 = ctypes.c_int32
 I64 = ctypes.c_int64
 U32 = ctypes.c_uint32
 
-LMGS_OK, LMGS_ERR_INVALID, LMGS_ERR_CUDA, LMGS_ERR_OOM, LMGS_ERR_UNSUPPORTED = range(5)
+(LMGS_OK, LMGS_ERR_INVALID, LMGS_ERR_CUDA, LMGS_ERR_OOM, LMGS_ERR_UNSUPPORTED, LMGS_ERR_FORMAT,
+ LMGS_ERR_IO) = range(7)
 LMGS_FLAG_STAGE_TIMES = 1
 MAX_STAGES = 8
 
 # every symbol include/lmgs.h declares
 EXPORTS = ("lmgs_abi_version", "lmgs_context_create", "lmgs_context_destroy", "lmgs_last_error",
            "lmgs_render", "lmgs_render_batch", "lmgs_get_stats", "lmgs_copy_instances",
-           "lmgs_project", "lmgs_composite_blocks")
+           "lmgs_project", "lmgs_composite_blocks", "lmgs_checkpoint_info_read",
+           "lmgs_checkpoint_load", "lmgs_checkpoint_save", "lmgs_encode_rgb8")
 
 
 class Camera(ctypes.Structure):
@@ -60,6 +62,12 @@ class Stats(ctypes.Structure):
                 ("stage_ms", F * MAX_STAGES), ("stage_names", ctypes.c_char_p * MAX_STAGES)]
 
 
+class CheckpointInfo(ctypes.Structure):
+    _fields_ = [("version", U32), ("sh_degree", U32), ("count", I64), ("row_floats", I32),
+                ("has_grid", I32), ("data_offset", I64), ("grid_bbox", F * 6),
+                ("grid_nx", U32), ("grid_ny", U32), ("grid_table_offset", I64)]
+
+
 _lib = None
 
 
@@ -86,6 +94,12 @@ def lib():
     L.lmgs_project.argtypes = [P, ctypes.POINTER(Gaussians), ctypes.POINTER(Camera),
                                ctypes.POINTER(Settings), P, P, P, P, P, P, P, P]
     L.lmgs_composite_blocks.argtypes = [P, P, P, I32, P, I64, P, P, P, P, P]
+    L.lmgs_checkpoint_info_read.argtypes = [ctypes.c_char_p, ctypes.POINTER(CheckpointInfo), P,
+                                            ctypes.c_int]
+    L.lmgs_checkpoint_load.argtypes = [ctypes.c_char_p, P, P, P, P, P, P, P, P, ctypes.c_int]
+    L.lmgs_checkpoint_save.argtypes = [ctypes.c_char_p, ctypes.POINTER(Gaussians),
+                                       ctypes.POINTER(CheckpointInfo), P, P, P, ctypes.c_int]
+    L.lmgs_encode_rgb8.argtypes = [P, I64, P, P]
     got = L.lmgs_abi_version()
     if got != ABI_VERSION:
         raise LmgsError(f"liblmgs ABI {got} != expected {ABI_VERSION}")
