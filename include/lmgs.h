@@ -23,6 +23,8 @@
  *                          data_io.py:256-316 load_gaussian_checkpoint /
  *                          save_gaussian_checkpoint (LMGS format), into / from
  *                          device SoA arrays
+ *   lmgs_backward          gaussian_core.py:438-486 backward_render (+ the chain
+ *                          of render_loss_and_grads 600-629 to SH and logits)
  *   lmgs_encode_rgb8       render_runtime.py:397-401 encode_frame's pixels
  *                          (round(clip(rgb, 0, 1) * 255), half to even)
  *
@@ -42,7 +44,7 @@
 extern "C" {
 #endif
 
-#define LMGS_ABI_VERSION 2
+#define LMGS_ABI_VERSION 3
 
 typedef enum lmgs_status {
   LMGS_OK = 0,
@@ -87,7 +89,7 @@ typedef struct lmgs_gaussians {
 typedef struct lmgs_settings {
   int32_t tile_size;       /* >= 1, <= 64 (reference default 16)             */
   int32_t sh_eval_degree;  /* 1 = reference eval_sh_colors; 3 = full degree 3 */
-  float background[3];
+  double background[3];  /* fp64 like the reference (common.py DTYPE) */
   uint32_t flags;          /* LMGS_FLAG_*                                    */
 } lmgs_settings;
 
@@ -146,6 +148,19 @@ int lmgs_get_stats(lmgs_context* ctx, lmgs_stats* out);
  * then by (fp64 depth, prim id).  Either pointer may be NULL.  Device buffers,
  * K entries. */
 int lmgs_copy_instances(lmgs_context* ctx, uint64_t* keys, int64_t* prim_ids, void* stream);
+
+/* Backward of the blend for the view last rendered on ctx (same Gaussians,
+ * camera and settings; tile_size <= 32): backward_render (gaussian_core.py:
+ * 438-486) in fp64 with the reference's semantics — d_colors [count,3],
+ * d_opacities [count], d_mean2d [count,2], touched [count] (zeroed, rows of
+ * non-rendered Gaussians stay 0) — and, when non-NULL, the chain rule of
+ * render_loss_and_grads (600-629): d_sh [count,sh_coeffs,3] and d_logits
+ * [count] are ACCUMULATED (+=) so several views can be summed.  image_grad is
+ * the loss gradient w.r.t. the [H,W,3] image (fp32, device). */
+int lmgs_backward(lmgs_context* ctx, const lmgs_gaussians* g, const lmgs_camera* cam,
+                  const lmgs_settings* s, const float* image_grad, double* d_colors,
+                  double* d_opacities, double* d_mean2d, int32_t* touched, double* d_sh,
+                  double* d_logits, void* stream);
 
 /* Stage K1 alone (project_splats): per input Gaussian, fp64 geometry.
  * mean2d [count,2], cov2d [count,3] = (c00,c01,c11) incl. the 0.3 floor,

@@ -13,7 +13,7 @@ from pathlib import Path
 from .errors import InvalidInputError, LmgsError, ShapeError
 
 LIB_PATH = Path(__file__).resolve().parent / "liblmgs.so"
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 P = ctypes.c_void_p
 D = ctypes.c_double
@@ -31,7 +31,8 @@ MAX_STAGES = 8
 EXPORTS = ("lmgs_abi_version", "lmgs_context_create", "lmgs_context_destroy", "lmgs_last_error",
            "lmgs_render", "lmgs_render_batch", "lmgs_get_stats", "lmgs_copy_instances",
            "lmgs_project", "lmgs_composite_blocks", "lmgs_checkpoint_info_read",
-           "lmgs_checkpoint_load", "lmgs_checkpoint_save", "lmgs_encode_rgb8")
+           "lmgs_checkpoint_load", "lmgs_checkpoint_save", "lmgs_encode_rgb8",
+           "lmgs_backward")
 
 
 class Camera(ctypes.Structure):
@@ -46,7 +47,7 @@ class Gaussians(ctypes.Structure):
 
 
 class Settings(ctypes.Structure):
-    _fields_ = [("tile_size", I32), ("sh_eval_degree", I32), ("background", F * 3),
+    _fields_ = [("tile_size", I32), ("sh_eval_degree", I32), ("background", D * 3),
                 ("flags", U32)]
 
 
@@ -100,6 +101,8 @@ def lib():
     L.lmgs_checkpoint_save.argtypes = [ctypes.c_char_p, ctypes.POINTER(Gaussians),
                                        ctypes.POINTER(CheckpointInfo), P, P, P, ctypes.c_int]
     L.lmgs_encode_rgb8.argtypes = [P, I64, P, P]
+    L.lmgs_backward.argtypes = [P, ctypes.POINTER(Gaussians), ctypes.POINTER(Camera),
+                                ctypes.POINTER(Settings), P, P, P, P, P, P, P, P]
     got = L.lmgs_abi_version()
     if got != ABI_VERSION:
         raise LmgsError(f"liblmgs ABI {got} != expected {ABI_VERSION}")

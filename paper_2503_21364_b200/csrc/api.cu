@@ -414,7 +414,7 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
   ba.tile_size = st->tile_size;
   ba.tiles_x = ca.tiles_x;
   ba.tiles_y = ca.tiles_y;
-  for (int i = 0; i < 3; ++i) ba.bg[i] = st->background[i];
+  for (int i = 0; i < 3; ++i) ba.bg[i] = (float)st->background[i];
   ba.rgb = out->rgb;
   ba.alpha = out->alpha;
   ba.depth = out->depth;
@@ -527,6 +527,56 @@ int lmgs_copy_instances(lmgs_context* c, uint64_t* keys, int64_t* prim_ids, void
   a.prims_out = prim_ids;
   a.k = c->stats.n_instances;
   launch_export_instances(a, static_cast<cudaStream_t>(stream));
+  LMGS_CUDA(c, cudaGetLastError());
+  return LMGS_OK;
+}
+
+int lmgs_backward(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
+                  const lmgs_settings* s, const float* image_grad, double* d_colors,
+                  double* d_opacities, double* d_mean2d, int32_t* touched, double* d_sh,
+                  double* d_logits, void* stream) {
+  if (int r = validate(c, g, cam, s)) return r;
+  if (!image_grad || !d_colors || !d_opacities || !d_mean2d || !touched)
+    return fail(c, LMGS_ERR_INVALID, "null backward output");
+  if (s->tile_size > 32) return fail(c, LMGS_ERR_UNSUPPORTED, "backward supports tile_size <= 32");
+  const CamArgs ca = make_cam(cam, s->tile_size);
+  const int64_t tiles = (int64_t)ca.tiles_x * ca.tiles_y;
+  if (c->stats.n_gaussians != g->count || c->stats.n_tiles != tiles || !c->last_ranges)
+    return fail(c, LMGS_ERR_INVALID, "lmgs_backward needs the view's lmgs_render first");
+  DeviceGuard guard(c->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t n = g->count;
+  if (n > 0) {
+    LMGS_CUDA(c, cudaMemsetAsync(d_colors, 0, sizeof(double) * 3 * n, st));
+    LMGS_CUDA(c, cudaMemsetAsync(d_opacities, 0, sizeof(double) * n, st));
+    LMGS_CUDA(c, cudaMemsetAsync(d_mean2d, 0, sizeof(double) * 2 * n, st));
+    LMGS_CUDA(c, cudaMemsetAsync(touched, 0, sizeof(int32_t) * n, st));
+  }
+  BackwardArgs a{};
+  a.means = g->means;
+  a.quats = g->quats;
+  a.scales = g->scales;
+  a.logits = g->opacity_logits;
+  a.sh = g->sh;
+  a.n = n;
+  a.sh_coeffs = g->sh_coeffs;
+  a.eval_degree = s->sh_eval_degree < g->sh_degree ? s->sh_eval_degree : g->sh_degree;
+  a.cam = ca;
+  a.keys_slot = &c->d_scal->slots.inst_keys;
+  a.ranges = c->last_ranges;
+  a.width = cam->width;
+  a.height = cam->height;
+  a.tile_size = s->tile_size;
+  a.tiles_x = ca.tiles_x;
+  for (int i = 0; i < 3; ++i) a.bg[i] = s->background[i];
+  a.image_grad = image_grad;
+  a.d_colors = d_colors;
+  a.d_opacities = d_opacities;
+  a.d_mean2d = d_mean2d;
+  a.touched = touched;
+  a.d_sh = d_sh;
+  a.d_logits = d_logits;
+  if (c->stats.n_instances > 0 || d_sh || d_logits) launch_backward(a, (int)tiles, st);
   LMGS_CUDA(c, cudaGetLastError());
   return LMGS_OK;
 }

@@ -213,6 +213,32 @@ int launch_blend(const BlendArgs& a, cudaStream_t s);  // returns 0 or LMGS_ERR_
 void launch_fill_background(float* rgb, float* alpha, float* depth, float* trans, int64_t n_pix,
                             const float bg[3], cudaStream_t s);
 
+// Backward of the blend + chain to SH / logits (backward.cu), over the tile
+// lists of the preceding render of the same view on the same context.
+struct BackwardArgs {
+  const float* means;
+  const float* quats;
+  const float* scales;
+  const float* logits;
+  const float* sh;
+  int64_t n;
+  int32_t sh_coeffs;
+  int32_t eval_degree;
+  CamArgs cam;
+  void* const* keys_slot;
+  const int2* ranges;
+  int32_t width, height, tile_size, tiles_x;
+  double bg[3];
+  const float* image_grad;  // [H,W,3]
+  double* d_colors;         // [n,3]  (zeroed per view)
+  double* d_opacities;      // [n]
+  double* d_mean2d;         // [n,2]
+  int32_t* touched;         // [n]
+  double* d_sh;             // [n,coeffs,3] accumulated (nullable)
+  double* d_logits;         // [n] accumulated (nullable)
+};
+int launch_backward(const BackwardArgs& a, int tiles, cudaStream_t s);  // kernels launched or -err
+
 constexpr int kMaxCompositeBlocks = 64;
 // `order` is a host array (n_blocks <= kMaxCompositeBlocks), passed by value.
 void launch_composite(const float* rgb, const float* trans, const float* depth, int n_blocks,

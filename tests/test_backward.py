@@ -1,0 +1,135 @@
+"""Backward of the blend and the training-loss chain against
+the unmodified reference (tests/golden/backward/make_backward_golden.py):
+
+* ``backward_render`` (gaussian_core.py:438-486) of a seeded random image
+  gradient: d_colors, d_opacities, d_mean2d per Gaussian, touched counts;
+* ``render_loss_and_grads`` (600-629): loss, d_sh, d_opacity_logits and the
+  DensifyStats increments over two cameras.
+
+Both sides compute in fp64 from the same fp64 geometry (K1's projection is
+bit-exact), so the tolerance is set by summation order (per-pixel terms are
+accumulated with atomics here, in tile/pixel order there) and the 1-ulp exp
+differences between libdevice and the host libm: rtol 1e-9 on sums with an
+absolute floor of 1e-9 x the array's largest magnitude.  The loss path feeds
+the forward's fp32 image (rgb tolerance 1e-4, test_gpu_pipeline) into the
+gradient, so it is checked at rtol 1e-4 of each array's scale.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+BW = GOLDEN / "backward"
+CASES = ["ts16", "ts8_bg", "ts32"]
+
+
+def _load(name):
+    from paper_2503_21364_b200 import scenes
+    from paper_2503_21364_b200.camera import Camera
+
+    z = np.load(BW / name)
+
+    def cam(sfx=""):
+        return Camera(float(z["cam_fx" + sfx]), float(z["cam_fy" + sfx]), float(z["cam_cx" + sfx]),
+                      float(z["cam_cy" + sfx]), int(z["cam_w" + sfx]), int(z["cam_h" + sfx]),
+                      z["cam_r" + sfx], z["cam_t" + sfx])
+
+    g = scenes.HostGaussians(z["means"], z["quats"], z["scales"], z["opacity_logits"], z["sh"],
+                             int(z["sh_degree"]))
+    return z, g, cam
+
+
+def _close(got, ref, rtol, what):
+    scale = max(float(np.abs(ref).max()), 1e-300)
+    np.testing.assert_allclose(got, ref, rtol=rtol, atol=rtol * scale, err_msg=what)
+
+
+def test_golden_fixtures_consistent():
+    """CPU: the fixtures hold what the tests read (every kept splat touched
+    something in these scenes, gradients finite)."""
+    for c in CASES:
+        z = np.load(BW / f"backward_{c}.npz")
+        n = z["means"].shape[0]
+        assert z["d_colors"].shape == (n, 3) and z["d_mean2d"].shape == (n, 2)
+        assert np.isfinite(z["d_colors"]).all() and np.isfinite(z["d_opacities"]).all()
+        assert (z["touched"] > 0).sum() > n // 2
+    z = np.load(BW / "loss_grads.npz")
+    assert z["d_sh"].shape == z["sh"].shape and 0 < float(z["loss"]) < 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", CASES)
+def test_backward_render_matches_reference(case):
+    import torch
+
+    from paper_2503_21364_b200 import GaussianModel
+    from paper_2503_21364_b200.train import backward_render
+
+    z, g, cam = _load(f"backward_{case}.npz")
+    model = GaussianModel.from_host(g)
+    bg = tuple(float(v) for v in z["background"])
+    fwd, gr = backward_render(model, cam(), torch.as_tensor(z["image_grad"]).cuda(),
+                              int(z["tile_size"]), bg)
+    np.testing.assert_allclose(fwd.rgb.cpu().numpy(), z["image"], atol=1e-4)
+    tch = gr.touched.cpu().numpy().astype(np.int64)
+    # touched is a count of w > 0 tests in fp64 on both sides
+    assert int(np.abs(tch - z["touched"]).sum()) <= 2, case
+    _close(gr.d_colors.cpu().numpy(), z["d_colors"], 1e-9, "d_colors")
+    _close(gr.d_opacities.cpu().numpy(), z["d_opacities"], 1e-9, "d_opacities")
+    _close(gr.d_mean2d.cpu().numpy(), z["d_mean2d"], 1e-9, "d_mean2d")
+
+
+@pytest.mark.gpu
+def test_backward_is_linear_in_image_grad():
+    """Size-independent property: grads(a*g1 + g2) = a*grads(g1) + grads(g2)."""
+    import torch
+
+    from paper_2503_21364_b200 import GaussianModel, scenes
+    from paper_2503_21364_b200.train import backward_render
+
+    g = scenes.synthetic_gaussians(20_000, seed=5, sh_degree=1)
+    model = GaussianModel.from_host(g)
+    cam = scenes.orbit_cameras(1, 320, 240, seed=5)[0]
+    gen = torch.Generator().manual_seed(0)
+    # dyadic gradients so that 0.5*g1 + g2 is exact in the fp32 input
+    g1 = torch.randint(-1024, 1025, (240, 320, 3), generator=gen).float() / 1024
+    g2 = torch.randint(-1024, 1025, (240, 320, 3), generator=gen).float() / 1024
+    _, a = backward_render(model, cam, g1.cuda())
+    _, b = backward_render(model, cam, g2.cuda())
+    _, c = backward_render(model, cam, (0.5 * g1 + g2).cuda())
+    for f in ("d_colors", "d_opacities", "d_mean2d"):
+        want = 0.5 * getattr(a, f) + getattr(b, f)
+        _close(getattr(c, f).cpu().numpy(), want.cpu().numpy(), 1e-9, f)
+    assert bool((a.touched == c.touched).all())
+
+
+@pytest.mark.gpu
+def test_render_loss_and_grads_matches_reference():
+    from paper_2503_21364_b200 import GaussianModel
+    from paper_2503_21364_b200.train import render_loss_and_grads
+
+    z, g, cam = _load("loss_grads.npz")
+    model = GaussianModel.from_host(g)
+    cams = [cam("_0"), cam("_1")]
+    loss, grads, stats = render_loss_and_grads(model, cams, [z["gt0"], z["gt1"]],
+                                               int(z["tile_size"]))
+    assert abs(loss - float(z["loss"])) <= 1e-6 * float(z["loss"])
+    _close(grads["sh"].cpu().numpy(), z["d_sh"], 1e-4, "d_sh")
+    _close(grads["opacity_logits"].cpu().numpy(), z["d_logits"], 1e-4, "d_logits")
+    np.testing.assert_array_equal(stats.steps_seen.cpu().numpy(), z["steps_seen"])
+    _close(stats.grad_norm_sum.cpu().numpy(), z["grad_norm_sum"], 1e-4, "grad_norm_sum")
+
+
+@pytest.mark.gpu
+def test_backward_rejects_mismatched_shapes():
+    import torch
+
+    from paper_2503_21364_b200 import GaussianModel, scenes
+    from paper_2503_21364_b200.errors import ShapeError
+    from paper_2503_21364_b200.train import backward_render
+
+    g = scenes.synthetic_gaussians(100, seed=1, sh_degree=1)
+    cam = scenes.orbit_cameras(1, 64, 48, seed=1)[0]
+    with pytest.raises(ShapeError):
+        backward_render(GaussianModel.from_host(g), cam, torch.zeros(48, 63, 3).cuda())
