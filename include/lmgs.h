@@ -89,7 +89,7 @@ typedef struct lmgs_gaussians {
 typedef struct lmgs_settings {
   int32_t tile_size;       /* >= 1, <= 64 (reference default 16)             */
   int32_t sh_eval_degree;  /* 1 = reference eval_sh_colors; 3 = full degree 3 */
-  double background[3];  /* fp64 like the reference (common.py DTYPE) */
+  double background[3];   /* fp64 like the reference (common.py DTYPE)     */
   uint32_t flags;          /* LMGS_FLAG_*                                    */
 } lmgs_settings;
 
