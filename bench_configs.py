@@ -5,6 +5,9 @@
 One JSON line per configuration (BASELINE.json `configs`):
   c2  1M Gaussians, 1920x1080, single view (16 orbit views timed back to back)
   c4  6M Gaussians, 3840x2160, single view (8 orbit views timed back to back)
+  bw  training step: render_loss_and_grads over 4 views of
+      the c2 scene (1M Gaussians, 1080p): forward, fp64 backward of the blend,
+      chain to SH/logits; the backward kernel alone is timed too
   c5  50M-Gaussian city in 8 spatial blocks (6.25M each), 1080p: every block
       rendered with background 0 into (premultiplied RGB, T, depth) layers and
       composited front to back in block order (the single-GPU run of the block
@@ -61,6 +64,31 @@ def batch_config(name: str, n: int, w: int, h: int, views: int, steps: int) -> d
             "processed_per_frame": st["per_frame"]["processed"],
             "stage_gbs": {k: st["alg_bytes"][k] / (per[k] / 1e3) / 1e9 for k in per if per[k]},
             "host_generate_s": gen_s}
+
+
+def train_config(n: int, w: int, h: int, views: int, steps: int) -> dict:
+    from paper_2503_21364_b200.raster import context
+    from paper_2503_21364_b200.train import _backward, render_loss_and_grads
+
+    g = scenes.synthetic_gaussians(n, seed=0)
+    model = GaussianModel.from_host(g, validate=False)
+    cams = scenes.orbit_cameras(views, w, h, seed=0)
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    gts = [torch.rand((h, w, 3), generator=gen, device="cuda", dtype=torch.float64)
+           for _ in cams]
+    ms_step = _events_ms(lambda: render_loss_and_grads(model, cams, gts), steps, 1)
+    ctx = context(0)
+    fwd = render(cams[0], model, 16, (0.0, 0.0, 0.0), 1, ctx=ctx)
+    gimg = torch.randn((h, w, 3), generator=gen, device="cuda")
+    ms_fwd = _events_ms(lambda: render(cams[0], model, 16, (0.0, 0.0, 0.0), 1, ctx=ctx),
+                        steps, 1)
+    render(cams[0], model, 16, (0.0, 0.0, 0.0), 1, ctx=ctx)
+    ms_bwd = _events_ms(lambda: _backward(ctx, model, cams[0], gimg, 16, (0.0, 0.0, 0.0), 1),
+                        steps, 1)
+    return {"config": "bw", "gaussians": n, "width": w, "height": h, "views": views,
+            "train_views_per_s": views / (ms_step / 1e3), "ms_per_view_train": ms_step / views,
+            "ms_forward_view0": ms_fwd, "ms_backward_view0": ms_bwd,
+            "instances_view0": fwd.n_instances}
 
 
 def city_config(per_block: int, steps: int) -> dict:
@@ -139,6 +167,8 @@ def main():
             line = batch_config("c2", 1_000_000, 1920, 1080, 16, a.steps)
         elif c == "c4":
             line = batch_config("c4", 6_000_000, 3840, 2160, 8, a.steps)
+        elif c == "bw":
+            line = train_config(1_000_000, 1920, 1080, 4, a.steps)
         elif c == "c5":
             line = city_config(6_250_000, a.steps)
         else:

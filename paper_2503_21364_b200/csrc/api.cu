@@ -103,7 +103,7 @@ struct lmgs_context {
   int device = 0;
   int sms = 148;
   std::string err;
-  DevBuf gbuf, tbuf, ibuf;
+  DevBuf gbuf, tbuf, ibuf, bwbuf;
   Scalars* d_scal = nullptr;
   uint64_t* h_pinned = nullptr;  // [0..2] = n_kept, n_vis, K
   cudaEvent_t ev[2 * kNumStages] = {};
@@ -472,6 +472,7 @@ void lmgs_context_destroy(lmgs_context* c) {
   c->gbuf.release();
   c->tbuf.release();
   c->ibuf.release();
+  c->bwbuf.release();
   if (c->d_scal) cudaFree(c->d_scal);
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   for (int i = 0; i < 2 * kNumStages; ++i)
@@ -538,7 +539,6 @@ int lmgs_backward(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* c
   if (int r = validate(c, g, cam, s)) return r;
   if (!image_grad || !d_colors || !d_opacities || !d_mean2d || !touched)
     return fail(c, LMGS_ERR_INVALID, "null backward output");
-  if (s->tile_size > 32) return fail(c, LMGS_ERR_UNSUPPORTED, "backward supports tile_size <= 32");
   const CamArgs ca = make_cam(cam, s->tile_size);
   const int64_t tiles = (int64_t)ca.tiles_x * ca.tiles_y;
   if (c->stats.n_gaussians != g->count || c->stats.n_tiles != tiles || !c->last_ranges)
@@ -552,7 +552,15 @@ int lmgs_backward(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* c
     LMGS_CUDA(c, cudaMemsetAsync(d_mean2d, 0, sizeof(double) * 2 * n, st));
     LMGS_CUDA(c, cudaMemsetAsync(touched, 0, sizeof(int32_t) * n, st));
   }
+  if ((size_t)n * sizeof(BwRec) > c->bwbuf.bytes) {
+    LMGS_CUDA(c, cudaStreamSynchronize(st));  // an earlier backward may still read it
+    LMGS_CUDA(c, c->bwbuf.reserve((size_t)(n > 0 ? n : 1) * sizeof(BwRec)));
+  }
   BackwardArgs a{};
+  a.recs = static_cast<BwRec*>(c->bwbuf.ptr);
+  a.region = s->tile_size < 16 ? s->tile_size : 16;
+  a.regions_x = (s->tile_size + a.region - 1) / a.region;
+  a.regions = a.regions_x * a.regions_x;
   a.means = g->means;
   a.quats = g->quats;
   a.scales = g->scales;

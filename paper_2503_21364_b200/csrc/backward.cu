@@ -6,19 +6,26 @@
 // (geometry.cuh) so conic, opacity, mean and radius are bit-identical to the
 // reference's, and colours are re-evaluated in fp64 (eval_sh_colors, 129-142).
 //
-// Per tile (one CTA, pixel state in shared memory), over the tile list of the
-// preceding render on the same context:
+// k_bw_prep computes each Gaussian's fp64 splat (mean, conic, opacity,
+// radius^2, clamped colour) once per view.  k_backward then replays each
+// tile's list of the preceding render on the same context, one CTA per 16x16
+// region of a tile, one warp per 8x4 pixel block, one pixel per lane:
 //   pass A  the forward blend in fp64 -> every pixel's total colour C_tot
 //           (including T_final * background);
 //   pass B  the forward blend again; at each applied step the reference's
 //           reverse-mode quantities: w = T_before sigma, suffix = C_tot - sum
 //           of w c up to and including this step (the reference accumulates
 //           the same suffix back to front), d_sigma = g . (c T_before -
-//           suffix / max(1 - sigma, 1e-6)); per-splat sums of g w, d_sigma
-//           sigma / alpha, d_sigma sigma (conic @ (pix - mean)) and w > 0 are
-//           gathered in shared fp64 and flushed with one atomic per splat.
+//           suffix / max(1 - sigma, 1e-6)); the six per-splat sums (g w,
+//           d_sigma sigma / alpha, d_sigma sigma (conic @ (pix - mean))) are
+//           reduced across the warp with 8 fp64 shuffles, gathered per CTA in
+//           shared memory and flushed with one global atomic per splat/value;
+//           touched = popc(ballot(w > 0)).
 // A pixel stops when its T < TERM_EPS (later steps have sigma = 0: no
-// contribution), a tile when all its pixels have.
+// contribution), a region when all its pixels have.  Splats whose circle
+// misses the box of a warp's live pixels are skipped (exact).
+#include <climits>
+
 #include "device_util.cuh"
 #include "geometry.cuh"
 #include "lmgs_internal.cuh"
@@ -26,7 +33,7 @@
 namespace lmgs {
 namespace {
 
-constexpr int kBwThreads = 256;
+constexpr int kBwThreads = 256;  // 16x16 region = 8 warps of 8x4 pixels
 constexpr int kBwBatch = 64;
 __constant__ double kShC2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
                                 -1.0925484305920792, 0.5462742152960396};
@@ -85,145 +92,198 @@ __device__ __forceinline__ void sh_raw(const float* sh, int deg, double x, doubl
   }
 }
 
+// Per-Gaussian fp64 splat record of this view, computed once (K1's code):
+// mean, conic, opacity, radius^2, clamped colour.
+__global__ void k_bw_prep(BackwardArgs a) {
+  const CamArgs& cam = a.cam;
+  for (int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; id < a.n;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const double m0 = a.means[3 * id], m1 = a.means[3 * id + 1], m2 = a.means[3 * id + 2];
+    const double x = mkl_dot3(m0, cam.r[0], m1, cam.r[1], m2, cam.r[2]) + cam.t[0];
+    const double y = mkl_dot3(m0, cam.r[3], m1, cam.r[4], m2, cam.r[5]) + cam.t[1];
+    const double z = mkl_dot3(m0, cam.r[6], m1, cam.r[7], m2, cam.r[8]) + cam.t[2];
+    const float4 q = reinterpret_cast<const float4*>(a.quats)[id];
+    double mx, my, ca, cb, cc, radius;
+    splat_geometry(cam, x, y, z, q, a.scales[3 * id], a.scales[3 * id + 1], a.scales[3 * id + 2],
+                   &mx, &my, &ca, &cb, &cc, &radius);
+    const double det = ca * cc - cb * cb;  // _blend 308-310
+    BwRec r;
+    r.mx = mx;
+    r.my = my;
+    r.ca = cc / det;
+    r.cb = -cb / det;
+    r.cc = ca / det;
+    r.op = 1.0 / (1.0 + exp(-(double)a.logits[id]));  // opacities (67-69)
+    r.r2 = radius * radius;
+    double dx, dy, dz, raw[3];
+    view_dir(cam, m0, m1, m2, &dx, &dy, &dz);
+    sh_raw(a.sh + id * a.sh_coeffs * 3, a.eval_degree, dx, dy, dz, raw);
+    r.col[0] = fmin(fmax(raw[0], 0.0), 1.0);
+    r.col[1] = fmin(fmax(raw[1], 0.0), 1.0);
+    r.col[2] = fmin(fmax(raw[2], 0.0), 1.0);
+    a.recs[id] = r;
+  }
+}
+
+// Sum six per-lane values over the warp with 8 fp64 shuffles (a transpose
+// reduction: each exchange halves what a lane carries).  Returns the full sum
+// of value idx(lane) in lanes with owner(lane); see bw_owner.
+__device__ __forceinline__ double warp_sum6(const double v[6], int lane) {
+  const bool h = lane & 16, b = lane & 8, c = lane & 4;
+  double a0 = (h ? v[3] : v[0]) + __shfl_xor_sync(~0u, h ? v[0] : v[3], 16);
+  double a1 = (h ? v[4] : v[1]) + __shfl_xor_sync(~0u, h ? v[1] : v[4], 16);
+  double a2 = (h ? v[5] : v[2]) + __shfl_xor_sync(~0u, h ? v[2] : v[5], 16);
+  a2 = a2 + __shfl_xor_sync(~0u, a2, 8);
+  const double k = (b ? a1 : a0) + __shfl_xor_sync(~0u, b ? a0 : a1, 8);
+  double m = (c ? a2 : k) + __shfl_xor_sync(~0u, c ? k : a2, 4);
+  m = m + __shfl_xor_sync(~0u, m, 2);
+  m = m + __shfl_xor_sync(~0u, m, 1);
+  return m;
+}
+// lanes 0,8,4,16,24,20 hold values 0..5
+__device__ __forceinline__ int bw_owner(int lane) {
+  if (lane & 3) return -1;
+  const int base = (lane & 16) ? 3 : 0;
+  if (lane & 4) return (lane & 8) ? -1 : base + 2;
+  return base + ((lane & 8) ? 1 : 0);
+}
+
+// One CTA per (tile, 16x16 region of it); one warp per 8x4 pixel block, one
+// pixel per lane, pixel state in registers.  Splats are staged per CTA batch
+// in shared memory; each warp skips splats whose circle misses the bounding
+// box of its still-active pixels (exact: sigma is 0 outside the circle at
+// every pixel centre, and fp64 rounding is monotone).
 __global__ void __launch_bounds__(kBwThreads) k_backward(BackwardArgs a) {
-  extern __shared__ __align__(16) double s_px[];  // [7][np]: T, C0-2, Ctot0-2
-  __shared__ double s_mx[kBwBatch], s_my[kBwBatch], s_ca[kBwBatch], s_cb[kBwBatch],
-      s_cc[kBwBatch], s_op[kBwBatch], s_r2[kBwBatch], s_z[kBwBatch], s_col[kBwBatch][3];
+  __shared__ BwRec s_rec[kBwBatch];
+  __shared__ uint32_t s_id[kBwBatch];
   __shared__ double s_acc[kBwBatch][6];  // d_colors 3, d_opacity, d_mean 2
   __shared__ int s_touch[kBwBatch];
-  __shared__ uint32_t s_id[kBwBatch];
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ts = a.tile_size;
-  const int tile = blockIdx.x;
-  const int x0 = (tile % a.tiles_x) * ts, y0 = (tile / a.tiles_x) * ts;
-  const int tw = min(ts, a.width - x0), th = min(ts, a.height - y0);
-  const int np = tw * th;
-  double* sT = s_px;
-  double* sC = sT + np;           // [3][np] running colour
-  double* sTot = sC + 3 * np;     // [3][np] total colour
+  const int tile = blockIdx.x / a.regions, reg = blockIdx.x % a.regions;
+  const int rx = reg % a.regions_x, ry = reg / a.regions_x;
+  const int rs = a.region;  // region side (<= 16)
+  const int tx0 = (tile % a.tiles_x) * ts, ty0 = (tile / a.tiles_x) * ts;
+  const int tx1 = min(tx0 + ts, a.width), ty1 = min(ty0 + ts, a.height);
+  const int x0 = tx0 + rx * rs, y0 = ty0 + ry * rs;
+  const int x1 = min(x0 + rs, tx1), y1 = min(y0 + rs, ty1);
   const int2 range = a.ranges[tile];
-  if (range.y <= range.x) return;
+  if (range.y <= range.x || x0 >= x1 || y0 >= y1) return;
+  const int bw = (x1 - x0 + 7) >> 3;  // 8x4 blocks across the region
+  const int px = x0 + (warp % bw) * 8 + (lane & 7);
+  const int py = y0 + (warp / bw) * 4 + (lane >> 3);
+  const bool in_img = warp < bw * ((y1 - y0 + 3) >> 2) && px < x1 && py < y1;
+  const double pxd = (double)px + 0.5, pyd = (double)py + 0.5;
   const uint64_t* __restrict__ list = static_cast<const uint64_t*>(*a.keys_slot);
-  const CamArgs& cam = a.cam;
-  const int ncoef = a.sh_coeffs;
+  const int own = bw_owner(lane);
 
+  double g0 = 0.0, g1 = 0.0, g2 = 0.0, t0 = 0.0, t1 = 0.0, t2 = 0.0;
+  if (in_img) {
+    const int64_t o = (int64_t)py * a.width + px;
+    g0 = (double)a.image_grad[3 * o + 0];
+    g1 = (double)a.image_grad[3 * o + 1];
+    g2 = (double)a.image_grad[3 * o + 2];
+  }
   for (int pass = 0; pass < 2; ++pass) {
-    for (int p = tid; p < np; p += kBwThreads) {
-      sT[p] = 1.0;
-      sC[p] = sC[np + p] = sC[2 * np + p] = 0.0;
-    }
-    __syncthreads();
+    double T = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
+    bool live = in_img;
     for (int b0 = range.x; b0 < range.y; b0 += kBwBatch) {
       const int nb = min(kBwBatch, range.y - b0);
-      for (int j = tid; j < nb; j += kBwThreads) {  // re-project in fp64 (K1's code)
+      for (int j = tid; j < nb; j += blockDim.x) {
         const uint32_t id = (uint32_t)list[b0 + j];
-        const double m0 = a.means[3 * (size_t)id], m1 = a.means[3 * (size_t)id + 1],
-                     m2 = a.means[3 * (size_t)id + 2];
-        const double x = mkl_dot3(m0, cam.r[0], m1, cam.r[1], m2, cam.r[2]) + cam.t[0];
-        const double y = mkl_dot3(m0, cam.r[3], m1, cam.r[4], m2, cam.r[5]) + cam.t[1];
-        const double z = mkl_dot3(m0, cam.r[6], m1, cam.r[7], m2, cam.r[8]) + cam.t[2];
-        const float4 q = reinterpret_cast<const float4*>(a.quats)[id];
-        double mx, my, ca, cb, cc, radius;
-        splat_geometry(cam, x, y, z, q, a.scales[3 * (size_t)id], a.scales[3 * (size_t)id + 1],
-                       a.scales[3 * (size_t)id + 2], &mx, &my, &ca, &cb, &cc, &radius);
-        const double det = ca * cc - cb * cb;  // _blend 308-310
-        s_ca[j] = cc / det;
-        s_cb[j] = -cb / det;
-        s_cc[j] = ca / det;
-        s_op[j] = 1.0 / (1.0 + exp(-(double)a.logits[id]));  // opacities (67-69)
-        s_mx[j] = mx;
-        s_my[j] = my;
-        s_r2[j] = radius * radius;
-        s_z[j] = z;
-        double dx, dy, dz, raw[3];
-        view_dir(cam, m0, m1, m2, &dx, &dy, &dz);
-        sh_raw(a.sh + (size_t)id * ncoef * 3, a.eval_degree, dx, dy, dz, raw);
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) s_col[j][ch] = fmin(fmax(raw[ch], 0.0), 1.0);
         s_id[j] = id;
-#pragma unroll
-        for (int c = 0; c < 6; ++c) s_acc[j][c] = 0.0;
-        s_touch[j] = 0;
-      }
-      __syncthreads();
-      bool active = false;
-      for (int p = tid; p < np; p += kBwThreads) {
-        double T = sT[p];
-        if (!(T >= kTermEps)) continue;
-        double c0 = sC[p], c1 = sC[np + p], c2 = sC[2 * np + p];
-        const int lx = p % tw, ly = p / tw;
-        const double pxd = (double)(x0 + lx) + 0.5, pyd = (double)(y0 + ly) + 0.5;
-        double g0 = 0.0, g1 = 0.0, g2 = 0.0, t0 = 0.0, t1 = 0.0, t2 = 0.0;
+        s_rec[j] = a.recs[id];
         if (pass == 1) {
-          const int64_t o = (int64_t)(y0 + ly) * a.width + (x0 + lx);
-          g0 = (double)a.image_grad[3 * o + 0];
-          g1 = (double)a.image_grad[3 * o + 1];
-          g2 = (double)a.image_grad[3 * o + 2];
-          t0 = sTot[p];
-          t1 = sTot[np + p];
-          t2 = sTot[2 * np + p];
+#pragma unroll
+          for (int q = 0; q < 6; ++q) s_acc[j][q] = 0.0;
+          s_touch[j] = 0;
         }
-        for (int k = 0; k < nb; ++k) {
-          const double dx = pxd - s_mx[k], dy = pyd - s_my[k];  // 311
-          const double maha =
-              (s_ca[k] * (dx * dx) + ((2.0 * s_cb[k]) * dx) * dy) + s_cc[k] * (dy * dy);
-          double sig = s_op[k] * exp(-0.5 * maha);  // 313
-          const bool inside = (dx * dx + dy * dy) <= s_r2[k];  // 314 (active here)
-          sig = inside ? (sig > kSigmaMax ? kSigmaMax : sig) : 0.0;
-          const double w = T * sig;
-          c0 = c0 + w * s_col[k][0];
-          c1 = c1 + w * s_col[k][1];
-          c2 = c2 + w * s_col[k][2];
-          if (pass == 1 && sig > 0.0) {  // backward_render 461-484
-            const double s0 = t0 - c0, s1 = t1 - c1, s2 = t2 - c2;  // suffix
-            double denom = 1.0 - sig;
-            denom = denom < 1e-6 ? 1e-6 : denom;
-            const double dsig = (g0 * (s_col[k][0] * T - s0 / denom) +
-                                 g1 * (s_col[k][1] * T - s1 / denom)) +
-                                g2 * (s_col[k][2] * T - s2 / denom);
-            atomicAdd(&s_acc[k][0], g0 * w);
-            atomicAdd(&s_acc[k][1], g1 * w);
-            atomicAdd(&s_acc[k][2], g2 * w);
-            atomicAdd(&s_acc[k][3], dsig * sig / s_op[k]);
-            atomicAdd(&s_acc[k][4], dsig * (sig * (s_ca[k] * dx + s_cb[k] * dy)));
-            atomicAdd(&s_acc[k][5], dsig * (sig * (s_cb[k] * dx + s_cc[k] * dy)));
-            if (w > 0.0) atomicAdd(&s_touch[k], 1);
-          }
-          T = T * (1.0 - sig);
-          if (!(T >= kTermEps)) break;
-        }
-        sT[p] = T;
-        sC[p] = c0;
-        sC[np + p] = c1;
-        sC[2 * np + p] = c2;
-        active |= T >= kTermEps;
       }
-      const int live = __syncthreads_or(active);
-      if (pass == 1)
-        for (int j = tid; j < nb; j += kBwThreads) {
-          const uint32_t id = s_id[j];
-          if (s_touch[j] || s_acc[j][3] != 0.0 || s_acc[j][0] != 0.0 || s_acc[j][1] != 0.0 ||
-              s_acc[j][2] != 0.0) {
-            atomicAdd(a.d_colors + 3 * (size_t)id + 0, s_acc[j][0]);
-            atomicAdd(a.d_colors + 3 * (size_t)id + 1, s_acc[j][1]);
-            atomicAdd(a.d_colors + 3 * (size_t)id + 2, s_acc[j][2]);
-            atomicAdd(a.d_opacities + id, s_acc[j][3]);
-            atomicAdd(a.d_mean2d + 2 * (size_t)id + 0, s_acc[j][4]);
-            atomicAdd(a.d_mean2d + 2 * (size_t)id + 1, s_acc[j][5]);
-            if (s_touch[j]) atomicAdd(a.touched + id, s_touch[j]);
+      __syncthreads();
+      const unsigned lm = __ballot_sync(~0u, live);
+      if (lm) {
+        // bounding box of the warp's active pixel centres
+        const int bx0 = __reduce_min_sync(~0u, live ? px : INT_MAX);
+        const int bx1 = __reduce_max_sync(~0u, live ? px : INT_MIN);
+        const int by0 = __reduce_min_sync(~0u, live ? py : INT_MAX);
+        const int by1 = __reduce_max_sync(~0u, live ? py : INT_MIN);
+        const double fx0 = bx0 + 0.5, fx1 = bx1 + 0.5, fy0 = by0 + 0.5, fy1 = by1 + 0.5;
+        for (int c = 0; c < nb; c += 32) {
+          bool hit = false;
+          if (c + lane < nb) {
+            const BwRec& r = s_rec[c + lane];
+            const double ex = fmax(fmax(fx0 - r.mx, r.mx - fx1), 0.0);
+            const double ey = fmax(fmax(fy0 - r.my, r.my - fy1), 0.0);
+            hit = ex * ex + ey * ey <= r.r2;
           }
+          unsigned m = __ballot_sync(~0u, hit);
+          while (m) {
+            const int k = c + __ffs(m) - 1;
+            m &= m - 1;
+            const BwRec& r = s_rec[k];
+            double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            bool touch = false;
+            if (live) {
+              const double dx = pxd - r.mx, dy = pyd - r.my;  // 311
+              const double maha = (r.ca * (dx * dx) + ((2.0 * r.cb) * dx) * dy) + r.cc * (dy * dy);
+              double sig = r.op * exp(-0.5 * maha);            // 313
+              const bool inside = (dx * dx + dy * dy) <= r.r2;  // 314
+              sig = inside ? (sig > kSigmaMax ? kSigmaMax : sig) : 0.0;
+              const double w = T * sig;
+              c0 = c0 + w * r.col[0];
+              c1 = c1 + w * r.col[1];
+              c2 = c2 + w * r.col[2];
+              if (pass == 1 && sig > 0.0) {  // backward_render 461-484
+                const double s0 = t0 - c0, s1 = t1 - c1, s2 = t2 - c2;  // suffix
+                double denom = 1.0 - sig;
+                denom = denom < 1e-6 ? 1e-6 : denom;
+                const double dsig = (g0 * (r.col[0] * T - s0 / denom) +
+                                     g1 * (r.col[1] * T - s1 / denom)) +
+                                    g2 * (r.col[2] * T - s2 / denom);
+                v[0] = g0 * w;
+                v[1] = g1 * w;
+                v[2] = g2 * w;
+                v[3] = dsig * sig / r.op;
+                v[4] = dsig * (sig * (r.ca * dx + r.cb * dy));
+                v[5] = dsig * (sig * (r.cb * dx + r.cc * dy));
+                touch = w > 0.0;
+              }
+              T = T * (1.0 - sig);
+              live = T >= kTermEps;
+            }
+            if (pass == 1) {
+              const unsigned tm = __ballot_sync(~0u, touch);
+              const bool any = __any_sync(~0u, v[3] != 0.0 || v[0] != 0.0 || v[1] != 0.0 ||
+                                                    v[2] != 0.0 || v[4] != 0.0 || v[5] != 0.0);
+              if (any) {
+                const double sum = warp_sum6(v, lane);
+                if (own >= 0 && sum != 0.0) atomicAdd(&s_acc[k][own], sum);
+              }
+              if (lane == 0 && tm) atomicAdd(&s_touch[k], __popc(tm));
+            }
+          }
+        }
+      }
+      const int more = __syncthreads_or(live);
+      if (pass == 1)
+        for (int j = tid; j < nb; j += blockDim.x) {
+          const uint32_t id = s_id[j];
+          const double* acc = s_acc[j];
+          if (s_touch[j]) atomicAdd(a.touched + id, s_touch[j]);
+          if (acc[0] != 0.0) atomicAdd(a.d_colors + 3 * (size_t)id + 0, acc[0]);
+          if (acc[1] != 0.0) atomicAdd(a.d_colors + 3 * (size_t)id + 1, acc[1]);
+          if (acc[2] != 0.0) atomicAdd(a.d_colors + 3 * (size_t)id + 2, acc[2]);
+          if (acc[3] != 0.0) atomicAdd(a.d_opacities + id, acc[3]);
+          if (acc[4] != 0.0) atomicAdd(a.d_mean2d + 2 * (size_t)id + 0, acc[4]);
+          if (acc[5] != 0.0) atomicAdd(a.d_mean2d + 2 * (size_t)id + 1, acc[5]);
         }
       __syncthreads();
-      if (!live) break;
+      if (!more) break;
     }
-    if (pass == 0) {  // C_tot = sum w c + T_final * background (326)
-      for (int p = tid; p < np; p += kBwThreads) {
-        sTot[p] = sC[p] + sT[p] * a.bg[0];
-        sTot[np + p] = sC[np + p] + sT[p] * a.bg[1];
-        sTot[2 * np + p] = sC[2 * np + p] + sT[p] * a.bg[2];
-      }
-    }
-    __syncthreads();
+    // C_tot = sum w c + T_final * background (326)
+    t0 = c0 + T * a.bg[0];
+    t1 = c1 + T * a.bg[1];
+    t2 = c2 + T * a.bg[2];
   }
 }
 
@@ -267,17 +327,17 @@ __global__ void k_backward_chain(BackwardArgs a, int64_t n) {
 }  // namespace
 
 int launch_backward(const BackwardArgs& a, int tiles, cudaStream_t s) {
-  if (a.tile_size > 32) return LMGS_ERR_UNSUPPORTED;
   int launched = 0;
+  if (a.n > 0) {
+    int64_t g = (a.n + 255) / 256;
+    if (g > 148 * 16) g = 148 * 16;
+    k_bw_prep<<<(unsigned)g, 256, 0, s>>>(a);
+    ++launched;
+  }
   if (tiles > 0) {
-    const size_t smem = sizeof(double) * 7 * (size_t)a.tile_size * a.tile_size;
-    static bool set = false;
-    if (!set) {
-      cudaFuncSetAttribute(k_backward, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(sizeof(double) * 7 * 32 * 32));
-      set = true;
-    }
-    k_backward<<<tiles, kBwThreads, smem, s>>>(a);
+    const int rs = a.region;
+    const int threads = ((rs + 7) / 8) * ((rs + 3) / 4) * 32;
+    k_backward<<<(unsigned)(tiles * a.regions), threads, 0, s>>>(a);
     ++launched;
   }
   if (a.n > 0 && (a.d_sh || a.d_logits)) {

@@ -215,6 +215,10 @@ void launch_fill_background(float* rgb, float* alpha, float* depth, float* trans
 
 // Backward of the blend + chain to SH / logits (backward.cu), over the tile
 // lists of the preceding render of the same view on the same context.
+struct BwRec {  // fp64 splat of one view (80 B)
+  double mx, my, ca, cb, cc, op, r2;
+  double col[3];
+};
 struct BackwardArgs {
   const float* means;
   const float* quats;
@@ -228,7 +232,9 @@ struct BackwardArgs {
   void* const* keys_slot;
   const int2* ranges;
   int32_t width, height, tile_size, tiles_x;
+  int32_t region, regions_x, regions;  // CTA region side (<= 16), regions per tile
   double bg[3];
+  BwRec* recs;                         // [n] scratch
   const float* image_grad;  // [H,W,3]
   double* d_colors;         // [n,3]  (zeroed per view)
   double* d_opacities;      // [n]
