@@ -558,9 +558,8 @@ int lmgs_backward(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* c
   }
   BackwardArgs a{};
   a.recs = static_cast<BwRec*>(c->bwbuf.ptr);
-  a.region = s->tile_size < 16 ? s->tile_size : 16;
-  a.regions_x = (s->tile_size + a.region - 1) / a.region;
-  a.regions = a.regions_x * a.regions_x;
+  a.blocks_x = (s->tile_size + 7) / 8;
+  a.blocks = a.blocks_x * ((s->tile_size + 3) / 4);
   a.means = g->means;
   a.quats = g->quats;
   a.scales = g->scales;

@@ -33,8 +33,6 @@
 namespace lmgs {
 namespace {
 
-constexpr int kBwThreads = 256;  // 16x16 region = 8 warps of 8x4 pixels
-constexpr int kBwBatch = 64;
 __constant__ double kShC2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
                                 -1.0925484305920792, 0.5462742152960396};
 __constant__ double kShC3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658,
@@ -125,9 +123,41 @@ __global__ void k_bw_prep(BackwardArgs a) {
   }
 }
 
+// exp(x) to ~1 ulp (the reference's libm exp is within 0.5-1 ulp): Cody-Waite
+// reduction by ln 2 and a degree-13 Taylor polynomial in explicit FMAs
+// (this file is built with -fmad=false), scaled by 2^k in two steps when the
+// result is subnormal.  About half the instructions of libdevice's exp.
+__device__ __forceinline__ double exp_bw(double x) {
+  if (!(x > -745.2)) return 0.0;
+  const double kf = rint(x * 1.4426950408889634);
+  double r = __fma_rn(-kf, 6.93147180369123816490e-01, x);  // ln2 hi (exact product)
+  r = __fma_rn(-kf, 1.90821492927058770002e-10, r);         // ln2 lo
+  double p = 1.6059043836821613e-10;                         // 1/13!
+  p = __fma_rn(p, r, 2.08767569878680990e-09);               // 1/12!
+  p = __fma_rn(p, r, 2.50521083854417188e-08);
+  p = __fma_rn(p, r, 2.75573192239858907e-07);
+  p = __fma_rn(p, r, 2.75573192239858907e-06);
+  p = __fma_rn(p, r, 2.48015873015873016e-05);
+  p = __fma_rn(p, r, 1.98412698412698413e-04);
+  p = __fma_rn(p, r, 1.38888888888888889e-03);
+  p = __fma_rn(p, r, 8.33333333333333333e-03);
+  p = __fma_rn(p, r, 4.16666666666666667e-02);
+  p = __fma_rn(p, r, 1.66666666666666667e-01);
+  p = __fma_rn(p, r, 0.5);
+  p = __fma_rn(p, r, 1.0);
+  p = __fma_rn(p, r, 1.0);
+  int k = (int)kf;
+  if (k < -1020) {  // 2^k subnormal: scale in two normal steps
+    p = __dmul_rn(p, __longlong_as_double((long long)(k + 600 + 1023) << 52));
+    return __dmul_rn(p, __longlong_as_double((long long)(-600 + 1023) << 52));
+  }
+  if (k > 1023) return __longlong_as_double(0x7ff0000000000000LL);
+  return __dmul_rn(p, __longlong_as_double((long long)(k + 1023) << 52));
+}
+
 // Sum six per-lane values over the warp with 8 fp64 shuffles (a transpose
 // reduction: each exchange halves what a lane carries).  Returns the full sum
-// of value idx(lane) in lanes with owner(lane); see bw_owner.
+// of value bw_owner(lane) in the owner lanes.
 __device__ __forceinline__ double warp_sum6(const double v[6], int lane) {
   const bool h = lane & 16, b = lane & 8, c = lane & 4;
   double a0 = (h ? v[3] : v[0]) + __shfl_xor_sync(~0u, h ? v[0] : v[3], 16);
@@ -148,33 +178,30 @@ __device__ __forceinline__ int bw_owner(int lane) {
   return base + ((lane & 8) ? 1 : 0);
 }
 
-// One CTA per (tile, 16x16 region of it); one warp per 8x4 pixel block, one
-// pixel per lane, pixel state in registers.  Splats are staged per CTA batch
-// in shared memory; each warp skips splats whose circle misses the bounding
-// box of its still-active pixels (exact: sigma is 0 outside the circle at
-// every pixel centre, and fp64 rounding is monotone).
-__global__ void __launch_bounds__(kBwThreads) k_backward(BackwardArgs a) {
-  __shared__ BwRec s_rec[kBwBatch];
-  __shared__ uint32_t s_id[kBwBatch];
-  __shared__ double s_acc[kBwBatch][6];  // d_colors 3, d_opacity, d_mean 2
-  __shared__ int s_touch[kBwBatch];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// One warp (= one CTA) per 8x4 pixel block of a tile, one pixel per lane,
+// pixel state in registers; no block-level synchronisation, so a block that
+// has terminated frees its SM slot at once.  The tile list is walked in
+// batches of 32: each lane loads one splat's cull data (mean, radius^2),
+// prefetched a batch ahead; splats whose circle misses the bounding box of
+// the still-active pixel centres are skipped (exact: sigma is 0 outside the
+// circle and fp64 rounding is monotone); hit splats' full records are staged
+// in the warp's shared buffer.  Gradients of a splat are warp-reduced and
+// added to global memory by the owner lanes.
+__global__ void __launch_bounds__(32) k_backward(BackwardArgs a) {
+  __shared__ BwRec s_rec[32];
+  const int lane = threadIdx.x;
   const int ts = a.tile_size;
-  const int tile = blockIdx.x / a.regions, reg = blockIdx.x % a.regions;
-  const int rx = reg % a.regions_x, ry = reg / a.regions_x;
-  const int rs = a.region;  // region side (<= 16)
+  const int tile = blockIdx.x / a.blocks, blk = blockIdx.x % a.blocks;
   const int tx0 = (tile % a.tiles_x) * ts, ty0 = (tile / a.tiles_x) * ts;
   const int tx1 = min(tx0 + ts, a.width), ty1 = min(ty0 + ts, a.height);
-  const int x0 = tx0 + rx * rs, y0 = ty0 + ry * rs;
-  const int x1 = min(x0 + rs, tx1), y1 = min(y0 + rs, ty1);
+  const int px = tx0 + (blk % a.blocks_x) * 8 + (lane & 7);
+  const int py = ty0 + (blk / a.blocks_x) * 4 + (lane >> 3);
+  const bool in_img = px < tx1 && py < ty1;
   const int2 range = a.ranges[tile];
-  if (range.y <= range.x || x0 >= x1 || y0 >= y1) return;
-  const int bw = (x1 - x0 + 7) >> 3;  // 8x4 blocks across the region
-  const int px = x0 + (warp % bw) * 8 + (lane & 7);
-  const int py = y0 + (warp / bw) * 4 + (lane >> 3);
-  const bool in_img = warp < bw * ((y1 - y0 + 3) >> 2) && px < x1 && py < y1;
+  if (range.y <= range.x || !__any_sync(~0u, in_img)) return;
   const double pxd = (double)px + 0.5, pyd = (double)py + 0.5;
   const uint64_t* __restrict__ list = static_cast<const uint64_t*>(*a.keys_slot);
+  const double4* __restrict__ cull = reinterpret_cast<const double4*>(a.recs);
   const int own = bw_owner(lane);
 
   double g0 = 0.0, g1 = 0.0, g2 = 0.0, t0 = 0.0, t1 = 0.0, t2 = 0.0;
@@ -187,98 +214,93 @@ __global__ void __launch_bounds__(kBwThreads) k_backward(BackwardArgs a) {
   for (int pass = 0; pass < 2; ++pass) {
     double T = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
     bool live = in_img;
-    for (int b0 = range.x; b0 < range.y; b0 += kBwBatch) {
-      const int nb = min(kBwBatch, range.y - b0);
-      for (int j = tid; j < nb; j += blockDim.x) {
-        const uint32_t id = (uint32_t)list[b0 + j];
-        s_id[j] = id;
-        s_rec[j] = a.recs[id];
+    // prefetch of the first batch
+    uint32_t nid = 0;
+    double4 ncd = make_double4(0.0, 0.0, -1.0, 0.0);
+    if (range.x + lane < range.y) {
+      nid = (uint32_t)list[range.x + lane];
+      ncd = cull[3 * (size_t)nid];  // BwRec is 3 x 32 B, cull data first
+    }
+    for (int b0 = range.x; b0 < range.y; b0 += 32) {
+      const uint32_t id = nid;
+      const double4 cd = ncd;
+      const int nb = min(32, range.y - b0);
+      if (b0 + 32 + lane < range.y) {
+        nid = (uint32_t)list[b0 + 32 + lane];
+        ncd = cull[3 * (size_t)nid];
+      }
+      // bounding box of the active pixel centres
+      const int bx0 = __reduce_min_sync(~0u, live ? px : INT_MAX);
+      const int bx1 = __reduce_max_sync(~0u, live ? px : INT_MIN);
+      const int by0 = __reduce_min_sync(~0u, live ? py : INT_MAX);
+      const int by1 = __reduce_max_sync(~0u, live ? py : INT_MIN);
+      bool hit = false;
+      if (lane < nb) {
+        const double ex = fmax(fmax((bx0 + 0.5) - cd.x, cd.x - (bx1 + 0.5)), 0.0);
+        const double ey = fmax(fmax((by0 + 0.5) - cd.y, cd.y - (by1 + 0.5)), 0.0);
+        hit = ex * ex + ey * ey <= cd.z;
+      }
+      unsigned m = __ballot_sync(~0u, hit);
+      __syncwarp();
+      if (hit) {
+        const double4* src = cull + 3 * (size_t)id;
+        double4* dst = reinterpret_cast<double4*>(&s_rec[lane]);
+        dst[0] = cd;
+        dst[1] = src[1];
+        dst[2] = src[2];
+      }
+      __syncwarp();
+      while (m) {
+        const int k = __ffs(m) - 1;
+        m &= m - 1;
+        const BwRec& r = s_rec[k];
+        double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        bool app = false, touch = false;
+        if (live) {
+          const double dx = pxd - r.mx, dy = pyd - r.my;  // 311
+          const double maha = (r.ca * (dx * dx) + ((2.0 * r.cb) * dx) * dy) + r.cc * (dy * dy);
+          double sig = r.op * exp_bw(-0.5 * maha);         // 313
+          const bool inside = (dx * dx + dy * dy) <= r.r2;  // 314
+          sig = inside ? (sig > kSigmaMax ? kSigmaMax : sig) : 0.0;
+          const double w = T * sig;
+          c0 = c0 + w * r.col[0];
+          c1 = c1 + w * r.col[1];
+          c2 = c2 + w * r.col[2];
+          if (pass == 1 && sig > 0.0) {  // backward_render 461-484
+            const double s0 = t0 - c0, s1 = t1 - c1, s2 = t2 - c2;  // suffix
+            double denom = 1.0 - sig;
+            denom = denom < 1e-6 ? 1e-6 : denom;
+            const double dsig = (g0 * (r.col[0] * T - s0 / denom) +
+                                 g1 * (r.col[1] * T - s1 / denom)) +
+                                g2 * (r.col[2] * T - s2 / denom);
+            v[0] = g0 * w;
+            v[1] = g1 * w;
+            v[2] = g2 * w;
+            v[3] = dsig * sig / r.op;
+            v[4] = dsig * (sig * (r.ca * dx + r.cb * dy));
+            v[5] = dsig * (sig * (r.cb * dx + r.cc * dy));
+            app = true;
+            touch = w > 0.0;
+          }
+          T = T * (1.0 - sig);
+          live = T >= kTermEps;
+        }
         if (pass == 1) {
-#pragma unroll
-          for (int q = 0; q < 6; ++q) s_acc[j][q] = 0.0;
-          s_touch[j] = 0;
-        }
-      }
-      __syncthreads();
-      const unsigned lm = __ballot_sync(~0u, live);
-      if (lm) {
-        // bounding box of the warp's active pixel centres
-        const int bx0 = __reduce_min_sync(~0u, live ? px : INT_MAX);
-        const int bx1 = __reduce_max_sync(~0u, live ? px : INT_MIN);
-        const int by0 = __reduce_min_sync(~0u, live ? py : INT_MAX);
-        const int by1 = __reduce_max_sync(~0u, live ? py : INT_MIN);
-        const double fx0 = bx0 + 0.5, fx1 = bx1 + 0.5, fy0 = by0 + 0.5, fy1 = by1 + 0.5;
-        for (int c = 0; c < nb; c += 32) {
-          bool hit = false;
-          if (c + lane < nb) {
-            const BwRec& r = s_rec[c + lane];
-            const double ex = fmax(fmax(fx0 - r.mx, r.mx - fx1), 0.0);
-            const double ey = fmax(fmax(fy0 - r.my, r.my - fy1), 0.0);
-            hit = ex * ex + ey * ey <= r.r2;
-          }
-          unsigned m = __ballot_sync(~0u, hit);
-          while (m) {
-            const int k = c + __ffs(m) - 1;
-            m &= m - 1;
-            const BwRec& r = s_rec[k];
-            double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-            bool touch = false;
-            if (live) {
-              const double dx = pxd - r.mx, dy = pyd - r.my;  // 311
-              const double maha = (r.ca * (dx * dx) + ((2.0 * r.cb) * dx) * dy) + r.cc * (dy * dy);
-              double sig = r.op * exp(-0.5 * maha);            // 313
-              const bool inside = (dx * dx + dy * dy) <= r.r2;  // 314
-              sig = inside ? (sig > kSigmaMax ? kSigmaMax : sig) : 0.0;
-              const double w = T * sig;
-              c0 = c0 + w * r.col[0];
-              c1 = c1 + w * r.col[1];
-              c2 = c2 + w * r.col[2];
-              if (pass == 1 && sig > 0.0) {  // backward_render 461-484
-                const double s0 = t0 - c0, s1 = t1 - c1, s2 = t2 - c2;  // suffix
-                double denom = 1.0 - sig;
-                denom = denom < 1e-6 ? 1e-6 : denom;
-                const double dsig = (g0 * (r.col[0] * T - s0 / denom) +
-                                     g1 * (r.col[1] * T - s1 / denom)) +
-                                    g2 * (r.col[2] * T - s2 / denom);
-                v[0] = g0 * w;
-                v[1] = g1 * w;
-                v[2] = g2 * w;
-                v[3] = dsig * sig / r.op;
-                v[4] = dsig * (sig * (r.ca * dx + r.cb * dy));
-                v[5] = dsig * (sig * (r.cb * dx + r.cc * dy));
-                touch = w > 0.0;
-              }
-              T = T * (1.0 - sig);
-              live = T >= kTermEps;
+          if (__any_sync(~0u, app)) {  // all six terms are 0 unless sigma > 0
+            const unsigned tm = __ballot_sync(~0u, touch);
+            const double sum = warp_sum6(v, lane);
+            const uint32_t sid = __shfl_sync(~0u, id, k);
+            if (own >= 0 && sum != 0.0) {
+              double* dst = own < 3 ? a.d_colors + 3 * (size_t)sid + own
+                          : own == 3 ? a.d_opacities + sid
+                                     : a.d_mean2d + 2 * (size_t)sid + (own - 4);
+              atomicAdd(dst, sum);
             }
-            if (pass == 1) {
-              const unsigned tm = __ballot_sync(~0u, touch);
-              const bool any = __any_sync(~0u, v[3] != 0.0 || v[0] != 0.0 || v[1] != 0.0 ||
-                                                    v[2] != 0.0 || v[4] != 0.0 || v[5] != 0.0);
-              if (any) {
-                const double sum = warp_sum6(v, lane);
-                if (own >= 0 && sum != 0.0) atomicAdd(&s_acc[k][own], sum);
-              }
-              if (lane == 0 && tm) atomicAdd(&s_touch[k], __popc(tm));
-            }
+            if (lane == 1 && tm) atomicAdd(a.touched + sid, __popc(tm));
           }
         }
       }
-      const int more = __syncthreads_or(live);
-      if (pass == 1)
-        for (int j = tid; j < nb; j += blockDim.x) {
-          const uint32_t id = s_id[j];
-          const double* acc = s_acc[j];
-          if (s_touch[j]) atomicAdd(a.touched + id, s_touch[j]);
-          if (acc[0] != 0.0) atomicAdd(a.d_colors + 3 * (size_t)id + 0, acc[0]);
-          if (acc[1] != 0.0) atomicAdd(a.d_colors + 3 * (size_t)id + 1, acc[1]);
-          if (acc[2] != 0.0) atomicAdd(a.d_colors + 3 * (size_t)id + 2, acc[2]);
-          if (acc[3] != 0.0) atomicAdd(a.d_opacities + id, acc[3]);
-          if (acc[4] != 0.0) atomicAdd(a.d_mean2d + 2 * (size_t)id + 0, acc[4]);
-          if (acc[5] != 0.0) atomicAdd(a.d_mean2d + 2 * (size_t)id + 1, acc[5]);
-        }
-      __syncthreads();
-      if (!more) break;
+      if (!__any_sync(~0u, live)) break;
     }
     // C_tot = sum w c + T_final * background (326)
     t0 = c0 + T * a.bg[0];
@@ -335,9 +357,7 @@ int launch_backward(const BackwardArgs& a, int tiles, cudaStream_t s) {
     ++launched;
   }
   if (tiles > 0) {
-    const int rs = a.region;
-    const int threads = ((rs + 7) / 8) * ((rs + 3) / 4) * 32;
-    k_backward<<<(unsigned)(tiles * a.regions), threads, 0, s>>>(a);
+    k_backward<<<(unsigned)((int64_t)tiles * a.blocks), 32, 0, s>>>(a);
     ++launched;
   }
   if (a.n > 0 && (a.d_sh || a.d_logits)) {

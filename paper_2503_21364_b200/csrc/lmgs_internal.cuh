@@ -215,9 +215,11 @@ void launch_fill_background(float* rgb, float* alpha, float* depth, float* trans
 
 // Backward of the blend + chain to SH / logits (backward.cu), over the tile
 // lists of the preceding render of the same view on the same context.
-struct BwRec {  // fp64 splat of one view (80 B)
-  double mx, my, ca, cb, cc, op, r2;
+struct __align__(32) BwRec {  // fp64 splat of one view; the first 32 B are the cull data
+  double mx, my, r2, op;
+  double ca, cb, cc;
   double col[3];
+  double pad[2];
 };
 struct BackwardArgs {
   const float* means;
@@ -232,7 +234,7 @@ struct BackwardArgs {
   void* const* keys_slot;
   const int2* ranges;
   int32_t width, height, tile_size, tiles_x;
-  int32_t region, regions_x, regions;  // CTA region side (<= 16), regions per tile
+  int32_t blocks_x, blocks;            // 8x4 pixel blocks across / per tile
   double bg[3];
   BwRec* recs;                         // [n] scratch
   const float* image_grad;  // [H,W,3]
