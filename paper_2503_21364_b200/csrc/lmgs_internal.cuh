@@ -219,7 +219,8 @@ struct __align__(32) BwRec {  // fp64 splat of one view; the first 32 B are the 
   double mx, my, r2, op;
   double ca, cb, cc;
   double col[3];
-  double pad[2];
+  double rop;  // 1 / op
+  double pad;
 };
 struct BackwardArgs {
   const float* means;
