@@ -150,17 +150,27 @@ int lmgs_get_stats(lmgs_context* ctx, lmgs_stats* out);
 int lmgs_copy_instances(lmgs_context* ctx, uint64_t* keys, int64_t* prim_ids, void* stream);
 
 /* Backward of the blend for the view last rendered on ctx (same Gaussians,
- * camera and settings; tile_size <= 32): backward_render (gaussian_core.py:
+ * camera and settings): backward_render (gaussian_core.py:
  * 438-486) in fp64 with the reference's semantics — d_colors [count,3],
  * d_opacities [count], d_mean2d [count,2], touched [count] (zeroed, rows of
  * non-rendered Gaussians stay 0) — and, when non-NULL, the chain rule of
  * render_loss_and_grads (600-629): d_sh [count,sh_coeffs,3] and d_logits
- * [count] are ACCUMULATED (+=) so several views can be summed.  image_grad is
- * the loss gradient w.r.t. the [H,W,3] image (fp32, device). */
+ * [count] are ACCUMULATED (+=) so several views can be summed, and so are
+ * the DensifyStats increments (488-511) when grad_norm_sum / steps_seen are
+ * non-NULL: += |d_mean2d| and += 1 for every Gaussian with touched > 0.
+ * image_grad is the loss gradient w.r.t. the [H,W,3] image (fp32, device). */
 int lmgs_backward(lmgs_context* ctx, const lmgs_gaussians* g, const lmgs_camera* cam,
                   const lmgs_settings* s, const float* image_grad, double* d_colors,
                   double* d_opacities, double* d_mean2d, int32_t* touched, double* d_sh,
-                  double* d_logits, void* stream);
+                  double* d_logits, double* grad_norm_sum, int64_t* steps_seen,
+                  void* stream);
+
+/* The mean-squared-error step of render_loss_and_grads (gaussian_core.py:
+ * 615-617) for one view: diff = rgb - gt over n_values = H*W*3 values,
+ * loss_sum[0] += sum(diff^2) (fp64, device), image_grad = 2 diff / n_values
+ * (fp32, the lmgs_backward input).  gt is fp64 when gt_is_f64, else fp32. */
+int lmgs_mse_grad(const float* rgb, const void* gt, int gt_is_f64, int64_t n_values,
+                  float* image_grad, double* loss_sum, void* stream);
 
 /* Stage K1 alone (project_splats): per input Gaussian, fp64 geometry.
  * mean2d [count,2], cov2d [count,3] = (c00,c01,c11) incl. the 0.3 floor,

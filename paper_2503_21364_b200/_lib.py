@@ -32,7 +32,7 @@ EXPORTS = ("lmgs_abi_version", "lmgs_context_create", "lmgs_context_destroy", "l
            "lmgs_render", "lmgs_render_batch", "lmgs_get_stats", "lmgs_copy_instances",
            "lmgs_project", "lmgs_composite_blocks", "lmgs_checkpoint_info_read",
            "lmgs_checkpoint_load", "lmgs_checkpoint_save", "lmgs_encode_rgb8",
-           "lmgs_backward")
+           "lmgs_backward", "lmgs_mse_grad")
 
 
 class Camera(ctypes.Structure):
@@ -102,7 +102,8 @@ def lib():
                                        ctypes.POINTER(CheckpointInfo), P, P, P, ctypes.c_int]
     L.lmgs_encode_rgb8.argtypes = [P, I64, P, P]
     L.lmgs_backward.argtypes = [P, ctypes.POINTER(Gaussians), ctypes.POINTER(Camera),
-                                ctypes.POINTER(Settings), P, P, P, P, P, P, P, P]
+                                ctypes.POINTER(Settings), P, P, P, P, P, P, P, P, P, P]
+    L.lmgs_mse_grad.argtypes = [P, P, ctypes.c_int, I64, P, P, P]
     got = L.lmgs_abi_version()
     if got != ABI_VERSION:
         raise LmgsError(f"liblmgs ABI {got} != expected {ABI_VERSION}")

@@ -535,7 +535,8 @@ int lmgs_copy_instances(lmgs_context* c, uint64_t* keys, int64_t* prim_ids, void
 int lmgs_backward(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
                   const lmgs_settings* s, const float* image_grad, double* d_colors,
                   double* d_opacities, double* d_mean2d, int32_t* touched, double* d_sh,
-                  double* d_logits, void* stream) {
+                  double* d_logits, double* grad_norm_sum, int64_t* steps_seen,
+                  void* stream) {
   if (int r = validate(c, g, cam, s)) return r;
   if (!image_grad || !d_colors || !d_opacities || !d_mean2d || !touched)
     return fail(c, LMGS_ERR_INVALID, "null backward output");
@@ -546,12 +547,6 @@ int lmgs_backward(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* c
   DeviceGuard guard(c->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t n = g->count;
-  if (n > 0) {
-    LMGS_CUDA(c, cudaMemsetAsync(d_colors, 0, sizeof(double) * 3 * n, st));
-    LMGS_CUDA(c, cudaMemsetAsync(d_opacities, 0, sizeof(double) * n, st));
-    LMGS_CUDA(c, cudaMemsetAsync(d_mean2d, 0, sizeof(double) * 2 * n, st));
-    LMGS_CUDA(c, cudaMemsetAsync(touched, 0, sizeof(int32_t) * n, st));
-  }
   if ((size_t)n * sizeof(BwRec) > c->bwbuf.bytes) {
     LMGS_CUDA(c, cudaStreamSynchronize(st));  // an earlier backward may still read it
     LMGS_CUDA(c, c->bwbuf.reserve((size_t)(n > 0 ? n : 1) * sizeof(BwRec)));
@@ -583,7 +578,9 @@ int lmgs_backward(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* c
   a.touched = touched;
   a.d_sh = d_sh;
   a.d_logits = d_logits;
-  if (c->stats.n_instances > 0 || d_sh || d_logits) launch_backward(a, (int)tiles, st);
+  a.grad_norm_sum = grad_norm_sum;
+  a.steps_seen = steps_seen;
+  launch_backward(a, (int)tiles, st);
   LMGS_CUDA(c, cudaGetLastError());
   return LMGS_OK;
 }

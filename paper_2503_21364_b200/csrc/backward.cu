@@ -121,6 +121,11 @@ __global__ void k_bw_prep(BackwardArgs a) {
     r.col[1] = fmin(fmax(raw[1], 0.0), 1.0);
     r.col[2] = fmin(fmax(raw[2], 0.0), 1.0);
     a.recs[id] = r;
+    // this view's per-Gaussian outputs start at zero (k_backward adds into them)
+    a.d_colors[3 * id] = a.d_colors[3 * id + 1] = a.d_colors[3 * id + 2] = 0.0;
+    a.d_opacities[id] = 0.0;
+    a.d_mean2d[2 * id] = a.d_mean2d[2 * id + 1] = 0.0;
+    a.touched[id] = 0;
   }
 }
 
@@ -323,6 +328,11 @@ __global__ void k_backward_chain(BackwardArgs a, int64_t n) {
        i += (int64_t)gridDim.x * blockDim.x) {
     const double dc0 = a.d_colors[3 * i], dc1 = a.d_colors[3 * i + 1],
                  dc2 = a.d_colors[3 * i + 2], dop = a.d_opacities[i];
+    if (a.steps_seen && a.touched[i] > 0) {  // DensifyStats.accumulate (504-508)
+      const double mx = a.d_mean2d[2 * i], my = a.d_mean2d[2 * i + 1];
+      a.grad_norm_sum[i] += sqrt(mx * mx + my * my);
+      a.steps_seen[i] += 1;
+    }
     if (a.d_logits && dop != 0.0) {
       const double alpha = 1.0 / (1.0 + exp(-(double)a.logits[i]));
       a.d_logits[i] += (dop * alpha) * (1.0 - alpha);
@@ -367,7 +377,7 @@ int launch_backward(const BackwardArgs& a, int tiles, cudaStream_t s) {
     k_backward<<<(unsigned)((int64_t)tiles * a.blocks), 32, 0, s>>>(a);
     ++launched;
   }
-  if (a.n > 0 && (a.d_sh || a.d_logits)) {
+  if (a.n > 0 && (a.d_sh || a.d_logits || a.steps_seen)) {
     int64_t g = (a.n + 255) / 256;
     if (g > 148 * 16) g = 148 * 16;
     k_backward_chain<<<(unsigned)g, 256, 0, s>>>(a, a.n);
@@ -377,3 +387,48 @@ int launch_backward(const BackwardArgs& a, int tiles, cudaStream_t s) {
 }
 
 }  // namespace lmgs
+
+namespace lmgs {
+namespace {
+
+template <typename G>
+__global__ void k_mse_grad(const float* __restrict__ rgb, const G* __restrict__ gt, int64_t n,
+                           float* __restrict__ grad, double* loss_sum) {
+  double acc = 0.0;
+  const double scale = 2.0 / (double)n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double d = (double)rgb[i] - (double)gt[i];
+    acc = acc + d * d;
+    grad[i] = (float)(scale * d);
+  }
+  for (int o = 16; o; o >>= 1) acc = acc + __shfl_xor_sync(~0u, acc, o);
+  __shared__ double part[8];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = t + part[w];
+    atomicAdd(loss_sum, t);
+  }
+}
+
+}  // namespace
+}  // namespace lmgs
+
+extern "C" int lmgs_mse_grad(const float* rgb, const void* gt, int gt_is_f64, int64_t n_values,
+                             float* image_grad, double* loss_sum, void* stream) {
+  if (n_values < 0 || (n_values > 0 && (!rgb || !gt || !image_grad || !loss_sum)))
+    return LMGS_ERR_INVALID;
+  if (n_values == 0) return LMGS_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int64_t g = (n_values + 255) / 256;
+  if (g > 148 * 8) g = 148 * 8;
+  if (gt_is_f64)
+    lmgs::k_mse_grad<double><<<(unsigned)g, 256, 0, s>>>(rgb, static_cast<const double*>(gt),
+                                                         n_values, image_grad, loss_sum);
+  else
+    lmgs::k_mse_grad<float><<<(unsigned)g, 256, 0, s>>>(rgb, static_cast<const float*>(gt),
+                                                        n_values, image_grad, loss_sum);
+  return cudaGetLastError() == cudaSuccess ? LMGS_OK : LMGS_ERR_CUDA;
+}

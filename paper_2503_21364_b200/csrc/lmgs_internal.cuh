@@ -245,6 +245,8 @@ struct BackwardArgs {
   int32_t* touched;         // [n]
   double* d_sh;             // [n,coeffs,3] accumulated (nullable)
   double* d_logits;         // [n] accumulated (nullable)
+  double* grad_norm_sum;    // [n] DensifyStats, accumulated (nullable)
+  int64_t* steps_seen;      // [n] DensifyStats, accumulated (nullable)
 };
 int launch_backward(const BackwardArgs& a, int tiles, cudaStream_t s);  // kernels launched or -err
 

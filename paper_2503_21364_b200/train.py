@@ -62,7 +62,8 @@ class DensifyStats:
 
 
 def _backward(ctx, model: GaussianModel, camera, image_grad: torch.Tensor, tile_size: int,
-              background, sh_eval_degree: int, d_sh=None, d_logits=None) -> RenderGrads:
+              background, sh_eval_degree: int, d_sh=None, d_logits=None,
+              stats: "DensifyStats | None" = None) -> RenderGrads:
     h, w = int(camera.height), int(camera.width)
     if tuple(image_grad.shape) != (h, w, 3):
         raise ShapeError("image gradient shape does not match forward record")
@@ -81,7 +82,10 @@ def _backward(ctx, model: GaussianModel, camera, image_grad: torch.Tensor, tile_
             ctx.handle, ctypes.byref(ga), ctypes.byref(cam), ctypes.byref(st), _ptr(g),
             _ptr(out.d_colors), _ptr(out.d_opacities), _ptr(out.d_mean2d), _ptr(out.touched),
             _ptr(d_sh) if d_sh is not None else None,
-            _ptr(d_logits) if d_logits is not None else None, s.cuda_stream), "lmgs_backward")
+            _ptr(d_logits) if d_logits is not None else None,
+            _ptr(stats.grad_norm_sum) if stats is not None else None,
+            _ptr(stats.steps_seen) if stats is not None else None, s.cuda_stream),
+            "lmgs_backward")
     return out
 
 
@@ -102,15 +106,27 @@ def render_loss_and_grads(model: GaussianModel, cameras, gt_images, tile_size: i
     d_sh = torch.zeros((n, model.sh.shape[1], 3), dtype=torch.float64, device=dev)
     d_logit = torch.zeros((n,), dtype=torch.float64, device=dev)
     stats = DensifyStats.zeros(n, dev)
-    total = 0.0
-    for cam, gt in zip(cameras, gt_images):
+    loss_sum = torch.zeros((len(cameras) or 1,), dtype=torch.float64, device=dev)
+    numels = []
+    for i, (cam, gt) in enumerate(zip(cameras, gt_images)):
         fwd = render(cam, model, tile_size, background, sh_eval_degree, ctx=ctx)
-        gt_t = torch.as_tensor(gt, dtype=torch.float64, device=dev)
-        diff = fwd.rgb.double() - gt_t
-        total += float((diff ** 2).mean())
-        g_img = 2.0 * diff / diff.numel()
-        grads = _backward(ctx, model, cam, g_img, tile_size, background, sh_eval_degree,
-                          d_sh, d_logit)
-        stats.accumulate(grads)
+        gt_t = torch.as_tensor(gt, device=dev)
+        if gt_t.dtype not in (torch.float32, torch.float64):
+            gt_t = gt_t.to(torch.float64)
+        gt_t = gt_t.contiguous()
+        if tuple(gt_t.shape) != tuple(fwd.rgb.shape):
+            raise ShapeError("ground-truth image shape does not match the camera")
+        g_img = torch.empty_like(fwd.rgb)
+        with torch.cuda.device(dev):
+            _lib.check(None, _lib.lib().lmgs_mse_grad(
+                _ptr(fwd.rgb), _ptr(gt_t), int(gt_t.dtype == torch.float64), fwd.rgb.numel(),
+                _ptr(g_img), _ptr(loss_sum[i:]), torch.cuda.current_stream(dev).cuda_stream),
+                "lmgs_mse_grad")
+        numels.append(fwd.rgb.numel())
+        _backward(ctx, model, cam, g_img, tile_size, background, sh_eval_degree, d_sh, d_logit,
+                  stats)
     k = max(1, len(cameras))
+    # total += mean(diff^2) per view (615-616): one device->host read per call
+    per_view = loss_sum.cpu().tolist()
+    total = sum(v / m for v, m in zip(per_view, numels))
     return total / k, {"sh": d_sh / k, "opacity_logits": d_logit / k}, stats
