@@ -129,6 +129,16 @@ __global__ void k_bw_prep(BackwardArgs a) {
   }
 }
 
+#ifdef LMGS_BW_COUNT
+__device__ unsigned long long g_bw_count[2][4];
+}  // namespace
+}  // namespace lmgs
+extern "C" int lmgs_debug_bw_count(unsigned long long* host_out) {
+  return (int)cudaMemcpyFromSymbol(host_out, lmgs::g_bw_count, sizeof(lmgs::g_bw_count));
+}
+namespace lmgs {
+namespace {
+#endif
 // exp(x) to ~1 ulp (the reference's libm exp is within 0.5-1 ulp): Cody-Waite
 // reduction by ln 2 and a degree-13 Taylor polynomial in explicit FMAs
 // (this file is built with -fmad=false), scaled by 2^k in two steps when the
@@ -265,6 +275,18 @@ __global__ void __launch_bounds__(32, LMGS_BW_MINB) k_backward(BackwardArgs a) {
         const BwRec& r = s_rec[k];
         double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
         bool app = false, touch = false;
+#ifdef LMGS_BW_COUNT
+        {
+          const double ddx = pxd - r.mx, ddy = pyd - r.my;
+          const bool ins = live && (ddx * ddx + ddy * ddy) <= r.r2;
+          const unsigned lv = __ballot_sync(~0u, live), iv = __ballot_sync(~0u, ins);
+          if (lane == 0) {
+            atomicAdd(&g_bw_count[pass][0], 1ull);
+            atomicAdd(&g_bw_count[pass][1], (unsigned long long)__popc(lv));
+            atomicAdd(&g_bw_count[pass][2], (unsigned long long)__popc(iv));
+          }
+        }
+#endif
         if (live) {
           const double dx = pxd - r.mx, dy = pyd - r.my;  // 311
           const double maha = (r.ca * (dx * dx) + ((2.0 * r.cb) * dx) * dy) + r.cc * (dy * dy);
