@@ -133,3 +133,114 @@ def test_backward_rejects_mismatched_shapes():
     cam = scenes.orbit_cameras(1, 64, 48, seed=1)[0]
     with pytest.raises(ShapeError):
         backward_render(GaussianModel.from_host(g), cam, torch.zeros(48, 63, 3).cuda())
+
+
+def _random_model(seed, n, extent=3.0):
+    """test_gaussian_core.py:29-43 (random_model), drawn in f32."""
+    from paper_2503_21364_b200 import scenes
+
+    rng = np.random.default_rng(seed)
+    quats = rng.standard_normal((n, 4))
+    quats /= np.linalg.norm(quats, axis=1, keepdims=True)
+    sh = np.zeros((n, 4, 3))
+    sh[:, 0] = rng.uniform(0.2, 2.5, (n, 3))
+    sh[:, 1:] = rng.uniform(-0.1, 0.1, (n, 3, 3))
+    f = np.float32
+    return scenes.HostGaussians(rng.uniform(-extent, extent, (n, 3)).astype(f), quats.astype(f),
+                                rng.uniform(0.05, 0.4, (n, 3)).astype(f),
+                                rng.uniform(-1.5, 2.0, n).astype(f), sh.astype(f), 1)
+
+
+def _front_camera(w, h):
+    from paper_2503_21364_b200.camera import look_at_camera
+
+    return look_at_camera((0.0, -8.0, 0.0), (0.0, 0.0, 0.0), fov_deg=60.0, width=w, height=h)
+
+
+@pytest.mark.gpu
+def test_backward_zero_contribution_zero_gradient():
+    """test_gaussian_core.py:300-307: untouched splats get exactly zero gradient."""
+    import torch
+
+    from paper_2503_21364_b200 import GaussianModel
+    from paper_2503_21364_b200.train import backward_render
+
+    g = _random_model(14, 10)
+    _, gr = backward_render(GaussianModel.from_host(g), _front_camera(32, 32),
+                            torch.ones(32, 32, 3).cuda())
+    un = (gr.touched == 0).cpu()
+    assert bool((gr.d_colors.cpu()[un] == 0).all()) and bool((gr.d_opacities.cpu()[un] == 0).all())
+    assert int((~un).sum()) > 0
+
+
+@pytest.mark.gpu
+def test_backward_single_splat_analytic():
+    """test_gaussian_core.py:310-328: one saturated splat on the pixel centre,
+    dL/dc = 2 (sigma c - gt) sigma with sigma = SIGMA_MAX."""
+    import torch
+
+    from paper_2503_21364_b200 import GaussianModel, scenes
+    from paper_2503_21364_b200.camera import Camera
+    from paper_2503_21364_b200.train import backward_render
+
+    c0 = 0.28209479177387814
+    cam = Camera(40.0, 40.0, 0.5, 0.5, 1, 1, np.eye(3), np.zeros(3))
+    sh = np.zeros((1, 4, 3), np.float32)
+    sh[0, 0] = 0.8 / c0
+    g = scenes.HostGaussians(np.array([[0.0, 0.0, 5.0]], np.float32),
+                             np.array([[1.0, 0.0, 0.0, 0.0]], np.float32),
+                             np.full((1, 3), 500.0, np.float32), np.array([200.0], np.float32), sh, 1)
+    model = GaussianModel.from_host(g)
+    from paper_2503_21364_b200 import render
+
+    image = render(cam, model, 16, (0.0, 0.0, 0.0), 1).rgb
+    _, gr = backward_render(model, cam, 2.0 * (image - 0.5))
+    sigma = 0.9999
+    expected = 2.0 * (0.8 * sigma - 0.5) * sigma
+    assert torch.allclose(gr.d_colors[0].cpu(), torch.full((3,), expected, dtype=torch.float64),
+                          atol=1e-4)
+
+
+@pytest.mark.gpu
+def test_gradients_match_finite_differences():
+    """test_gaussian_core.py:331-374: analytic SH / opacity-logit gradients of
+    the MSE loss against central differences of the fp64 oracle render (step
+    2^-12, exact in f32), relative tolerance 1e-3, at least 30 checked."""
+    import oracle
+
+    from paper_2503_21364_b200 import GaussianModel
+    from paper_2503_21364_b200.train import render_loss_and_grads
+
+    g = _random_model(15, 10)
+    cam = _front_camera(24, 24)
+    gt = np.random.default_rng(1).uniform(0, 1, (24, 24, 3))
+    _, grads, _ = render_loss_and_grads(GaussianModel.from_host(g), [cam], [gt])
+    d_sh = grads["sh"].cpu().numpy()
+    d_lg = grads["opacity_logits"].cpu().numpy()
+
+    def loss_of(gg):
+        return float(((oracle.render(gg, cam)["image"] - gt) ** 2).mean())
+
+    h = 2.0 ** -12
+    rng = np.random.default_rng(0)
+    checked = 0
+    for _ in range(60):
+        gg = type(g)(g.means.copy(), g.quats.copy(), g.scales.copy(), g.opacity_logits.copy(),
+                     g.sh.copy(), 1)
+        if rng.uniform() < 0.5:
+            i, k, c = int(rng.integers(10)), int(rng.integers(4)), int(rng.integers(3))
+            analytic, arr, idx = float(d_sh[i, k, c]), gg.sh, (i, k, c)
+        else:
+            i = int(rng.integers(10))
+            analytic, arr, idx = float(d_lg[i]), gg.opacity_logits, (i,)
+        x = arr[idx]
+        arr[idx] = x + np.float32(h)
+        up = loss_of(gg)
+        arr[idx] = x - np.float32(h)
+        dn = loss_of(gg)
+        fd = (up - dn) / (2 * h)
+        if abs(fd) < 1e-8 and abs(analytic) < 1e-8:
+            continue
+        assert abs(analytic - fd) <= 1e-3 * max(abs(fd), abs(analytic), 1e-6), (analytic, fd)
+        checked += 1
+    assert checked >= 30
