@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define LMGS_ABI_VERSION 3
+#define LMGS_ABI_VERSION 4
 
 typedef enum lmgs_status {
   LMGS_OK = 0,
@@ -79,11 +79,19 @@ typedef struct lmgs_gaussians {
   const float* scales;          /* [count,3] > 0, linear           */
   const float* opacity_logits;  /* [count]                         */
   const float* sh;              /* [count, sh_coeffs, 3]           */
-  const int64_t* prim_ids;      /* [count] ascending original ids (render_image's
-                                   `subset`, 593-595) or NULL = row index        */
+  const int64_t* prim_ids;      /* [count] original ids (render_image's `subset`,
+                                   593-595; depth ties are broken by them) or
+                                   NULL = row index                              */
   int64_t count;
   int32_t sh_degree;            /* model degree, sh_coeffs == (sh_degree+1)^2 */
   int32_t sh_coeffs;
+  /* Paged sets (a device pool of 128-row pages, offload.py): row r takes
+   * part only if (r & 127) < page_mask[r >> 7] (the live leading rows of its
+   * page, 0..128); other rows are treated as culled.  NULL = every row.
+   * page_shift must be 7. */
+  const uint8_t* page_mask;
+  int32_t page_shift;
+  int32_t reserved;
 } lmgs_gaussians;
 
 typedef struct lmgs_settings {

@@ -13,7 +13,7 @@ from pathlib import Path
 from .errors import InvalidInputError, LmgsError, ShapeError
 
 LIB_PATH = Path(__file__).resolve().parent / "liblmgs.so"
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 P = ctypes.c_void_p
 D = ctypes.c_double
@@ -43,7 +43,8 @@ class Camera(ctypes.Structure):
 
 class Gaussians(ctypes.Structure):
     _fields_ = [("means", P), ("quats", P), ("scales", P), ("opacity_logits", P), ("sh", P),
-                ("prim_ids", P), ("count", I64), ("sh_degree", I32), ("sh_coeffs", I32)]
+                ("prim_ids", P), ("count", I64), ("sh_degree", I32), ("sh_coeffs", I32),
+                ("page_mask", P), ("page_shift", I32), ("reserved", I32)]
 
 
 class Settings(ctypes.Structure):

@@ -214,6 +214,8 @@ int validate(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
     return fail(c, LMGS_ERR_INVALID, "null Gaussian array");
   if (g->count > 0 && (reinterpret_cast<uintptr_t>(g->quats) & 15))
     return fail(c, LMGS_ERR_INVALID, "quats must be 16-byte aligned");
+  if (g->page_mask && g->page_shift != 7)
+    return fail(c, LMGS_ERR_INVALID, "page_shift must be 7 (128-row pages)");
   if (s->tile_size < 1) return fail(c, LMGS_ERR_INVALID, "tile_size must be >= 1");
   if (s->tile_size > 64) return fail(c, LMGS_ERR_UNSUPPORTED, "tile_size > 64 not supported");
   if (cam->width < 1 || cam->height < 1) return fail(c, LMGS_ERR_INVALID, "bad image size");
@@ -258,6 +260,8 @@ PreprocessArgs make_pre(lmgs_context* c, const lmgs_gaussians* g, const CamArgs&
   pa.logits = g->opacity_logits;
   pa.sh = g->sh;
   pa.n = g->count;
+  pa.page_mask = g->page_mask;
+  pa.page_shift = g->page_shift;
   pa.sh_coeffs = g->sh_coeffs;
   pa.eval_degree = st->sh_eval_degree < g->sh_degree ? st->sh_eval_degree : g->sh_degree;
   pa.cam = ca;
@@ -345,7 +349,8 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
     rb.iota_vals = true;
     rb.hist_ready = true;
     launched += radix_sort(rb, n, 0, kDepthPasses, s);
-    launched += launch_depth_fixup(&sc->slots.depth_keys, &sc->slots.depth_ids, n, c->key64, s);
+    launched += launch_depth_fixup(&sc->slots.depth_keys, &sc->slots.depth_ids, n, c->key64,
+                                   g->prim_ids, s);
   }
   tm.end(1);
 

@@ -53,6 +53,8 @@ struct PreprocessArgs {
   int32_t sh_coeffs;
   int32_t eval_degree;
   CamArgs cam;
+  const uint8_t* page_mask;  // nullable: rows of pages with mask 0 are culled
+  int32_t page_shift;
   // outputs
   uint64_t* depth_keys;    // [n] fp64 depth bits; kCulledKey if culled or off-screen
   uint64_t* rects;         // [n] inclusive tile rect (visible splats; count = its area)
@@ -153,7 +155,7 @@ int launch_depth_keys(const uint64_t* key64, const unsigned long long* zrange, i
 
 // K2b: order runs of equal 32-bit keys by (fp64 depth, id) — _sort_order's exact key
 int launch_depth_fixup(void* const* keys_slot, void* const* ids_slot, int64_t n,
-                        const uint64_t* key64, cudaStream_t s);
+                        const uint64_t* key64, const int64_t* prim_ids, cudaStream_t s);
 
 // K4: walk Gaussians in depth order, scan their tile counts (decoupled
 // look-back) and emit one key (tile << 32 | id) per overlapped tile — the

@@ -114,6 +114,7 @@ __device__ __forceinline__ void sh_color(const float* __restrict__ sh, int ncoef
 // 128 x 7 CTAs per SM: 28 warps to hide the fp64 dependency chains, 7 x 30 KB
 // of TMA-staged inputs in flight per SM.
 constexpr int kPreThreads = LMGS_PRE_THREADS;
+static_assert(kPreThreads == 128, "paged sets map one K1 block to one 128-row page");
 
 // Returns the splat's tile count (0: culled or off-screen); *keep = near-kept.
 template <bool SMEM>
@@ -237,12 +238,21 @@ __device__ __forceinline__ void count_kept(const PreprocessArgs& a, bool keep, u
   }
 }
 
+// a row of an inactive page (paged sets): culled
+__device__ __forceinline__ void cull_row(const PreprocessArgs& a, int64_t i) {
+  if (a.kept) a.kept[i] = 0;
+  a.depth_keys[i] = kCulledKey;
+  a.rects[i] = 0;
+}
+
 // direct loads (tail block, unaligned inputs)
 __global__ void __launch_bounds__(kPreThreads) k_preprocess_direct(PreprocessArgs a, int64_t first) {
   const int64_t i = first + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool keep = false;
   uint32_t cnt = 0;
-  if (i < a.n) {
+  if (i < a.n && a.page_mask && (int)(i & 127) >= (int)a.page_mask[i >> 7]) {
+    cull_row(a, i);
+  } else if (i < a.n) {
     const float4 q = __ldg(reinterpret_cast<const float4*>(a.quats) + i);
     cnt = process_one<false>(a, i, a.means[3 * i], a.means[3 * i + 1], a.means[3 * i + 2], q,
                              a.scales[3 * i], a.scales[3 * i + 1], a.scales[3 * i + 2],
@@ -267,6 +277,11 @@ __global__ void __launch_bounds__(kPreThreads, LMGS_PRE_MIN_CTAS) k_preprocess_t
   __shared__ __align__(8) uint64_t s_bar[2];
   const int tid = threadIdx.x;
   const int64_t i0 = (int64_t)blockIdx.x * kPreThreads;
+  if (a.page_mask && a.page_mask[i0 >> 7] == 0) {  // the block is one inactive page
+    cull_row(a, i0 + tid);
+    count_kept(a, false, 0, i0 + tid);
+    return;
+  }
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
@@ -289,10 +304,14 @@ __global__ void __launch_bounds__(kPreThreads, LMGS_PRE_MIN_CTAS) k_preprocess_t
   // the SH wait happens inside process_one just before the colour is needed
   a.sh_wait = &s_bar[1];
   bool keep = false;
-  const uint32_t cnt =
-      process_one<true>(a, i, s_means[3 * tid], s_means[3 * tid + 1], s_means[3 * tid + 2], q,
-                        s_scales[3 * tid], s_scales[3 * tid + 1], s_scales[3 * tid + 2],
-                        s_logits[tid], s_sh + tid * a.sh_coeffs * 3, &keep);
+  uint32_t cnt = 0;
+  if (a.page_mask && tid >= (int)a.page_mask[i0 >> 7]) {  // past the page's live rows
+    cull_row(a, i);
+  } else {
+    cnt = process_one<true>(a, i, s_means[3 * tid], s_means[3 * tid + 1], s_means[3 * tid + 2], q,
+                            s_scales[3 * tid], s_scales[3 * tid + 1], s_scales[3 * tid + 2],
+                            s_logits[tid], s_sh + tid * a.sh_coeffs * 3, &keep);
+  }
   count_kept(a, keep, cnt, i);
   // every thread must observe the SH barrier before the block may exit
   mbar_wait(&s_bar[1], 0);

@@ -85,23 +85,26 @@ __global__ void __launch_bounds__(256) k_depth_keys(const uint64_t* __restrict__
 }
 
 // ---------------------------------------------------------------------------
-// K2b: exact fix-up of a run of equal keys: order by (fp64 depth bits, id).
-// The radix sort is stable and its payload is the input index, so a run is
-// already in id order; an in-place insertion sort is linear on the common
-// run (exact duplicates) and runs are short.
+// K2b: exact fix-up of a run of equal keys: order by (fp64 depth bits, prim
+// id).  The radix sort is stable and its payload is the input index, so a run
+// is already in row order — the prim-id order unless a paged set maps rows to
+// ids out of order; an in-place insertion sort is linear on the common run
+// (exact duplicates) and runs are short.
 
-__device__ __forceinline__ bool less64(uint64_t ka, uint32_t ia, uint64_t kb, uint32_t ib) {
+__device__ __forceinline__ bool less64(uint64_t ka, int64_t ia, uint64_t kb, int64_t ib) {
   return ka < kb || (ka == kb && ia < ib);
 }
 
-__device__ void fix_run(uint32_t* ids, int len, const uint64_t* __restrict__ key64) {
+__device__ void fix_run(uint32_t* ids, int len, const uint64_t* __restrict__ key64,
+                        const int64_t* __restrict__ pid) {
   for (int a = 1; a < len; ++a) {
     const uint32_t ki = ids[a];
     const uint64_t kd = key64[ki];
+    const int64_t pi = pid ? pid[ki] : (int64_t)ki;
     int b = a - 1;
     while (b >= 0) {
       const uint32_t ib = ids[b];
-      if (!less64(kd, ki, key64[ib], ib)) break;
+      if (!less64(kd, pi, key64[ib], pid ? pid[ib] : (int64_t)ib)) break;
       ids[b + 1] = ib;
       --b;
     }
@@ -113,7 +116,8 @@ __device__ void fix_run(uint32_t* ids, int len, const uint64_t* __restrict__ key
 // its predecessor and continues into its successor
 constexpr int kFixupPer = 4;
 __global__ void k_depth_fixup(void* const* keys_slot, void* const* ids_slot, int64_t n,
-                              const uint64_t* __restrict__ key64) {
+                              const uint64_t* __restrict__ key64,
+                              const int64_t* __restrict__ pid) {
   const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kFixupPer;
   if (i0 >= n) return;
   const uint32_t* __restrict__ keys = static_cast<const uint32_t*>(*keys_slot);
@@ -130,7 +134,7 @@ __global__ void k_depth_fixup(void* const* keys_slot, void* const* ids_slot, int
     if (k[u - 1] == k[u] || k[u + 1] != k[u]) continue;  // not the head of a run
     int64_t len = 2;
     while (i + len < n && keys[i + len] == k[u]) ++len;
-    fix_run(static_cast<uint32_t*>(*ids_slot) + i, (int)len, key64);
+    fix_run(static_cast<uint32_t*>(*ids_slot) + i, (int)len, key64, pid);
   }
 }
 
@@ -391,10 +395,11 @@ int launch_depth_keys(const uint64_t* key64, const unsigned long long* zrange, i
 }
 
 int launch_depth_fixup(void* const* keys_slot, void* const* ids_slot, int64_t n,
-                       const uint64_t* key64, cudaStream_t s) {
+                       const uint64_t* key64, const int64_t* prim_ids, cudaStream_t s) {
   if (n <= 1) return 0;
   const int64_t threads = (n + kFixupPer - 1) / kFixupPer;
-  k_depth_fixup<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(keys_slot, ids_slot, n, key64);
+  k_depth_fixup<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(keys_slot, ids_slot, n, key64,
+                                                                   prim_ids);
   return 1;
 }
 

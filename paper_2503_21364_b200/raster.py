@@ -109,11 +109,13 @@ class GaussianModel:
         return sum(t.numel() * 4 for t in (self.means, self.quats, self.scales,
                                            self.opacity_logits, self.sh))
 
-    def _abi(self, prim_ids=None) -> _lib.Gaussians:
+    def _abi(self, prim_ids=None, page_mask=None, page_shift: int = 0) -> _lib.Gaussians:
         g = _lib.Gaussians()
         g.means, g.quats, g.scales = _ptr(self.means), _ptr(self.quats), _ptr(self.scales)
         g.opacity_logits, g.sh = _ptr(self.opacity_logits), _ptr(self.sh)
         g.prim_ids = _ptr(prim_ids)
+        g.page_mask = _ptr(page_mask)
+        g.page_shift = int(page_shift)
         g.count = self.count
         g.sh_degree = self.sh_degree
         g.sh_coeffs = int(self.sh.shape[1])
@@ -230,13 +232,16 @@ class RenderOutput:
 def render(camera, gaussians: GaussianModel, tile_size: int = 16, background=(0.0, 0.0, 0.0),
            sh_eval_degree: int = 3, with_instances: bool = False, stage_times: bool = False,
            prim_ids: torch.Tensor | None = None, stream=None, ctx=None,
-           out: dict | None = None) -> RenderOutput:
+           out: dict | None = None, page_mask: torch.Tensor | None = None,
+           page_shift: int = 7) -> RenderOutput:
     """Render one view of device-resident Gaussians (north-star operator).
 
-    ``prim_ids`` (ascending int64, optional) are the original ids used for
-    depth-tie breaking and reported in ``inst_prim_ids`` (render_image's
-    ``subset``).  ``out`` may pre-supply output tensors (e.g. slices of a
-    batch buffer) under the RenderOutput field names.
+    ``prim_ids`` (int64, optional) are the original ids used for depth-tie
+    breaking and reported in ``inst_prim_ids`` (render_image's ``subset``).
+    ``out`` may pre-supply output tensors (e.g. slices of a batch buffer)
+    under the RenderOutput field names.  ``page_mask`` (device uint8 per
+    128-row page: its number of live leading rows, 0..128) restricts the
+    render to those rows (the paged device pool of ``offload``).
     """
     if not isinstance(gaussians, GaussianModel):
         raise InvalidInputError("gaussians must be a GaussianModel (device SoA)")
@@ -268,7 +273,10 @@ def render(camera, gaussians: GaussianModel, tile_size: int = 16, background=(0.
         prim_ids = prim_ids.to(device=dev, dtype=torch.int64).contiguous()
     fr = _lib.Frame(_ptr(rgb), _ptr(alpha), _ptr(depth), _ptr(trans), _ptr(touched), _ptr(kept),
                     _ptr(ranges), _ptr(nproc))
-    g = gaussians._abi(prim_ids)
+    if page_mask is not None and (page_mask.dtype != torch.uint8 or page_mask.device != dev
+                                  or page_mask.numel() < -(-n // (1 << int(page_shift)))):
+        raise InvalidInputError("page_mask must be a device uint8 tensor covering every page")
+    g = gaussians._abi(prim_ids, page_mask, page_shift if page_mask is not None else 0)
     cam = abi_camera(camera)
     st = abi_settings(ts, sh_eval_degree, background,
                       _lib.LMGS_FLAG_STAGE_TIMES if stage_times else 0)
