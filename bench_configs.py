@@ -8,6 +8,10 @@ One JSON line per configuration (BASELINE.json `configs`):
   bw  training step: render_loss_and_grads over 4 views of
       the c2 scene (1M Gaussians, 1080p): forward, fp64 backward of the blend,
       chain to SH/logits; the backward kernel alone is timed too
+  stream  offload-fed rendering: the c3 scene (6M, SH3,
+      1080p) streamed through a FrustumSession whose device budget is 40 % of
+      the model, 64 frames along a sweep that sees 19-37 % of it; against the
+      same frames rendered with the whole model resident
   c5  50M-Gaussian city in 8 spatial blocks (6.25M each), 1080p: every block
       rendered with background 0 into (premultiplied RGB, T, depth) layers and
       composited front to back in block order (the single-GPU run of the block
@@ -91,6 +95,50 @@ def train_config(n: int, w: int, h: int, views: int, steps: int) -> dict:
             "instances_view0": fwd.n_instances}
 
 
+def stream_config(n: int, frames: int, budget_frac: float) -> dict:
+    from paper_2503_21364_b200 import offload as o
+    from paper_2503_21364_b200.camera import look_at_camera
+
+    g = scenes.synthetic_gaussians(n, seed=0)
+    xs = np.linspace(-3.0, 3.0, frames)
+    cams = [look_at_camera((x, -1.0, 0.3), (x + 1.0, 3.0, 0.0), fov_deg=40.0, width=1920,
+                           height=1080, near=0.01, far=300.0) for x in xs]
+    budget = int(budget_frac * n * o.ref_row_bytes(16))
+    cfg = o.SessionConfig(mode="frustum_voxel", budget_bytes=budget, voxel_size=0.5,
+                          sh_eval_degree=3)
+    t0 = time.perf_counter()
+    sess = o.FrustumSession(g, cfg)
+    setup_s = time.perf_counter() - t0
+    for cam in cams[:2]:  # warm-up (first loads, allocations)
+        sess.step(cam)
+    torch.cuda.synchronize()
+    bytes0, loads0 = sess.store.stats.bytes_in, sess.store.stats.loads
+    rows0 = sum(e - s for v, (s, e) in sess.store.host.groups.items())
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    a.record()
+    rows = 0
+    for cam in cams:
+        _, k = sess.step(cam)
+        rows += k
+    b.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    ms = a.elapsed_time(b)
+    ref_bytes = sess.store.stats.bytes_in - bytes0
+    dev_bytes = ref_bytes // o.ref_row_bytes(16) * (o.row_bytes(16) + 8)
+    model = GaussianModel.from_host(g, validate=False)
+    ms_static = _events_ms(lambda: [render(c, model, 16, (0.0, 0.0, 0.0), 3) for c in cams], 1, 1)
+    return {"config": "stream", "gaussians": n, "frames": frames, "width": 1920, "height": 1080,
+            "budget_frac": budget_frac, "voxels": sess.index.n_voxels,
+            "frames_per_s": frames / (ms / 1e3), "ms_per_frame": ms / frames,
+            "wall_frames_per_s": frames / wall,
+            "static_full_ms_per_frame": ms_static / frames,
+            "rows_rendered_per_frame": rows / frames, "loads": sess.store.stats.loads - loads0,
+            "h2d_gb": dev_bytes / 1e9, "h2d_gbs": dev_bytes / (ms / 1e3) / 1e9,
+            "stalls_virtual": sess.stalls, "setup_s": setup_s, "host_rows": rows0}
+
+
 def city_config(per_block: int, steps: int) -> dict:
     t0 = time.perf_counter()
     city = scenes.city_scene(per_block=per_block)
@@ -169,6 +217,8 @@ def main():
             line = batch_config("c4", 6_000_000, 3840, 2160, 8, a.steps)
         elif c == "bw":
             line = train_config(1_000_000, 1920, 1080, 4, a.steps)
+        elif c == "stream":
+            line = stream_config(6_000_000, 64, 0.4)
         elif c == "c5":
             line = city_config(6_250_000, a.steps)
         else:
