@@ -120,9 +120,11 @@ static_assert(kPreThreads == 128, "paged sets map one K1 block to one 128-row pa
 template <bool SMEM>
 __device__ __forceinline__ uint32_t process_one(const PreprocessArgs& a, int64_t i, double m0, double m1,
                                             double m2, float4 q, double s0, double s1, double s2,
-                                            float logit, const float* sh, bool* keep_out) {
+                                            float logit, const float* sh, bool* keep_out,
+                                            uint64_t* zbits_out) {
   bool keep = false;
   uint32_t cnt = 0;
+  uint64_t zb = 0;
   {
     const CamArgs& cam = a.cam;
     // p = means @ r_wc.T + t_wc (195): MKL FMA chain, then + t
@@ -145,7 +147,8 @@ __device__ __forceinline__ uint32_t process_one(const PreprocessArgs& a, int64_t
       a.rects[i] = cnt ? pack_rect(x0, y0, x1, y1) : 0;  // read only for visible splats
       // off-screen splats sort behind every visible one (K2 orders only the
       // n_vis visible splats)
-      a.depth_keys[i] = cnt ? (uint64_t)__double_as_longlong(z) : kCulledKey;
+      zb = (uint64_t)__double_as_longlong(z);
+      a.depth_keys[i] = cnt ? zb : kCulledKey;
       // conic (_blend 309-310), fp64 then pre-scaled to the exp2 domain in fp32
       const double det = ca * cc - cb * cb;
       const double ica = cc / det, icb = -cb / det, icc = ca / det;
@@ -189,6 +192,7 @@ __device__ __forceinline__ uint32_t process_one(const PreprocessArgs& a, int64_t
     }
   }
   *keep_out = keep;
+  *zbits_out = zb;
   return cnt;
 }
 
@@ -197,13 +201,13 @@ __device__ __forceinline__ uint32_t process_one(const PreprocessArgs& a, int64_t
 // One atomic per counter per CTA: per-warp atomics on these five addresses
 // serialised in L2 and doubled the kernel's time.
 __device__ __forceinline__ void count_kept(const PreprocessArgs& a, bool keep, uint32_t cnt,
-                                           int64_t i) {
+                                           uint64_t zbits) {
   __shared__ unsigned long long s_acc[kPreThreads / 32][5];
   const unsigned ballot = __ballot_sync(0xffffffffu, keep);
   const unsigned vis = __ballot_sync(0xffffffffu, cnt > 0);
   unsigned long long k = cnt;
   unsigned long long zlo = ~0ull, zhi = 0ull;
-  if (cnt) zlo = zhi = a.depth_keys[i];
+  if (cnt) zlo = zhi = zbits;
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     k += __shfl_xor_sync(0xffffffffu, k, o);
@@ -250,15 +254,16 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess_direct(PreprocessArg
   const int64_t i = first + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool keep = false;
   uint32_t cnt = 0;
+  uint64_t zb = 0;
   if (i < a.n && a.page_mask && (int)(i & 127) >= (int)a.page_mask[i >> 7]) {
     cull_row(a, i);
   } else if (i < a.n) {
     const float4 q = __ldg(reinterpret_cast<const float4*>(a.quats) + i);
     cnt = process_one<false>(a, i, a.means[3 * i], a.means[3 * i + 1], a.means[3 * i + 2], q,
                              a.scales[3 * i], a.scales[3 * i + 1], a.scales[3 * i + 2],
-                             a.logits[i], a.sh + i * a.sh_coeffs * 3, &keep);
+                             a.logits[i], a.sh + i * a.sh_coeffs * 3, &keep, &zb);
   }
-  count_kept(a, keep, cnt, i);
+  count_kept(a, keep, cnt, zb);
 }
 
 // ---------------------------------------------------------------------------
@@ -279,7 +284,7 @@ __global__ void __launch_bounds__(kPreThreads, LMGS_PRE_MIN_CTAS) k_preprocess_t
   const int64_t i0 = (int64_t)blockIdx.x * kPreThreads;
   if (a.page_mask && a.page_mask[i0 >> 7] == 0) {  // the block is one inactive page
     cull_row(a, i0 + tid);
-    count_kept(a, false, 0, i0 + tid);
+    count_kept(a, false, 0, 0);
     return;
   }
   if (tid == 0) {
@@ -305,14 +310,15 @@ __global__ void __launch_bounds__(kPreThreads, LMGS_PRE_MIN_CTAS) k_preprocess_t
   a.sh_wait = &s_bar[1];
   bool keep = false;
   uint32_t cnt = 0;
+  uint64_t zb = 0;
   if (a.page_mask && tid >= (int)a.page_mask[i0 >> 7]) {  // past the page's live rows
     cull_row(a, i);
   } else {
     cnt = process_one<true>(a, i, s_means[3 * tid], s_means[3 * tid + 1], s_means[3 * tid + 2], q,
                             s_scales[3 * tid], s_scales[3 * tid + 1], s_scales[3 * tid + 2],
-                            s_logits[tid], s_sh + tid * a.sh_coeffs * 3, &keep);
+                            s_logits[tid], s_sh + tid * a.sh_coeffs * 3, &keep, &zb);
   }
-  count_kept(a, keep, cnt, i);
+  count_kept(a, keep, cnt, zb);
   // every thread must observe the SH barrier before the block may exit
   mbar_wait(&s_bar[1], 0);
 }
