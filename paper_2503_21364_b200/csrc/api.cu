@@ -240,6 +240,7 @@ CamArgs make_cam(const lmgs_camera* cam, int ts) {
   a.width = cam->width;
   a.height = cam->height;
   a.tile_size = ts;
+  a.inv_tile = 1.0 / ts;
   a.tiles_x = (cam->width + ts - 1) / ts;
   a.tiles_y = (cam->height + ts - 1) / ts;
   return a;

@@ -40,6 +40,7 @@ __host__ __device__ inline uint64_t pack_rect(uint32_t x0, uint32_t y0, uint32_t
 struct CamArgs {
   double r[9], t[3], center[3];
   double fx, fy, cx, cy, lim_x, lim_y;
+  double inv_tile;  // 1 / tile_size (first guesses only; tile tests are exact)
   int32_t width, height, tile_size, tiles_x, tiles_y;
 };
 

@@ -22,12 +22,12 @@ namespace {
 // Inclusive tile index range [a, b] along one axis for lo/hi of a splat's
 // bbox, identical to the reference comparisons hi >= t0 and lo <= t0 + tw
 // with tw = min(ts, size - t0).  Empty when a > b.
-__device__ __forceinline__ void axis_range(double lo, double hi, int size, int ts, int nt,
-                                           int* a, int* b) {
+__device__ __forceinline__ void axis_range(double lo, double hi, int size, int ts, double its,
+                                           int nt, int* a, int* b) {
   int j;
   if (!(lo > -2.0 * ts)) j = 0;
   else if (lo > (double)size + 2.0 * ts) j = nt;
-  else j = max((int)floor(lo / (double)ts) - 2, 0);
+  else j = max((int)floor(lo * its) - 2, 0);  // a guess: the loops below are exact
   while (j < nt) {
     int end = min((j + 1) * ts, size);
     if (lo <= (double)end) break;
@@ -36,7 +36,7 @@ __device__ __forceinline__ void axis_range(double lo, double hi, int size, int t
   int k;
   if (!(hi < (double)size + 2.0 * ts)) k = nt - 1;
   else if (hi < -2.0 * ts) k = -1;
-  else k = min((int)floor(hi / (double)ts) + 2, nt - 1);
+  else k = min((int)floor(hi * its) + 2, nt - 1);
   while (k >= 0 && !((double)(k * ts) <= hi)) --k;
   *a = j;
   *b = k;
@@ -141,8 +141,10 @@ __device__ __forceinline__ uint32_t process_one(const PreprocessArgs& a, int64_t
       splat_geometry(cam, x, y, z, q, s0, s1, s2, &mx, &my, &ca, &cb, &cc, &radius);
       // tile rectangle (362-373)
       int x0, x1, y0, y1;
-      axis_range(mx - radius, mx + radius, cam.width, cam.tile_size, cam.tiles_x, &x0, &x1);
-      axis_range(my - radius, my + radius, cam.height, cam.tile_size, cam.tiles_y, &y0, &y1);
+      axis_range(mx - radius, mx + radius, cam.width, cam.tile_size, cam.inv_tile, cam.tiles_x, &x0,
+                 &x1);
+      axis_range(my - radius, my + radius, cam.height, cam.tile_size, cam.inv_tile, cam.tiles_y, &y0,
+                 &y1);
       if (x0 <= x1 && y0 <= y1) cnt = (uint32_t)(x1 - x0 + 1) * (uint32_t)(y1 - y0 + 1);
       a.rects[i] = cnt ? pack_rect(x0, y0, x1, y1) : 0;  // read only for visible splats
       // off-screen splats sort behind every visible one (K2 orders only the
@@ -150,8 +152,11 @@ __device__ __forceinline__ uint32_t process_one(const PreprocessArgs& a, int64_t
       zb = (uint64_t)__double_as_longlong(z);
       a.depth_keys[i] = cnt ? zb : kCulledKey;
       // conic (_blend 309-310), fp64 then pre-scaled to the exp2 domain in fp32
+      // (the fp32 conic below is the blend's; one reciprocal instead of three
+      // divisions changes it by < 1 fp64 ulp before the fp32 rounding)
       const double det = ca * cc - cb * cb;
-      const double ica = cc / det, icb = -cb / det, icc = ca / det;
+      const double rdet = 1.0 / det;
+      const double ica = cc * rdet, icb = -cb * rdet, icc = ca * rdet;
       const float log2_alpha =
           logit < -15.0f ? logit * (float)kLog2e : -log2f(1.0f + expf(-logit));
       float col[3] = {0.f, 0.f, 0.f};
@@ -160,8 +165,9 @@ __device__ __forceinline__ uint32_t process_one(const PreprocessArgs& a, int64_t
         const double dx = m0 - cam.center[0], dy = m1 - cam.center[1], dz = m2 - cam.center[2];
         double nrm = sqrt((dx * dx + dy * dy) + dz * dz);
         nrm = fmax(nrm, 1e-12);
+        const double rn = 1.0 / nrm;
         sh_color<SMEM>(sh, a.sh_coeffs, a.eval_degree,
-                 (float)(dx / nrm), (float)(dy / nrm), (float)(dz / nrm), col);
+                 (float)(dx * rn), (float)(dy * rn), (float)(dz * rn), col);
       }
       BlendRec rec;
       rec.mx = mx;
