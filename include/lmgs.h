@@ -16,6 +16,9 @@
  *                          (the per-tile lists the reference builds at 362-392)
  *   lmgs_render_batch      render_runtime.py:250-308 run_session's per-pose loop,
  *                          batched over camera views on one device
+ *   lmgs_render_strips     (new) spatial-block render whose layers are stored
+ *                          straight into the compositing GPUs' strip buffers;
+ *                          lmgs_signal_flags / lmgs_wait_flags order it
  *   lmgs_composite_blocks  (new) front-to-back "over" of per-block premultiplied
  *                          images; replaces render_runtime.py:189-191 (BlockSession
  *                          concatenating resident cells into one model)
@@ -187,6 +190,36 @@ int lmgs_mse_grad(const float* rgb, const void* gt, int gt_is_f64, int64_t n_val
 int lmgs_project(lmgs_context* ctx, const lmgs_gaussians* g, const lmgs_camera* cam,
                  const lmgs_settings* s, double* mean2d, double* cov2d, double* depth,
                  double* radius, float* colors, float* opacity, uint8_t* kept, void* stream);
+
+/* Spatial blocks over peer memory (the exchange fused into the blend).
+ * lmgs_render_strips renders like lmgs_render with background 0 semantics
+ * of a block layer, but writes every finished pixel of row y straight into
+ * strip y / strip_rows of the targets — typically the receive buffers of
+ * the GPUs that composite those strips, mapped into this process (NVLink
+ * peer pointers from symmetric memory), so the exchange overlaps the blend
+ * tile by tile and no separate collective moves the layers. */
+#define LMGS_MAX_STRIPS 8
+typedef struct lmgs_strip_targets {
+  int32_t n_strips;               /* 1..LMGS_MAX_STRIPS                              */
+  int32_t strip_rows;             /* rows per strip (the last may be shorter)         */
+  float* rgb[LMGS_MAX_STRIPS];    /* [strip_rows, W, 3]: C + T_final * background      */
+  float* trans[LMGS_MAX_STRIPS];  /* [strip_rows, W]: T_final (nullable)              */
+  float* depth[LMGS_MAX_STRIPS];  /* [strip_rows, W]: sum w z (nullable)              */
+} lmgs_strip_targets;
+int lmgs_render_strips(lmgs_context* ctx, const lmgs_gaussians* g, const lmgs_camera* cam,
+                       const lmgs_settings* s, const lmgs_strip_targets* targets,
+                       int32_t* touched, void* stream);
+
+/* Release-store `value` to n device flags (system scope, after a system
+ * fence): tells the owners of the strips written by lmgs_render_strips that
+ * this block's layers are complete.  flags is a host array of (peer) device
+ * pointers, n <= 64. */
+int lmgs_signal_flags(uint32_t* const* flags, int32_t n, uint32_t value, void* stream);
+
+/* Stream-ordered wait until every flags[i] >= value (acquire, system scope),
+ * i < n; the next work on `stream` (e.g. lmgs_composite_blocks over the
+ * received layers) sees the peers' stores. */
+int lmgs_wait_flags(const uint32_t* flags, int32_t n, uint32_t value, void* stream);
 
 /* Front-to-back composite of n_blocks per-block renders (background 0):
  * rgb_b premultiplied [H*W*3], trans_b [H*W] (T_final), depth_b [H*W]

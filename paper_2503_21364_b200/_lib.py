@@ -32,7 +32,8 @@ EXPORTS = ("lmgs_abi_version", "lmgs_context_create", "lmgs_context_destroy", "l
            "lmgs_render", "lmgs_render_batch", "lmgs_get_stats", "lmgs_copy_instances",
            "lmgs_project", "lmgs_composite_blocks", "lmgs_checkpoint_info_read",
            "lmgs_checkpoint_load", "lmgs_checkpoint_save", "lmgs_encode_rgb8",
-           "lmgs_backward", "lmgs_mse_grad")
+           "lmgs_backward", "lmgs_mse_grad", "lmgs_render_strips", "lmgs_signal_flags",
+           "lmgs_wait_flags")
 
 
 class Camera(ctypes.Structure):
@@ -50,6 +51,14 @@ class Gaussians(ctypes.Structure):
 class Settings(ctypes.Structure):
     _fields_ = [("tile_size", I32), ("sh_eval_degree", I32), ("background", D * 3),
                 ("flags", U32)]
+
+
+MAX_STRIPS = 8
+
+
+class StripTargets(ctypes.Structure):
+    _fields_ = [("n_strips", I32), ("strip_rows", I32), ("rgb", P * MAX_STRIPS),
+                ("trans", P * MAX_STRIPS), ("depth", P * MAX_STRIPS)]
 
 
 class Frame(ctypes.Structure):
@@ -105,6 +114,10 @@ def lib():
     L.lmgs_backward.argtypes = [P, ctypes.POINTER(Gaussians), ctypes.POINTER(Camera),
                                 ctypes.POINTER(Settings), P, P, P, P, P, P, P, P, P, P]
     L.lmgs_mse_grad.argtypes = [P, P, ctypes.c_int, I64, P, P, P]
+    L.lmgs_render_strips.argtypes = [P, ctypes.POINTER(Gaussians), ctypes.POINTER(Camera),
+                                     ctypes.POINTER(Settings), ctypes.POINTER(StripTargets), P, P]
+    L.lmgs_signal_flags.argtypes = [ctypes.POINTER(P), I32, U32, P]
+    L.lmgs_wait_flags.argtypes = [P, I32, U32, P]
     got = L.lmgs_abi_version()
     if got != ABI_VERSION:
         raise LmgsError(f"liblmgs ABI {got} != expected {ABI_VERSION}")

@@ -290,7 +290,8 @@ struct StageTimer {
 };
 
 int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
-               const lmgs_settings* st, const lmgs_frame* out, cudaStream_t s) {
+               const lmgs_settings* st, const lmgs_frame* out, cudaStream_t s,
+               const lmgs_strip_targets* strips = nullptr) {
   const bool timed = (st->flags & LMGS_FLAG_STAGE_TIMES) && c->events_ok;
   StageTimer tm{c, s, timed};
   const CamArgs ca = make_cam(cam, st->tile_size);
@@ -428,6 +429,15 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
   ba.touched = out->touched;
   ba.n_processed = out->n_processed;
   ba.work_counter = &sc->blend_counter;
+  if (strips) {
+    ba.n_strips = strips->n_strips;
+    ba.strip_rows = strips->strip_rows;
+    for (int i = 0; i < strips->n_strips; ++i) {
+      ba.srgb[i] = strips->rgb[i];
+      ba.strans[i] = strips->trans[i];
+      ba.sdepth[i] = strips->depth[i];
+    }
+  }
   if (int r = launch_blend(ba, s)) return fail(c, r, "unsupported tile size");
   launched += tiles > 0 ? 1 : 0;
   tm.end(4);
@@ -495,6 +505,22 @@ int lmgs_render(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
   if (!out || !out->rgb) return fail(c, LMGS_ERR_INVALID, "frame.rgb is required");
   DeviceGuard guard(c->device);
   return render_one(c, g, cam, s, out, static_cast<cudaStream_t>(stream));
+}
+
+int lmgs_render_strips(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
+                       const lmgs_settings* s, const lmgs_strip_targets* t, int32_t* touched,
+                       void* stream) {
+  if (int r = validate(c, g, cam, s)) return r;
+  if (!t || t->n_strips < 1 || t->n_strips > LMGS_MAX_STRIPS || t->strip_rows < 1 ||
+      (int64_t)t->n_strips * t->strip_rows < cam->height ||
+      (int64_t)(t->n_strips - 1) * t->strip_rows >= cam->height)
+    return fail(c, LMGS_ERR_INVALID, "strip targets must cover the image rows exactly");
+  for (int i = 0; i < t->n_strips; ++i)
+    if (!t->rgb[i]) return fail(c, LMGS_ERR_INVALID, "null strip rgb target");
+  lmgs_frame f{};
+  f.touched = touched;
+  DeviceGuard guard(c->device);
+  return render_one(c, g, cam, s, &f, static_cast<cudaStream_t>(stream), t);
 }
 
 int lmgs_render_batch(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cams,

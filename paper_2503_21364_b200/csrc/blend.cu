@@ -227,13 +227,7 @@ __global__ void __launch_bounds__(256) k_blend(BlendArgs a) {
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
     if (!valid[p]) continue;
-    const int64_t o = (int64_t)(y0 + lys[p]) * a.width + (x0 + lxs[p]);
-    a.rgb[3 * o + 0] = fmaf(T[p], a.bg[0], C0[p]);
-    a.rgb[3 * o + 1] = fmaf(T[p], a.bg[1], C1[p]);
-    a.rgb[3 * o + 2] = fmaf(T[p], a.bg[2], C2[p]);
-    if (a.alpha) a.alpha[o] = 1.0f - T[p];
-    if (a.depth) a.depth[o] = D[p];
-    if (a.trans) a.trans[o] = T[p];
+    put_pixel(a, x0 + lxs[p], y0 + lys[p], T[p], C0[p], C1[p], C2[p], D[p]);
   }
 }
 
@@ -452,13 +446,7 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
       if (!valid[q]) continue;
-      const int64_t o = (int64_t)(y0 + ly[q]) * a.width + (x0 + lx);
-      a.rgb[3 * o + 0] = fmaf(T[q], a.bg[0], C0[q]);
-      a.rgb[3 * o + 1] = fmaf(T[q], a.bg[1], C1[q]);
-      a.rgb[3 * o + 2] = fmaf(T[q], a.bg[2], C2[q]);
-      if (a.alpha) a.alpha[o] = 1.0f - T[q];
-      if (a.depth) a.depth[o] = D[q];
-      if (a.trans) a.trans[o] = T[q];
+      put_pixel(a, x0 + lx, y0 + ly[q], T[q], C0[q], C1[q], C2[q], D[q]);
     }
   }
 }

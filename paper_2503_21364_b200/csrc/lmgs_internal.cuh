@@ -210,7 +210,38 @@ struct BlendArgs {
   int32_t* touched;
   int32_t* n_processed;
   int* work_counter;  // device scalar for the persistent 16x16 kernel (nullable)
+  // strip targets (lmgs_render_strips): when n_strips > 0, pixel row y goes to
+  // strip y / strip_rows at row y % strip_rows of srgb / strans / sdepth
+  // (possibly peer-GPU pointers) instead of rgb / alpha / depth / trans
+  int32_t n_strips, strip_rows;
+  float* srgb[8];
+  float* strans[8];
+  float* sdepth[8];
 };
+
+// the one place the blend kernels write a finished pixel
+__device__ __forceinline__ void put_pixel(const BlendArgs& a, int x, int y, float T, float c0,
+                                          float c1, float c2, float d) {
+  const float r = fmaf(T, a.bg[0], c0), g = fmaf(T, a.bg[1], c1), b = fmaf(T, a.bg[2], c2);
+  if (a.n_strips == 0) {
+    const int64_t o = (int64_t)y * a.width + x;
+    a.rgb[3 * o + 0] = r;
+    a.rgb[3 * o + 1] = g;
+    a.rgb[3 * o + 2] = b;
+    if (a.alpha) a.alpha[o] = 1.0f - T;
+    if (a.depth) a.depth[o] = d;
+    if (a.trans) a.trans[o] = T;
+  } else {
+    const int s = y / a.strip_rows;
+    const int64_t o = (int64_t)(y - s * a.strip_rows) * a.width + x;
+    float* rgb = a.srgb[s];
+    rgb[3 * o + 0] = r;
+    rgb[3 * o + 1] = g;
+    rgb[3 * o + 2] = b;
+    if (a.strans[s]) a.strans[s][o] = T;
+    if (a.sdepth[s]) a.sdepth[s][o] = d;
+  }
+}
 int launch_blend(const BlendArgs& a, cudaStream_t s);  // returns 0 or LMGS_ERR_UNSUPPORTED
 
 void launch_fill_background(float* rgb, float* alpha, float* depth, float* trans, int64_t n_pix,

@@ -82,3 +82,56 @@ void launch_composite(const float* rgb, const float* trans, const float* depth, 
 }
 
 }  // namespace lmgs
+
+// ---------------------------------------------------------------------------
+// Peer flags for the strip exchange (lmgs_render_strips): the producer
+// fences its peer stores at system scope and release-stores the epoch into
+// each owner's flag; the owner's stream spins on acquire loads before the
+// composite reads the received layers.
+
+namespace lmgs {
+namespace {
+
+constexpr int kMaxFlags = 64;
+struct FlagPtrs {
+  uint32_t* p[kMaxFlags];
+};
+
+__global__ void k_signal_flags(FlagPtrs f, int n, uint32_t value) {
+  __threadfence_system();
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f.p[i]), "r"(value) : "memory");
+}
+
+__global__ void k_wait_flags(const uint32_t* flags, int n, uint32_t value) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    uint32_t v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + i) : "memory");
+    } while ((int32_t)(v - value) < 0);  // wrap-safe v >= value
+  }
+  __syncthreads();
+  __threadfence_system();
+}
+
+}  // namespace
+}  // namespace lmgs
+
+extern "C" int lmgs_signal_flags(uint32_t* const* flags, int32_t n, uint32_t value, void* stream) {
+  if (n < 0 || n > lmgs::kMaxFlags || (n > 0 && !flags)) return LMGS_ERR_INVALID;
+  if (n == 0) return LMGS_OK;
+  lmgs::FlagPtrs f{};
+  for (int i = 0; i < n; ++i) {
+    if (!flags[i]) return LMGS_ERR_INVALID;
+    f.p[i] = flags[i];
+  }
+  lmgs::k_signal_flags<<<1, 64, 0, static_cast<cudaStream_t>(stream)>>>(f, n, value);
+  return cudaGetLastError() == cudaSuccess ? LMGS_OK : LMGS_ERR_CUDA;
+}
+
+extern "C" int lmgs_wait_flags(const uint32_t* flags, int32_t n, uint32_t value, void* stream) {
+  if (n < 0 || (n > 0 && !flags)) return LMGS_ERR_INVALID;
+  if (n == 0) return LMGS_OK;
+  lmgs::k_wait_flags<<<1, 64, 0, static_cast<cudaStream_t>(stream)>>>(flags, n, value);
+  return cudaGetLastError() == cudaSuccess ? LMGS_OK : LMGS_ERR_CUDA;
+}

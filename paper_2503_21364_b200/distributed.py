@@ -213,3 +213,156 @@ class BlockParallelRenderer:
         allp = allp.reshape((world,) + tuple(packed.shape))
         out = torch.cat([allp[r, : bounds[r + 1] - bounds[r]] for r in range(world)], dim=0)
         return out[..., :3], out[..., 3], out[..., 4]
+
+
+# ---------------------------------------------------------------------------
+# spatial blocks with the exchange fused into the blend (peer memory)
+
+
+def symmetric_buffers(n_floats: int, n_flags: int, group, device):
+    """A symmetric-memory buffer of n_floats on every rank of ``group`` and the
+    peer addresses of all ranks' buffers and signal pads (NVLink mappings)."""
+    import torch.distributed._symmetric_memory as symm
+
+    buf = symm.empty(n_floats, dtype=torch.float32, device=device)
+    hdl = symm.rendezvous(buf, group)
+    if hdl.signal_pad_size < 4 * n_flags:
+        raise ValueError("signal pad too small for the block flags")
+    symmetric_buffers.handles.append(hdl)  # keep the mappings alive
+    return buf, [int(p) for p in hdl.buffer_ptrs], [int(p) for p in hdl.signal_pad_ptrs]
+
+
+symmetric_buffers.handles = []
+
+
+class PeerBlockRenderer:
+    """Spatial-block rendering whose layer exchange happens inside the blend.
+
+    Every rank owns a symmetric-memory receive buffer for its image strip
+    (rows [r*S, (r+1)*S), S = ceil(H / world)) holding all blocks' layers:
+    premultiplied RGB, T_final and depth, block-major.  A rank renders each
+    of its blocks with ``lmgs_render_strips``: the blend kernel stores every
+    finished pixel straight into the receive buffer of the strip's owner
+    through its NVLink peer mapping, so the transfer overlaps the blend tile
+    by tile and no collective moves layers.  Then it release-stores the frame
+    epoch into each owner's flag for that block (``lmgs_signal_flags``).  An
+    owner's stream waits for all blocks' flags (``lmgs_wait_flags``),
+    composites its strip front to back (``lmgs_composite_blocks``) and
+    signals "consumed" back to every producer, which waits for it before
+    overwriting the buffers in the next frame.  The finished strips are
+    gathered with one ``all_gather_into_tensor`` (``gather=True``).
+
+    Signal pad words: [0, n_blocks) = block layers received, [n_blocks,
+    n_blocks + world) = strip consumed by owner o.
+    """
+
+    def __init__(self, local_blocks: dict, block_bboxes: np.ndarray, n_blocks: int, width: int,
+                 height: int, group=None, tile_size: int = 16, sh_eval_degree: int = 3,
+                 buffers: Callable | None = None):
+        """``buffers(n_floats, n_flags) -> (local buffer tensor, [peer buffer
+        addresses], [peer flag-pad addresses])``; default: symmetric memory
+        (``symmetric_buffers``)."""
+        from .raster import context
+
+        self.local_blocks = local_blocks
+        self.block_bboxes = np.asarray(block_bboxes)
+        self.n_blocks = int(n_blocks)
+        self.w, self.h = int(width), int(height)
+        self.group = group if group is not None else dist.group.WORLD
+        self.rank = dist.get_rank(self.group)
+        self.world = dist.get_world_size(self.group)
+        if self.world > 8:
+            raise ValueError("at most 8 strips (LMGS_MAX_STRIPS)")
+        self.tile_size, self.sh_eval_degree = int(tile_size), int(sh_eval_degree)
+        self.strip = -(-self.h // self.world)
+        self.n_strips = -(-self.h // self.strip)
+        self.npix = self.strip * self.w
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        n = self.n_blocks * self.npix * CHANNELS
+        make = buffers or (lambda nf, nflag: symmetric_buffers(nf, nflag, self.group,
+                                                               self.device))
+        self.buf, self.peers, self.pads = make(n, self.n_blocks + self.world)
+        self.epoch = 0
+        self.ctx = context(self.device.index)
+        dist.barrier(group=self.group)
+
+    # byte offsets inside one receive buffer
+    def _rgb_off(self, b):
+        return 4 * (b * self.npix * 3)
+
+    def _trans_off(self, b):
+        return 4 * (self.n_blocks * self.npix * 3 + b * self.npix)
+
+    def _depth_off(self, b):
+        return 4 * (self.n_blocks * self.npix * 4 + b * self.npix)
+
+    def local_layers(self):
+        """(rgb (B, npix*3), trans (B, npix), depth (B, npix)) views of this
+        rank's receive buffer."""
+        nb, npx = self.n_blocks, self.npix
+        rgb = self.buf[: nb * npx * 3].view(nb, npx * 3)
+        trans = self.buf[nb * npx * 3: nb * npx * 4].view(nb, npx)
+        depth = self.buf[nb * npx * 4:].view(nb, npx)
+        return rgb, trans, depth
+
+    def render(self, camera, background=(0.0, 0.0, 0.0), gather: bool = True):
+        import ctypes
+
+        from . import _lib
+        from .raster import abi_camera, abi_settings, composite_blocks
+
+        L = _lib.lib()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        self.epoch += 1
+        ep = self.epoch
+        world, nb = self.world, self.n_blocks
+        # the owners must have consumed the previous frame's layers
+        _lib.check(None, L.lmgs_wait_flags(self.pads[self.rank] + 4 * nb, world,
+                                           (ep - 1) & 0xFFFFFFFF, stream), "lmgs_wait_flags")
+        cam = abi_camera(camera)
+        st = abi_settings(self.tile_size, self.sh_eval_degree, (0.0, 0.0, 0.0))
+        for b in assign_blocks(nb, world)[self.rank]:
+            model = self.local_blocks[b]
+            t = _lib.StripTargets()
+            t.n_strips, t.strip_rows = self.n_strips, self.strip
+            for o in range(self.n_strips):
+                t.rgb[o] = self.peers[o] + self._rgb_off(b)
+                t.trans[o] = self.peers[o] + self._trans_off(b)
+                t.depth[o] = self.peers[o] + self._depth_off(b)
+            g = model._abi()
+            _lib.check(self.ctx.handle, L.lmgs_render_strips(
+                self.ctx.handle, ctypes.byref(g), ctypes.byref(cam), ctypes.byref(st),
+                ctypes.byref(t), None, stream), "lmgs_render_strips")
+            flags = (ctypes.c_void_p * self.n_strips)(
+                *[self.pads[o] + 4 * b for o in range(self.n_strips)])
+            _lib.check(None, L.lmgs_signal_flags(flags, self.n_strips, ep, stream),
+                       "lmgs_signal_flags")
+        # my strip: wait for every block, composite front to back
+        rgb_s, alpha_s, depth_s = None, None, None
+        if self.rank < self.n_strips:
+            _lib.check(None, L.lmgs_wait_flags(self.pads[self.rank], nb, ep, stream),
+                       "lmgs_wait_flags")
+            order = block_order(np.asarray(camera.center), self.block_bboxes)
+            rgb, trans, depth = self.local_layers()
+            rows = min(self.strip, self.h - self.rank * self.strip)
+            c_rgb, c_alpha, c_depth = composite_blocks(
+                rgb.view(nb, self.strip, self.w, 3), trans.view(nb, self.strip, self.w), order,
+                background, depth.view(nb, self.strip, self.w))
+            rgb_s, alpha_s, depth_s = c_rgb[:rows], c_alpha[:rows], c_depth[:rows]
+        consumed = (ctypes.c_void_p * world)(*[self.pads[p] + 4 * (nb + self.rank)
+                                               for p in range(world)])
+        _lib.check(None, L.lmgs_signal_flags(consumed, world, ep, stream), "lmgs_signal_flags")
+        if not gather:
+            return rgb_s, alpha_s, depth_s
+        packed = torch.zeros((self.strip, self.w, CHANNELS), dtype=torch.float32,
+                             device=self.device)
+        if rgb_s is not None:
+            rows = rgb_s.shape[0]
+            packed[:rows, :, :3] = rgb_s
+            packed[:rows, :, 3] = alpha_s
+            packed[:rows, :, 4] = depth_s
+        allp = torch.empty((world * self.strip, self.w, CHANNELS), dtype=torch.float32,
+                           device=self.device)
+        dist.all_gather_into_tensor(allp, packed, group=self.group)
+        out = allp[: self.h]
+        return out[..., :3], out[..., 3], out[..., 4]
