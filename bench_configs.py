@@ -12,6 +12,10 @@ One JSON line per configuration (BASELINE.json `configs`):
       1080p) streamed through a FrustumSession whose device budget is 40 % of
       the model, 64 frames along a sweep that sees 19-37 % of it; against the
       same frames rendered with the whole model resident
+  c5peer  the c5 frame through PeerBlockRenderer (exchange fused into the
+      blend, symmetric memory) on a 1-rank NCCL group, against the NCCL-exchange
+      BlockParallelRenderer on the same rank (the fused path's overhead; the
+      NVLink transfer itself needs >1 GPU)
   c5  50M-Gaussian city in 8 spatial blocks (6.25M each), 1080p: every block
       rendered with background 0 into (premultiplied RGB, T, depth) layers and
       composited front to back in block order (the single-GPU run of the block
@@ -139,6 +143,34 @@ def stream_config(n: int, frames: int, budget_frac: float) -> dict:
             "stalls_virtual": sess.stalls, "setup_s": setup_s, "host_rows": rows0}
 
 
+def c5peer_config(per_block: int, steps: int) -> dict:
+    import os
+
+    import torch.distributed as dist
+
+    from paper_2503_21364_b200.distributed import BlockParallelRenderer, PeerBlockRenderer
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29671")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    city = scenes.city_scene(per_block=per_block)
+    models = {b: GaussianModel.from_host(g, validate=False) for b, g in enumerate(city.blocks)}
+    cam = city.camera
+    nb = len(models)
+    peer = PeerBlockRenderer(models, city.block_bboxes, nb, cam.width, cam.height)
+    nccl = BlockParallelRenderer(models, city.block_bboxes, nb)
+    ms_peer = _events_ms(lambda: peer.render(cam), steps, 1)
+    ms_nccl = _events_ms(lambda: nccl.render(cam), steps, 1)
+    a = peer.render(cam)
+    b = nccl.render(cam)
+    torch.cuda.synchronize()
+    same = bool(torch.equal(a[0], b[0]))
+    dist.destroy_process_group()
+    return {"config": "c5peer", "gaussians": per_block * nb, "blocks": nb,
+            "ms_per_frame_peer_fused": ms_peer, "ms_per_frame_nccl_exchange": ms_nccl,
+            "bit_equal": same, "ranks": 1}
+
+
 def city_config(per_block: int, steps: int) -> dict:
     t0 = time.perf_counter()
     city = scenes.city_scene(per_block=per_block)
@@ -219,6 +251,8 @@ def main():
             line = train_config(1_000_000, 1920, 1080, 4, a.steps)
         elif c == "stream":
             line = stream_config(6_000_000, 64, 0.4)
+        elif c == "c5peer":
+            line = c5peer_config(6_250_000, a.steps)
         elif c == "c5":
             line = city_config(6_250_000, a.steps)
         else:
