@@ -283,6 +283,7 @@ struct BackwardArgs {
   int64_t* steps_seen;      // [n] DensifyStats, accumulated (nullable)
 };
 int launch_backward(const BackwardArgs& a, int tiles, cudaStream_t s);  // kernels launched or -err
+int launch_backward_replay(const BackwardArgs& a, int tiles, cudaStream_t s);  // backward.cu
 
 constexpr int kMaxCompositeBlocks = 64;
 // `order` is a host array (n_blocks <= kMaxCompositeBlocks), passed by value.
