@@ -105,6 +105,9 @@ typedef struct lmgs_settings {
 } lmgs_settings;
 
 #define LMGS_FLAG_STAGE_TIMES 1u  /* record per-stage CUDA events (lmgs_get_stats) */
+#define LMGS_FLAG_NO_TOUCHED_FIX 2u /* skip K7b: touched may then differ from the
+                                       reference where fp32 and fp64 transmittance
+                                       straddle TERM_EPS (a few per million)       */
 
 /* Per-view outputs (device).  rgb is required; the rest may be NULL. */
 typedef struct lmgs_frame {
@@ -159,6 +162,10 @@ int lmgs_get_stats(lmgs_context* ctx, lmgs_stats* out);
  * then by (fp64 depth, prim id).  Either pointer may be NULL.  Device buffers,
  * K entries. */
 int lmgs_copy_instances(lmgs_context* ctx, uint64_t* keys, int64_t* prim_ids, void* stream);
+
+/* Pixels the last render queued for the exact-touched replay (K7b):
+ * synchronises with the render's stream. */
+int lmgs_touched_fix_count(lmgs_context* ctx, uint32_t* count);
 
 /* Backward of the blend for the view last rendered on ctx (same Gaussians,
  * camera and settings): backward_render (gaussian_core.py:

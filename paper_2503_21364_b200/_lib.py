@@ -25,6 +25,7 @@ U32 = ctypes.c_uint32
 (LMGS_OK, LMGS_ERR_INVALID, LMGS_ERR_CUDA, LMGS_ERR_OOM, LMGS_ERR_UNSUPPORTED, LMGS_ERR_FORMAT,
  LMGS_ERR_IO) = range(7)
 LMGS_FLAG_STAGE_TIMES = 1
+LMGS_FLAG_NO_TOUCHED_FIX = 2
 MAX_STAGES = 8
 
 # every symbol include/lmgs.h declares
@@ -33,7 +34,7 @@ EXPORTS = ("lmgs_abi_version", "lmgs_context_create", "lmgs_context_destroy", "l
            "lmgs_project", "lmgs_composite_blocks", "lmgs_checkpoint_info_read",
            "lmgs_checkpoint_load", "lmgs_checkpoint_save", "lmgs_encode_rgb8",
            "lmgs_backward", "lmgs_mse_grad", "lmgs_render_strips", "lmgs_signal_flags",
-           "lmgs_wait_flags")
+           "lmgs_wait_flags", "lmgs_touched_fix_count")
 
 
 class Camera(ctypes.Structure):
@@ -118,6 +119,7 @@ def lib():
                                      ctypes.POINTER(Settings), ctypes.POINTER(StripTargets), P, P]
     L.lmgs_signal_flags.argtypes = [ctypes.POINTER(P), I32, U32, P]
     L.lmgs_wait_flags.argtypes = [P, I32, U32, P]
+    L.lmgs_touched_fix_count.argtypes = [P, ctypes.POINTER(U32)]
     got = L.lmgs_abi_version()
     if got != ABI_VERSION:
         raise LmgsError(f"liblmgs ABI {got} != expected {ABI_VERSION}")
@@ -159,6 +161,13 @@ class Context:
             self.close()
         except Exception:
             pass
+
+    def touched_fix_count(self) -> int:
+        """Pixels the last render replayed for exact touched counts (syncs)."""
+        v = ctypes.c_uint32()
+        check(self.handle, lib().lmgs_touched_fix_count(self.handle, ctypes.byref(v)),
+              "lmgs_touched_fix_count")
+        return int(v.value)
 
     def stats(self) -> dict:
         s = Stats()

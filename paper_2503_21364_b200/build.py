@@ -28,7 +28,8 @@ INCLUDE = PKG.parent / "include"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
           f"-I{INCLUDE}", "--expt-relaxed-constexpr"]
-PER_FILE = {"preprocess.cu": ["-fmad=false"], "backward_exact.cu": ["-fmad=false"]}
+PER_FILE = {"preprocess.cu": ["-fmad=false"], "backward_exact.cu": ["-fmad=false"],
+            "touched_fix.cu": ["-fmad=false"]}
 # extra nvcc flags for tuning experiments (e.g. "-DLMGS_PRE_MIN_CTAS=6")
 EXTRA = os.environ.get("LMGS_NVCC_FLAGS", "").split()
 

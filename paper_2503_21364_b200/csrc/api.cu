@@ -94,6 +94,7 @@ struct Scalars {  // device-side small state
   unsigned long long zrange[2];  // min / max visible fp64 depth bits
   uint32_t emit_ticket;
   int blend_counter;
+  uint32_t fix_count;  // pixels queued for the exact-touched replay (K7b)
   DevSlots slots;
 };
 
@@ -103,7 +104,7 @@ struct lmgs_context {
   int device = 0;
   int sms = 148;
   std::string err;
-  DevBuf gbuf, tbuf, ibuf, bwbuf;
+  DevBuf gbuf, tbuf, ibuf, bwbuf, fixbuf;
   Scalars* d_scal = nullptr;
   uint64_t* h_pinned = nullptr;  // [0..2] = n_kept, n_vis, K
   cudaEvent_t ev[2 * kNumStages] = {};
@@ -429,6 +430,18 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
   ba.touched = out->touched;
   ba.n_processed = out->n_processed;
   ba.work_counter = &sc->blend_counter;
+  const bool fix = out->touched != nullptr && !(st->flags & LMGS_FLAG_NO_TOUCHED_FIX);
+  if (fix) {
+    const int64_t cap = (int64_t)cam->width * cam->height / 8 + 1024;
+    if ((size_t)cap * 4 > c->fixbuf.bytes) {
+      LMGS_CUDA(c, cudaStreamSynchronize(s));
+      LMGS_CUDA(c, c->fixbuf.reserve((size_t)cap * 4));
+    }
+    LMGS_CUDA(c, cudaMemsetAsync(&sc->fix_count, 0, sizeof(uint32_t), s));
+    ba.fix_count = &sc->fix_count;
+    ba.fix_list = static_cast<uint32_t*>(c->fixbuf.ptr);
+    ba.fix_cap = (int32_t)(c->fixbuf.bytes / 4);
+  }
   if (strips) {
     ba.n_strips = strips->n_strips;
     ba.strip_rows = strips->strip_rows;
@@ -440,6 +453,24 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
   }
   if (int r = launch_blend(ba, s)) return fail(c, r, "unsupported tile size");
   launched += tiles > 0 ? 1 : 0;
+  if (fix && tiles > 0) {
+    TouchedFixArgs fa{};
+    fa.keys_slot = &sc->slots.inst_keys;
+    fa.ranges = ranges;
+    fa.recs = c->recs;
+    fa.tile_size = st->tile_size;
+    fa.tiles_x = ca.tiles_x;
+    fa.fix_count = &sc->fix_count;
+    fa.fix_list = ba.fix_list;
+    fa.fix_cap = ba.fix_cap;
+    fa.touched = out->touched;
+    fa.means = g->means;
+    fa.quats = g->quats;
+    fa.scales = g->scales;
+    fa.logits = g->opacity_logits;
+    fa.cam = ca;
+    launched += launch_touched_fix(fa, s);
+  }
   tm.end(4);
   c->stats.n_launches = launched;
   c->last_timed = timed;
@@ -489,6 +520,7 @@ void lmgs_context_destroy(lmgs_context* c) {
   c->tbuf.release();
   c->ibuf.release();
   c->bwbuf.release();
+  c->fixbuf.release();
   if (c->d_scal) cudaFree(c->d_scal);
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   for (int i = 0; i < 2 * kNumStages; ++i)
@@ -505,6 +537,13 @@ int lmgs_render(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
   if (!out || !out->rgb) return fail(c, LMGS_ERR_INVALID, "frame.rgb is required");
   DeviceGuard guard(c->device);
   return render_one(c, g, cam, s, out, static_cast<cudaStream_t>(stream));
+}
+
+int lmgs_touched_fix_count(lmgs_context* c, uint32_t* count) {
+  if (!c || !count) return LMGS_ERR_INVALID;
+  DeviceGuard guard(c->device);
+  LMGS_CUDA(c, cudaMemcpy(count, &c->d_scal->fix_count, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return LMGS_OK;
 }
 
 int lmgs_render_strips(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,

@@ -29,6 +29,21 @@ namespace {
 // smallest float >= 1e-4: (double)T >= 1e-4  <=>  T >= kTermEpsF for fp32 T
 constexpr float kTermEpsF = 1.00000005e-4f;
 constexpr float kSigmaMaxF = 0.9999f;
+
+// Exact `touched` (K7b): a pixel whose fp32 transmittance passed TERM_EPS
+// within a relative band of kFixBand — where fp32 and the reference's fp64
+// could disagree on which splats the pixel still takes — is queued for an
+// fp64 replay that corrects the counts.  Tc = T before the last splat the
+// pixel took while active (its T before the crossing, once it crossed).
+constexpr float kFixBand = 1e-4f;  // 10x the measured fp32/fp64 T gap (< 1e-5 at the crossing)
+__device__ __forceinline__ bool crossing_uncertain(float T, float Tc) {
+  if (T < kTermEpsF) return Tc < kTermEpsF * (1.0f + kFixBand) || T >= kTermEpsF * (1.0f - kFixBand);
+  return T < kTermEpsF * (1.0f + kFixBand);
+}
+__device__ __forceinline__ void queue_fix(const BlendArgs& a, int tile, int lx, int ly) {
+  const uint32_t slot = atomicAdd(a.fix_count, 1u);
+  if (slot < (uint32_t)a.fix_cap) a.fix_list[slot] = ((uint32_t)tile << 12) | (ly << 6) | lx;
+}
 constexpr int kBatch = 256;
 constexpr int kMaxWarps = 8;
 
@@ -68,7 +83,7 @@ __global__ void __launch_bounds__(256) k_blend(BlendArgs a) {
   const int2 range = a.ranges[tile];
   const uint64_t* __restrict__ list = static_cast<const uint64_t*>(*a.keys_slot);
 
-  float T[PPT], C0[PPT], C1[PPT], C2[PPT], D[PPT], px[PPT], py[PPT];
+  float T[PPT], C0[PPT], C1[PPT], C2[PPT], D[PPT], px[PPT], py[PPT], Tc[PPT];
   int lxs[PPT], lys[PPT], last[PPT];
   bool valid[PPT];
   float bx0 = 3.0e38f, bx1 = -3.0e38f, by0 = 3.0e38f, by1 = -3.0e38f;
@@ -88,6 +103,7 @@ __global__ void __launch_bounds__(256) k_blend(BlendArgs a) {
     lys[p] = ly;
     valid[p] = pix < ts * ts && x0 + lx < a.width && y0 + ly < a.height;
     T[p] = valid[p] ? 1.0f : 0.0f;  // invalid pixels never go active
+    Tc[p] = 1.0f;
     C0[p] = C1[p] = C2[p] = D[p] = 0.0f;
     px[p] = (float)lx + 0.5f;  // _pixel_centers (335-337), tile-local
     py[p] = (float)ly + 0.5f;
@@ -119,7 +135,8 @@ __global__ void __launch_bounds__(256) k_blend(BlendArgs a) {
       const BlendRec rec = a.recs[id];
       const double mxl = rec.mx - (double)x0, myl = rec.my - (double)y0;
       const double ax = fabs(mxl) + ts, ay = fabs(myl) + ts;
-      const double band = (rec.r2 + ax * ax + ay * ay) * 0x1p-18;
+      const double band =  // explicit rounding: touched_fix.cu recomputes it bit for bit
+          __dmul_rn(__dadd_rn(__dadd_rn(rec.r2, __dmul_rn(ax, ax)), __dmul_rn(ay, ay)), 0x1p-18);
       const float fx = (float)mxl, fy = (float)myl;
       const float r = sqrtf((float)rec.r2) * 1.0001f + 1e-3f;
       s_geo[j] = make_float4(fx, fy, rec.qa, rec.qb);
@@ -180,6 +197,7 @@ __global__ void __launch_bounds__(256) k_blend(BlendArgs a) {
             C1[p] = fmaf(w, c.y, C1[p]);
             C2[p] = fmaf(w, c.z, C2[p]);
             D[p] = fmaf(w, c.w, D[p]);
+            Tc[p] = T[p];
             T[p] = T[p] * (1.0f - sig);
             contrib_n += contrib;
             if (T[p] < kTermEpsF) last[p] = b0 - range.x + k;
@@ -228,6 +246,7 @@ __global__ void __launch_bounds__(256) k_blend(BlendArgs a) {
   for (int p = 0; p < PPT; ++p) {
     if (!valid[p]) continue;
     put_pixel(a, x0 + lxs[p], y0 + lys[p], T[p], C0[p], C1[p], C2[p], D[p]);
+    if (a.fix_count && crossing_uncertain(T[p], Tc[p])) queue_fix(a, tile, lxs[p], lys[p]);
   }
 }
 
@@ -279,7 +298,7 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
     const int lx = (sub & 1) * 8 + (lane & 7);
     int ly[NP];
     bool valid[NP];
-    float T[NP], C0[NP], C1[NP], C2[NP], D[NP];
+    float T[NP], C0[NP], C1[NP], C2[NP], D[NP], Tc[NP];
     bool any_valid = false;
     float bx0 = 3.0e38f, bx1 = -3.0e38f, by0 = 3.0e38f, by1 = -3.0e38f;
     const float px = (float)lx + 0.5f;
@@ -288,6 +307,7 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
       ly[q] = (sub >> 1) * kRows + (lane >> 3) + 4 * q;
       valid[q] = x0 + lx < a.width && y0 + ly[q] < a.height;
       T[q] = valid[q] ? 1.0f : 0.0f;  // invalid pixels never go active
+      Tc[q] = 1.0f;
       C0[q] = C1[q] = C2[q] = D[q] = 0.0f;
       any_valid |= valid[q];
       if (valid[q]) {  // warp pixel box (pixel centres, tile-local)
@@ -373,7 +393,8 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
           const float4 g2 = __ldg(rec4 + 4 * (size_t)cid + 2);  // qc, log2a, r, g
           const float4 g3 = __ldg(rec4 + 4 * (size_t)cid + 3);  // b, z
           const double ax = fabs(mxl) + 16.0, ay = fabs(myl) + 16.0;
-          const double band = (r2 + ax * ax + ay * ay) * 0x1p-18;
+          const double band =  // explicit rounding (touched_fix.cu)
+              __dmul_rn(__dadd_rn(__dadd_rn(r2, __dmul_rn(ax, ax)), __dmul_rn(ay, ay)), 0x1p-18);
           s_geo[warp][lane] = make_float4(fx, fy, c1.z, c1.w);
           s_geo2[warp][lane] = make_float4(g2.x, g2.y, __double2float_rd(r2 - band),
                                            __double2float_ru(r2 + band));
@@ -423,6 +444,7 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
           C1[q] = fmaf(w, c.y, C1[q]);
           C2[q] = fmaf(w, c.z, C2[q]);
           D[q] = fmaf(w, c.w, D[q]);
+          Tc[q] = take ? T[q] : Tc[q];
           T[q] = T[q] * (1.0f - sig);
           contrib_bits += contrib;
           active |= T[q] >= kTermEpsF;
@@ -447,6 +469,7 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
     for (int q = 0; q < NP; ++q) {
       if (!valid[q]) continue;
       put_pixel(a, x0 + lx, y0 + ly[q], T[q], C0[q], C1[q], C2[q], D[q]);
+      if (a.fix_count && crossing_uncertain(T[q], Tc[q])) queue_fix(a, tile, lx, ly[q]);
     }
   }
 }

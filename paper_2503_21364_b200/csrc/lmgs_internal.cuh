@@ -214,6 +214,10 @@ struct BlendArgs {
   // strip y / strip_rows at row y % strip_rows of srgb / strans / sdepth
   // (possibly peer-GPU pointers) instead of rgb / alpha / depth / trans
   int32_t n_strips, strip_rows;
+  // exact-touched fix-up queue (nullable): pixels for the fp64 replay
+  uint32_t* fix_count;
+  uint32_t* fix_list;
+  int32_t fix_cap;
   float* srgb[8];
   float* strans[8];
   float* sdepth[8];
@@ -246,6 +250,24 @@ int launch_blend(const BlendArgs& a, cudaStream_t s);  // returns 0 or LMGS_ERR_
 
 void launch_fill_background(float* rgb, float* alpha, float* depth, float* trans, int64_t n_pix,
                             const float bg[3], cudaStream_t s);
+
+// K7b: exact touched counts for the pixels the blend queued (touched_fix.cu)
+struct TouchedFixArgs {
+  void* const* keys_slot;
+  const int2* ranges;
+  const BlendRec* recs;
+  int32_t tile_size, tiles_x;
+  const uint32_t* fix_count;
+  const uint32_t* fix_list;
+  int32_t fix_cap;
+  int32_t* touched;
+  const float* means;
+  const float* quats;
+  const float* scales;
+  const float* logits;
+  CamArgs cam;
+};
+int launch_touched_fix(const TouchedFixArgs& a, cudaStream_t s);
 
 // Backward of the blend + chain to SH / logits (backward.cu), over the tile
 // lists of the preceding render of the same view on the same context.

@@ -1,0 +1,175 @@
+// K7b: exact `touched` (rasterize's per-splat count of w > 0, gaussian_core.py
+// 323) for the pixels whose fp32 transmittance crossed TERM_EPS within the
+// blend's uncertainty band (blend.cu: crossing_uncertain).  Everywhere else
+// the fp32 blend's decisions are the reference's: circle tests are exact
+// (guard band + fp64), w > 0 is exact (exponent check + fp64), and a pixel
+// far from TERM_EPS is active in both.  For a queued pixel one warp walks the
+// tile list again: threads evaluate 256 splats at a time — the blend's fp32
+// quantities with the blend's exact expressions, and for the splats the
+// pixel is inside, sigma in fp64 from K1's geometry (geometry.cuh, this file
+// is built with -fmad=false) as _blend (306-322) computes it — then thread 0
+// runs both recurrences in list order over the inside splats and adds (fp64
+// decision - fp32 decision) to each splat's count, until both transmittances
+// are below TERM_EPS.
+#include "device_util.cuh"
+#include "geometry.cuh"
+#include "lmgs_internal.cuh"
+
+namespace lmgs {
+namespace {
+
+constexpr float kTermEpsF = 1.00000005e-4f;  // as blend.cu
+constexpr float kSigmaMaxF = 0.9999f;
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+constexpr int kFixThreads = 256;
+
+#ifdef LMGS_FIX_STATS
+// debug: histogram of |T32 / T64 - 1| at the end of each replayed pixel
+__device__ unsigned int g_fix_hist[8];
+#endif
+
+// One CTA per queued pixel.  Each round, the CTA's threads take 256
+// consecutive splats of the tile list: the blend's fp32 circle test and
+// exponent, and for the splats the pixel is inside (a few percent) sigma in
+// fp64 from K1's geometry; those are compacted in list order into shared
+// memory and thread 0 runs the fp32 and fp64 recurrences over them.
+__global__ void __launch_bounds__(kFixThreads) k_touched_fix(TouchedFixArgs a) {
+  __shared__ float s_pow[kFixThreads];
+  __shared__ double s_sig[kFixThreads];
+  __shared__ uint32_t s_id[kFixThreads];
+  __shared__ int s_woff[kFixThreads / 32 + 1];
+  __shared__ int s_done;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t n = min(*a.fix_count, (uint32_t)a.fix_cap);
+  const uint64_t* __restrict__ list = static_cast<const uint64_t*>(*a.keys_slot);
+  const CamArgs& cam = a.cam;
+  const int ts = a.tile_size;
+  for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const uint32_t v = a.fix_list[i];
+    const int tile = (int)(v >> 12), ly = (int)((v >> 6) & 63), lx = (int)(v & 63);
+    const int x0 = (tile % a.tiles_x) * ts, y0 = (tile / a.tiles_x) * ts;
+    const float px = (float)lx + 0.5f, py = (float)ly + 0.5f;  // tile-local (blend)
+    const double pxd = (double)(x0 + lx) + 0.5, pyd = (double)(y0 + ly) + 0.5;  // 335-337
+    const int2 range = a.ranges[tile];
+    float T32 = 1.0f;  // thread 0's recurrences
+    double T64 = 1.0;
+    if (tid == 0) s_done = 0;
+    __syncthreads();
+    for (int b = range.x; b < range.y; b += kFixThreads) {
+      const int j = b + tid;
+      bool inside = false;
+      float power = 0.0f;
+      uint32_t id = 0;
+      BlendRec rec;
+      if (j < range.y) {
+        id = (uint32_t)list[j];
+        rec = a.recs[id];
+        // the blend's fp32 view of the splat (blend.cu, same expressions)
+        const double mxl = rec.mx - (double)x0, myl = rec.my - (double)y0;
+        const double ax = fabs(mxl) + (double)ts, ay = fabs(myl) + (double)ts;
+        const double band =
+            __dmul_rn(__dadd_rn(__dadd_rn(rec.r2, __dmul_rn(ax, ax)), __dmul_rn(ay, ay)), 0x1p-18);
+        const float fx = (float)mxl, fy = (float)myl;
+        const float dx = px - fx, dy = py - fy;
+        const float d2 = fmaf(dx, dx, dy * dy);
+        inside = d2 <= __double2float_rd(rec.r2 - band);
+        if (!inside && d2 <= __double2float_ru(rec.r2 + band)) {
+          const double ddx = pxd - rec.mx, ddy = pyd - rec.my;
+          inside = __dadd_rn(__dmul_rn(ddx, ddx), __dmul_rn(ddy, ddy)) <= rec.r2;
+        }
+        power = fmaf(fmaf(rec.qa, dx, rec.qb * dy), dx, fmaf(rec.qc * dy, dy, rec.log2_alpha));
+      }
+      // compact the inside splats in list order
+      const uint32_t m = __ballot_sync(0xffffffffu, inside);
+      if (lane == 0) s_woff[warp] = __popc(m);
+      __syncthreads();
+      if (tid == 0) {
+        int acc = 0;
+        for (int w = 0; w < kFixThreads / 32; ++w) {
+          const int c = s_woff[w];
+          s_woff[w] = acc;
+          acc += c;
+        }
+        s_woff[kFixThreads / 32] = acc;
+      }
+      __syncthreads();
+      if (inside) {
+        const int pos = s_woff[warp] + __popc(m & lanemask_lt());
+        // _blend 308-313 in fp64 from K1's geometry
+        const double m0 = a.means[3 * (size_t)id], m1 = a.means[3 * (size_t)id + 1],
+                     m2 = a.means[3 * (size_t)id + 2];
+        const double x = mkl_dot3(m0, cam.r[0], m1, cam.r[1], m2, cam.r[2]) + cam.t[0];
+        const double y = mkl_dot3(m0, cam.r[3], m1, cam.r[4], m2, cam.r[5]) + cam.t[1];
+        const double z = mkl_dot3(m0, cam.r[6], m1, cam.r[7], m2, cam.r[8]) + cam.t[2];
+        const float4 q = reinterpret_cast<const float4*>(a.quats)[id];
+        double mx, my, c00, c01, c11, radius;
+        splat_geometry(cam, x, y, z, q, a.scales[3 * (size_t)id], a.scales[3 * (size_t)id + 1],
+                       a.scales[3 * (size_t)id + 2], &mx, &my, &c00, &c01, &c11, &radius);
+        const double det = c00 * c11 - c01 * c01;
+        const double ca = c11 / det, cb = -c01 / det, cc = c00 / det;
+        const double ddx = pxd - mx, ddy = pyd - my;
+        const double maha = (ca * (ddx * ddx) + ((2.0 * cb) * ddx) * ddy) + cc * (ddy * ddy);
+        const double op = 1.0 / (1.0 + exp(-(double)a.logits[id]));
+        s_sig[pos] = op * exp(-0.5 * maha);
+        s_pow[pos] = power;
+        s_id[pos] = id;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        const int cnt = s_woff[kFixThreads / 32];
+        for (int k = 0; k < cnt; ++k) {
+          const float pw = s_pow[k];
+          // the blend's step (blend.cu k_blend16w / k_blend), inside = true
+          const bool take32 = T32 >= kTermEpsF;
+          bool c32 = take32 && pw > -1060.0f;
+          if (take32 && !c32 && pw >= -1080.0f) c32 = exp2((double)pw) * (double)T32 > 0.0;
+          const float sig32 = take32 ? fminf(ex2_approx(pw), kSigmaMaxF) : 0.0f;
+          T32 = T32 * (1.0f - sig32);
+          // the reference's step (_blend 314-323)
+          const bool take64 = T64 >= kTermEps;
+          const double sig64 = take64 ? fmin(s_sig[k], kSigmaMax) : 0.0;
+          const bool c64 = T64 * sig64 > 0.0;
+          T64 = T64 * (1.0 - sig64);
+          if (c64 != c32) atomicAdd(a.touched + s_id[k], c64 ? 1 : -1);
+          if (T32 < kTermEpsF && T64 < kTermEps) {
+            s_done = 1;
+            break;
+          }
+        }
+      }
+      __syncthreads();
+      if (s_done) break;
+    }
+#ifdef LMGS_FIX_STATS
+    if (tid == 0) {
+      const double rel = T64 > 0 ? fabs((double)T32 / T64 - 1.0) : 0.0;
+      int bin = rel < 1e-7 ? 0 : rel < 1e-6 ? 1 : rel < 1e-5 ? 2 : rel < 1e-4 ? 3 : rel < 1e-3 ? 4 : 5;
+      atomicAdd(&g_fix_hist[bin], 1u);
+    }
+#endif
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+#ifdef LMGS_FIX_STATS
+}  // namespace lmgs
+extern "C" int lmgs_debug_fix_hist(unsigned int* out) {
+  return (int)cudaMemcpyFromSymbol(out, lmgs::g_fix_hist, sizeof(lmgs::g_fix_hist));
+}
+namespace lmgs {
+#endif
+
+int launch_touched_fix(const TouchedFixArgs& a, cudaStream_t s) {
+  k_touched_fix<<<148 * 8, kFixThreads, 0, s>>>(a);
+  return 1;
+}
+
+}  // namespace lmgs
