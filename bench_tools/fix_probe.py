@@ -23,4 +23,4 @@ if len(sys.argv) > 1:  # liblmgs built with -DLMGS_FIX_STATS
 
     h = (ctypes.c_uint * 8)()
     _lib.lib().lmgs_debug_fix_hist(h)
-    print("rel |T32/T64-1| bins <1e-7,<1e-6,<1e-5,<1e-4,<1e-3,>=1e-3:", list(h)[:6])
+    print("rel bins <1e-7..>=1e-3:", list(h)[:6], "rounds total", h[6], "max", h[7])

@@ -61,29 +61,55 @@ __global__ void __launch_bounds__(kFixThreads) k_touched_fix(TouchedFixArgs a) {
     double T64 = 1.0;
     if (tid == 0) s_done = 0;
     __syncthreads();
+#ifdef LMGS_FIX_STATS
+    int rounds = 0;
+#endif
+    // software pipeline: round r + 1's ids and first record sectors load
+    // while round r is evaluated and scanned
+    uint32_t nid = 0;
+    double2 n0 = make_double2(0.0, 0.0), n1 = n0;
+    if (range.x + tid < range.y) {
+      nid = (uint32_t)list[range.x + tid];
+      const double2* r16 = reinterpret_cast<const double2*>(a.recs + nid);
+      n0 = r16[0];
+      n1 = r16[1];
+    }
     for (int b = range.x; b < range.y; b += kFixThreads) {
+#ifdef LMGS_FIX_STATS
+      ++rounds;
+#endif
       const int j = b + tid;
       bool inside = false;
       float power = 0.0f;
-      uint32_t id = 0;
-      BlendRec rec;
+      const uint32_t id = nid;
+      const double2 s0 = n0, s1 = n1;
+      if (j + kFixThreads < range.y) {
+        nid = (uint32_t)list[j + kFixThreads];
+        const double2* r16 = reinterpret_cast<const double2*>(a.recs + nid);
+        n0 = r16[0];
+        n1 = r16[1];
+      }
       if (j < range.y) {
-        id = (uint32_t)list[j];
-        rec = a.recs[id];
+        // first record sector: mx, my, r^2, qa, qb (the second only when inside)
+        const double rmx = s0.x, rmy = s0.y, rr2 = s1.x;
+        const float2 qab = *reinterpret_cast<const float2*>(&s1.y);
         // the blend's fp32 view of the splat (blend.cu, same expressions)
-        const double mxl = rec.mx - (double)x0, myl = rec.my - (double)y0;
+        const double mxl = rmx - (double)x0, myl = rmy - (double)y0;
         const double ax = fabs(mxl) + (double)ts, ay = fabs(myl) + (double)ts;
         const double band =
-            __dmul_rn(__dadd_rn(__dadd_rn(rec.r2, __dmul_rn(ax, ax)), __dmul_rn(ay, ay)), 0x1p-18);
+            __dmul_rn(__dadd_rn(__dadd_rn(rr2, __dmul_rn(ax, ax)), __dmul_rn(ay, ay)), 0x1p-18);
         const float fx = (float)mxl, fy = (float)myl;
         const float dx = px - fx, dy = py - fy;
         const float d2 = fmaf(dx, dx, dy * dy);
-        inside = d2 <= __double2float_rd(rec.r2 - band);
-        if (!inside && d2 <= __double2float_ru(rec.r2 + band)) {
-          const double ddx = pxd - rec.mx, ddy = pyd - rec.my;
-          inside = __dadd_rn(__dmul_rn(ddx, ddx), __dmul_rn(ddy, ddy)) <= rec.r2;
+        inside = d2 <= __double2float_rd(rr2 - band);
+        if (!inside && d2 <= __double2float_ru(rr2 + band)) {
+          const double ddx = pxd - rmx, ddy = pyd - rmy;
+          inside = __dadd_rn(__dmul_rn(ddx, ddx), __dmul_rn(ddy, ddy)) <= rr2;
         }
-        power = fmaf(fmaf(rec.qa, dx, rec.qb * dy), dx, fmaf(rec.qc * dy, dy, rec.log2_alpha));
+        if (inside) {
+          const float2 cl = reinterpret_cast<const float2*>(a.recs + id)[4];  // qc, log2 alpha
+          power = fmaf(fmaf(qab.x, dx, qab.y * dy), dx, fmaf(cl.x * dy, dy, cl.y));
+        }
       }
       // compact the inside splats in list order
       const uint32_t m = __ballot_sync(0xffffffffu, inside);
@@ -151,6 +177,8 @@ __global__ void __launch_bounds__(kFixThreads) k_touched_fix(TouchedFixArgs a) {
       const double rel = T64 > 0 ? fabs((double)T32 / T64 - 1.0) : 0.0;
       int bin = rel < 1e-7 ? 0 : rel < 1e-6 ? 1 : rel < 1e-5 ? 2 : rel < 1e-4 ? 3 : rel < 1e-3 ? 4 : 5;
       atomicAdd(&g_fix_hist[bin], 1u);
+      atomicAdd(&g_fix_hist[6], (unsigned)rounds);
+      atomicMax(&g_fix_hist[7], (unsigned)rounds);
     }
 #endif
     __syncthreads();
