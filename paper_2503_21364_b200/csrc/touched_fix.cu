@@ -28,22 +28,26 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 
 constexpr int kFixThreads = 256;
+constexpr int kProdWarps = kFixThreads / 32 - 1;  // warps 1..7 produce, warp 0 scans
+constexpr int kRound = 32 * kProdWarps;           // splats per round
 
 #ifdef LMGS_FIX_STATS
 // debug: histogram of |T32 / T64 - 1| at the end of each replayed pixel
 __device__ unsigned int g_fix_hist[8];
 #endif
 
-// One CTA per queued pixel.  Each round, the CTA's threads take 256
-// consecutive splats of the tile list: the blend's fp32 circle test and
-// exponent, and for the splats the pixel is inside (a few percent) sigma in
-// fp64 from K1's geometry; those are compacted in list order into shared
-// memory and thread 0 runs the fp32 and fp64 recurrences over them.
+// One CTA per queued pixel, as a two-stage pipeline over rounds of 224
+// consecutive splats of the tile list.  Producer warps (1..7) take 32 splats
+// each: the blend's fp32 circle test and exponent, and for the splats the
+// pixel is inside (a few percent) sigma in fp64 from K1's geometry, compacted
+// in list order into the warp's slots of the round's buffer.  Meanwhile
+// thread 0 runs the fp32 and fp64 recurrences over the previous round's
+// buffer (double-buffered, one barrier per round).
 __global__ void __launch_bounds__(kFixThreads) k_touched_fix(TouchedFixArgs a) {
-  __shared__ float s_pow[kFixThreads];
-  __shared__ double s_sig[kFixThreads];
-  __shared__ uint32_t s_id[kFixThreads];
-  __shared__ int s_woff[kFixThreads / 32 + 1];
+  __shared__ float s_pow[2][kProdWarps][32];
+  __shared__ double s_sig[2][kProdWarps][32];
+  __shared__ uint32_t s_id[2][kProdWarps][32];
+  __shared__ int s_cnt[2][kProdWarps];
   __shared__ int s_done;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t n = min(*a.fix_count, (uint32_t)a.fix_cap);
@@ -57,115 +61,110 @@ __global__ void __launch_bounds__(kFixThreads) k_touched_fix(TouchedFixArgs a) {
     const float px = (float)lx + 0.5f, py = (float)ly + 0.5f;  // tile-local (blend)
     const double pxd = (double)(x0 + lx) + 0.5, pyd = (double)(y0 + ly) + 0.5;  // 335-337
     const int2 range = a.ranges[tile];
+    const int nr = (range.y - range.x + kRound - 1) / kRound;
     float T32 = 1.0f;  // thread 0's recurrences
     double T64 = 1.0;
     if (tid == 0) s_done = 0;
-    __syncthreads();
-#ifdef LMGS_FIX_STATS
-    int rounds = 0;
-#endif
-    // software pipeline: round r + 1's ids and first record sectors load
-    // while round r is evaluated and scanned
+    // producers prefetch their first splat (id, first record sector)
+    const int pt = 32 * (warp - 1) + lane;  // producer slot within a round
     uint32_t nid = 0;
     double2 n0 = make_double2(0.0, 0.0), n1 = n0;
-    if (range.x + tid < range.y) {
-      nid = (uint32_t)list[range.x + tid];
+    if (warp > 0 && range.x + pt < range.y) {
+      nid = (uint32_t)list[range.x + pt];
       const double2* r16 = reinterpret_cast<const double2*>(a.recs + nid);
       n0 = r16[0];
       n1 = r16[1];
     }
-    for (int b = range.x; b < range.y; b += kFixThreads) {
+    __syncthreads();
 #ifdef LMGS_FIX_STATS
-      ++rounds;
+    int rounds = 0;
 #endif
-      const int j = b + tid;
-      bool inside = false;
-      float power = 0.0f;
-      const uint32_t id = nid;
-      const double2 s0 = n0, s1 = n1;
-      if (j + kFixThreads < range.y) {
-        nid = (uint32_t)list[j + kFixThreads];
-        const double2* r16 = reinterpret_cast<const double2*>(a.recs + nid);
-        n0 = r16[0];
-        n1 = r16[1];
-      }
-      if (j < range.y) {
-        // first record sector: mx, my, r^2, qa, qb (the second only when inside)
-        const double rmx = s0.x, rmy = s0.y, rr2 = s1.x;
-        const float2 qab = *reinterpret_cast<const float2*>(&s1.y);
-        // the blend's fp32 view of the splat (blend.cu, same expressions)
-        const double mxl = rmx - (double)x0, myl = rmy - (double)y0;
-        const double ax = fabs(mxl) + (double)ts, ay = fabs(myl) + (double)ts;
-        const double band =
-            __dmul_rn(__dadd_rn(__dadd_rn(rr2, __dmul_rn(ax, ax)), __dmul_rn(ay, ay)), 0x1p-18);
-        const float fx = (float)mxl, fy = (float)myl;
-        const float dx = px - fx, dy = py - fy;
-        const float d2 = fmaf(dx, dx, dy * dy);
-        inside = d2 <= __double2float_rd(rr2 - band);
-        if (!inside && d2 <= __double2float_ru(rr2 + band)) {
-          const double ddx = pxd - rmx, ddy = pyd - rmy;
-          inside = __dadd_rn(__dmul_rn(ddx, ddx), __dmul_rn(ddy, ddy)) <= rr2;
+    for (int r = 0; r <= nr; ++r) {
+      const int buf = r & 1;
+      if (warp > 0 && r < nr) {  // produce round r
+        const int j = range.x + r * kRound + pt;
+        const uint32_t id = nid;
+        const double2 s0 = n0, s1 = n1;
+        if (j + kRound < range.y) {  // prefetch round r + 1
+          nid = (uint32_t)list[j + kRound];
+          const double2* r16 = reinterpret_cast<const double2*>(a.recs + nid);
+          n0 = r16[0];
+          n1 = r16[1];
         }
+        bool inside = false;
+        float power = 0.0f;
+        if (j < range.y) {
+          // first record sector: mx, my, r^2, qa, qb (the second only when inside)
+          const double rmx = s0.x, rmy = s0.y, rr2 = s1.x;
+          const float2 qab = *reinterpret_cast<const float2*>(&s1.y);
+          // the blend's fp32 view of the splat (blend.cu, same expressions)
+          const double mxl = rmx - (double)x0, myl = rmy - (double)y0;
+          const double ax = fabs(mxl) + (double)ts, ay = fabs(myl) + (double)ts;
+          const double band = __dmul_rn(
+              __dadd_rn(__dadd_rn(rr2, __dmul_rn(ax, ax)), __dmul_rn(ay, ay)), 0x1p-18);
+          const float fx = (float)mxl, fy = (float)myl;
+          const float dx = px - fx, dy = py - fy;
+          const float d2 = fmaf(dx, dx, dy * dy);
+          inside = d2 <= __double2float_rd(rr2 - band);
+          if (!inside && d2 <= __double2float_ru(rr2 + band)) {
+            const double ddx = pxd - rmx, ddy = pyd - rmy;
+            inside = __dadd_rn(__dmul_rn(ddx, ddx), __dmul_rn(ddy, ddy)) <= rr2;
+          }
+          if (inside) {
+            const float2 cl = reinterpret_cast<const float2*>(a.recs + id)[4];  // qc, log2 a
+            power = fmaf(fmaf(qab.x, dx, qab.y * dy), dx, fmaf(cl.x * dy, dy, cl.y));
+          }
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, inside);
+        if (lane == 0) s_cnt[buf][warp - 1] = __popc(m);
         if (inside) {
-          const float2 cl = reinterpret_cast<const float2*>(a.recs + id)[4];  // qc, log2 alpha
-          power = fmaf(fmaf(qab.x, dx, qab.y * dy), dx, fmaf(cl.x * dy, dy, cl.y));
+          const int pos = __popc(m & lanemask_lt());
+          // _blend 308-313 in fp64 from K1's geometry
+          const double m0 = a.means[3 * (size_t)id], m1 = a.means[3 * (size_t)id + 1],
+                       m2 = a.means[3 * (size_t)id + 2];
+          const double x = mkl_dot3(m0, cam.r[0], m1, cam.r[1], m2, cam.r[2]) + cam.t[0];
+          const double y = mkl_dot3(m0, cam.r[3], m1, cam.r[4], m2, cam.r[5]) + cam.t[1];
+          const double z = mkl_dot3(m0, cam.r[6], m1, cam.r[7], m2, cam.r[8]) + cam.t[2];
+          const float4 q = reinterpret_cast<const float4*>(a.quats)[id];
+          double mx, my, c00, c01, c11, radius;
+          splat_geometry(cam, x, y, z, q, a.scales[3 * (size_t)id],
+                         a.scales[3 * (size_t)id + 1], a.scales[3 * (size_t)id + 2], &mx, &my,
+                         &c00, &c01, &c11, &radius);
+          const double det = c00 * c11 - c01 * c01;
+          const double ca = c11 / det, cb = -c01 / det, cc = c00 / det;
+          const double ddx = pxd - mx, ddy = pyd - my;
+          const double maha = (ca * (ddx * ddx) + ((2.0 * cb) * ddx) * ddy) + cc * (ddy * ddy);
+          const double op = 1.0 / (1.0 + exp(-(double)a.logits[id]));
+          s_sig[buf][warp - 1][pos] = op * exp(-0.5 * maha);
+          s_pow[buf][warp - 1][pos] = power;
+          s_id[buf][warp - 1][pos] = id;
         }
       }
-      // compact the inside splats in list order
-      const uint32_t m = __ballot_sync(0xffffffffu, inside);
-      if (lane == 0) s_woff[warp] = __popc(m);
-      __syncthreads();
-      if (tid == 0) {
-        int acc = 0;
-        for (int w = 0; w < kFixThreads / 32; ++w) {
-          const int c = s_woff[w];
-          s_woff[w] = acc;
-          acc += c;
-        }
-        s_woff[kFixThreads / 32] = acc;
-      }
-      __syncthreads();
-      if (inside) {
-        const int pos = s_woff[warp] + __popc(m & lanemask_lt());
-        // _blend 308-313 in fp64 from K1's geometry
-        const double m0 = a.means[3 * (size_t)id], m1 = a.means[3 * (size_t)id + 1],
-                     m2 = a.means[3 * (size_t)id + 2];
-        const double x = mkl_dot3(m0, cam.r[0], m1, cam.r[1], m2, cam.r[2]) + cam.t[0];
-        const double y = mkl_dot3(m0, cam.r[3], m1, cam.r[4], m2, cam.r[5]) + cam.t[1];
-        const double z = mkl_dot3(m0, cam.r[6], m1, cam.r[7], m2, cam.r[8]) + cam.t[2];
-        const float4 q = reinterpret_cast<const float4*>(a.quats)[id];
-        double mx, my, c00, c01, c11, radius;
-        splat_geometry(cam, x, y, z, q, a.scales[3 * (size_t)id], a.scales[3 * (size_t)id + 1],
-                       a.scales[3 * (size_t)id + 2], &mx, &my, &c00, &c01, &c11, &radius);
-        const double det = c00 * c11 - c01 * c01;
-        const double ca = c11 / det, cb = -c01 / det, cc = c00 / det;
-        const double ddx = pxd - mx, ddy = pyd - my;
-        const double maha = (ca * (ddx * ddx) + ((2.0 * cb) * ddx) * ddy) + cc * (ddy * ddy);
-        const double op = 1.0 / (1.0 + exp(-(double)a.logits[id]));
-        s_sig[pos] = op * exp(-0.5 * maha);
-        s_pow[pos] = power;
-        s_id[pos] = id;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        const int cnt = s_woff[kFixThreads / 32];
-        for (int k = 0; k < cnt; ++k) {
-          const float pw = s_pow[k];
-          // the blend's step (blend.cu k_blend16w / k_blend), inside = true
-          const bool take32 = T32 >= kTermEpsF;
-          bool c32 = take32 && pw > -1060.0f;
-          if (take32 && !c32 && pw >= -1080.0f) c32 = exp2((double)pw) * (double)T32 > 0.0;
-          const float sig32 = take32 ? fminf(ex2_approx(pw), kSigmaMaxF) : 0.0f;
-          T32 = T32 * (1.0f - sig32);
-          // the reference's step (_blend 314-323)
-          const bool take64 = T64 >= kTermEps;
-          const double sig64 = take64 ? fmin(s_sig[k], kSigmaMax) : 0.0;
-          const bool c64 = T64 * sig64 > 0.0;
-          T64 = T64 * (1.0 - sig64);
-          if (c64 != c32) atomicAdd(a.touched + s_id[k], c64 ? 1 : -1);
-          if (T32 < kTermEpsF && T64 < kTermEps) {
-            s_done = 1;
-            break;
+      if (tid == 0 && r > 0 && !s_done) {  // scan round r - 1
+        const int pb = buf ^ 1;
+#ifdef LMGS_FIX_STATS
+        ++rounds;
+#endif
+        for (int w = 0; w < kProdWarps && !s_done; ++w) {
+          const int cnt = s_cnt[pb][w];
+          for (int k = 0; k < cnt; ++k) {
+            const float pw = s_pow[pb][w][k];
+            // the blend's step (blend.cu k_blend16w / k_blend), inside = true
+            const bool take32 = T32 >= kTermEpsF;
+            bool c32 = take32 && pw > -1060.0f;
+            if (take32 && !c32 && pw >= -1080.0f) c32 = exp2((double)pw) * (double)T32 > 0.0;
+            const float sig32 = take32 ? fminf(ex2_approx(pw), kSigmaMaxF) : 0.0f;
+            T32 = T32 * (1.0f - sig32);
+            // the reference's step (_blend 314-323)
+            const bool take64 = T64 >= kTermEps;
+            const double sig64 = take64 ? fmin(s_sig[pb][w][k], kSigmaMax) : 0.0;
+            const bool c64 = T64 * sig64 > 0.0;
+            T64 = T64 * (1.0 - sig64);
+            if (c64 != c32) atomicAdd(a.touched + s_id[pb][w][k], c64 ? 1 : -1);
+            if (T32 < kTermEpsF && T64 < kTermEps) {
+              s_done = 1;
+              break;
+            }
           }
         }
       }
