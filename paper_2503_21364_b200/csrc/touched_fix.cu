@@ -27,7 +27,10 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-constexpr int kFixThreads = 256;
+#ifndef LMGS_FIX_THREADS
+#define LMGS_FIX_THREADS 256
+#endif
+constexpr int kFixThreads = LMGS_FIX_THREADS;
 constexpr int kProdWarps = kFixThreads / 32 - 1;  // warps 1..7 produce, warp 0 scans
 constexpr int kRound = 32 * kProdWarps;           // splats per round
 
@@ -195,7 +198,7 @@ namespace lmgs {
 #endif
 
 int launch_touched_fix(const TouchedFixArgs& a, cudaStream_t s) {
-  k_touched_fix<<<148 * 8, kFixThreads, 0, s>>>(a);
+  k_touched_fix<<<148 * (2048 / kFixThreads), kFixThreads, 0, s>>>(a);
   return 1;
 }
 
