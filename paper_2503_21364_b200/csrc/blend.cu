@@ -497,7 +497,11 @@ int launch_blend(const BlendArgs& a, cudaStream_t s) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_blend16w<kBlendNP>, 256, 0);
       if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
+#ifdef LMGS_BLEND_CTAS_PER_SM  // experiment: leave room for other streams' kernels
+    int grid = sms * min(blocks_per_sm, LMGS_BLEND_CTAS_PER_SM);
+#else
     int grid = sms * blocks_per_sm;
+#endif
     const int need = (items + kWarpsPerBlock16 - 1) / kWarpsPerBlock16;
     if (grid > need) grid = need;
     k_blend16w<kBlendNP><<<grid, 256, 0, s>>>(a, items);
