@@ -489,18 +489,19 @@ int launch_blend(const BlendArgs& a, cudaStream_t s) {
     cudaMemsetAsync(a.work_counter, 0, sizeof(int), s);
     if (a.n_processed) cudaMemsetAsync(a.n_processed, 0, sizeof(int) * tiles, s);
     const int items = tiles * (8 / kBlendNP);
-    static int blocks_per_sm = 0, sms = 0;
-    if (!blocks_per_sm) {
-      int dev = 0;
-      cudaGetDevice(&dev);
+    static int bps_cache[kMaxDevices] = {}, sms_cache[kMaxDevices] = {};
+    const int dev = current_device();
+    if (!bps_cache[dev]) {
+      int bps = 0, sms = 0;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_blend16w<kBlendNP>, 256, 0);
-      if (blocks_per_sm < 1) blocks_per_sm = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_blend16w<kBlendNP>, 256, 0);
+      sms_cache[dev] = sms > 0 ? sms : 148;
+      bps_cache[dev] = bps > 0 ? bps : 1;
     }
 #ifdef LMGS_BLEND_CTAS_PER_SM  // experiment: leave room for other streams' kernels
-    int grid = sms * min(blocks_per_sm, LMGS_BLEND_CTAS_PER_SM);
+    int grid = sms_cache[dev] * min(bps_cache[dev], LMGS_BLEND_CTAS_PER_SM);
 #else
-    int grid = sms * blocks_per_sm;
+    int grid = sms_cache[dev] * bps_cache[dev];
 #endif
     const int need = (items + kWarpsPerBlock16 - 1) / kWarpsPerBlock16;
     if (grid > need) grid = need;

@@ -37,6 +37,14 @@ __host__ __device__ inline uint64_t pack_rect(uint32_t x0, uint32_t y0, uint32_t
   return (uint64_t)x0 | ((uint64_t)y0 << 16) | ((uint64_t)x1 << 32) | ((uint64_t)y1 << 48);
 }
 
+// Per-device launch caches (function attributes are per device context).
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < 0 ? 0 : (d >= kMaxDevices ? kMaxDevices - 1 : d);
+}
+
 struct CamArgs {
   double r[9], t[3], center[3];
   double fx, fy, cx, cy, lim_x, lim_y;

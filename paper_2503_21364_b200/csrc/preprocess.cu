@@ -343,11 +343,12 @@ int launch_preprocess(const PreprocessArgs& a, cudaStream_t s) {
   const int64_t full = aligned ? a.n / kPreThreads : 0;
   if (full > 0) {
     const size_t smem = sizeof(float) * kPreThreads * (3 + 4 + 3 + 1 + 3 * a.sh_coeffs);
-    static size_t set = 0;
-    if (smem > set) {
+    static size_t set[kMaxDevices] = {};
+    const int dev = current_device();
+    if (smem > set[dev]) {
       cudaFuncSetAttribute(k_preprocess_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
-      set = smem;
+      set[dev] = smem;
     }
     k_preprocess_tma<<<(unsigned)full, kPreThreads, smem, s>>>(a);
     ++launched;

@@ -338,11 +338,12 @@ template <typename K, bool VALS>
 void launch_onesweep(const RadixSortBuffers& b, int64_t n, int begin_bit, int p, int64_t blocks,
                      cudaStream_t s) {
   constexpr size_t smem = onesweep_smem<K, VALS>();
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[kMaxDevices] = {};
+  const int dev = current_device();
+  if (!attr_set[dev]) {
     cudaFuncSetAttribute(k_onesweep<K, VALS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    attr_set = true;
+    attr_set[dev] = true;
   }
   k_onesweep<K, VALS><<<(unsigned)blocks, kSortThreads, smem, s>>>(
       static_cast<K*>(b.keys[0]), static_cast<K*>(b.keys[1]), b.vals[0], b.vals[1], n, begin_bit,
