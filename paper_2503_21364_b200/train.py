@@ -10,8 +10,8 @@ Mirrors the reference's training consumers of the forward path:
   (sh_color_grad_to_coeffs, 145-166) and opacity logits, plus the
   ``DensifyStats`` increments (488-511).
 
-The device work runs in liblmgs (``lmgs_backward``): fp64, with each tile's
-splats re-projected by K1's own fp64 code, over the tile lists of the forward
+The device work runs in liblmgs (``lmgs_backward``): fp64, from per-view splat
+records computed by K1's own fp64 code, over the tile lists of the forward
 render of the same view.  Rows of the outputs are indexed by input Gaussian
 (the reference's per-splat arrays are over its kept splats; rows of culled
 Gaussians stay zero here).
@@ -109,7 +109,8 @@ def render_loss_and_grads(model: GaussianModel, cameras, gt_images, tile_size: i
     loss_sum = torch.zeros((len(cameras) or 1,), dtype=torch.float64, device=dev)
     numels = []
     for i, (cam, gt) in enumerate(zip(cameras, gt_images)):
-        fwd = render(cam, model, tile_size, background, sh_eval_degree, ctx=ctx)
+        # the loss needs the image only; the backward recounts touched exactly
+        fwd = render(cam, model, tile_size, background, sh_eval_degree, ctx=ctx, touched_fix=False)
         gt_t = torch.as_tensor(gt, device=dev)
         if gt_t.dtype not in (torch.float32, torch.float64):
             gt_t = gt_t.to(torch.float64)
