@@ -125,3 +125,42 @@ def test_peer_renderer_two_processes_cuda_ipc():
         p.join(120)
     assert sorted(res) == [(0, True), (1, True)]
     assert all(p.exitcode == 0 for p in ps)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ts,n_strips", [(16, 3), (8, 2), (24, 5), (16, 1)])
+def test_render_strips_equals_render(ts, n_strips):
+    """lmgs_render_strips writes exactly the pixels lmgs_render does (C + T bg,
+    T_final, depth), row y into strip y // strip_rows (ragged last strip)."""
+    import ctypes
+
+    import torch
+
+    from paper_2503_21364_b200 import GaussianModel, _lib, render, scenes
+    from paper_2503_21364_b200.raster import abi_camera, abi_settings, context
+
+    g = scenes.synthetic_gaussians(20_000, seed=9)
+    cam = scenes.orbit_cameras(1, 150, 97, seed=9)[0]
+    model = GaussianModel.from_host(g)
+    bg = (0.1, 0.2, 0.3)
+    ref = render(cam, model, ts, bg, 3, out={"transmittance": torch.empty((97, 150),
+                                                                          device="cuda")})
+    rows = -(-97 // n_strips)
+    rgb = [torch.zeros((rows, 150, 3), device="cuda") for _ in range(n_strips)]
+    trans = [torch.zeros((rows, 150), device="cuda") for _ in range(n_strips)]
+    depth = [torch.zeros((rows, 150), device="cuda") for _ in range(n_strips)]
+    t = _lib.StripTargets()
+    t.n_strips, t.strip_rows = n_strips, rows
+    for i in range(n_strips):
+        t.rgb[i], t.trans[i], t.depth[i] = rgb[i].data_ptr(), trans[i].data_ptr(), \
+            depth[i].data_ptr()
+    ctx = context(0)
+    g_abi, c_abi, s_abi = model._abi(), abi_camera(cam), abi_settings(ts, 3, bg)
+    _lib.check(ctx.handle, _lib.lib().lmgs_render_strips(
+        ctx.handle, ctypes.byref(g_abi), ctypes.byref(c_abi), ctypes.byref(s_abi),
+        ctypes.byref(t), None, torch.cuda.current_stream().cuda_stream), "lmgs_render_strips")
+    torch.cuda.synchronize()
+    got_rgb = torch.cat(rgb)[:97]
+    assert torch.equal(got_rgb, ref.rgb)
+    assert torch.equal(torch.cat(trans)[:97], ref.transmittance)
+    assert torch.equal(torch.cat(depth)[:97], ref.depth)
