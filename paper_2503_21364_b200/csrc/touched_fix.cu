@@ -28,7 +28,7 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 
 #ifndef LMGS_FIX_THREADS
-#define LMGS_FIX_THREADS 256
+#define LMGS_FIX_THREADS 128  // 64: 663, 128: 671, 256: 667, 512: 637 frames/s (c3 bench)
 #endif
 constexpr int kFixThreads = LMGS_FIX_THREADS;
 constexpr int kProdWarps = kFixThreads / 32 - 1;  // warps 1..7 produce, warp 0 scans
