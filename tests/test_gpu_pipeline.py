@@ -98,3 +98,17 @@ def test_repeated_renders_reuse_arena():
     again = [render(c, model).rgb.cpu().numpy() for c in reversed(cams)][::-1]
     for a, b in zip(first, again):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("logit_shift,ts", [(6.0, 16), (3.0, 8), (-2.0, 16)])
+def test_touched_exact_opaque_and_faint_scenes(logit_shift, ts):
+    """K7b under stress: near-opaque splats (sigma clamped at SIGMA_MAX, most
+    pixels terminate after a few splats) and faint ones (long walks, T ends
+    near TERM_EPS): touched and tile lists stay bit-exact vs the oracle."""
+    g = scenes.synthetic_gaussians(120_000, seed=13)
+    g = scenes.HostGaussians(g.means, g.quats, g.scales,
+                             (g.opacity_logits + np.float32(logit_shift)).astype(np.float32),
+                             g.sh, g.sh_degree)
+    cam = scenes.orbit_cameras(1, 320, 240, seed=13)[0]
+    r = _full_frame_check(g, cam, ts=ts)
+    assert r["err"] <= IMG_TOL and r["touched_mismatch"] == 0
