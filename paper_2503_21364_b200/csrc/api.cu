@@ -314,7 +314,10 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
 
   if (int r = ensure_gaussians(c, n > 0 ? n : 1, s)) return r;
   if (int r = ensure_tiles(c, tiles, s)) return r;
-  int2* ranges = out->tile_ranges ? reinterpret_cast<int2*>(out->tile_ranges) : c->ranges;
+  // ranges live in the context arena (lmgs_backward and lmgs_copy_instances
+  // read them after the call, whatever the caller did with its buffers);
+  // the caller's tile_ranges gets a copy
+  int2* ranges = c->ranges;
   c->last_ranges = ranges;
   Scalars* sc = c->d_scal;
   LMGS_CUDA(c, cudaMemsetAsync(sc->counts, 0, sizeof(sc->counts), s));
@@ -409,6 +412,9 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
     launched += radix_sort(rb, k, 32, tile_passes, s);
     launched += launch_ranges_from_counts(c->tile_count, (int)tiles, ranges, s);
   }
+  if (out->tile_ranges && tiles > 0)
+    LMGS_CUDA(c, cudaMemcpyAsync(out->tile_ranges, ranges, sizeof(int2) * tiles,
+                                 cudaMemcpyDeviceToDevice, s));
   tm.end(3);
 
   // K7

@@ -180,6 +180,13 @@ class RenderRecord:
     t_final: torch.Tensor         # (H,W)
     n_processed: torch.Tensor     # (T,)
     _tiles: list = field(default=None, repr=False)
+    # what the render drew, so train.backward_render(image_grad, record) can
+    # replay it (the reference's backward_render signature, 438)
+    _model: object = field(default=None, repr=False)
+    _camera: object = field(default=None, repr=False)
+    _prim_ids: object = field(default=None, repr=False)
+    _rows: object = field(default=None, repr=False)  # model row of each record splat
+    _sh_eval_degree: int = field(default=1, repr=False)
 
     @property
     def tiles(self) -> list:
@@ -341,10 +348,14 @@ def render_image(model, camera, tile_size: int = 16, background=(0.0, 0.0, 0.0),
     touched_m = touched[kept]
     if not with_record:
         return o.rgb, touched_m
+    kept_pos = torch.nonzero(kept).reshape(-1)
+    rows = kept_pos if inv is None else torch.argsort(inv)[kept_pos]
     rec = RenderRecord(cam.width, cam.height, int(tile_size),
                        torch.as_tensor(np.asarray(background, dtype=np.float64)),
                        src_ids[kept].cpu(), o.tile_ranges.cpu(), o.inst_prim_ids.cpu(),
-                       o.inst_keys.cpu(), o.transmittance.double().cpu(), o.n_processed.cpu())
+                       o.inst_keys.cpu(), o.transmittance.double().cpu(), o.n_processed.cpu(),
+                       _model=src, _camera=cam, _prim_ids=prim_ids, _rows=rows,
+                       _sh_eval_degree=int(sh_eval_degree))
     return o.rgb, touched_m, rec
 
 

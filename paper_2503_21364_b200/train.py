@@ -89,10 +89,34 @@ def _backward(ctx, model: GaussianModel, camera, image_grad: torch.Tensor, tile_
     return out
 
 
-def backward_render(model: GaussianModel, camera, image_grad: torch.Tensor, tile_size: int = 16,
-                    background=(0.0, 0.0, 0.0), sh_eval_degree: int = 1
-                    ) -> tuple[RenderOutput, RenderGrads]:
-    """Forward render of the view, then backward_render (438-486) of ``image_grad``."""
+def backward_render(model, camera, image_grad=None, tile_size: int = 16,
+                    background=(0.0, 0.0, 0.0), sh_eval_degree: int = 1):
+    """backward_render (438-486) of ``image_grad``, two call forms:
+
+    * ``backward_render(image_grad, record)`` — the reference's signature:
+      ``record`` is the RenderRecord of ``render_image(..., with_record=True)``;
+      returns RenderGrads with rows aligned with the record's splats
+      (``record.prim_id``), like the reference's;
+    * ``backward_render(model, camera, image_grad, tile_size, background,
+      sh_eval_degree)`` — renders the view and returns ``(RenderOutput,
+      RenderGrads)`` with rows indexed by input Gaussian.
+    """
+    from .raster import RenderRecord
+
+    if isinstance(camera, RenderRecord):
+        rec, g = camera, model
+        m = rec._model
+        if m is None:
+            raise ShapeError("record has no render source (use render_image(..., with_record=True))")
+        bg = tuple(float(v) for v in rec.background.tolist())
+        ctx = context(m.device.index)
+        render(rec._camera, m, rec.tile_size, bg, rec._sh_eval_degree, ctx=ctx,
+               prim_ids=rec._prim_ids, touched_fix=False)
+        full = _backward(ctx, m, rec._camera, torch.as_tensor(g), rec.tile_size, bg,
+                         rec._sh_eval_degree)
+        r = rec._rows
+        return RenderGrads(full.d_colors[r], full.d_opacities[r], full.d_mean2d[r],
+                           full.touched[r].long())
     ctx = context(model.device.index)
     fwd = render(camera, model, tile_size, background, sh_eval_degree, ctx=ctx)
     return fwd, _backward(ctx, model, camera, image_grad, tile_size, background, sh_eval_degree)

@@ -266,3 +266,30 @@ def test_backward_tile_size_invariant(ts):
     assert bool((got.touched == ref.touched).all())
     for f in ("d_colors", "d_opacities", "d_mean2d"):
         _close(getattr(got, f).cpu().numpy(), getattr(ref, f).cpu().numpy(), 1e-9, f)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("use_subset", [False, True])
+def test_backward_render_reference_signature(use_subset):
+    """backward_render(image_grad, record) as the reference calls it (438):
+    rows aligned with the record's splats, values as the golden's."""
+    import torch
+
+    from paper_2503_21364_b200 import GaussianModel, render_image
+    from paper_2503_21364_b200.train import backward_render
+
+    z, g, cam = _load("backward_ts16.npz")
+    model = GaussianModel.from_host(g)
+    subset = None
+    if use_subset:  # every Gaussian, shuffled: same image, record in caller order
+        subset = np.random.default_rng(3).permutation(g.count)
+    _, touched, rec = render_image(model, cam(), int(z["tile_size"]), (0.0, 0.0, 0.0),
+                                   with_record=True, subset=subset)
+    gr = backward_render(torch.as_tensor(z["image_grad"]).cuda(), rec)
+    pid = rec.prim_id.numpy()
+    assert gr.d_colors.shape == (len(pid), 3)
+    _close(gr.d_colors.cpu().numpy(), z["d_colors"][pid], 1e-9, "d_colors")
+    _close(gr.d_opacities.cpu().numpy(), z["d_opacities"][pid], 1e-9, "d_opacities")
+    _close(gr.d_mean2d.cpu().numpy(), z["d_mean2d"][pid], 1e-9, "d_mean2d")
+    assert int(np.abs(gr.touched.cpu().numpy() - z["touched"][pid]).sum()) <= 2
+    np.testing.assert_array_equal(gr.touched.cpu().numpy(), touched.cpu().numpy())
