@@ -160,7 +160,8 @@ int lmgs_get_stats(lmgs_context* ctx, lmgs_stats* out);
  * (the Gaussian's row in the input arrays), prim_ids[K] = original Gaussian id
  * (TileRecord.order mapped through splats.prim_id).  Lists are sorted by tile,
  * then by (fp64 depth, prim id).  Either pointer may be NULL.  Device buffers,
- * K entries. */
+ * K entries.  The render's lmgs_gaussians.prim_ids array (when given) must
+ * still be valid; everything else lives in the context. */
 int lmgs_copy_instances(lmgs_context* ctx, uint64_t* keys, int64_t* prim_ids, void* stream);
 
 /* Pixels the last render queued for the exact-touched replay (K7b):
