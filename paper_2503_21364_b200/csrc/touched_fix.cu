@@ -39,6 +39,73 @@ constexpr int kRound = 32 * kProdWarps;           // splats per round
 __device__ unsigned int g_fix_hist[8];
 #endif
 
+// a list entry's id and first record sector (mx, my, r^2, qa, qb)
+struct FixRec {
+  uint32_t id;
+  bool valid;
+  double2 s0, s1;
+};
+// the circle test of one splat at the pixel and, when inside, what fp64 sigma
+// needs: the blend's fp32 exponent terms and K1's inputs
+struct FixIn {
+  uint32_t id;
+  bool inside;
+  float dx, dy, qa, qb;
+  float2 cl;  // qc, log2 alpha
+  float4 q;
+  float m0, m1, m2, sc0, sc1, sc2, logit;
+};
+
+__device__ __forceinline__ void load_rec(const TouchedFixArgs& a, const uint64_t* list,
+                                         int2 range, int j, FixRec& r) {
+  r.valid = j < range.y;
+  if (r.valid) {
+    r.id = (uint32_t)list[j];
+    const double2* r16 = reinterpret_cast<const double2*>(a.recs + r.id);
+    r.s0 = r16[0];
+    r.s1 = r16[1];
+  }
+}
+
+__device__ __forceinline__ void test_and_load(const TouchedFixArgs& a, const FixRec& r, int x0,
+                                              int y0, int ts, float px, float py, double pxd,
+                                              double pyd, FixIn& f) {
+  f.inside = false;
+  f.id = r.id;
+  if (!r.valid) return;
+  const double rmx = r.s0.x, rmy = r.s0.y, rr2 = r.s1.x;
+  const float2 qab = *reinterpret_cast<const float2*>(&r.s1.y);
+  // the blend's fp32 view of the splat (blend.cu, same expressions)
+  const double mxl = rmx - (double)x0, myl = rmy - (double)y0;
+  const double ax = fabs(mxl) + (double)ts, ay = fabs(myl) + (double)ts;
+  const double band =
+      __dmul_rn(__dadd_rn(__dadd_rn(rr2, __dmul_rn(ax, ax)), __dmul_rn(ay, ay)), 0x1p-18);
+  const float fx = (float)mxl, fy = (float)myl;
+  const float dx = px - fx, dy = py - fy;
+  const float d2 = fmaf(dx, dx, dy * dy);
+  bool inside = d2 <= __double2float_rd(rr2 - band);
+  if (!inside && d2 <= __double2float_ru(rr2 + band)) {
+    const double ddx = pxd - rmx, ddy = pyd - rmy;
+    inside = __dadd_rn(__dmul_rn(ddx, ddx), __dmul_rn(ddy, ddy)) <= rr2;
+  }
+  f.inside = inside;
+  if (!inside) return;
+  const uint32_t id = r.id;
+  f.dx = dx;
+  f.dy = dy;
+  f.qa = qab.x;
+  f.qb = qab.y;
+  f.cl = reinterpret_cast<const float2*>(a.recs + id)[4];
+  f.q = reinterpret_cast<const float4*>(a.quats)[id];
+  f.m0 = a.means[3 * (size_t)id];
+  f.m1 = a.means[3 * (size_t)id + 1];
+  f.m2 = a.means[3 * (size_t)id + 2];
+  f.sc0 = a.scales[3 * (size_t)id];
+  f.sc1 = a.scales[3 * (size_t)id + 1];
+  f.sc2 = a.scales[3 * (size_t)id + 2];
+  f.logit = a.logits[id];
+}
+
 // One CTA per queued pixel, as a two-stage pipeline over rounds of 224
 // consecutive splats of the tile list.  Producer warps (1..7) take 32 splats
 // each: the blend's fp32 circle test and exponent, and for the splats the
@@ -68,15 +135,18 @@ __global__ void __launch_bounds__(kFixThreads) k_touched_fix(TouchedFixArgs a) {
     float T32 = 1.0f;  // thread 0's recurrences
     double T64 = 1.0;
     if (tid == 0) s_done = 0;
-    // producers prefetch their first splat (id, first record sector)
+    // producer pipeline, three rounds deep: round r + 2's ids and first
+    // record sectors load, round r + 1 takes the circle test and (inside
+    // lanes) issues the loads of its geometry inputs, round r computes fp64
+    // sigma from inputs that arrived during the previous round
     const int pt = 32 * (warp - 1) + lane;  // producer slot within a round
-    uint32_t nid = 0;
-    double2 n0 = make_double2(0.0, 0.0), n1 = n0;
-    if (warp > 0 && range.x + pt < range.y) {
-      nid = (uint32_t)list[range.x + pt];
-      const double2* r16 = reinterpret_cast<const double2*>(a.recs + nid);
-      n0 = r16[0];
-      n1 = r16[1];
+    FixRec ra{}, rb{};  // rounds r + 1 and r + 2: id + first record sector
+    FixIn ia{};         // round r: circle test result and geometry inputs
+    if (warp > 0) {
+      load_rec(a, list, range, range.x + pt, ra);
+      load_rec(a, list, range, range.x + kRound + pt, rb);
+      test_and_load(a, ra, x0, y0, ts, px, py, pxd, pyd, ia);
+      ra = rb;
     }
     __syncthreads();
 #ifdef LMGS_FIX_STATS
@@ -85,59 +155,32 @@ __global__ void __launch_bounds__(kFixThreads) k_touched_fix(TouchedFixArgs a) {
     for (int r = 0; r <= nr; ++r) {
       const int buf = r & 1;
       if (warp > 0 && r < nr) {  // produce round r
-        const int j = range.x + r * kRound + pt;
-        const uint32_t id = nid;
-        const double2 s0 = n0, s1 = n1;
-        if (j + kRound < range.y) {  // prefetch round r + 1
-          nid = (uint32_t)list[j + kRound];
-          const double2* r16 = reinterpret_cast<const double2*>(a.recs + nid);
-          n0 = r16[0];
-          n1 = r16[1];
-        }
-        bool inside = false;
-        float power = 0.0f;
-        if (j < range.y) {
-          // first record sector: mx, my, r^2, qa, qb (the second only when inside)
-          const double rmx = s0.x, rmy = s0.y, rr2 = s1.x;
-          const float2 qab = *reinterpret_cast<const float2*>(&s1.y);
-          // the blend's fp32 view of the splat (blend.cu, same expressions)
-          const double mxl = rmx - (double)x0, myl = rmy - (double)y0;
-          const double ax = fabs(mxl) + (double)ts, ay = fabs(myl) + (double)ts;
-          const double band = __dmul_rn(
-              __dadd_rn(__dadd_rn(rr2, __dmul_rn(ax, ax)), __dmul_rn(ay, ay)), 0x1p-18);
-          const float fx = (float)mxl, fy = (float)myl;
-          const float dx = px - fx, dy = py - fy;
-          const float d2 = fmaf(dx, dx, dy * dy);
-          inside = d2 <= __double2float_rd(rr2 - band);
-          if (!inside && d2 <= __double2float_ru(rr2 + band)) {
-            const double ddx = pxd - rmx, ddy = pyd - rmy;
-            inside = __dadd_rn(__dmul_rn(ddx, ddx), __dmul_rn(ddy, ddy)) <= rr2;
-          }
-          if (inside) {
-            const float2 cl = reinterpret_cast<const float2*>(a.recs + id)[4];  // qc, log2 a
-            power = fmaf(fmaf(qab.x, dx, qab.y * dy), dx, fmaf(cl.x * dy, dy, cl.y));
-          }
-        }
+        const FixIn cur = ia;
+        FixRec nx{};
+        load_rec(a, list, range, range.x + (r + 2) * kRound + pt, nx);
+        test_and_load(a, ra, x0, y0, ts, px, py, pxd, pyd, ia);  // round r + 1
+        ra = nx;
+        const bool inside = cur.inside;
         const uint32_t m = __ballot_sync(0xffffffffu, inside);
         if (lane == 0) s_cnt[buf][warp - 1] = __popc(m);
         if (inside) {
           const int pos = __popc(m & lanemask_lt());
+          const uint32_t id = cur.id;
+          const float power = fmaf(fmaf(cur.qa, cur.dx, cur.qb * cur.dy), cur.dx,
+                                   fmaf(cur.cl.x * cur.dy, cur.dy, cur.cl.y));
           // _blend 308-313 in fp64 from K1's geometry
-          const double m0 = a.means[3 * (size_t)id], m1 = a.means[3 * (size_t)id + 1],
-                       m2 = a.means[3 * (size_t)id + 2];
+          const double m0 = cur.m0, m1 = cur.m1, m2 = cur.m2;
           const double x = mkl_dot3(m0, cam.r[0], m1, cam.r[1], m2, cam.r[2]) + cam.t[0];
           const double y = mkl_dot3(m0, cam.r[3], m1, cam.r[4], m2, cam.r[5]) + cam.t[1];
           const double z = mkl_dot3(m0, cam.r[6], m1, cam.r[7], m2, cam.r[8]) + cam.t[2];
-          const float4 q = reinterpret_cast<const float4*>(a.quats)[id];
           double mx, my, c00, c01, c11, radius;
-          splat_geometry(cam, x, y, z, q, a.scales[3 * (size_t)id],
-                         a.scales[3 * (size_t)id + 1], a.scales[3 * (size_t)id + 2], &mx, &my,
-                         &c00, &c01, &c11, &radius);
+          splat_geometry(cam, x, y, z, cur.q, cur.sc0, cur.sc1, cur.sc2, &mx, &my, &c00, &c01,
+                         &c11, &radius);
           const double det = c00 * c11 - c01 * c01;
           const double ca = c11 / det, cb = -c01 / det, cc = c00 / det;
           const double ddx = pxd - mx, ddy = pyd - my;
           const double maha = (ca * (ddx * ddx) + ((2.0 * cb) * ddx) * ddy) + cc * (ddy * ddy);
-          const double op = 1.0 / (1.0 + exp(-(double)a.logits[id]));
+          const double op = 1.0 / (1.0 + exp(-(double)cur.logit));
           s_sig[buf][warp - 1][pos] = op * exp(-0.5 * maha);
           s_pow[buf][warp - 1][pos] = power;
           s_id[buf][warp - 1][pos] = id;
