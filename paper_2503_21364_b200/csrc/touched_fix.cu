@@ -241,7 +241,10 @@ namespace lmgs {
 #endif
 
 int launch_touched_fix(const TouchedFixArgs& a, cudaStream_t s) {
-  k_touched_fix<<<148 * (2048 / kFixThreads), kFixThreads, 0, s>>>(a);
+#ifndef LMGS_FIX_CTAS_PER_SM
+#define LMGS_FIX_CTAS_PER_SM (2048 / kFixThreads)
+#endif
+  k_touched_fix<<<148 * LMGS_FIX_CTAS_PER_SM, kFixThreads, 0, s>>>(a);
   return 1;
 }
 
