@@ -615,7 +615,7 @@ int lmgs_backward(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* c
                   double* d_logits, double* grad_norm_sum, int64_t* steps_seen,
                   void* stream) {
   if (int r = validate(c, g, cam, s)) return r;
-  if (!image_grad || !d_colors || !d_opacities || !d_mean2d || !touched)
+  if (!image_grad || (g->count > 0 && (!d_colors || !d_opacities || !d_mean2d || !touched)))
     return fail(c, LMGS_ERR_INVALID, "null backward output");
   const CamArgs ca = make_cam(cam, s->tile_size);
   const int64_t tiles = (int64_t)ca.tiles_x * ca.tiles_y;

@@ -293,3 +293,29 @@ def test_backward_render_reference_signature(use_subset):
     _close(gr.d_mean2d.cpu().numpy(), z["d_mean2d"][pid], 1e-9, "d_mean2d")
     assert int(np.abs(gr.touched.cpu().numpy() - z["touched"][pid]).sum()) <= 2
     np.testing.assert_array_equal(gr.touched.cpu().numpy(), touched.cpu().numpy())
+
+
+@pytest.mark.gpu
+def test_backward_empty_and_culled_scenes():
+    """No splats on screen: zero gradients, zero touched, loss of the background."""
+    import torch
+
+    from paper_2503_21364_b200 import GaussianModel, scenes
+    from paper_2503_21364_b200.camera import Camera
+    from paper_2503_21364_b200.train import backward_render, render_loss_and_grads
+
+    cam = Camera(40.0, 40.0, 16.0, 16.0, 32, 32, np.eye(3), np.zeros(3))
+    g0 = scenes.synthetic_gaussians(0, seed=0, sh_degree=1)
+    _, gr = backward_render(GaussianModel.from_host(g0), cam, torch.ones(32, 32, 3).cuda())
+    assert gr.d_colors.numel() == 0
+    behind = scenes.HostGaussians(np.array([[0, 0, -2.0]] * 5, np.float32),
+                                  np.tile(np.array([[1, 0, 0, 0]], np.float32), (5, 1)),
+                                  np.full((5, 3), 0.3, np.float32), np.zeros(5, np.float32),
+                                  np.ones((5, 4, 3), np.float32), 1)
+    m = GaussianModel.from_host(behind)
+    _, gr = backward_render(m, cam, torch.ones(32, 32, 3).cuda(), 16, (0.2, 0.3, 0.4))
+    assert float(gr.d_colors.abs().sum()) == 0.0 and int(gr.touched.sum()) == 0
+    gt = np.full((32, 32, 3), 0.5)
+    loss, grads, stats = render_loss_and_grads(m, [cam], [gt], 16, (0.2, 0.3, 0.4))
+    assert abs(loss - float(np.mean((np.array([0.2, 0.3, 0.4]) - 0.5) ** 2))) < 1e-6
+    assert float(grads["sh"].abs().sum()) == 0.0 and int(stats.steps_seen.sum()) == 0
