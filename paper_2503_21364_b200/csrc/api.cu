@@ -666,7 +666,7 @@ int lmgs_project(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* ca
                  const lmgs_settings* s, double* mean2d, double* cov2d, double* depth,
                  double* radius, float* colors, float* opacity, uint8_t* kept, void* stream) {
   if (int r = validate(c, g, cam, s)) return r;
-  if (!mean2d || !cov2d || !depth || !radius || !colors || !opacity)
+  if (g->count > 0 && (!mean2d || !cov2d || !depth || !radius || !colors || !opacity))
     return fail(c, LMGS_ERR_INVALID, "null output");
   DeviceGuard guard(c->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -170,13 +170,15 @@ int lmgs_checkpoint_info_read(const char* path, lmgs_checkpoint_info* info, char
 int lmgs_checkpoint_load(const char* path, float* means, float* quats, float* scales,
                          float* logits, float* sh, uint32_t* grid_table_host, void* stream,
                          char* err, int err_len) {
-  if (!path || !means || !quats || !scales || !logits || !sh) return LMGS_ERR_INVALID;
+  if (!path) return LMGS_ERR_INVALID;
   File file;
   file.f = fopen(path, "rb");
   if (!file.f)
     return set_err(err, err_len, LMGS_ERR_IO, std::string(path) + ": " + strerror(errno));
   lmgs_checkpoint_info info;
   if (int r = read_info(file.f, path, &info, err, err_len)) return r;
+  if (info.count > 0 && (!means || !quats || !scales || !logits || !sh))
+    return set_err(err, err_len, LMGS_ERR_INVALID, "null destination array");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int stride = info.row_floats;
   const size_t chunk_bytes = kChunkRows * (size_t)stride * 4;
