@@ -319,3 +319,53 @@ def test_backward_empty_and_culled_scenes():
     loss, grads, stats = render_loss_and_grads(m, [cam], [gt], 16, (0.2, 0.3, 0.4))
     assert abs(loss - float(np.mean((np.array([0.2, 0.3, 0.4]) - 0.5) ** 2))) < 1e-6
     assert float(grads["sh"].abs().sum()) == 0.0 and int(stats.steps_seen.sum()) == 0
+
+
+@pytest.mark.gpu
+def test_degree3_sh_gradients_match_finite_differences():
+    """Our extension beyond the reference (which evaluates degrees 0-1 only):
+    with sh_eval_degree=3 the chain to coefficients 4-15 (standard real SH
+    basis) matches central differences of the fp64 oracle render at degree 3."""
+    import oracle
+
+    from paper_2503_21364_b200 import GaussianModel, scenes
+    from paper_2503_21364_b200.train import render_loss_and_grads
+
+    rng = np.random.default_rng(4)
+    n = 12
+    quats = rng.standard_normal((n, 4))
+    quats /= np.linalg.norm(quats, axis=1, keepdims=True)
+    sh = np.zeros((n, 16, 3))
+    sh[:, 0] = rng.uniform(0.8, 1.6, (n, 3))  # keep the clamp gate open
+    sh[:, 1:] = rng.uniform(-0.2, 0.2, (n, 15, 3))
+    f = np.float32
+    g = scenes.HostGaussians(rng.uniform(-2.5, 2.5, (n, 3)).astype(f), quats.astype(f),
+                             rng.uniform(0.2, 0.5, (n, 3)).astype(f),
+                             rng.uniform(-1.0, 1.5, n).astype(f), sh.astype(f), 3)
+    cam = _front_camera(24, 24)
+    gt = rng.uniform(0, 1, (24, 24, 3))
+    _, grads, _ = render_loss_and_grads(GaussianModel.from_host(g), [cam], [gt], 16,
+                                        sh_eval_degree=3)
+    d_sh = grads["sh"].cpu().numpy()
+
+    def loss_of(gg):
+        return float(((oracle.render(gg, cam, sh_eval_degree=3)["image"] - gt) ** 2).mean())
+
+    h = 2.0 ** -12
+    checked = 0
+    for i in range(n):
+        for k in (4, 7, 9, 12, 15):
+            c = (i + k) % 3
+            gg = type(g)(g.means, g.quats, g.scales, g.opacity_logits, g.sh.copy(), 3)
+            x = gg.sh[i, k, c]
+            gg.sh[i, k, c] = x + np.float32(h)
+            up = loss_of(gg)
+            gg.sh[i, k, c] = x - np.float32(h)
+            dn = loss_of(gg)
+            fd = (up - dn) / (2 * h)
+            an = float(d_sh[i, k, c])
+            if abs(fd) < 1e-8 and abs(an) < 1e-8:
+                continue
+            assert abs(an - fd) <= 1e-3 * max(abs(fd), abs(an), 1e-6), (i, k, c, an, fd)
+            checked += 1
+    assert checked >= 30
