@@ -204,7 +204,7 @@ def run_ours(args, rank, world, local):
     all_cams = scenes.orbit_cameras(views * world, W, H, seed=0)
     cams = all_cams[rank * views:(rank + 1) * views]
     renderer = BatchRenderer(model, W, H, views, tile_size=16, sh_eval_degree=3,
-                             n_streams=args.streams)
+                             n_streams=args.streams, group=args.group)
 
     # warm-up (also sizes every arena)
     for _ in range(args.warmup):
@@ -290,6 +290,7 @@ def run_ours(args, rank, world, local):
                                    f"{views} orbit views per GPU, tile 16",
                        "gaussians": N_GAUSS, "views_per_gpu": views, "width": W, "height": H,
                        "parallelism": f"camera-batch dp{world}",
+                       "views_per_k1_launch": args.group,
                        "l2": "no flush: scene 1.42 GB and per-view buffers > 126 MB L2",
                        "geometry": "fp64 (bit-exact tile lists)", "blend": "fp32"},
             "gpu_launches": renderer.launches_per_step * args.steps,
@@ -319,6 +320,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=3,
                     help="contexts/streams the view batch alternates over")
+    ap.add_argument("--group", type=int, default=2,
+                    help="views per shared K1 launch (lmgs_render_group; 1 = lmgs_render)")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":

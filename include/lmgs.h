@@ -152,6 +152,20 @@ int lmgs_render_batch(lmgs_context* ctx, const lmgs_gaussians* g, const lmgs_cam
                       int32_t n_views, const lmgs_settings* s, const lmgs_frame* out,
                       void* stream);
 
+/* Render a group of n_views (1..LMGS_MAX_GROUP) views of the same Gaussians,
+ * view v on its own context ctxs[v] (distinct, one device) and stream
+ * streams[v].  The preprocess of the whole group is ONE launch on streams[0]
+ * that stages each block of Gaussians once and projects it for every view
+ * (inputs read from HBM once per group, not once per view); each view's
+ * depth sort, emission, tile sort and blend then run on its own stream.
+ * Outputs are identical to n_views lmgs_render calls.  Same reference
+ * interface as lmgs_render: the per-pose loop of run_session
+ * (render_runtime.py:250-308) over render_image (gaussian_core.py:582-597). */
+#define LMGS_MAX_GROUP 8
+int lmgs_render_group(lmgs_context* const* ctxs, int32_t n_views, const lmgs_gaussians* g,
+                      const lmgs_camera* cams, const lmgs_settings* s, const lmgs_frame* out,
+                      void* const* streams);
+
 /* Statistics of the last lmgs_render on this context (stage times require the
  * stream to have completed: call after synchronising). */
 int lmgs_get_stats(lmgs_context* ctx, lmgs_stats* out);

@@ -34,7 +34,8 @@ EXPORTS = ("lmgs_abi_version", "lmgs_context_create", "lmgs_context_destroy", "l
            "lmgs_project", "lmgs_composite_blocks", "lmgs_checkpoint_info_read",
            "lmgs_checkpoint_load", "lmgs_checkpoint_save", "lmgs_encode_rgb8",
            "lmgs_backward", "lmgs_mse_grad", "lmgs_render_strips", "lmgs_signal_flags",
-           "lmgs_wait_flags", "lmgs_touched_fix_count")
+           "lmgs_wait_flags", "lmgs_touched_fix_count", "lmgs_render_group")
+MAX_GROUP = 8  # LMGS_MAX_GROUP
 
 
 class Camera(ctypes.Structure):
@@ -101,6 +102,9 @@ def lib():
                               ctypes.POINTER(Settings), ctypes.POINTER(Frame), P]
     L.lmgs_render_batch.argtypes = [P, ctypes.POINTER(Gaussians), ctypes.POINTER(Camera), I32,
                                     ctypes.POINTER(Settings), ctypes.POINTER(Frame), P]
+    L.lmgs_render_group.argtypes = [ctypes.POINTER(P), I32, ctypes.POINTER(Gaussians),
+                                    ctypes.POINTER(Camera), ctypes.POINTER(Settings),
+                                    ctypes.POINTER(Frame), ctypes.POINTER(P)]
     L.lmgs_get_stats.argtypes = [P, ctypes.POINTER(Stats)]
     L.lmgs_copy_instances.argtypes = [P, P, P, P]
     L.lmgs_project.argtypes = [P, ctypes.POINTER(Gaussians), ctypes.POINTER(Camera),

@@ -28,7 +28,8 @@ def tile_passes(tiles: int) -> int:
 class BatchRenderer:
     def __init__(self, model: GaussianModel, width: int, height: int, max_views: int,
                  tile_size: int = 16, sh_eval_degree: int = 3, background=(0.0, 0.0, 0.0),
-                 with_touched: bool = True, n_streams: int = 2):
+                 with_touched: bool = True, n_streams: int = 2, group: int = 1,
+                 page_mask: torch.Tensor | None = None):
         self.model = model
         self.dev = model.device
         self.w, self.h, self.ts = int(width), int(height), int(tile_size)
@@ -46,13 +47,21 @@ class BatchRenderer:
         n = model.count
         self.touched = torch.empty((v, n), dtype=torch.int32, device=dev) if with_touched else None
         self.kept = torch.empty((v, n), dtype=torch.uint8, device=dev)
-        self.ctxs = [_lib.Context(dev.index) for _ in range(n_streams)]
-        self.streams = [torch.cuda.Stream(device=dev) for _ in range(n_streams)]
+        # group > 1: views go through lmgs_render_group `group` at a time (one
+        # K1 launch reads the scene once for the whole group); n_streams sets
+        # of `group` contexts/streams alternate between consecutive groups
+        self.group = max(1, min(int(group), _lib.MAX_GROUP))
+        nctx = n_streams * self.group
+        self.ctxs = [_lib.Context(dev.index) for _ in range(nctx)]
+        self.streams = [torch.cuda.Stream(device=dev) for _ in range(nctx)]
         self.done = [torch.cuda.Event() for _ in range(n_streams)]
         self.view_done = [torch.cuda.Event() for _ in range(v)]
         self.stats = []
         self.launches_per_step = None  # liblmgs kernels per render() call (set by stage_times)
-        self._g = model._abi()
+        # page_mask (device uint8 per 128-row page, as render()): rows past a
+        # page's live count are culled
+        self._page_mask = page_mask
+        self._g = model._abi(None, page_mask, 7 if page_mask is not None else 0)
 
     def _frame(self, i) -> _lib.Frame:
         return _lib.Frame(_ptr(self.rgb[i]), _ptr(self.alpha[i]), _ptr(self.depth[i]), None,
@@ -77,20 +86,19 @@ class BatchRenderer:
         if stage_times:
             tot = {}
             inst = pairs = vis = launches = 0
-            ctx = self.ctxs[0]
-            for i, cam in enumerate(cams):
-                c = abi_camera(cam)
-                fr = self._frame(i)
-                _lib.check(ctx.handle, L.lmgs_render(ctx.handle, ctypes.byref(g), ctypes.byref(c),
-                                                     ctypes.byref(st), ctypes.byref(fr),
-                                                     caller.cuda_stream), "lmgs_render")
-                s = ctx.stats()
-                for k, v in s["stage_ms"].items():
-                    tot[k] = tot.get(k, 0.0) + v
-                inst += s["n_instances"]
-                vis += s["n_visible"]
-                launches += s["n_launches"]
-                pairs += self._pairs(i)
+            G = self.group
+            for start in range(0, len(cams), G):
+                idx = list(range(start, min(start + G, len(cams))))
+                ctxs = self.ctxs[:len(idx)]
+                self._launch(L, g, st, ctxs, [caller] * len(idx), cams, idx)
+                for j, i in enumerate(idx):
+                    s = ctxs[j].stats()
+                    for k, v in s["stage_ms"].items():
+                        tot[k] = tot.get(k, 0.0) + v
+                    inst += s["n_instances"]
+                    vis += s["n_visible"]
+                    launches += s["n_launches"]
+                    pairs += self._pairs(i)
             self.launches_per_step = launches
             nv = len(cams)
             n = self.model.count
@@ -102,7 +110,8 @@ class BatchRenderer:
             p = tile_passes(t)
             proc = self._processed_total(len(cams)) / nv
             alg = {  # algorithmic bytes per frame
-                "preprocess": n * (44 + s_read + 89),
+                # the inputs are read once per group of views
+                "preprocess": n * ((44 + s_read) / self.group + 89),
                 "depth_sort": n * (4 + 4 * 16 - 4 + 4),
                 "emit": 16 * v_avg + 8 * k_avg,
                 "tile_sort": 16 * p * k_avg + 8 * k_avg + 8 * t,
@@ -111,27 +120,46 @@ class BatchRenderer:
             return {"stage_ms": tot, "alg_bytes": alg,
                     "per_frame": {"instances": k_avg, "visible": v_avg, "pairs": pairs / nv,
                                   "processed": proc, "tile_passes": p}}
-        ns = len(self.streams)
+        G = self.group
+        nsets = len(self.streams) // G
         for s in self.streams:
             s.wait_stream(caller)
-        for i, cam in enumerate(cams):
-            j = i % ns
-            ctx, s = self.ctxs[j], self.streams[j]
-            c = abi_camera(cam)
-            fr = self._frame(i)
-            _lib.check(ctx.handle, L.lmgs_render(ctx.handle, ctypes.byref(g), ctypes.byref(c),
-                                                 ctypes.byref(st), ctypes.byref(fr),
-                                                 s.cuda_stream), "lmgs_render")
-            self.view_done[i].record(s)
-            if host_rgb is not None:
-                copy_stream.wait_event(self.view_done[i])
-                with torch.cuda.stream(copy_stream):
-                    host_rgb[i].copy_(self.rgb[i], non_blocking=True)
+        for gi, start in enumerate(range(0, len(cams), G)):
+            idx = list(range(start, min(start + G, len(cams))))
+            base = (gi % nsets) * G
+            streams = self.streams[base:base + len(idx)]
+            self._launch(L, g, st, self.ctxs[base:base + len(idx)], streams, cams, idx)
+            for j, i in enumerate(idx):
+                self.view_done[i].record(streams[j])
+                if host_rgb is not None:
+                    copy_stream.wait_event(self.view_done[i])
+                    with torch.cuda.stream(copy_stream):
+                        host_rgb[i].copy_(self.rgb[i], non_blocking=True)
         for s in self.streams:
             caller.wait_stream(s)
         if host_rgb is not None:
             caller.wait_stream(copy_stream)
         return None
+
+    def _launch(self, L, g, st, ctxs, streams, cams, idx):
+        """Views idx on ctxs / streams: lmgs_render for one view, else one
+        lmgs_render_group (shared K1 launch on streams[0])."""
+        if len(idx) == 1:
+            ctx, i = ctxs[0], idx[0]
+            c = abi_camera(cams[i])
+            fr = self._frame(i)
+            _lib.check(ctx.handle, L.lmgs_render(ctx.handle, ctypes.byref(g), ctypes.byref(c),
+                                                 ctypes.byref(st), ctypes.byref(fr),
+                                                 streams[0].cuda_stream), "lmgs_render")
+            return
+        n = len(idx)
+        handles = (ctypes.c_void_p * n)(*[c.handle for c in ctxs])
+        cam_arr = (_lib.Camera * n)(*[abi_camera(cams[i]) for i in idx])
+        frames = (_lib.Frame * n)(*[self._frame(i) for i in idx])
+        sptrs = (ctypes.c_void_p * n)(*[s.cuda_stream for s in streams])
+        _lib.check(ctxs[0].handle, L.lmgs_render_group(handles, n, ctypes.byref(g), cam_arr,
+                                                       ctypes.byref(st), frames, sptrs),
+                   "lmgs_render_group")
 
     def _pairs(self, i) -> float:
         """Pixel-instance pairs evaluated by the blend of view i: sum_t P_t n_t."""

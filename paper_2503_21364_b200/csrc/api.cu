@@ -18,6 +18,7 @@
 #include "lmgs_internal.cuh"
 
 using namespace lmgs;
+static_assert(LMGS_MAX_GROUP == kMaxPreViews, "one K1 launch per group");
 
 namespace {
 
@@ -109,6 +110,8 @@ struct lmgs_context {
   uint64_t* h_pinned = nullptr;  // [0..2] = n_kept, n_vis, K
   cudaEvent_t ev[2 * kNumStages] = {};
   cudaEvent_t counts_ready = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_pre = nullptr;  // lmgs_render_group cross-stream order
+  int pre_share = 1;  // views sharing the last K1 launch (its stage time is split)
   bool events_ok = false;
   int64_t cap_n = -1, cap_t = -1, cap_k = -1;
   // per-Gaussian arena
@@ -290,14 +293,24 @@ struct StageTimer {
   }
 };
 
-int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
-               const lmgs_settings* st, const lmgs_frame* out, cudaStream_t s,
-               const lmgs_strip_targets* strips = nullptr) {
-  const bool timed = (st->flags & LMGS_FLAG_STAGE_TIMES) && c->events_ok;
-  StageTimer tm{c, s, timed};
-  const CamArgs ca = make_cam(cam, st->tile_size);
-  const int64_t n = g->count;
-  const int64_t tiles = (int64_t)ca.tiles_x * ca.tiles_y;
+// one view's launch state between its K1 and the rest of its pipeline
+struct ViewPlan {
+  CamArgs ca;
+  int64_t n = 0, tiles = 0;
+  int tile_passes = 1;
+  int2* ranges = nullptr;
+  bool timed = false;
+  int launched = 0;
+};
+
+// stats, arenas and counter resets of one view (stream-ordered on s)
+int view_prepare(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
+                 const lmgs_settings* st, const lmgs_frame* out, cudaStream_t s, ViewPlan* vp) {
+  vp->timed = (st->flags & LMGS_FLAG_STAGE_TIMES) && c->events_ok;
+  vp->ca = make_cam(cam, st->tile_size);
+  const CamArgs& ca = vp->ca;
+  const int64_t n = vp->n = g->count;
+  const int64_t tiles = vp->tiles = (int64_t)ca.tiles_x * ca.tiles_y;
   c->stats = lmgs_stats{};
   c->stats.n_gaussians = n;
   c->stats.n_tiles = (int32_t)tiles;
@@ -306,30 +319,56 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
   c->stats.n_stages = kNumStages;
   for (int i = 0; i < kNumStages; ++i) c->stats.stage_names[i] = kStageNames[i];
   c->last_timed = false;
+  c->pre_share = 1;
   c->last_prim_ids = g->prim_ids;
   const int tile_bits = bits_for(tiles);
   if (tile_bits > 8 * kMaxTilePasses)
     return fail(c, LMGS_ERR_UNSUPPORTED, "more than 2^24 tiles in one view");
-  const int tile_passes = tile_bits ? (tile_bits + 7) / 8 : 1;
+  vp->tile_passes = tile_bits ? (tile_bits + 7) / 8 : 1;
 
   if (int r = ensure_gaussians(c, n > 0 ? n : 1, s)) return r;
   if (int r = ensure_tiles(c, tiles, s)) return r;
   // ranges live in the context arena (lmgs_backward and lmgs_copy_instances
   // read them after the call, whatever the caller did with its buffers);
   // the caller's tile_ranges gets a copy
-  int2* ranges = c->ranges;
-  c->last_ranges = ranges;
+  vp->ranges = c->ranges;
+  c->last_ranges = vp->ranges;
   Scalars* sc = c->d_scal;
   LMGS_CUDA(c, cudaMemsetAsync(sc->counts, 0, sizeof(sc->counts), s));
   LMGS_CUDA(c, cudaMemsetAsync(&sc->zrange[0], 0xff, sizeof(sc->zrange[0]), s));
   LMGS_CUDA(c, cudaMemsetAsync(&sc->zrange[1], 0, sizeof(sc->zrange[1]), s));
   if (out->touched && n > 0) LMGS_CUDA(c, cudaMemsetAsync(out->touched, 0, sizeof(int32_t) * n, s));
+  return LMGS_OK;
+}
 
+int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
+                const lmgs_settings* st, const lmgs_frame* out, cudaStream_t s, ViewPlan* vp,
+                const lmgs_strip_targets* strips);
+
+int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
+               const lmgs_settings* st, const lmgs_frame* out, cudaStream_t s,
+               const lmgs_strip_targets* strips = nullptr) {
+  ViewPlan vp;
+  if (int r = view_prepare(c, g, cam, st, out, s, &vp)) return r;
+  StageTimer tm{c, s, vp.timed};
   // K1
-  int launched = 0;
   tm.begin(0);
-  launched += launch_preprocess(make_pre(c, g, ca, st, out->kept), s);
+  vp.launched += launch_preprocess(make_pre(c, g, vp.ca, st, out->kept), s);
   tm.end(0);
+  return view_finish(c, g, cam, st, out, s, &vp, strips);
+}
+
+// K2..K7 of one view whose K1 has been enqueued before `s`'s current tail
+int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
+                const lmgs_settings* st, const lmgs_frame* out, cudaStream_t s, ViewPlan* vp,
+                const lmgs_strip_targets* strips) {
+  StageTimer tm{c, s, vp->timed};
+  const CamArgs& ca = vp->ca;
+  const int64_t n = vp->n, tiles = vp->tiles;
+  const int tile_passes = vp->tile_passes;
+  int2* ranges = vp->ranges;
+  Scalars* sc = c->d_scal;
+  int launched = vp->launched;
   LMGS_CUDA(c, cudaMemcpyAsync(c->h_pinned, sc->counts, sizeof(sc->counts),
                                cudaMemcpyDeviceToHost, s));
   LMGS_CUDA(c, cudaEventRecord(c->counts_ready, s));
@@ -479,7 +518,7 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
   }
   tm.end(4);
   c->stats.n_launches = launched;
-  c->last_timed = timed;
+  c->last_timed = vp->timed;
   LMGS_CUDA(c, cudaGetLastError());
   return LMGS_OK;
 }
@@ -506,7 +545,9 @@ int lmgs_context_create(int device, lmgs_context** out) {
     lmgs_context_destroy(c);
     return e == cudaErrorMemoryAllocation ? LMGS_ERR_OOM : LMGS_ERR_CUDA;
   }
-  if (cudaEventCreateWithFlags(&c->counts_ready, cudaEventDisableTiming) != cudaSuccess) {
+  if (cudaEventCreateWithFlags(&c->counts_ready, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_pre, cudaEventDisableTiming) != cudaSuccess) {
     cudaGetLastError();
     lmgs_context_destroy(c);
     return LMGS_ERR_CUDA;
@@ -532,6 +573,8 @@ void lmgs_context_destroy(lmgs_context* c) {
   for (int i = 0; i < 2 * kNumStages; ++i)
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
   if (c->counts_ready) cudaEventDestroy(c->counts_ready);
+  if (c->ev_in) cudaEventDestroy(c->ev_in);
+  if (c->ev_pre) cudaEventDestroy(c->ev_pre);
   delete c;
 }
 
@@ -579,6 +622,60 @@ int lmgs_render_batch(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camer
   return LMGS_OK;
 }
 
+int lmgs_render_group(lmgs_context* const* ctxs, int32_t n_views, const lmgs_gaussians* g,
+                      const lmgs_camera* cams, const lmgs_settings* s, const lmgs_frame* out,
+                      void* const* streams) {
+  if (!ctxs || n_views < 1 || n_views > LMGS_MAX_GROUP || !cams || !out || !streams)
+    return ctxs && n_views >= 1 && ctxs[0] ? fail(ctxs[0], LMGS_ERR_INVALID, "bad view group")
+                                           : LMGS_ERR_INVALID;
+  for (int v = 0; v < n_views; ++v) {
+    lmgs_context* c = ctxs[v];
+    if (!c) return LMGS_ERR_INVALID;
+    if (int r = validate(c, g, cams + v, s)) return r;
+    if (!out[v].rgb) return fail(c, LMGS_ERR_INVALID, "frame.rgb is required");
+    if (c->device != ctxs[0]->device)
+      return fail(c, LMGS_ERR_INVALID, "group contexts must share one device");
+    for (int u = 0; u < v; ++u)
+      if (ctxs[u] == c) return fail(c, LMGS_ERR_INVALID, "group contexts must be distinct");
+  }
+  DeviceGuard guard(ctxs[0]->device);
+  cudaStream_t s0 = static_cast<cudaStream_t>(streams[0]);
+  ViewPlan vp[LMGS_MAX_GROUP];
+  PreprocessMulti m;
+  m.nv = n_views;
+  for (int v = 0; v < n_views; ++v) {
+    lmgs_context* c = ctxs[v];
+    cudaStream_t sv = static_cast<cudaStream_t>(streams[v]);
+    if (int r = view_prepare(c, g, cams + v, s, out + v, sv, vp + v)) return r;
+    m.v[v] = make_pre(c, g, vp[v].ca, s, out[v].kept);
+    if (sv != s0) {  // K1 (on streams[0]) follows each view's resets
+      LMGS_CUDA(c, cudaEventRecord(c->ev_in, sv));
+      LMGS_CUDA(c, cudaStreamWaitEvent(s0, c->ev_in, 0));
+    }
+  }
+  for (int v = 0; v < n_views; ++v) {
+    ctxs[v]->pre_share = n_views;
+    if (vp[v].timed) LMGS_CUDA(ctxs[v], cudaEventRecord(ctxs[v]->ev[0], s0));
+  }
+  const int k1 = launch_preprocess_multi(m, s0);
+  for (int v = 0; v < n_views; ++v) {
+    lmgs_context* c = ctxs[v];
+    cudaStream_t sv = static_cast<cudaStream_t>(streams[v]);
+    vp[v].launched = v == 0 ? k1 : 0;  // the shared launch is counted once
+    if (vp[v].timed) LMGS_CUDA(c, cudaEventRecord(c->ev[1], s0));
+    if (sv != s0) {
+      LMGS_CUDA(c, cudaEventRecord(c->ev_pre, s0));
+      LMGS_CUDA(c, cudaStreamWaitEvent(sv, c->ev_pre, 0));
+    }
+  }
+  for (int v = 0; v < n_views; ++v) {
+    if (int r = view_finish(ctxs[v], g, cams + v, s, out + v, static_cast<cudaStream_t>(streams[v]),
+                            vp + v, nullptr))
+      return r;
+  }
+  return LMGS_OK;
+}
+
 int lmgs_get_stats(lmgs_context* c, lmgs_stats* out) {
   if (!c || !out) return LMGS_ERR_INVALID;
   DeviceGuard guard(c->device);
@@ -587,7 +684,7 @@ int lmgs_get_stats(lmgs_context* c, lmgs_stats* out) {
     for (int i = 0; i < kNumStages; ++i) {
       float ms = 0.f;
       LMGS_CUDA(c, cudaEventElapsedTime(&ms, c->ev[2 * i], c->ev[2 * i + 1]));
-      c->stats.stage_ms[i] = ms;
+      c->stats.stage_ms[i] = i == 0 ? ms / (float)c->pre_share : ms;
     }
   }
   *out = c->stats;

@@ -73,7 +73,6 @@ struct PreprocessArgs {
   unsigned long long* n_vis;   // scalar (atomic): tiles touched > 0
   unsigned long long* n_inst;  // scalar (atomic): sum of tile counts = K
   unsigned long long* zrange;  // [2] fp64 bits of min / max visible depth (atomic)
-  uint64_t* sh_wait;           // set in-kernel: mbarrier guarding staged SH (TMA path)
   // optional fp64 dump for lmgs_project
   double* dbg_mean2d;
   double* dbg_cov2d;
@@ -84,6 +83,16 @@ struct PreprocessArgs {
 };
 
 int launch_preprocess(const PreprocessArgs& a, cudaStream_t s);  // returns kernels launched
+
+// K1 over several views of the same Gaussians: every block stages its inputs
+// once and projects them for each view (v[i] share the input arrays, n and
+// page mask; outputs and counters are per view).
+constexpr int kMaxPreViews = 8;
+struct PreprocessMulti {
+  PreprocessArgs v[kMaxPreViews];
+  int32_t nv;
+};
+int launch_preprocess_multi(const PreprocessMulti& m, cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // LSD radix sort (onesweep: one histogram pass + one scatter pass per digit

@@ -120,8 +120,8 @@ static_assert(kPreThreads == 128, "paged sets map one K1 block to one 128-row pa
 template <bool SMEM>
 __device__ __forceinline__ uint32_t process_one(const PreprocessArgs& a, int64_t i, double m0, double m1,
                                             double m2, float4 q, double s0, double s1, double s2,
-                                            float logit, const float* sh, bool* keep_out,
-                                            uint64_t* zbits_out) {
+                                            float logit, const float* sh, uint64_t* sh_wait,
+                                            bool* keep_out, uint64_t* zbits_out) {
   bool keep = false;
   uint32_t cnt = 0;
   uint64_t zb = 0;
@@ -160,7 +160,7 @@ __device__ __forceinline__ uint32_t process_one(const PreprocessArgs& a, int64_t
       const float log2_alpha =
           logit < -15.0f ? logit * (float)kLog2e : -log2f(1.0f + expf(-logit));
       float col[3] = {0.f, 0.f, 0.f};
-      if (SMEM) mbar_wait(a.sh_wait, 0);
+      if (SMEM) mbar_wait(sh_wait, 0);
       if (cnt || a.dbg_colors) {
         const double dx = m0 - cam.center[0], dy = m1 - cam.center[1], dz = m2 - cam.center[2];
         double nrm = sqrt((dx * dx + dy * dy) + dz * dz);
@@ -205,10 +205,12 @@ __device__ __forceinline__ uint32_t process_one(const PreprocessArgs& a, int64_t
 // block-aggregated counters: near-kept splats (M), visible splats, instances
 // (K), and the visible depth range (positive fp64 bits order like integers).
 // One atomic per counter per CTA: per-warp atomics on these five addresses
-// serialised in L2 and doubled the kernel's time.
+// serialised in L2 and doubled the kernel's time.  `slot` = the view within a
+// multi-view block (its own shared partials, so views need no extra barrier).
 __device__ __forceinline__ void count_kept(const PreprocessArgs& a, bool keep, uint32_t cnt,
-                                           uint64_t zbits) {
-  __shared__ unsigned long long s_acc[kPreThreads / 32][5];
+                                           uint64_t zbits, int slot = 0) {
+  __shared__ unsigned long long s_acc_all[kMaxPreViews][kPreThreads / 32][5];
+  auto& s_acc = s_acc_all[slot];
   const unsigned ballot = __ballot_sync(0xffffffffu, keep);
   const unsigned vis = __ballot_sync(0xffffffffu, cnt > 0);
   unsigned long long k = cnt;
@@ -256,29 +258,51 @@ __device__ __forceinline__ void cull_row(const PreprocessArgs& a, int64_t i) {
 }
 
 // direct loads (tail block, unaligned inputs)
-__global__ void __launch_bounds__(kPreThreads) k_preprocess_direct(PreprocessArgs a, int64_t first) {
+__global__ void __launch_bounds__(kPreThreads) k_preprocess_direct(
+    const __grid_constant__ PreprocessMulti m, int64_t first) {
+  const PreprocessArgs& a0 = m.v[0];
   const int64_t i = first + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  bool keep = false;
-  uint32_t cnt = 0;
-  uint64_t zb = 0;
-  if (i < a.n && a.page_mask && (int)(i & 127) >= (int)a.page_mask[i >> 7]) {
-    cull_row(a, i);
-  } else if (i < a.n) {
-    const float4 q = __ldg(reinterpret_cast<const float4*>(a.quats) + i);
-    cnt = process_one<false>(a, i, a.means[3 * i], a.means[3 * i + 1], a.means[3 * i + 2], q,
-                             a.scales[3 * i], a.scales[3 * i + 1], a.scales[3 * i + 2],
-                             a.logits[i], a.sh + i * a.sh_coeffs * 3, &keep, &zb);
+  const bool live = i < a0.n;
+  const bool dead = live && a0.page_mask && (int)(i & 127) >= (int)a0.page_mask[i >> 7];
+  for (int vi = 0; vi < m.nv; ++vi) {
+    const PreprocessArgs& a = m.v[vi];
+    bool keep = false;
+    uint32_t cnt = 0;
+    uint64_t zb = 0;
+    if (dead) {
+      cull_row(a, i);
+    } else if (live) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(a.quats) + i);
+      cnt = process_one<false>(a, i, a.means[3 * i], a.means[3 * i + 1], a.means[3 * i + 2], q,
+                               a.scales[3 * i], a.scales[3 * i + 1], a.scales[3 * i + 2],
+                               a.logits[i], a.sh + i * a.sh_coeffs * 3, nullptr, &keep, &zb);
+    }
+    count_kept(a, keep, cnt, zb, vi);
   }
-  count_kept(a, keep, cnt, zb);
 }
 
 // ---------------------------------------------------------------------------
 // TMA-staged path: one thread issues cp.async.bulk copies of the block's
 // means / quats / scales / logits (one mbarrier) and of its SH coefficients
 // (a second mbarrier); the SH bytes stream into shared memory while the fp64
-// geometry of the block is being computed.
+// geometry of the block is being computed.  With several views the staged
+// block is projected once per view: the 236 B/Gaussian of inputs are read
+// from HBM once per group of views instead of once per view.
 
-__global__ void __launch_bounds__(kPreThreads, LMGS_PRE_MIN_CTAS) k_preprocess_tma(PreprocessArgs a) {
+// NV (= m.nv) is a template argument so that every view's camera and output
+// pointers are constant-bank operands: with a runtime view index they would be
+// loaded into registers (and spill).
+// Views after the first keep more state in flight (the unrolled view bodies
+// overlap); at 7 CTAs/SM (72 registers) they spill, so a multi-view block
+// runs at LMGS_PRE_MULTI_MIN_CTAS.
+#ifndef LMGS_PRE_MULTI_MIN_CTAS
+#define LMGS_PRE_MULTI_MIN_CTAS 5
+#endif
+template <int NV>
+__global__ void __launch_bounds__(kPreThreads, NV == 1 ? LMGS_PRE_MIN_CTAS : LMGS_PRE_MULTI_MIN_CTAS)
+    k_preprocess_tma(
+    const __grid_constant__ PreprocessMulti m) {
+  const PreprocessArgs& a = m.v[0];  // inputs (shared by every view)
   extern __shared__ __align__(128) float smem_f[];
   float* s_means = smem_f;                       // [256*3]
   float* s_quats = s_means + kPreThreads * 3;    // [256*4]
@@ -289,8 +313,11 @@ __global__ void __launch_bounds__(kPreThreads, LMGS_PRE_MIN_CTAS) k_preprocess_t
   const int tid = threadIdx.x;
   const int64_t i0 = (int64_t)blockIdx.x * kPreThreads;
   if (a.page_mask && a.page_mask[i0 >> 7] == 0) {  // the block is one inactive page
-    cull_row(a, i0 + tid);
-    count_kept(a, false, 0, 0);
+#pragma unroll
+    for (int vi = 0; vi < NV; ++vi) {
+      cull_row(m.v[vi], i0 + tid);
+      count_kept(m.v[vi], false, 0, 0, vi);
+    }
     return;
   }
   if (tid == 0) {
@@ -311,20 +338,27 @@ __global__ void __launch_bounds__(kPreThreads, LMGS_PRE_MIN_CTAS) k_preprocess_t
   }
   mbar_wait(&s_bar[0], 0);
   const int64_t i = i0 + tid;
-  const float4 q = reinterpret_cast<const float4*>(s_quats)[tid];
-  // the SH wait happens inside process_one just before the colour is needed
-  a.sh_wait = &s_bar[1];
-  bool keep = false;
-  uint32_t cnt = 0;
-  uint64_t zb = 0;
-  if (a.page_mask && tid >= (int)a.page_mask[i0 >> 7]) {  // past the page's live rows
-    cull_row(a, i);
-  } else {
-    cnt = process_one<true>(a, i, s_means[3 * tid], s_means[3 * tid + 1], s_means[3 * tid + 2], q,
-                            s_scales[3 * tid], s_scales[3 * tid + 1], s_scales[3 * tid + 2],
-                            s_logits[tid], s_sh + tid * a.sh_coeffs * 3, &keep, &zb);
+  const bool dead = a.page_mask && tid >= (int)a.page_mask[i0 >> 7];  // past the page's live rows
+#pragma unroll
+  for (int vi = 0; vi < NV; ++vi) {
+    // re-read the staged inputs every view (a compiler barrier keeps them
+    // from being hoisted into registers that would live across views)
+    asm volatile("" ::: "memory");
+    const float4 q = reinterpret_cast<const float4*>(s_quats)[tid];
+    const PreprocessArgs& av = m.v[vi];
+    bool keep = false;
+    uint32_t cnt = 0;
+    uint64_t zb = 0;
+    if (dead) {
+      cull_row(av, i);
+    } else {
+      // the SH wait happens inside process_one just before the colour is needed
+      cnt = process_one<true>(av, i, s_means[3 * tid], s_means[3 * tid + 1], s_means[3 * tid + 2],
+                              q, s_scales[3 * tid], s_scales[3 * tid + 1], s_scales[3 * tid + 2],
+                              s_logits[tid], s_sh + tid * a.sh_coeffs * 3, &s_bar[1], &keep, &zb);
+    }
+    count_kept(av, keep, cnt, zb, vi);
   }
-  count_kept(a, keep, cnt, zb);
   // every thread must observe the SH barrier before the block may exit
   mbar_wait(&s_bar[1], 0);
 }
@@ -333,7 +367,15 @@ __global__ void __launch_bounds__(kPreThreads, LMGS_PRE_MIN_CTAS) k_preprocess_t
 }  // namespace
 
 int launch_preprocess(const PreprocessArgs& a, cudaStream_t s) {
-  if (a.n <= 0) return 0;
+  PreprocessMulti m;
+  m.v[0] = a;
+  m.nv = 1;
+  return launch_preprocess_multi(m, s);
+}
+
+int launch_preprocess_multi(const PreprocessMulti& m, cudaStream_t s) {
+  const PreprocessArgs& a = m.v[0];
+  if (a.n <= 0 || m.nv < 1 || m.nv > kMaxPreViews) return 0;
   int launched = 0;
   // full blocks through TMA when every chunk is 16-byte aligned and sized
   const bool aligned =
@@ -343,21 +385,31 @@ int launch_preprocess(const PreprocessArgs& a, cudaStream_t s) {
   const int64_t full = aligned ? a.n / kPreThreads : 0;
   if (full > 0) {
     const size_t smem = sizeof(float) * kPreThreads * (3 + 4 + 3 + 1 + 3 * a.sh_coeffs);
-    static size_t set[kMaxDevices] = {};
+    static size_t set[kMaxPreViews][kMaxDevices] = {};
     const int dev = current_device();
-    if (smem > set[dev]) {
-      cudaFuncSetAttribute(k_preprocess_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-      set[dev] = smem;
+    void (*kern)(PreprocessMulti) = nullptr;
+    switch (m.nv) {
+      case 1: kern = k_preprocess_tma<1>; break;
+      case 2: kern = k_preprocess_tma<2>; break;
+      case 3: kern = k_preprocess_tma<3>; break;
+      case 4: kern = k_preprocess_tma<4>; break;
+      case 5: kern = k_preprocess_tma<5>; break;
+      case 6: kern = k_preprocess_tma<6>; break;
+      case 7: kern = k_preprocess_tma<7>; break;
+      default: kern = k_preprocess_tma<8>; break;
     }
-    k_preprocess_tma<<<(unsigned)full, kPreThreads, smem, s>>>(a);
+    if (smem > set[m.nv - 1][dev]) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      set[m.nv - 1][dev] = smem;
+    }
+    kern<<<(unsigned)full, kPreThreads, smem, s>>>(m);
     ++launched;
   }
   const int64_t first = full * kPreThreads;
   const int64_t rest = a.n - first;
   if (rest > 0) {
     k_preprocess_direct<<<(unsigned)((rest + kPreThreads - 1) / kPreThreads), kPreThreads, 0, s>>>(
-        a, first);
+        m, first);
     ++launched;
   }
   return launched;

@@ -1,0 +1,83 @@
+"""Grouped views (lmgs_render_group): one K1 launch projects a staged block of
+Gaussians for up to 8 views, each view then runs its own pipeline.  The bar is
+bit-identity with one lmgs_render call per view for every output buffer (the
+per-view math is unchanged; only the input staging is shared), plus the
+oracle check of a grouped view."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2503_21364_b200 import GaussianModel, scenes
+from paper_2503_21364_b200.batch import BatchRenderer
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("rgb", "alpha", "depth", "touched", "kept", "ranges", "nproc")
+
+
+def _render_all(model, cams, w, h, group, stage_times=False, page_mask=None, n_streams=2):
+    r = BatchRenderer(model, w, h, len(cams), sh_eval_degree=3, n_streams=n_streams, group=group,
+                      page_mask=page_mask)
+    r.render(cams, stage_times=stage_times)
+    torch.cuda.synchronize()
+    return {f: getattr(r, f)[:len(cams)].cpu().clone() for f in FIELDS}
+
+
+@pytest.fixture(scope="module")
+def scene():
+    # 20,000 + 37 rows: full 128-row TMA blocks plus a direct-load tail block
+    g = scenes.synthetic_gaussians(20_037, seed=3)
+    return g, GaussianModel.from_host(g)
+
+
+@pytest.mark.parametrize("group", [2, 3, 4, 8])
+def test_group_equals_per_view(scene, group):
+    _, model = scene
+    cams = scenes.orbit_cameras(11, 320, 200, seed=1)  # 11 views: a ragged last group
+    ref = _render_all(model, cams, 320, 200, 1)
+    got = _render_all(model, cams, 320, 200, group)
+    for f in FIELDS:
+        assert torch.equal(ref[f], got[f]), f
+
+
+def test_group_stage_times_path_equal(scene):
+    _, model = scene
+    cams = scenes.orbit_cameras(5, 256, 256, seed=2)
+    ref = _render_all(model, cams, 256, 256, 1)
+    got = _render_all(model, cams, 256, 256, 4, stage_times=True)
+    for f in FIELDS:
+        assert torch.equal(ref[f], got[f]), f
+
+
+def test_group_paged_rows_culled(scene):
+    """Paged sets: pages with live count 0 and rows past a page's count are
+    culled for every view of the group."""
+    g, model = scene
+    pages = -(-model.count // 128)
+    rng = np.random.default_rng(0)
+    live = rng.integers(0, 129, size=pages).astype(np.uint8)
+    live[::5] = 0
+    mask = torch.from_numpy(live).cuda()
+    cams = scenes.orbit_cameras(6, 256, 192, seed=4)
+    ref = _render_all(model, cams, 256, 192, 1, page_mask=mask)
+    got = _render_all(model, cams, 256, 192, 6, page_mask=mask)
+    for f in FIELDS:
+        assert torch.equal(ref[f], got[f]), f
+    rows = np.arange(model.count)
+    dead = rows % 128 >= live[rows // 128]
+    assert not got["kept"].numpy()[:, dead].any()
+
+
+def test_grouped_view_matches_oracle():
+    g = scenes.synthetic_gaussians(10_000, seed=0)
+    model = GaussianModel.from_host(g)
+    cams = scenes.orbit_cameras(4, 256, 256, seed=0)
+    got = _render_all(model, cams, 256, 256, 4)
+    for v in (0, 3):
+        o = oracle.render(g, cams[v], 16, sh_eval_degree=3)
+        kept = got["kept"][v].numpy().astype(bool)
+        assert np.array_equal(got["touched"][v].numpy()[kept], o["touched"])
+        err = float(np.abs(got["rgb"][v].double().numpy() - o["image"]).max())
+        assert err <= 1e-4, err
