@@ -207,21 +207,22 @@ __device__ __forceinline__ uint32_t process_one(const PreprocessArgs& a, int64_t
 // One atomic per counter per CTA: per-warp atomics on these five addresses
 // serialised in L2 and doubled the kernel's time.  `slot` = the view within a
 // multi-view block (its own shared partials, so views need no extra barrier).
+// Warp sums and extrema are single REDUX instructions on 32-bit values: the
+// per-warp instance count fits (< 32 * 2^24 tiles), and the depth range is
+// kept at the resolution of the fp64 bits' high word, widened outward (min
+// with low word 0, max with low word ~0).  K2 only needs a range that covers
+// every visible depth: its keys stay monotone and the exact fp64 order is
+// restored inside equal-key runs (k_depth_fixup).
 __device__ __forceinline__ void count_kept(const PreprocessArgs& a, bool keep, uint32_t cnt,
                                            uint64_t zbits, int slot = 0) {
-  __shared__ unsigned long long s_acc_all[kMaxPreViews][kPreThreads / 32][5];
+  __shared__ uint32_t s_acc_all[kMaxPreViews][kPreThreads / 32][5];
   auto& s_acc = s_acc_all[slot];
   const unsigned ballot = __ballot_sync(0xffffffffu, keep);
   const unsigned vis = __ballot_sync(0xffffffffu, cnt > 0);
-  unsigned long long k = cnt;
-  unsigned long long zlo = ~0ull, zhi = 0ull;
-  if (cnt) zlo = zhi = zbits;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    k += __shfl_xor_sync(0xffffffffu, k, o);
-    zlo = min(zlo, __shfl_xor_sync(0xffffffffu, zlo, o));
-    zhi = max(zhi, __shfl_xor_sync(0xffffffffu, zhi, o));
-  }
+  const uint32_t zh = (uint32_t)(zbits >> 32);
+  const uint32_t k = __reduce_add_sync(0xffffffffu, cnt);
+  const uint32_t zlo = __reduce_min_sync(0xffffffffu, cnt ? zh : 0xffffffffu);
+  const uint32_t zhi = __reduce_max_sync(0xffffffffu, cnt ? zh : 0u);
   const int warp = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0) {
     s_acc[warp][0] = __popc(ballot);
@@ -232,7 +233,8 @@ __device__ __forceinline__ void count_kept(const PreprocessArgs& a, bool keep, u
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned long long kept = 0, nv = 0, inst = 0, lo = ~0ull, hi = 0ull;
+    unsigned long long kept = 0, nv = 0, inst = 0;
+    uint32_t lo = 0xffffffffu, hi = 0u;
     for (int w = 0; w < kPreThreads / 32; ++w) {
       kept += s_acc[w][0];
       nv += s_acc[w][1];
@@ -243,8 +245,8 @@ __device__ __forceinline__ void count_kept(const PreprocessArgs& a, bool keep, u
     if (kept) atomicAdd(a.n_kept, kept);
     if (nv) {
       atomicAdd(a.n_vis, nv);
-      atomicMin(a.zrange, lo);
-      atomicMax(a.zrange + 1, hi);
+      atomicMin(a.zrange, (unsigned long long)lo << 32);
+      atomicMax(a.zrange + 1, ((unsigned long long)hi << 32) | 0xffffffffull);
     }
     if (inst) atomicAdd(a.n_inst, inst);
   }
