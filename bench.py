@@ -42,12 +42,12 @@ W, H = 1920, 1080
 # dram__bytes_read.sum + dram__bytes_write.sum per launch of each stage's kernels
 # on a c3 view, from the committed full ncu captures (profiles/r02/*_summary.txt;
 # stage = sum of its kernels).  Reported as `traffic` beside the algorithmic bytes.
-NCU_TRAFFIC_R03 = {  # profiles/r03/ncu_launch_table.txt: DRAM MB per launch, c3 view
-    "preprocess": 2070.1e6,
-    "depth_sort": 48.1e6 + 3 * 43.1e6 + 106.2e6,
-    "emit": 260.8e6,
-    "tile_sort": 2 * 294.6e6,
-    "blend": 171.6e6 + 108.5e6,  # k_blend16w + k_touched_fix (K7b)
+NCU_TRAFFIC = {  # profiles/r05/ncu_launch_table.txt: DRAM bytes per c3 view
+    "preprocess": 2736.1e6 / 2,  # one k_preprocess_tma<2> launch serves two views
+    "depth_sort": 48.1e6 + 3 * 43.1e6 + 106.7e6,
+    "emit": 260.3e6,
+    "tile_sort": 2 * 294.8e6,
+    "blend": 171.8e6 + 114.0e6,  # k_blend16w + k_touched_fix (K7b)
 }
 
 
@@ -256,9 +256,9 @@ def run_ours(args, rank, world, local):
         achieved = alg[dom] / (dom_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                 "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": NCU_TRAFFIC_R03.get(dom),
-                "traffic_source": "profiles/r03 ncu launch list (dram bytes per launch, c3 view)",
-                "stage_traffic": NCU_TRAFFIC_R03,
+                "traffic": NCU_TRAFFIC.get(dom),
+                "traffic_source": "profiles/r05 ncu launch list (dram bytes per c3 view)",
+                "stage_traffic": NCU_TRAFFIC,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"
                 if "hbm_gbs" in pk else "fallback 6650 GB/s (B200_PROFILING.md)",
                 "stage_ms_per_frame": {k: v / frames for k, v in st.items()},

@@ -61,12 +61,13 @@ def batch_config(name: str, n: int, w: int, h: int, views: int, steps: int) -> d
     gen_s = time.perf_counter() - t0
     model = GaussianModel.from_host(g, validate=False)
     cams = scenes.orbit_cameras(views, w, h, seed=0)
-    r = BatchRenderer(model, w, h, views, tile_size=16, sh_eval_degree=3, n_streams=3)
+    r = BatchRenderer(model, w, h, views, tile_size=16, sh_eval_degree=3, n_streams=3, group=2)
     ms = _events_ms(lambda: r.render(cams), steps, 2)
     st = r.render(cams, stage_times=True)
     torch.cuda.synchronize()
     per = {k: v / views for k, v in st["stage_ms"].items()}
     return {"config": name, "gaussians": n, "width": w, "height": h, "views": views,
+            "views_per_k1_launch": 2,
             "frames_per_s": views / (ms / 1e3), "ms_per_frame": ms / views,
             "stage_ms_per_frame": per, "instances_per_frame": st["per_frame"]["instances"],
             "processed_per_frame": st["per_frame"]["processed"],
