@@ -626,8 +626,8 @@ int lmgs_render_group(lmgs_context* const* ctxs, int32_t n_views, const lmgs_gau
                       const lmgs_camera* cams, const lmgs_settings* s, const lmgs_frame* out,
                       void* const* streams) {
   if (!ctxs || n_views < 1 || n_views > LMGS_MAX_GROUP || !cams || !out || !streams)
-    return ctxs && n_views >= 1 && ctxs[0] ? fail(ctxs[0], LMGS_ERR_INVALID, "bad view group")
-                                           : LMGS_ERR_INVALID;
+    return ctxs && ctxs[0] ? fail(ctxs[0], LMGS_ERR_INVALID, "bad view group (1..8 views)")
+                           : LMGS_ERR_INVALID;
   for (int v = 0; v < n_views; ++v) {
     lmgs_context* c = ctxs[v];
     if (!c) return LMGS_ERR_INVALID;

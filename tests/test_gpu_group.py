@@ -81,3 +81,30 @@ def test_grouped_view_matches_oracle():
         assert np.array_equal(got["touched"][v].numpy()[kept], o["touched"])
         err = float(np.abs(got["rgb"][v].double().numpy() - o["image"]).max())
         assert err <= 1e-4, err
+
+
+def test_group_argument_errors(scene):
+    """lmgs_render_group rejects empty / oversized groups and repeated contexts
+    (each view needs its own arena) with the reference's InvalidInputError."""
+    import ctypes
+
+    from paper_2503_21364_b200 import _lib
+    from paper_2503_21364_b200.errors import InvalidInputError
+    from paper_2503_21364_b200.raster import abi_camera, abi_settings
+
+    _, model = scene
+    L = _lib.lib()
+    cams = scenes.orbit_cameras(2, 64, 48, seed=0)
+    r = BatchRenderer(model, 64, 48, 2, group=2)
+    g = model._abi()
+    st = abi_settings(16, 3, (0.0, 0.0, 0.0), 0)
+    frames = (_lib.Frame * 2)(r._frame(0), r._frame(1))
+    cam_arr = (_lib.Camera * 2)(*[abi_camera(c) for c in cams])
+    s = torch.cuda.current_stream().cuda_stream
+    sptrs = (ctypes.c_void_p * 2)(s, s)
+    c0 = r.ctxs[0].handle
+    for handles, n in (((c0, c0), 2), ((c0, r.ctxs[1].handle), 0), ((c0, r.ctxs[1].handle), 9)):
+        arr = (ctypes.c_void_p * 2)(*handles)
+        with pytest.raises(InvalidInputError):
+            _lib.check(c0, L.lmgs_render_group(arr, n, ctypes.byref(g), cam_arr, ctypes.byref(st),
+                                               frames, sptrs), "lmgs_render_group")
