@@ -108,3 +108,43 @@ def test_group_argument_errors(scene):
         with pytest.raises(InvalidInputError):
             _lib.check(c0, L.lmgs_render_group(arr, n, ctypes.byref(g), cam_arr, ctypes.byref(st),
                                                frames, sptrs), "lmgs_render_group")
+
+
+def test_group_mixed_image_sizes(scene):
+    """Views of one group may differ in image size: each keeps its own
+    tile grid (K1 takes every view's camera), outputs equal render()'s."""
+    import ctypes
+
+    from paper_2503_21364_b200 import _lib, render
+    from paper_2503_21364_b200.raster import _ptr, abi_camera, abi_settings
+
+    _, model = scene
+    L = _lib.lib()
+    specs = [(320, 200), (97, 131), (640, 360)]
+    cams = [scenes.orbit_cameras(3, w, h, seed=9)[i] for i, (w, h) in enumerate(specs)]
+    ctxs = [_lib.Context(0) for _ in specs]
+    outs, frames = [], []
+    for w, h in specs:
+        o = {"rgb": torch.empty((h, w, 3), device="cuda"), "alpha": torch.empty((h, w), device="cuda"),
+             "touched": torch.empty(model.count, dtype=torch.int32, device="cuda"),
+             "kept": torch.empty(model.count, dtype=torch.uint8, device="cuda"),
+             "ranges": torch.empty((-(-w // 16) * -(-h // 16), 2), dtype=torch.int32, device="cuda")}
+        outs.append(o)
+        frames.append(_lib.Frame(_ptr(o["rgb"]), _ptr(o["alpha"]), None, None, _ptr(o["touched"]),
+                                 _ptr(o["kept"]), _ptr(o["ranges"]), None))
+    n = len(specs)
+    s = torch.cuda.current_stream().cuda_stream
+    _lib.check(ctxs[0].handle, L.lmgs_render_group(
+        (ctypes.c_void_p * n)(*[c.handle for c in ctxs]), n, ctypes.byref(model._abi()),
+        (_lib.Camera * n)(*[abi_camera(c) for c in cams]),
+        ctypes.byref(abi_settings(16, 3, (0.1, 0.2, 0.3), 0)), (_lib.Frame * n)(*frames),
+        (ctypes.c_void_p * n)(*([s] * n))), "lmgs_render_group")
+    torch.cuda.synchronize()
+    for cam, o in zip(cams, outs):
+        ref = render(cam, model, 16, (0.1, 0.2, 0.3))
+        torch.cuda.synchronize()
+        assert torch.equal(o["rgb"], ref.rgb)
+        assert torch.equal(o["alpha"], ref.alpha)
+        assert torch.equal(o["touched"], ref.touched)
+        assert torch.equal(o["kept"], ref.kept)
+        assert torch.equal(o["ranges"], ref.tile_ranges)
