@@ -132,7 +132,19 @@ __global__ void k_depth_fixup(void* const* keys_slot, void* const* ids_slot, int
     const int64_t i = i0 - 1 + u;
     if (i >= n || k[u] == kDepthKeyNone) break;  // invisible tail
     if (k[u - 1] == k[u] || k[u + 1] != k[u]) continue;  // not the head of a run
+    // keys[i + 2] is often already in registers; most runs have length 2
     int64_t len = 2;
+    if (u + 2 <= kFixupPer + 1 && k[u + 2] != k[u]) {
+      uint32_t* run = static_cast<uint32_t*>(*ids_slot) + i;
+      const uint32_t a0 = run[0], a1 = run[1];  // independent loads
+      const uint64_t d0 = key64[a0], d1 = key64[a1];
+      const int64_t p0 = pid ? pid[a0] : (int64_t)a0, p1 = pid ? pid[a1] : (int64_t)a1;
+      if (less64(d1, p1, d0, p0)) {
+        run[0] = a1;
+        run[1] = a0;
+      }
+      continue;
+    }
     while (i + len < n && keys[i + len] == k[u]) ++len;
     fix_run(static_cast<uint32_t*>(*ids_slot) + i, (int)len, key64, pid);
   }

@@ -1,0 +1,11 @@
+#!/bin/bash
+# depth fix-up: length-2 runs ordered with two independent gathers
+out=gpurun_out/r11; mkdir -p $out
+timeout 900 python -m pytest tests -q -m gpu -x > $out/pytest_gpu.log 2>&1
+timeout 300 python bench_tools/stress_parity.py 19 150 > $out/stress.log 2>&1
+for rep in 1 2; do
+  timeout 300 python bench.py --steps 5 --warmup 3 --e2e-steps 1 --no-cpu-baseline > $out/b.log 2>&1
+  tail -1 $out/b.log | python -c "import json,sys; d=json.load(sys.stdin); print('fix2', round(d['value'],1), {k: round(v,4) for k,v in d['roofline']['stage_ms_per_frame'].items()})" >> $out/summary.txt
+done
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    --log-file $out/launches.csv python profiles/view_probe.py 1 > /dev/null 2>&1
