@@ -114,7 +114,10 @@ __device__ void fix_run(uint32_t* ids, int len, const uint64_t* __restrict__ key
 
 // one thread per 4 consecutive keys: runs start where a key differs from
 // its predecessor and continues into its successor
-constexpr int kFixupPer = 4;
+#ifndef LMGS_FIXUP_PER
+#define LMGS_FIXUP_PER 4
+#endif
+constexpr int kFixupPer = LMGS_FIXUP_PER;
 __global__ void k_depth_fixup(void* const* keys_slot, void* const* ids_slot, int64_t n,
                               const uint64_t* __restrict__ key64,
                               const int64_t* __restrict__ pid) {
