@@ -41,6 +41,12 @@ __device__ __forceinline__ void unpack_rect(uint64_t rect, int& x0, int& y0, int
 // range the runs it leaves are short (c3: 39% of splats in runs, longest 7),
 // and the fix-up sorts them.  Invisible splats get kDepthKeyNone.
 
+#ifndef LMGS_DEPTH_KEYS_U
+#define LMGS_DEPTH_KEYS_U 4
+#endif
+#ifndef LMGS_DEPTH_KEYS_CTAS_PER_SM
+#define LMGS_DEPTH_KEYS_CTAS_PER_SM 8
+#endif
 __global__ void __launch_bounds__(256) k_depth_keys(const uint64_t* __restrict__ key64,
                                                     const unsigned long long* zrange, int64_t n,
                                                     uint32_t* __restrict__ key32,
@@ -53,8 +59,8 @@ __global__ void __launch_bounds__(256) k_depth_keys(const uint64_t* __restrict__
   const double span = zmax - zmin;
   const double top = (double)(kDepthKeyNone - 1);
   const double scale = span > 0.0 ? top / span : 0.0;
-  // 4 keys per thread per step (independent loads in flight)
-  constexpr int U = 4;
+  // LMGS_DEPTH_KEYS_U keys per thread per step (independent loads in flight)
+  constexpr int U = LMGS_DEPTH_KEYS_U;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
   for (int64_t i0 = ((int64_t)blockIdx.x * blockDim.x) * U + threadIdx.x; i0 < n; i0 += stride) {
     uint64_t kb[U];
@@ -405,7 +411,8 @@ inline unsigned grid_for(int64_t n, int threads, int64_t cap = 148 * 16) {
 int launch_depth_keys(const uint64_t* key64, const unsigned long long* zrange, int64_t n,
                       uint32_t* key32, uint32_t* hist, cudaStream_t s) {
   if (n <= 0) return 0;
-  k_depth_keys<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(key64, zrange, n, key32, hist);
+  k_depth_keys<<<grid_for(n, 256, 148 * LMGS_DEPTH_KEYS_CTAS_PER_SM), 256, 0, s>>>(key64, zrange, n,
+                                                                                 key32, hist);
   return 1;
 }
 
