@@ -257,7 +257,7 @@ int bits_for(int64_t v) {  // bits needed to represent values in [0, v)
 }
 
 PreprocessArgs make_pre(lmgs_context* c, const lmgs_gaussians* g, const CamArgs& ca,
-                        const lmgs_settings* st, uint8_t* kept) {
+                        const lmgs_settings* st, uint8_t* kept, int32_t* touched = nullptr) {
   PreprocessArgs pa{};
   pa.means = g->means;
   pa.quats = g->quats;
@@ -274,6 +274,7 @@ PreprocessArgs make_pre(lmgs_context* c, const lmgs_gaussians* g, const CamArgs&
   pa.rects = c->rects;
   pa.recs = c->recs;
   pa.kept = kept;
+  pa.touched_zero = touched;
   pa.n_kept = &c->d_scal->counts[0];
   pa.n_vis = &c->d_scal->counts[1];
   pa.n_inst = &c->d_scal->counts[2];
@@ -337,7 +338,7 @@ int view_prepare(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* ca
   LMGS_CUDA(c, cudaMemsetAsync(sc->counts, 0, sizeof(sc->counts), s));
   LMGS_CUDA(c, cudaMemsetAsync(&sc->zrange[0], 0xff, sizeof(sc->zrange[0]), s));
   LMGS_CUDA(c, cudaMemsetAsync(&sc->zrange[1], 0, sizeof(sc->zrange[1]), s));
-  if (out->touched && n > 0) LMGS_CUDA(c, cudaMemsetAsync(out->touched, 0, sizeof(int32_t) * n, s));
+  // out->touched is zeroed by K1 (make_pre: touched_zero), one pass fewer
   return LMGS_OK;
 }
 
@@ -353,7 +354,7 @@ int render_one(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
   StageTimer tm{c, s, vp.timed};
   // K1
   tm.begin(0);
-  vp.launched += launch_preprocess(make_pre(c, g, vp.ca, st, out->kept), s);
+  vp.launched += launch_preprocess(make_pre(c, g, vp.ca, st, out->kept, out->touched), s);
   tm.end(0);
   return view_finish(c, g, cam, st, out, s, &vp, strips);
 }
@@ -647,7 +648,7 @@ int lmgs_render_group(lmgs_context* const* ctxs, int32_t n_views, const lmgs_gau
     lmgs_context* c = ctxs[v];
     cudaStream_t sv = static_cast<cudaStream_t>(streams[v]);
     if (int r = view_prepare(c, g, cams + v, s, out + v, sv, vp + v)) return r;
-    m.v[v] = make_pre(c, g, vp[v].ca, s, out[v].kept);
+    m.v[v] = make_pre(c, g, vp[v].ca, s, out[v].kept, out[v].touched);
     if (sv != s0) {  // K1 (on streams[0]) follows each view's resets
       LMGS_CUDA(c, cudaEventRecord(c->ev_in, sv));
       LMGS_CUDA(c, cudaStreamWaitEvent(s0, c->ev_in, 0));

@@ -69,6 +69,7 @@ struct PreprocessArgs {
   uint64_t* rects;         // [n] inclusive tile rect (visible splats; count = its area)
   BlendRec* recs;          // [n]
   uint8_t* kept;           // [n] nullable
+  int32_t* touched_zero;   // [n] nullable: zeroed here (the blend then adds to it)
   unsigned long long* n_kept;  // scalar (atomic): z > near
   unsigned long long* n_vis;   // scalar (atomic): tiles touched > 0
   unsigned long long* n_inst;  // scalar (atomic): sum of tile counts = K

@@ -133,6 +133,7 @@ __device__ __forceinline__ uint32_t process_one(const PreprocessArgs& a, int64_t
     const double z = mkl_dot3(m0, cam.r[6], m1, cam.r[7], m2, cam.r[8]) + cam.t[2];
     keep = z > kNearCullZ;  // 196
     if (a.kept) a.kept[i] = keep;
+    if (a.touched_zero) a.touched_zero[i] = 0;
     if (!keep) {
       a.depth_keys[i] = kCulledKey;
       a.rects[i] = 0;
@@ -255,6 +256,7 @@ __device__ __forceinline__ void count_kept(const PreprocessArgs& a, bool keep, u
 // a row of an inactive page (paged sets): culled
 __device__ __forceinline__ void cull_row(const PreprocessArgs& a, int64_t i) {
   if (a.kept) a.kept[i] = 0;
+  if (a.touched_zero) a.touched_zero[i] = 0;
   a.depth_keys[i] = kCulledKey;
   a.rects[i] = 0;
 }
