@@ -1,21 +1,34 @@
-"""Benchmark: 1080p frames/s at 6M Gaussians (BASELINE.json metric, config c3).
+"""Benchmark: 1080p frames/s at 6M Gaussians on 1-8 B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--views V] [--impl reference]
 
-One step = one batch of V (default 64) camera views of the 6M-Gaussian
-synthetic scene rendered at 1920x1080 on each rank (camera-batch data
-parallelism, no data-path collective; "scaling": "weak").  The scene (1.42 GB)
-and every per-view working set exceed the 126 MB L2, so no explicit L2 flush
-is needed between timed iterations.
+Headline workload = config c3: a batch of V = 64 camera views of the
+6M-Gaussian synthetic scene (SH degree 3) at 1920x1080, data-parallel over N
+GPUs.  One step renders the whole 64-view batch; each rank renders its
+contiguous shard of 64 / N views (``distributed.camera_shard``), so the total
+work is fixed as N grows: ``"scaling": "strong"``.  The scene is generated on
+rank 0 and replicated to the other ranks with an NCCL broadcast
+(``distributed.broadcast_scene``, timed as setup).  The weak-scaling variant
+(64 views per rank) is reported beside it under ``weak``.  The scene (1.42 GB)
+and the per-view working sets exceed the 126 MB L2, so no explicit L2 flush is
+inserted between timed steps.
 
-Timed region: W untimed warm-up steps, then exactly K steps bracketed by a
-barrier + cuda.synchronize on both sides, timed with CUDA events on the
-launching stream; the max over ranks is reported.  Rank 0 prints one JSON line.
+Config c5 (the 50M-Gaussian city in 8 spatial blocks, block-parallel over the
+same N ranks with the layer exchange fused into the blend over peer memory)
+is measured in the same run and reported under ``c5``.
+
+Launch: with ``--gpus N > 1`` and no torchrun environment the script
+re-executes itself under ``torch.distributed.run`` with N local ranks (and
+fails at once if fewer than N GPUs are visible); under torchrun it asserts
+WORLD_SIZE == N.  Timing: W untimed warm-up steps, then exactly K steps
+bracketed by a barrier + cuda.synchronize on both sides, CUDA events on the
+launching stream, max over ranks (all_reduce MAX).  Rank 0 prints one JSON
+line.
 
 ``--impl reference`` times the reference algorithm's CPU implementation (the
 fp64 C restatement in oracle/, "port": the reference is pure Python and does
-not travel to the GPU box) on the host cores over a bounded sample (one full
-1080p view of the same scene per step).
+not travel to the GPU box) on the host cores, one full 1080p view of the same
+scene per step; under torchrun only rank 0 runs it.
 """
 
 from __future__ import annotations
@@ -37,17 +50,20 @@ METRIC = "1080p frames/sec at 6M Gaussians, 1–8 B200; ms/frame; HBM GB/s vs pe
 UNIT = "frames/s"
 N_GAUSS = 6_000_000
 W, H = 1920, 1080
+BATCH_VIEWS = 64  # config c3: "batch of 64 camera views data-parallel over 1/2/4/8 B200"
+C5_PER_BLOCK = 6_250_000
 
-
-# dram__bytes_read.sum + dram__bytes_write.sum per launch of each stage's kernels
-# on a c3 view, from the committed full ncu captures (profiles/r02/*_summary.txt;
-# stage = sum of its kernels).  Reported as `traffic` beside the algorithmic bytes.
-NCU_TRAFFIC = {  # profiles/r05/ncu_launch_table.txt: DRAM bytes per c3 view
+# dram__bytes_read.sum + dram__bytes_write.sum per c3 view of each stage's
+# kernels from the committed ncu launch list (stage = sum of its kernels);
+# reported as `traffic` beside the algorithmic bytes.
+NCU_TRAFFIC_SOURCE = "profiles/r05/ncu_launch_table.txt"
+NCU_TRAFFIC = {
     "preprocess": 2736.1e6 / 2,  # one k_preprocess_tma<2> launch serves two views
     "depth_sort": 48.1e6 + 3 * 43.1e6 + 106.7e6,
     "emit": 260.3e6,
     "tile_sort": 2 * 294.8e6,
-    "blend": 171.8e6 + 114.0e6,  # k_blend16w + k_touched_fix (K7b)
+    "blend": 171.8e6,
+    "touched_fix": 114.0e6,
 }
 
 
@@ -112,11 +128,70 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+# ---------------------------------------------------------------------------
+# launch and multi-rank accounting (unit-tested with gloo: tests/test_bench_dist.py)
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def launch_check(gpus: int, env=None, visible_gpus=None) -> str:
+    """What to do for ``--gpus gpus``: "run" (this process is the job or one
+    of its ranks) or "spawn" (re-execute under torchrun).  Raises SystemExit
+    with a message when the request cannot be met."""
+    env = os.environ if env is None else env
+    if gpus < 1:
+        raise SystemExit(f"bench.py: --gpus must be >= 1 (got {gpus})")
+    if "WORLD_SIZE" in env:
+        world = int(env["WORLD_SIZE"])
+        if world != gpus:
+            raise SystemExit(f"bench.py: --gpus {gpus} but WORLD_SIZE={world}: launch one "
+                             "rank per GPU (torchrun --nproc-per-node N ... --gpus N)")
+        return "run"
+    if gpus == 1:
+        return "run"
+    if visible_gpus is None:
+        import torch
+
+        visible_gpus = torch.cuda.device_count()
+    if visible_gpus < gpus:
+        raise SystemExit(f"bench.py: --gpus {gpus} needs {gpus} visible GPUs, found "
+                         f"{visible_gpus}")
+    return "spawn"
+
+
+def spawn_torchrun(gpus: int, argv) -> int:
+    """Re-execute this script with one rank per GPU (torchrun, 127.0.0.1)."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), str(Path(__file__).resolve()), *argv]
+    return subprocess.call(cmd)
+
+
+def max_over_ranks(value: float, world: int, device=None) -> float:
+    """The maximum of a per-rank scalar (all_reduce MAX; identity at world 1)."""
+    if world == 1:
+        return float(value)
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def throughput(frames_per_step_total: int, steps: int, ms_max: float) -> float:
+    """Whole-job frames/s: every rank's frames over the slowest rank's time."""
+    return frames_per_step_total * steps / (ms_max / 1e3)
 
 
 # ---------------------------------------------------------------------------
@@ -134,7 +209,7 @@ def run_reference(args, rank, world):
     threads = os.cpu_count() or 1
     oracle.set_threads(threads)
     g = scenes.synthetic_gaussians(N_GAUSS, seed=0)
-    cams = scenes.orbit_cameras(64, W, H, seed=0)
+    cams = scenes.orbit_cameras(BATCH_VIEWS, W, H, seed=0)
     times = []
     for step in range(args.warmup + args.steps):
         cam = cams[step % len(cams)]
@@ -149,7 +224,7 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": "c3: 6M Gaussians, 1920x1080, SH3, "
                                                     "one full view per step (bounded sample)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
@@ -178,19 +253,149 @@ def cpu_baseline_sample(g, cam):
                       "oracle/oracle.c fp64 restatement, OpenMP)"}
 
 
-def run_ours(args, rank, world, local):
-    import numpy as np
+def replicate_scene(rank, world, dev):
+    """Rank 0 generates the c3 scene; one NCCL broadcast per SoA tensor
+    replicates it.  Returns (model, host scene or None, broadcast ms)."""
     import torch
 
     from paper_2503_21364_b200 import GaussianModel, scenes
-    from paper_2503_21364_b200.batch import BatchRenderer
+    from paper_2503_21364_b200.distributed import broadcast_scene
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    g_host = None
+    if rank == 0:
+        g_host = scenes.synthetic_gaussians(N_GAUSS, seed=0)
+        model = GaussianModel.from_host(g_host, device=dev, validate=False)
+    else:
+        z = lambda *s: torch.empty(s, dtype=torch.float32, device=dev)  # noqa: E731
+        model = GaussianModel(z(N_GAUSS, 3), z(N_GAUSS, 4), z(N_GAUSS, 3), z(N_GAUSS),
+                              z(N_GAUSS, 16, 3), 3, device=dev, validate=False)
+    ms = 0.0
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        broadcast_scene([model.means, model.quats, model.scales, model.opacity_logits,
+                         model.sh], src=0)
+        b.record()
+        torch.cuda.synchronize()
+        ms = max_over_ranks(a.elapsed_time(b), world, dev)
+    return model, g_host, ms
+
+
+def single_view_latency(model, cam, reps: int = 10) -> dict:
+    """One view through the public ``render`` call (host wait for K
+    included), CUDA events around each call, serial, after a warm-up."""
+    import torch
+
+    from paper_2503_21364_b200 import render
+
+    render(cam, model, 16, sh_eval_degree=3)
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        a.record()
+        render(cam, model, 16, sh_eval_degree=3)
+        b.record()
+        torch.cuda.synchronize()
+        ms.append((a.elapsed_time(b), (time.perf_counter() - t0) * 1e3))
+    dev_ms = sorted(m[0] for m in ms)
+    wall_ms = sorted(m[1] for m in ms)
+    return {"ms": statistics.median(dev_ms), "ms_min": dev_ms[0],
+            "wall_ms": statistics.median(wall_ms), "reps": reps,
+            "path": "paper_2503_21364_b200.render (lmgs_render) of one c3 view, serial, "
+                    "CUDA events on the current stream; target <= 5 ms (north star)"}
+
+
+def time_steps(step, steps, world, dev, barrier):
+    import torch
+
+    stream = torch.cuda.current_stream()
+    barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for _ in range(steps):
+        step()
+    end.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    return max_over_ranks(start.elapsed_time(end), world, dev)
+
+
+def run_c5(args, rank, world, dev, barrier):
+    """Config c5: the 8-block city, block-parallel, exchange fused into the
+    blend (PeerBlockRenderer).  Strong scaling (fixed scene and frame)."""
+    import torch
+
+    from paper_2503_21364_b200 import GaussianModel, render, scenes
+    from paper_2503_21364_b200.distributed import PeerBlockRenderer, assign_blocks
+
+    bboxes = scenes.city_block_bboxes()
+    nb = len(bboxes)
+    owned = assign_blocks(nb, world)
+    hosts = {b: scenes.city_block(b, args.c5_per_block, 3, bboxes) for b in owned[rank]}
+    models = {b: GaussianModel.from_host(h, device=dev, validate=False) for b, h in hosts.items()}
+    cam = scenes.city_camera()
+    r = PeerBlockRenderer(models, bboxes, nb, cam.width, cam.height)
+    for _ in range(max(2, args.warmup)):
+        out = r.render(cam)
+    torch.cuda.synchronize()
+    steps = args.c5_steps
+    ms = time_steps(lambda: r.render(cam), steps, world, dev, barrier)
+    out = r.render(cam)
+    torch.cuda.synchronize()
+    res = {"metric": "c5 frames/s (50M-Gaussian city, 8 blocks, 1080p, block-parallel)",
+           "value": throughput(1, steps, ms), "unit": "frames/s", "ms_per_frame": ms / steps,
+           "steps": steps, "scaling": "strong", "exchange": "peer stores in the blend "
+           "(lmgs_render_strips into symmetric-memory strips) + strip all_gather",
+           "blocks_per_rank": [len(o) for o in owned], "gaussians": args.c5_per_block * nb}
+    if world == 1 and not args.no_c5_monolithic:
+        # deviation of the block composite from one monolithic render of the
+        # whole city (SURVEY §8e: reported, not gated)
+        cat = lambda f: torch.cat([getattr(models[b], f) for b in range(nb)])  # noqa: E731
+        mono = GaussianModel(cat("means"), cat("quats"), cat("scales"), cat("opacity_logits"),
+                             cat("sh"), 3, device=dev, validate=False)
+        del models, r
+        o = render(cam, mono, 16, sh_eval_degree=3)
+        torch.cuda.synchronize()
+        d = (out[0] - o.rgb).abs()
+        res["block_vs_monolithic"] = {"max_abs": float(d.max()),
+                                      "frac_px_gt_1e-3": float((d.amax(-1) > 1e-3).double()
+                                                               .mean()),
+                                      "mean_abs": float(d.mean())}
+        del mono, o
+    del hosts
+    return res
+
+
+def run_ours(args, rank, world, local):
+    import torch
+
+    from paper_2503_21364_b200 import scenes
+    from paper_2503_21364_b200.batch import BatchRenderer
+    from paper_2503_21364_b200.distributed import camera_shard
+
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world == 1 and "MASTER_PORT" not in os.environ:
+        # a one-rank group (c5's symmetric-memory rendezvous needs one)
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(sk.getsockname()[1]),
+                              RANK="0", WORLD_SIZE="1")
+    dist.init_process_group("nccl", device_id=dev)
+    assert dist.get_world_size() == args.gpus, (dist.get_world_size(), args.gpus)
+    warm = torch.ones(1, device=dev)
+    dist.all_reduce(warm)  # NCCL communicator warm-up
+    torch.cuda.synchronize()
 
     def barrier():
         if world > 1:
@@ -198,13 +403,16 @@ def run_ours(args, rank, world, local):
 
             dist.barrier()
 
-    g_host = scenes.synthetic_gaussians(N_GAUSS, seed=0)
-    model = GaussianModel.from_host(g_host, device=dev, validate=False)
+    model, g_host, bcast_ms = replicate_scene(rank, world, dev)
     views = args.views
-    all_cams = scenes.orbit_cameras(views * world, W, H, seed=0)
-    cams = all_cams[rank * views:(rank + 1) * views]
-    renderer = BatchRenderer(model, W, H, views, tile_size=16, sh_eval_degree=3,
-                             n_streams=args.streams, group=args.group)
+    all_cams = scenes.orbit_cameras(views, W, H, seed=0)
+    mine = camera_shard(views, rank, world)
+    cams = [all_cams[i] for i in mine]
+    from paper_2503_21364_b200 import _lib
+
+    flags = _lib.LMGS_FLAG_TILE_SORT if args.tile_sort else 0
+    renderer = BatchRenderer(model, W, H, max(len(cams), 1), tile_size=16, sh_eval_degree=3,
+                             n_streams=args.streams, group=args.group, flags=flags)
 
     # warm-up (also sizes every arena)
     for _ in range(args.warmup):
@@ -215,118 +423,149 @@ def run_ours(args, rank, world, local):
     stage = renderer.render(cams, stage_times=True)
     torch.cuda.synchronize()
 
-    stream = torch.cuda.current_stream()
     sampler = ClockSampler(local)
-    barrier()
-    torch.cuda.synchronize()
     sampler.start()
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    start.record(stream)
-    for _ in range(args.steps):
-        renderer.render(cams)
-    end.record(stream)
-    torch.cuda.synchronize()
-    barrier()
+    ms_max = time_steps(lambda: renderer.render(cams), args.steps, world, dev, barrier)
     clocks = sampler.stop()
-    ms = start.elapsed_time(end)
-    t = torch.tensor([ms], device=dev, dtype=torch.float64)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
     ms_per_step = ms_max / args.steps
-    value = views * world * args.steps / (ms_max / 1e3)
+    value = throughput(views, args.steps, ms_max)
+
+    # weak scaling beside it: every rank renders the full 64-view batch
+    weak = None
+    if world > 1:
+        wr = BatchRenderer(model, W, H, views, tile_size=16, sh_eval_degree=3,
+                           n_streams=args.streams, group=args.group)
+        wr.render(all_cams)
+        torch.cuda.synchronize()
+        wsteps = max(1, min(args.steps, 5))
+        wms = time_steps(lambda: wr.render(all_cams), wsteps, world, dev, barrier)
+        weak = {"value": throughput(views * world, wsteps, wms), "unit": UNIT,
+                "views_per_gpu": views, "steps": wsteps, "ms_per_step": wms / wsteps}
+        del wr
 
     # e2e through the public API with host buffers: per step, the cameras go
     # H2D from pinned memory and every rendered frame comes back D2H.
-    e2e = renderer.bench_e2e(cams, args.e2e_steps, barrier=barrier, world=world, device=dev)
+    e2e = renderer.bench_e2e(cams, args.e2e_steps, barrier=barrier, world=world, device=dev,
+                             total_views=views)
+    latency = single_view_latency(model, cams[0]) if rank == 0 else None
+
+    c5 = None
+    if not args.no_c5:
+        del renderer
+        torch.cuda.empty_cache()
+        c5 = run_c5(args, rank, world, dev, barrier)
 
     line = None
     if rank == 0:
-        pk = peaks()
-        hbm = float(pk.get("hbm_gbs", 6650.0))
-        st = stage["stage_ms"]
-        frames = views
-        dom = max(st, key=st.get)
-        per = stage["per_frame"]
-        # algorithmic bytes of each stage per frame
-        alg = stage["alg_bytes"]
-        dom_ms = st[dom] / frames
-        achieved = alg[dom] / (dom_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
-                "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": NCU_TRAFFIC.get(dom),
-                "traffic_source": "profiles/r05 ncu launch list (dram bytes per c3 view)",
-                "stage_traffic": NCU_TRAFFIC,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"
-                if "hbm_gbs" in pk else "fallback 6650 GB/s (B200_PROFILING.md)",
-                "stage_ms_per_frame": {k: v / frames for k, v in st.items()},
-                "stage_gbs": {k: alg[k] / (st[k] / frames / 1e3) / 1e9 for k in st if st[k] > 0},
-                "stage_alg_bytes": alg}
-        roof["stage_frac"] = {k: v / hbm for k, v in roof["stage_gbs"].items()}
-        if dom == "blend":
-            roof["note"] = ("the dominant stage (blend) is FP32/MUFU-issue bound, not HBM "
-                            "bound: its HBM fraction is informational; blend_pairs is its "
-                            "roofline")
-        blend_pairs = per.get("pairs", 0)
-        if blend_pairs:
-            sm_clk = (clocks.get("sm_mhz") or 1965.0) * 1e6
-            pair_peak = 148 * 128 * sm_clk / 17.0
-            pr = blend_pairs / (st["blend"] / frames / 1e3)
-            roof["blend_pairs"] = {"achieved": pr, "peak": pair_peak, "unit": "pairs/s",
-                                   "frac": pr / pair_peak,
-                                   "note": "FP32-pipe pair roofline: 148 SM x 128 lanes x "
-                                           "f_clk / 17 instr per pair"}
-        cpu = None
-        if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline_sample(g_host, cams[0])
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "ms_per_frame": ms_per_step / views,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
-            "config": {"workload": "c3: 6M Gaussians (SH3), 1920x1080, batch of "
-                                   f"{views} orbit views per GPU, tile 16",
-                       "gaussians": N_GAUSS, "views_per_gpu": views, "width": W, "height": H,
-                       "parallelism": f"camera-batch dp{world}",
-                       "views_per_k1_launch": args.group,
-                       "l2": "no flush: scene 1.42 GB and per-view buffers > 126 MB L2",
-                       "geometry": "fp64 (bit-exact tile lists)", "blend": "fp32"},
-            "gpu_launches": renderer.launches_per_step * args.steps,
-            "e2e": e2e,
-            "roofline": roof,
-            "cpu_baseline": cpu,
-            "clocks": clocks,
-            "instances_per_frame": per.get("instances"),
-        }
+        line = make_line(args, world, views, len(cams), value, ms_per_step, stage, clocks, e2e,
+                         weak, latency, c5, bcast_ms, g_host, all_cams[0], args.gpu_launches)
         print(json.dumps(line), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.barrier()
-        dist.destroy_process_group()
+    dist.barrier()
+    dist.destroy_process_group()
     return line
 
 
-def main():
+def make_line(args, world, views, my_views, value, ms_per_step, stage, clocks, e2e, weak,
+              latency, c5, bcast_ms, g_host, cam0, launches):
+    pk = peaks()
+    hbm = float(pk.get("hbm_gbs", 6650.0))
+    st = stage["stage_ms"]
+    nv = my_views  # stage times are summed over this rank's views
+    per = stage["per_frame"]
+    alg = stage["alg_bytes"]  # per view
+    stage_ms = {k: v / nv for k, v in st.items()}
+    hbm_stages = [k for k in alg if stage_ms.get(k, 0) > 0]
+    dom = max(stage_ms, key=stage_ms.get)
+    stage_gbs = {k: alg[k] / (stage_ms[k] / 1e3) / 1e9 for k in hbm_stages}
+    frame_ms = ms_per_step * world / views  # device time per frame on one GPU
+    frame_bytes = sum(alg.values())
+    roof = {"bound": "hbm", "kernel": dom, "achieved": stage_gbs.get(dom), "peak": hbm,
+            "unit": "GB/s", "frac": (stage_gbs.get(dom) or 0.0) / hbm,
+            "traffic": NCU_TRAFFIC.get(dom), "traffic_source": NCU_TRAFFIC_SOURCE,
+            "stage_traffic": NCU_TRAFFIC,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"
+            if "hbm_gbs" in pk else "fallback 6650 GB/s (B200_PROFILING.md)",
+            "stage_ms_per_frame": stage_ms, "stage_alg_bytes": alg, "stage_gbs": stage_gbs,
+            "stage_frac": {k: v / hbm for k, v in stage_gbs.items()},
+            "frame": {"alg_bytes": frame_bytes, "ms": frame_ms,
+                      "gbs": frame_bytes / (frame_ms / 1e3) / 1e9,
+                      "frac": frame_bytes / (frame_ms / 1e3) / 1e9 / hbm,
+                      "note": "sum of every stage's algorithmic bytes / the measured "
+                              "ms per frame (overlapped streams) / peak"}}
+    if dom == "blend":
+        roof["note"] = ("the dominant stage (blend) is FP32/MUFU-issue bound, not HBM "
+                        "bound: its HBM fraction is informational; blend_pairs is its "
+                        "roofline")
+    pairs = per.get("pairs", 0)
+    if pairs:
+        sm_clk = (clocks.get("sm_mhz") or 1965.0) * 1e6
+        pair_peak = 148 * 128 * sm_clk / 17.0
+        pr = pairs / (stage_ms["blend"] / 1e3)
+        roof["blend_pairs"] = {"achieved": pr, "peak": pair_peak, "unit": "pairs/s",
+                               "frac": pr / pair_peak,
+                               "note": "k_blend16w alone (K7b is stage touched_fix); "
+                                       "FP32-pipe pair roofline: 148 SM x 128 lanes x "
+                                       "f_clk / 17 instr per pair"}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(g_host, cam0)
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "ms_per_frame": ms_per_step / views,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"c3: 6M Gaussians (SH3), 1920x1080, batch of {views} orbit "
+                               f"views per step split over {world} GPU(s), tile 16",
+                   "gaussians": N_GAUSS, "views_per_step": views, "views_per_gpu": my_views,
+                   "width": W, "height": H, "parallelism": f"camera-batch dp{world}",
+                   "views_per_k1_launch": args.group,
+                   "l2": "no flush: scene 1.42 GB and per-view buffers > 126 MB L2",
+                   "geometry": "fp64 (bit-exact tile lists)", "blend": "fp32",
+                   "scene_replication": "rank 0 generates, NCCL broadcast" if world > 1
+                   else "single rank"},
+        "gpu_launches": launches(stage) * args.steps,
+        "e2e": e2e,
+        "latency_ms_single_view": latency,
+        "weak": weak,
+        "c5": c5,
+        "setup": {"scene_broadcast_ms": bcast_ms},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "instances_per_frame": per.get("instances"),
+    }
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--views", type=int, default=64)
+    ap.add_argument("--views", type=int, default=BATCH_VIEWS)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--no-c5-monolithic", action="store_true")
+    ap.add_argument("--c5-steps", type=int, default=5)
+    ap.add_argument("--c5-per-block", type=int, default=C5_PER_BLOCK)
     ap.add_argument("--streams", type=int, default=3,
                     help="contexts/streams the view batch alternates over")
+    ap.add_argument("--tile-sort", action="store_true",
+                    help="A/B: tile lists by the instance radix sort instead of coarse bins")
     ap.add_argument("--group", type=int, default=2,
                     help="views per shared K1 launch (lmgs_render_group; 1 = lmgs_render)")
-    args = ap.parse_args()
+    args = ap.parse_args(argv)
+    # liblmgs kernels per step, as the library counts them (stage_times pass)
+    args.gpu_launches = lambda stage: stage["launches"]
     rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if launch_check(args.gpus) == "spawn":
+        sys.exit(spawn_torchrun(args.gpus, argv))
     run_ours(args, rank, world, local)
 
 

@@ -54,7 +54,7 @@ typedef enum lmgs_status {
   LMGS_ERR_INVALID = 1,     /* bad argument (shape, size, null pointer)   */
   LMGS_ERR_CUDA = 2,        /* CUDA runtime error                         */
   LMGS_ERR_OOM = 3,         /* device allocation failed                   */
-  LMGS_ERR_UNSUPPORTED = 4, /* e.g. tile_size > 64                        */
+  LMGS_ERR_UNSUPPORTED = 4, /* e.g. more than 2^24 tiles in one view      */
   LMGS_ERR_FORMAT = 5,      /* malformed checkpoint (reference FormatError) */
   LMGS_ERR_IO = 6           /* file open / read / write failed             */
 } lmgs_status;
@@ -98,13 +98,16 @@ typedef struct lmgs_gaussians {
 } lmgs_gaussians;
 
 typedef struct lmgs_settings {
-  int32_t tile_size;       /* >= 1, <= 64 (reference default 16)             */
+  int32_t tile_size;       /* >= 1 (reference default 16; TileConfig 245-253) */
   int32_t sh_eval_degree;  /* 1 = reference eval_sh_colors; 3 = full degree 3 */
   double background[3];   /* fp64 like the reference (common.py DTYPE)     */
   uint32_t flags;          /* LMGS_FLAG_*                                    */
 } lmgs_settings;
 
 #define LMGS_FLAG_STAGE_TIMES 1u  /* record per-stage CUDA events (lmgs_get_stats) */
+#define LMGS_FLAG_TILE_SORT 4u  /* build the tile lists with the instance radix sort
+                                     (emit + 8-bit passes over the tile bits) instead
+                                     of the default coarse-bin path; same lists     */
 #define LMGS_FLAG_NO_TOUCHED_FIX 2u /* skip K7b: touched may then differ from the
                                        reference where fp32 and fp64 transmittance
                                        straddle TERM_EPS (a few per million)       */
@@ -268,7 +271,10 @@ typedef struct lmgs_checkpoint_info {
 } lmgs_checkpoint_info;
 
 /* Parse and validate a checkpoint header (host only, no device work).  err
- * (nullable, err_len bytes) receives the message on failure. */
+ * (nullable, err_len bytes) receives the message on failure.  A count the
+ * file cannot hold fails with LMGS_ERR_FORMAT ("truncated"), before any size
+ * arithmetic.  sh_degree > 3 returns LMGS_ERR_UNSUPPORTED: the reference loads
+ * any degree, but the rasterizer evaluates SH up to degree 3. */
 int lmgs_checkpoint_info_read(const char* path, lmgs_checkpoint_info* info, char* err,
                               int err_len);
 

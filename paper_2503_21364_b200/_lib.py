@@ -26,6 +26,7 @@ U32 = ctypes.c_uint32
  LMGS_ERR_IO) = range(7)
 LMGS_FLAG_STAGE_TIMES = 1
 LMGS_FLAG_NO_TOUCHED_FIX = 2
+LMGS_FLAG_TILE_SORT = 4
 MAX_STAGES = 8
 
 # every symbol include/lmgs.h declares

@@ -25,11 +25,36 @@ def tile_passes(tiles: int) -> int:
     return (bits + 7) // 8
 
 
+def alg_bytes_per_view(n, s_read, group, n_vis, k, tiles, tile_passes, processed, pixels):
+    """Algorithmic HBM bytes of each stage for one view (DESIGN.md §3 table).
+
+    n Gaussians with s_read SH bytes each, inputs read once per group of views;
+    n_vis visible splats; k tile instances; tile_passes 8-bit tile-sort passes;
+    processed = sum over tiles of the blend's break index n_t.
+    """
+    return {
+        # inputs 44 + S B read once per group; out 64-B record + 8-B depth bits
+        # + 8-B rect + 1-B kept + 4-B touched zeroing = 85 B per Gaussian
+        "preprocess": n * ((44 + s_read) / group + 85),
+        # depth keys: read 8 N, write 4 N; pass 1: read 4 N keys, write 4 N keys +
+        # 4 N ids (implicit payload); passes 2-3: read + write 8 N each; fix-up
+        # reads the 4 N keys
+        "depth_sort": n * (12 + 12 + 16 + 16 + 4),
+        # ranked ids 4 B + rect gather 8 B per visible splat, 8-B key per instance
+        "emit": 12 * n_vis + 8 * k,
+        # each pass reads and writes every 8-B key; ranges 8 B per tile
+        "tile_sort": 16 * tile_passes * k + 8 * tiles,
+        # per processed instance an 8-B key + 64-B record; rgb, alpha, depth per
+        # pixel; one range per tile; touched per Gaussian
+        "blend": 72 * processed + 8 * tiles + 20 * pixels + 4 * n,
+    }
+
+
 class BatchRenderer:
     def __init__(self, model: GaussianModel, width: int, height: int, max_views: int,
                  tile_size: int = 16, sh_eval_degree: int = 3, background=(0.0, 0.0, 0.0),
                  with_touched: bool = True, n_streams: int = 2, group: int = 1,
-                 page_mask: torch.Tensor | None = None):
+                 page_mask: torch.Tensor | None = None, flags: int = 0):
         self.model = model
         self.dev = model.device
         self.w, self.h, self.ts = int(width), int(height), int(tile_size)
@@ -37,6 +62,7 @@ class BatchRenderer:
         self.max_views = int(max_views)
         self.sh_eval_degree = int(sh_eval_degree)
         self.background = background
+        self.flags = int(flags)  # extra LMGS_FLAG_* (e.g. LMGS_FLAG_TILE_SORT)
         dev = self.dev
         v = self.max_views
         self.rgb = torch.empty((v, self.h, self.w, 3), dtype=torch.float32, device=dev)
@@ -80,7 +106,7 @@ class BatchRenderer:
         assert len(cams) <= self.max_views
         L = _lib.lib()
         caller = torch.cuda.current_stream(self.dev)
-        flags = _lib.LMGS_FLAG_STAGE_TIMES if stage_times else 0
+        flags = (_lib.LMGS_FLAG_STAGE_TIMES if stage_times else 0) | self.flags
         st = abi_settings(self.ts, self.sh_eval_degree, self.background, flags)
         g = self._g
         if stage_times:
@@ -109,15 +135,8 @@ class BatchRenderer:
             t = self.tx * self.ty
             p = tile_passes(t)
             proc = self._processed_total(len(cams)) / nv
-            alg = {  # algorithmic bytes per frame
-                # the inputs are read once per group of views
-                "preprocess": n * ((44 + s_read) / self.group + 89),
-                "depth_sort": n * (4 + 4 * 16 - 4 + 4),
-                "emit": 16 * v_avg + 8 * k_avg,
-                "tile_sort": 16 * p * k_avg + 8 * k_avg + 8 * t,
-                "blend": 72 * proc + 8 * t + 20 * pix + 4 * n,
-            }
-            return {"stage_ms": tot, "alg_bytes": alg,
+            alg = alg_bytes_per_view(n, s_read, self.group, v_avg, k_avg, t, p, proc, pix)
+            return {"stage_ms": tot, "alg_bytes": alg, "launches": launches,
                     "per_frame": {"instances": k_avg, "visible": v_avg, "pairs": pairs / nv,
                                   "processed": proc, "tile_passes": p}}
         G = self.group
@@ -176,7 +195,8 @@ class BatchRenderer:
     def _processed_total(self, nv) -> float:
         return float(self.nproc[:nv].double().sum().item())
 
-    def bench_e2e(self, cams, steps: int, barrier=None, world: int = 1, device=None) -> dict:
+    def bench_e2e(self, cams, steps: int, barrier=None, world: int = 1, device=None,
+                  total_views: int | None = None) -> dict:
         """Frames/s through the public API with host buffers: per step the
         camera poses travel H2D (kernel parameters, from pinned host structs)
         and every RGB frame is copied D2H into pinned host memory on a copy
@@ -211,7 +231,8 @@ class BatchRenderer:
         ms = float(t.item())
         h2d = nv * ctypes.sizeof(_lib.Camera)
         d2h = nv * self.h * self.w * 3 * 4
-        return {"value": nv * world * steps / (ms / 1e3), "unit": "frames/s",
+        total = nv * world if total_views is None else int(total_views)
+        return {"value": total * steps / (ms / 1e3), "unit": "frames/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
                 "wall_s": wall,
                 "path": "BatchRenderer.render (lmgs_render C-ABI) with cameras from host, "

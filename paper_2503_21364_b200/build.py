@@ -41,8 +41,37 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
+TORCH_OPS_SRC = CSRC / "torch_ops.cpp"
+TORCH_OPS_LIB = PKG / "_lmgs_torch.so"
+
+
 def _sources():
     return sorted(CSRC.glob("*.cu"))
+
+
+def build_torch_ops(force: bool = False) -> Path:
+    """The TORCH_LIBRARY(lmgs) operators (csrc/torch_ops.cpp): a g++-built
+    shared object over liblmgs.so (rpath $ORIGIN) and libtorch, in-tree."""
+    if not (force or _stale(TORCH_OPS_LIB, [TORCH_OPS_SRC, LIB, INCLUDE / "lmgs.h",
+                                            Path(__file__)])):
+        return TORCH_OPS_LIB
+    import torch
+    from torch.utils import cpp_extension as ce
+
+    abi = int(torch.compiled_with_cxx11_abi())
+    incs = [f"-I{p}" for p in ce.include_paths(device_type="cuda")]
+    libs = [f"-L{p}" for p in ce.library_paths(device_type="cuda")]
+    rpaths = [f"-Wl,-rpath,{p}" for p in ce.library_paths(device_type="cuda")]
+    tmp = TORCH_OPS_LIB.with_suffix(".so.tmp")
+    cmd = ["g++", "-O2", "-std=c++17", "-shared", "-fPIC", f"-D_GLIBCXX_USE_CXX11_ABI={abi}",
+           *incs, str(TORCH_OPS_SRC), "-o", str(tmp), f"-L{PKG}", "-llmgs",
+           "-Wl,-rpath,$ORIGIN", *libs, *rpaths, "-lc10", "-lc10_cuda", "-ltorch_cpu",
+           "-ltorch_cuda", "-ltorch"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"torch ops build failed:\n{r.stderr[-4000:]}")
+    os.replace(tmp, TORCH_OPS_LIB)
+    return TORCH_OPS_LIB
 
 
 def _deps():
@@ -76,11 +105,13 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         objs = list(ex.map(lambda s: _compile(s, force, log), srcs))
     if force or _stale(LIB, objs):
         tmp = LIB.with_suffix(".so.tmp")
-        cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart_static"]
+        cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart_static",
+               "-Xlinker", "-soname=liblmgs.so"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
         os.replace(tmp, LIB)
+    build_torch_ops(force)
     if verbose:
         for name, err in log:
             print(f"--- {name}\n{err}", file=sys.stderr)

@@ -25,8 +25,9 @@ namespace {
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
-const char* kStageNames[] = {"preprocess", "depth_sort", "emit", "tile_sort", "blend"};
-constexpr int kNumStages = 5;
+const char* kStageNames[] = {"preprocess", "depth_sort", "emit", "tile_sort", "blend",
+                             "touched_fix"};
+constexpr int kNumStages = 6;
 
 // grow-only device buffer
 struct DevBuf {
@@ -92,10 +93,12 @@ struct Scalars {  // device-side small state
   uint32_t depth_counters[kMaxPasses];
   uint32_t tile_counters[kMaxPasses];
   unsigned long long counts[3];  // n_kept, n_vis, n_inst (one D2H copy)
+  unsigned long long n_entries;  // bin path: (splat, bin) entries
   unsigned long long zrange[2];  // min / max visible fp64 depth bits
   uint32_t emit_ticket;
   int blend_counter;
   uint32_t fix_count;  // pixels queued for the exact-touched replay (K7b)
+  uint32_t np_count;   // pixels whose fp64 break index differs (exact n_processed)
   DevSlots slots;
 };
 
@@ -105,7 +108,11 @@ struct lmgs_context {
   int device = 0;
   int sms = 148;
   std::string err;
-  DevBuf gbuf, tbuf, ibuf, bwbuf, fixbuf;
+  DevBuf gbuf, tbuf, ibuf, bwbuf, fixbuf, npbuf;  // npbuf: override (-1) + list, W*H each
+  DevBuf binbuf;  // bin path: bin counts / starts, piece starts and counts
+  int64_t cap_bins = -1, cap_pieces = -1;
+  uint32_t *bin_count = nullptr, *bin_start = nullptr, *piece_start = nullptr,
+           *piece_counts = nullptr;
   Scalars* d_scal = nullptr;
   uint64_t* h_pinned = nullptr;  // [0..2] = n_kept, n_vis, K
   cudaEvent_t ev[2 * kNumStages] = {};
@@ -204,6 +211,24 @@ int ensure_instances(lmgs_context* c, int64_t k, cudaStream_t s) {
   return LMGS_OK;
 }
 
+int ensure_bins(lmgs_context* c, int64_t bins, int64_t pieces, cudaStream_t s) {
+  if (bins <= c->cap_bins && pieces <= c->cap_pieces && c->bin_count) return LMGS_OK;
+  const size_t need = align_up(4 * bins) + 2 * align_up(4 * (bins + 1)) +
+                      align_up(4 * 64 * pieces) + 4 * kAlign;
+  if (need > c->binbuf.bytes) {
+    LMGS_CUDA(c, cudaStreamSynchronize(s));
+    LMGS_CUDA(c, c->binbuf.reserve(need));
+  }
+  Carver cv{static_cast<char*>(c->binbuf.ptr)};
+  c->bin_count = cv.take<uint32_t>(bins);
+  c->bin_start = cv.take<uint32_t>(bins + 1);
+  c->piece_start = cv.take<uint32_t>(bins + 1);
+  c->piece_counts = cv.take<uint32_t>(64 * pieces);
+  c->cap_bins = bins;
+  c->cap_pieces = pieces;
+  return LMGS_OK;
+}
+
 int validate(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
              const lmgs_settings* s) {
   if (!c) return LMGS_ERR_INVALID;
@@ -221,9 +246,10 @@ int validate(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
   if (g->page_mask && g->page_shift != 7)
     return fail(c, LMGS_ERR_INVALID, "page_shift must be 7 (128-row pages)");
   if (s->tile_size < 1) return fail(c, LMGS_ERR_INVALID, "tile_size must be >= 1");
-  if (s->tile_size > 64) return fail(c, LMGS_ERR_UNSUPPORTED, "tile_size > 64 not supported");
   if (cam->width < 1 || cam->height < 1) return fail(c, LMGS_ERR_INVALID, "bad image size");
-  if (cam->width > 65535 * s->tile_size || cam->height > 65535 * s->tile_size)
+  if ((int64_t)cam->width * cam->height >= ((int64_t)1 << 32))
+    return fail(c, LMGS_ERR_UNSUPPORTED, "more than 2^32 pixels in one view");
+  if (cam->width > 65535ll * s->tile_size || cam->height > 65535ll * s->tile_size)
     return fail(c, LMGS_ERR_UNSUPPORTED, "image too large for 16-bit tile coordinates");
   if (!(cam->fx > 0) || !(cam->fy > 0))
     return fail(c, LMGS_ERR_INVALID, "focal lengths must be positive");
@@ -413,6 +439,72 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
     return fail(c, LMGS_ERR_UNSUPPORTED, "more than 2^30 tile instances in one view");
   if (int r = ensure_instances(c, k > 0 ? k : 1, s)) return r;
 
+  const int bins_x = (ca.tiles_x + 7) / 8, bins_y = (ca.tiles_y + 7) / 8;
+  const int64_t n_bins = (int64_t)bins_x * bins_y;
+  if (n_bins <= kMaxBins && !(st->flags & LMGS_FLAG_TILE_SORT)) {
+    // default: tile lists through coarse bins (bins.cu)
+    const int64_t pieces = k / kPiece + n_bins + 1;
+    if (int r = ensure_bins(c, n_bins, pieces, s)) return r;
+    const int bin_passes = bits_for(n_bins) > 8 ? 2 : 1;
+    BinArgs bn{};
+    bn.order_slot = &sc->slots.depth_ids;
+    bn.rects = c->rects;
+    bn.n_vis = &sc->counts[1];
+    bn.tiles_x = ca.tiles_x;
+    bn.tiles_y = ca.tiles_y;
+    bn.bins_x = bins_x;
+    bn.n_bins = (int32_t)n_bins;
+    bn.n_bin_passes = bin_passes;
+    bn.entries = c->inst_keys[0];
+    bn.entry_cap = (uint64_t)c->cap_k;
+    bn.lookback = c->emit_lookback;
+    bn.ticket = &sc->emit_ticket;
+    bn.hist = sc->tile_hist;
+    bn.n_entries = &sc->n_entries;
+    bn.entries_slot = &sc->slots.bin_entries;
+    bn.keys_slot = &sc->slots.inst_keys;
+    bn.buf[0] = c->inst_keys[0];
+    bn.buf[1] = c->inst_keys[1];
+    bn.bin_count = c->bin_count;
+    bn.bin_start = c->bin_start;
+    bn.piece_start = c->piece_start;
+    bn.piece_counts = c->piece_counts;
+    bn.tile_count = c->tile_count;
+    bn.ranges = ranges;
+    tm.begin(2);
+    LMGS_CUDA(c, cudaMemsetAsync(sc->tile_hist, 0, sizeof(sc->tile_hist), s));
+    LMGS_CUDA(c, cudaMemsetAsync(&sc->emit_ticket, 0, sizeof(uint32_t), s));
+    LMGS_CUDA(c, cudaMemsetAsync(&sc->n_entries, 0, sizeof(sc->n_entries), s));
+    if (n_vis > 0) {
+      LMGS_CUDA(c, cudaMemsetAsync(c->emit_lookback, 0, sizeof(uint64_t) * emit_chunks(n_vis), s));
+      launched += launch_bin_emit(bn, n_vis, s);
+    }
+    tm.end(2);
+    tm.begin(3);
+    {
+      RadixSortBuffers rb{};
+      rb.keys[0] = c->inst_keys[0];
+      rb.keys[1] = c->inst_keys[1];
+      rb.key_bytes = 8;
+      rb.plan = &sc->tile_plan;
+      rb.hist = sc->tile_hist;
+      rb.lookback = c->tile_lookback;
+      rb.counters = sc->tile_counters;
+      rb.keys_result = &sc->slots.bin_entries;
+      rb.hist_ready = true;
+      rb.seg_counts = c->bin_count;
+      rb.seg_shift = 32;
+      rb.seg_mask = 0xffff;
+      rb.n_dev = &sc->n_entries;
+      LMGS_CUDA(c, cudaMemsetAsync(c->bin_count, 0, sizeof(uint32_t) * n_bins, s));
+      launched += radix_sort(rb, k, 32, bin_passes, s);
+      launched += launch_bin_lists(bn, pieces, s);
+    }
+    if (out->tile_ranges && tiles > 0)
+      LMGS_CUDA(c, cudaMemcpyAsync(out->tile_ranges, ranges, sizeof(int2) * tiles,
+                                   cudaMemcpyDeviceToDevice, s));
+    tm.end(3);
+  } else {
   // K4
   tm.begin(2);
   LMGS_CUDA(c, cudaMemsetAsync(sc->tile_hist, 0, sizeof(sc->tile_hist), s));
@@ -456,6 +548,7 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
     LMGS_CUDA(c, cudaMemcpyAsync(out->tile_ranges, ranges, sizeof(int2) * tiles,
                                  cudaMemcpyDeviceToDevice, s));
   tm.end(3);
+  }
 
   // K7
   tm.begin(4);
@@ -478,7 +571,9 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
   ba.work_counter = &sc->blend_counter;
   const bool fix = out->touched != nullptr && !(st->flags & LMGS_FLAG_NO_TOUCHED_FIX);
   if (fix) {
-    const int64_t cap = (int64_t)cam->width * cam->height / 8 + 1024;
+    // one entry per pixel: a pixel is queued at most once, so the queue
+    // cannot overflow
+    const int64_t cap = (int64_t)cam->width * cam->height;
     if ((size_t)cap * 4 > c->fixbuf.bytes) {
       LMGS_CUDA(c, cudaStreamSynchronize(s));
       LMGS_CUDA(c, c->fixbuf.reserve((size_t)cap * 4));
@@ -486,7 +581,22 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
     LMGS_CUDA(c, cudaMemsetAsync(&sc->fix_count, 0, sizeof(uint32_t), s));
     ba.fix_count = &sc->fix_count;
     ba.fix_list = static_cast<uint32_t*>(c->fixbuf.ptr);
-    ba.fix_cap = (int32_t)(c->fixbuf.bytes / 4);
+    if (out->n_processed) {
+      // override i32, list u32, need u8: W * H entries each
+      const size_t third = align_up((size_t)cap * 4);
+      if (3 * third > c->npbuf.bytes) {
+        LMGS_CUDA(c, cudaStreamSynchronize(s));
+        LMGS_CUDA(c, c->npbuf.reserve(3 * third));
+        // every override entry is -1 between views (k_nproc_reset restores it)
+        LMGS_CUDA(c, cudaMemsetAsync(c->npbuf.ptr, 0xff, c->npbuf.bytes, s));
+      }
+      char* nb = static_cast<char*>(c->npbuf.ptr);
+      LMGS_CUDA(c, cudaMemsetAsync(&sc->np_count, 0, sizeof(uint32_t), s));
+      ba.np_count = &sc->np_count;
+      ba.np_override = reinterpret_cast<int32_t*>(nb);
+      ba.np_list = reinterpret_cast<const uint32_t*>(nb + third);
+      ba.np_need = reinterpret_cast<const uint8_t*>(nb + 2 * third);
+    }
   }
   if (strips) {
     ba.n_strips = strips->n_strips;
@@ -497,8 +607,11 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
       ba.sdepth[i] = strips->depth[i];
     }
   }
-  if (int r = launch_blend(ba, s)) return fail(c, r, "unsupported tile size");
+  if (int r = launch_blend(ba, s)) return fail(c, r, "too many blend blocks for this tile size");
   launched += tiles > 0 ? 1 : 0;
+  tm.end(4);
+  // K7b
+  tm.begin(5);
   if (fix && tiles > 0) {
     TouchedFixArgs fa{};
     fa.keys_slot = &sc->slots.inst_keys;
@@ -508,16 +621,24 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
     fa.tiles_x = ca.tiles_x;
     fa.fix_count = &sc->fix_count;
     fa.fix_list = ba.fix_list;
-    fa.fix_cap = ba.fix_cap;
+    fa.width = cam->width;
     fa.touched = out->touched;
     fa.means = g->means;
     fa.quats = g->quats;
     fa.scales = g->scales;
     fa.logits = g->opacity_logits;
     fa.cam = ca;
+    if (ba.np_count) {
+      fa.np_count = &sc->np_count;
+      fa.np_list = const_cast<uint32_t*>(ba.np_list);
+      fa.np_need = const_cast<uint8_t*>(ba.np_need);
+      fa.np_override = ba.np_override;
+      fa.n_processed = out->n_processed;
+    }
     launched += launch_touched_fix(fa, s);
+    if (ba.np_count) launched += launch_nproc_fix(ba, s);
   }
-  tm.end(4);
+  tm.end(5);
   c->stats.n_launches = launched;
   c->last_timed = vp->timed;
   LMGS_CUDA(c, cudaGetLastError());
@@ -569,6 +690,8 @@ void lmgs_context_destroy(lmgs_context* c) {
   c->ibuf.release();
   c->bwbuf.release();
   c->fixbuf.release();
+  c->npbuf.release();
+  c->binbuf.release();
   if (c->d_scal) cudaFree(c->d_scal);
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   for (int i = 0; i < 2 * kNumStages; ++i)

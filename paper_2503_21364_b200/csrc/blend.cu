@@ -40,12 +40,20 @@ __device__ __forceinline__ bool crossing_uncertain(float T, float Tc) {
   if (T < kTermEpsF) return Tc < kTermEpsF * (1.0f + kFixBand) || T >= kTermEpsF * (1.0f - kFixBand);
   return T < kTermEpsF * (1.0f + kFixBand);
 }
-__device__ __forceinline__ void queue_fix(const BlendArgs& a, int tile, int lx, int ly) {
+// The queue holds W * H entries (each pixel is queued at most once), so it
+// cannot overflow.  Entry = fix_entry(): tile << 8 | ly << 4 | lx for 16x16
+// tiles (tile < 2^24, the cheap form inside k_blend16w), else the pixel index
+// y * W + x.
+__device__ __forceinline__ uint32_t fix_entry16(int tile, int lx, int ly) {
+  return ((uint32_t)tile << 8) | ((uint32_t)ly << 4) | (uint32_t)lx;
+}
+__device__ __forceinline__ void queue_fix(const BlendArgs& a, uint32_t entry) {
   const uint32_t slot = atomicAdd(a.fix_count, 1u);
-  if (slot < (uint32_t)a.fix_cap) a.fix_list[slot] = ((uint32_t)tile << 12) | (ly << 6) | lx;
+  a.fix_list[slot] = entry;
 }
 constexpr int kBatch = 256;
 constexpr int kMaxWarps = 8;
+constexpr int kMaxBlockW = 64;  // k_blend pixel block edge (256 threads x 16 pixels)
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -61,8 +69,12 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 
 // PPT pixels per thread; SWZ: 16x16 tile on 256 threads with each warp owning
 // an 8x4 pixel block (tighter warp bboxes than 16x2 rows).
-template <int PPT, bool SWZ>
-__global__ void __launch_bounds__(256) k_blend(BlendArgs a) {
+// NPFIX: recompute n_processed of one tile exactly (no image outputs): each
+// pixel's break index from the fp32 recurrence, except the pixels K7b found
+// to cross TERM_EPS at a different splat in fp64, whose fp64 index
+// (a.np_override) is taken instead.
+template <int PPT, bool SWZ, bool NPFIX>
+__device__ __forceinline__ void blend_block(const BlendArgs& a, const int tile, const int sub) {
   __shared__ float4 s_geo[kBatch];   // mx_local, my_local, qa, qb
   __shared__ float4 s_geo2[kBatch];  // qc, log2_alpha, r2_lo, r2_hi
   __shared__ float4 s_col[kBatch];   // r, g, b, z
@@ -76,8 +88,12 @@ __global__ void __launch_bounds__(256) k_blend(BlendArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nthreads = blockDim.x;
   const int nwarps = (nthreads + 31) >> 5;
-  const int tile = blockIdx.x;
+  // tiles above 64 px are split into 64x64 sub-blocks, one CTA each, that
+  // walk the same list (the tile's break index is the max of theirs)
+  const int subs = a.subs_x * a.subs_x;
   const int ts = a.tile_size;
+  const int bw = ts < kMaxBlockW ? ts : kMaxBlockW;
+  const int sx0 = (sub % a.subs_x) * bw, sy0 = (sub / a.subs_x) * bw;
   const int tile_x = tile % a.tiles_x, tile_y = tile / a.tiles_x;
   const int x0 = tile_x * ts, y0 = tile_y * ts;
   const int2 range = a.ranges[tile];
@@ -96,12 +112,12 @@ __global__ void __launch_bounds__(256) k_blend(BlendArgs a) {
       pix = ly * 16 + lx;
     } else {
       pix = tid + p * nthreads;
-      lx = pix % ts;
-      ly = pix / ts;
+      lx = sx0 + pix % bw;
+      ly = sy0 + pix / bw;
     }
     lxs[p] = lx;
     lys[p] = ly;
-    valid[p] = pix < ts * ts && x0 + lx < a.width && y0 + ly < a.height;
+    valid[p] = pix < bw * bw && lx < ts && ly < ts && x0 + lx < a.width && y0 + ly < a.height;
     T[p] = valid[p] ? 1.0f : 0.0f;  // invalid pixels never go active
     Tc[p] = 1.0f;
     C0[p] = C1[p] = C2[p] = D[p] = 0.0f;
@@ -210,7 +226,7 @@ __global__ void __launch_bounds__(256) k_blend(BlendArgs a) {
       if (lane == 0) s_cnt[warp][k] = (uint16_t)wsum;
     }
     __syncthreads();
-    if (a.touched) {
+    if (!NPFIX && a.touched) {
       for (int j = tid; j < nb; j += nthreads) {
         int s = 0;
 #pragma unroll
@@ -220,6 +236,29 @@ __global__ void __launch_bounds__(256) k_blend(BlendArgs a) {
     }
   }
 
+  if (NPFIX) {
+    // per pixel: its break index (list length while still active)
+    const int len = range.y - range.x;
+    int v = 0;
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) {
+      if (!valid[p]) continue;
+      const int o = a.np_override[(int64_t)(y0 + lys[p]) * a.width + x0 + lxs[p]];
+      v = max(v, o >= 0 ? o : (T[p] >= kTermEpsF ? len : last[p] + 1));
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if (lane == 0) s_last[warp] = v;
+    __syncthreads();
+    if (tid == 0) {
+      int m = 0;
+      for (int w = 0; w < nwarps; ++w) m = max(m, s_last[w]);
+      // blocks of one tile run in sequence in this CTA (see k_nproc_fix)
+      a.n_processed[tile] = sub == 0 ? m : max(a.n_processed[tile], m);
+    }
+    __syncthreads();
+    return;
+  }
   // n_processed: the break index of _blend's loop (324-325)
   int my_last = -1;
   bool my_live = false;
@@ -238,16 +277,49 @@ __global__ void __launch_bounds__(256) k_blend(BlendArgs a) {
     if (tid == 0) {
       int m = -1;
       for (int w = 0; w < nwarps; ++w) m = max(m, s_last[w]);
-      a.n_processed[tile] = any_live ? (range.y - range.x) : (m + 1);
+      const int v = any_live ? (range.y - range.x) : (m + 1);
+      if (subs == 1) a.n_processed[tile] = v;
+      else atomicMax(a.n_processed + tile, v);  // zeroed by launch_blend
     }
   }
   // outputs: C + T * bg (326), alpha = 1 - T_final, depth, T_final
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
-    if (!valid[p]) continue;
+    if (NPFIX || !valid[p]) continue;
     put_pixel(a, x0 + lxs[p], y0 + lys[p], T[p], C0[p], C1[p], C2[p], D[p]);
-    if (a.fix_count && crossing_uncertain(T[p], Tc[p])) queue_fix(a, tile, lxs[p], lys[p]);
+    if (a.fix_count && crossing_uncertain(T[p], Tc[p]))
+      queue_fix(a, ts == 16 ? fix_entry16(tile, lxs[p], lys[p])
+                            : (uint32_t)(y0 + lys[p]) * (uint32_t)a.width + (uint32_t)(x0 + lxs[p]));
   }
+}
+
+template <int PPT, bool SWZ>
+__global__ void __launch_bounds__(256) k_blend(BlendArgs a) {
+  const int subs = a.subs_x * a.subs_x;
+  blend_block<PPT, SWZ, false>(a, blockIdx.x / subs, blockIdx.x % subs);
+}
+
+// Exact n_processed for the tiles K7b flagged (np_need: a corrected pixel set
+// the tile's fp32 break index; a tile listed twice is recomputed twice, to
+// the same value).
+template <int PPT, bool SWZ>
+__global__ void __launch_bounds__(256) k_nproc_fix(BlendArgs a) {
+  const uint32_t n = *a.np_count;
+  for (uint32_t e = blockIdx.x; e < n; e += gridDim.x) {
+    if (!a.np_need[e]) continue;
+    const uint32_t pix = a.np_list[e];
+    const int tile = (int)(pix / (uint32_t)a.width) / a.tile_size * a.tiles_x +
+                     (int)(pix % (uint32_t)a.width) / a.tile_size;
+    for (int sub = 0; sub < a.subs_x * a.subs_x; ++sub)
+      blend_block<PPT, SWZ, true>(a, tile, sub);
+  }
+}
+
+// the overrides are reset for the next view once k_nproc_fix has read them
+__global__ void k_nproc_reset(BlendArgs a) {
+  const uint32_t n = *a.np_count;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x)
+    a.np_override[a.np_list[e]] = -1;
 }
 
 // ---------------------------------------------------------------------------
@@ -469,7 +541,7 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
     for (int q = 0; q < NP; ++q) {
       if (!valid[q]) continue;
       put_pixel(a, x0 + lx, y0 + ly[q], T[q], C0[q], C1[q], C2[q], D[q]);
-      if (a.fix_count && crossing_uncertain(T[q], Tc[q])) queue_fix(a, tile, lx, ly[q]);
+      if (a.fix_count && crossing_uncertain(T[q], Tc[q])) queue_fix(a, fix_entry16(tile, lx, ly[q]));
     }
   }
 }
@@ -481,10 +553,33 @@ constexpr int kBlendNP = LMGS_BLEND_NP;
 
 }  // namespace
 
-int launch_blend(const BlendArgs& a, cudaStream_t s) {
+int launch_nproc_fix(const BlendArgs& args, cudaStream_t s) {
+  BlendArgs a = args;
+  const int ts = a.tile_size;
+  const int ext = ts < max(a.width, a.height) ? ts : max(a.width, a.height);
+  a.subs_x = (ext + kMaxBlockW - 1) / kMaxBlockW;
+  const int grid = 16;  // tiles to recompute are rare
+  if (ts == 16) {
+    k_nproc_fix<1, true><<<grid, 256, 0, s>>>(a);
+  } else if (ts < 16) {
+    k_nproc_fix<1, false><<<grid, ((ts * ts + 31) / 32) * 32, 0, s>>>(a);
+  } else if (ts <= 32) {
+    k_nproc_fix<4, false><<<grid, 256, 0, s>>>(a);
+  } else {
+    k_nproc_fix<16, false><<<grid, 256, 0, s>>>(a);
+  }
+  k_nproc_reset<<<16, 256, 0, s>>>(a);
+  return 2;
+}
+
+int launch_blend(const BlendArgs& args, cudaStream_t s) {
+  BlendArgs a = args;
   const int ts = a.tile_size;
   const int tiles = a.tiles_x * a.tiles_y;
   if (tiles <= 0) return 0;
+  // the blocks of a tile larger than the image only need to cover the image
+  const int ext = ts < max(a.width, a.height) ? ts : max(a.width, a.height);
+  a.subs_x = (ext + kMaxBlockW - 1) / kMaxBlockW;
   if (ts == 16 && a.work_counter) {
     cudaMemsetAsync(a.work_counter, 0, sizeof(int), s);
     if (a.n_processed) cudaMemsetAsync(a.n_processed, 0, sizeof(int) * tiles, s);
@@ -516,7 +611,10 @@ int launch_blend(const BlendArgs& a, cudaStream_t s) {
   } else if (ts <= 64) {
     k_blend<16, false><<<tiles, 256, 0, s>>>(a);
   } else {
-    return LMGS_ERR_UNSUPPORTED;
+    const int64_t ctas = (int64_t)tiles * a.subs_x * a.subs_x;
+    if (ctas >= ((int64_t)1 << 31)) return LMGS_ERR_UNSUPPORTED;
+    if (a.n_processed) cudaMemsetAsync(a.n_processed, 0, sizeof(int) * tiles, s);
+    k_blend<16, false><<<(unsigned)ctas, 256, 0, s>>>(a);
   }
   return 0;
 }

@@ -118,9 +118,19 @@ int read_info(FILE* f, const char* path, lmgs_checkpoint_info* info, char* err, 
   if (info->sh_degree > 3)
     return set_err(err, err_len, LMGS_ERR_UNSUPPORTED,
                    std::string(path) + ": sh_degree " + std::to_string(info->sh_degree));
-  info->count = (int64_t)count;
   info->row_floats = row_floats(info->sh_degree);
   info->data_offset = (int64_t)kHeaderBytes;
+  // the count is untrusted: bound it by the bytes the file holds before any
+  // multiplication (the reference's reader fails with "truncated" there)
+  if (fseek(f, 0, SEEK_END) != 0)
+    return set_err(err, err_len, LMGS_ERR_IO, std::string(path) + ": seek failed");
+  const int64_t file_bytes = (int64_t)ftell(f);
+  const uint64_t row_bytes = 4ull * (uint64_t)info->row_floats;
+  const uint64_t avail = file_bytes > info->data_offset ? (uint64_t)(file_bytes - info->data_offset) : 0;
+  if (count > avail / row_bytes)
+    return set_err(err, err_len, LMGS_ERR_FORMAT,
+                   std::string(path) + ": truncated at byte offset " + std::to_string(file_bytes));
+  info->count = (int64_t)count;
   const int64_t data_bytes = info->count * (int64_t)info->row_floats * 4;
   if (fseek(f, (long)(info->data_offset + data_bytes), SEEK_SET) != 0)
     return set_err(err, err_len, LMGS_ERR_FORMAT, std::string(path) + ": truncated rows");

@@ -143,6 +143,10 @@ struct RadixSortBuffers {
   // the sorted key bits must cover the segment bits (tile sort: ranges)
   uint32_t* seg_counts;
   int seg_shift;
+  uint64_t seg_mask;  // segment = (key >> seg_shift) & seg_mask (0 = all bits)
+  // nullable: the key count on the device (n is then an upper bound sizing
+  // the grid and the look-back; kernels use min(n, *n_dev))
+  const unsigned long long* n_dev;
 };
 
 size_t radix_lookback_words(int64_t capacity);
@@ -156,7 +160,7 @@ struct DevSlots {
   void* depth_keys;  // K2 result: fp32 depth keys in (depth, id) order
   void* depth_ids;   // K2 result: Gaussian ids in (depth, id) order
   void* inst_keys;   // K5 result: tile << 32 | id, sorted by tile then depth rank
-  void* unused;
+  void* bin_entries; // bin path: entries sorted by bin (bins.cu)
 };
 
 // ---------------------------------------------------------------------------
@@ -198,6 +202,35 @@ struct EmitArgs {
 inline int64_t emit_chunks(int64_t n_vis) { return (n_vis + kEmitChunk - 1) / kEmitChunk; }
 int launch_emit(const EmitArgs& a, cudaStream_t s);
 
+// ---------------------------------------------------------------------------
+// Tile lists through coarse bins of 8x8 tiles (bins.cu): the default K4-K6.
+constexpr int kPiece = 2048;  // entries per piece of a bin's entry run
+constexpr int kMaxBins = 1 << 16;
+struct BinArgs {
+  void* const* order_slot;            // -> uint32_t[n_vis] ids in depth-rank order
+  const uint64_t* rects;              // tile rect per splat
+  const unsigned long long* n_vis;    // device: visible splats
+  int32_t tiles_x, tiles_y, bins_x, n_bins, n_bin_passes;
+  uint64_t* entries;                  // B1 output (= buf[0])
+  uint64_t entry_cap;                 // entries / instance capacity
+  uint64_t* lookback;                 // [emit_chunks] status words (zeroed)
+  uint32_t* ticket;                   // chunk ticket (zeroed)
+  uint32_t* hist;                     // [2][256] bin digit histograms (zeroed)
+  unsigned long long* n_entries;      // device: E (zeroed)
+  void* const* entries_slot;          // -> the bin-sorted entries (radix result)
+  void** keys_slot;                   // <- the instance keys buffer (the other one)
+  void* buf[2];                       // the two instance-sized buffers
+  uint32_t* bin_count;                // [n_bins] entries per bin (zeroed; sort's last pass)
+  uint32_t* bin_start;                // [n_bins + 1]
+  uint32_t* piece_start;              // [n_bins + 1]
+  uint32_t* piece_counts;             // [pieces][64]
+  uint32_t* tile_count;               // [T]
+  int2* ranges;                       // [T]
+};
+int launch_bin_emit(const BinArgs& a, int64_t n_vis_bound, cudaStream_t s);
+// B3-B6 + K6 (after the bin sort); piece_bound >= the number of pieces
+int launch_bin_lists(const BinArgs& a, int64_t piece_bound, cudaStream_t s);
+
 // K6: tile ranges [start, end) = exclusive scan of the per-tile counts the
 // tile sort's last pass accumulated (empty tiles included)
 int launch_ranges_from_counts(const uint32_t* counts, int tiles, int2* ranges, cudaStream_t s);
@@ -220,6 +253,7 @@ struct BlendArgs {
   const int2* ranges;
   const BlendRec* recs;
   int32_t width, height, tile_size, tiles_x, tiles_y;
+  int32_t subs_x;  // set by launch_blend: 64x64 sub-blocks per tile edge (> 1 above 64 px)
   float bg[3];
   float* rgb;
   float* alpha;
@@ -232,10 +266,16 @@ struct BlendArgs {
   // strip y / strip_rows at row y % strip_rows of srgb / strans / sdepth
   // (possibly peer-GPU pointers) instead of rgb / alpha / depth / trans
   int32_t n_strips, strip_rows;
-  // exact-touched fix-up queue (nullable): pixels for the fp64 replay
+  // exact-touched fix-up queue (nullable): pixels (y * W + x) for the fp64
+  // replay; fix_list holds W * H entries
   uint32_t* fix_count;
   uint32_t* fix_list;
-  int32_t fix_cap;
+  // exact n_processed (launch_nproc_fix): pixels K7b corrected and their fp64
+  // break index per pixel (-1 = none; reset after use)
+  const uint32_t* np_count;
+  const uint32_t* np_list;
+  const uint8_t* np_need;
+  int32_t* np_override;
   float* srgb[8];
   float* strans[8];
   float* sdepth[8];
@@ -265,6 +305,9 @@ __device__ __forceinline__ void put_pixel(const BlendArgs& a, int x, int y, floa
   }
 }
 int launch_blend(const BlendArgs& a, cudaStream_t s);  // returns 0 or LMGS_ERR_UNSUPPORTED
+// after K7b: n_processed of the tiles holding a corrected pixel, recomputed
+// exactly (returns kernels launched)
+int launch_nproc_fix(const BlendArgs& a, cudaStream_t s);
 
 void launch_fill_background(float* rgb, float* alpha, float* depth, float* trans, int64_t n_pix,
                             const float bg[3], cudaStream_t s);
@@ -274,16 +317,23 @@ struct TouchedFixArgs {
   void* const* keys_slot;
   const int2* ranges;
   const BlendRec* recs;
-  int32_t tile_size, tiles_x;
+  int32_t tile_size, tiles_x, width;
   const uint32_t* fix_count;
-  const uint32_t* fix_list;
-  int32_t fix_cap;
+  const uint32_t* fix_list;  // pixels y * width + x
   int32_t* touched;
   const float* means;
   const float* quats;
   const float* scales;
   const float* logits;
   CamArgs cam;
+  // nullable: a replayed pixel whose fp64 break index differs from the fp32
+  // one is appended to np_list (np_need: its tile must be recomputed) and its
+  // fp64 index stored in np_override; n_processed is corrected in place
+  uint32_t* np_count;
+  uint32_t* np_list;
+  uint8_t* np_need;
+  int32_t* np_override;
+  int32_t* n_processed;
 };
 int launch_touched_fix(const TouchedFixArgs& a, cudaStream_t s);
 

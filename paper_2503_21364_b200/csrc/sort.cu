@@ -82,8 +82,10 @@ __global__ void __launch_bounds__(kRadix) k_radix_plan(const uint32_t* __restric
                                                        int64_t n, int n_passes, RadixPlan* plan,
                                                        const int* gate, void* keys0,
                                                        void* keys1, void* vals0, void* vals1,
-                                                       void** keys_result, void** vals_result) {
+                                                       void** keys_result, void** vals_result,
+                                                       const unsigned long long* n_dev) {
   const bool off = gated_off(gate);
+  if (n_dev) n = min(n, (int64_t)*n_dev);
   __shared__ uint32_t s_scan[kRadix];
   __shared__ int s_trivial[kMaxPasses];
   const int d = threadIdx.x;
@@ -143,7 +145,9 @@ template <typename K, bool VALS>
 __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
     K* keys0, K* keys1, uint32_t* vals0, uint32_t* vals1, int64_t n, int begin_bit, int pass,
     const RadixPlan* __restrict__ plan, uint32_t* lookback, uint32_t* counter, int64_t lb_stride,
-    bool iota_vals, uint32_t* seg_counts, int seg_shift) {
+    bool iota_vals, uint32_t* seg_counts, int seg_shift, uint64_t seg_mask,
+    const unsigned long long* n_dev) {
+  if (n_dev) n = min(n, (int64_t)*n_dev);  // the grid covers an upper bound
   if (!plan->active[pass]) {
     // no pass moves data (every digit trivial): the result buffers are the
     // inputs, so pass 0 materialises the implicit payload and the single
@@ -154,7 +158,7 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
              i += (int64_t)gridDim.x * blockDim.x)
           vals0[i] = (uint32_t)i;
       if (seg_counts && blockIdx.x == 0 && threadIdx.x == 0 && n > 0)
-        seg_counts[(uint64_t)keys0[0] >> seg_shift] = (uint32_t)n;
+        seg_counts[((uint64_t)keys0[0] >> seg_shift) & seg_mask] = (uint32_t)n;
     }
     return;
   }
@@ -171,15 +175,16 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_bid = atomicAdd(counter + pass, 1u);
+  __syncthreads();
+  const uint32_t bid = s_bid;
+  const int64_t base = (int64_t)bid * kSortTile;
+  if (base >= n) return;  // (the grid may cover an upper bound of n)
   for (int i = tid; i < kWarps * kRadix; i += kSortThreads) {
     (&s_match[0][0])[i] = 0;
     (&s_wcnt[0][0])[i] = 0;
   }
   s_hist[tid] = 0;  // kSortThreads == kRadix
   __syncthreads();
-  const uint32_t bid = s_bid;
-  const int64_t base = (int64_t)bid * kSortTile;
-  if (base >= n) return;
   const int count = (int)min((int64_t)kSortTile, n - base);
   const int src = plan->src[pass];
   const K* __restrict__ kin = src ? keys1 : keys0;
@@ -320,10 +325,10 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
     if (segs) {
       // the staged tile is sorted on every key bit sorted so far: runs of one
       // segment are contiguous; a run [i0, i1] adds (i1 + 1) - i0
-      const uint64_t sg = (uint64_t)k >> seg_shift;
-      if (i == 0 || ((uint64_t)s_keys[i - 1] >> seg_shift) != sg)
+      const uint64_t sg = ((uint64_t)k >> seg_shift) & seg_mask;
+      if (i == 0 || (((uint64_t)s_keys[i - 1] >> seg_shift) & seg_mask) != sg)
         atomicAdd(seg_counts + sg, (uint32_t)(-i));
-      if (i + 1 == count || ((uint64_t)s_keys[i + 1] >> seg_shift) != sg)
+      if (i + 1 == count || (((uint64_t)s_keys[i + 1] >> seg_shift) & seg_mask) != sg)
         atomicAdd(seg_counts + sg, (uint32_t)(i + 1));
     }
   }
@@ -347,7 +352,8 @@ void launch_onesweep(const RadixSortBuffers& b, int64_t n, int begin_bit, int p,
   }
   k_onesweep<K, VALS><<<(unsigned)blocks, kSortThreads, smem, s>>>(
       static_cast<K*>(b.keys[0]), static_cast<K*>(b.keys[1]), b.vals[0], b.vals[1], n, begin_bit,
-      p, b.plan, b.lookback, b.counters, blocks, b.iota_vals, b.seg_counts, b.seg_shift);
+      p, b.plan, b.lookback, b.counters, blocks, b.iota_vals, b.seg_counts, b.seg_shift,
+      b.seg_mask ? b.seg_mask : ~0ull, b.n_dev);
 }
 
 template <typename K>
@@ -370,7 +376,7 @@ int radix_sort_impl(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_p
     ++launched;
   }
   k_radix_plan<<<1, kRadix, 0, s>>>(b.hist, n, n_passes, b.plan, b.gate, k0, k1, b.vals[0],
-                                    b.vals[1], b.keys_result, b.vals_result);
+                                    b.vals[1], b.keys_result, b.vals_result, b.n_dev);
   ++launched;
   if (blocks == 0) return launched;
   for (int p = 0; p < n_passes; ++p) {

@@ -117,23 +117,37 @@ __global__ void __launch_bounds__(kFixThreads) k_touched_fix(TouchedFixArgs a) {
   __shared__ float s_pow[2][kProdWarps][32];
   __shared__ double s_sig[2][kProdWarps][32];
   __shared__ uint32_t s_id[2][kProdWarps][32];
+  __shared__ int s_pos[2][kProdWarps][32];  // list position (from the tile's start)
   __shared__ int s_cnt[2][kProdWarps];
   __shared__ int s_done;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t n = min(*a.fix_count, (uint32_t)a.fix_cap);
+  const uint32_t n = *a.fix_count;  // <= W * H = the queue's capacity
   const uint64_t* __restrict__ list = static_cast<const uint64_t*>(*a.keys_slot);
   const CamArgs& cam = a.cam;
   const int ts = a.tile_size;
   for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
-    const uint32_t v = a.fix_list[i];
-    const int tile = (int)(v >> 12), ly = (int)((v >> 6) & 63), lx = (int)(v & 63);
+    // blend.cu fix_entry: tile << 8 | ly << 4 | lx for 16x16 tiles, else y * W + x
+    const uint32_t e = a.fix_list[i];
+    int tile, lx, ly;
+    if (ts == 16) {
+      tile = (int)(e >> 8);
+      ly = (int)((e >> 4) & 15);
+      lx = (int)(e & 15);
+    } else {
+      const int gx = (int)(e % (uint32_t)a.width), gy = (int)(e / (uint32_t)a.width);
+      tile = (gy / ts) * a.tiles_x + gx / ts;
+      lx = gx % ts;
+      ly = gy % ts;
+    }
     const int x0 = (tile % a.tiles_x) * ts, y0 = (tile / a.tiles_x) * ts;
+    const uint32_t v = (uint32_t)(y0 + ly) * (uint32_t)a.width + (uint32_t)(x0 + lx);  // pixel
     const float px = (float)lx + 0.5f, py = (float)ly + 0.5f;  // tile-local (blend)
     const double pxd = (double)(x0 + lx) + 0.5, pyd = (double)(y0 + ly) + 0.5;  // 335-337
     const int2 range = a.ranges[tile];
     const int nr = (range.y - range.x + kRound - 1) / kRound;
     float T32 = 1.0f;  // thread 0's recurrences
     double T64 = 1.0;
+    int brk32 = -1, brk64 = -1;  // break indices: 1 + position of the crossing splat
     if (tid == 0) s_done = 0;
     // producer pipeline, three rounds deep: round r + 2's ids and first
     // record sectors load, round r + 1 takes the circle test and (inside
@@ -184,6 +198,7 @@ __global__ void __launch_bounds__(kFixThreads) k_touched_fix(TouchedFixArgs a) {
           s_sig[buf][warp - 1][pos] = op * exp(-0.5 * maha);
           s_pow[buf][warp - 1][pos] = power;
           s_id[buf][warp - 1][pos] = id;
+          s_pos[buf][warp - 1][pos] = r * kRound + pt;
         }
       }
       if (tid == 0 && r > 0 && !s_done) {  // scan round r - 1
@@ -207,6 +222,8 @@ __global__ void __launch_bounds__(kFixThreads) k_touched_fix(TouchedFixArgs a) {
             const bool c64 = T64 * sig64 > 0.0;
             T64 = T64 * (1.0 - sig64);
             if (c64 != c32) atomicAdd(a.touched + s_id[pb][w][k], c64 ? 1 : -1);
+            if (brk32 < 0 && T32 < kTermEpsF) brk32 = s_pos[pb][w][k] + 1;
+            if (brk64 < 0 && T64 < kTermEps) brk64 = s_pos[pb][w][k] + 1;
             if (T32 < kTermEpsF && T64 < kTermEps) {
               s_done = 1;
               break;
@@ -226,6 +243,25 @@ __global__ void __launch_bounds__(kFixThreads) k_touched_fix(TouchedFixArgs a) {
       atomicMax(&g_fix_hist[7], (unsigned)rounds);
     }
 #endif
+    if (tid == 0 && a.np_count) {
+      const int len = range.y - range.x;
+      if (brk32 < 0) brk32 = len;
+      if (brk64 < 0) brk64 = len;
+      if (brk32 != brk64) {
+        // The blend's n_processed[tile] = max(others, brk32) with every other
+        // pixel exact.  A later fp64 break only raises the max; an earlier one
+        // changes it only if this pixel set it, and then the tile is
+        // recomputed (launch_nproc_fix) with the fp64 index of every corrected
+        // pixel (np_override).
+        a.np_override[v] = brk64;
+        uint8_t need = 0;
+        if (brk64 > brk32) atomicMax(a.n_processed + tile, brk64);
+        else need = atomicAdd(a.n_processed + tile, 0) == brk32;
+        const uint32_t slot = atomicAdd(a.np_count, 1u);
+        a.np_list[slot] = v;
+        a.np_need[slot] = need;
+      }
+    }
     __syncthreads();
   }
 }

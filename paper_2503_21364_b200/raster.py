@@ -28,12 +28,17 @@ from .errors import InvalidInputError, ShapeError
 _CONTEXTS: dict = {}
 
 
-def context(device: int | None = None) -> _lib.Context:
+def context(device: int | None = None, stream=None) -> _lib.Context:
+    """The context of (device, stream): a context's arenas are stream-ordered,
+    so concurrent streams never share one (lmgs.h threading rule)."""
     if device is None:
         device = torch.cuda.current_device()
-    ctx = _CONTEXTS.get(device)
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    key = (int(device), int(stream.cuda_stream))
+    ctx = _CONTEXTS.get(key)
     if ctx is None:
-        ctx = _CONTEXTS[device] = _lib.Context(device)
+        ctx = _CONTEXTS[key] = _lib.Context(device)
     return ctx
 
 
@@ -240,7 +245,8 @@ def render(camera, gaussians: GaussianModel, tile_size: int = 16, background=(0.
            sh_eval_degree: int = 3, with_instances: bool = False, stage_times: bool = False,
            prim_ids: torch.Tensor | None = None, stream=None, ctx=None,
            out: dict | None = None, page_mask: torch.Tensor | None = None,
-           page_shift: int = 7, touched_fix: bool = True) -> RenderOutput:
+           page_shift: int = 7, touched_fix: bool = True,
+           tile_sort: bool = False) -> RenderOutput:
     """Render one view of device-resident Gaussians (north-star operator).
 
     ``prim_ids`` (int64, optional) are the original ids used for depth-tie
@@ -250,13 +256,16 @@ def render(camera, gaussians: GaussianModel, tile_size: int = 16, background=(0.
     fp64 replay that makes ``touched`` exact (K7b).  ``page_mask`` (device uint8 per
     128-row page: its number of live leading rows, 0..128) restricts the
     render to those rows (the paged device pool of ``offload``).
+    ``tile_sort=True`` builds the tile lists with the instance radix sort
+    instead of the default coarse-bin path (identical lists; for A/B tests).
     """
     if not isinstance(gaussians, GaussianModel):
         raise InvalidInputError("gaussians must be a GaussianModel (device SoA)")
     if int(tile_size) < 1:
         raise InvalidInputError("tile_size must be >= 1")
-    ctx = context(gaussians.device.index) if ctx is None else ctx
     dev = gaussians.device
+    if ctx is None:
+        ctx = context(dev.index, stream if stream is not None else torch.cuda.current_stream(dev))
     w, h = int(camera.width), int(camera.height)
     ts = int(tile_size)
     tx, ty = -(-w // ts), -(-h // ts)
@@ -288,7 +297,8 @@ def render(camera, gaussians: GaussianModel, tile_size: int = 16, background=(0.
     cam = abi_camera(camera)
     st = abi_settings(ts, sh_eval_degree, background,
                       (_lib.LMGS_FLAG_STAGE_TIMES if stage_times else 0)
-                      | (0 if touched_fix else _lib.LMGS_FLAG_NO_TOUCHED_FIX))
+                      | (0 if touched_fix else _lib.LMGS_FLAG_NO_TOUCHED_FIX)
+                      | (_lib.LMGS_FLAG_TILE_SORT if tile_sort else 0))
     sh = _stream_handle(stream)
     L = _lib.lib()
     with torch.cuda.device(dev):
@@ -361,8 +371,8 @@ def render_image(model, camera, tile_size: int = 16, background=(0.0, 0.0, 0.0),
 
 def project(camera, gaussians: GaussianModel, sh_eval_degree: int = 1, stream=None) -> dict:
     """Stage K1 alone (project_splats, 187-230): fp64 geometry per Gaussian."""
-    ctx = context(gaussians.device.index)
     dev = gaussians.device
+    ctx = context(dev.index, stream if stream is not None else torch.cuda.current_stream(dev))
     n = gaussians.count
     mean2d = torch.empty((n, 2), dtype=torch.float64, device=dev)
     cov2d = torch.empty((n, 3), dtype=torch.float64, device=dev)
@@ -397,10 +407,17 @@ def composite_blocks(rgb: torch.Tensor, trans: torch.Tensor, order, background=(
         else None
     order_np = np.ascontiguousarray(np.asarray(order, dtype=np.int32))
     bg = np.ascontiguousarray(np.asarray(background, dtype=np.float32).reshape(3))
+    # contiguous copies stay bound until the kernel is enqueued on `stream`;
+    # the caching allocator then orders their reuse after it
+    rgb_c, trans_c = rgb.contiguous(), trans.contiguous()
+    depth_c = depth.contiguous() if depth is not None else None
     st = _lib.lib().lmgs_composite_blocks(
-        _ptr(rgb.contiguous()), _ptr(trans.contiguous()),
-        _ptr(depth.contiguous()) if depth is not None else None, int(b), order_np.ctypes.data,
+        _ptr(rgb_c), _ptr(trans_c), _ptr(depth_c), int(b), order_np.ctypes.data,
         h * w, bg.ctypes.data, _ptr(out_rgb), _ptr(out_alpha), _ptr(out_depth),
         _stream_handle(stream))
+    cur = torch.cuda.current_stream(rgb.device) if stream is None else stream
+    for t in (rgb_c, trans_c, depth_c):
+        if t is not None:
+            t.record_stream(cur)
     _lib.check(None, st, "lmgs_composite_blocks")
     return out_rgb, out_alpha, out_depth

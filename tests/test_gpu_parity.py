@@ -17,6 +17,14 @@ from paper_2503_21364_b200.errors import InvalidInputError, ShapeError
 pytestmark = pytest.mark.gpu
 
 IMG_TOL = 1e-4  # max-abs per channel, written in the north star
+# depth = sum_i w_i z_i (north-star output, not in the reference): the fp32
+# blend's relative error times the frame's depth scale
+DEPTH_REL_TOL = 1e-4
+
+
+def _depth_ok(r):
+    """|depth - oracle| <= 1e-4 * max(1, max |oracle depth|)."""
+    return r["derr"] <= DEPTH_REL_TOL * max(1.0, r["dmax"])
 # touched counts are exact: pixels whose fp32 transmittance crosses TERM_EPS
 # within the uncertainty band are replayed in fp64 (K7b, touched_fix.cu)
 
@@ -105,8 +113,9 @@ def _full_frame_check(g, cam, ts=16, bg=(0.0, 0.0, 0.0), deg=3):
     err = float(np.abs(img - o["image"]).max())
     aerr = float(np.abs(out.alpha.cpu().double().numpy() - o["alpha"]).max())
     derr = float(np.abs(out.depth.cpu().double().numpy() - o["depth"]).max())
+    dmax = float(np.abs(o["depth"]).max()) if o["depth"].size else 0.0
     nproc = out.n_processed.cpu().numpy()
-    return dict(err=err, aerr=aerr, derr=derr, touched_mismatch=mism,
+    return dict(err=err, aerr=aerr, derr=derr, dmax=dmax, touched_mismatch=mism,
                 nproc_mismatch=int((nproc != o["n_processed"]).sum()), K=o["K"], oracle=o)
 
 
@@ -114,7 +123,7 @@ def test_c1_full_frame_vs_oracle():
     g = scenes.synthetic_gaussians(10_000, seed=0)
     cam = scenes.orbit_cameras(1, 256, 256, seed=0)[0]
     r = _full_frame_check(g, cam)
-    assert r["err"] <= IMG_TOL and r["aerr"] <= IMG_TOL
+    assert r["err"] <= IMG_TOL and r["aerr"] <= IMG_TOL and _depth_ok(r)
     assert r["touched_mismatch"] == 0 and r["nproc_mismatch"] == 0
 
 
@@ -127,8 +136,8 @@ def test_c2_full_frame_vs_oracle():
     print(f"c2: K={r['K']} max|rgb|={r['err']:.2e} max|alpha|={r['aerr']:.2e} "
           f"depth={r['derr']:.2e} touched_mism={r['touched_mismatch']} "
           f"nproc_mism={r['nproc_mismatch']}")
-    assert r["err"] <= IMG_TOL and r["aerr"] <= IMG_TOL
-    assert r["touched_mismatch"] == 0
+    assert r["err"] <= IMG_TOL and r["aerr"] <= IMG_TOL and _depth_ok(r)
+    assert r["touched_mismatch"] == 0 and r["nproc_mismatch"] == 0
 
 
 @pytest.mark.slow
@@ -137,9 +146,22 @@ def test_c3_view_full_frame_vs_oracle():
     g = scenes.synthetic_gaussians(6_000_000, seed=0)
     cam = scenes.orbit_cameras(64, 1920, 1080, seed=0)[5]
     r = _full_frame_check(g, cam)
-    print(f"c3 view: K={r['K']} max|rgb|={r['err']:.2e} touched_mism={r['touched_mismatch']}")
-    assert r["err"] <= IMG_TOL and r["aerr"] <= IMG_TOL
-    assert r["touched_mismatch"] == 0
+    print(f"c3 view: K={r['K']} max|rgb|={r['err']:.2e} depth={r['derr']:.2e} "
+          f"touched_mism={r['touched_mismatch']} nproc_mism={r['nproc_mismatch']}")
+    assert r["err"] <= IMG_TOL and r["aerr"] <= IMG_TOL and _depth_ok(r)
+    assert r["touched_mismatch"] == 0 and r["nproc_mismatch"] == 0
+
+
+@pytest.mark.slow
+def test_c4_full_frame_vs_oracle():
+    """Config 4 at its named size: 6M Gaussians at 3840x2160, full frame."""
+    g = scenes.synthetic_gaussians(6_000_000, seed=0)
+    cam = scenes.orbit_cameras(1, 3840, 2160, seed=0)[0]
+    r = _full_frame_check(g, cam)
+    print(f"c4: K={r['K']} max|rgb|={r['err']:.2e} depth={r['derr']:.2e} "
+          f"touched_mism={r['touched_mismatch']} nproc_mism={r['nproc_mismatch']}")
+    assert r["err"] <= IMG_TOL and r["aerr"] <= IMG_TOL and _depth_ok(r)
+    assert r["touched_mismatch"] == 0 and r["nproc_mismatch"] == 0
 
 
 @pytest.mark.parametrize("ts", [1, 5, 8, 16, 24, 32, 48, 64])
@@ -148,6 +170,29 @@ def test_tile_sizes_vs_oracle(ts):
     cam = scenes.orbit_cameras(1, 100, 70, seed=11)[0]
     r = _full_frame_check(g, cam, ts=ts, bg=(0.1, 0.2, 0.3))
     assert r["err"] <= IMG_TOL and r["touched_mismatch"] == 0 and r["nproc_mismatch"] == 0
+    assert _depth_ok(r)
+
+
+@pytest.mark.parametrize("ts", [65, 96, 128, 256, 1000])
+def test_tile_sizes_above_64_vs_oracle(ts):
+    """TileConfig accepts any tile_size >= 1 (gaussian_core.py:245-253): tiles
+    above 64 px blend as 64x64 sub-blocks that share the tile's list."""
+    g = scenes.synthetic_gaussians(20_000, seed=12)
+    cam = scenes.orbit_cameras(1, 300, 220, seed=12)[0]
+    r = _full_frame_check(g, cam, ts=ts, bg=(0.3, 0.1, 0.2))
+    assert r["err"] <= IMG_TOL and r["aerr"] <= IMG_TOL and _depth_ok(r)
+    assert r["touched_mismatch"] == 0 and r["nproc_mismatch"] == 0
+
+
+@pytest.mark.parametrize("ts,w,h", [(1, 1920, 1080), (2, 3840, 2160)])
+def test_tiny_tiles_at_full_resolution(ts, w, h):
+    """More than 2^20 tiles (2,073,600 at 1080p with 1-px tiles, 2,073,600 at
+    4K with 2-px tiles): tile ids, the K7b queue and ranges stay exact."""
+    g = scenes.synthetic_gaussians(30_000, seed=13)
+    cam = scenes.orbit_cameras(1, w, h, seed=13)[0]
+    r = _full_frame_check(g, cam, ts=ts)
+    assert r["err"] <= IMG_TOL and r["aerr"] <= IMG_TOL and _depth_ok(r)
+    assert r["touched_mismatch"] == 0 and r["nproc_mismatch"] == 0
 
 
 def _tied_depth_scene(n_run, seed=0):
@@ -178,7 +223,7 @@ def test_depth_ties_below_fp32_resolution(n_run):
     cam = look_at_camera((0.3, 0.02, -3.0), (1.0, 0.0, 5.0), up=(0, -1, 0), fov_deg=40,
                          width=96, height=64)
     r = _full_frame_check(g, cam, deg=0)
-    assert r["err"] <= IMG_TOL and r["touched_mismatch"] == 0
+    assert r["err"] <= IMG_TOL and r["touched_mismatch"] == 0 and _depth_ok(r)
 
 
 def test_empty_model_is_background():
