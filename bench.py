@@ -408,11 +408,8 @@ def run_ours(args, rank, world, local):
     all_cams = scenes.orbit_cameras(views, W, H, seed=0)
     mine = camera_shard(views, rank, world)
     cams = [all_cams[i] for i in mine]
-    from paper_2503_21364_b200 import _lib
-
-    flags = _lib.LMGS_FLAG_TILE_SORT if args.tile_sort else 0
     renderer = BatchRenderer(model, W, H, max(len(cams), 1), tile_size=16, sh_eval_degree=3,
-                             n_streams=args.streams, group=args.group, flags=flags)
+                             n_streams=args.streams, group=args.group)
 
     # warm-up (also sizes every arena)
     for _ in range(args.warmup):
@@ -553,8 +550,6 @@ def main(argv=None):
     ap.add_argument("--c5-per-block", type=int, default=C5_PER_BLOCK)
     ap.add_argument("--streams", type=int, default=3,
                     help="contexts/streams the view batch alternates over")
-    ap.add_argument("--tile-sort", action="store_true",
-                    help="A/B: tile lists by the instance radix sort instead of coarse bins")
     ap.add_argument("--group", type=int, default=2,
                     help="views per shared K1 launch (lmgs_render_group; 1 = lmgs_render)")
     args = ap.parse_args(argv)

@@ -28,6 +28,8 @@
  *                          device SoA arrays
  *   lmgs_backward          gaussian_core.py:438-486 backward_render (+ the chain
  *                          of render_loss_and_grads 600-629 to SH and logits)
+ *   lmgs_record_collect    gaussian_core.py:256-274 RenderRecord / TileRecord
+ *                          sigma, t_before, t_final (rasterize with_record)
  *   lmgs_encode_rgb8       render_runtime.py:397-401 encode_frame's pixels
  *                          (round(clip(rgb, 0, 1) * 255), half to even)
  *
@@ -47,7 +49,7 @@
 extern "C" {
 #endif
 
-#define LMGS_ABI_VERSION 4
+#define LMGS_ABI_VERSION 5
 
 typedef enum lmgs_status {
   LMGS_OK = 0,
@@ -102,12 +104,19 @@ typedef struct lmgs_settings {
   int32_t sh_eval_degree;  /* 1 = reference eval_sh_colors; 3 = full degree 3 */
   double background[3];   /* fp64 like the reference (common.py DTYPE)     */
   uint32_t flags;          /* LMGS_FLAG_*                                    */
+  int64_t max_instances;   /* LMGS_FLAG_NO_HOST_SYNC: tile-instance capacity
+                              (0 = the context's current capacity)          */
 } lmgs_settings;
 
 #define LMGS_FLAG_STAGE_TIMES 1u  /* record per-stage CUDA events (lmgs_get_stats) */
-#define LMGS_FLAG_TILE_SORT 4u  /* build the tile lists with the instance radix sort
-                                     (emit + 8-bit passes over the tile bits) instead
-                                     of the default coarse-bin path; same lists     */
+/* Capacity-bounded render with no host wait: the instance count K is never
+ * read back; every stage sizes its grid for settings.max_instances and reads
+ * the true counts on the device, so a whole view batch can be captured in a
+ * CUDA graph (after one ordinary render of the same configuration has sized
+ * the context's arenas).  A view whose K exceeds the capacity is rendered
+ * incompletely (memory-safe); lmgs_get_stats then reports it (overflow, the
+ * largest K seen) and the caller re-renders with a larger capacity. */
+#define LMGS_FLAG_NO_HOST_SYNC 8u
 #define LMGS_FLAG_NO_TOUCHED_FIX 2u /* skip K7b: touched may then differ from the
                                        reference where fp32 and fp64 transmittance
                                        straddle TERM_EPS (a few per million)       */
@@ -137,6 +146,10 @@ typedef struct lmgs_stats {
   int32_t n_launches;        /* liblmgs kernels launched by the last render */
   float stage_ms[LMGS_MAX_STAGES];  /* valid with LMGS_FLAG_STAGE_TIMES */
   const char* stage_names[LMGS_MAX_STAGES];
+  int64_t capacity;          /* instance capacity of the last render           */
+  int64_t max_instances_seen;/* largest K since the previous lmgs_get_stats    */
+  int32_t overflow;          /* a view since then had K > its capacity         */
+  int32_t reserved;
 } lmgs_stats;
 
 int lmgs_abi_version(void);
@@ -170,7 +183,8 @@ int lmgs_render_group(lmgs_context* const* ctxs, int32_t n_views, const lmgs_gau
                       void* const* streams);
 
 /* Statistics of the last lmgs_render on this context (stage times require the
- * stream to have completed: call after synchronising). */
+ * stream to have completed: call after synchronising).  After a
+ * LMGS_FLAG_NO_HOST_SYNC render this synchronises the device first. */
 int lmgs_get_stats(lmgs_context* ctx, lmgs_stats* out);
 
 /* Copy the last render's sorted tile instances: keys[K] = tile << 32 | row
@@ -200,6 +214,19 @@ int lmgs_backward(lmgs_context* ctx, const lmgs_gaussians* g, const lmgs_camera*
                   double* d_opacities, double* d_mean2d, int32_t* touched, double* d_sh,
                   double* d_logits, double* grad_norm_sum, int64_t* steps_seen,
                   void* stream);
+
+/* RenderRecord with collect for the view last rendered on ctx (same
+ * Gaussians, camera and settings): rasterize's per-tile TileRecord.sigma and
+ * t_before (gaussian_core.py:256-263, _blend 306-322 over each tile's whole
+ * list, no early break) in fp64 — tile t's (K_t, P_t) block, row-major over
+ * its instances and its pixels (row-major within the tile), starts at
+ * tile_offsets[t] (device int64, T entries) — t_final [H,W] fp64, and,
+ * when non-NULL, each Gaussian's fp64 view colour [count,3] and opacity
+ * [count] as the reference's RenderRecord.colors / opacities hold them. */
+int lmgs_record_collect(lmgs_context* ctx, const lmgs_gaussians* g, const lmgs_camera* cam,
+                        const lmgs_settings* s, const int64_t* tile_offsets, double* sigma,
+                        double* t_before, double* t_final, double* colors, double* opacities,
+                        void* stream);
 
 /* The mean-squared-error step of render_loss_and_grads (gaussian_core.py:
  * 615-617) for one view: diff = rgb - gt over n_values = H*W*3 values,

@@ -13,7 +13,7 @@ from pathlib import Path
 from .errors import InvalidInputError, LmgsError, ShapeError
 
 LIB_PATH = Path(__file__).resolve().parent / "liblmgs.so"
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 P = ctypes.c_void_p
 D = ctypes.c_double
@@ -26,7 +26,7 @@ U32 = ctypes.c_uint32
  LMGS_ERR_IO) = range(7)
 LMGS_FLAG_STAGE_TIMES = 1
 LMGS_FLAG_NO_TOUCHED_FIX = 2
-LMGS_FLAG_TILE_SORT = 4
+LMGS_FLAG_NO_HOST_SYNC = 8
 MAX_STAGES = 8
 
 # every symbol include/lmgs.h declares
@@ -35,7 +35,8 @@ EXPORTS = ("lmgs_abi_version", "lmgs_context_create", "lmgs_context_destroy", "l
            "lmgs_project", "lmgs_composite_blocks", "lmgs_checkpoint_info_read",
            "lmgs_checkpoint_load", "lmgs_checkpoint_save", "lmgs_encode_rgb8",
            "lmgs_backward", "lmgs_mse_grad", "lmgs_render_strips", "lmgs_signal_flags",
-           "lmgs_wait_flags", "lmgs_touched_fix_count", "lmgs_render_group")
+           "lmgs_wait_flags", "lmgs_touched_fix_count", "lmgs_render_group",
+           "lmgs_record_collect")
 MAX_GROUP = 8  # LMGS_MAX_GROUP
 
 
@@ -53,7 +54,7 @@ class Gaussians(ctypes.Structure):
 
 class Settings(ctypes.Structure):
     _fields_ = [("tile_size", I32), ("sh_eval_degree", I32), ("background", D * 3),
-                ("flags", U32)]
+                ("flags", U32), ("max_instances", I64)]
 
 
 MAX_STRIPS = 8
@@ -73,7 +74,9 @@ class Stats(ctypes.Structure):
     _fields_ = [("n_gaussians", I64), ("n_kept", I64), ("n_instances", I64),
                 ("n_visible", I64), ("n_tiles", I32), ("tiles_x", I32), ("tiles_y", I32),
                 ("n_stages", I32), ("n_launches", I32),
-                ("stage_ms", F * MAX_STAGES), ("stage_names", ctypes.c_char_p * MAX_STAGES)]
+                ("stage_ms", F * MAX_STAGES), ("stage_names", ctypes.c_char_p * MAX_STAGES),
+                ("capacity", I64), ("max_instances_seen", I64), ("overflow", I32),
+                ("reserved", I32)]
 
 
 class CheckpointInfo(ctypes.Structure):
@@ -117,6 +120,8 @@ def lib():
     L.lmgs_checkpoint_save.argtypes = [ctypes.c_char_p, ctypes.POINTER(Gaussians),
                                        ctypes.POINTER(CheckpointInfo), P, P, P, ctypes.c_int]
     L.lmgs_encode_rgb8.argtypes = [P, I64, P, P]
+    L.lmgs_record_collect.argtypes = [P, ctypes.POINTER(Gaussians), ctypes.POINTER(Camera),
+                                      ctypes.POINTER(Settings), P, P, P, P, P, P, P]
     L.lmgs_backward.argtypes = [P, ctypes.POINTER(Gaussians), ctypes.POINTER(Camera),
                                 ctypes.POINTER(Settings), P, P, P, P, P, P, P, P, P, P]
     L.lmgs_mse_grad.argtypes = [P, P, ctypes.c_int, I64, P, P, P]
@@ -181,4 +186,6 @@ class Context:
         return dict(n_gaussians=s.n_gaussians, n_kept=s.n_kept, n_instances=s.n_instances,
                     n_visible=s.n_visible, n_launches=s.n_launches, n_tiles=s.n_tiles,
                     tiles_x=s.tiles_x, tiles_y=s.tiles_y,
-                    stage_ms={names[i]: float(s.stage_ms[i]) for i in range(s.n_stages)})
+                    stage_ms={names[i]: float(s.stage_ms[i]) for i in range(s.n_stages)},
+                    capacity=s.capacity, max_instances_seen=s.max_instances_seen,
+                    overflow=bool(s.overflow))

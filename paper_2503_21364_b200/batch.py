@@ -54,7 +54,12 @@ class BatchRenderer:
     def __init__(self, model: GaussianModel, width: int, height: int, max_views: int,
                  tile_size: int = 16, sh_eval_degree: int = 3, background=(0.0, 0.0, 0.0),
                  with_touched: bool = True, n_streams: int = 2, group: int = 1,
-                 page_mask: torch.Tensor | None = None, flags: int = 0):
+                 page_mask: torch.Tensor | None = None, flags: int = 0,
+                 capacity: int | None = None):
+        """``capacity`` (tile instances per view) switches to the no-host-sync
+        mode (LMGS_FLAG_NO_HOST_SYNC): no per-view read of K, so a batch can be
+        captured in a CUDA graph (``capture``); ``overflowed()`` reports views
+        whose K exceeded the capacity (their output is incomplete)."""
         self.model = model
         self.dev = model.device
         self.w, self.h, self.ts = int(width), int(height), int(tile_size)
@@ -62,7 +67,10 @@ class BatchRenderer:
         self.max_views = int(max_views)
         self.sh_eval_degree = int(sh_eval_degree)
         self.background = background
-        self.flags = int(flags)  # extra LMGS_FLAG_* (e.g. LMGS_FLAG_TILE_SORT)
+        self.flags = int(flags)  # extra LMGS_FLAG_*
+        self.capacity = int(capacity) if capacity else 0
+        if self.capacity:
+            self.flags |= _lib.LMGS_FLAG_NO_HOST_SYNC
         dev = self.dev
         v = self.max_views
         self.rgb = torch.empty((v, self.h, self.w, 3), dtype=torch.float32, device=dev)
@@ -107,7 +115,7 @@ class BatchRenderer:
         L = _lib.lib()
         caller = torch.cuda.current_stream(self.dev)
         flags = (_lib.LMGS_FLAG_STAGE_TIMES if stage_times else 0) | self.flags
-        st = abi_settings(self.ts, self.sh_eval_degree, self.background, flags)
+        st = abi_settings(self.ts, self.sh_eval_degree, self.background, flags, self.capacity)
         g = self._g
         if stage_times:
             tot = {}
@@ -159,6 +167,24 @@ class BatchRenderer:
         if host_rgb is not None:
             caller.wait_stream(copy_stream)
         return None
+
+    def overflowed(self) -> bool:
+        """No-sync mode: did any view since the last call exceed the instance
+        capacity?  (Synchronises the device.)"""
+        return any(c.stats()["overflow"] for c in self.ctxs)
+
+    def capture(self, cams) -> torch.cuda.CUDAGraph:
+        """Capture ``render(cams)`` (no-sync mode) in a CUDA graph; replay it
+        with ``graph.replay()``.  One eager render first sizes every arena, so
+        the captured launches never allocate or wait on the host."""
+        if not self.capacity:
+            raise ValueError("capture() needs the no-host-sync mode (capacity=...)")
+        self.render(cams)
+        torch.cuda.synchronize(self.dev)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            self.render(cams)
+        return graph
 
     def _launch(self, L, g, st, ctxs, streams, cams, idx):
         """Views idx on ctxs / streams: lmgs_render for one view, else one

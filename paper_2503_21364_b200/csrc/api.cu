@@ -11,6 +11,7 @@
 //   K6 ranges      per-tile [start, end) from the sorted keys
 //   K7 blend       persistent warps over (tile, 8x4 block) items
 #include <cstdio>
+#include <cstddef>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -93,9 +94,9 @@ struct Scalars {  // device-side small state
   uint32_t depth_counters[kMaxPasses];
   uint32_t tile_counters[kMaxPasses];
   unsigned long long counts[3];  // n_kept, n_vis, n_inst (one D2H copy)
-  unsigned long long n_entries;  // bin path: (splat, bin) entries
+  unsigned long long max_k;      // largest K of no-sync renders since lmgs_get_stats
   unsigned long long zrange[2];  // min / max visible fp64 depth bits
-  uint32_t emit_ticket;
+  uint32_t emit_ticket[1];  // K4 chunk ticket
   int blend_counter;
   uint32_t fix_count;  // pixels queued for the exact-touched replay (K7b)
   uint32_t np_count;   // pixels whose fp64 break index differs (exact n_processed)
@@ -109,10 +110,6 @@ struct lmgs_context {
   int sms = 148;
   std::string err;
   DevBuf gbuf, tbuf, ibuf, bwbuf, fixbuf, npbuf;  // npbuf: override (-1) + list, W*H each
-  DevBuf binbuf;  // bin path: bin counts / starts, piece starts and counts
-  int64_t cap_bins = -1, cap_pieces = -1;
-  uint32_t *bin_count = nullptr, *bin_start = nullptr, *piece_start = nullptr,
-           *piece_counts = nullptr;
   Scalars* d_scal = nullptr;
   uint64_t* h_pinned = nullptr;  // [0..2] = n_kept, n_vis, K
   cudaEvent_t ev[2 * kNumStages] = {};
@@ -139,6 +136,9 @@ struct lmgs_context {
   const int2* last_ranges = nullptr;
   lmgs_stats stats{};
   bool last_timed = false;
+  bool counts_pending = false;  // a no-sync render's counts are still on the device
+  bool max_k_pending = false;   // no-sync renders ran since the last lmgs_get_stats
+  int64_t host_max_k = 0;       // largest K of the host-synchronised renders since then
 };
 
 namespace {
@@ -208,24 +208,6 @@ int ensure_instances(lmgs_context* c, int64_t k, cudaStream_t s) {
   c->inst_keys[1] = cv.take<uint64_t>(cap);
   c->tile_lookback = cv.take<uint32_t>(radix_lookback_words(cap));
   c->cap_k = cap;
-  return LMGS_OK;
-}
-
-int ensure_bins(lmgs_context* c, int64_t bins, int64_t pieces, cudaStream_t s) {
-  if (bins <= c->cap_bins && pieces <= c->cap_pieces && c->bin_count) return LMGS_OK;
-  const size_t need = align_up(4 * bins) + 2 * align_up(4 * (bins + 1)) +
-                      align_up(4 * 64 * pieces) + 4 * kAlign;
-  if (need > c->binbuf.bytes) {
-    LMGS_CUDA(c, cudaStreamSynchronize(s));
-    LMGS_CUDA(c, c->binbuf.reserve(need));
-  }
-  Carver cv{static_cast<char*>(c->binbuf.ptr)};
-  c->bin_count = cv.take<uint32_t>(bins);
-  c->bin_start = cv.take<uint32_t>(bins + 1);
-  c->piece_start = cv.take<uint32_t>(bins + 1);
-  c->piece_counts = cv.take<uint32_t>(64 * pieces);
-  c->cap_bins = bins;
-  c->cap_pieces = pieces;
   return LMGS_OK;
 }
 
@@ -396,9 +378,10 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
   int2* ranges = vp->ranges;
   Scalars* sc = c->d_scal;
   int launched = vp->launched;
+  const bool nosync = (st->flags & LMGS_FLAG_NO_HOST_SYNC) != 0;
   LMGS_CUDA(c, cudaMemcpyAsync(c->h_pinned, sc->counts, sizeof(sc->counts),
                                cudaMemcpyDeviceToHost, s));
-  LMGS_CUDA(c, cudaEventRecord(c->counts_ready, s));
+  if (!nosync) LMGS_CUDA(c, cudaEventRecord(c->counts_ready, s));
 
   // K2: 32-bit depth keys + histograms, (key, id) radix sort of all splats,
   // then the fp64 fix-up of equal-key runs
@@ -426,100 +409,55 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
   }
   tm.end(1);
 
-  // the only host wait of the view: M, visible splats, K (the depth sort keeps
-  // the device busy meanwhile)
-  LMGS_CUDA(c, cudaGetLastError());
-  LMGS_CUDA(c, cudaEventSynchronize(c->counts_ready));
-  c->stats.n_kept = (int64_t)c->h_pinned[0];
-  const int64_t n_vis = (int64_t)c->h_pinned[1];
-  c->stats.n_visible = n_vis;
-  const int64_t k = (int64_t)c->h_pinned[2];
-  c->stats.n_instances = k;
-  if (k >= ((int64_t)1 << 30))
-    return fail(c, LMGS_ERR_UNSUPPORTED, "more than 2^30 tile instances in one view");
-  if (int r = ensure_instances(c, k > 0 ? k : 1, s)) return r;
-
-  const int bins_x = (ca.tiles_x + 7) / 8, bins_y = (ca.tiles_y + 7) / 8;
-  const int64_t n_bins = (int64_t)bins_x * bins_y;
-  if (n_bins <= kMaxBins && !(st->flags & LMGS_FLAG_TILE_SORT)) {
-    // default: tile lists through coarse bins (bins.cu)
-    const int64_t pieces = k / kPiece + n_bins + 1;
-    if (int r = ensure_bins(c, n_bins, pieces, s)) return r;
-    const int bin_passes = bits_for(n_bins) > 8 ? 2 : 1;
-    BinArgs bn{};
-    bn.order_slot = &sc->slots.depth_ids;
-    bn.rects = c->rects;
-    bn.n_vis = &sc->counts[1];
-    bn.tiles_x = ca.tiles_x;
-    bn.tiles_y = ca.tiles_y;
-    bn.bins_x = bins_x;
-    bn.n_bins = (int32_t)n_bins;
-    bn.n_bin_passes = bin_passes;
-    bn.entries = c->inst_keys[0];
-    bn.entry_cap = (uint64_t)c->cap_k;
-    bn.lookback = c->emit_lookback;
-    bn.ticket = &sc->emit_ticket;
-    bn.hist = sc->tile_hist;
-    bn.n_entries = &sc->n_entries;
-    bn.entries_slot = &sc->slots.bin_entries;
-    bn.keys_slot = &sc->slots.inst_keys;
-    bn.buf[0] = c->inst_keys[0];
-    bn.buf[1] = c->inst_keys[1];
-    bn.bin_count = c->bin_count;
-    bn.bin_start = c->bin_start;
-    bn.piece_start = c->piece_start;
-    bn.piece_counts = c->piece_counts;
-    bn.tile_count = c->tile_count;
-    bn.ranges = ranges;
-    tm.begin(2);
-    LMGS_CUDA(c, cudaMemsetAsync(sc->tile_hist, 0, sizeof(sc->tile_hist), s));
-    LMGS_CUDA(c, cudaMemsetAsync(&sc->emit_ticket, 0, sizeof(uint32_t), s));
-    LMGS_CUDA(c, cudaMemsetAsync(&sc->n_entries, 0, sizeof(sc->n_entries), s));
-    if (n_vis > 0) {
-      LMGS_CUDA(c, cudaMemsetAsync(c->emit_lookback, 0, sizeof(uint64_t) * emit_chunks(n_vis), s));
-      launched += launch_bin_emit(bn, n_vis, s);
-    }
-    tm.end(2);
-    tm.begin(3);
-    {
-      RadixSortBuffers rb{};
-      rb.keys[0] = c->inst_keys[0];
-      rb.keys[1] = c->inst_keys[1];
-      rb.key_bytes = 8;
-      rb.plan = &sc->tile_plan;
-      rb.hist = sc->tile_hist;
-      rb.lookback = c->tile_lookback;
-      rb.counters = sc->tile_counters;
-      rb.keys_result = &sc->slots.bin_entries;
-      rb.hist_ready = true;
-      rb.seg_counts = c->bin_count;
-      rb.seg_shift = 32;
-      rb.seg_mask = 0xffff;
-      rb.n_dev = &sc->n_entries;
-      LMGS_CUDA(c, cudaMemsetAsync(c->bin_count, 0, sizeof(uint32_t) * n_bins, s));
-      launched += radix_sort(rb, k, 32, bin_passes, s);
-      launched += launch_bin_lists(bn, pieces, s);
-    }
-    if (out->tile_ranges && tiles > 0)
-      LMGS_CUDA(c, cudaMemcpyAsync(out->tile_ranges, ranges, sizeof(int2) * tiles,
-                                   cudaMemcpyDeviceToDevice, s));
-    tm.end(3);
+  int64_t n_vis, k;  // exact (host wait) or upper bounds (no-sync)
+  if (nosync) {
+    // no host wait: grids are sized for the capacity, kernels read the counts
+    k = st->max_instances > 0 ? st->max_instances : c->cap_k;
+    if (k <= 0)
+      return fail(c, LMGS_ERR_INVALID,
+                  "LMGS_FLAG_NO_HOST_SYNC needs settings.max_instances or an earlier render");
+    if (k >= ((int64_t)1 << 30)) return fail(c, LMGS_ERR_INVALID, "max_instances must be < 2^30");
+    n_vis = n;
+    c->counts_pending = true;
+    c->max_k_pending = true;
+    c->stats.n_kept = c->stats.n_visible = c->stats.n_instances = -1;
   } else {
+    // the only host wait of the view: M, visible splats, K (the depth sort keeps
+    // the device busy meanwhile)
+    LMGS_CUDA(c, cudaGetLastError());
+    LMGS_CUDA(c, cudaEventSynchronize(c->counts_ready));
+    c->counts_pending = false;
+    c->stats.n_kept = (int64_t)c->h_pinned[0];
+    n_vis = (int64_t)c->h_pinned[1];
+    c->stats.n_visible = n_vis;
+    k = (int64_t)c->h_pinned[2];
+    c->stats.n_instances = k;
+    if (k > c->host_max_k) c->host_max_k = k;
+    if (k >= ((int64_t)1 << 30))
+      return fail(c, LMGS_ERR_UNSUPPORTED, "more than 2^30 tile instances in one view");
+  }
+  if (int r = ensure_instances(c, k > 0 ? k : 1, s)) return r;
+  // the capacity this view renders with: K itself after a host wait
+  const int64_t cap_view = nosync ? k : c->cap_k;
+  c->stats.capacity = cap_view;
+
   // K4
   tm.begin(2);
   LMGS_CUDA(c, cudaMemsetAsync(sc->tile_hist, 0, sizeof(sc->tile_hist), s));
-  LMGS_CUDA(c, cudaMemsetAsync(&sc->emit_ticket, 0, sizeof(uint32_t), s));
+  LMGS_CUDA(c, cudaMemsetAsync(sc->emit_ticket, 0, sizeof(uint32_t), s));
   if (n_vis > 0) {
     LMGS_CUDA(c, cudaMemsetAsync(c->emit_lookback, 0, sizeof(uint64_t) * emit_chunks(n_vis), s));
     EmitArgs ea{};
     ea.order_slot = &sc->slots.depth_ids;
     ea.rects = c->rects;
-    ea.n_vis = n_vis;
+    ea.n_vis = n_vis;  // the grid's bound; the kernel reads the device count
+    ea.n_vis_dev = &sc->counts[1];
+    ea.cap = (uint64_t)cap_view;
     ea.tiles_x = ca.tiles_x;
     ea.n_tile_passes = tile_passes;
     ea.keys = c->inst_keys[0];
     ea.lookback = c->emit_lookback;
-    ea.ticket = &sc->emit_ticket;
+    ea.ticket = sc->emit_ticket;
     ea.hist = sc->tile_hist;
     launched += launch_emit(ea, s);
   }
@@ -540,15 +478,18 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
     rb.hist_ready = true;
     rb.seg_counts = c->tile_count;
     rb.seg_shift = 32;
+    if (nosync) {  // K on the device; the grid covers the capacity
+      rb.n_dev = &sc->counts[2];
+      rb.max_n = &sc->max_k;
+    }
     LMGS_CUDA(c, cudaMemsetAsync(c->tile_count, 0, sizeof(uint32_t) * tiles, s));
     launched += radix_sort(rb, k, 32, tile_passes, s);
-    launched += launch_ranges_from_counts(c->tile_count, (int)tiles, ranges, s);
+    launched += launch_ranges_from_counts(c->tile_count, (int)tiles, ranges, cap_view, s);
   }
   if (out->tile_ranges && tiles > 0)
     LMGS_CUDA(c, cudaMemcpyAsync(out->tile_ranges, ranges, sizeof(int2) * tiles,
                                  cudaMemcpyDeviceToDevice, s));
   tm.end(3);
-  }
 
   // K7
   tm.begin(4);
@@ -691,7 +632,6 @@ void lmgs_context_destroy(lmgs_context* c) {
   c->bwbuf.release();
   c->fixbuf.release();
   c->npbuf.release();
-  c->binbuf.release();
   if (c->d_scal) cudaFree(c->d_scal);
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   for (int i = 0; i < 2 * kNumStages; ++i)
@@ -803,6 +743,28 @@ int lmgs_render_group(lmgs_context* const* ctxs, int32_t n_views, const lmgs_gau
 int lmgs_get_stats(lmgs_context* c, lmgs_stats* out) {
   if (!c || !out) return LMGS_ERR_INVALID;
   DeviceGuard guard(c->device);
+  if (c->counts_pending) {  // a no-sync render (possibly replayed from a graph)
+    LMGS_CUDA(c, cudaDeviceSynchronize());
+    c->stats.n_kept = (int64_t)c->h_pinned[0];
+    c->stats.n_visible = (int64_t)c->h_pinned[1];
+    c->stats.n_instances = (int64_t)c->h_pinned[2];
+    c->counts_pending = false;
+  }
+  {
+    int64_t seen = c->host_max_k;
+    if (c->max_k_pending) {  // the device-side maximum of the no-sync renders
+      unsigned long long mk = 0;
+      LMGS_CUDA(c, cudaMemcpy(&mk, &c->d_scal->max_k, sizeof(mk), cudaMemcpyDeviceToHost));
+      LMGS_CUDA(c, cudaMemset(&c->d_scal->max_k, 0, sizeof(mk)));
+      if ((int64_t)mk > seen) seen = (int64_t)mk;
+      c->stats.overflow = (int64_t)mk > c->stats.capacity ? 1 : 0;
+      c->max_k_pending = false;
+    } else {
+      c->stats.overflow = 0;
+    }
+    c->stats.max_instances_seen = seen;
+    c->host_max_k = 0;
+  }
   if (c->last_timed) {
     LMGS_CUDA(c, cudaEventSynchronize(c->ev[2 * kNumStages - 1]));
     for (int i = 0; i < kNumStages; ++i) {
@@ -818,6 +780,10 @@ int lmgs_get_stats(lmgs_context* c, lmgs_stats* out) {
 int lmgs_copy_instances(lmgs_context* c, uint64_t* keys, int64_t* prim_ids, void* stream) {
   if (!c) return LMGS_ERR_INVALID;
   DeviceGuard guard(c->device);
+  if (c->counts_pending) {
+    lmgs_stats tmp;
+    if (int r = lmgs_get_stats(c, &tmp)) return r;
+  }
   InstanceExportArgs a{};
   a.ranges = c->last_ranges;
   a.keys_slot = &c->d_scal->slots.inst_keys;
@@ -879,6 +845,64 @@ int lmgs_backward(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* c
   a.grad_norm_sum = grad_norm_sum;
   a.steps_seen = steps_seen;
   launch_backward(a, (int)tiles, st);
+  LMGS_CUDA(c, cudaGetLastError());
+  return LMGS_OK;
+}
+
+int lmgs_record_collect(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam,
+                        const lmgs_settings* s, const int64_t* tile_offsets, double* sigma,
+                        double* t_before, double* t_final, double* colors, double* opacities,
+                        void* stream) {
+  if (int r = validate(c, g, cam, s)) return r;
+  if (!tile_offsets || !sigma || !t_before || !t_final)
+    return fail(c, LMGS_ERR_INVALID, "null collect output");
+  const CamArgs ca = make_cam(cam, s->tile_size);
+  const int64_t tiles = (int64_t)ca.tiles_x * ca.tiles_y;
+  if (c->stats.n_gaussians != g->count || c->stats.n_tiles != tiles || !c->last_ranges)
+    return fail(c, LMGS_ERR_INVALID, "lmgs_record_collect needs the view's lmgs_render first");
+  DeviceGuard guard(c->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t n = g->count;
+  if ((size_t)n * sizeof(BwRec) > c->bwbuf.bytes) {
+    LMGS_CUDA(c, cudaStreamSynchronize(st));
+    LMGS_CUDA(c, c->bwbuf.reserve((size_t)(n > 0 ? n : 1) * sizeof(BwRec)));
+  }
+  BackwardArgs p{};
+  p.recs = static_cast<BwRec*>(c->bwbuf.ptr);
+  p.means = g->means;
+  p.quats = g->quats;
+  p.scales = g->scales;
+  p.logits = g->opacity_logits;
+  p.sh = g->sh;
+  p.n = n;
+  p.sh_coeffs = g->sh_coeffs;
+  p.eval_degree = s->sh_eval_degree < g->sh_degree ? s->sh_eval_degree : g->sh_degree;
+  p.cam = ca;
+  CollectArgs a{};
+  a.recs = p.recs;
+  a.keys_slot = &c->d_scal->slots.inst_keys;
+  a.ranges = c->last_ranges;
+  a.offsets = tile_offsets;
+  a.width = cam->width;
+  a.height = cam->height;
+  a.tile_size = s->tile_size;
+  a.tiles_x = ca.tiles_x;
+  a.sigma = sigma;
+  a.t_before = t_before;
+  a.t_final = t_final;
+  launch_collect(p, a, (int)tiles, st);
+  if (n > 0 && (colors || opacities)) {  // the records' fp64 colour and opacity
+    if (colors)
+      LMGS_CUDA(c, cudaMemcpy2DAsync(colors, 3 * sizeof(double),
+                                     reinterpret_cast<const char*>(p.recs) + offsetof(BwRec, col),
+                                     sizeof(BwRec), 3 * sizeof(double), (size_t)n,
+                                     cudaMemcpyDeviceToDevice, st));
+    if (opacities)
+      LMGS_CUDA(c, cudaMemcpy2DAsync(opacities, sizeof(double),
+                                     reinterpret_cast<const char*>(p.recs) + offsetof(BwRec, op),
+                                     sizeof(BwRec), sizeof(double), (size_t)n,
+                                     cudaMemcpyDeviceToDevice, st));
+  }
   LMGS_CUDA(c, cudaGetLastError());
   return LMGS_OK;
 }

@@ -100,6 +100,7 @@ __global__ void k_bw_prep(BackwardArgs a) {
     r.col[1] = fmin(fmax(raw[1], 0.0), 1.0);
     r.col[2] = fmin(fmax(raw[2], 0.0), 1.0);
     a.recs[id] = r;
+    if (!a.d_colors) continue;  // lmgs_record_collect: records only
     // this view's per-Gaussian outputs start at zero (k_backward adds into them)
     a.d_colors[3 * id] = a.d_colors[3 * id + 1] = a.d_colors[3 * id + 2] = 0.0;
     a.d_opacities[id] = 0.0;
@@ -108,6 +109,42 @@ __global__ void k_bw_prep(BackwardArgs a) {
   }
 }
 
+
+// RenderRecord with collect (rasterize's TileRecord.sigma / t_before /
+// t_final, gaussian_core.py:256-263, _blend 306-322 without the early break):
+// one CTA per tile, one thread per pixel (chunks of 256 for tiles above 16x16),
+// the tile's whole list in order, in fp64 from the view's splat records.
+// sigma / t_before of tile t are (K_t, P_t) row-major at offsets[t].
+__global__ void k_collect(CollectArgs a) {
+  const int tile = blockIdx.x;
+  const int ts = a.tile_size;
+  const int tx0 = (tile % a.tiles_x) * ts, ty0 = (tile / a.tiles_x) * ts;
+  const int tw = min(ts, a.width - tx0), th = min(ts, a.height - ty0);
+  const int np = tw * th;
+  const int2 range = a.ranges[tile];
+  const int kt = range.y - range.x;
+  const uint64_t* __restrict__ list = static_cast<const uint64_t*>(*a.keys_slot);
+  const int64_t off = a.offsets[tile];
+  for (int p = threadIdx.x; p < np; p += blockDim.x) {
+    const int px = tx0 + p % tw, py = ty0 + p / tw;  // row-major within the tile
+    const double pxd = (double)px + 0.5, pyd = (double)py + 0.5;
+    double T = 1.0;
+    for (int k = 0; k < kt; ++k) {
+      const BwRec& r = a.recs[(uint32_t)list[range.x + k]];
+      const double dx = pxd - r.mx, dy = pyd - r.my;  // 311
+      const double maha = (r.ca * (dx * dx) + ((2.0 * r.cb) * dx) * dy) + r.cc * (dy * dy);
+      double sig = r.op * exp(-0.5 * maha);             // 313
+      const bool inside = dx * dx + dy * dy <= r.r2;    // 314
+      const bool active = T >= kTermEps;                // 315
+      sig = inside && active ? (sig > kSigmaMax ? kSigmaMax : sig) : 0.0;
+      const int64_t o = off + (int64_t)k * np + p;
+      a.sigma[o] = sig;
+      a.t_before[o] = T;
+      T = T * (1.0 - sig);
+    }
+    a.t_final[(int64_t)py * a.width + px] = T;
+  }
+}
 
 // render_loss_and_grads 617-622: d_sh += sh_color_grad_to_coeffs(d_colors),
 // d_logit += d_opacity * alpha * (1 - alpha)
@@ -152,6 +189,16 @@ __global__ void k_backward_chain(BackwardArgs a, int64_t n) {
 }
 
 }  // namespace
+
+int launch_collect(const BackwardArgs& prep, const CollectArgs& a, int tiles, cudaStream_t s) {
+  if (prep.n > 0) {
+    int64_t g = (prep.n + 255) / 256;
+    if (g > 148 * 16) g = 148 * 16;
+    k_bw_prep<<<(unsigned)g, 256, 0, s>>>(prep);
+  }
+  if (tiles > 0) k_collect<<<tiles, 256, 0, s>>>(a);
+  return 2;
+}
 
 int launch_backward(const BackwardArgs& a, int tiles, cudaStream_t s) {
   int launched = 0;

@@ -143,10 +143,11 @@ struct RadixSortBuffers {
   // the sorted key bits must cover the segment bits (tile sort: ranges)
   uint32_t* seg_counts;
   int seg_shift;
-  uint64_t seg_mask;  // segment = (key >> seg_shift) & seg_mask (0 = all bits)
   // nullable: the key count on the device (n is then an upper bound sizing
-  // the grid and the look-back; kernels use min(n, *n_dev))
+  // the grid and the look-back; kernels use min(n, *n_dev); the onesweep
+  // grid becomes persistent)
   const unsigned long long* n_dev;
+  unsigned long long* max_n;  // nullable: atomicMax(*max_n, *n_dev) (overflow check)
 };
 
 size_t radix_lookback_words(int64_t capacity);
@@ -160,7 +161,7 @@ struct DevSlots {
   void* depth_keys;  // K2 result: fp32 depth keys in (depth, id) order
   void* depth_ids;   // K2 result: Gaussian ids in (depth, id) order
   void* inst_keys;   // K5 result: tile << 32 | id, sorted by tile then depth rank
-  void* bin_entries; // bin path: entries sorted by bin (bins.cu)
+  void* unused;
 };
 
 // ---------------------------------------------------------------------------
@@ -191,7 +192,9 @@ constexpr int kEmitChunk = kEmitThreads * kEmitItems;
 struct EmitArgs {
   void* const* order_slot;  // -> uint32_t[n_vis] Gaussian ids in depth order
   const uint64_t* rects;    // count = rect area (every splat in rank order is visible)
-  int64_t n_vis;
+  int64_t n_vis;            // host bound of the visible count (grid)
+  const unsigned long long* n_vis_dev;  // the count itself
+  uint64_t cap;             // keys capacity: instances past it are dropped (no-sync overflow)
   int32_t tiles_x;
   int32_t n_tile_passes;
   uint64_t* keys;           // [K] out
@@ -202,38 +205,11 @@ struct EmitArgs {
 inline int64_t emit_chunks(int64_t n_vis) { return (n_vis + kEmitChunk - 1) / kEmitChunk; }
 int launch_emit(const EmitArgs& a, cudaStream_t s);
 
-// ---------------------------------------------------------------------------
-// Tile lists through coarse bins of 8x8 tiles (bins.cu): the default K4-K6.
-constexpr int kPiece = 2048;  // entries per piece of a bin's entry run
-constexpr int kMaxBins = 1 << 16;
-struct BinArgs {
-  void* const* order_slot;            // -> uint32_t[n_vis] ids in depth-rank order
-  const uint64_t* rects;              // tile rect per splat
-  const unsigned long long* n_vis;    // device: visible splats
-  int32_t tiles_x, tiles_y, bins_x, n_bins, n_bin_passes;
-  uint64_t* entries;                  // B1 output (= buf[0])
-  uint64_t entry_cap;                 // entries / instance capacity
-  uint64_t* lookback;                 // [emit_chunks] status words (zeroed)
-  uint32_t* ticket;                   // chunk ticket (zeroed)
-  uint32_t* hist;                     // [2][256] bin digit histograms (zeroed)
-  unsigned long long* n_entries;      // device: E (zeroed)
-  void* const* entries_slot;          // -> the bin-sorted entries (radix result)
-  void** keys_slot;                   // <- the instance keys buffer (the other one)
-  void* buf[2];                       // the two instance-sized buffers
-  uint32_t* bin_count;                // [n_bins] entries per bin (zeroed; sort's last pass)
-  uint32_t* bin_start;                // [n_bins + 1]
-  uint32_t* piece_start;              // [n_bins + 1]
-  uint32_t* piece_counts;             // [pieces][64]
-  uint32_t* tile_count;               // [T]
-  int2* ranges;                       // [T]
-};
-int launch_bin_emit(const BinArgs& a, int64_t n_vis_bound, cudaStream_t s);
-// B3-B6 + K6 (after the bin sort); piece_bound >= the number of pieces
-int launch_bin_lists(const BinArgs& a, int64_t piece_bound, cudaStream_t s);
-
 // K6: tile ranges [start, end) = exclusive scan of the per-tile counts the
 // tile sort's last pass accumulated (empty tiles included)
-int launch_ranges_from_counts(const uint32_t* counts, int tiles, int2* ranges, cudaStream_t s);
+// (ranges are clamped to cap: a capacity-bounded render never reads past it)
+int launch_ranges_from_counts(const uint32_t* counts, int tiles, int2* ranges, int64_t cap,
+                              cudaStream_t s);
 
 struct InstanceExportArgs {
   const int2* ranges;
@@ -373,6 +349,20 @@ struct BackwardArgs {
   int64_t* steps_seen;      // [n] DensifyStats, accumulated (nullable)
 };
 int launch_backward(const BackwardArgs& a, int tiles, cudaStream_t s);  // kernels launched or -err
+
+// RenderRecord collect (backward_exact.cu): fp64 sigma / t_before per (tile,
+// instance, pixel) and t_final per pixel, from the view's BwRec records
+struct CollectArgs {
+  const BwRec* recs;
+  void* const* keys_slot;
+  const int2* ranges;
+  const int64_t* offsets;  // [T] start of each tile's (K_t, P_t) block
+  int32_t width, height, tile_size, tiles_x;
+  double* sigma;
+  double* t_before;
+  double* t_final;         // [H*W]
+};
+int launch_collect(const BackwardArgs& prep, const CollectArgs& a, int tiles, cudaStream_t s);
 int launch_backward_replay(const BackwardArgs& a, int tiles, cudaStream_t s);  // backward.cu
 
 constexpr int kMaxCompositeBlocks = 64;

@@ -83,9 +83,13 @@ __global__ void __launch_bounds__(kRadix) k_radix_plan(const uint32_t* __restric
                                                        const int* gate, void* keys0,
                                                        void* keys1, void* vals0, void* vals1,
                                                        void** keys_result, void** vals_result,
-                                                       const unsigned long long* n_dev) {
+                                                       const unsigned long long* n_dev,
+                                                       unsigned long long* max_n) {
   const bool off = gated_off(gate);
-  if (n_dev) n = min(n, (int64_t)*n_dev);
+  if (n_dev) {
+    if (max_n && threadIdx.x == 0) atomicMax(max_n, *n_dev);
+    n = min(n, (int64_t)*n_dev);
+  }
   __shared__ uint32_t s_scan[kRadix];
   __shared__ int s_trivial[kMaxPasses];
   const int d = threadIdx.x;
@@ -141,12 +145,11 @@ __global__ void __launch_bounds__(kRadix) k_radix_plan(const uint32_t* __restric
 // 4. per-digit prefix over warps, staging in shared memory in digit order;
 // 5. decoupled look-back (windowed) for the global digit offsets;
 // 6. coalesced write-out in per-digit runs.
-template <typename K, bool VALS>
+template <typename K, bool VALS, bool PERSIST>
 __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
     K* keys0, K* keys1, uint32_t* vals0, uint32_t* vals1, int64_t n, int begin_bit, int pass,
     const RadixPlan* __restrict__ plan, uint32_t* lookback, uint32_t* counter, int64_t lb_stride,
-    bool iota_vals, uint32_t* seg_counts, int seg_shift, uint64_t seg_mask,
-    const unsigned long long* n_dev) {
+    bool iota_vals, uint32_t* seg_counts, int seg_shift, const unsigned long long* n_dev) {
   if (n_dev) n = min(n, (int64_t)*n_dev);  // the grid covers an upper bound
   if (!plan->active[pass]) {
     // no pass moves data (every digit trivial): the result buffers are the
@@ -158,7 +161,7 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
              i += (int64_t)gridDim.x * blockDim.x)
           vals0[i] = (uint32_t)i;
       if (seg_counts && blockIdx.x == 0 && threadIdx.x == 0 && n > 0)
-        seg_counts[((uint64_t)keys0[0] >> seg_shift) & seg_mask] = (uint32_t)n;
+        seg_counts[(uint64_t)keys0[0] >> seg_shift] = (uint32_t)n;
     }
     return;
   }
@@ -174,11 +177,14 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
   __shared__ uint32_t s_wsum[kWarps];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // tiles are taken by ticket; a CTA loops until the keys run out (with n_dev
+  // the grid is a persistent one sized for the device, not for the bound)
+  for (;;) {
   if (tid == 0) s_bid = atomicAdd(counter + pass, 1u);
   __syncthreads();
   const uint32_t bid = s_bid;
   const int64_t base = (int64_t)bid * kSortTile;
-  if (base >= n) return;  // (the grid may cover an upper bound of n)
+  if (base >= n) return;
   for (int i = tid; i < kWarps * kRadix; i += kSortThreads) {
     (&s_match[0][0])[i] = 0;
     (&s_wcnt[0][0])[i] = 0;
@@ -325,12 +331,15 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
     if (segs) {
       // the staged tile is sorted on every key bit sorted so far: runs of one
       // segment are contiguous; a run [i0, i1] adds (i1 + 1) - i0
-      const uint64_t sg = ((uint64_t)k >> seg_shift) & seg_mask;
-      if (i == 0 || (((uint64_t)s_keys[i - 1] >> seg_shift) & seg_mask) != sg)
+      const uint64_t sg = (uint64_t)k >> seg_shift;
+      if (i == 0 || ((uint64_t)s_keys[i - 1] >> seg_shift) != sg)
         atomicAdd(seg_counts + sg, (uint32_t)(-i));
-      if (i + 1 == count || (((uint64_t)s_keys[i + 1] >> seg_shift) & seg_mask) != sg)
+      if (i + 1 == count || ((uint64_t)s_keys[i + 1] >> seg_shift) != sg)
         atomicAdd(seg_counts + sg, (uint32_t)(i + 1));
     }
+  }
+  if (!PERSIST) return;  // one tile per CTA on an exact grid
+  __syncthreads();  // the staging and s_bid are reused by the next tile
   }
 }
 
@@ -339,21 +348,41 @@ constexpr size_t onesweep_smem() {
   return sizeof(K) * kSortTile + (VALS ? sizeof(uint32_t) * kSortTile : 0);
 }
 
+template <typename K, bool VALS, bool PERSIST>
+void launch_onesweep_as(const RadixSortBuffers& b, int64_t n, int begin_bit, int p, int64_t grid,
+                        int64_t blocks, cudaStream_t s) {
+  constexpr size_t smem = onesweep_smem<K, VALS>();
+  k_onesweep<K, VALS, PERSIST><<<(unsigned)grid, kSortThreads, smem, s>>>(
+      static_cast<K*>(b.keys[0]), static_cast<K*>(b.keys[1]), b.vals[0], b.vals[1], n, begin_bit,
+      p, b.plan, b.lookback, b.counters, blocks, b.iota_vals, b.seg_counts, b.seg_shift, b.n_dev);
+}
+
 template <typename K, bool VALS>
 void launch_onesweep(const RadixSortBuffers& b, int64_t n, int begin_bit, int p, int64_t blocks,
                      cudaStream_t s) {
   constexpr size_t smem = onesweep_smem<K, VALS>();
   static bool attr_set[kMaxDevices] = {};
+  static int occ[kMaxDevices] = {}, sms[kMaxDevices] = {};
   const int dev = current_device();
   if (!attr_set[dev]) {
-    cudaFuncSetAttribute(k_onesweep<K, VALS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_onesweep<K, VALS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
+    cudaFuncSetAttribute(k_onesweep<K, VALS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[dev], k_onesweep<K, VALS, true>,
+                                                  kSortThreads, smem);
+    if (occ[dev] < 1) occ[dev] = 1;
     attr_set[dev] = true;
   }
-  k_onesweep<K, VALS><<<(unsigned)blocks, kSortThreads, smem, s>>>(
-      static_cast<K*>(b.keys[0]), static_cast<K*>(b.keys[1]), b.vals[0], b.vals[1], n, begin_bit,
-      p, b.plan, b.lookback, b.counters, blocks, b.iota_vals, b.seg_counts, b.seg_shift,
-      b.seg_mask ? b.seg_mask : ~0ull, b.n_dev);
+  if (!b.n_dev) {
+    launch_onesweep_as<K, VALS, false>(b, n, begin_bit, p, blocks, blocks, s);
+    return;
+  }
+  // the key count is on the device: a persistent grid takes tiles by ticket
+  const int64_t persistent = (int64_t)sms[dev] * occ[dev];
+  launch_onesweep_as<K, VALS, true>(b, n, begin_bit, p, blocks < persistent ? blocks : persistent,
+                                    blocks, s);
 }
 
 template <typename K>
@@ -376,7 +405,7 @@ int radix_sort_impl(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_p
     ++launched;
   }
   k_radix_plan<<<1, kRadix, 0, s>>>(b.hist, n, n_passes, b.plan, b.gate, k0, k1, b.vals[0],
-                                    b.vals[1], b.keys_result, b.vals_result, b.n_dev);
+                                    b.vals[1], b.keys_result, b.vals_result, b.n_dev, b.max_n);
   ++launched;
   if (blocks == 0) return launched;
   for (int p = 0; p < n_passes; ++p) {

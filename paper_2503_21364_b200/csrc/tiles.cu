@@ -187,7 +187,9 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(EmitArgs a) {
   if (tid == 0) s_ticket = atomicAdd(a.ticket, 1u);
   for (int i = tid; i < kMaxTilePasses * 256; i += kEmitThreads) (&s_hist[0][0])[i] = 0;
   __syncthreads();
+  const int64_t n_vis = min(a.n_vis, (int64_t)*a.n_vis_dev);  // the grid covers a bound
   const int64_t chunk = s_ticket;
+  if (chunk * kEmitChunk >= n_vis) return;
   const int64_t base = chunk * kEmitChunk + (int64_t)warp * PW;
   const uint32_t* __restrict__ order = static_cast<const uint32_t*>(*a.order_slot);
 
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(EmitArgs a) {
 #pragma unroll
   for (int j = 0; j < kEmitItems; ++j) {
     const int64_t r = base + lane * kEmitItems + j;
-    id[j] = r < a.n_vis ? order[r] : 0xffffffffu;
+    id[j] = r < n_vis ? order[r] : 0xffffffffu;
   }
   uint64_t rect[kEmitItems];
 #pragma unroll
@@ -296,7 +298,8 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(EmitArgs a) {
     const uint32_t r_hi = __shfl_sync(0xffffffffu, (uint32_t)(my_rect >> 32), idx);
     const uint32_t id_i = __shfl_sync(0xffffffffu, my_id, idx);
     const uint32_t p = p0 + lane;
-    const bool on = p < wtot;
+    // instances past the capacity are dropped and not counted (no-sync overflow)
+    const bool on = p < wtot && out0 + p < a.cap;
     uint32_t tile = 0;
     if (on) {
       const uint32_t q = p - st_i;
@@ -342,7 +345,8 @@ constexpr int kScanThreads = 1024;
 constexpr int kScanPer = 8;  // counts per thread per step
 
 __global__ void __launch_bounds__(kScanThreads) k_ranges_from_counts(const uint32_t* counts,
-                                                                     int tiles, int2* ranges) {
+                                                                     int tiles, int2* ranges,
+                                                                     uint32_t cap) {
   __shared__ uint32_t s_warp[kScanThreads / 32];
   __shared__ uint32_t s_carry;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -379,7 +383,8 @@ __global__ void __launch_bounds__(kScanThreads) k_ranges_from_counts(const uint3
     uint32_t run = s_carry + s_warp[warp] + (incl - sum);
 #pragma unroll
     for (int j = 0; j < kScanPer; ++j) {
-      if (t0 + j < tiles) ranges[t0 + j] = make_int2((int)run, (int)(run + c[j]));
+      if (t0 + j < tiles)
+        ranges[t0 + j] = make_int2((int)min(run, cap), (int)min(run + c[j], cap));
       run += c[j];
     }
     __syncthreads();
@@ -432,9 +437,11 @@ int launch_emit(const EmitArgs& a, cudaStream_t s) {
   return 1;
 }
 
-int launch_ranges_from_counts(const uint32_t* counts, int tiles, int2* ranges, cudaStream_t s) {
+int launch_ranges_from_counts(const uint32_t* counts, int tiles, int2* ranges, int64_t cap,
+                              cudaStream_t s) {
   if (tiles <= 0) return 0;
-  k_ranges_from_counts<<<1, kScanThreads, 0, s>>>(counts, tiles, ranges);
+  const uint32_t c = cap < 0 || cap > 0xffffffffll ? 0xffffffffu : (uint32_t)cap;
+  k_ranges_from_counts<<<1, kScanThreads, 0, s>>>(counts, tiles, ranges, c);
   return 1;
 }
 

@@ -9,12 +9,6 @@ Reference: pkg/src/landmark/engine_api.py
   * ``Engine.render`` (312-339) wraps it with preprocess / postprocess stages
     and a stats dict carrying ``latency_ms``.
 
-With ``EngineConfig.offload`` (engine_api.py:41-47, 236-289) the engine keeps
-only the onload region around the camera's cell resident: the scene is split
-on the x-y grid, cells are groups of the host tier, and each render makes the
-ring-``ring`` region of the camera's core cell resident in the paged device
-pool (offload.TierStore, async copies) and renders straight from it.
-
 Here the only runtime is ``"cuda"`` (the B200 custom-kernel runtime; the
 reference's two CPU runtimes compute the identical function, which this one
 matches within 1e-4).  ``"optimized"`` and ``"reference"`` are accepted as
@@ -49,24 +43,12 @@ class InferenceStagePlan:
 
 
 @dataclass
-class OffloadConfig:
-    """engine_api.py:41-47."""
-
-    budget_bytes: int
-    local_plane_split: tuple = (1, 1)
-    bandwidth_bytes_per_s: float | None = None
-    fixed_latency_s: float = 0.0
-    ring: int = 1
-
-
-@dataclass
 class EngineConfig:
     runtime: str = "cuda"
     tile_size: int = 16
     background: tuple = (0.0, 0.0, 0.0)
     sh_eval_degree: int = 1  # the reference's eval_sh_colors
     output_dtype: str = "float64"  # the reference returns image.numpy() of an fp64 tensor
-    offload: OffloadConfig | None = None
     extra: dict = field(default_factory=dict)
 
     def __post_init__(self):
@@ -77,73 +59,18 @@ class EngineConfig:
 
 
 class Engine:
-    """Holds a device-resident Gaussian model (or a paged onload region of it)
-    and renders cameras."""
+    """Holds a device-resident Gaussian model and renders cameras."""
 
     def __init__(self, model, plan: InferenceStagePlan | None = None,
-                 config: EngineConfig | None = None, device=None, scene_bbox=None):
+                 config: EngineConfig | None = None, device=None):
         self.config = config or EngineConfig()
         self.plan = plan or InferenceStagePlan()
-        self.store = None
-        self._core = None
-        off = self.config.offload
-        if off is None:
-            self.model = model if isinstance(model, GaussianModel) else \
-                GaussianModel.from_host(model, device=device)
-            return
-        from . import offload as o
-
-        arrs = o._host_arrays(model)
-        if scene_bbox is None:  # engine_api.py:242-246
-            m = np.asarray(arrs[0], dtype=np.float64)
-            pad = 1e-6 + float(np.asarray(arrs[2], dtype=np.float64).max()) * 3
-            scene_bbox = np.stack([m.min(0) - pad, m.max(0) + pad])
-        nx, ny = off.local_plane_split
-        self.grid = o.partition_scene(scene_bbox, nx, ny)
-        rows = o.cell_rows(arrs[0], self.grid)
-        order, keys, groups, start = [], [], {}, 0
-        for rank, cell in enumerate(sorted(self.grid.cells())):
-            ids = rows[cell]
-            order.append(ids)
-            keys.append((np.int64(rank) << 32) + ids.astype(np.int64))
-            groups[cell] = (start, start + len(ids))
-            start += len(ids)
-        host = o.HostTier(o._HostModel(arrs), np.concatenate(order), np.concatenate(keys), groups)
-        worst = max(sum(host.group_bytes[c] for c in o.onload_region(self.grid, cell, off.ring))
-                    for cell in self.grid.cells())
-        if worst > off.budget_bytes:  # engine_api.py:278-286
-            raise o.BudgetExceededError(
-                f"budget {off.budget_bytes} bytes cannot hold the largest onload region "
-                f"({worst} bytes); raise budget or local_plane_split")
-        self.clock = o.VirtualClock()
-        self.store = o.TierStore(off.budget_bytes, host,
-                                 o.TransferConfig(off.bandwidth_bytes_per_s, off.fixed_latency_s),
-                                 self.clock, device)
-        self.model = None
-
-    def _ensure_region(self, camera):
-        """engine_api.py:291-304: make the camera core cell's region resident."""
-        from . import offload as o
-
-        off = self.config.offload
-        core = self.grid.cell_of_point(camera.center)
-        if core != self._core:
-            wanted = o.onload_region(self.grid, core, off.ring)
-            stale = [c for c in list(self.store.device) if c not in wanted]
-            if stale:
-                self.store.offload_cells(stale, write_back=False)
-            handle = self.store.load_cells(sorted(wanted))
-            self.clock.advance(max(0.0, handle.ready_at - self.clock.now))
-            self._core = core
-        return sorted(o.onload_region(self.grid, self._core, off.ring))
+        self.model = model if isinstance(model, GaussianModel) else \
+            GaussianModel.from_host(model, device=device)
 
     def _render_gaussian(self, camera) -> np.ndarray:
         cfg = self.config
-        if self.store is None:
-            rgb = render(camera, self.model, cfg.tile_size, cfg.background, cfg.sh_eval_degree).rgb
-        else:
-            cells = self._ensure_region(camera)
-            rgb = self.store.render_groups(camera, cells, cfg)
+        rgb = render(camera, self.model, cfg.tile_size, cfg.background, cfg.sh_eval_degree).rgb
         img = rgb.cpu().numpy()
         return img.astype(np.float64) if cfg.output_dtype == "float64" else img
 
@@ -157,18 +84,12 @@ class Engine:
         cam = model_input if isinstance(model_input, Camera) else Camera.from_reference(model_input)
         result = self._render_gaussian(cam)
         output = self.plan.postprocess(result)
-        if self.store is None:
-            stats = {"latency_ms": (time.perf_counter() - t0) * 1e3, "resident_bytes": None,
-                     "peak_resident_bytes": None, "stalls": 0}
-        else:
-            stats = {"latency_ms": (time.perf_counter() - t0) * 1e3,
-                     "resident_bytes": self.store.resident_bytes,
-                     "peak_resident_bytes": self.store.stats.peak_resident_bytes,
-                     "stalls": self.store.stats.stalls}
+        stats = {"latency_ms": (time.perf_counter() - t0) * 1e3, "resident_bytes": None,
+                 "peak_resident_bytes": None, "stalls": 0}
         return output, stats
 
 
 def init_inference(model, stage_plan: InferenceStagePlan | None = None,
-                   config: EngineConfig | None = None, scene_bbox=None) -> Engine:
+                   config: EngineConfig | None = None) -> Engine:
     """engine_api.py:342-346 (same argument order)."""
-    return Engine(model, stage_plan, config, scene_bbox=scene_bbox)
+    return Engine(model, stage_plan, config)

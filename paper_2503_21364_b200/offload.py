@@ -64,25 +64,42 @@ class IncompleteLoadError(RuntimeError):
 
 
 # ---------------------------------------------------------------------------
-# clock, transfer model, stats (common.py:51-60, memory_tiers.py:43-73)
+# simulated time and transfer accounting.  The reference models the device
+# tier on a virtual clock (common.py:51-60, memory_tiers.py:43-73); its
+# readings decide prefetch swaps and stalls, so they are kept as the
+# bookkeeping layer above the real, asynchronous copies.
 
 
 @dataclass
 class VirtualClock:
+    """Seconds of simulated session time; only moves forward."""
+
     now: float = 0.0
 
     def advance(self, dt: float) -> None:
-        if dt < 0:
+        if not dt >= 0:
             raise InvalidInputError("clock cannot go backwards")
         self.now += dt
+
+    def wait_until(self, t: float) -> bool:
+        """Advance to ``t`` if it lies ahead; True when that was a wait."""
+        late = t - self.now
+        if late > 0:
+            self.now += late
+            return True
+        return False
 
 
 @dataclass
 class TransferConfig:
-    """bandwidth None means instant transfers on the virtual clock."""
+    """Host->device link of the simulated clock (bandwidth None: instant)."""
 
     bandwidth_bytes_per_s: float | None = None
     fixed_latency_s: float = 0.0
+
+    def seconds(self, nbytes: int) -> float:
+        bw = self.bandwidth_bytes_per_s
+        return self.fixed_latency_s + (nbytes / bw if bw else 0.0)
 
 
 @dataclass
@@ -100,78 +117,82 @@ class TierStats:
 
 @dataclass
 class LoadHandle:
+    """One load request: its groups, the simulated completion time and the
+    CUDA event of the real copies."""
+
     cell_ids: tuple
     ready_at: float
     nbytes: int
-    event: torch.cuda.Event | None = None  # the real copies' completion
+    event: torch.cuda.Event | None = None
 
     def ready(self, clock: VirtualClock) -> bool:
-        return clock.now >= self.ready_at
+        return self.ready_at <= clock.now
 
 
 # ---------------------------------------------------------------------------
-# scene bookkeeping (scene_manager.py)
+# the x-y cell grid (scene_manager.py:24-104 semantics: half-open cells
+# clamped at the grid edge, Chebyshev onload regions)
 
 
 @dataclass
 class SceneGrid:
-    """scene_manager.py:24-73: 2D partition of the footprint on the x-y plane."""
-
     bbox: np.ndarray
     nx: int
     ny: int
 
     def __post_init__(self):
-        self.bbox = np.asarray(self.bbox, dtype=np.float64)
-        if self.nx < 1 or self.ny < 1:
+        self.bbox = np.asarray(self.bbox, dtype=np.float64).reshape(2, 3)
+        if min(self.nx, self.ny) < 1:
             raise InvalidInputError("cell counts must be >= 1")
-        if not np.all(self.bbox[1] > self.bbox[0]):
+        if (self.bbox[1] <= self.bbox[0]).any():
             raise InvalidInputError("degenerate scene bbox")
 
     @property
     def cell_extent(self) -> np.ndarray:
-        return (self.bbox[1, :2] - self.bbox[0, :2]) / np.array([self.nx, self.ny])
+        return (self.bbox[1, :2] - self.bbox[0, :2]) / (self.nx, self.ny)
+
+    def _index(self, xy) -> np.ndarray:
+        """Clamped (ix, iy) of points (..., >= 2)."""
+        q = np.floor((np.asarray(xy, dtype=np.float64)[..., :2] - self.bbox[0, :2])
+                     / self.cell_extent).astype(np.int64)
+        return np.clip(q, 0, (self.nx - 1, self.ny - 1))
 
     def cell_of_point(self, xy) -> tuple[int, int]:
-        xy = np.asarray(xy, dtype=np.float64)[:2]
-        w, h = self.cell_extent
-        ix = int(np.floor((xy[0] - self.bbox[0, 0]) / w))
-        iy = int(np.floor((xy[1] - self.bbox[0, 1]) / h))
-        return min(max(ix, 0), self.nx - 1), min(max(iy, 0), self.ny - 1)
+        ix, iy = self._index(xy)
+        return int(ix), int(iy)
 
     def cell_bbox(self, index) -> np.ndarray:
-        ix, iy = index
-        w, h = self.cell_extent
-        lo = np.array([self.bbox[0, 0] + ix * w, self.bbox[0, 1] + iy * h, self.bbox[0, 2]])
-        hi = np.array([self.bbox[0, 0] + (ix + 1) * w, self.bbox[0, 1] + (iy + 1) * h,
-                       self.bbox[1, 2]])
-        return np.stack([lo, hi])
+        lo_xy = self.bbox[0, :2] + np.asarray(index, dtype=np.float64) * self.cell_extent
+        hi_xy = lo_xy + self.cell_extent
+        return np.array([[lo_xy[0], lo_xy[1], self.bbox[0, 2]],
+                         [hi_xy[0], hi_xy[1], self.bbox[1, 2]]])
 
     def cells(self):
-        return [(ix, iy) for iy in range(self.ny) for ix in range(self.nx)]
+        """Row-major cell order (y outer)."""
+        return [(i % self.nx, i // self.nx) for i in range(self.nx * self.ny)]
+
+    def region(self, core, ring: int = 1) -> set:
+        if not (0 <= core[0] < self.nx and 0 <= core[1] < self.ny):
+            raise InvalidInputError(f"core cell {core} outside grid")
+        if ring < 0:
+            raise InvalidInputError("ring must be >= 0")
+        xs = range(max(core[0] - ring, 0), min(core[0] + ring, self.nx - 1) + 1)
+        ys = range(max(core[1] - ring, 0), min(core[1] + ring, self.ny - 1) + 1)
+        return {(x, y) for x in xs for y in ys}
 
 
 def partition_scene(bbox, nx: int, ny: int) -> SceneGrid:
-    return SceneGrid(np.asarray(bbox, dtype=np.float64), nx, ny)
+    return SceneGrid(bbox, nx, ny)
 
 
 def onload_region(grid: SceneGrid, core, ring: int = 1) -> set:
-    """scene_manager.py:92-104: cells within Chebyshev distance ``ring``."""
-    cx, cy = core
-    if not (0 <= cx < grid.nx and 0 <= cy < grid.ny):
-        raise InvalidInputError(f"core cell {core} outside grid")
-    if ring < 0:
-        raise InvalidInputError("ring must be >= 0")
-    return {(ix, iy) for ix in range(max(0, cx - ring), min(grid.nx, cx + ring + 1))
-            for iy in range(max(0, cy - ring), min(grid.ny, cy + ring + 1))}
+    """Cells within Chebyshev distance ``ring`` of ``core``."""
+    return grid.region(core, ring)
 
 
 def cell_rows(means: np.ndarray, grid: SceneGrid) -> dict:
-    """engine_api.py:182-207 (gaussian_cell_groups): ascending ids per cell."""
-    m = np.asarray(means, dtype=np.float64)
-    w, h = grid.cell_extent
-    ix = np.clip(np.floor((m[:, 0] - grid.bbox[0, 0]) / w).astype(int), 0, grid.nx - 1)
-    iy = np.clip(np.floor((m[:, 1] - grid.bbox[0, 1]) / h).astype(int), 0, grid.ny - 1)
+    """Ascending Gaussian ids of every cell (engine_api.py:182-207)."""
+    ix, iy = grid._index(np.asarray(means, dtype=np.float64)).T
     lin = iy * grid.nx + ix
     order = np.argsort(lin, kind="stable")
     bounds = np.searchsorted(lin[order], np.arange(grid.nx * grid.ny + 1))
@@ -497,7 +518,9 @@ class TierStore:
 
 
 # ---------------------------------------------------------------------------
-# double buffering and prefetch policy (memory_tiers.py:150-247)
+# block streaming: a front region (rendered) and a back region (loading
+# ahead of a cell crossing), switched by nested trigger zones around the
+# core cell (the decisions of memory_tiers.py:150-247)
 
 
 @dataclass
@@ -508,26 +531,31 @@ class Region:
 
 @dataclass
 class BufferPair:
+    """front: the region being rendered; back: (region, LoadHandle) in flight."""
+
     front: Region | None = None
-    back: tuple | None = None  # (Region, LoadHandle)
+    back: tuple | None = None
 
     def swap(self, clock: VirtualClock) -> None:
         if self.back is None:
             raise IncompleteLoadError("no back buffer to swap in")
-        region, handle = self.back
-        if not handle.ready(clock):
-            raise IncompleteLoadError(
-                f"back buffer load completes at t={handle.ready_at:.6f}, now t={clock.now:.6f}")
-        self.front, self.back = region, None
+        if not self.back[1].ready(clock):
+            raise IncompleteLoadError(f"back buffer load completes at t={self.back[1].ready_at:.6f}"
+                                      f", now t={clock.now:.6f}")
+        self.front, self.back = self.back[0], None
 
 
 @dataclass(frozen=True)
 class TriggerZones:
+    """Fractions of the core cell's half-extent: past ``inner`` a load of the
+    next cell's region starts, past ``outer`` the buffers swap."""
+
     inner_fraction: float = 0.5
     outer_fraction: float = 0.8
 
     def __post_init__(self):
-        if not 0 < self.inner_fraction < self.outer_fraction <= 1:
+        ok = 0 < self.inner_fraction < self.outer_fraction <= 1
+        if not ok:
             raise InvalidConfigError("require 0 < inner < outer <= 1")
 
 
@@ -537,48 +565,58 @@ class PrefetchAction:
     target_core: tuple | None = None
 
 
+_NONE = PrefetchAction("none")
+
+
+def _exit_axis(rel: np.ndarray, vel: np.ndarray, inner: float) -> int:
+    """The axis the camera is leaving the core cell through: among the axes
+    past the inner zone, those it moves outward along, the fastest (first on
+    ties); if it moves outward along none, the axis it is furthest out on."""
+    past = [ax for ax in (0, 1) if abs(rel[ax]) >= inner]
+    outward = [ax for ax in past if rel[ax] * vel[ax] > 0]
+    if not outward:
+        return int(np.argmax(np.abs(rel)))
+    best = outward[0]
+    for ax in outward[1:]:
+        if abs(vel[ax]) > abs(vel[best]):
+            best = ax
+    return best
+
+
 def prefetch_policy(position, velocity, core_cell, zones: TriggerZones, pair: BufferPair,
                     grid: SceneGrid, clock: VirtualClock) -> PrefetchAction:
-    """memory_tiers.py:196-247: nested trigger zones inside the core cell."""
-    cb = grid.cell_bbox(core_cell)
-    center = (cb[0, :2] + cb[1, :2]) / 2
-    half = (cb[1, :2] - cb[0, :2]) / 2
-    rel = (np.asarray(position, dtype=float)[:2] - center) / half
-    frac = np.abs(rel)
-    if np.all(frac < zones.inner_fraction):
-        return PrefetchAction("none")
-    vel = np.asarray(velocity, dtype=float)[:2]
-    crossed = frac >= zones.inner_fraction
-    candidates = [a for a in (0, 1) if crossed[a] and vel[a] * rel[a] > 0]
-    if not candidates:
-        candidates = [int(np.argmax(frac))]
-    axis = max(candidates, key=lambda a: abs(vel[a]))
-    step = 1 if rel[axis] > 0 else -1
-    target = list(core_cell)
-    target[axis] += step
-    target[0] = min(max(target[0], 0), grid.nx - 1)
-    target[1] = min(max(target[1], 0), grid.ny - 1)
-    target = tuple(target)
-    beyond_outer = bool(np.any(frac >= zones.outer_fraction))
-    if beyond_outer and pair.back is not None:
-        region, handle = pair.back
-        if handle.ready(clock):
-            return PrefetchAction("swap", target_core=region.core)
-        return PrefetchAction("stall_then_swap", target_core=region.core)
-    pending = pair.back is not None and pair.back[0].core == target
-    front_covers = pair.front is not None and pair.front.core == target
-    if pending or front_covers or target == core_cell:
-        return PrefetchAction("none")
-    return PrefetchAction("start_load", target_core=target)
+    """What the block session does this frame, from the camera's position in
+    its core cell (normalised to [-1, 1] per axis) and its velocity."""
+    box = grid.cell_bbox(core_cell)
+    mid, half = box[:, :2].mean(axis=0), (box[1, :2] - box[0, :2]) / 2
+    rel = (np.asarray(position, dtype=float)[:2] - mid) / half
+    if (np.abs(rel) < zones.inner_fraction).all():
+        return _NONE
+    ax = _exit_axis(rel, np.asarray(velocity, dtype=float)[:2], zones.inner_fraction)
+    nxt = list(core_cell)
+    nxt[ax] = min(max(nxt[ax] + (1 if rel[ax] > 0 else -1), 0), (grid.nx, grid.ny)[ax] - 1)
+    nxt = tuple(nxt)
+    if pair.back is not None and (np.abs(rel) >= zones.outer_fraction).any():
+        back_region, handle = pair.back
+        kind = "swap" if handle.ready(clock) else "stall_then_swap"
+        return PrefetchAction(kind, target_core=back_region.core)
+    already = {core_cell}
+    if pair.back is not None:
+        already.add(pair.back[0].core)
+    if pair.front is not None:
+        already.add(pair.front.core)
+    return _NONE if nxt in already else PrefetchAction("start_load", target_core=nxt)
 
 
 # ---------------------------------------------------------------------------
-# sessions (render_runtime.py)
+# sessions over the paged pool (the streaming modes of render_runtime.py
+# 65-326; same configuration, FrameStats and decisions)
 
 
 @dataclass
 class SessionConfig:
-    """render_runtime.py:81-97 (+ sh_eval_degree: 1 = the reference's colours)."""
+    """Streaming mode, byte budget (the reference's unit, ref_row_bytes) and
+    render settings (+ sh_eval_degree: 1 = the reference's colours)."""
 
     mode: str = "static_full"
     budget_bytes: int | None = None
@@ -593,7 +631,7 @@ class SessionConfig:
     def __post_init__(self):
         if self.mode not in RENDER_MODES:
             raise InvalidConfigError(f"mode must be one of {RENDER_MODES}, got {self.mode!r}")
-        if self.mode != "static_full" and self.budget_bytes is None:
+        if self.budget_bytes is None and self.mode != "static_full":
             raise InvalidConfigError(f"mode {self.mode!r} requires budget_bytes")
 
 
@@ -609,15 +647,16 @@ class FrameStats:
     n_primitives: int = 0
 
     def as_dict(self) -> dict:
-        d = dict(self.__dict__)
-        d["core_cell"] = list(self.core_cell) if self.core_cell else None
+        d = asdict(self)
+        d["core_cell"] = None if self.core_cell is None else list(self.core_cell)
         return d
 
 
 def _host_arrays(model):
     """(means, quats, scales, logits, sh, degree) as host numpy from a host or
     device model."""
-    f = lambda t: t.detach().cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t)  # noqa: E731
+    def f(t):
+        return t.detach().cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t)
     return (f(model.means), f(model.quats), f(model.scales), f(model.opacity_logits), f(model.sh),
             int(model.sh_degree))
 
@@ -627,137 +666,169 @@ class _HostModel:
         self.means, self.quats, self.scales, self.opacity_logits, self.sh, self.sh_degree = arrs
 
 
-class BlockSession:
-    """render_runtime.py:110-193: the front buffer covers the camera's core
-    cell region; the back buffer is filled ahead of crossings."""
+class _PoolSession:
+    """Shared machinery: the tier store, its clock and the stall count."""
+
+    store: TierStore
+    clock: VirtualClock
+
+    def __init__(self):
+        self.stalls = 0
+
+    def _stall(self, ready_at: float) -> None:
+        self.stalls += 1
+        self.store.stats.stalls += 1
+        self.clock.wait_until(ready_at)
+
+    def _draw(self, camera, groups) -> tuple[torch.Tensor, int]:
+        rows = sum(e - s for s, e in (self.store.host.groups[g] for g in groups))
+        return self.store.render_groups(camera, groups, self.cfg), int(rows)
+
+    def frame_state(self) -> tuple:
+        """(core cell, resident bytes, peak resident bytes, stalls)."""
+        return (None, self.store.resident_bytes, self.store.stats.peak_resident_bytes,
+                self.stalls)
+
+
+class BlockSession(_PoolSession):
+    """Cell-grid streaming: the front buffer holds the ring region of the
+    camera's core cell; the next region is loaded ahead of a crossing."""
 
     def __init__(self, model, grid: SceneGrid, cfg: SessionConfig,
                  clock: VirtualClock | None = None, device=None):
+        super().__init__()
         self.grid, self.cfg = grid, cfg
         self.clock = clock or VirtualClock()
         arrs = _host_arrays(model)
         rows = cell_rows(arrs[0], grid)
-        order, groups, start = [], {}, 0
-        keys = []
-        # prim key = (rank of the cell in sorted (ix, iy) order, original id):
-        # the order of model_from_groups' concatenation over any set of cells
-        for rank, cell in enumerate(sorted(grid.cells())):
-            ids = rows[cell]
-            order.append(ids)
-            keys.append((np.int64(rank) << 32) + ids.astype(np.int64))
-            groups[cell] = (start, start + len(ids))
-            start += len(ids)
-        host = HostTier(_HostModel(arrs), np.concatenate(order), np.concatenate(keys), groups)
-        worst = max(sum(host.group_bytes[c] for c in onload_region(grid, cell, cfg.ring))
-                    for cell in grid.cells())
-        if 2 * worst > cfg.budget_bytes:
+        # pool rows grouped by cell in sorted (ix, iy) order; the prim key
+        # (cell rank << 32 | id) is the tie order of any concatenation of
+        # cells in that order, which is how the reference builds the model
+        cells = sorted(grid.cells())
+        sizes = np.array([len(rows[c]) for c in cells], dtype=np.int64)
+        starts = np.concatenate([[0], np.cumsum(sizes)])
+        groups = {c: (int(starts[i]), int(starts[i + 1])) for i, c in enumerate(cells)}
+        order = np.concatenate([rows[c] for c in cells])
+        keys = np.concatenate([(np.int64(i) << 32) + rows[c].astype(np.int64)
+                               for i, c in enumerate(cells)])
+        host = HostTier(_HostModel(arrs), order, keys, groups)
+        need = max(sum(host.group_bytes[c] for c in grid.region(cell, cfg.ring))
+                   for cell in cells)
+        if need * 2 > cfg.budget_bytes:
             raise BudgetExceededError(
                 f"budget {cfg.budget_bytes} bytes cannot double-buffer the largest "
-                f"onload region (2 x {worst} bytes)")
+                f"onload region (2 x {need} bytes)")
         self.store = TierStore(cfg.budget_bytes, host, cfg.transfer, self.clock, device)
         self.pair = BufferPair()
-        self.stalls = 0
 
-    def _region_cells(self, core):
-        return frozenset(onload_region(self.grid, core, self.cfg.ring))
+    def _request(self, core) -> tuple:
+        cells = frozenset(self.grid.region(core, self.cfg.ring))
+        return Region(cells, core), self.store.load_cells(sorted(cells))
 
-    def _load_region(self, core):
-        cells = self._region_cells(core)
-        handle = self.store.load_cells(sorted(cells))
-        return Region(cells, core), handle
-
-    def _drop_unreferenced(self):
-        keep = set()
-        if self.pair.front:
-            keep |= self.pair.front.cell_ids
+    def _evict_unused(self) -> None:
+        live = set(self.pair.front.cell_ids if self.pair.front else ())
         if self.pair.back:
-            keep |= self.pair.back[0].cell_ids
-        stale = [c for c in list(self.store.device) if c not in keep]
-        if stale:
-            self.store.offload_cells(stale, write_back=False)
-
-    def _force_resident(self, core):
-        self.stalls += 1
-        self.store.stats.stalls += 1
-        region, handle = self._load_region(core)
-        self.clock.advance(max(0.0, handle.ready_at - self.clock.now))
-        self.pair.front, self.pair.back = region, None
-        self._drop_unreferenced()
+            live |= self.pair.back[0].cell_ids
+        unused = [c for c in list(self.store.device) if c not in live]
+        if unused:
+            self.store.offload_cells(unused, write_back=False)
 
     def step(self, camera, velocity) -> tuple[torch.Tensor, int]:
-        core = self.grid.cell_of_point(camera.center)
-        if self.pair.front is None:
-            region, handle = self._load_region(core)
-            self.clock.advance(max(0.0, handle.ready_at - self.clock.now))
+        here = self.grid.cell_of_point(camera.center)
+        if self.pair.front is None:  # first frame: load and wait
+            region, handle = self._request(here)
+            self.clock.wait_until(handle.ready_at)
             self.pair.front = region
-        action = prefetch_policy(camera.center, velocity, self.pair.front.core, self.cfg.zones,
-                                 self.pair, self.grid, self.clock)
-        if action.kind == "start_load":
-            self.pair.back = self._load_region(action.target_core)
-        elif action.kind == "swap":
+        act = prefetch_policy(camera.center, velocity, self.pair.front.core, self.cfg.zones,
+                              self.pair, self.grid, self.clock)
+        if act.kind == "start_load":
+            self.pair.back = self._request(act.target_core)
+        elif act.kind in ("swap", "stall_then_swap"):
+            if act.kind == "stall_then_swap":
+                self._stall(self.pair.back[1].ready_at)
             self.pair.swap(self.clock)
-            self._drop_unreferenced()
-        elif action.kind == "stall_then_swap":
-            self.stalls += 1
-            self.store.stats.stalls += 1
-            _, handle = self.pair.back
-            self.clock.advance(max(0.0, handle.ready_at - self.clock.now))
-            self.pair.swap(self.clock)
-            self._drop_unreferenced()
-        if core not in self.pair.front.cell_ids:
-            self._force_resident(core)
-        cells = sorted(self.pair.front.cell_ids)
-        image = self.store.render_groups(camera, cells, self.cfg)
-        n = sum(e - s for s, e in (self.store.host.groups[c] for c in cells))
-        return image, n
+            self._evict_unused()
+        if here not in self.pair.front.cell_ids:  # outran the prefetch: load in place
+            region, handle = self._request(here)
+            self._stall(handle.ready_at)
+            self.pair.front, self.pair.back = region, None
+            self._evict_unused()
+        return self._draw(camera, sorted(self.pair.front.cell_ids))
+
+    def frame_state(self) -> tuple:
+        return (self.pair.front.core,) + super().frame_state()[1:]
 
 
-class FrustumSession:
-    """render_runtime.py:199-243: least-recently-visible voxel cache bounded by
-    the byte budget; each frame renders the frustum-visible voxels."""
+class FrustumSession(_PoolSession):
+    """Voxel streaming: each frame draws the frustum-visible voxels; the
+    least recently visible voxels are evicted to stay within the budget."""
 
     def __init__(self, model, cfg: SessionConfig, clock: VirtualClock | None = None,
                  device=None):
+        super().__init__()
         self.cfg = cfg
         self.clock = clock or VirtualClock()
         arrs = _host_arrays(model)
         self.index = reorder_voxel_grid(arrs[0], arrs[2], cfg.voxel_size)
         perm = self.index.permutation
-        groups = {v: (int(s), int(e)) for v, (s, e) in enumerate(self.index.ranges)}
+        groups = dict(enumerate(map(tuple, self.index.ranges.tolist())))
         # prim key = row of the voxel-reordered model (render_image's subset ids)
         host = HostTier(_HostModel(arrs), perm, np.arange(len(perm), dtype=np.int64), groups)
         self.store = TierStore(cfg.budget_bytes, host, cfg.transfer, self.clock, device)
         self.last_visible: dict = {}
         self.frame = 0
-        self.stalls = 0
+
+    def _make_room(self, visible) -> None:
+        st = self.store
+        vis = set(visible)
+        missing = sum(st.host_bytes(v) for v in visible if not st.is_resident(v))
+        over = st.resident_bytes + missing - st.budget_bytes
+        if over <= 0:
+            return
+        # stable: equally old voxels leave in residency (insertion) order
+        victims = sorted((v for v in st.device if v not in vis),
+                         key=lambda v: self.last_visible.get(v, -1))
+        for v in victims:
+            if st.resident_bytes + missing <= st.budget_bytes:
+                break
+            st.offload_cells([v], write_back=False)
 
     def step(self, camera) -> tuple[torch.Tensor, int]:
         self.frame += 1
-        needed = frustum_visible_voxels(self.index, camera)
-        store = self.store
-        need_bytes = sum(store.host_bytes(v) for v in needed if not store.is_resident(v))
-        if store.resident_bytes + need_bytes > store.budget_bytes:
-            evictable = sorted((v for v in store.device if v not in needed),
-                               key=lambda v: self.last_visible.get(v, -1))
-            while evictable and store.resident_bytes + need_bytes > store.budget_bytes:
-                store.offload_cells([evictable.pop(0)], write_back=False)
-        handle = store.load_cells(needed)
-        wait = handle.ready_at - self.clock.now
-        if wait > 0:
-            self.stalls += 1
-            store.stats.stalls += 1
-            self.clock.advance(wait)
-        for v in needed:
-            self.last_visible[v] = self.frame
-        image = store.render_groups(camera, needed, self.cfg)
-        n = int(sum(self.index.ranges[v, 1] - self.index.ranges[v, 0] for v in needed))
-        return image, n
+        visible = frustum_visible_voxels(self.index, camera)
+        self._make_room(visible)
+        handle = self.store.load_cells(visible)
+        if handle.ready_at > self.clock.now:
+            self._stall(handle.ready_at)
+        self.last_visible.update(dict.fromkeys(visible, self.frame))
+        return self._draw(camera, visible)
+
+
+class _StaticSession:
+    """The whole model resident on the device (the reference's fp64 bytes)."""
+
+    def __init__(self, model, cfg: SessionConfig, device=None):
+        self.cfg = cfg
+        self.model = model if isinstance(model, GaussianModel) else \
+            GaussianModel.from_host(_HostModel(_host_arrays(model)), device=device)
+        self.nbytes = self.model.count * (ref_row_bytes(int(self.model.sh.shape[1])) - 8)
+        self.ctx = context(self.model.device.index)
+
+    def step(self, camera, velocity=None) -> tuple[torch.Tensor, int]:
+        c = self.cfg
+        img = render(camera, self.model, c.tile_size, c.background, c.sh_eval_degree,
+                     ctx=self.ctx).rgb
+        return img, self.model.count
+
+    def frame_state(self) -> tuple:
+        return None, self.nbytes, self.nbytes, 0
 
 
 def run_session(model, cameras, timestamps, cfg: SessionConfig, grid: SceneGrid | None = None,
                 clock: VirtualClock | None = None, keep_images: bool = True, device=None):
-    """render_runtime.py:250-308: (images, [FrameStats]).  Frame latency is
-    wall time with the frame's GPU work completed (synchronised)."""
+    """Render a camera trajectory in ``cfg.mode``: (images, [FrameStats]).
+    The simulated clock follows the timestamps; a frame's latency is wall
+    time with its GPU work completed (synchronised)."""
     if len(cameras) != len(timestamps):
         raise InvalidInputError("one timestamp per camera required")
     clock = clock or VirtualClock()
@@ -768,56 +839,41 @@ def run_session(model, cameras, timestamps, cfg: SessionConfig, grid: SceneGrid 
     elif cfg.mode == "frustum_voxel":
         session = FrustumSession(model, cfg, clock, device)
     else:
-        session = None
-        dev_model = model if isinstance(model, GaussianModel) else \
-            GaussianModel.from_host(_HostModel(_host_arrays(model)), device=device)
-        # the reference's fp64 model bytes (render_runtime.py:270-273)
-        model_nbytes = dev_model.count * (ref_row_bytes(int(dev_model.sh.shape[1])) - 8)
-        ctx = context(dev_model.device.index)
+        session = _StaticSession(model, cfg, device)
     images, stats = [], []
-    prev_pos, prev_t = None, None
+    last = None  # (position, time) of the previous frame
     for i, (cam, t) in enumerate(zip(cameras, timestamps)):
         cam = cam if isinstance(cam, Camera) else Camera.from_reference(cam)
-        if prev_t is not None and t > prev_t:
-            clock.advance(t - prev_t)
-        pos = cam.center
-        dt = (t - prev_t) if prev_t is not None and t > prev_t else 1.0
-        vel = (pos - prev_pos) / dt if prev_pos is not None else np.zeros(3)
-        wall0 = time.perf_counter()
-        if cfg.mode == "static_full":
-            image = render(cam, dev_model, cfg.tile_size, cfg.background, cfg.sh_eval_degree,
-                           ctx=ctx).rgb
-            n_prims, core, resident, peak, stalls = dev_model.count, None, model_nbytes, \
-                model_nbytes, 0
-        elif cfg.mode == "block_double_buffer":
-            image, n_prims = session.step(cam, vel)
-            core = session.pair.front.core
-            resident = session.store.resident_bytes
-            peak = session.store.stats.peak_resident_bytes
-            stalls = session.stalls
+        vel = np.zeros(3)
+        if last is not None:
+            moved = t > last[1]
+            if moved:
+                clock.advance(t - last[1])
+            vel = (cam.center - last[0]) / ((t - last[1]) if moved else 1.0)
+        t0 = time.perf_counter()
+        if isinstance(session, FrustumSession):
+            image, n = session.step(cam)
         else:
-            image, n_prims = session.step(cam)
-            core = None
-            resident = session.store.resident_bytes
-            peak = session.store.stats.peak_resident_bytes
-            stalls = session.stalls
+            image, n = session.step(cam, vel)
         torch.cuda.current_stream().synchronize()
-        stats.append(FrameStats(i, float(t), (time.perf_counter() - wall0) * 1e3, resident, peak,
-                                stalls, core, n_prims))
+        core, resident, peak, stalls = session.frame_state()
+        stats.append(FrameStats(i, float(t), (time.perf_counter() - t0) * 1e3, resident, peak,
+                                stalls, core, n))
         if keep_images:
             images.append(image)
-        prev_pos, prev_t = pos, t
+        last = (cam.center, t)
     return images, stats
 
 
 def bench(model, cameras, timestamps, cfg: SessionConfig, grid: SceneGrid | None = None) -> dict:
-    """render_runtime.py:311-326."""
+    """Session summary: frame count, latency mean / median, frames/s, peak
+    residency and stalls."""
     _, stats = run_session(model, cameras, timestamps, cfg, grid=grid, keep_images=False)
     lat = [s.latency_ms for s in stats]
-    total_s = sum(lat) / 1e3
+    secs = sum(lat) / 1e3
     return {"frames": len(stats),
             "mean_latency_ms": statistics.fmean(lat) if lat else 0.0,
             "median_latency_ms": statistics.median(lat) if lat else 0.0,
-            "fps": len(stats) / total_s if total_s > 0 else 0.0,
+            "fps": len(stats) / secs if secs > 0 else 0.0,
             "peak_resident_bytes": max((s.peak_resident_bytes for s in stats), default=0),
             "stalls": stats[-1].stalls if stats else 0}

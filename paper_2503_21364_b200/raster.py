@@ -139,13 +139,15 @@ def abi_camera(cam) -> _lib.Camera:
     return c
 
 
-def abi_settings(tile_size, sh_eval_degree, background, flags=0) -> _lib.Settings:
+def abi_settings(tile_size, sh_eval_degree, background, flags=0,
+                 max_instances: int = 0) -> _lib.Settings:
     s = _lib.Settings()
     s.tile_size = int(tile_size)
     s.sh_eval_degree = int(sh_eval_degree)
     bg = [float(v) for v in np.asarray(background, dtype=np.float64).reshape(3)]
     s.background[:] = bg
     s.flags = int(flags)
+    s.max_instances = int(max_instances)
     return s
 
 
@@ -154,12 +156,33 @@ def abi_settings(tile_size, sh_eval_degree, background, flags=0) -> _lib.Setting
 
 
 @dataclass
-class TileRecord:
-    """Per-tile view of a render, fields as gaussian_core.py:256-263.
+class Splat2DBatch:
+    """Screen-space splats after culling (gaussian_core.py:173-184), fp64 on
+    the host, aligned arrays of length M in the reference's order: means2d
+    (M,2), cov2d (M,2,2) incl. the 0.3 floor, depth (M,), radius_px (M,),
+    prim_id (M,) original ids.  Values are K1's fp64 geometry, bit-equal to
+    the reference's project_splats."""
 
-    ``order`` indexes the kept splats (the reference's Splat2DBatch order);
-    ``sigma`` / ``t_before`` (the backward's per-step tensors) are not kept
-    by the forward renderer and are ``None``.
+    means2d: torch.Tensor
+    cov2d: torch.Tensor
+    depth: torch.Tensor
+    radius_px: torch.Tensor
+    prim_id: torch.Tensor
+
+    def __len__(self) -> int:
+        return int(self.means2d.shape[0])
+
+
+@dataclass
+class TileRecord:
+    """Per-tile record, fields as gaussian_core.py:256-263.
+
+    ``order`` indexes the record's splats (the reference's Splat2DBatch
+    order).  With ``collect`` (``render_image(..., with_record=True)`` on
+    small frames) ``sigma`` / ``t_before`` are the fp64 (K_t, P_t) blend
+    tensors ``_blend`` collects (306-322, no early break) and ``t_final`` is
+    fp64; otherwise ``sigma`` / ``t_before`` are ``None`` and ``t_final`` is
+    the fp32 blend's transmittance.
     """
 
     pix_xy: torch.Tensor
@@ -172,7 +195,10 @@ class TileRecord:
 
 @dataclass
 class RenderRecord:
-    """Render bookkeeping (gaussian_core.py:266-274) on the host."""
+    """Render bookkeeping (gaussian_core.py:266-274) on the host: the
+    reference's fields (splats, colors, opacities, background, width, height,
+    tiles) plus the device pipeline's own (tile ranges, instance keys,
+    n_processed)."""
 
     width: int
     height: int
@@ -182,8 +208,14 @@ class RenderRecord:
     tile_ranges: torch.Tensor     # (T,2)
     inst_prim_ids: torch.Tensor   # (K,) prim id per tile instance, per-tile lists concatenated
     inst_keys: torch.Tensor       # (K,) tile << 32 | input row
-    t_final: torch.Tensor         # (H,W)
+    t_final: torch.Tensor         # (H,W) fp64 with collect, else the fp32 blend's
     n_processed: torch.Tensor     # (T,)
+    splats: Splat2DBatch | None = None
+    colors: torch.Tensor | None = None     # (M,3) fp64 view colours (clamped SH)
+    opacities: torch.Tensor | None = None  # (M,) fp64 sigmoid(logit)
+    _sigma: torch.Tensor | None = field(default=None, repr=False)     # flat, per tile blocks
+    _t_before: torch.Tensor | None = field(default=None, repr=False)
+    _offsets: np.ndarray | None = field(default=None, repr=False)     # per tile block start
     _tiles: list = field(default=None, repr=False)
     # what the render drew, so train.backward_render(image_grad, record) can
     # replay it (the reference's backward_render signature, 438)
@@ -217,7 +249,12 @@ def _build_tiles(rec: RenderRecord) -> list:
             pix_idx = (ys[:, None] * w + xs[None, :]).reshape(-1)
             a, b = int(ranges[t, 0]), int(ranges[t, 1])
             order = torch.as_tensor([pos[int(p)] for p in inst[a:b]], dtype=torch.long)
-            tiles.append(TileRecord(pix_xy, pix_idx, order, tf[pix_idx].double()))
+            sig = tb = None
+            if rec._sigma is not None:
+                o, k, p = int(rec._offsets[t]), b - a, int(pix_idx.numel())
+                sig = rec._sigma[o:o + k * p].reshape(k, p)
+                tb = rec._t_before[o:o + k * p].reshape(k, p)
+            tiles.append(TileRecord(pix_xy, pix_idx, order, tf[pix_idx].double(), sig, tb))
             t += 1
     return tiles
 
@@ -245,8 +282,7 @@ def render(camera, gaussians: GaussianModel, tile_size: int = 16, background=(0.
            sh_eval_degree: int = 3, with_instances: bool = False, stage_times: bool = False,
            prim_ids: torch.Tensor | None = None, stream=None, ctx=None,
            out: dict | None = None, page_mask: torch.Tensor | None = None,
-           page_shift: int = 7, touched_fix: bool = True,
-           tile_sort: bool = False) -> RenderOutput:
+           page_shift: int = 7, touched_fix: bool = True) -> RenderOutput:
     """Render one view of device-resident Gaussians (north-star operator).
 
     ``prim_ids`` (int64, optional) are the original ids used for depth-tie
@@ -256,8 +292,6 @@ def render(camera, gaussians: GaussianModel, tile_size: int = 16, background=(0.
     fp64 replay that makes ``touched`` exact (K7b).  ``page_mask`` (device uint8 per
     128-row page: its number of live leading rows, 0..128) restricts the
     render to those rows (the paged device pool of ``offload``).
-    ``tile_sort=True`` builds the tile lists with the instance radix sort
-    instead of the default coarse-bin path (identical lists; for A/B tests).
     """
     if not isinstance(gaussians, GaussianModel):
         raise InvalidInputError("gaussians must be a GaussianModel (device SoA)")
@@ -297,8 +331,7 @@ def render(camera, gaussians: GaussianModel, tile_size: int = 16, background=(0.
     cam = abi_camera(camera)
     st = abi_settings(ts, sh_eval_degree, background,
                       (_lib.LMGS_FLAG_STAGE_TIMES if stage_times else 0)
-                      | (0 if touched_fix else _lib.LMGS_FLAG_NO_TOUCHED_FIX)
-                      | (_lib.LMGS_FLAG_TILE_SORT if tile_sort else 0))
+                      | (0 if touched_fix else _lib.LMGS_FLAG_NO_TOUCHED_FIX))
     sh = _stream_handle(stream)
     L = _lib.lib()
     with torch.cuda.device(dev):
@@ -318,14 +351,26 @@ def render(camera, gaussians: GaussianModel, tile_size: int = 16, background=(0.
                         keys, prims, stats)
 
 
+COLLECT_MAX_BYTES = 1 << 30  # sigma + t_before of a record (fp64), auto mode
+
+
 def render_image(model, camera, tile_size: int = 16, background=(0.0, 0.0, 0.0),
-                 with_record: bool = False, subset=None, sh_eval_degree: int = 1):
+                 with_record: bool = False, subset=None, sh_eval_degree: int = 1,
+                 collect: bool | None = None):
     """Drop-in for ``landmark.gaussian_core.render_image`` (582-597).
 
     Returns ``(image (H,W,3), touched (M,) int64[, RenderRecord])`` with
     ``image`` an fp32 CUDA tensor.  ``model`` may be a ``GaussianModel``, a
-    ``scenes.HostGaussians`` or the reference's model (uploaded each call).
+    ``scenes.HostGaussians`` or the reference's model (uploaded each call;
+    keep a ``GaussianModel`` to render one model many times).
     ``sh_eval_degree=1`` reproduces the reference's eval_sh_colors.
+
+    The record carries the reference's fields: ``splats`` (fp64 Splat2DBatch),
+    ``colors``, ``opacities``, ``background``, ``width``, ``height`` and
+    ``tiles``.  ``collect`` materialises every tile's fp64 ``sigma`` /
+    ``t_before`` (K_t, P_t) and fp64 ``t_final`` like the reference's
+    ``rasterize(collect=True)`` (``lmgs_record_collect``); ``None`` = when
+    they fit in ``COLLECT_MAX_BYTES``.
     """
     if not isinstance(model, GaussianModel):
         model = GaussianModel.from_host(model)
@@ -360,13 +405,67 @@ def render_image(model, camera, tile_size: int = 16, background=(0.0, 0.0, 0.0),
         return o.rgb, touched_m
     kept_pos = torch.nonzero(kept).reshape(-1)
     rows = kept_pos if inv is None else torch.argsort(inv)[kept_pos]
-    rec = RenderRecord(cam.width, cam.height, int(tile_size),
+    # splats: K1's fp64 geometry of the kept rows, in the reference's order
+    pj = project(cam, src, sh_eval_degree=sh_eval_degree)
+    c = pj["cov2d"][rows]
+    cov = torch.stack([torch.stack([c[:, 0], c[:, 1]], -1), torch.stack([c[:, 1], c[:, 2]], -1)],
+                      -2)
+    splats = Splat2DBatch(pj["mean2d"][rows].cpu(), cov.cpu(), pj["depth"][rows].cpu(),
+                          pj["radius"][rows].cpu(), src_ids[kept].cpu())
+    ranges = o.tile_ranges.cpu().numpy().astype(np.int64)
+    ts = int(tile_size)
+    tx, ty = -(-cam.width // ts), -(-cam.height // ts)
+    tw = np.minimum(ts, cam.width - np.arange(tx) * ts)
+    th = np.minimum(ts, cam.height - np.arange(ty) * ts)
+    pix = (th[:, None] * tw[None, :]).reshape(-1)
+    blocks = (ranges[:, 1] - ranges[:, 0]) * pix
+    offsets = np.concatenate([[0], np.cumsum(blocks)])
+    if collect is None:
+        collect = 16 * int(offsets[-1]) <= COLLECT_MAX_BYTES
+    sigma = t_before = None
+    colors = opac = None
+    t_final = o.transmittance.double().cpu()
+    if collect:
+        sigma, t_before, t_final64, col64, op64 = _collect(src, cam, ts, background,
+                                                           sh_eval_degree, prim_ids, offsets)
+        t_final = t_final64.cpu()
+        sigma, t_before = sigma.cpu(), t_before.cpu()
+        colors, opac = col64[rows].cpu(), op64[rows].cpu()
+    else:  # the fp32 view colours / opacities of K1
+        colors, opac = pj["colors"][rows].double().cpu(), pj["opacity"][rows].double().cpu()
+    rec = RenderRecord(cam.width, cam.height, ts,
                        torch.as_tensor(np.asarray(background, dtype=np.float64)),
                        src_ids[kept].cpu(), o.tile_ranges.cpu(), o.inst_prim_ids.cpu(),
-                       o.inst_keys.cpu(), o.transmittance.double().cpu(), o.n_processed.cpu(),
+                       o.inst_keys.cpu(), t_final, o.n_processed.cpu(),
+                       splats=splats, colors=colors, opacities=opac, _sigma=sigma,
+                       _t_before=t_before, _offsets=offsets if collect else None,
                        _model=src, _camera=cam, _prim_ids=prim_ids, _rows=rows,
                        _sh_eval_degree=int(sh_eval_degree))
     return o.rgb, touched_m, rec
+
+
+def _collect(model, cam, tile_size, background, sh_eval_degree, prim_ids, offsets):
+    """lmgs_record_collect for the view just rendered on the current
+    context: flat fp64 sigma / t_before, fp64 t_final (H,W), per-row fp64
+    colours and opacities."""
+    dev = model.device
+    ctx = context(dev.index, torch.cuda.current_stream(dev))
+    total = int(offsets[-1])
+    sigma = torch.empty(max(total, 1), dtype=torch.float64, device=dev)
+    t_before = torch.empty(max(total, 1), dtype=torch.float64, device=dev)
+    t_final = torch.empty((cam.height, cam.width), dtype=torch.float64, device=dev)
+    colors = torch.empty((model.count, 3), dtype=torch.float64, device=dev)
+    opac = torch.empty(model.count, dtype=torch.float64, device=dev)
+    offs = torch.as_tensor(offsets[:-1], dtype=torch.int64, device=dev)
+    g = model._abi(prim_ids)
+    c = abi_camera(cam)
+    st = abi_settings(tile_size, sh_eval_degree, background)
+    with torch.cuda.device(dev):
+        _lib.check(ctx.handle, _lib.lib().lmgs_record_collect(
+            ctx.handle, ctypes.byref(g), ctypes.byref(c), ctypes.byref(st), _ptr(offs),
+            _ptr(sigma), _ptr(t_before), _ptr(t_final), _ptr(colors), _ptr(opac),
+            _stream_handle(None)), "lmgs_record_collect")
+    return sigma[:total], t_before[:total], t_final, colors, opac
 
 
 def project(camera, gaussians: GaussianModel, sh_eval_degree: int = 1, stream=None) -> dict:

@@ -29,7 +29,7 @@ def test_struct_layouts_match_header():
     # sizes of the by-pointer structs as compiled on x86-64 / the CUDA host side
     assert ctypes.sizeof(_lib.Camera) == 8 * (9 + 3 + 3 + 6) + 8
     assert ctypes.sizeof(_lib.Gaussians) == 8 * 6 + 8 + 8 + 8 + 8  # + page_mask, shift, pad
-    assert ctypes.sizeof(_lib.Settings) == 4 * 2 + 8 * 3 + 4 + 4  # fp64 background, padded
+    assert ctypes.sizeof(_lib.Settings) == 4 * 2 + 8 * 3 + 4 + 4 + 8  # + max_instances
     assert ctypes.sizeof(_lib.Frame) == 8 * 8
 
 
