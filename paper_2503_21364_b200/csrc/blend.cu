@@ -346,9 +346,9 @@ constexpr int kWarpsPerBlock16 = 8;
 #endif
 template <int NP>
 __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, int n_items) {
-  __shared__ float4 s_geo[kWarpsPerBlock16][32];   // mx_local, my_local, qa, qb
-  __shared__ float4 s_geo2[kWarpsPerBlock16][32];  // qc, log2_alpha, r2_lo, r2_hi
-  __shared__ float4 s_col[kWarpsPerBlock16][32];   // r, g, b, z
+  // per hit splat: {mx_local, my_local, qa, qb}, {qc, log2_alpha, r2_lo, r2_hi},
+  // {r, g, b, z} side by side (one address per splat)
+  __shared__ float4 s_rec[kWarpsPerBlock16][32][3];
   __shared__ double s_mx[kWarpsPerBlock16][32], s_my[kWarpsPerBlock16][32],
       s_r2[kWarpsPerBlock16][32];
   __shared__ uint32_t s_id[kWarpsPerBlock16][32];
@@ -467,10 +467,10 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
           const double ax = fabs(mxl) + 16.0, ay = fabs(myl) + 16.0;
           const double band =  // explicit rounding (touched_fix.cu)
               __dmul_rn(__dadd_rn(__dadd_rn(r2, __dmul_rn(ax, ax)), __dmul_rn(ay, ay)), 0x1p-18);
-          s_geo[warp][lane] = make_float4(fx, fy, c1.z, c1.w);
-          s_geo2[warp][lane] = make_float4(g2.x, g2.y, __double2float_rd(r2 - band),
-                                           __double2float_ru(r2 + band));
-          s_col[warp][lane] = make_float4(g2.z, g2.w, g3.x, g3.y);
+          s_rec[warp][lane][0] = make_float4(fx, fy, c1.z, c1.w);
+          s_rec[warp][lane][1] = make_float4(g2.x, g2.y, __double2float_rd(r2 - band),
+                                             __double2float_ru(r2 + band));
+          s_rec[warp][lane][2] = make_float4(g2.z, g2.w, g3.x, g3.y);
           s_mx[warp][lane] = mx;
           s_my[warp][lane] = my;
           s_r2[warp][lane] = r2;
@@ -483,33 +483,31 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
       while (m) {
         const int k = __ffs(m) - 1;
         m &= m - 1;
-        const float4 g = s_geo[warp][k];
-        const float4 h = s_geo2[warp][k];
-        const float4 c = s_col[warp][k];
+        const float4 g = s_rec[warp][k][0];
+        const float4 h = s_rec[warp][k][1];
+        const float4 c = s_rec[warp][k][2];
         const float dx = px - g.x;
         uint32_t contrib_bits = 0;
         bool active = false;
+        // Common path, branch-free: a pixel takes the splat when it is active
+        // and certainly inside the circle (fp32 below the guard band); sigma
+        // is 0 otherwise, which leaves C and T bit-identical (fmaf(0, c, C) =
+        // C, T * (1 - 0) = T).  The rare fp64 decisions — d.d within the
+        // guard band of r^2, or w > 0 where fp32 ex2 underflows — are flagged
+        // and settled after the vote below, so this path carries no branch.
+        uint32_t rare = 0;  // bit q: the pixel needs the exact path
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
-          // branch-free common path: sigma is computed for every pixel and
-          // forced to 0 when the pixel is outside the circle or already
-          // inactive, which leaves C and T bit-identical (fmaf(0, c, C) = C,
-          // T * (1 - 0) = T); only the rare fp64 decisions branch.  (Skipping
-          // splats that cover no active pixel with an extra vote measured slower.)
           const bool on = T[q] >= kTermEpsF;
           const float dy = ((float)ly[q] + 0.5f) - g.y;
           const float d2 = fmaf(dx, dx, dy * dy);
-          bool inside = d2 <= h.z;
-          if (on && !inside && d2 <= h.w) {  // guard band: the reference's fp64 test
-            const double ddx = ((double)(x0 + lx) + 0.5) - s_mx[warp][k];
-            const double ddy = ((double)(y0 + ly[q]) + 0.5) - s_my[warp][k];
-            inside = __dadd_rn(__dmul_rn(ddx, ddx), __dmul_rn(ddy, ddy)) <= s_r2[warp][k];
-          }
+          const bool inside = d2 <= h.z;
           const float power = fmaf(fmaf(g.z, dx, g.w * dy), dx, fmaf(h.x * dy, dy, h.y));
           const bool take = on && inside;
-          bool contrib = take && power > -1060.0f;
-          if (take && !contrib && power >= -1080.0f)  // fp32 ex2 underflows first
-            contrib = exp2((double)power) * (double)T[q] > 0.0;
+          const bool band = !inside && d2 <= h.w;      // fp64 circle test needed
+          const bool tiny = power <= -1060.0f && power >= -1080.0f;  // fp64 w > 0 test
+          rare |= (on && (band || (inside && tiny))) ? 1u << q : 0u;
+          const bool contrib = take && power > -1060.0f;
           const float sig = take ? fminf(ex2_approx(power), kSigmaMaxF) : 0.0f;
           const float w = T[q] * sig;
           C0[q] = fmaf(w, c.x, C0[q]);
@@ -519,8 +517,40 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
           Tc[q] = take ? T[q] : Tc[q];
           T[q] = T[q] * (1.0f - sig);
           contrib_bits += contrib;
-          active |= T[q] >= kTermEpsF;
         }
+        if (__any_sync(0xffffffffu, rare)) {
+#pragma unroll
+          for (int q = 0; q < NP; ++q) {
+            if (!(rare >> q & 1u)) continue;
+            const float dy = ((float)ly[q] + 0.5f) - g.y;
+            const float d2 = fmaf(dx, dx, dy * dy);
+            const float power = fmaf(fmaf(g.z, dx, g.w * dy), dx, fmaf(h.x * dy, dy, h.y));
+            if (d2 <= h.z) {
+              // taken above with sigma = 0 (ex2 underflow): only w > 0 is open,
+              // judged in fp64 on T before the splat (unchanged)
+              contrib_bits += exp2((double)power) * (double)T[q] > 0.0;
+              continue;
+            }
+            // guard band: the reference's fp64 circle test
+            const double ddx = ((double)(x0 + lx) + 0.5) - s_mx[warp][k];
+            const double ddy = ((double)(y0 + ly[q]) + 0.5) - s_my[warp][k];
+            if (!(__dadd_rn(__dmul_rn(ddx, ddx), __dmul_rn(ddy, ddy)) <= s_r2[warp][k])) continue;
+            bool contrib = power > -1060.0f;
+            if (!contrib && power >= -1080.0f)  // fp32 ex2 underflows first
+              contrib = exp2((double)power) * (double)T[q] > 0.0;
+            const float sig = fminf(ex2_approx(power), kSigmaMaxF);
+            const float w = T[q] * sig;
+            C0[q] = fmaf(w, c.x, C0[q]);
+            C1[q] = fmaf(w, c.y, C1[q]);
+            C2[q] = fmaf(w, c.z, C2[q]);
+            D[q] = fmaf(w, c.w, D[q]);
+            Tc[q] = T[q];
+            T[q] = T[q] * (1.0f - sig);
+            contrib_bits += contrib;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < NP; ++q) active |= T[q] >= kTermEpsF;
         const int wsum = NP == 1 ? __popc(__ballot_sync(0xffffffffu, contrib_bits))
                                  : __reduce_add_sync(0xffffffffu, contrib_bits);
         if (lane == k) my_touch += wsum;

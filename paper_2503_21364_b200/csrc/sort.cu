@@ -45,6 +45,20 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
+// keys and values stream through each pass once: evict-first hints keep them
+// from displacing the look-back words and the other streams' working sets
+#ifdef LMGS_SORT_STREAMING
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T* p) { return __ldcs(p); }
+template <typename T>
+__device__ __forceinline__ void st_stream(T* p, T v) { __stcs(p, v); }
+#else
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T* p) { return *p; }
+template <typename T>
+__device__ __forceinline__ void st_stream(T* p, T v) { *p = v; }
+#endif
+
 template <typename K>
 __device__ __forceinline__ uint32_t digit_of(K key, int shift) {
   return (uint32_t)((uint64_t)key >> shift) & 0xffu;
@@ -208,8 +222,8 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const int i = wbase + j * 32 + lane;
-    key[j] = i < count ? kin[base + i] : (K)~(K)0;
-    if (VALS) val[j] = iota ? (uint32_t)(base + i) : (i < count ? vin[base + i] : 0u);
+    key[j] = i < count ? ld_stream(kin + base + i) : (K)~(K)0;
+    if (VALS) val[j] = iota ? (uint32_t)(base + i) : (i < count ? ld_stream(vin + base + i) : 0u);
   }
 #ifdef LMGS_DBG_COPY
 #pragma unroll
@@ -326,8 +340,8 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
   for (int i = tid; i < count; i += kSortThreads) {
     const K k = s_keys[i];
     const uint32_t o = s_global[digit_of(k, shift)] + i;
-    kout[o] = k;
-    if (VALS) vout[o] = s_vals[i];
+    st_stream(kout + o, k);
+    if (VALS) st_stream(vout + o, s_vals[i]);
     if (segs) {
       // the staged tile is sorted on every key bit sorted so far: runs of one
       // segment are contiguous; a run [i0, i1] adds (i1 + 1) - i0
