@@ -117,6 +117,10 @@ typedef struct lmgs_settings {
  * incompletely (memory-safe); lmgs_get_stats then reports it (overflow, the
  * largest K seen) and the caller re-renders with a larger capacity. */
 #define LMGS_FLAG_NO_HOST_SYNC 8u
+/* Queue pixels for the exact-touched replay within a relative band of 1e-2
+ * around TERM_EPS instead of 1e-4 (100x more pixels replayed): the check that
+ * the default band misses no fp32/fp64 disagreement (tests/test_gpu_parity). */
+#define LMGS_FLAG_WIDE_FIX_BAND 16u
 #define LMGS_FLAG_NO_TOUCHED_FIX 2u /* skip K7b: touched may then differ from the
                                        reference where fp32 and fp64 transmittance
                                        straddle TERM_EPS (a few per million)       */

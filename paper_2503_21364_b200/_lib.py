@@ -27,6 +27,7 @@ U32 = ctypes.c_uint32
 LMGS_FLAG_STAGE_TIMES = 1
 LMGS_FLAG_NO_TOUCHED_FIX = 2
 LMGS_FLAG_NO_HOST_SYNC = 8
+LMGS_FLAG_WIDE_FIX_BAND = 16
 MAX_STAGES = 8
 
 # every symbol include/lmgs.h declares

@@ -522,6 +522,7 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
     LMGS_CUDA(c, cudaMemsetAsync(&sc->fix_count, 0, sizeof(uint32_t), s));
     ba.fix_count = &sc->fix_count;
     ba.fix_list = static_cast<uint32_t*>(c->fixbuf.ptr);
+    ba.fix_band = (st->flags & LMGS_FLAG_WIDE_FIX_BAND) ? 1e-2f : 1e-4f;
     if (out->n_processed) {
       // override i32, list u32, need u8: W * H entries each
       const size_t third = align_up((size_t)cap * 4);

@@ -35,10 +35,13 @@ constexpr float kSigmaMaxF = 0.9999f;
 // could disagree on which splats the pixel still takes — is queued for an
 // fp64 replay that corrects the counts.  Tc = T before the last splat the
 // pixel took while active (its T before the crossing, once it crossed).
-constexpr float kFixBand = 1e-4f;  // 10x the measured fp32/fp64 T gap (< 1e-5 at the crossing)
-__device__ __forceinline__ bool crossing_uncertain(float T, float Tc) {
-  if (T < kTermEpsF) return Tc < kTermEpsF * (1.0f + kFixBand) || T >= kTermEpsF * (1.0f - kFixBand);
-  return T < kTermEpsF * (1.0f + kFixBand);
+// The band is BlendArgs.fix_band: 1e-4 by default (10x the measured fp32/fp64
+// T gap, < 1e-5 at the crossing), 1e-2 with LMGS_FLAG_WIDE_FIX_BAND (the
+// check that the default band misses no disagreement).
+__device__ __forceinline__ bool crossing_uncertain(float T, float Tc, float band) {
+  const float hi = kTermEpsF * (1.0f + band), lo = kTermEpsF * (1.0f - band);
+  if (T < kTermEpsF) return Tc < hi || T >= lo;
+  return T < hi;
 }
 // The queue holds W * H entries (each pixel is queued at most once), so it
 // cannot overflow.  Entry = fix_entry(): tile << 8 | ly << 4 | lx for 16x16
@@ -287,7 +290,7 @@ __device__ __forceinline__ void blend_block(const BlendArgs& a, const int tile, 
   for (int p = 0; p < PPT; ++p) {
     if (NPFIX || !valid[p]) continue;
     put_pixel(a, x0 + lxs[p], y0 + lys[p], T[p], C0[p], C1[p], C2[p], D[p]);
-    if (a.fix_count && crossing_uncertain(T[p], Tc[p]))
+    if (a.fix_count && crossing_uncertain(T[p], Tc[p], a.fix_band))
       queue_fix(a, ts == 16 ? fix_entry16(tile, lxs[p], lys[p])
                             : (uint32_t)(y0 + lys[p]) * (uint32_t)a.width + (uint32_t)(x0 + lxs[p]));
   }
@@ -480,6 +483,7 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
       uint32_t m = __ballot_sync(0xffffffffu, hit);
       __syncwarp();
       uint32_t my_touch = 0;  // pixels with w > 0 for this lane's splat (cid)
+      uint32_t my_ballot = 0;  // NP == 1: the pixels themselves
       while (m) {
         const int k = __ffs(m) - 1;
         m &= m - 1;
@@ -487,7 +491,8 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
         const float4 h = s_rec[warp][k][1];
         const float4 c = s_rec[warp][k][2];
         const float dx = px - g.x;
-        uint32_t contrib_bits = 0;
+        uint32_t contrib_bits = 0;  // NP > 1: pixels with w > 0
+        bool contrib1 = false;      // NP == 1: the pixel has w > 0
         bool active = false;
         // Common path, branch-free: a pixel takes the splat when it is active
         // and certainly inside the circle (fp32 below the guard band); sigma
@@ -495,7 +500,7 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
         // C, T * (1 - 0) = T).  The rare fp64 decisions — d.d within the
         // guard band of r^2, or w > 0 where fp32 ex2 underflows — are flagged
         // and settled after the vote below, so this path carries no branch.
-        uint32_t rare = 0;  // bit q: the pixel needs the exact path
+        bool any_rare = false;  // some pixel needs the exact path
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
           const bool on = T[q] >= kTermEpsF;
@@ -504,10 +509,11 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
           const bool inside = d2 <= h.z;
           const float power = fmaf(fmaf(g.z, dx, g.w * dy), dx, fmaf(h.x * dy, dy, h.y));
           const bool take = on && inside;
-          const bool band = !inside && d2 <= h.w;      // fp64 circle test needed
-          const bool tiny = power <= -1060.0f && power >= -1080.0f;  // fp64 w > 0 test
-          rare |= (on && (band || (inside && tiny))) ? 1u << q : 0u;
-          const bool contrib = take && power > -1060.0f;
+          // fp64 circle test (guard band) or fp64 w > 0 test (fp32 ex2 underflow)
+          // (inside implies d2 <= h.w: r2_lo <= r2_hi); bitwise, so no branch
+          const bool tiny = power <= -1060.0f;
+          any_rare |= on & (d2 <= h.w) & (!inside | tiny);
+          const bool contrib = take && !tiny;
           const float sig = take ? fminf(ex2_approx(power), kSigmaMaxF) : 0.0f;
           const float w = T[q] * sig;
           C0[q] = fmaf(w, c.x, C0[q]);
@@ -516,19 +522,26 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
           D[q] = fmaf(w, c.w, D[q]);
           Tc[q] = take ? T[q] : Tc[q];
           T[q] = T[q] * (1.0f - sig);
-          contrib_bits += contrib;
+          if (NP == 1) contrib1 |= contrib;
+          else contrib_bits += contrib;
         }
-        if (__any_sync(0xffffffffu, rare)) {
+        if (__any_sync(0xffffffffu, any_rare)) {
 #pragma unroll
           for (int q = 0; q < NP; ++q) {
-            if (!(rare >> q & 1u)) continue;
             const float dy = ((float)ly[q] + 0.5f) - g.y;
             const float d2 = fmaf(dx, dx, dy * dy);
             const float power = fmaf(fmaf(g.z, dx, g.w * dy), dx, fmaf(h.x * dy, dy, h.y));
+            // redone on the current state: a rare pixel's T was left unchanged
+            // (not taken, or taken with sigma = 0); a pixel taken with sigma > 0
+            // has power > -1060 and is inside, so the test is false for it
+            const bool on = T[q] >= kTermEpsF;
+            if (!(on && (d2 <= h.z ? power <= -1060.0f : d2 <= h.w))) continue;
             if (d2 <= h.z) {
               // taken above with sigma = 0 (ex2 underflow): only w > 0 is open,
               // judged in fp64 on T before the splat (unchanged)
-              contrib_bits += exp2((double)power) * (double)T[q] > 0.0;
+              const bool cw = exp2((double)power) * (double)T[q] > 0.0;
+              if (NP == 1) contrib1 |= cw;
+              else contrib_bits += cw;
               continue;
             }
             // guard band: the reference's fp64 circle test
@@ -546,14 +559,19 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
             D[q] = fmaf(w, c.w, D[q]);
             Tc[q] = T[q];
             T[q] = T[q] * (1.0f - sig);
-            contrib_bits += contrib;
+            if (NP == 1) contrib1 |= contrib;
+            else contrib_bits += contrib;
           }
         }
 #pragma unroll
         for (int q = 0; q < NP; ++q) active |= T[q] >= kTermEpsF;
-        const int wsum = NP == 1 ? __popc(__ballot_sync(0xffffffffu, contrib_bits))
-                                 : __reduce_add_sync(0xffffffffu, contrib_bits);
-        if (lane == k) my_touch += wsum;
+        if (NP == 1) {  // the owner keeps its splat's ballot; counted after the batch
+          const uint32_t b = __ballot_sync(0xffffffffu, contrib1);
+          my_ballot = lane == k ? b : my_ballot;
+        } else {
+          const int wsum = __reduce_add_sync(0xffffffffu, contrib_bits);
+          if (lane == k) my_touch += wsum;
+        }
         // pixels only go inactive on a splat they are inside: the warp's break
         // index is the first splat after which none of its pixels is active
         if (!__any_sync(0xffffffffu, active)) {
@@ -562,6 +580,7 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
           break;
         }
       }
+      if (NP == 1) my_touch = __popc(my_ballot);
       if (my_touch && a.touched) atomicAdd(a.touched + cid, (int)my_touch);
       __syncwarp();
     }
@@ -571,7 +590,8 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
     for (int q = 0; q < NP; ++q) {
       if (!valid[q]) continue;
       put_pixel(a, x0 + lx, y0 + ly[q], T[q], C0[q], C1[q], C2[q], D[q]);
-      if (a.fix_count && crossing_uncertain(T[q], Tc[q])) queue_fix(a, fix_entry16(tile, lx, ly[q]));
+      if (a.fix_count && crossing_uncertain(T[q], Tc[q], a.fix_band))
+        queue_fix(a, fix_entry16(tile, lx, ly[q]));
     }
   }
 }

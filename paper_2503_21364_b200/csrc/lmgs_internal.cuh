@@ -246,6 +246,7 @@ struct BlendArgs {
   // replay; fix_list holds W * H entries
   uint32_t* fix_count;
   uint32_t* fix_list;
+  float fix_band;  // relative band around TERM_EPS that queues a pixel
   // exact n_processed (launch_nproc_fix): pixels K7b corrected and their fp64
   // break index per pixel (-1 = none; reset after use)
   const uint32_t* np_count;

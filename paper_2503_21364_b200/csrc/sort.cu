@@ -199,12 +199,6 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
   const uint32_t bid = s_bid;
   const int64_t base = (int64_t)bid * kSortTile;
   if (base >= n) return;
-  for (int i = tid; i < kWarps * kRadix; i += kSortThreads) {
-    (&s_match[0][0])[i] = 0;
-    (&s_wcnt[0][0])[i] = 0;
-  }
-  s_hist[tid] = 0;  // kSortThreads == kRadix
-  __syncthreads();
   const int count = (int)min((int64_t)kSortTile, n - base);
   const int src = plan->src[pass];
   const K* __restrict__ kin = src ? keys1 : keys0;
@@ -225,6 +219,13 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
     key[j] = i < count ? ld_stream(kin + base + i) : (K)~(K)0;
     if (VALS) val[j] = iota ? (uint32_t)(base + i) : (i < count ? ld_stream(vin + base + i) : 0u);
   }
+  // the loads above are in flight while the ranking state is cleared
+  for (int i = tid; i < kWarps * kRadix; i += kSortThreads) {
+    (&s_match[0][0])[i] = 0;
+    (&s_wcnt[0][0])[i] = 0;
+  }
+  s_hist[tid] = 0;  // kSortThreads == kRadix
+  __syncthreads();
 #ifdef LMGS_DBG_COPY
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {

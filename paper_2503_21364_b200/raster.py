@@ -282,14 +282,16 @@ def render(camera, gaussians: GaussianModel, tile_size: int = 16, background=(0.
            sh_eval_degree: int = 3, with_instances: bool = False, stage_times: bool = False,
            prim_ids: torch.Tensor | None = None, stream=None, ctx=None,
            out: dict | None = None, page_mask: torch.Tensor | None = None,
-           page_shift: int = 7, touched_fix: bool = True) -> RenderOutput:
+           page_shift: int = 7, touched_fix: bool = True,
+           wide_fix_band: bool = False) -> RenderOutput:
     """Render one view of device-resident Gaussians (north-star operator).
 
     ``prim_ids`` (int64, optional) are the original ids used for depth-tie
     breaking and reported in ``inst_prim_ids`` (render_image's ``subset``).
     ``out`` may pre-supply output tensors (e.g. slices of a batch buffer)
     under the RenderOutput field names.  ``touched_fix=False`` skips the
-    fp64 replay that makes ``touched`` exact (K7b).  ``page_mask`` (device uint8 per
+    fp64 replay that makes ``touched`` exact (K7b); ``wide_fix_band`` replays
+    every pixel within 1e-2 of TERM_EPS instead of 1e-4 (a check of the band).  ``page_mask`` (device uint8 per
     128-row page: its number of live leading rows, 0..128) restricts the
     render to those rows (the paged device pool of ``offload``).
     """
@@ -331,7 +333,8 @@ def render(camera, gaussians: GaussianModel, tile_size: int = 16, background=(0.
     cam = abi_camera(camera)
     st = abi_settings(ts, sh_eval_degree, background,
                       (_lib.LMGS_FLAG_STAGE_TIMES if stage_times else 0)
-                      | (0 if touched_fix else _lib.LMGS_FLAG_NO_TOUCHED_FIX))
+                      | (0 if touched_fix else _lib.LMGS_FLAG_NO_TOUCHED_FIX)
+                      | (_lib.LMGS_FLAG_WIDE_FIX_BAND if wide_fix_band else 0))
     sh = _stream_handle(stream)
     L = _lib.lib()
     with torch.cuda.device(dev):

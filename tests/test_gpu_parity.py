@@ -279,3 +279,27 @@ def test_touched_fix_replays_only_crossing_pixels():
     assert 0 < queued < 0.01 * 1920 * 1080
     assert 0 < diff <= 64
     assert torch.equal(exact.rgb, raw.rgb)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("n,view", [(1_000_000, 0), (6_000_000, 5), (6_000_000, 40)])
+def test_fix_band_misses_nothing(n, view):
+    """K7b's band (1e-4 relative around TERM_EPS) is the measured fp32/fp64
+    transmittance gap x 10, not a proof.  Replaying every pixel within 1e-2
+    instead (100x the pixels) must not change a single touched count or
+    break index: no disagreement lies outside the default band."""
+    from paper_2503_21364_b200.raster import context
+
+    g = scenes.synthetic_gaussians(n, seed=0)
+    m = GaussianModel.from_host(g, validate=False)
+    cam = scenes.orbit_cameras(64, 1920, 1080, seed=0)[view]
+    ctx = context(0)
+    a = render(cam, m, 16, (0.0, 0.0, 0.0), 3, ctx=ctx)
+    qa = ctx.touched_fix_count()
+    b = render(cam, m, 16, (0.0, 0.0, 0.0), 3, ctx=ctx, wide_fix_band=True)
+    qb = ctx.touched_fix_count()
+    torch.cuda.synchronize()
+    assert qb > 20 * qa > 0
+    assert torch.equal(a.touched, b.touched)
+    assert torch.equal(a.n_processed, b.n_processed)
+    assert torch.equal(a.rgb, b.rgb)
