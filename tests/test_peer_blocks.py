@@ -164,3 +164,44 @@ def test_render_strips_equals_render(ts, n_strips):
     assert torch.equal(got_rgb, ref.rgb)
     assert torch.equal(torch.cat(trans)[:97], ref.transmittance)
     assert torch.equal(torch.cat(depth)[:97], ref.depth)
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_c5_full_size_blocks_and_composite_vs_oracle():
+    """Config 5 at its named size: 8 city blocks of 6.25M Gaussians (50M),
+    1080p.  Every block layer (premultiplied RGB with background 0, T_final)
+    against the CPU oracle's render of the same block (1e-4), block tile lists
+    bit-exact for the front block, and the CUDA front-to-back composite
+    against the oracle layers composited in the same block order."""
+    import torch
+
+    import oracle
+    from paper_2503_21364_b200 import GaussianModel, render, scenes
+    from paper_2503_21364_b200.distributed import _composite_cuda, block_order, composite_numpy
+
+    bbs = scenes.city_block_bboxes()
+    cam = scenes.city_camera()
+    order = block_order(np.asarray(cam.center), bbs)
+    gpu_layers, ref_layers = [], []
+    for b in range(len(bbs)):
+        g = scenes.city_block(b, 6_250_000, 3, bbs)
+        m = GaussianModel.from_host(g, validate=False)
+        trans = torch.empty((cam.height, cam.width), dtype=torch.float32, device=m.device)
+        o = render(cam, m, 16, (0.0, 0.0, 0.0), 3, out={"transmittance": trans},
+                   with_instances=(b == order[0]))
+        torch.cuda.synchronize()
+        ref = oracle.render(g, cam, 16, (0.0, 0.0, 0.0), sh_eval_degree=3)
+        assert np.abs(o.rgb.cpu().double().numpy() - ref["image"]).max() <= 1e-4, b
+        assert np.abs(trans.cpu().double().numpy() - ref["t_final"]).max() <= 1e-4, b
+        if b == order[0]:
+            assert o.n_instances == ref["K"]
+            np.testing.assert_array_equal(o.inst_prim_ids.cpu().numpy(), ref["inst_prim"])
+        gpu_layers.append(torch.cat([o.rgb, trans[..., None], o.depth[..., None]], -1))
+        ref_layers.append(np.concatenate([ref["image"], ref["t_final"][..., None],
+                                          ref["depth"][..., None]], -1))
+        del m, o, trans, ref, g
+    rgb, alpha, _ = _composite_cuda(torch.stack(gpu_layers), order, (0.0, 0.0, 0.0))
+    want_rgb, want_alpha, _ = composite_numpy(np.stack(ref_layers), order, (0.0, 0.0, 0.0))
+    assert np.abs(rgb.cpu().double().numpy() - want_rgb).max() <= 1e-4
+    assert np.abs(alpha.cpu().double().numpy() - want_alpha).max() <= 1e-4
