@@ -43,6 +43,14 @@ int main(int argc, char** argv) {
   b.keys[0] = k0; b.keys[1] = k1; b.key_bytes = kb; b.vals[0] = v0; b.vals[1] = v1;
   b.plan = plan; b.hist = hist; b.lookback = lb; b.counters = ctr;
   b.keys_result = slots; b.vals_result = slots + 1; b.iota_vals = vals != 0;
+  // optional 5th argument 1: device-side count -> persistent onesweep grid
+  unsigned long long* d_n = nullptr;
+  if (argc > 5 && atoi(argv[5])) {
+    cudaMalloc(&d_n, sizeof(unsigned long long));
+    unsigned long long hn = (unsigned long long)n;
+    cudaMemcpy(d_n, &hn, sizeof(hn), cudaMemcpyHostToDevice);
+    b.n_dev = d_n;
+  }
   const int begin = kb == 8 ? 32 : 0;
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   float best = 1e9;

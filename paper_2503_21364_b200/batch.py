@@ -120,6 +120,7 @@ class BatchRenderer:
         if stage_times:
             tot = {}
             inst = pairs = vis = launches = 0
+            max_k = 0
             G = self.group
             for start in range(0, len(cams), G):
                 idx = list(range(start, min(start + G, len(cams))))
@@ -130,6 +131,7 @@ class BatchRenderer:
                     for k, v in s["stage_ms"].items():
                         tot[k] = tot.get(k, 0.0) + v
                     inst += s["n_instances"]
+                    max_k = max(max_k, s["n_instances"])
                     vis += s["n_visible"]
                     launches += s["n_launches"]
                     pairs += self._pairs(i)
@@ -144,7 +146,7 @@ class BatchRenderer:
             p = tile_passes(t)
             proc = self._processed_total(len(cams)) / nv
             alg = alg_bytes_per_view(n, s_read, self.group, v_avg, k_avg, t, p, proc, pix)
-            return {"stage_ms": tot, "alg_bytes": alg, "launches": launches,
+            return {"stage_ms": tot, "alg_bytes": alg, "launches": launches, "max_instances": max_k,
                     "per_frame": {"instances": k_avg, "visible": v_avg, "pairs": pairs / nv,
                                   "processed": proc, "tile_passes": p}}
         G = self.group

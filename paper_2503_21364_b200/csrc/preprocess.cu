@@ -66,35 +66,38 @@ __device__ __forceinline__ void sh_color(const float* __restrict__ sh, int ncoef
     for (int q = 0; q < 48; ++q)
       if (q < nload) v[q] = SMEM ? sh[q] : __ldg(sh + q);
   }
+  // fp32 colour (the image tolerance, 1e-4, not bit-exactness, applies): this
+  // file is built with -fmad=false for the fp64 geometry, so the colour's
+  // multiply-adds are written as explicit FMAs (half the instructions)
+  const float b1 = -C1 * y, b2 = C1 * z, b3 = -C1 * x;
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) c[ch] = C0 * v[ch];
   if (deg >= 1 && ncoef >= 4) {
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch)
-      c[ch] = ((c[ch] - (C1 * y) * v[3 + ch]) + (C1 * z) * v[6 + ch]) - (C1 * x) * v[9 + ch];
+      c[ch] = __fmaf_rn(b3, v[9 + ch], __fmaf_rn(b2, v[6 + ch], __fmaf_rn(b1, v[3 + ch], c[ch])));
   }
   if (deg >= 2 && ncoef >= 9) {
-    float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
-    const float C20 = 1.0925484305920792f, C21 = -1.0925484305920792f,
-                C22 = 0.31539156525252005f, C23 = -1.0925484305920792f,
-                C24 = 0.5462742152960396f;
+    const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    const float b[5] = {1.0925484305920792f * xy, -1.0925484305920792f * yz,
+                        0.31539156525252005f * (2.0f * zz - xx - yy),
+                        -1.0925484305920792f * xz, 0.5462742152960396f * (xx - yy)};
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch)
-      c[ch] = c[ch] + C20 * xy * v[12 + ch] + C21 * yz * v[15 + ch] +
-              C22 * (2.0f * zz - xx - yy) * v[18 + ch] + C23 * xz * v[21 + ch] +
-              C24 * (xx - yy) * v[24 + ch];
+    for (int k = 0; k < 5; ++k)
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) c[ch] = __fmaf_rn(b[k], v[12 + 3 * k + ch], c[ch]);
     if (deg >= 3 && ncoef >= 16) {
-      const float C30 = -0.5900435899266435f, C31 = 2.890611442640554f,
-                  C32 = -0.4570457994644658f, C33 = 0.3731763325901154f,
-                  C34 = -0.4570457994644658f, C35 = 1.445305721320277f,
-                  C36 = -0.5900435899266435f;
+      const float d[7] = {-0.5900435899266435f * y * (3.0f * xx - yy),
+                          2.890611442640554f * xy * z,
+                          -0.4570457994644658f * y * (4.0f * zz - xx - yy),
+                          0.3731763325901154f * z * (2.0f * zz - 3.0f * xx - 3.0f * yy),
+                          -0.4570457994644658f * x * (4.0f * zz - xx - yy),
+                          1.445305721320277f * z * (xx - yy),
+                          -0.5900435899266435f * x * (xx - 3.0f * yy)};
 #pragma unroll
-      for (int ch = 0; ch < 3; ++ch)
-        c[ch] = c[ch] + C30 * y * (3.0f * xx - yy) * v[27 + ch] + C31 * xy * z * v[30 + ch] +
-                C32 * y * (4.0f * zz - xx - yy) * v[33 + ch] +
-                C33 * z * (2.0f * zz - 3.0f * xx - 3.0f * yy) * v[36 + ch] +
-                C34 * x * (4.0f * zz - xx - yy) * v[39 + ch] + C35 * z * (xx - yy) * v[42 + ch] +
-                C36 * x * (xx - 3.0f * yy) * v[45 + ch];
+      for (int k = 0; k < 7; ++k)
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) c[ch] = __fmaf_rn(d[k], v[27 + 3 * k + ch], c[ch]);
     }
   }
 #pragma unroll

@@ -209,6 +209,26 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
   const bool iota = iota_vals && pass == plan->first_active;
   const int shift = begin_bit + 8 * pass;
 
+#ifdef LMGS_SORT_RELOAD
+  // only the digits stay in registers (4 per word); keys and values are
+  // re-read (L2) for the scatter, which frees ~40 registers per thread
+  uint32_t dg[(kSortItems + 3) / 4];
+  uint32_t pos[kSortItems];
+  const int wbase = warp * 32 * kSortItems;
+  {
+    K key[kSortItems];
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+      const int i = wbase + j * 32 + lane;
+      key[j] = i < count ? ld_stream(kin + base + i) : (K)~(K)0;
+    }
+#pragma unroll
+    for (int q = 0; q < (kSortItems + 3) / 4; ++q) dg[q] = 0;
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) dg[j >> 2] |= digit_of(key[j], shift) << (8 * (j & 3));
+  }
+#define LMGS_DIGIT(j) ((dg[(j) >> 2] >> (8 * ((j) & 3))) & 0xffu)
+#else
   K key[kSortItems];
   uint32_t val[VALS ? kSortItems : 1];
   uint32_t pos[kSortItems];
@@ -219,6 +239,8 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
     key[j] = i < count ? ld_stream(kin + base + i) : (K)~(K)0;
     if (VALS) val[j] = iota ? (uint32_t)(base + i) : (i < count ? ld_stream(vin + base + i) : 0u);
   }
+#define LMGS_DIGIT(j) digit_of(key[j], shift)
+#endif
   // the loads above are in flight while the ranking state is cleared
   for (int i = tid; i < kWarps * kRadix; i += kSortThreads) {
     (&s_match[0][0])[i] = 0;
@@ -226,7 +248,7 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
   }
   s_hist[tid] = 0;  // kSortThreads == kRadix
   __syncthreads();
-#ifdef LMGS_DBG_COPY
+#if defined(LMGS_DBG_COPY) && !defined(LMGS_SORT_RELOAD)
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const int i = wbase + j * 32 + lane;
@@ -235,12 +257,14 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
       if (VALS) vout[base + i] = val[j];
     }
   }
-  return;
+  if (!PERSIST) return;
+  __syncthreads();
+  continue;
 #endif
   // 2. early counts, published with the look-back before ranking
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j)
-    if (wbase + j * 32 + lane < count) atomicAdd(&s_hist[digit_of(key[j], shift)], 1u);
+    if (wbase + j * 32 + lane < count) atomicAdd(&s_hist[LMGS_DIGIT(j)], 1u);
   __syncthreads();
   uint32_t* lb = lookback + ((int64_t)pass * lb_stride) * kRadix;
   const uint32_t total = s_hist[tid];  // thread d == digit d
@@ -298,7 +322,7 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const bool valid = wbase + j * 32 + lane < count;
-    const uint32_t d = digit_of(key[j], shift);
+    const uint32_t d = LMGS_DIGIT(j);
     if (valid) atomicOr(my_match + d, 1u << lane);
     __syncwarp();
     const uint32_t peers = valid ? my_match[d] : (1u << lane);
@@ -329,12 +353,19 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
-    if (wbase + j * 32 + lane < count) {
-      const uint32_t p = pos[j] + my_cnt[digit_of(key[j], shift)];
+    const int i = wbase + j * 32 + lane;
+    if (i < count) {
+      const uint32_t p = pos[j] + my_cnt[LMGS_DIGIT(j)];
+#ifdef LMGS_SORT_RELOAD
+      s_keys[p] = kin[base + i];
+      if (VALS) s_vals[p] = iota ? (uint32_t)(base + i) : vin[base + i];
+#else
       s_keys[p] = key[j];
       if (VALS) s_vals[p] = val[j];
+#endif
     }
   }
+#undef LMGS_DIGIT
   __syncthreads();
   // 6. coalesced write-out: consecutive threads, consecutive staged positions
   const bool segs = seg_counts && pass == plan->last_active;
