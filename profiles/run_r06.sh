@@ -1,7 +1,20 @@
 #!/bin/bash
-# shared-divisor fp64 division in K1: parity + bench
+# Round-2 measurement set (run under gpurun from the repo root): GPU tests,
+# smoke, bench line, the reference arm, ncu launch list of a short bench
+# (time + DRAM bytes per launch), full ncu captures of the top kernels.
 set -x
 out=gpurun_out/r06; mkdir -p $out
-timeout 900 python -m pytest tests -q -m gpu -x > $out/pytest_gpu.log 2>&1
-timeout 300 python bench_tools/stress_parity.py 7 200 > $out/stress.log 2>&1
-for i in 1 2; do timeout 300 python bench.py --steps 5 --warmup 3 --e2e-steps 1 --no-cpu-baseline > $out/bench_$i.log 2>&1; done
+python -m pytest tests -q -m gpu -p no:cacheprovider > $out/pytest_gpu.log 2>&1
+python __graft_entry__.py > $out/smoke.log 2>&1
+python bench.py --steps 20 --warmup 5 > $out/bench.log 2>&1
+tail -1 $out/bench.log > $out/bench.json
+python bench.py --impl reference --steps 2 --warmup 1 > $out/bench_ref.log 2>&1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    --csv --log-file $out/launches.csv python bench.py --steps 1 --warmup 1 --views 4 --e2e-steps 1 \
+    --no-cpu-baseline --no-c5 > $out/launches.log 2>&1
+python profiles/launch_table.py $out/launches.csv > $out/ncu_launch_table.txt
+for k in k_blend16w k_preprocess_tma k_onesweep k_emit k_touched_fix k_depth_fixup; do
+  ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 -o $out/$k -f \
+      python profiles/view_probe.py 2 > $out/ncu_$k.log 2>&1
+  python profiles/ncu_summary.py $out/$k.ncu-rep > $out/${k}_summary.txt 2>&1
+done
