@@ -18,16 +18,12 @@ __device__ __forceinline__ double bmm_dot3(double a0, double b0, double a1, doub
   return (a0 * b0 + a1 * b1) + a2 * b2;
 }
 
-// Camera-space point (x, y, z) of a near-kept Gaussian -> mean2d, cov2d
-// (incl. the 0.3 floor) and radius, in fp64, op for op as the reference
-// (project_splats 199-225, quat_to_rotmat 93-102, covariance_3d 105-117).
-// Shared by K1 and the exact replay so both see bit-identical values.
-__device__ __forceinline__ void splat_geometry(const CamArgs& cam, double x, double y, double z,
-                                               float4 q, double s0, double s1, double s2,
-                                               double* mx, double* my, double* ca_out,
-                                               double* cb_out, double* cc_out, double* radius) {
-  *mx = cam.fx * x / z + cam.cx;  // 201
-  *my = cam.fy * y / z + cam.cy;
+// The world-space covariance of a Gaussian, view-independent: quat_to_rotmat
+// (93-102) and covariance_3d (105-117) op for op.  S = {S00, S01, S02, S11,
+// S12, S22}: the bmm's S10 / S20 / S21 are the same products in the same
+// order as S01 / S02 / S12 (fp64 multiplication commutes), so equal bits.
+__device__ __forceinline__ void covariance_3d(float4 q, double s0, double s1, double s2,
+                                              double S[6]) {
   // quat_to_rotmat (93-102)
   const double qw = q.x, qx = q.y, qy = q.z, qz = q.w;
   const double nr = sqrt(((qw * qw + qx * qx) + qy * qy) + qz * qz);
@@ -42,15 +38,25 @@ __device__ __forceinline__ void splat_geometry(const CamArgs& cam, double x, dou
   const double M00 = r00 * s0, M01 = r01 * s1, M02 = r02 * s2;
   const double M10 = r10 * s0, M11 = r11 * s1, M12 = r12 * s2;
   const double M20 = r20 * s0, M21 = r21 * s1, M22 = r22 * s2;
-  const double S00 = bmm_dot3(M00, M00, M01, M01, M02, M02);
-  const double S01 = bmm_dot3(M00, M10, M01, M11, M02, M12);
-  const double S02 = bmm_dot3(M00, M20, M01, M21, M02, M22);
-  const double S10 = bmm_dot3(M10, M00, M11, M01, M12, M02);
-  const double S11 = bmm_dot3(M10, M10, M11, M11, M12, M12);
-  const double S12 = bmm_dot3(M10, M20, M11, M21, M12, M22);
-  const double S20 = bmm_dot3(M20, M00, M21, M01, M22, M02);
-  const double S21 = bmm_dot3(M20, M10, M21, M11, M22, M12);
-  const double S22 = bmm_dot3(M20, M20, M21, M21, M22, M22);
+  S[0] = bmm_dot3(M00, M00, M01, M01, M02, M02);
+  S[1] = bmm_dot3(M00, M10, M01, M11, M02, M12);
+  S[2] = bmm_dot3(M00, M20, M01, M21, M02, M22);
+  S[3] = bmm_dot3(M10, M10, M11, M11, M12, M12);
+  S[4] = bmm_dot3(M10, M20, M11, M21, M12, M22);
+  S[5] = bmm_dot3(M20, M20, M21, M21, M22, M22);
+}
+
+// Camera-space point (x, y, z) of a near-kept Gaussian and its world
+// covariance -> mean2d, cov2d (incl. the 0.3 floor) and radius, in fp64, op
+// for op as the reference (project_splats 199-225).
+__device__ __forceinline__ void splat_projection(const CamArgs& cam, double x, double y, double z,
+                                                 const double S[6], double* mx, double* my,
+                                                 double* ca_out, double* cb_out, double* cc_out,
+                                                 double* radius) {
+  *mx = cam.fx * x / z + cam.cx;  // 201
+  *my = cam.fy * y / z + cam.cy;
+  const double S00 = S[0], S01 = S[1], S02 = S[2], S11 = S[3], S12 = S[4], S22 = S[5];
+  const double S10 = S01, S20 = S02, S21 = S12;
   // clamped Jacobian (205-218); `fx / z` is torch's reciprocal(z) * fx
   const double tx = fmin(fmax(x / z, -cam.lim_x), cam.lim_x) * z;
   const double ty = fmin(fmax(y / z, -cam.lim_y), cam.lim_y) * z;
@@ -82,6 +88,16 @@ __device__ __forceinline__ void splat_geometry(const CamArgs& cam, double x, dou
   const double h = 0.5 * (ca - cc);
   const double lam = 0.5 * (ca + cc) + sqrt(h * h + cb * cb);
   *radius = 3.0 * sqrt(lam);
+}
+
+// Both of the above (K1 and the exact replays share these bit-identical values).
+__device__ __forceinline__ void splat_geometry(const CamArgs& cam, double x, double y, double z,
+                                               float4 q, double s0, double s1, double s2,
+                                               double* mx, double* my, double* ca_out,
+                                               double* cb_out, double* cc_out, double* radius) {
+  double S[6];
+  covariance_3d(q, s0, s1, s2, S);
+  splat_projection(cam, x, y, z, S, mx, my, ca_out, cb_out, cc_out, radius);
 }
 
 }  // namespace lmgs

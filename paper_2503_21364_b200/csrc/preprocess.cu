@@ -120,11 +120,14 @@ constexpr int kPreThreads = LMGS_PRE_THREADS;
 static_assert(kPreThreads == 128, "paged sets map one K1 block to one 128-row page");
 
 // Returns the splat's tile count (0: culled or off-screen); *keep = near-kept.
+// S (nullable): the Gaussian's world covariance, computed once for all the
+// views of a block (covariance_3d is view-independent)
 template <bool SMEM>
 __device__ __forceinline__ uint32_t process_one(const PreprocessArgs& a, int64_t i, double m0, double m1,
                                             double m2, float4 q, double s0, double s1, double s2,
                                             float logit, const float* sh, uint64_t* sh_wait,
-                                            bool* keep_out, uint64_t* zbits_out) {
+                                            bool* keep_out, uint64_t* zbits_out,
+                                            const double* S = nullptr) {
   bool keep = false;
   uint32_t cnt = 0;
   uint64_t zb = 0;
@@ -142,7 +145,8 @@ __device__ __forceinline__ uint32_t process_one(const PreprocessArgs& a, int64_t
       a.rects[i] = 0;
     } else {
       double mx, my, ca, cb, cc, radius;
-      splat_geometry(cam, x, y, z, q, s0, s1, s2, &mx, &my, &ca, &cb, &cc, &radius);
+      if (S) splat_projection(cam, x, y, z, S, &mx, &my, &ca, &cb, &cc, &radius);
+      else splat_geometry(cam, x, y, z, q, s0, s1, s2, &mx, &my, &ca, &cb, &cc, &radius);
       // tile rectangle (362-373)
       int x0, x1, y0, y1;
       axis_range(mx - radius, mx + radius, cam.width, cam.tile_size, cam.inv_tile, cam.tiles_x, &x0,
@@ -346,6 +350,11 @@ __global__ void __launch_bounds__(kPreThreads, NV == 1 ? LMGS_PRE_MIN_CTAS : LMG
   mbar_wait(&s_bar[0], 0);
   const int64_t i = i0 + tid;
   const bool dead = a.page_mask && tid >= (int)a.page_mask[i0 >> 7];  // past the page's live rows
+  // the world covariance once for the whole group of views
+  double S[6];
+  if (NV > 1 && !dead)
+    covariance_3d(reinterpret_cast<const float4*>(s_quats)[tid], s_scales[3 * tid],
+                  s_scales[3 * tid + 1], s_scales[3 * tid + 2], S);
 #pragma unroll
   for (int vi = 0; vi < NV; ++vi) {
     // re-read the staged inputs every view (a compiler barrier keeps them
@@ -362,7 +371,8 @@ __global__ void __launch_bounds__(kPreThreads, NV == 1 ? LMGS_PRE_MIN_CTAS : LMG
       // the SH wait happens inside process_one just before the colour is needed
       cnt = process_one<true>(av, i, s_means[3 * tid], s_means[3 * tid + 1], s_means[3 * tid + 2],
                               q, s_scales[3 * tid], s_scales[3 * tid + 1], s_scales[3 * tid + 2],
-                              s_logits[tid], s_sh + tid * a.sh_coeffs * 3, &s_bar[1], &keep, &zb);
+                              s_logits[tid], s_sh + tid * a.sh_coeffs * 3, &s_bar[1], &keep, &zb,
+                              NV > 1 ? S : nullptr);
     }
     count_kept(av, keep, cnt, zb, vi);
   }

@@ -13,8 +13,13 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     --csv --log-file $out/launches.csv python bench.py --steps 1 --warmup 1 --views 4 --e2e-steps 1 \
     --no-cpu-baseline --no-c5 > $out/launches.log 2>&1
 python profiles/launch_table.py $out/launches.csv > $out/ncu_launch_table.txt
-for k in k_blend16w k_preprocess_tma k_onesweep k_emit k_touched_fix k_depth_fixup; do
-  ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 -o $out/$k -f \
-      python profiles/view_probe.py 2 > $out/ncu_$k.log 2>&1
-  python profiles/ncu_summary.py $out/$k.ncu-rep > $out/${k}_summary.txt 2>&1
+# view_probe renders views one at a time (k_preprocess_tma<1>); per view the
+# launch order is 3 u32 onesweep passes then 2 u64 ones, so -s 3 picks the
+# first tile-sort pass of view 0
+for ks in "k_blend16w 2" "k_preprocess_tma 2" "k_onesweep 3" "k_emit 2" "k_touched_fix 2" \
+          "k_depth_fixup 2"; do
+  set -- $ks
+  ncu --set full --clock-control none --import-source on -k regex:$1 -s $2 -c 1 -o $out/$1 -f \
+      python profiles/view_probe.py 2 > $out/ncu_$1.log 2>&1
+  python profiles/ncu_summary.py $out/$1.ncu-rep > $out/${1}_summary.txt 2>&1
 done
