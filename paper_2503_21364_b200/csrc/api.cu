@@ -474,7 +474,7 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
     rb.hist = sc->tile_hist;
     rb.lookback = c->tile_lookback;
     rb.counters = sc->tile_counters;
-    rb.keys_result = &sc->slots.inst_keys;
+    rb.keys_result = &sc->slots.inst_ids;
     rb.hist_ready = true;
     rb.seg_counts = c->tile_count;
     rb.seg_shift = 32;
@@ -483,7 +483,7 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
       rb.max_n = &sc->max_k;
     }
     LMGS_CUDA(c, cudaMemsetAsync(c->tile_count, 0, sizeof(uint32_t) * tiles, s));
-    launched += radix_sort(rb, k, 32, tile_passes, s);
+    launched += tile_sort(rb, k, bits_for(tiles), s);
     launched += launch_ranges_from_counts(c->tile_count, (int)tiles, ranges, cap_view, s);
   }
   if (out->tile_ranges && tiles > 0)
@@ -494,7 +494,7 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
   // K7
   tm.begin(4);
   BlendArgs ba{};
-  ba.keys_slot = &sc->slots.inst_keys;
+  ba.keys_slot = &sc->slots.inst_ids;
   ba.ranges = ranges;
   ba.recs = c->recs;
   ba.width = cam->width;
@@ -556,7 +556,7 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
   tm.begin(5);
   if (fix && tiles > 0) {
     TouchedFixArgs fa{};
-    fa.keys_slot = &sc->slots.inst_keys;
+    fa.keys_slot = &sc->slots.inst_ids;
     fa.ranges = ranges;
     fa.recs = c->recs;
     fa.tile_size = st->tile_size;
@@ -787,11 +787,12 @@ int lmgs_copy_instances(lmgs_context* c, uint64_t* keys, int64_t* prim_ids, void
   }
   InstanceExportArgs a{};
   a.ranges = c->last_ranges;
-  a.keys_slot = &c->d_scal->slots.inst_keys;
+  a.keys_slot = &c->d_scal->slots.inst_ids;
   a.prim_ids = c->last_prim_ids;
   a.keys_out = keys;
   a.prims_out = prim_ids;
   a.k = c->stats.n_instances;
+  a.tiles = c->stats.n_tiles;
   launch_export_instances(a, static_cast<cudaStream_t>(stream));
   LMGS_CUDA(c, cudaGetLastError());
   return LMGS_OK;
@@ -829,7 +830,7 @@ int lmgs_backward(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* c
   a.sh_coeffs = g->sh_coeffs;
   a.eval_degree = s->sh_eval_degree < g->sh_degree ? s->sh_eval_degree : g->sh_degree;
   a.cam = ca;
-  a.keys_slot = &c->d_scal->slots.inst_keys;
+  a.keys_slot = &c->d_scal->slots.inst_ids;
   a.ranges = c->last_ranges;
   a.width = cam->width;
   a.height = cam->height;
@@ -881,7 +882,7 @@ int lmgs_record_collect(lmgs_context* c, const lmgs_gaussians* g, const lmgs_cam
   p.cam = ca;
   CollectArgs a{};
   a.recs = p.recs;
-  a.keys_slot = &c->d_scal->slots.inst_keys;
+  a.keys_slot = &c->d_scal->slots.inst_ids;
   a.ranges = c->last_ranges;
   a.offsets = tile_offsets;
   a.width = cam->width;

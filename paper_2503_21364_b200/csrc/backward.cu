@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(32, LMGS_BW_MINB) k_backward(BackwardArgs a) {
   const int2 range = a.ranges[tile];
   if (range.y <= range.x || !__any_sync(~0u, in_img)) return;
   const double pxd = (double)px + 0.5, pyd = (double)py + 0.5;
-  const uint64_t* __restrict__ list = static_cast<const uint64_t*>(*a.keys_slot);
+  const uint32_t* __restrict__ list = static_cast<const uint32_t*>(*a.keys_slot);
   const double4* __restrict__ cull = reinterpret_cast<const double4*>(a.recs);
   const int own = bw_owner(lane);
 
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(32, LMGS_BW_MINB) k_backward(BackwardArgs a) {
     uint32_t nid = 0;
     double4 ncd = make_double4(0.0, 0.0, -1.0, 0.0);
     if (range.x + lane < range.y) {
-      nid = (uint32_t)list[range.x + lane];
+      nid = list[range.x + lane];
       ncd = cull[3 * (size_t)nid];  // BwRec is 3 x 32 B, cull data first
     }
     for (int b0 = range.x; b0 < range.y; b0 += 32) {
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(32, LMGS_BW_MINB) k_backward(BackwardArgs a) {
       const double4 cd = ncd;
       const int nb = min(32, range.y - b0);
       if (b0 + 32 + lane < range.y) {
-        nid = (uint32_t)list[b0 + 32 + lane];
+        nid = list[b0 + 32 + lane];
         ncd = cull[3 * (size_t)nid];
       }
       // bounding box of the active pixel centres

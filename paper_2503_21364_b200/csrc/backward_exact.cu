@@ -123,14 +123,14 @@ __global__ void k_collect(CollectArgs a) {
   const int np = tw * th;
   const int2 range = a.ranges[tile];
   const int kt = range.y - range.x;
-  const uint64_t* __restrict__ list = static_cast<const uint64_t*>(*a.keys_slot);
+  const uint32_t* __restrict__ list = static_cast<const uint32_t*>(*a.keys_slot);
   const int64_t off = a.offsets[tile];
   for (int p = threadIdx.x; p < np; p += blockDim.x) {
     const int px = tx0 + p % tw, py = ty0 + p / tw;  // row-major within the tile
     const double pxd = (double)px + 0.5, pyd = (double)py + 0.5;
     double T = 1.0;
     for (int k = 0; k < kt; ++k) {
-      const BwRec& r = a.recs[(uint32_t)list[range.x + k]];
+      const BwRec& r = a.recs[list[range.x + k]];
       const double dx = pxd - r.mx, dy = pyd - r.my;  // 311
       const double maha = (r.ca * (dx * dx) + ((2.0 * r.cb) * dx) * dy) + r.cc * (dy * dy);
       double sig = r.op * exp(-0.5 * maha);             // 313

@@ -100,7 +100,7 @@ __device__ __forceinline__ void blend_block(const BlendArgs& a, const int tile, 
   const int tile_x = tile % a.tiles_x, tile_y = tile / a.tiles_x;
   const int x0 = tile_x * ts, y0 = tile_y * ts;
   const int2 range = a.ranges[tile];
-  const uint64_t* __restrict__ list = static_cast<const uint64_t*>(*a.keys_slot);
+  const uint32_t* __restrict__ list = static_cast<const uint32_t*>(*a.keys_slot);
 
   float T[PPT], C0[PPT], C1[PPT], C2[PPT], D[PPT], px[PPT], py[PPT], Tc[PPT];
   int lxs[PPT], lys[PPT], last[PPT];
@@ -150,7 +150,7 @@ __device__ __forceinline__ void blend_block(const BlendArgs& a, const int tile, 
     if (__syncthreads_count(mine_active) == 0) break;
     const int nb = min(kBatch, range.y - b0);
     for (int j = tid; j < nb; j += nthreads) {
-      const uint32_t id = (uint32_t)list[b0 + j];
+      const uint32_t id = list[b0 + j];
       const BlendRec rec = a.recs[id];
       const double mxl = rec.mx - (double)x0, myl = rec.my - (double)y0;
       const double ax = fabs(mxl) + ts, ay = fabs(myl) + ts;
@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
   constexpr int kRows = 4 * NP;  // block height
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t* __restrict__ list = static_cast<const uint64_t*>(*a.keys_slot);
+  const uint32_t* __restrict__ list = static_cast<const uint32_t*>(*a.keys_slot);
   const float4* __restrict__ rec4 = reinterpret_cast<const float4*>(a.recs);
 
   while (true) {
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
     uint32_t id = 0;
     float4 g0 = make_float4(0.f, 0.f, 0.f, 0.f), g1 = g0;
     if (range.x + lane < range.y) {
-      id = (uint32_t)list[range.x + lane];
+      id = list[range.x + lane];
       g0 = __ldg(rec4 + 4 * (size_t)id);
       g1 = __ldg(rec4 + 4 * (size_t)id + 1);
     }
@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
       }
       const float4 c0 = g0, c1 = g1;
       if (j + 32 < range.y) {  // prefetch the next batch
-        id = (uint32_t)list[j + 32];
+        id = list[j + 32];
         g0 = __ldg(rec4 + 4 * (size_t)id);
         g1 = __ldg(rec4 + 4 * (size_t)id + 1);
       }

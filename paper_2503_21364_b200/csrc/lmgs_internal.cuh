@@ -154,13 +154,18 @@ size_t radix_lookback_words(int64_t capacity);
 // sorts bits [begin_bit, begin_bit + 8*n_passes) of n keys (stable).
 int radix_sort(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_passes,
                cudaStream_t s);  // returns kernels launched
+// K5: stable sort of k keys tile << 32 | id on the tile bits [32, 32 +
+// tile_bits); every pass runs and the last one writes the ids alone (uint32_t,
+// in the buffer keys_result names).  seg_counts (required) gets the per-tile
+// counts.  keys[0] holds the input; both buffers hold k u64 keys.
+int tile_sort(const RadixSortBuffers& b, int64_t k, int tile_bits, cudaStream_t s);
 
 // Device-side slots naming where a sort's result landed (written by the plan
 // kernel, read by consumers) so the pipeline never syncs on it.
 struct DevSlots {
   void* depth_keys;  // K2 result: fp32 depth keys in (depth, id) order
   void* depth_ids;   // K2 result: Gaussian ids in (depth, id) order
-  void* inst_keys;   // K5 result: tile << 32 | id, sorted by tile then depth rank
+  void* inst_ids;    // K5 result: uint32_t ids, sorted by tile then depth rank
   void* unused;
 };
 
@@ -218,6 +223,7 @@ struct InstanceExportArgs {
   uint64_t* keys_out;
   int64_t* prims_out;
   int64_t k;
+  int tiles;
 };
 void launch_export_instances(const InstanceExportArgs& a, cudaStream_t s);
 
@@ -225,7 +231,7 @@ void launch_export_instances(const InstanceExportArgs& a, cudaStream_t s);
 // blend (blend.cu) and compositing (raster.cu)
 
 struct BlendArgs {
-  void* const* keys_slot;  // -> uint64_t[K] tile << 32 | id
+  void* const* keys_slot;  // -> uint32_t[K] ids, per tile in list order
   const int2* ranges;
   const BlendRec* recs;
   int32_t width, height, tile_size, tiles_x, tiles_y;

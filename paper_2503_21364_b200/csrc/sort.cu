@@ -5,15 +5,19 @@
 //       so equal keys stay in id order; runs of equal fp32 keys are then fixed
 //       up by the exact fp64 depth — _sort_order, gaussian_core.py:277-283);
 //   K5  the instance keys tile << 32 | id, sorted on the tile bits only
-//       (stable: the emitted array is already in depth-rank order).
+//       (stable: the emitted array is already in depth-rank order).  The last
+//       pass writes the 32-bit ids alone, which is all the blend reads
+//       (tile_sort below).
 //
 // Per sort: one histogram kernel computes every digit's global histogram in a
-// single read; a 1-block plan kernel scans them, marks digits all keys share
-// as trivial (skipped on the device) and routes the ping-pong buffers; then
-// one onesweep kernel per digit: a tile of kSortTile keys is ranked in shared
-// memory (warp match + per-warp counters, stable), staged in shared memory in
-// digit order, its global digit offsets found by decoupled look-back over the
-// preceding tiles, and written out in coalesced per-digit runs.
+// single read (for K2 and K5 the producer builds it); a 1-block plan kernel
+// scans them, marks digits all keys share as trivial (skipped on the device;
+// not for K5, whose passes change the key format) and routes the ping-pong
+// buffers; then one onesweep kernel per digit: a tile of kSortTile keys is
+// ranked in shared memory (warp match + per-warp counters, stable), staged in
+// shared memory in digit order, its global digit offsets found by decoupled
+// look-back over the preceding tiles, and written out in coalesced per-digit
+// runs.
 #include "lmgs_internal.cuh"
 
 namespace lmgs {
@@ -27,6 +31,16 @@ constexpr int kWarps = kSortThreads / 32;
 #define LMGS_LOOK_WINDOW 8
 #endif
 constexpr int kLookWindow = LMGS_LOOK_WINDOW;
+#ifndef LMGS_RANK_MODE
+#define LMGS_RANK_MODE 2
+#endif
+#ifndef LMGS_RANK_GROUP
+#define LMGS_RANK_GROUP 2
+#endif
+constexpr int kMatchBufs = LMGS_RANK_MODE == 2 ? LMGS_RANK_GROUP : 1;
+#ifndef LMGS_SORT_MIN_CTAS_NARROW
+#define LMGS_SORT_MIN_CTAS_NARROW 4  // 32-bit keys without values: fewer registers
+#endif
 
 // Look-back status words carry their payload (flag | value) in one atomic
 // word and publish nothing else, so relaxed gpu-scope accesses suffice; an
@@ -44,20 +58,6 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
 }
-
-// keys and values stream through each pass once: evict-first hints keep them
-// from displacing the look-back words and the other streams' working sets
-#ifdef LMGS_SORT_STREAMING
-template <typename T>
-__device__ __forceinline__ T ld_stream(const T* p) { return __ldcs(p); }
-template <typename T>
-__device__ __forceinline__ void st_stream(T* p, T v) { __stcs(p, v); }
-#else
-template <typename T>
-__device__ __forceinline__ T ld_stream(const T* p) { return *p; }
-template <typename T>
-__device__ __forceinline__ void st_stream(T* p, T v) { *p = v; }
-#endif
 
 template <typename K>
 __device__ __forceinline__ uint32_t digit_of(K key, int shift) {
@@ -91,14 +91,15 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_hist(const K* __restrict
 }
 
 // one block of kRadix threads: scan each digit histogram, detect trivial
-// passes, route buffers, publish where the result will land.
+// passes (unless every pass must run), route buffers, publish where the
+// result will land.
 __global__ void __launch_bounds__(kRadix) k_radix_plan(const uint32_t* __restrict__ hist,
                                                        int64_t n, int n_passes, RadixPlan* plan,
                                                        const int* gate, void* keys0,
                                                        void* keys1, void* vals0, void* vals1,
                                                        void** keys_result, void** vals_result,
                                                        const unsigned long long* n_dev,
-                                                       unsigned long long* max_n) {
+                                                       unsigned long long* max_n, bool force_all) {
   const bool off = gated_off(gate);
   if (n_dev) {
     if (max_n && threadIdx.x == 0) atomicMax(max_n, *n_dev);
@@ -128,7 +129,8 @@ __global__ void __launch_bounds__(kRadix) k_radix_plan(const uint32_t* __restric
   if (d == 0) {
     int cur = 0, first = -1, last = -1;
     for (int p = 0; p < kMaxPasses; ++p) {
-      const int act = !off && p < n_passes && !s_trivial[p] && n > 1;
+      const int act =
+          !off && p < n_passes && (force_all ? n >= 1 : (!s_trivial[p] && n > 1));
       plan->active[p] = act;
       plan->src[p] = cur;
       if (act) {
@@ -148,6 +150,49 @@ __global__ void __launch_bounds__(kRadix) k_radix_plan(const uint32_t* __restric
   }
 }
 
+// Output format of a pass and how its last pass counts tile runs.
+enum : int { kOutSame = 0, kOutIds = 1 };
+enum : int { kSegNone = 0, kSegKey = 1 };
+
+struct PassArgs {
+  void* keys[2];  // ping-pong buffers, each large enough for n keys of the wider format
+  uint32_t* vals[2];
+  int64_t n;
+  int shift;  // this pass's digit = (key >> shift) & 0xff
+  int pass;
+  const RadixPlan* plan;
+  uint32_t* lookback;
+  uint32_t* counter;
+  int64_t lb_stride;
+  bool iota_vals;
+  uint32_t id_mask;  // kOutIds: out = key & id_mask
+  uint32_t* seg_counts;
+  int seg_shift;  // kSegKey: segment = key >> seg_shift
+  const unsigned long long* n_dev;
+};
+
+template <typename KI, int OUT>
+struct OutKey {
+  using type = KI;
+};
+template <typename KI>
+struct OutKey<KI, kOutIds> {
+  using type = uint32_t;
+};
+
+template <typename KI, int OUT>
+__device__ __forceinline__ typename OutKey<KI, OUT>::type out_key(KI k, const PassArgs& a) {
+  if constexpr (OUT == kOutIds)
+    return (uint32_t)k & a.id_mask;
+  else
+    return k;
+}
+
+template <typename KI, bool VALS>
+constexpr int sort_min_ctas() {
+  return (sizeof(KI) == 4 && !VALS) ? LMGS_SORT_MIN_CTAS_NARROW : LMGS_SORT_MIN_CTAS;
+}
+
 // one onesweep scatter pass (digit `pass`)
 //
 // 1. load kSortTile keys (warp-striped, coalesced);
@@ -158,31 +203,35 @@ __global__ void __launch_bounds__(kRadix) k_radix_plan(const uint32_t* __restric
 //    back, cleared by the lowest lane) — MATCH.ANY serialises on this part;
 // 4. per-digit prefix over warps, staging in shared memory in digit order;
 // 5. decoupled look-back (windowed) for the global digit offsets;
-// 6. coalesced write-out in per-digit runs.
-template <typename K, bool VALS, bool PERSIST>
-__global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
-    K* keys0, K* keys1, uint32_t* vals0, uint32_t* vals1, int64_t n, int begin_bit, int pass,
-    const RadixPlan* __restrict__ plan, uint32_t* lookback, uint32_t* counter, int64_t lb_stride,
-    bool iota_vals, uint32_t* seg_counts, int seg_shift, const unsigned long long* n_dev) {
-  if (n_dev) n = min(n, (int64_t)*n_dev);  // the grid covers an upper bound
+// 6. coalesced write-out in per-digit runs, in the pass's output format.
+template <typename KI, int OUT, int SEG, bool VALS, bool PERSIST>
+__global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
+    k_onesweep(PassArgs a) {
+  using KO = typename OutKey<KI, OUT>::type;
+  int64_t n = a.n;
+  if (a.n_dev) n = min(n, (int64_t)*a.n_dev);  // the grid covers an upper bound
+  const RadixPlan* __restrict__ plan = a.plan;
+  const int pass = a.pass;
   if (!plan->active[pass]) {
     // no pass moves data (every digit trivial): the result buffers are the
     // inputs, so pass 0 materialises the implicit payload and the single
-    // segment instead of separate launches
+    // segment instead of separate launches (formats never change here: only
+    // sorts whose passes may be skipped get here)
     if (pass == 0 && plan->first_active < 0) {
-      if (VALS && iota_vals)
+      if (VALS && a.iota_vals)
         for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
              i += (int64_t)gridDim.x * blockDim.x)
-          vals0[i] = (uint32_t)i;
-      if (seg_counts && blockIdx.x == 0 && threadIdx.x == 0 && n > 0)
-        seg_counts[(uint64_t)keys0[0] >> seg_shift] = (uint32_t)n;
+          a.vals[0][i] = (uint32_t)i;
+      if (SEG == kSegKey && a.seg_counts && blockIdx.x == 0 && threadIdx.x == 0 && n > 0)
+        a.seg_counts[(uint64_t) static_cast<const KI*>(a.keys[0])[0] >> a.seg_shift] =
+            (uint32_t)n;
     }
     return;
   }
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  K* s_keys = reinterpret_cast<K*>(smem_raw);  // [kSortTile] staging
-  uint32_t* s_vals = reinterpret_cast<uint32_t*>(smem_raw + sizeof(K) * kSortTile);
-  __shared__ uint32_t s_match[kWarps][kRadix];
+  KI* s_keys = reinterpret_cast<KI*>(smem_raw);  // [kSortTile] staging
+  uint32_t* s_vals = reinterpret_cast<uint32_t*>(smem_raw + sizeof(KI) * kSortTile);
+  __shared__ uint32_t s_match[kMatchBufs][kWarps][kRadix];
   __shared__ uint32_t s_wcnt[kWarps][kRadix];
   __shared__ uint32_t s_hist[kRadix];
   __shared__ uint32_t s_local_start[kRadix];
@@ -191,82 +240,49 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
   __shared__ uint32_t s_wsum[kWarps];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int src = plan->src[pass];
+  // selects, not a.keys[src]: a dynamically indexed parameter goes to the stack
+  const KI* __restrict__ kin = static_cast<const KI*>(src ? a.keys[1] : a.keys[0]);
+  KO* __restrict__ kout = static_cast<KO*>(src ? a.keys[0] : a.keys[1]);
+  const uint32_t* __restrict__ vin = src ? a.vals[1] : a.vals[0];
+  uint32_t* __restrict__ vout = src ? a.vals[0] : a.vals[1];
+  // implicit payload on the first pass that moves data: value = input index
+  const bool iota = a.iota_vals && pass == plan->first_active;
+  const int shift = a.shift;
   // tiles are taken by ticket; a CTA loops until the keys run out (with n_dev
   // the grid is a persistent one sized for the device, not for the bound)
   for (;;) {
-  if (tid == 0) s_bid = atomicAdd(counter + pass, 1u);
+  if (tid == 0) s_bid = atomicAdd(a.counter + pass, 1u);
   __syncthreads();
   const uint32_t bid = s_bid;
   const int64_t base = (int64_t)bid * kSortTile;
   if (base >= n) return;
   const int count = (int)min((int64_t)kSortTile, n - base);
-  const int src = plan->src[pass];
-  const K* __restrict__ kin = src ? keys1 : keys0;
-  K* __restrict__ kout = src ? keys0 : keys1;
-  const uint32_t* __restrict__ vin = src ? vals1 : vals0;
-  uint32_t* __restrict__ vout = src ? vals0 : vals1;
-  // implicit payload on the first pass that moves data: value = input index
-  const bool iota = iota_vals && pass == plan->first_active;
-  const int shift = begin_bit + 8 * pass;
 
-#ifdef LMGS_SORT_RELOAD
-  // only the digits stay in registers (4 per word); keys and values are
-  // re-read (L2) for the scatter, which frees ~40 registers per thread
-  uint32_t dg[(kSortItems + 3) / 4];
-  uint32_t pos[kSortItems];
-  const int wbase = warp * 32 * kSortItems;
-  {
-    K key[kSortItems];
-#pragma unroll
-    for (int j = 0; j < kSortItems; ++j) {
-      const int i = wbase + j * 32 + lane;
-      key[j] = i < count ? ld_stream(kin + base + i) : (K)~(K)0;
-    }
-#pragma unroll
-    for (int q = 0; q < (kSortItems + 3) / 4; ++q) dg[q] = 0;
-#pragma unroll
-    for (int j = 0; j < kSortItems; ++j) dg[j >> 2] |= digit_of(key[j], shift) << (8 * (j & 3));
-  }
-#define LMGS_DIGIT(j) ((dg[(j) >> 2] >> (8 * ((j) & 3))) & 0xffu)
-#else
-  K key[kSortItems];
+  KI key[kSortItems];
   uint32_t val[VALS ? kSortItems : 1];
   uint32_t pos[kSortItems];
   const int wbase = warp * 32 * kSortItems;
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const int i = wbase + j * 32 + lane;
-    key[j] = i < count ? ld_stream(kin + base + i) : (K)~(K)0;
-    if (VALS) val[j] = iota ? (uint32_t)(base + i) : (i < count ? ld_stream(vin + base + i) : 0u);
+    key[j] = i < count ? kin[base + i] : (KI)~(KI)0;
+    if (VALS) val[j] = iota ? (uint32_t)(base + i) : (i < count ? vin[base + i] : 0u);
   }
-#define LMGS_DIGIT(j) digit_of(key[j], shift)
-#endif
   // the loads above are in flight while the ranking state is cleared
   for (int i = tid; i < kWarps * kRadix; i += kSortThreads) {
-    (&s_match[0][0])[i] = 0;
+#pragma unroll
+    for (int r = 0; r < kMatchBufs; ++r) (&s_match[r][0][0])[i] = 0;
     (&s_wcnt[0][0])[i] = 0;
   }
   s_hist[tid] = 0;  // kSortThreads == kRadix
   __syncthreads();
-#if defined(LMGS_DBG_COPY) && !defined(LMGS_SORT_RELOAD)
-#pragma unroll
-  for (int j = 0; j < kSortItems; ++j) {
-    const int i = wbase + j * 32 + lane;
-    if (i < count) {
-      kout[base + i] = key[j];
-      if (VALS) vout[base + i] = val[j];
-    }
-  }
-  if (!PERSIST) return;
-  __syncthreads();
-  continue;
-#endif
   // 2. early counts, published with the look-back before ranking
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j)
-    if (wbase + j * 32 + lane < count) atomicAdd(&s_hist[LMGS_DIGIT(j)], 1u);
+    if (wbase + j * 32 + lane < count) atomicAdd(&s_hist[digit_of(key[j], shift)], 1u);
   __syncthreads();
-  uint32_t* lb = lookback + ((int64_t)pass * lb_stride) * kRadix;
+  uint32_t* lb = a.lookback + ((int64_t)pass * a.lb_stride) * kRadix;
   const uint32_t total = s_hist[tid];  // thread d == digit d
   {
     const int d = tid;
@@ -290,11 +306,7 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
     // independent loads (one L2 round trip per window, not per predecessor),
     // then walks it from the nearest one, re-polling only unpublished entries.
     uint32_t excl = 0;
-#ifdef LMGS_DBG_NO_LOOKBACK
-    if (false) {
-#else
     if (bid != 0) {
-#endif
       int64_t look = (int64_t)bid - 1;
       bool done = false;
       while (!done) {
@@ -317,12 +329,66 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
   }
   // 3. stable in-warp ranking, items in (j, lane) order
   const uint32_t lt = lanemask_lt();
-  uint32_t* my_match = s_match[warp];
   uint32_t* my_cnt = s_wcnt[warp];
+#if LMGS_RANK_MODE == 1
+  // peers by MATCH.ANY; the leader advances the warp's digit counter
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const bool valid = wbase + j * 32 + lane < count;
-    const uint32_t d = LMGS_DIGIT(j);
+    const uint32_t d = digit_of(key[j], shift);
+    const uint32_t peers = __match_any_sync(0xffffffffu, valid ? d : 256u + lane);
+    const int leader = __ffs(peers) - 1;
+    uint32_t before = 0;
+    if (valid && lane == leader) {
+      before = my_cnt[d];
+      my_cnt[d] = before + (uint32_t)__popc(peers);
+    }
+    before = __shfl_sync(0xffffffffu, before, leader);
+    pos[j] = before + __popc(peers & lt);
+    __syncwarp();
+  }
+#elif LMGS_RANK_MODE == 2
+  // LMGS_RANK_GROUP items at a time, each with its own match words, so their
+  // shared-memory round trips overlap; the leaders' counter updates are
+  // atomics issued in item order by the one warp
+#pragma unroll
+  for (int j0 = 0; j0 < kSortItems; j0 += LMGS_RANK_GROUP) {
+    uint32_t peers[LMGS_RANK_GROUP];
+#pragma unroll
+    for (int r = 0; r < LMGS_RANK_GROUP; ++r) {
+      const int j = j0 + r;
+      if (wbase + j * 32 + lane < count) atomicOr(&s_match[r][warp][digit_of(key[j], shift)], 1u << lane);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < LMGS_RANK_GROUP; ++r) {
+      const int j = j0 + r;
+      const bool valid = wbase + j * 32 + lane < count;
+      peers[r] = valid ? s_match[r][warp][digit_of(key[j], shift)] : (1u << lane);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < LMGS_RANK_GROUP; ++r) {
+      const int j = j0 + r;
+      const bool valid = wbase + j * 32 + lane < count;
+      const uint32_t d = digit_of(key[j], shift);
+      const int leader = __ffs(peers[r]) - 1;
+      uint32_t before = 0;
+      if (valid && lane == leader) {
+        before = atomicAdd(my_cnt + d, (uint32_t)__popc(peers[r]));
+        s_match[r][warp][d] = 0;
+      }
+      before = __shfl_sync(0xffffffffu, before, leader);
+      pos[j] = before + __popc(peers[r] & lt);
+    }
+    __syncwarp();
+  }
+#else
+  uint32_t* my_match = s_match[0][warp];
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const bool valid = wbase + j * 32 + lane < count;
+    const uint32_t d = digit_of(key[j], shift);
     if (valid) atomicOr(my_match + d, 1u << lane);
     __syncwarp();
     const uint32_t peers = valid ? my_match[d] : (1u << lane);
@@ -338,6 +404,7 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
     pos[j] = before + __popc(peers & lt);
     __syncwarp();
   }
+#endif
   __syncthreads();
   // 4. per digit: exclusive prefix over warps
   {
@@ -355,33 +422,27 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
   for (int j = 0; j < kSortItems; ++j) {
     const int i = wbase + j * 32 + lane;
     if (i < count) {
-      const uint32_t p = pos[j] + my_cnt[LMGS_DIGIT(j)];
-#ifdef LMGS_SORT_RELOAD
-      s_keys[p] = kin[base + i];
-      if (VALS) s_vals[p] = iota ? (uint32_t)(base + i) : vin[base + i];
-#else
+      const uint32_t p = pos[j] + my_cnt[digit_of(key[j], shift)];
       s_keys[p] = key[j];
       if (VALS) s_vals[p] = val[j];
-#endif
     }
   }
-#undef LMGS_DIGIT
   __syncthreads();
   // 6. coalesced write-out: consecutive threads, consecutive staged positions
-  const bool segs = seg_counts && pass == plan->last_active;
+  const bool segs = SEG != kSegNone && a.seg_counts && pass == plan->last_active;
   for (int i = tid; i < count; i += kSortThreads) {
-    const K k = s_keys[i];
+    const KI k = s_keys[i];
     const uint32_t o = s_global[digit_of(k, shift)] + i;
-    st_stream(kout + o, k);
-    if (VALS) st_stream(vout + o, s_vals[i]);
+    kout[o] = out_key<KI, OUT>(k, a);
+    if (VALS) vout[o] = s_vals[i];
     if (segs) {
       // the staged tile is sorted on every key bit sorted so far: runs of one
       // segment are contiguous; a run [i0, i1] adds (i1 + 1) - i0
-      const uint64_t sg = (uint64_t)k >> seg_shift;
-      if (i == 0 || ((uint64_t)s_keys[i - 1] >> seg_shift) != sg)
-        atomicAdd(seg_counts + sg, (uint32_t)(-i));
-      if (i + 1 == count || ((uint64_t)s_keys[i + 1] >> seg_shift) != sg)
-        atomicAdd(seg_counts + sg, (uint32_t)(i + 1));
+      const uint64_t sg = (uint64_t)k >> a.seg_shift;
+      const uint64_t sp = i > 0 ? (uint64_t)s_keys[i - 1] >> a.seg_shift : ~0ull;
+      const uint64_t sn = i + 1 < count ? (uint64_t)s_keys[i + 1] >> a.seg_shift : ~0ull;
+      if (sp != sg) atomicAdd(a.seg_counts + sg, (uint32_t)(-i));
+      if (sn != sg) atomicAdd(a.seg_counts + sg, (uint32_t)(i + 1));
     }
   }
   if (!PERSIST) return;  // one tile per CTA on an exact grid
@@ -389,74 +450,96 @@ __global__ void __launch_bounds__(kSortThreads, LMGS_SORT_MIN_CTAS) k_onesweep(
   }
 }
 
-template <typename K, bool VALS>
+template <typename KI, bool VALS>
 constexpr size_t onesweep_smem() {
-  return sizeof(K) * kSortTile + (VALS ? sizeof(uint32_t) * kSortTile : 0);
+  return sizeof(KI) * kSortTile + (VALS ? sizeof(uint32_t) * kSortTile : 0);
 }
 
-template <typename K, bool VALS, bool PERSIST>
-void launch_onesweep_as(const RadixSortBuffers& b, int64_t n, int begin_bit, int p, int64_t grid,
-                        int64_t blocks, cudaStream_t s) {
-  constexpr size_t smem = onesweep_smem<K, VALS>();
-  k_onesweep<K, VALS, PERSIST><<<(unsigned)grid, kSortThreads, smem, s>>>(
-      static_cast<K*>(b.keys[0]), static_cast<K*>(b.keys[1]), b.vals[0], b.vals[1], n, begin_bit,
-      p, b.plan, b.lookback, b.counters, blocks, b.iota_vals, b.seg_counts, b.seg_shift, b.n_dev);
-}
-
-template <typename K, bool VALS>
-void launch_onesweep(const RadixSortBuffers& b, int64_t n, int begin_bit, int p, int64_t blocks,
-                     cudaStream_t s) {
-  constexpr size_t smem = onesweep_smem<K, VALS>();
+template <typename KI, int OUT, int SEG, bool VALS>
+void launch_pass(const PassArgs& a, int64_t blocks, cudaStream_t s) {
+  constexpr size_t smem = onesweep_smem<KI, VALS>();
   static bool attr_set[kMaxDevices] = {};
   static int occ[kMaxDevices] = {}, sms[kMaxDevices] = {};
   const int dev = current_device();
   if (!attr_set[dev]) {
-    cudaFuncSetAttribute(k_onesweep<K, VALS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    cudaFuncSetAttribute(k_onesweep<K, VALS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    cudaFuncSetAttribute(k_onesweep<KI, OUT, SEG, VALS, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_onesweep<KI, OUT, SEG, VALS, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[dev], k_onesweep<K, VALS, true>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[dev], k_onesweep<KI, OUT, SEG, VALS, true>,
                                                   kSortThreads, smem);
     if (occ[dev] < 1) occ[dev] = 1;
     attr_set[dev] = true;
   }
-  if (!b.n_dev) {
-    launch_onesweep_as<K, VALS, false>(b, n, begin_bit, p, blocks, blocks, s);
+  if (!a.n_dev) {
+    k_onesweep<KI, OUT, SEG, VALS, false><<<(unsigned)blocks, kSortThreads, smem, s>>>(a);
     return;
   }
   // the key count is on the device: a persistent grid takes tiles by ticket
   const int64_t persistent = (int64_t)sms[dev] * occ[dev];
-  launch_onesweep_as<K, VALS, true>(b, n, begin_bit, p, blocks < persistent ? blocks : persistent,
-                                    blocks, s);
+  k_onesweep<KI, OUT, SEG, VALS, true>
+      <<<(unsigned)(blocks < persistent ? blocks : persistent), kSortThreads, smem, s>>>(a);
+}
+
+PassArgs pass_args(const RadixSortBuffers& b, int64_t n, int shift, int p, int64_t blocks) {
+  PassArgs a{};
+  a.keys[0] = b.keys[0];
+  a.keys[1] = b.keys[1];
+  a.vals[0] = b.vals[0];
+  a.vals[1] = b.vals[1];
+  a.n = n;
+  a.shift = shift;
+  a.pass = p;
+  a.plan = b.plan;
+  a.lookback = b.lookback;
+  a.counter = b.counters;
+  a.lb_stride = blocks;
+  a.iota_vals = b.iota_vals;
+  a.seg_counts = b.seg_counts;
+  a.seg_shift = b.seg_shift;
+  a.n_dev = b.n_dev;
+  a.id_mask = 0xffffffffu;
+  return a;
+}
+
+// memsets, the histogram (unless the producer built it) and the plan
+int sort_setup(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_passes, int64_t blocks,
+               bool force_all, cudaStream_t s) {
+  int launched = 0;
+  if (!b.hist_ready) cudaMemsetAsync(b.hist, 0, sizeof(uint32_t) * kMaxPasses * kRadix, s);
+  cudaMemsetAsync(b.counters, 0, sizeof(uint32_t) * kMaxPasses, s);
+  if (blocks > 0 && n_passes > 0)
+    cudaMemsetAsync(b.lookback, 0, sizeof(uint32_t) * (size_t)n_passes * blocks * kRadix, s);
+  if (n > 0 && n_passes > 0 && !b.hist_ready) {
+    int hist_blocks = (int)((n + kSortThreads * 16 - 1) / (kSortThreads * 16));
+    if (hist_blocks > 148 * 4) hist_blocks = 148 * 4;
+    if (b.key_bytes == 4)
+      k_radix_hist<uint32_t><<<hist_blocks, kSortThreads, 0, s>>>(
+          static_cast<const uint32_t*>(b.keys[0]), n, begin_bit, n_passes, b.hist, b.gate);
+    else
+      k_radix_hist<uint64_t><<<hist_blocks, kSortThreads, 0, s>>>(
+          static_cast<const uint64_t*>(b.keys[0]), n, begin_bit, n_passes, b.hist, b.gate);
+    ++launched;
+  }
+  k_radix_plan<<<1, kRadix, 0, s>>>(b.hist, n, n_passes, b.plan, b.gate, b.keys[0], b.keys[1],
+                                    b.vals[0], b.vals[1], b.keys_result, b.vals_result, b.n_dev,
+                                    b.max_n, force_all);
+  return launched + 1;
 }
 
 template <typename K>
 int radix_sort_impl(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_passes,
                     cudaStream_t s) {
-  int launched = 0;
   if (n_passes > kMaxPasses) n_passes = kMaxPasses;
   const int64_t blocks = (n + kSortTile - 1) / kSortTile;
-  if (!b.hist_ready) cudaMemsetAsync(b.hist, 0, sizeof(uint32_t) * kMaxPasses * kRadix, s);
-  cudaMemsetAsync(b.counters, 0, sizeof(uint32_t) * kMaxPasses, s);
-  if (blocks > 0 && n_passes > 0)
-    cudaMemsetAsync(b.lookback, 0, sizeof(uint32_t) * (size_t)n_passes * blocks * kRadix, s);
-  K* k0 = static_cast<K*>(b.keys[0]);
-  K* k1 = static_cast<K*>(b.keys[1]);
-  if (n > 0 && n_passes > 0 && !b.hist_ready) {
-    int hist_blocks = (int)((n + kSortThreads * 16 - 1) / (kSortThreads * 16));
-    if (hist_blocks > 148 * 4) hist_blocks = 148 * 4;
-    k_radix_hist<K><<<hist_blocks, kSortThreads, 0, s>>>(k0, n, begin_bit, n_passes, b.hist,
-                                                         b.gate);
-    ++launched;
-  }
-  k_radix_plan<<<1, kRadix, 0, s>>>(b.hist, n, n_passes, b.plan, b.gate, k0, k1, b.vals[0],
-                                    b.vals[1], b.keys_result, b.vals_result, b.n_dev, b.max_n);
-  ++launched;
+  int launched = sort_setup(b, n, begin_bit, n_passes, blocks, false, s);
   if (blocks == 0) return launched;
   for (int p = 0; p < n_passes; ++p) {
-    if (b.vals[1]) launch_onesweep<K, true>(b, n, begin_bit, p, blocks, s);
-    else launch_onesweep<K, false>(b, n, begin_bit, p, blocks, s);
+    const PassArgs a = pass_args(b, n, begin_bit + 8 * p, p, blocks);
+    if (b.vals[1]) launch_pass<K, kOutSame, kSegNone, true>(a, blocks, s);
+    else if (b.seg_counts) launch_pass<K, kOutSame, kSegKey, false>(a, blocks, s);
+    else launch_pass<K, kOutSame, kSegNone, false>(a, blocks, s);
   }
   return launched + n_passes;
 }
@@ -472,6 +555,19 @@ int radix_sort(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_passes
                cudaStream_t s) {
   if (b.key_bytes == 4) return radix_sort_impl<uint32_t>(b, n, begin_bit, n_passes, s);
   return radix_sort_impl<uint64_t>(b, n, begin_bit, n_passes, s);
+}
+
+int tile_sort(const RadixSortBuffers& b, int64_t k, int tile_bits, cudaStream_t s) {
+  const int n_passes = tile_bits ? (tile_bits + 7) / 8 : 1;
+  const int64_t blocks = (k + kSortTile - 1) / kSortTile;
+  int launched = sort_setup(b, k, 32, n_passes, blocks, true, s);
+  if (blocks == 0) return launched;
+  for (int p = 0; p < n_passes; ++p) {
+    const PassArgs a = pass_args(b, k, 32 + 8 * p, p, blocks);
+    if (p + 1 == n_passes) launch_pass<uint64_t, kOutIds, kSegKey, false>(a, blocks, s);
+    else launch_pass<uint64_t, kOutSame, kSegNone, false>(a, blocks, s);
+  }
+  return launched + n_passes;
 }
 
 }  // namespace lmgs

@@ -393,15 +393,17 @@ __global__ void __launch_bounds__(kScanThreads) k_ranges_from_counts(const uint3
   }
 }
 
-// instance export: keys = tile << 32 | row, prims = original id
-__global__ void k_export(InstanceExportArgs a) {
-  const uint64_t* __restrict__ keys = static_cast<const uint64_t*>(*a.keys_slot);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.k; i += stride) {
-    const uint64_t key = keys[i];
-    const uint32_t id = (uint32_t)key;
-    if (a.keys_out) a.keys_out[i] = key;
-    if (a.prims_out) a.prims_out[i] = a.prim_ids ? a.prim_ids[id] : (int64_t)id;
+// instance export: keys = tile << 32 | row, prims = original id; one CTA per
+// tile (the sorted ids carry no tile bits: the tile is the range's)
+__global__ void k_export(InstanceExportArgs a, int tiles) {
+  const uint32_t* __restrict__ ids = static_cast<const uint32_t*>(*a.keys_slot);
+  for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int2 r = a.ranges[t];
+    for (int64_t i = r.x + (int64_t)threadIdx.x; i < r.y && i < a.k; i += blockDim.x) {
+      const uint32_t id = ids[i];
+      if (a.keys_out) a.keys_out[i] = ((uint64_t)t << 32) | id;
+      if (a.prims_out) a.prims_out[i] = a.prim_ids ? a.prim_ids[id] : (int64_t)id;
+    }
   }
 }
 
@@ -446,8 +448,8 @@ int launch_ranges_from_counts(const uint32_t* counts, int tiles, int2* ranges, i
 }
 
 void launch_export_instances(const InstanceExportArgs& a, cudaStream_t s) {
-  if (a.k <= 0) return;
-  k_export<<<grid_for(a.k, 256), 256, 0, s>>>(a);
+  if (a.k <= 0 || a.tiles <= 0) return;
+  k_export<<<a.tiles < 148 * 16 ? a.tiles : 148 * 16, 128, 0, s>>>(a, a.tiles);
 }
 
 }  // namespace lmgs

@@ -56,11 +56,11 @@ struct FixIn {
   float m0, m1, m2, sc0, sc1, sc2, logit;
 };
 
-__device__ __forceinline__ void load_rec(const TouchedFixArgs& a, const uint64_t* list,
+__device__ __forceinline__ void load_rec(const TouchedFixArgs& a, const uint32_t* list,
                                          int2 range, int j, FixRec& r) {
   r.valid = j < range.y;
   if (r.valid) {
-    r.id = (uint32_t)list[j];
+    r.id = list[j];
     const double2* r16 = reinterpret_cast<const double2*>(a.recs + r.id);
     r.s0 = r16[0];
     r.s1 = r16[1];
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kFixThreads) k_touched_fix(TouchedFixArgs a) {
   __shared__ int s_done;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t n = *a.fix_count;  // <= W * H = the queue's capacity
-  const uint64_t* __restrict__ list = static_cast<const uint64_t*>(*a.keys_slot);
+  const uint32_t* __restrict__ list = static_cast<const uint32_t*>(*a.keys_slot);
   const CamArgs& cam = a.cam;
   const int ts = a.tile_size;
   for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
