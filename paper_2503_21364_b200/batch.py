@@ -42,11 +42,12 @@ def alg_bytes_per_view(n, s_read, group, n_vis, k, tiles, tile_passes, processed
         "depth_sort": n * (12 + 12 + 16 + 16 + 4),
         # ranked ids 4 B + rect gather 8 B per visible splat, 8-B key per instance
         "emit": 12 * n_vis + 8 * k,
-        # each pass reads and writes every 8-B key; ranges 8 B per tile
-        "tile_sort": 16 * tile_passes * k + 8 * tiles,
-        # per processed instance an 8-B key + 64-B record; rgb, alpha, depth per
+        # each pass reads every 8-B key; all but the last write 8-B keys, the
+        # last writes the 4-B ids; ranges 8 B per tile
+        "tile_sort": (16 * tile_passes - 4) * k + 8 * tiles,
+        # per processed instance a 4-B id + 64-B record; rgb, alpha, depth per
         # pixel; one range per tile; touched per Gaussian
-        "blend": 72 * processed + 8 * tiles + 20 * pixels + 4 * n,
+        "blend": 68 * processed + 8 * tiles + 20 * pixels + 4 * n,
     }
 
 
