@@ -198,6 +198,22 @@ def throughput(frames_per_step_total: int, steps: int, ms_max: float) -> float:
 # reference arm: the CPU implementation of the path (oracle port), host cores
 
 
+def arm_config(args, world):
+    """The workload both arms report (the reference arm times a bounded sample
+    of it, described in its cpu_baseline.sample)."""
+    views = args.views
+    my_views = views // world  # rank 0's shard (distributed.camera_shard)
+    return {"workload": f"c3: 6M Gaussians (SH3), 1920x1080, batch of {views} orbit "
+                        f"views per step split over {world} GPU(s), tile 16",
+            "gaussians": N_GAUSS, "views_per_step": views, "views_per_gpu": my_views,
+            "width": W, "height": H, "parallelism": f"camera-batch dp{world}",
+            "views_per_k1_launch": args.group, "launch_mode": args.mode,
+            "l2": "no flush: scene 1.42 GB and per-view buffers > 126 MB L2",
+            "geometry": "fp64 (bit-exact tile lists)", "blend": "fp32",
+            "scene_replication": "rank 0 generates, NCCL broadcast" if world > 1
+            else "single rank"}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -225,8 +241,7 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": "c3: 6M Gaussians, 1920x1080, SH3, "
-                                                    "one full view per step (bounded sample)"},
+        "data": "synthetic", "config": arm_config(args, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": "one full 1080p view of the 6M-Gaussian scene per step "
                                    "(oracle/oracle.c fp64 restatement, OpenMP)"},
@@ -534,15 +549,7 @@ def make_line(args, world, views, my_views, value, ms_per_step, stage, clocks, e
         "ms_per_frame": ms_per_step / views,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": f"c3: 6M Gaussians (SH3), 1920x1080, batch of {views} orbit "
-                               f"views per step split over {world} GPU(s), tile 16",
-                   "gaussians": N_GAUSS, "views_per_step": views, "views_per_gpu": my_views,
-                   "width": W, "height": H, "parallelism": f"camera-batch dp{world}",
-                   "views_per_k1_launch": args.group, "launch_mode": args.mode,
-                   "l2": "no flush: scene 1.42 GB and per-view buffers > 126 MB L2",
-                   "geometry": "fp64 (bit-exact tile lists)", "blend": "fp32",
-                   "scene_replication": "rank 0 generates, NCCL broadcast" if world > 1
-                   else "single rank"},
+        "config": arm_config(args, world),
         "gpu_launches": launches(stage) * args.steps,
         "e2e": e2e,
         "latency_ms_single_view": latency,
