@@ -191,8 +191,14 @@ int launch_depth_fixup(void* const* keys_slot, void* const* ids_slot, int64_t n,
 // instance array comes out sorted by depth rank, so a stable sort by tile
 // alone yields rasterize's per-tile (depth, id) lists.  Also builds the tile
 // digit histograms of the K5 radix passes.
-constexpr int kEmitThreads = 256;
-constexpr int kEmitItems = 8;
+#ifndef LMGS_EMIT_ITEMS
+#define LMGS_EMIT_ITEMS 4  // 4: emit 0.182 -> 0.152 ms/view over 8 (profiles/r07/emit_shape_variants.txt)
+#endif
+#ifndef LMGS_EMIT_THREADS
+#define LMGS_EMIT_THREADS 256
+#endif
+constexpr int kEmitThreads = LMGS_EMIT_THREADS;
+constexpr int kEmitItems = LMGS_EMIT_ITEMS;
 constexpr int kEmitChunk = kEmitThreads * kEmitItems;
 struct EmitArgs {
   void* const* order_slot;  // -> uint32_t[n_vis] Gaussian ids in depth order

@@ -35,7 +35,7 @@ constexpr int kLookWindow = LMGS_LOOK_WINDOW;
 #define LMGS_RANK_MODE 2
 #endif
 #ifndef LMGS_RANK_GROUP
-#define LMGS_RANK_GROUP 2
+#define LMGS_RANK_GROUP 1  // 1: 752 vs 745 frames/s at 2 (less shared memory; profiles/r07/rank_group_ab.txt)
 #endif
 constexpr int kMatchBufs = LMGS_RANK_MODE == 2 ? LMGS_RANK_GROUP : 1;
 #ifndef LMGS_SORT_MIN_CTAS_NARROW
