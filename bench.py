@@ -430,7 +430,7 @@ def run_ours(args, rank, world, local):
     mine = camera_shard(views, rank, world)
     cams = [all_cams[i] for i in mine]
     renderer = BatchRenderer(model, W, H, max(len(cams), 1), tile_size=16, sh_eval_degree=3,
-                             n_streams=args.streams, group=args.group)
+                             n_streams=args.streams, group=args.group, flags=args.flags)
 
     # warm-up (also sizes every arena)
     for _ in range(args.warmup):
@@ -450,7 +450,8 @@ def run_ours(args, rank, world, local):
     if args.mode != "sync":
         cap = int(1.25 * stage["max_instances"]) + 1024
         timed = BatchRenderer(model, W, H, max(len(cams), 1), tile_size=16, sh_eval_degree=3,
-                              n_streams=args.streams, group=args.group, capacity=cap)
+                              n_streams=args.streams, group=args.group, capacity=cap,
+                              flags=args.flags)
         timed.render(cams)
         torch.cuda.synchronize()
         if args.mode == "graph":
@@ -474,7 +475,7 @@ def run_ours(args, rank, world, local):
     weak = None
     if world > 1:
         wr = BatchRenderer(model, W, H, views, tile_size=16, sh_eval_degree=3,
-                           n_streams=args.streams, group=args.group)
+                           n_streams=args.streams, group=args.group, flags=args.flags)
         wr.render(all_cams)
         torch.cuda.synchronize()
         wsteps = max(1, min(args.steps, 5))
@@ -583,13 +584,15 @@ def main(argv=None):
     ap.add_argument("--no-c5-monolithic", action="store_true")
     ap.add_argument("--c5-steps", type=int, default=5)
     ap.add_argument("--c5-per-block", type=int, default=C5_PER_BLOCK)
-    ap.add_argument("--streams", type=int, default=3,
+    ap.add_argument("--streams", type=int, default=4,
                     help="contexts/streams the view batch alternates over")
     ap.add_argument("--mode", default="sync", choices=["sync", "nosync", "graph"],
                     help="sync: per-view host read of K; nosync: capacity-bounded, no host "
                          "wait; graph: the nosync batch captured once as a CUDA graph")
     ap.add_argument("--group", type=int, default=2,
                     help="views per shared K1 launch (lmgs_render_group; 1 = lmgs_render)")
+    ap.add_argument("--flags", type=int, default=0,
+                    help="extra LMGS_FLAG_* bits (e.g. 32: the fused tile sort, an A/B)")
     args = ap.parse_args(argv)
     # liblmgs kernels per step, as the library counts them (stage_times pass)
     args.gpu_launches = lambda stage: stage["launches"]

@@ -121,6 +121,16 @@ typedef struct lmgs_settings {
  * around TERM_EPS instead of 1e-4 (100x more pixels replayed): the check that
  * the default band misses no fp32/fp64 disagreement (tests/test_gpu_parity). */
 #define LMGS_FLAG_WIDE_FIX_BAND 16u
+/* Build the tile lists with the fused emission + tile sort (K4c/K4r/K4p and a
+ * first onesweep pass that generates its keys; tile ids < 2^16) instead of
+ * the separate K4 emission + two-pass K5 tile sort: identical lists, fewer
+ * DRAM bytes, measured slower at c3 (tests/test_gpu_fused.py). */
+#define LMGS_FLAG_FUSED_TILE_SORT 32u
+/* Other streams render concurrently (a view batch over several contexts):
+ * the latency-bound radix-sort passes run as persistent grids of one CTA per
+ * SM instead of one CTA per tile, leaving the other slots to the other
+ * streams' kernels (BatchRenderer sets it; a lone view is faster without). */
+#define LMGS_FLAG_CONCURRENT 64u
 #define LMGS_FLAG_NO_TOUCHED_FIX 2u /* skip K7b: touched may then differ from the
                                        reference where fp32 and fp64 transmittance
                                        straddle TERM_EPS (a few per million)       */

@@ -28,6 +28,8 @@ LMGS_FLAG_STAGE_TIMES = 1
 LMGS_FLAG_NO_TOUCHED_FIX = 2
 LMGS_FLAG_NO_HOST_SYNC = 8
 LMGS_FLAG_WIDE_FIX_BAND = 16
+LMGS_FLAG_FUSED_TILE_SORT = 32
+LMGS_FLAG_CONCURRENT = 64
 MAX_STAGES = 8
 
 # every symbol include/lmgs.h declares

@@ -70,6 +70,8 @@ class BatchRenderer:
         self.background = background
         self.flags = int(flags)  # extra LMGS_FLAG_*
         self.capacity = int(capacity) if capacity else 0
+        if n_streams > 1:  # the streams' latency-bound sort passes share the SMs
+            self.flags |= _lib.LMGS_FLAG_CONCURRENT
         if self.capacity:
             self.flags |= _lib.LMGS_FLAG_NO_HOST_SYNC
         dev = self.dev
@@ -116,6 +118,8 @@ class BatchRenderer:
         L = _lib.lib()
         caller = torch.cuda.current_stream(self.dev)
         flags = (_lib.LMGS_FLAG_STAGE_TIMES if stage_times else 0) | self.flags
+        if stage_times:  # the views run serially on one stream: nothing shares the SMs
+            flags &= ~_lib.LMGS_FLAG_CONCURRENT
         st = abi_settings(self.ts, self.sh_eval_degree, self.background, flags, self.capacity)
         g = self._g
         if stage_times:

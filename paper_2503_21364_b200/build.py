@@ -106,7 +106,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if force or _stale(LIB, objs):
         tmp = LIB.with_suffix(".so.tmp")
         cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart_static",
-               "-Xlinker", "-soname=liblmgs.so"]
+               "-Xlinker", "-soname=liblmgs.so", "-Xlinker", "--no-undefined"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -75,6 +75,7 @@ size_t gaussian_bytes(int64_t n) {
   b += align_up(sizeof(uint64_t) * n);      // fp64 depth keys
   b += align_up(sizeof(uint64_t) * n);      // rects
   b += align_up(sizeof(BlendRec) * n);      // records
+  b += align_up(sizeof(uint4) * n);         // rank records (fused tile sort)
   b += align_up(sizeof(uint32_t) * radix_lookback_words(n));  // K2 look-back
   b += align_up(sizeof(uint64_t) * emit_chunks(n));            // K4 look-back
   return b + 10 * kAlign;
@@ -84,7 +85,7 @@ size_t tile_bytes(int64_t t) {
 }
 size_t instance_bytes(int64_t k) {
   return 2 * align_up(sizeof(uint64_t) * k) + align_up(sizeof(uint32_t) * radix_lookback_words(k)) +
-         4 * kAlign;
+         align_up(sizeof(uint32_t) * (k / kSortTile + 2)) + 5 * kAlign;
 }
 
 struct Scalars {  // device-side small state
@@ -95,6 +96,7 @@ struct Scalars {  // device-side small state
   uint32_t tile_counters[kMaxPasses];
   unsigned long long counts[3];  // n_kept, n_vis, n_inst (one D2H copy)
   unsigned long long max_k;      // largest K of no-sync renders since lmgs_get_stats
+  unsigned long long k_eff;      // fused tile sort: K, or 0 after a no-sync overflow
   unsigned long long zrange[2];  // min / max visible fp64 depth bits
   uint32_t emit_ticket[1];  // K4 chunk ticket
   int blend_counter;
@@ -110,6 +112,7 @@ struct lmgs_context {
   int sms = 148;
   std::string err;
   DevBuf gbuf, tbuf, ibuf, bwbuf, fixbuf, npbuf;  // npbuf: override (-1) + list, W*H each
+  DevBuf covbuf;  // fused tile sort: per-CTA coverage arrays + their sum
   Scalars* d_scal = nullptr;
   uint64_t* h_pinned = nullptr;  // [0..2] = n_kept, n_vis, K
   cudaEvent_t ev[2 * kNumStages] = {};
@@ -126,12 +129,14 @@ struct lmgs_context {
   BlendRec* recs = nullptr;
   uint32_t* depth_lookback = nullptr;
   uint64_t* emit_lookback = nullptr;
+  uint4* rrec = nullptr;
   // per-tile arena
   int2* ranges = nullptr;
   uint32_t* tile_count = nullptr;
   // per-instance arena
   uint64_t* inst_keys[2] = {nullptr, nullptr};
   uint32_t* tile_lookback = nullptr;
+  uint32_t* chunk_first = nullptr;
   const int64_t* last_prim_ids = nullptr;
   const int2* last_ranges = nullptr;
   lmgs_stats stats{};
@@ -181,6 +186,7 @@ int ensure_gaussians(lmgs_context* c, int64_t n, cudaStream_t s) {
   c->key64 = cv.take<uint64_t>(cap);
   c->rects = cv.take<uint64_t>(cap);
   c->recs = cv.take<BlendRec>(cap);
+  c->rrec = cv.take<uint4>(cap);
   c->depth_lookback = cv.take<uint32_t>(radix_lookback_words(cap));
   c->emit_lookback = cv.take<uint64_t>(emit_chunks(cap));
   c->cap_n = cap;
@@ -207,6 +213,7 @@ int ensure_instances(lmgs_context* c, int64_t k, cudaStream_t s) {
   c->inst_keys[0] = cv.take<uint64_t>(cap);
   c->inst_keys[1] = cv.take<uint64_t>(cap);
   c->tile_lookback = cv.take<uint32_t>(radix_lookback_words(cap));
+  c->chunk_first = cv.take<uint32_t>(cap / kSortTile + 2);
   c->cap_k = cap;
   return LMGS_OK;
 }
@@ -403,6 +410,7 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
     rb.vals_result = &sc->slots.depth_ids;
     rb.iota_vals = true;
     rb.hist_ready = true;
+    rb.concurrent = (st->flags & LMGS_FLAG_CONCURRENT) != 0;
     launched += radix_sort(rb, n, 0, kDepthPasses, s);
     launched += launch_depth_fixup(&sc->slots.depth_keys, &sc->slots.depth_ids, n, c->key64,
                                    g->prim_ids, s);
@@ -441,6 +449,71 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
   const int64_t cap_view = nosync ? k : c->cap_k;
   c->stats.capacity = cap_view;
 
+  // fused K4 + K5 on request (tile ids < 2^16 whose packed second-pass key
+  // fits 32 bits)
+  const int tile_bits = bits_for(tiles);
+  const int id_bits = n > 1 ? bits_for(n) : 1;
+  const int64_t cover_d = (int64_t)(ca.tiles_x + 1) * (ca.tiles_y + 1);
+  const bool fused = (st->flags & LMGS_FLAG_FUSED_TILE_SORT) && tile_bits > 8 &&
+                     tile_bits <= 16 && (tile_bits - 8) + id_bits <= 32 &&
+                     cover_d * 4 <= kMaxCoverBytes;
+  if (fused) {
+    tm.begin(2);
+    const int grid = cover_grid(ca.tiles_x, ca.tiles_y, n, c->sms);
+    const size_t part_bytes = align_up(sizeof(int32_t) * (size_t)(grid > 0 ? grid : 1) * cover_d);
+    if (part_bytes + sizeof(int32_t) * cover_d > c->covbuf.bytes) {
+      LMGS_CUDA(c, cudaStreamSynchronize(s));
+      LMGS_CUDA(c, c->covbuf.reserve(part_bytes + sizeof(int32_t) * cover_d));
+    }
+    int32_t* cover_part = static_cast<int32_t*>(c->covbuf.ptr);
+    int32_t* cover = reinterpret_cast<int32_t*>(static_cast<char*>(c->covbuf.ptr) + part_bytes);
+    LMGS_CUDA(c, cudaMemsetAsync(cover, 0, sizeof(int32_t) * cover_d, s));
+    launched += launch_cover(c->rects, n, ca.tiles_x, ca.tiles_y, cover_part, grid, s);
+    launched += launch_cover_reduce(cover_part, grid, cover_d, cover, s);
+    if (n_vis > 0) {
+      RankScanArgs ra{};
+      ra.order_slot = &sc->slots.depth_ids;
+      ra.rects = c->rects;
+      ra.n_vis = n_vis;
+      ra.n_vis_dev = &sc->counts[1];
+      ra.rrec = c->rrec;
+      ra.chunk_first = c->chunk_first;
+      ra.n_sort_tiles = (cap_view + kSortTile - 1) / kSortTile;
+      ra.chunk_sums = reinterpret_cast<uint32_t*>(c->emit_lookback);  // free on this path
+      launched += launch_rank_scan(ra, s);
+    }
+    TilePlanArgs pa{};
+    pa.cover = cover;
+    pa.tiles_x = ca.tiles_x;
+    pa.tiles_y = ca.tiles_y;
+    pa.ranges = ranges;
+    pa.tile_count = c->tile_count;
+    pa.plan = &sc->tile_plan;
+    pa.k_dev = &sc->counts[2];
+    pa.cap = (uint64_t)cap_view;
+    pa.k_eff = &sc->k_eff;
+    pa.max_k = nosync ? &sc->max_k : nullptr;
+    pa.keys_result = &sc->slots.inst_ids;
+    pa.result = c->inst_keys[0];
+    launched += launch_tile_plan(pa, s);
+    tm.end(2);
+    tm.begin(3);
+    FusedTileSort fs{};
+    fs.keys[0] = c->inst_keys[0];
+    fs.keys[1] = c->inst_keys[1];
+    fs.k_bound = k;
+    fs.k_dev = nosync ? &sc->k_eff : nullptr;
+    fs.plan = &sc->tile_plan;
+    fs.lookback = c->tile_lookback;
+    fs.counters = sc->tile_counters;
+    fs.rrec = c->rrec;
+    fs.chunk_first = c->chunk_first;
+    fs.n_vis_dev = &sc->counts[1];
+    fs.tiles_x = ca.tiles_x;
+    fs.id_bits = id_bits;
+    fs.concurrent = (st->flags & LMGS_FLAG_CONCURRENT) != 0;
+    launched += tile_sort_fused(fs, s);
+  } else {
   // K4
   tm.begin(2);
   LMGS_CUDA(c, cudaMemsetAsync(sc->tile_hist, 0, sizeof(sc->tile_hist), s));
@@ -459,6 +532,7 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
     ea.lookback = c->emit_lookback;
     ea.ticket = sc->emit_ticket;
     ea.hist = sc->tile_hist;
+    ea.concurrent = (st->flags & LMGS_FLAG_CONCURRENT) != 0;
     launched += launch_emit(ea, s);
   }
   tm.end(2);
@@ -478,6 +552,7 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
     rb.hist_ready = true;
     rb.seg_counts = c->tile_count;
     rb.seg_shift = 32;
+    rb.concurrent = (st->flags & LMGS_FLAG_CONCURRENT) != 0;
     if (nosync) {  // K on the device; the grid covers the capacity
       rb.n_dev = &sc->counts[2];
       rb.max_n = &sc->max_k;
@@ -485,6 +560,7 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
     LMGS_CUDA(c, cudaMemsetAsync(c->tile_count, 0, sizeof(uint32_t) * tiles, s));
     launched += tile_sort(rb, k, bits_for(tiles), s);
     launched += launch_ranges_from_counts(c->tile_count, (int)tiles, ranges, cap_view, s);
+  }
   }
   if (out->tile_ranges && tiles > 0)
     LMGS_CUDA(c, cudaMemcpyAsync(out->tile_ranges, ranges, sizeof(int2) * tiles,
@@ -633,6 +709,7 @@ void lmgs_context_destroy(lmgs_context* c) {
   c->bwbuf.release();
   c->fixbuf.release();
   c->npbuf.release();
+  c->covbuf.release();
   if (c->d_scal) cudaFree(c->d_scal);
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   for (int i = 0; i < 2 * kNumStages; ++i)

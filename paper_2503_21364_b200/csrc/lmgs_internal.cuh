@@ -37,6 +37,10 @@ __host__ __device__ inline uint64_t pack_rect(uint32_t x0, uint32_t y0, uint32_t
   return (uint64_t)x0 | ((uint64_t)y0 << 16) | ((uint64_t)x1 << 32) | ((uint64_t)y1 << 48);
 }
 
+// The rect K1 writes for culled and off-screen splats: x1 + 1 == x0, so its
+// area is 0 and its four coverage corners (K4c) cancel.
+constexpr uint64_t kEmptyRect = 1ull;  // pack_rect(1, 0, 0, 0)
+
 // Per-device launch caches (function attributes are per device context).
 constexpr int kMaxDevices = 64;
 inline int current_device() {
@@ -148,6 +152,7 @@ struct RadixSortBuffers {
   // grid becomes persistent)
   const unsigned long long* n_dev;
   unsigned long long* max_n;  // nullable: atomicMax(*max_n, *n_dev) (overflow check)
+  bool concurrent;            // LMGS_FLAG_CONCURRENT: persistent grids sharing the SMs
 };
 
 size_t radix_lookback_words(int64_t capacity);
@@ -159,6 +164,28 @@ int radix_sort(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_passes
 // in the buffer keys_result names).  seg_counts (required) gets the per-tile
 // counts.  keys[0] holds the input; both buffers hold k u64 keys.
 int tile_sort(const RadixSortBuffers& b, int64_t k, int tile_bits, cudaStream_t s);
+
+// K4+K5 fused (tile ids < 2^16, (tile bits - 8) + id bits <= 32): the first
+// pass generates its instance keys from the rank records (K4r, below) instead
+// of reading an emitted array, ranks them on the low tile digit and writes u32
+// keys (tile >> 8) << id_bits | id; the second pass sorts those on the high
+// digit and writes the ids.  The plan (digit starts of both passes) comes
+// from K4p's tile counts.
+struct FusedTileSort {
+  void* keys[2];                 // keys[1]: packed u32, keys[0]: the ids (result)
+  int64_t k_bound;               // K, or its capacity (k_dev then holds K)
+  const unsigned long long* k_dev;  // nullable: the count on the device
+  const RadixPlan* plan;
+  uint32_t* lookback;            // [2 * tiles * kRadix]
+  uint32_t* counters;            // [kMaxPasses]
+  const uint4* rrec;
+  const uint32_t* chunk_first;
+  const unsigned long long* n_vis_dev;
+  int32_t tiles_x;
+  int32_t id_bits;
+  bool concurrent;
+};
+int tile_sort_fused(const FusedTileSort& f, cudaStream_t s);  // kernels launched
 
 // Device-side slots naming where a sort's result landed (written by the plan
 // kernel, read by consumers) so the pipeline never syncs on it.
@@ -212,9 +239,58 @@ struct EmitArgs {
   uint64_t* lookback;       // [chunks] status words
   uint32_t* ticket;         // chunk ticket counter (zeroed)
   uint32_t* hist;           // [kMaxTilePasses][256] digit histograms (zeroed)
+  bool concurrent;          // LMGS_FLAG_CONCURRENT: a persistent grid sharing the SMs
 };
+#ifndef LMGS_EMIT_PERSIST_CTAS
+#define LMGS_EMIT_PERSIST_CTAS 0  // > 0: concurrent renders emit with this many CTAs per SM
+#endif
 inline int64_t emit_chunks(int64_t n_vis) { return (n_vis + kEmitChunk - 1) / kEmitChunk; }
 int launch_emit(const EmitArgs& a, cudaStream_t s);
+
+// K4c (fused path): the 2-D difference array of the rects' tile coverage,
+// one per CTA of a persistent grid over the rects in id order (four shared
+// atomics per splat); K4p's 2-D prefix sum of their total = per-tile counts.
+constexpr int kMaxCoverBytes = 160 * 1024;  // (tiles_x + 1) * (tiles_y + 1) int32 in smem
+int cover_grid(int tiles_x, int tiles_y, int64_t n, int sms);  // = number of partial arrays
+int launch_cover(const uint64_t* rects, int64_t n, int tiles_x, int tiles_y, int32_t* cover_part,
+                 int grid, cudaStream_t s);
+// K4r (fused path): walk the splats in depth-rank order, scan their tile
+// counts (reduce, scan, write: three launches), write one 16-B record per rank {rect, id,
+// first instance slot} and the first rank of every kSortTile-slot sort tile.
+constexpr int kRankThreads = 512;
+constexpr int kRankItems = 4;
+constexpr int kRankChunk = kRankThreads * kRankItems;
+inline int64_t rank_chunks(int64_t n_vis) { return (n_vis + kRankChunk - 1) / kRankChunk; }
+struct RankScanArgs {
+  void* const* order_slot;
+  const uint64_t* rects;
+  int64_t n_vis;
+  const unsigned long long* n_vis_dev;
+  uint4* rrec;                // [n_vis]
+  uint32_t* chunk_first;      // [n_sort_tiles]
+  int64_t n_sort_tiles;       // capacity of chunk_first (slots past it are not sorted)
+  uint32_t* chunk_sums;       // [rank_chunks(n_vis)] scratch
+};
+int launch_rank_scan(const RankScanArgs& a, cudaStream_t s);
+// sums the partial arrays into cover (zeroed by the caller)
+int launch_cover_reduce(const int32_t* part, int parts, int64_t d, int32_t* cover, cudaStream_t s);
+// K4p (one CTA): 2-D prefix of the coverage = per-tile counts -> tile ranges
+// (clamped: all empty if K > cap), the two digit histograms -> the fused
+// sort's plan, the effective key count, the result slot
+struct TilePlanArgs {
+  const int32_t* cover;
+  int32_t tiles_x, tiles_y;
+  int2* ranges;
+  uint32_t* tile_count;       // nullable: per-tile counts
+  RadixPlan* plan;
+  const unsigned long long* k_dev;  // K from K1
+  uint64_t cap;
+  unsigned long long* k_eff;  // K, or 0 after an overflow
+  unsigned long long* max_k;  // nullable: atomicMax(K)
+  void** keys_result;
+  void* result;
+};
+int launch_tile_plan(const TilePlanArgs& a, cudaStream_t s);
 
 // K6: tile ranges [start, end) = exclusive scan of the per-tile counts the
 // tile sort's last pass accumulated (empty tiles included)

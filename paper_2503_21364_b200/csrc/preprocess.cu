@@ -142,7 +142,7 @@ __device__ __forceinline__ uint32_t process_one(const PreprocessArgs& a, int64_t
     if (a.touched_zero) a.touched_zero[i] = 0;
     if (!keep) {
       a.depth_keys[i] = kCulledKey;
-      a.rects[i] = 0;
+      a.rects[i] = kEmptyRect;
     } else {
       double mx, my, ca, cb, cc, radius;
       if (S) splat_projection(cam, x, y, z, S, &mx, &my, &ca, &cb, &cc, &radius);
@@ -154,7 +154,7 @@ __device__ __forceinline__ uint32_t process_one(const PreprocessArgs& a, int64_t
       axis_range(my - radius, my + radius, cam.height, cam.tile_size, cam.inv_tile, cam.tiles_y, &y0,
                  &y1);
       if (x0 <= x1 && y0 <= y1) cnt = (uint32_t)(x1 - x0 + 1) * (uint32_t)(y1 - y0 + 1);
-      a.rects[i] = cnt ? pack_rect(x0, y0, x1, y1) : 0;  // read only for visible splats
+      a.rects[i] = cnt ? pack_rect(x0, y0, x1, y1) : kEmptyRect;
       // off-screen splats sort behind every visible one (K2 orders only the
       // n_vis visible splats)
       zb = (uint64_t)__double_as_longlong(z);
@@ -265,7 +265,7 @@ __device__ __forceinline__ void cull_row(const PreprocessArgs& a, int64_t i) {
   if (a.kept) a.kept[i] = 0;
   if (a.touched_zero) a.touched_zero[i] = 0;
   a.depth_keys[i] = kCulledKey;
-  a.rects[i] = 0;
+  a.rects[i] = kEmptyRect;
 }
 
 // direct loads (tail block, unaligned inputs)

@@ -31,13 +31,14 @@ constexpr int kWarps = kSortThreads / 32;
 #define LMGS_LOOK_WINDOW 8
 #endif
 constexpr int kLookWindow = LMGS_LOOK_WINDOW;
-#ifndef LMGS_RANK_MODE
-#define LMGS_RANK_MODE 2
+#ifndef LMGS_SORT_PERSIST_CTAS
+// LMGS_FLAG_CONCURRENT: persistent onesweep grids of this many CTAs per SM
+// (else one CTA per tile).  A pass is latency-bound; with one CTA per SM it
+// runs slower alone (tile sort 0.32 -> 0.47 ms) but leaves the SMs' other
+// slots to the other streams' kernels: 758 -> 779 frames/s at 3 streams, 783
+// at 4 (profiles/r10)
+#define LMGS_SORT_PERSIST_CTAS 1
 #endif
-#ifndef LMGS_RANK_GROUP
-#define LMGS_RANK_GROUP 1  // 1: 752 vs 745 frames/s at 2 (less shared memory; profiles/r07/rank_group_ab.txt)
-#endif
-constexpr int kMatchBufs = LMGS_RANK_MODE == 2 ? LMGS_RANK_GROUP : 1;
 #ifndef LMGS_SORT_MIN_CTAS_NARROW
 #define LMGS_SORT_MIN_CTAS_NARROW 4  // 32-bit keys without values: fewer registers
 #endif
@@ -151,8 +152,14 @@ __global__ void __launch_bounds__(kRadix) k_radix_plan(const uint32_t* __restric
 }
 
 // Output format of a pass and how its last pass counts tile runs.
-enum : int { kOutSame = 0, kOutIds = 1 };
+//   kOutPacked: u64 tile << 32 | id in, u32 (tile >> 8) << id_bits | id out
+//   (the first pass of the fused tile sort: its low tile digit is implied by
+//   the bucket the key lands in, so the second pass needs 4 bytes per key)
+enum : int { kOutSame = 0, kOutIds = 1, kOutPacked = 2 };
 enum : int { kSegNone = 0, kSegKey = 1 };
+// Where a pass's keys come from: the input buffer, or generated from the rank
+// records of the visible splats (fused emission, tile_sort_fused).
+enum : int { kSrcKeys = 0, kSrcEmit = 1 };
 
 struct PassArgs {
   void* keys[2];  // ping-pong buffers, each large enough for n keys of the wider format
@@ -169,6 +176,13 @@ struct PassArgs {
   uint32_t* seg_counts;
   int seg_shift;  // kSegKey: segment = key >> seg_shift
   const unsigned long long* n_dev;
+  int id_bits;  // kOutPacked
+  bool concurrent;  // persistent grid sized to share the SMs (LMGS_FLAG_CONCURRENT)
+  // kSrcEmit
+  const uint4* rrec;             // [n_vis] {rect lo, rect hi, id, first slot}
+  const uint32_t* chunk_first;   // [tiles] rank holding the tile's first slot
+  const unsigned long long* n_vis_dev;
+  int tiles_x;
 };
 
 template <typename KI, int OUT>
@@ -179,11 +193,17 @@ template <typename KI>
 struct OutKey<KI, kOutIds> {
   using type = uint32_t;
 };
+template <typename KI>
+struct OutKey<KI, kOutPacked> {
+  using type = uint32_t;
+};
 
 template <typename KI, int OUT>
 __device__ __forceinline__ typename OutKey<KI, OUT>::type out_key(KI k, const PassArgs& a) {
   if constexpr (OUT == kOutIds)
     return (uint32_t)k & a.id_mask;
+  else if constexpr (OUT == kOutPacked)
+    return ((uint32_t)((uint64_t)k >> 40) << a.id_bits) | (uint32_t)k;
   else
     return k;
 }
@@ -193,18 +213,117 @@ constexpr int sort_min_ctas() {
   return (sizeof(KI) == 4 && !VALS) ? LMGS_SORT_MIN_CTAS_NARROW : LMGS_SORT_MIN_CTAS;
 }
 
+// Fused emission (kSrcEmit): the tile's kSortTile instance slots [base, base +
+// count) are generated from the rank records instead of loaded.  Slot p
+// belongs to the last rank whose first slot is <= p: every covering rank
+// marks its first slot in a shared owner map (u16 offsets from the tile's
+// first rank; a rank owns >= 1 slot, so at most count + 1 ranks cover the
+// tile), a block max-scan fills the gaps, and each item decodes its tile from
+// the owner's rectangle (row-major inside it, as K4 emits them).  Items are
+// warp-striped like loaded keys, so the ranking below stays stable in slot
+// (= depth rank, then row-major tile) order.  The map aliases the staging
+// buffer, which is first written after the ranking.
+template <typename KI>
+__device__ __forceinline__ void emit_keys(const PassArgs& a, int64_t n, int64_t base, int count,
+                                          unsigned char* smem, KI (&key)[kSortItems]) {
+  static_assert(sizeof(KI) == 8, "emitted keys are tile << 32 | id");
+  uint16_t* s_owner = reinterpret_cast<uint16_t*>(smem);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t b = base / kSortTile;
+  const uint32_t r0 = a.chunk_first[b];
+  // ranks r0 .. r_last cover the tile (r_last = the next tile's first rank,
+  // which may start exactly at its first slot: the mark below skips it)
+  const uint32_t r_end = base + count < n ? a.chunk_first[b + 1] + 1 : (uint32_t)*a.n_vis_dev;
+  const int nr = (int)(r_end - r0);
+  const uint32_t slot0 = (uint32_t)base, slot_end = (uint32_t)(base + count);
+  static_assert(kSortItems % 2 == 0, "owner offsets are scanned in u16 pairs");
+  for (int i = tid; i < kSortTile / 8; i += kSortThreads)
+    reinterpret_cast<uint4*>(s_owner)[i] = make_uint4(0u, 0u, 0u, 0u);
+  __syncthreads();
+#pragma unroll 4
+  for (int j = tid; j < nr; j += kSortThreads) {
+    const uint32_t st = __ldg(reinterpret_cast<const uint32_t*>(a.rrec + r0 + j) + 3);
+    if (st < slot_end) s_owner[st > slot0 ? st - slot0 : 0u] = (uint16_t)j;
+  }
+  __syncthreads();
+  {
+    // inclusive max-scan of the marks (offsets grow with the slot): thread t
+    // owns slots [kSortItems * t, kSortItems * (t + 1))
+    __shared__ uint32_t s_wmax[kSortThreads / 32];
+    uint32_t v[kSortItems / 2];
+    const uint32_t* row = reinterpret_cast<const uint32_t*>(s_owner) + tid * (kSortItems / 2);
+#pragma unroll
+    for (int u = 0; u < kSortItems / 2; ++u) v[u] = row[u];
+    uint32_t m = 0;
+#pragma unroll
+    for (int u = 0; u < kSortItems / 2; ++u) m = max(m, max(v[u] & 0xffffu, v[u] >> 16));
+    uint32_t incl = m;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl = max(incl, x);
+    }
+    if (lane == 31) s_wmax[warp] = incl;
+    uint32_t carry = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) carry = 0;
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < kSortThreads / 32; ++w) carry = w < warp ? max(carry, s_wmax[w]) : carry;
+    uint32_t* wrow = reinterpret_cast<uint32_t*>(s_owner) + tid * (kSortItems / 2);
+#pragma unroll
+    for (int u = 0; u < kSortItems / 2; ++u) {
+      const uint32_t lo = max(carry, v[u] & 0xffffu);
+      const uint32_t hi = max(lo, v[u] >> 16);
+      carry = hi;
+      wrow[u] = lo | (hi << 16);
+    }
+  }
+  __syncthreads();
+  const int wbase = warp * 32 * kSortItems;
+  // records in groups of 4 (16 registers live, not 64; mostly L1 hits: a
+  // rank covers ~3.5 consecutive slots)
+  constexpr int G = 4;
+  static_assert(kSortItems % G == 0, "");
+#pragma unroll
+  for (int j0 = 0; j0 < kSortItems; j0 += G) {
+    uint4 rr[G];
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      const int i = wbase + (j0 + u) * 32 + lane;
+      rr[u] = __ldg(a.rrec + r0 + s_owner[i < count ? i : 0]);
+    }
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      const int i = wbase + (j0 + u) * 32 + lane;
+      const uint32_t q = slot0 + (uint32_t)i - rr[u].w;
+      const uint32_t x0 = rr[u].x & 0xffffu, y0 = rr[u].x >> 16, x1 = rr[u].y & 0xffffu;
+      const uint32_t w = x1 - x0 + 1;
+      // q / w without the integer-division sequence (q < area <= tiles < 2^16
+      // on this path): the float quotient is within one of the truth; fixed up
+      uint32_t dy = (uint32_t)__fdividef((float)q, (float)w);
+      if (dy * w > q) --dy;
+      else if ((dy + 1) * w <= q) ++dy;
+      const uint32_t tile = (y0 + dy) * (uint32_t)a.tiles_x + x0 + (q - dy * w);
+      key[j0 + u] = i < count ? (((uint64_t)tile << 32) | rr[u].z) : ~0ull;
+    }
+  }
+}
+
 // one onesweep scatter pass (digit `pass`)
 //
 // 1. load kSortTile keys (warp-striped, coalesced);
 // 2. early counts: the CTA's digit histogram by shared atomics, published at
 //    once to the look-back array so successors never wait on our ranking;
-// 3. stable rank inside each warp: lanes holding the same digit find each other
-//    through a per-warp shared "match" word (atomicOr of their lane bits, read
-//    back, cleared by the lowest lane) — MATCH.ANY serialises on this part;
+// 3. stable rank inside each warp: per warp and digit one 64-bit shared word
+//    {count, match}: lanes holding the same digit OR their lane bits into the
+//    match half, read the pair back with one 64-bit load (rank = count +
+//    lanes below), and the lowest of them stores {count + peers, 0} — no
+//    shuffle, no counter atomic (MATCH.ANY serialised; a separate match word +
+//    leader atomicAdd + shuffle cost ~39 SASS per key, this ~12);
 // 4. per-digit prefix over warps, staging in shared memory in digit order;
 // 5. decoupled look-back (windowed) for the global digit offsets;
 // 6. coalesced write-out in per-digit runs, in the pass's output format.
-template <typename KI, int OUT, int SEG, bool VALS, bool PERSIST>
+template <typename KI, int OUT, int SEG, bool VALS, bool PERSIST, int SRC = kSrcKeys>
 __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
     k_onesweep(PassArgs a) {
   using KO = typename OutKey<KI, OUT>::type;
@@ -231,9 +350,10 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   extern __shared__ __align__(16) unsigned char smem_raw[];
   KI* s_keys = reinterpret_cast<KI*>(smem_raw);  // [kSortTile] staging
   uint32_t* s_vals = reinterpret_cast<uint32_t*>(smem_raw + sizeof(KI) * kSortTile);
-  __shared__ uint32_t s_match[kMatchBufs][kWarps][kRadix];
-  __shared__ uint32_t s_wcnt[kWarps][kRadix];
-  __shared__ uint32_t s_hist[kRadix];
+  // digit kRadix collects the invalid items of a partial tile, so neither the
+  // counts nor the ranking need a validity predicate
+  __shared__ uint2 s_wm[kWarps][kRadix + 1];
+  __shared__ uint32_t s_hist[kRadix + 1];
   __shared__ uint32_t s_local_start[kRadix];
   __shared__ uint32_t s_global[kRadix];
   __shared__ uint32_t s_bid;
@@ -261,26 +381,30 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
 
   KI key[kSortItems];
   uint32_t val[VALS ? kSortItems : 1];
-  uint32_t pos[kSortItems];
+  uint32_t dg[kSortItems];  // digit (kRadix: invalid), then | rank in the warp << 16
   const int wbase = warp * 32 * kSortItems;
+  if constexpr (SRC == kSrcEmit) {
+    emit_keys(a, n, base, count, smem_raw, key);
+  } else {
 #pragma unroll
-  for (int j = 0; j < kSortItems; ++j) {
-    const int i = wbase + j * 32 + lane;
-    key[j] = i < count ? kin[base + i] : (KI)~(KI)0;
-    if (VALS) val[j] = iota ? (uint32_t)(base + i) : (i < count ? vin[base + i] : 0u);
+    for (int j = 0; j < kSortItems; ++j) {
+      const int i = wbase + j * 32 + lane;
+      key[j] = i < count ? kin[base + i] : (KI)~(KI)0;
+      if (VALS) val[j] = iota ? (uint32_t)(base + i) : (i < count ? vin[base + i] : 0u);
+    }
   }
   // the loads above are in flight while the ranking state is cleared
-  for (int i = tid; i < kWarps * kRadix; i += kSortThreads) {
-#pragma unroll
-    for (int r = 0; r < kMatchBufs; ++r) (&s_match[r][0][0])[i] = 0;
-    (&s_wcnt[0][0])[i] = 0;
-  }
+  for (int i = tid; i < kWarps * (kRadix + 1); i += kSortThreads)
+    (&s_wm[0][0])[i] = make_uint2(0u, 0u);
   s_hist[tid] = 0;  // kSortThreads == kRadix
+  if (tid == 0) s_hist[kRadix] = 0;
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j)
+    dg[j] = wbase + j * 32 + lane < count ? digit_of(key[j], shift) : (uint32_t)kRadix;
   __syncthreads();
   // 2. early counts, published with the look-back before ranking
 #pragma unroll
-  for (int j = 0; j < kSortItems; ++j)
-    if (wbase + j * 32 + lane < count) atomicAdd(&s_hist[digit_of(key[j], shift)], 1u);
+  for (int j = 0; j < kSortItems; ++j) atomicAdd(&s_hist[dg[j]], 1u);
   __syncthreads();
   uint32_t* lb = a.lookback + ((int64_t)pass * a.lb_stride) * kRadix;
   const uint32_t total = s_hist[tid];  // thread d == digit d
@@ -329,103 +453,46 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   }
   // 3. stable in-warp ranking, items in (j, lane) order
   const uint32_t lt = lanemask_lt();
-  uint32_t* my_cnt = s_wcnt[warp];
-#if LMGS_RANK_MODE == 1
-  // peers by MATCH.ANY; the leader advances the warp's digit counter
+  uint2* my = s_wm[warp];
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
-    const bool valid = wbase + j * 32 + lane < count;
-    const uint32_t d = digit_of(key[j], shift);
-    const uint32_t peers = __match_any_sync(0xffffffffu, valid ? d : 256u + lane);
-    const int leader = __ffs(peers) - 1;
-    uint32_t before = 0;
-    if (valid && lane == leader) {
-      before = my_cnt[d];
-      my_cnt[d] = before + (uint32_t)__popc(peers);
-    }
-    before = __shfl_sync(0xffffffffu, before, leader);
-    pos[j] = before + __popc(peers & lt);
+    atomicOr(&my[dg[j]].y, 1u << lane);
+    __syncwarp();
+    const uint2 cm = my[dg[j]];
+    __syncwarp();
+    const uint32_t below = cm.y & lt;
+    if (below == 0) my[dg[j]] = make_uint2(cm.x + __popc(cm.y), 0u);
+    dg[j] |= (cm.x + __popc(below)) << 16;
     __syncwarp();
   }
-#elif LMGS_RANK_MODE == 2
-  // LMGS_RANK_GROUP items at a time, each with its own match words, so their
-  // shared-memory round trips overlap; the leaders' counter updates are
-  // atomics issued in item order by the one warp
-#pragma unroll
-  for (int j0 = 0; j0 < kSortItems; j0 += LMGS_RANK_GROUP) {
-    uint32_t peers[LMGS_RANK_GROUP];
-#pragma unroll
-    for (int r = 0; r < LMGS_RANK_GROUP; ++r) {
-      const int j = j0 + r;
-      if (wbase + j * 32 + lane < count) atomicOr(&s_match[r][warp][digit_of(key[j], shift)], 1u << lane);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < LMGS_RANK_GROUP; ++r) {
-      const int j = j0 + r;
-      const bool valid = wbase + j * 32 + lane < count;
-      peers[r] = valid ? s_match[r][warp][digit_of(key[j], shift)] : (1u << lane);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < LMGS_RANK_GROUP; ++r) {
-      const int j = j0 + r;
-      const bool valid = wbase + j * 32 + lane < count;
-      const uint32_t d = digit_of(key[j], shift);
-      const int leader = __ffs(peers[r]) - 1;
-      uint32_t before = 0;
-      if (valid && lane == leader) {
-        before = atomicAdd(my_cnt + d, (uint32_t)__popc(peers[r]));
-        s_match[r][warp][d] = 0;
-      }
-      before = __shfl_sync(0xffffffffu, before, leader);
-      pos[j] = before + __popc(peers[r] & lt);
-    }
-    __syncwarp();
-  }
-#else
-  uint32_t* my_match = s_match[0][warp];
-#pragma unroll
-  for (int j = 0; j < kSortItems; ++j) {
-    const bool valid = wbase + j * 32 + lane < count;
-    const uint32_t d = digit_of(key[j], shift);
-    if (valid) atomicOr(my_match + d, 1u << lane);
-    __syncwarp();
-    const uint32_t peers = valid ? my_match[d] : (1u << lane);
-    __syncwarp();
-    const int leader = __ffs(peers) - 1;
-    uint32_t before = 0;
-    if (valid && lane == leader) {
-      before = my_cnt[d];
-      my_cnt[d] = before + (uint32_t)__popc(peers);
-      my_match[d] = 0;
-    }
-    before = __shfl_sync(0xffffffffu, before, leader);
-    pos[j] = before + __popc(peers & lt);
-    __syncwarp();
-  }
-#endif
   __syncthreads();
-  // 4. per digit: exclusive prefix over warps
+  // 4. per digit: exclusive prefix over warps (the invalid items go behind
+  // the tile's count, into staging slots the write-out never reads)
   {
     const int d = tid;
     uint32_t run = s_local_start[d];
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
-      const uint32_t c = s_wcnt[w][d];
-      s_wcnt[w][d] = run;
+      const uint32_t c = s_wm[w][d].x;
+      s_wm[w][d].x = run;
       run += c;
+    }
+    if (tid == 0) {
+      run = (uint32_t)count;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        const uint32_t c = s_wm[w][kRadix].x;
+        s_wm[w][kRadix].x = run;
+        run += c;
+      }
     }
   }
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
-    const int i = wbase + j * 32 + lane;
-    if (i < count) {
-      const uint32_t p = pos[j] + my_cnt[digit_of(key[j], shift)];
-      s_keys[p] = key[j];
-      if (VALS) s_vals[p] = val[j];
-    }
+    const uint32_t p = (dg[j] >> 16) + my[dg[j] & 0xffffu].x;
+    s_keys[p] = key[j];
+    if (VALS) s_vals[p] = val[j];
   }
   __syncthreads();
   // 6. coalesced write-out: consecutive threads, consecutive staged positions
@@ -455,30 +522,35 @@ constexpr size_t onesweep_smem() {
   return sizeof(KI) * kSortTile + (VALS ? sizeof(uint32_t) * kSortTile : 0);
 }
 
-template <typename KI, int OUT, int SEG, bool VALS>
+template <typename KI, int OUT, int SEG, bool VALS, int SRC = kSrcKeys>
 void launch_pass(const PassArgs& a, int64_t blocks, cudaStream_t s) {
   constexpr size_t smem = onesweep_smem<KI, VALS>();
+  static_assert(SRC == kSrcKeys || smem >= 2 * kSortTile, "the owner map aliases the staging");
   static bool attr_set[kMaxDevices] = {};
   static int occ[kMaxDevices] = {}, sms[kMaxDevices] = {};
   const int dev = current_device();
   if (!attr_set[dev]) {
-    cudaFuncSetAttribute(k_onesweep<KI, OUT, SEG, VALS, false>,
+    cudaFuncSetAttribute(k_onesweep<KI, OUT, SEG, VALS, false, SRC>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_onesweep<KI, OUT, SEG, VALS, true>,
+    cudaFuncSetAttribute(k_onesweep<KI, OUT, SEG, VALS, true, SRC>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[dev], k_onesweep<KI, OUT, SEG, VALS, true>,
-                                                  kSortThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &occ[dev], k_onesweep<KI, OUT, SEG, VALS, true, SRC>, kSortThreads, smem);
     if (occ[dev] < 1) occ[dev] = 1;
     attr_set[dev] = true;
   }
-  if (!a.n_dev) {
-    k_onesweep<KI, OUT, SEG, VALS, false><<<(unsigned)blocks, kSortThreads, smem, s>>>(a);
+  if (!a.n_dev && !a.concurrent) {
+    k_onesweep<KI, OUT, SEG, VALS, false, SRC><<<(unsigned)blocks, kSortThreads, smem, s>>>(a);
     return;
   }
   // the key count is on the device: a persistent grid takes tiles by ticket
-  const int64_t persistent = (int64_t)sms[dev] * occ[dev];
-  k_onesweep<KI, OUT, SEG, VALS, true>
+  // (concurrent streams: always, with LMGS_SORT_PERSIST_CTAS CTAs per SM,
+  // leaving room for the other streams' kernels)
+  const int per_sm = a.concurrent && LMGS_SORT_PERSIST_CTAS > 0 && LMGS_SORT_PERSIST_CTAS < occ[dev]
+                         ? LMGS_SORT_PERSIST_CTAS : occ[dev];
+  const int64_t persistent = (int64_t)sms[dev] * per_sm;
+  k_onesweep<KI, OUT, SEG, VALS, true, SRC>
       <<<(unsigned)(blocks < persistent ? blocks : persistent), kSortThreads, smem, s>>>(a);
 }
 
@@ -499,6 +571,7 @@ PassArgs pass_args(const RadixSortBuffers& b, int64_t n, int shift, int p, int64
   a.seg_counts = b.seg_counts;
   a.seg_shift = b.seg_shift;
   a.n_dev = b.n_dev;
+  a.concurrent = b.concurrent;
   a.id_mask = 0xffffffffu;
   return a;
 }
@@ -568,6 +641,38 @@ int tile_sort(const RadixSortBuffers& b, int64_t k, int tile_bits, cudaStream_t 
     else launch_pass<uint64_t, kOutSame, kSegNone, false>(a, blocks, s);
   }
   return launched + n_passes;
+}
+
+int tile_sort_fused(const FusedTileSort& f, cudaStream_t s) {
+  if (f.k_bound <= 0) return 0;
+  const int64_t blocks = (f.k_bound + kSortTile - 1) / kSortTile;
+  cudaMemsetAsync(f.counters, 0, sizeof(uint32_t) * kMaxPasses, s);
+  cudaMemsetAsync(f.lookback, 0, sizeof(uint32_t) * 2 * (size_t)blocks * kRadix, s);
+  PassArgs a{};
+  a.keys[0] = f.keys[0];
+  a.keys[1] = f.keys[1];
+  a.n = f.k_bound;
+  a.plan = f.plan;
+  a.lookback = f.lookback;
+  a.counter = f.counters;
+  a.lb_stride = blocks;
+  a.n_dev = f.k_dev;
+  a.concurrent = f.concurrent;
+  a.id_bits = f.id_bits;
+  a.id_mask = f.id_bits >= 32 ? 0xffffffffu : (1u << f.id_bits) - 1u;
+  a.rrec = f.rrec;
+  a.chunk_first = f.chunk_first;
+  a.n_vis_dev = f.n_vis_dev;
+  a.tiles_x = f.tiles_x;
+  // pass 0: generated keys, low tile digit -> keys[1] (u32 packed)
+  a.shift = 32;
+  a.pass = 0;
+  launch_pass<uint64_t, kOutPacked, kSegNone, false, kSrcEmit>(a, blocks, s);
+  // pass 1: the high tile digit of the packed keys -> keys[0] (u32 ids)
+  a.shift = f.id_bits;
+  a.pass = 1;
+  launch_pass<uint32_t, kOutIds, kSegNone, false>(a, blocks, s);
+  return 2;
 }
 
 }  // namespace lmgs

@@ -283,7 +283,7 @@ def render(camera, gaussians: GaussianModel, tile_size: int = 16, background=(0.
            prim_ids: torch.Tensor | None = None, stream=None, ctx=None,
            out: dict | None = None, page_mask: torch.Tensor | None = None,
            page_shift: int = 7, touched_fix: bool = True,
-           wide_fix_band: bool = False) -> RenderOutput:
+           wide_fix_band: bool = False, fused_tile_sort: bool = False) -> RenderOutput:
     """Render one view of device-resident Gaussians (north-star operator).
 
     ``prim_ids`` (int64, optional) are the original ids used for depth-tie
@@ -291,7 +291,9 @@ def render(camera, gaussians: GaussianModel, tile_size: int = 16, background=(0.
     ``out`` may pre-supply output tensors (e.g. slices of a batch buffer)
     under the RenderOutput field names.  ``touched_fix=False`` skips the
     fp64 replay that makes ``touched`` exact (K7b); ``wide_fix_band`` replays
-    every pixel within 1e-2 of TERM_EPS instead of 1e-4 (a check of the band).  ``page_mask`` (device uint8 per
+    every pixel within 1e-2 of TERM_EPS instead of 1e-4 (a check of the band);
+    ``fused_tile_sort`` builds the tile lists with the fused emission + tile
+    sort where it applies (identical lists; see LMGS_FLAG_FUSED_TILE_SORT).  ``page_mask`` (device uint8 per
     128-row page: its number of live leading rows, 0..128) restricts the
     render to those rows (the paged device pool of ``offload``).
     """
@@ -334,7 +336,8 @@ def render(camera, gaussians: GaussianModel, tile_size: int = 16, background=(0.
     st = abi_settings(ts, sh_eval_degree, background,
                       (_lib.LMGS_FLAG_STAGE_TIMES if stage_times else 0)
                       | (0 if touched_fix else _lib.LMGS_FLAG_NO_TOUCHED_FIX)
-                      | (_lib.LMGS_FLAG_WIDE_FIX_BAND if wide_fix_band else 0))
+                      | (_lib.LMGS_FLAG_WIDE_FIX_BAND if wide_fix_band else 0)
+                      | (_lib.LMGS_FLAG_FUSED_TILE_SORT if fused_tile_sort else 0))
     sh = _stream_handle(stream)
     L = _lib.lib()
     with torch.cuda.device(dev):

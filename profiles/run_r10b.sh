@@ -1,0 +1,13 @@
+#!/bin/bash
+# fused emission + tile sort: A/B tests, parity suite, bench stage times
+out=gpurun_out/r10b; mkdir -p $out
+timeout 600 python -m pytest tests/test_gpu_fused.py -q -x -p no:cacheprovider > $out/pytest_fused.log 2>&1
+tail -3 $out/pytest_fused.log
+timeout 900 python -m pytest tests -q -m gpu -x -p no:cacheprovider > $out/pytest_gpu.log 2>&1
+tail -3 $out/pytest_gpu.log
+timeout 300 python bench.py --steps 10 --warmup 3 --e2e-steps 1 --no-cpu-baseline --no-c5 > $out/bench.log 2>&1
+tail -1 $out/bench.log | python -c "import json,sys; d=json.load(sys.stdin); print(round(d['value'],1), d['e2e']['value'], {k: round(v,4) for k,v in d['roofline']['stage_ms_per_frame'].items()})"
+timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    --log-file $out/launches.csv python profiles/view_probe.py 1 > /dev/null 2>&1
+python profiles/launch_table.py $out/launches.csv > $out/launch_table.txt 2>&1
+cat $out/launch_table.txt

@@ -94,10 +94,10 @@ def test_sh_degrees_vs_oracle(deg):
     np.testing.assert_array_equal(out.inst_prim_ids.cpu().numpy(), o["inst_prim"])
 
 
-def _full_frame_check(g, cam, ts=16, bg=(0.0, 0.0, 0.0), deg=3):
+def _full_frame_check(g, cam, ts=16, bg=(0.0, 0.0, 0.0), deg=3, fused_tile_sort=False):
     model = GaussianModel.from_host(g, validate=False)
     out = render(cam, model, ts, bg, sh_eval_degree=deg, with_instances=True,
-                 out={"transmittance": None})
+                 out={"transmittance": None}, fused_tile_sort=fused_tile_sort)
     torch.cuda.synchronize()
     o = oracle.render(g, cam, ts, bg, sh_eval_degree=deg)
     assert out.n_instances == o["K"]
