@@ -67,6 +67,28 @@ __device__ __forceinline__ uint32_t digit_of(K key, int shift) {
 
 __device__ __forceinline__ bool gated_off(const int* gate) { return gate && *gate == 0; }
 
+// LMGS_SORT_TRACE (experiments only): %globaltimer at the phase boundaries of
+// every tile of the traced pass (pass index == LMGS_SORT_TRACE - 1; the last
+// sort to run that pass wins): ticket, loaded+counted, looked back, ranked,
+// staged, written — read back with lmgs_debug_sort_trace
+// (bench_tools/sort_trace.py).
+#ifdef LMGS_SORT_TRACE
+constexpr int kTraceTiles = 1 << 14;
+__device__ unsigned long long g_trace[kTraceTiles][7];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(k)                                                                     \
+  if (a.pass == LMGS_SORT_TRACE - 1 && threadIdx.x == 0 && bid < kTraceTiles) {      \
+    g_trace[bid][k] = gtimer();                                                      \
+    if (k == 0) g_trace[bid][6] = (unsigned long long)blockIdx.x;                    \
+  }
+#else
+#define TRACE(k)
+#endif
+
 // ---------------------------------------------------------------------------
 // histogram of every digit in one pass over the keys
 
@@ -378,6 +400,7 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   const int64_t base = (int64_t)bid * kSortTile;
   if (base >= n) return;
   const int count = (int)min((int64_t)kSortTile, n - base);
+  TRACE(0)
 
   KI key[kSortItems];
   uint32_t val[VALS ? kSortItems : 1];
@@ -406,6 +429,7 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) atomicAdd(&s_hist[dg[j]], 1u);
   __syncthreads();
+  TRACE(1)
   uint32_t* lb = a.lookback + ((int64_t)pass * a.lb_stride) * kRadix;
   const uint32_t total = s_hist[tid];  // thread d == digit d
   {
@@ -452,6 +476,10 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
     s_global[d] = plan->digit_start[pass][d] + excl - (wpre + incl - total);
   }
   // 3. stable in-warp ranking, items in (j, lane) order
+#ifdef LMGS_SORT_TRACE
+  __syncthreads();
+  TRACE(2)
+#endif
   const uint32_t lt = lanemask_lt();
   uint2* my = s_wm[warp];
 #pragma unroll
@@ -466,6 +494,7 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
     __syncwarp();
   }
   __syncthreads();
+  TRACE(3)
   // 4. per digit: exclusive prefix over warps (the invalid items go behind
   // the tile's count, into staging slots the write-out never reads)
   {
@@ -495,6 +524,7 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
     if (VALS) s_vals[p] = val[j];
   }
   __syncthreads();
+  TRACE(4)
   // 6. coalesced write-out: consecutive threads, consecutive staged positions
   const bool segs = SEG != kSegNone && a.seg_counts && pass == plan->last_active;
   for (int i = tid; i < count; i += kSortThreads) {
@@ -512,6 +542,10 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
       if (sn != sg) atomicAdd(a.seg_counts + sg, (uint32_t)(i + 1));
     }
   }
+#ifdef LMGS_SORT_TRACE
+  __syncthreads();
+  TRACE(5)
+#endif
   if (!PERSIST) return;  // one tile per CTA on an exact grid
   __syncthreads();  // the staging and s_bid are reused by the next tile
   }
@@ -676,3 +710,14 @@ int tile_sort_fused(const FusedTileSort& f, cudaStream_t s) {
 }
 
 }  // namespace lmgs
+
+#ifdef LMGS_SORT_TRACE
+extern "C" int lmgs_debug_sort_trace(void* host, size_t bytes) {
+  const size_t n = bytes < sizeof(lmgs::g_trace) ? bytes : sizeof(lmgs::g_trace);
+  return (int)cudaMemcpyFromSymbol(host, lmgs::g_trace, n);
+}
+extern "C" int lmgs_debug_sort_trace_reset() {
+  static unsigned long long zero[lmgs::kTraceTiles][7];
+  return (int)cudaMemcpyToSymbol(lmgs::g_trace, zero, sizeof(zero));
+}
+#endif
