@@ -26,6 +26,15 @@ namespace {
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
+// Experiments only (bench_tools/stage_skip_probe.py): bit i of
+// LMGS_SKIP_STAGES drops stage i's kernels (1 depth sort, 2 emit, 3 tile sort,
+// 4 blend) so the batch's frame time without them can be measured; outputs
+// are then garbage (stale but memory-safe arenas).
+#ifndef LMGS_SKIP_STAGES
+#define LMGS_SKIP_STAGES 0
+#endif
+constexpr unsigned kSkip = LMGS_SKIP_STAGES;
+
 const char* kStageNames[] = {"preprocess", "depth_sort", "emit", "tile_sort", "blend",
                              "touched_fix"};
 constexpr int kNumStages = 6;
@@ -395,7 +404,7 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
   tm.begin(1);
   {
     LMGS_CUDA(c, cudaMemsetAsync(sc->depth_hist, 0, sizeof(sc->depth_hist), s));
-    launched += launch_depth_keys(c->key64, sc->zrange, n, c->key32[0], sc->depth_hist, s);
+    if (!(kSkip & 2)) launched += launch_depth_keys(c->key64, sc->zrange, n, c->key32[0], sc->depth_hist, s);
     RadixSortBuffers rb{};
     rb.keys[0] = c->key32[0];
     rb.keys[1] = c->key32[1];
@@ -411,9 +420,11 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
     rb.iota_vals = true;
     rb.hist_ready = true;
     rb.concurrent = (st->flags & LMGS_FLAG_CONCURRENT) != 0;
-    launched += radix_sort(rb, n, 0, kDepthPasses, s);
-    launched += launch_depth_fixup(&sc->slots.depth_keys, &sc->slots.depth_ids, n, c->key64,
-                                   g->prim_ids, s);
+    if (!(kSkip & 2)) {
+      launched += radix_sort(rb, n, 0, kDepthPasses, s);
+      launched += launch_depth_fixup(&sc->slots.depth_keys, &sc->slots.depth_ids, n, c->key64,
+                                     g->prim_ids, s);
+    }
   }
   tm.end(1);
 
@@ -533,7 +544,7 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
     ea.ticket = sc->emit_ticket;
     ea.hist = sc->tile_hist;
     ea.concurrent = (st->flags & LMGS_FLAG_CONCURRENT) != 0;
-    launched += launch_emit(ea, s);
+    if (!(kSkip & 4)) launched += launch_emit(ea, s);
   }
   tm.end(2);
 
@@ -558,8 +569,10 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
       rb.max_n = &sc->max_k;
     }
     LMGS_CUDA(c, cudaMemsetAsync(c->tile_count, 0, sizeof(uint32_t) * tiles, s));
-    launched += tile_sort(rb, k, bits_for(tiles), s);
-    launched += launch_ranges_from_counts(c->tile_count, (int)tiles, ranges, cap_view, s);
+    if (!(kSkip & 8)) {
+      launched += tile_sort(rb, k, bits_for(tiles), id_bits, s);
+      launched += launch_ranges_from_counts(c->tile_count, (int)tiles, ranges, cap_view, s);
+    }
   }
   }
   if (out->tile_ranges && tiles > 0)
@@ -625,7 +638,8 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
       ba.sdepth[i] = strips->depth[i];
     }
   }
-  if (int r = launch_blend(ba, s)) return fail(c, r, "too many blend blocks for this tile size");
+  if (!(kSkip & 16))
+    if (int r = launch_blend(ba, s)) return fail(c, r, "too many blend blocks for this tile size");
   launched += tiles > 0 ? 1 : 0;
   tm.end(4);
   // K7b

@@ -344,6 +344,9 @@ constexpr int kWarpsPerBlock16 = 8;
 // With NP = 2 the per-splat work (shared loads, ballots, the touched atomic,
 // loop control) is shared by two pixels and the two pixels' dependency chains
 // interleave.
+#ifndef LMGS_BLEND_PAIRS
+#define LMGS_BLEND_PAIRS 0  // 1: two hits per trip, one break vote per pair (777.6 vs 777.3 frames/s: neutral, profiles/r10)
+#endif
 #ifndef LMGS_BLEND_MINB
 #define LMGS_BLEND_MINB 4  // 4 x 256 threads per SM (64 registers): measured best
 #endif
@@ -484,9 +487,9 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
       __syncwarp();
       uint32_t my_touch = 0;  // pixels with w > 0 for this lane's splat (cid)
       uint32_t my_ballot = 0;  // NP == 1: the pixels themselves
-      while (m) {
-        const int k = __ffs(m) - 1;
-        m &= m - 1;
+      // one hit splat k of the batch: the front-to-back update of this lane's
+      // pixels; returns whether one of them is still active
+      auto blend_one = [&](const int k) -> bool {
         const float4 g = s_rec[warp][k][0];
         const float4 h = s_rec[warp][k][1];
         const float4 c = s_rec[warp][k][2];
@@ -566,20 +569,52 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
 #pragma unroll
         for (int q = 0; q < NP; ++q) active |= T[q] >= kTermEpsF;
         if (NP == 1) {  // the owner keeps its splat's ballot; counted after the batch
-          const uint32_t b = __ballot_sync(0xffffffffu, contrib1);
-          my_ballot = lane == k ? b : my_ballot;
+          const uint32_t bl = __ballot_sync(0xffffffffu, contrib1);
+          my_ballot = lane == k ? bl : my_ballot;
         } else {
           const int wsum = __reduce_add_sync(0xffffffffu, contrib_bits);
           if (lane == k) my_touch += wsum;
         }
-        // pixels only go inactive on a splat they are inside: the warp's break
-        // index is the first splat after which none of its pixels is active
-        if (!__any_sync(0xffffffffu, active)) {
+        return active;
+      };
+#if LMGS_BLEND_PAIRS
+      // two hits per trip and one break vote per pair: a pixel that went
+      // inactive takes nothing more (sigma 0, no w > 0), so blending the
+      // second splat of a pair after the break changes nothing; when the pair
+      // ends with no pixel active, the vote on the first splat's state tells
+      // which of the two was the break
+      while (m) {
+        const int k = __ffs(m) - 1;
+        m &= m - 1;
+        const bool act1 = blend_one(k);
+        if (m) {
+          const int k2 = __ffs(m) - 1;
+          m &= m - 1;
+          const bool act2 = blend_one(k2);
+          if (!__any_sync(0xffffffffu, act2)) {
+            last = b - range.x + (__any_sync(0xffffffffu, act1) ? k2 : k);
+            live = false;
+            break;
+          }
+        } else if (!__any_sync(0xffffffffu, act1)) {
           last = b - range.x + k;
           live = false;
           break;
         }
       }
+#else
+      while (m) {
+        const int k = __ffs(m) - 1;
+        m &= m - 1;
+        // pixels only go inactive on a splat they are inside: the warp's break
+        // index is the first splat after which none of its pixels is active
+        if (!__any_sync(0xffffffffu, blend_one(k))) {
+          last = b - range.x + k;
+          live = false;
+          break;
+        }
+      }
+#endif
       if (NP == 1) my_touch = __popc(my_ballot);
       if (my_touch && a.touched) atomicAdd(a.touched + cid, (int)my_touch);
       __syncwarp();

@@ -163,7 +163,9 @@ int radix_sort(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_passes
 // tile_bits); every pass runs and the last one writes the ids alone (uint32_t,
 // in the buffer keys_result names).  seg_counts (required) gets the per-tile
 // counts.  keys[0] holds the input; both buffers hold k u64 keys.
-int tile_sort(const RadixSortBuffers& b, int64_t k, int tile_bits, cudaStream_t s);
+// id_bits: bits of the largest id (the 2-pass sort then runs its second pass
+// on packed 4-byte keys when (tile_bits - 8) + id_bits <= 32)
+int tile_sort(const RadixSortBuffers& b, int64_t k, int tile_bits, int id_bits, cudaStream_t s);
 
 // K4+K5 fused (tile ids < 2^16, (tile bits - 8) + id bits <= 32): the first
 // pass generates its instance keys from the rank records (K4r, below) instead

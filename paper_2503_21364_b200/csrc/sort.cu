@@ -39,6 +39,9 @@ constexpr int kLookWindow = LMGS_LOOK_WINDOW;
 // at 4 (profiles/r10)
 #define LMGS_SORT_PERSIST_CTAS 1
 #endif
+#ifndef LMGS_TILE_SORT_PACKED
+#define LMGS_TILE_SORT_PACKED 1  // two-pass tile sorts with a packed 4-byte second pass
+#endif
 #ifndef LMGS_SORT_MIN_CTAS_NARROW
 #define LMGS_SORT_MIN_CTAS_NARROW 4  // 32-bit keys without values: fewer registers
 #endif
@@ -178,7 +181,10 @@ __global__ void __launch_bounds__(kRadix) k_radix_plan(const uint32_t* __restric
 //   (the first pass of the fused tile sort: its low tile digit is implied by
 //   the bucket the key lands in, so the second pass needs 4 bytes per key)
 enum : int { kOutSame = 0, kOutIds = 1, kOutPacked = 2 };
-enum : int { kSegNone = 0, kSegKey = 1 };
+//   kSegLo: the keys are packed (tile >> 8) << id_bits | id (shift = id_bits)
+//   and the low tile digit is the bucket of the previous pass (lo_pass) the
+//   key's input position lies in
+enum : int { kSegNone = 0, kSegKey = 1, kSegLo = 2 };
 // Where a pass's keys come from: the input buffer, or generated from the rank
 // records of the visible splats (fused emission, tile_sort_fused).
 enum : int { kSrcKeys = 0, kSrcEmit = 1 };
@@ -197,6 +203,7 @@ struct PassArgs {
   uint32_t id_mask;  // kOutIds: out = key & id_mask
   uint32_t* seg_counts;
   int seg_shift;  // kSegKey: segment = key >> seg_shift
+  int lo_pass;    // kSegLo: the pass whose buckets give the low tile digit
   const unsigned long long* n_dev;
   int id_bits;  // kOutPacked
   bool concurrent;  // persistent grid sized to share the SMs (LMGS_FLAG_CONCURRENT)
@@ -372,6 +379,9 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   extern __shared__ __align__(16) unsigned char smem_raw[];
   KI* s_keys = reinterpret_cast<KI*>(smem_raw);  // [kSortTile] staging
   uint32_t* s_vals = reinterpret_cast<uint32_t*>(smem_raw + sizeof(KI) * kSortTile);
+  // kSegLo: the staged keys' low tile digits (the vals slot: kSegLo has none)
+  uint8_t* s_lo = reinterpret_cast<uint8_t*>(smem_raw + sizeof(KI) * kSortTile);
+  __shared__ uint32_t s_dstart[SEG == kSegLo ? kRadix : 1];
   // digit kRadix collects the invalid items of a partial tile, so neither the
   // counts nor the ranking need a validity predicate
   __shared__ uint2 s_wm[kWarps][kRadix + 1];
@@ -405,6 +415,7 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   KI key[kSortItems];
   uint32_t val[VALS ? kSortItems : 1];
   uint32_t dg[kSortItems];  // digit (kRadix: invalid), then | rank in the warp << 16
+  uint32_t lo4[SEG == kSegLo ? kSortItems / 4 : 1];  // kSegLo: low tile digits, 4 per word
   const int wbase = warp * 32 * kSortItems;
   if constexpr (SRC == kSrcEmit) {
     emit_keys(a, n, base, count, smem_raw, key);
@@ -417,6 +428,7 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
     }
   }
   // the loads above are in flight while the ranking state is cleared
+  if constexpr (SEG == kSegLo) s_dstart[tid] = plan->digit_start[a.lo_pass][tid];
   for (int i = tid; i < kWarps * (kRadix + 1); i += kSortThreads)
     (&s_wm[0][0])[i] = make_uint2(0u, 0u);
   s_hist[tid] = 0;  // kSortThreads == kRadix
@@ -428,6 +440,32 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   // 2. early counts, published with the look-back before ranking
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) atomicAdd(&s_hist[dg[j]], 1u);
+  if constexpr (SEG == kSegLo) {
+    // the bucket of input position p: the largest d with start[d] <= p.  A
+    // thread's items are increasing positions: search the first and the last,
+    // and walk the (rare) boundaries between them
+    auto bucket = [&](uint32_t p) {
+      int lo = 0, hi = kRadix - 1;
+#pragma unroll
+      for (int it = 0; it < kRadixBits; ++it) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_dstart[mid] <= p) lo = mid;
+        else hi = mid - 1;
+      }
+      return lo;
+    };
+    const uint32_t p0 = (uint32_t)base + wbase + lane;
+    int lo = bucket(p0);
+    const int lo_end = bucket(min(p0 + 32u * (kSortItems - 1), (uint32_t)(n - 1)));
+#pragma unroll
+    for (int j = 0; j < kSortItems / 4; ++j) lo4[j] = 0;
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+      if (lo != lo_end)
+        while (lo < lo_end && s_dstart[lo + 1] <= p0 + 32u * j) ++lo;
+      lo4[j / 4] |= (uint32_t)lo << (8 * (j % 4));
+    }
+  }
   __syncthreads();
   TRACE(1)
   uint32_t* lb = a.lookback + ((int64_t)pass * a.lb_stride) * kRadix;
@@ -522,6 +560,7 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
     const uint32_t p = (dg[j] >> 16) + my[dg[j] & 0xffffu].x;
     s_keys[p] = key[j];
     if (VALS) s_vals[p] = val[j];
+    if constexpr (SEG == kSegLo) s_lo[p] = (uint8_t)(lo4[j / 4] >> (8 * (j % 4)));
   }
   __syncthreads();
   TRACE(4)
@@ -535,9 +574,19 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
     if (segs) {
       // the staged tile is sorted on every key bit sorted so far: runs of one
       // segment are contiguous; a run [i0, i1] adds (i1 + 1) - i0
-      const uint64_t sg = (uint64_t)k >> a.seg_shift;
-      const uint64_t sp = i > 0 ? (uint64_t)s_keys[i - 1] >> a.seg_shift : ~0ull;
-      const uint64_t sn = i + 1 < count ? (uint64_t)s_keys[i + 1] >> a.seg_shift : ~0ull;
+      uint64_t sg, sp, sn;
+      if constexpr (SEG == kSegLo) {
+        auto seg = [&](int t) {
+          return (uint64_t)(digit_of(s_keys[t], shift) << 8 | s_lo[t]);
+        };
+        sg = (uint64_t)(digit_of(k, shift) << 8 | s_lo[i]);
+        sp = i > 0 ? seg(i - 1) : ~0ull;
+        sn = i + 1 < count ? seg(i + 1) : ~0ull;
+      } else {
+        sg = (uint64_t)k >> a.seg_shift;
+        sp = i > 0 ? (uint64_t)s_keys[i - 1] >> a.seg_shift : ~0ull;
+        sn = i + 1 < count ? (uint64_t)s_keys[i + 1] >> a.seg_shift : ~0ull;
+      }
       if (sp != sg) atomicAdd(a.seg_counts + sg, (uint32_t)(-i));
       if (sn != sg) atomicAdd(a.seg_counts + sg, (uint32_t)(i + 1));
     }
@@ -551,14 +600,15 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   }
 }
 
-template <typename KI, bool VALS>
+template <typename KI, bool VALS, int SEG = kSegNone>
 constexpr size_t onesweep_smem() {
-  return sizeof(KI) * kSortTile + (VALS ? sizeof(uint32_t) * kSortTile : 0);
+  return sizeof(KI) * kSortTile + (VALS ? sizeof(uint32_t) * kSortTile : 0) +
+         (SEG == kSegLo ? kSortTile : 0);
 }
 
 template <typename KI, int OUT, int SEG, bool VALS, int SRC = kSrcKeys>
 void launch_pass(const PassArgs& a, int64_t blocks, cudaStream_t s) {
-  constexpr size_t smem = onesweep_smem<KI, VALS>();
+  constexpr size_t smem = onesweep_smem<KI, VALS, SEG>();
   static_assert(SRC == kSrcKeys || smem >= 2 * kSortTile, "the owner map aliases the staging");
   static bool attr_set[kMaxDevices] = {};
   static int occ[kMaxDevices] = {}, sms[kMaxDevices] = {};
@@ -664,11 +714,26 @@ int radix_sort(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_passes
   return radix_sort_impl<uint64_t>(b, n, begin_bit, n_passes, s);
 }
 
-int tile_sort(const RadixSortBuffers& b, int64_t k, int tile_bits, cudaStream_t s) {
+int tile_sort(const RadixSortBuffers& b, int64_t k, int tile_bits, int id_bits, cudaStream_t s) {
   const int n_passes = tile_bits ? (tile_bits + 7) / 8 : 1;
   const int64_t blocks = (k + kSortTile - 1) / kSortTile;
   int launched = sort_setup(b, k, 32, n_passes, blocks, true, s);
   if (blocks == 0) return launched;
+  if (n_passes == 2 && (tile_bits - 8) + id_bits <= 32 && LMGS_TILE_SORT_PACKED) {
+    // the first pass writes 4-byte keys (tile >> 8) << id_bits | id (its low
+    // tile digit is the bucket a key lands in); the second sorts them on the
+    // high digit and writes the ids, counting tile runs with the low digit
+    // recovered from the first pass's bucket bounds
+    PassArgs a = pass_args(b, k, 32, 0, blocks);
+    a.id_bits = id_bits;
+    launch_pass<uint64_t, kOutPacked, kSegNone, false>(a, blocks, s);
+    a = pass_args(b, k, id_bits, 1, blocks);
+    a.id_bits = id_bits;
+    a.id_mask = id_bits >= 32 ? 0xffffffffu : (1u << id_bits) - 1u;
+    a.lo_pass = 0;
+    launch_pass<uint32_t, kOutIds, kSegLo, false>(a, blocks, s);
+    return launched + 2;
+  }
   for (int p = 0; p < n_passes; ++p) {
     const PassArgs a = pass_args(b, k, 32 + 8 * p, p, blocks);
     if (p + 1 == n_passes) launch_pass<uint64_t, kOutIds, kSegKey, false>(a, blocks, s);
