@@ -56,14 +56,14 @@ C5_PER_BLOCK = 6_250_000
 # dram__bytes_read.sum + dram__bytes_write.sum per c3 view of each stage's
 # kernels from the committed ncu launch list (stage = sum of its kernels);
 # reported as `traffic` beside the algorithmic bytes.
-NCU_TRAFFIC_SOURCE = "profiles/r06/ncu_launch_table.txt"
+NCU_TRAFFIC_SOURCE = "profiles/r10/ncu_launch_table.txt"
 NCU_TRAFFIC = {
-    "preprocess": 2782.0e6 / 2,  # one k_preprocess_tma<2> launch serves two views
-    "depth_sort": 48.1e6 + 3 * 43.0e6 + 106.1e6,
-    "emit": 258.7e6,
-    "tile_sort": 2 * 292.6e6,
-    "blend": 173.8e6,
-    "touched_fix": 112.6e6,
+    "preprocess": 2782.1e6 / 2,  # one k_preprocess_tma<2> launch serves two views
+    "depth_sort": 48.1e6 + 3 * 42.3e6 + 105.2e6,  # keys, 3 passes (concurrent grids), fix-up
+    "emit": 257.5e6,
+    "tile_sort": 222.6e6 + 123.8e6,  # u64 -> packed u32 pass, u32 -> ids pass
+    "blend": 162.5e6,
+    "touched_fix": 110.1e6,
 }
 
 

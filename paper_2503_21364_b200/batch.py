@@ -25,6 +25,14 @@ def tile_passes(tiles: int) -> int:
     return (bits + 7) // 8
 
 
+def packed_tile_sort(n, tiles, tile_passes) -> bool:
+    """Does the two-pass tile sort run its second pass on packed 4-byte keys
+    ((tile >> 8) << id_bits | id fits 32 bits; sort.cu tile_sort)?"""
+    id_bits = max(int(n - 1).bit_length(), 1)
+    tile_bits = max(int(tiles - 1).bit_length(), 1)
+    return tile_passes == 2 and (tile_bits - 8) + id_bits <= 32
+
+
 def alg_bytes_per_view(n, s_read, group, n_vis, k, tiles, tile_passes, processed, pixels):
     """Algorithmic HBM bytes of each stage for one view (DESIGN.md §3 table).
 
@@ -42,9 +50,11 @@ def alg_bytes_per_view(n, s_read, group, n_vis, k, tiles, tile_passes, processed
         "depth_sort": n * (12 + 12 + 16 + 16 + 4),
         # ranked ids 4 B + rect gather 8 B per visible splat, 8-B key per instance
         "emit": 12 * n_vis + 8 * k,
-        # each pass reads every 8-B key; all but the last write 8-B keys, the
-        # last writes the 4-B ids; ranges 8 B per tile
-        "tile_sort": (16 * tile_passes - 4) * k + 8 * tiles,
+        # each pass reads every key and writes it; the last writes the 4-B ids.
+        # Two passes with packed keys (sort.cu tile_sort): 8 -> 4 B, 4 -> 4 B;
+        # otherwise 8-B keys throughout; ranges 8 B per tile
+        "tile_sort": (20 if packed_tile_sort(n, tiles, tile_passes) else 16 * tile_passes - 4) * k
+        + 8 * tiles,
         # per processed instance a 4-B id + 64-B record; rgb, alpha, depth per
         # pixel; one range per tile; touched per Gaussian
         "blend": 68 * processed + 8 * tiles + 20 * pixels + 4 * n,

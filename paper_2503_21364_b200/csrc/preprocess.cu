@@ -306,6 +306,9 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess_direct(
 // Views after the first keep more state in flight (the unrolled view bodies
 // overlap); at 7 CTAs/SM (72 registers) they spill, so a multi-view block
 // runs at LMGS_PRE_MULTI_MIN_CTAS.
+#ifndef LMGS_PRE_VIEW_BARRIER
+#define LMGS_PRE_VIEW_BARRIER 1
+#endif
 #ifndef LMGS_PRE_MULTI_MIN_CTAS
 #define LMGS_PRE_MULTI_MIN_CTAS 5
 #endif
@@ -359,7 +362,9 @@ __global__ void __launch_bounds__(kPreThreads, NV == 1 ? LMGS_PRE_MIN_CTAS : LMG
   for (int vi = 0; vi < NV; ++vi) {
     // re-read the staged inputs every view (a compiler barrier keeps them
     // from being hoisted into registers that would live across views)
+#if LMGS_PRE_VIEW_BARRIER
     asm volatile("" ::: "memory");
+#endif
     const float4 q = reinterpret_cast<const float4*>(s_quats)[tid];
     const PreprocessArgs& av = m.v[vi];
     bool keep = false;

@@ -27,6 +27,9 @@ constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagIncl = 2u << 30;
 constexpr uint32_t kValueMask = (1u << 30) - 1;
 constexpr int kWarps = kSortThreads / 32;
+#ifndef LMGS_LOOKBACK_LATE
+#define LMGS_LOOKBACK_LATE 0
+#endif
 #ifndef LMGS_LOOK_WINDOW
 #define LMGS_LOOK_WINDOW 8
 #endif
@@ -486,6 +489,13 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) wpre += w < warp ? s_wsum[w] : 0;
     s_local_start[d] = wpre + incl - total;
+  }
+  const uint32_t local_start = s_local_start[tid];
+  // decoupled look-back for this tile's global digit offsets (thread d =
+  // digit d); LMGS_LOOKBACK_LATE runs it after the ranking, when the
+  // predecessors have had that long to publish
+  auto look_back = [&]() {
+    const int d = tid;
     // decoupled look-back for this tile's global digit offsets, right after
     // the early counts so the inclusive prefix is published before ranking.
     // Each digit's thread reads a window of kLookWindow predecessors with
@@ -511,8 +521,9 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
       }
       st_release(lb + (int64_t)bid * kRadix + d, kFlagIncl | (excl + total));
     }
-    s_global[d] = plan->digit_start[pass][d] + excl - (wpre + incl - total);
-  }
+    s_global[d] = plan->digit_start[pass][d] + excl - local_start;
+  };
+  if (!LMGS_LOOKBACK_LATE) look_back();
   // 3. stable in-warp ranking, items in (j, lane) order
 #ifdef LMGS_SORT_TRACE
   __syncthreads();
@@ -531,6 +542,7 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
     dg[j] |= (cm.x + __popc(below)) << 16;
     __syncwarp();
   }
+  if (LMGS_LOOKBACK_LATE) look_back();
   __syncthreads();
   TRACE(3)
   // 4. per digit: exclusive prefix over warps (the invalid items go behind
