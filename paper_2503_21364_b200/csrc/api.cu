@@ -34,6 +34,11 @@ inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 #define LMGS_SKIP_STAGES 0
 #endif
 constexpr unsigned kSkip = LMGS_SKIP_STAGES;
+// concurrent renders: K1 as a persistent grid of this many CTAs per SM (0:
+// one CTA per 128-row block)
+#ifndef LMGS_PRE_PERSIST_CTAS
+#define LMGS_PRE_PERSIST_CTAS 0  // 2-5: 749-780 vs 794 frames/s (profiles/r10/k1_persist_variants.txt)
+#endif
 
 const char* kStageNames[] = {"preprocess", "depth_sort", "emit", "tile_sort", "blend",
                              "touched_fix"};
@@ -797,8 +802,9 @@ int lmgs_render_group(lmgs_context* const* ctxs, int32_t n_views, const lmgs_gau
   DeviceGuard guard(ctxs[0]->device);
   cudaStream_t s0 = static_cast<cudaStream_t>(streams[0]);
   ViewPlan vp[LMGS_MAX_GROUP];
-  PreprocessMulti m;
+  PreprocessMulti m{};
   m.nv = n_views;
+  if (s->flags & LMGS_FLAG_CONCURRENT) m.persist_ctas = LMGS_PRE_PERSIST_CTAS;
   for (int v = 0; v < n_views; ++v) {
     lmgs_context* c = ctxs[v];
     cudaStream_t sv = static_cast<cudaStream_t>(streams[v]);

@@ -96,6 +96,8 @@ constexpr int kMaxPreViews = 8;
 struct PreprocessMulti {
   PreprocessArgs v[kMaxPreViews];
   int32_t nv;
+  int32_t persist_ctas;  // > 0: a persistent grid of this many CTAs per SM (set by the launcher's caller)
+  int64_t n_blocks;      // full 128-row blocks (set by launch_preprocess_multi)
 };
 int launch_preprocess_multi(const PreprocessMulti& m, cudaStream_t s);
 

@@ -127,7 +127,7 @@ __device__ __forceinline__ uint32_t process_one(const PreprocessArgs& a, int64_t
                                             double m2, float4 q, double s0, double s1, double s2,
                                             float logit, const float* sh, uint64_t* sh_wait,
                                             bool* keep_out, uint64_t* zbits_out,
-                                            const double* S = nullptr) {
+                                            const double* S = nullptr, uint32_t sh_phase = 0) {
   bool keep = false;
   uint32_t cnt = 0;
   uint64_t zb = 0;
@@ -168,7 +168,7 @@ __device__ __forceinline__ uint32_t process_one(const PreprocessArgs& a, int64_t
       const float log2_alpha =
           logit < -15.0f ? logit * (float)kLog2e : -log2f(1.0f + expf(-logit));
       float col[3] = {0.f, 0.f, 0.f};
-      if (SMEM) mbar_wait(sh_wait, 0);
+      if (SMEM) mbar_wait(sh_wait, sh_phase);
       if (cnt || a.dbg_colors) {
         const double dx = m0 - cam.center[0], dy = m1 - cam.center[1], dz = m2 - cam.center[2];
         double nrm = sqrt((dx * dx + dy * dy) + dz * dz);
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess_direct(
 #ifndef LMGS_PRE_MULTI_MIN_CTAS
 #define LMGS_PRE_MULTI_MIN_CTAS 5
 #endif
-template <int NV>
+template <int NV, bool LOOP>
 __global__ void __launch_bounds__(kPreThreads, NV == 1 ? LMGS_PRE_MIN_CTAS : LMGS_PRE_MULTI_MIN_CTAS)
     k_preprocess_tma(
     const __grid_constant__ PreprocessMulti m) {
@@ -325,21 +325,25 @@ __global__ void __launch_bounds__(kPreThreads, NV == 1 ? LMGS_PRE_MIN_CTAS : LMG
   float* s_sh = s_logits + kPreThreads;          // [256*ncoef*3]
   __shared__ __align__(8) uint64_t s_bar[2];
   const int tid = threadIdx.x;
-  const int64_t i0 = (int64_t)blockIdx.x * kPreThreads;
-  if (a.page_mask && a.page_mask[i0 >> 7] == 0) {  // the block is one inactive page
-#pragma unroll
-    for (int vi = 0; vi < NV; ++vi) {
-      cull_row(m.v[vi], i0 + tid);
-      count_kept(m.v[vi], false, 0, 0, vi);
-    }
-    return;
-  }
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
     mbar_init_fence();
   }
   __syncthreads();
+  // one block per CTA, or (m.blocks_per_cta: concurrent renders) a persistent
+  // grid walking blocks, the barriers' phase flipping every block
+  uint32_t phase = 0;
+  for (int64_t blk = blockIdx.x; blk < m.n_blocks; blk += LOOP ? gridDim.x : m.n_blocks, phase ^= 1) {
+  const int64_t i0 = blk * kPreThreads;
+  if (a.page_mask && a.page_mask[i0 >> 7] == 0) {  // the block is one inactive page
+#pragma unroll
+    for (int vi = 0; vi < NV; ++vi) {
+      cull_row(m.v[vi], i0 + tid);
+      count_kept(m.v[vi], false, 0, 0, vi);
+    }
+    continue;
+  }
   const uint32_t sh_bytes = (uint32_t)(kPreThreads * a.sh_coeffs * 3 * 4);
   if (tid == 0) {
     mbar_expect_tx(&s_bar[0], kPreThreads * (12 + 16 + 12 + 4));
@@ -350,7 +354,7 @@ __global__ void __launch_bounds__(kPreThreads, NV == 1 ? LMGS_PRE_MIN_CTAS : LMG
     mbar_expect_tx(&s_bar[1], sh_bytes);
     bulk_g2s(s_sh, a.sh + i0 * a.sh_coeffs * 3, sh_bytes, &s_bar[1]);
   }
-  mbar_wait(&s_bar[0], 0);
+  mbar_wait(&s_bar[0], phase);
   const int64_t i = i0 + tid;
   const bool dead = a.page_mask && tid >= (int)a.page_mask[i0 >> 7];  // past the page's live rows
   // the world covariance once for the whole group of views
@@ -377,19 +381,24 @@ __global__ void __launch_bounds__(kPreThreads, NV == 1 ? LMGS_PRE_MIN_CTAS : LMG
       cnt = process_one<true>(av, i, s_means[3 * tid], s_means[3 * tid + 1], s_means[3 * tid + 2],
                               q, s_scales[3 * tid], s_scales[3 * tid + 1], s_scales[3 * tid + 2],
                               s_logits[tid], s_sh + tid * a.sh_coeffs * 3, &s_bar[1], &keep, &zb,
-                              NV > 1 ? S : nullptr);
+                              NV > 1 ? S : nullptr, phase);
     }
     count_kept(av, keep, cnt, zb, vi);
   }
-  // every thread must observe the SH barrier before the block may exit
-  mbar_wait(&s_bar[1], 0);
+  // every thread must observe the SH barrier before the block may exit (or
+  // the staging be refilled)
+  mbar_wait(&s_bar[1], phase);
+  if (!LOOP) break;
+  fence_proxy_async_smem();  // this block's shared reads before the next block's TMA writes
+  __syncthreads();
+  }
 }
 
 
 }  // namespace
 
 int launch_preprocess(const PreprocessArgs& a, cudaStream_t s) {
-  PreprocessMulti m;
+  PreprocessMulti m{};
   m.v[0] = a;
   m.nv = 1;
   return launch_preprocess_multi(m, s);
@@ -407,24 +416,35 @@ int launch_preprocess_multi(const PreprocessMulti& m, cudaStream_t s) {
   const int64_t full = aligned ? a.n / kPreThreads : 0;
   if (full > 0) {
     const size_t smem = sizeof(float) * kPreThreads * (3 + 4 + 3 + 1 + 3 * a.sh_coeffs);
-    static size_t set[kMaxPreViews][kMaxDevices] = {};
+    static size_t set[2 * kMaxPreViews][kMaxDevices] = {};
     const int dev = current_device();
     void (*kern)(PreprocessMulti) = nullptr;
+    const bool loop = m.persist_ctas > 0;
     switch (m.nv) {
-      case 1: kern = k_preprocess_tma<1>; break;
-      case 2: kern = k_preprocess_tma<2>; break;
-      case 3: kern = k_preprocess_tma<3>; break;
-      case 4: kern = k_preprocess_tma<4>; break;
-      case 5: kern = k_preprocess_tma<5>; break;
-      case 6: kern = k_preprocess_tma<6>; break;
-      case 7: kern = k_preprocess_tma<7>; break;
-      default: kern = k_preprocess_tma<8>; break;
+      case 1: kern = loop ? k_preprocess_tma<1, true> : k_preprocess_tma<1, false>; break;
+      case 2: kern = loop ? k_preprocess_tma<2, true> : k_preprocess_tma<2, false>; break;
+      case 3: kern = loop ? k_preprocess_tma<3, true> : k_preprocess_tma<3, false>; break;
+      case 4: kern = loop ? k_preprocess_tma<4, true> : k_preprocess_tma<4, false>; break;
+      case 5: kern = k_preprocess_tma<5, false>; break;
+      case 6: kern = k_preprocess_tma<6, false>; break;
+      case 7: kern = k_preprocess_tma<7, false>; break;
+      default: kern = k_preprocess_tma<8, false>; break;
     }
-    if (smem > set[m.nv - 1][dev]) {
+    const int slot = (m.nv - 1) * 2 + (loop && m.nv <= 4 ? 1 : 0);
+    if (smem > set[slot][dev]) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      set[m.nv - 1][dev] = smem;
+      set[slot][dev] = smem;
     }
-    kern<<<(unsigned)full, kPreThreads, smem, s>>>(m);
+    PreprocessMulti mm = m;
+    mm.n_blocks = full;
+    int64_t grid = full;
+    if (loop && m.nv <= 4) {
+      static int sms[kMaxDevices] = {};
+      if (!sms[dev]) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+      const int64_t p = (int64_t)sms[dev] * m.persist_ctas;
+      if (grid > p) grid = p;
+    }
+    kern<<<(unsigned)grid, kPreThreads, smem, s>>>(mm);
     ++launched;
   }
   const int64_t first = full * kPreThreads;
