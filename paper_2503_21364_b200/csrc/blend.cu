@@ -344,6 +344,17 @@ constexpr int kWarpsPerBlock16 = 8;
 // With NP = 2 the per-splat work (shared loads, ballots, the touched atomic,
 // loop control) is shared by two pixels and the two pixels' dependency chains
 // interleave.
+// the first work item of a warp = its warp index (no counter round trip):
+// blend 0.413 -> 0.43 ms/view (a static first item unbalances the persistent
+// warps), off
+#ifndef LMGS_BLEND_STATIC_FIRST
+#define LMGS_BLEND_STATIC_FIRST 0
+#endif
+// list ids one batch further ahead than the records: blend 0.413 -> 0.398
+// ms/view (profiles/r10/blend_prefetch_variants.txt)
+#ifndef LMGS_BLEND_ID_AHEAD
+#define LMGS_BLEND_ID_AHEAD 1
+#endif
 #ifndef LMGS_BLEND_PAIRS
 #define LMGS_BLEND_PAIRS 0  // 1: two hits per trip, one break vote per pair (777.6 vs 777.3 frames/s: neutral, profiles/r10)
 #endif
@@ -365,10 +376,26 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
   const uint32_t* __restrict__ list = static_cast<const uint32_t*>(*a.keys_slot);
   const float4* __restrict__ rec4 = reinterpret_cast<const float4*>(a.recs);
 
+#if LMGS_BLEND_STATIC_FIRST
+  // the first item of every warp is its global warp index; the counter hands
+  // out the rest (no round trip before the first list load)
+  const int first_items = gridDim.x * kWarpsPerBlock16;
+  bool first = true;
+#endif
   while (true) {
     int item = 0;
+#if LMGS_BLEND_STATIC_FIRST
+    if (first) {
+      item = blockIdx.x * kWarpsPerBlock16 + warp;
+      first = false;
+    } else {
+      if (lane == 0) item = atomicAdd(a.work_counter, 1) + first_items;
+      item = __shfl_sync(0xffffffffu, item, 0);
+    }
+#else
     if (lane == 0) item = atomicAdd(a.work_counter, 1);
     item = __shfl_sync(0xffffffffu, item, 0);
+#endif
     if (item >= n_items) break;
     const int tile = item / kItemsPerTile, sub = item % kItemsPerTile;
     const int tile_x = tile % a.tiles_x, tile_y = tile / a.tiles_x;
@@ -416,6 +443,11 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
       g0 = __ldg(rec4 + 4 * (size_t)id);
       g1 = __ldg(rec4 + 4 * (size_t)id + 1);
     }
+#if LMGS_BLEND_ID_AHEAD
+    // the ids run one batch further ahead than the records, so a batch's
+    // record loads never wait on its id load
+    uint32_t id_next = range.x + 32 + lane < range.y ? list[range.x + 32 + lane] : 0u;
+#endif
     uint32_t box_mask = __ballot_sync(0xffffffffu, any_valid);  // lanes the box covers
     for (int b = range.x; b < range.y && live; b += 32) {
       const int j = b + lane;
@@ -450,7 +482,12 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
       }
       const float4 c0 = g0, c1 = g1;
       if (j + 32 < range.y) {  // prefetch the next batch
+#if LMGS_BLEND_ID_AHEAD
+        id = id_next;
+        if (j + 64 < range.y) id_next = list[j + 64];
+#else
         id = list[j + 32];
+#endif
         g0 = __ldg(rec4 + 4 * (size_t)id);
         g1 = __ldg(rec4 + 4 * (size_t)id + 1);
       }

@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   KI key[kSortItems];
   uint32_t val[VALS ? kSortItems : 1];
   uint32_t dg[kSortItems];  // digit (kRadix: invalid), then | rank in the warp << 16
-  uint32_t lo4[SEG == kSegLo ? kSortItems / 4 : 1];  // kSegLo: low tile digits, 4 per word
+  uint32_t lo_info = 0;  // kSegLo: the tile's first low digit | inner bucket starts << 16
   const int wbase = warp * 32 * kSortItems;
   if constexpr (SRC == kSrcEmit) {
     emit_keys(a, n, base, count, smem_raw, key);
@@ -435,7 +435,8 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
     }
   }
   // the loads above are in flight while the ranking state is cleared
-  if constexpr (SEG == kSegLo) s_dstart[tid] = plan->digit_start[a.lo_pass][tid];
+  uint32_t my_dstart = 0;  // kSegLo: start of bucket tid of the previous pass
+  if constexpr (SEG == kSegLo) my_dstart = plan->digit_start[a.lo_pass][tid];
   for (int i = tid; i < kWarps * (kRadix + 1); i += kSortThreads)
     (&s_wm[0][0])[i] = make_uint2(0u, 0u);
   s_hist[tid] = 0;  // kSortThreads == kRadix
@@ -448,30 +449,16 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) atomicAdd(&s_hist[dg[j]], 1u);
   if constexpr (SEG == kSegLo) {
-    // the bucket of input position p: the largest d with start[d] <= p.  A
-    // thread's items are increasing positions: search the first and the last,
-    // and walk the (rare) boundaries between them
-    auto bucket = [&](uint32_t p) {
-      int lo = 0, hi = kRadix - 1;
-#pragma unroll
-      for (int it = 0; it < kRadixBits; ++it) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_dstart[mid] <= p) lo = mid;
-        else hi = mid - 1;
-      }
-      return lo;
-    };
-    const uint32_t p0 = (uint32_t)base + wbase + lane;
-    int lo = bucket(p0);
-    const int lo_end = bucket(min(p0 + 32u * (kSortItems - 1), (uint32_t)(n - 1)));
-#pragma unroll
-    for (int j = 0; j < kSortItems / 4; ++j) lo4[j] = 0;
-#pragma unroll
-    for (int j = 0; j < kSortItems; ++j) {
-      if (lo != lo_end)
-        while (lo < lo_end && s_dstart[lo + 1] <= p0 + 32u * j) ++lo;
-      lo4[j / 4] |= (uint32_t)lo << (8 * (j % 4));
-    }
+    // the bucket of input position p is the number of buckets starting at or
+    // before p, less one (starts are non-decreasing).  The tile's first bucket
+    // and the buckets starting inside the tile come from two block counts;
+    // buckets average ~80K keys, so a 4096-key tile rarely holds a boundary
+    const uint32_t b0 = (uint32_t)base, b1 = (uint32_t)(base + count);
+    const int lo_first = __syncthreads_count(my_dstart <= b0) - 1;
+    const bool inner = my_dstart > b0 && my_dstart < b1;
+    const int n_inner = __syncthreads_count(inner);
+    if (inner) s_dstart[tid] = my_dstart;  // read at staging (the barriers below order it)
+    lo_info = (uint32_t)lo_first | (uint32_t)n_inner << 16;
   }
   __syncthreads();
   TRACE(1)
@@ -576,12 +563,27 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
     const uint32_t p = (dg[j] >> 16) + my[dg[j] & 0xffffu].x;
     s_keys[p] = key[j];
     if (VALS) s_vals[p] = val[j];
-    if constexpr (SEG == kSegLo) s_lo[p] = (uint8_t)(lo4[j / 4] >> (8 * (j % 4)));
+    if constexpr (SEG == kSegLo) {
+      // the key's input position's bucket: the tile's first one plus the
+      // inner buckets (lo_first + 1 ..) starting at or before it
+      const int lo_first = (int)(lo_info & 0xffffu), n_inner = (int)(lo_info >> 16);
+      int lo = lo_first;
+      for (int t = 1; t <= n_inner; ++t)
+        lo += s_dstart[lo_first + t] <= (uint32_t)base + wbase + j * 32 + lane;
+      s_lo[p] = (uint8_t)lo;
+    }
   }
   __syncthreads();
   TRACE(4)
   // 6. coalesced write-out: consecutive threads, consecutive staged positions
-  const bool segs = SEG != kSegNone && a.seg_counts && pass == plan->last_active;
+  bool segs = SEG != kSegNone && a.seg_counts && pass == plan->last_active;
+  if (SEG == kSegLo && segs && (lo_info >> 16) == 0) {
+    // one low digit for the whole tile (no bucket of the previous pass starts
+    // inside it): tile (d << 8 | lo) holds exactly the tile's count of digit d
+    const uint32_t c = s_hist[tid];
+    if (c) atomicAdd(a.seg_counts + ((uint32_t)tid << 8 | (lo_info & 0xffffu)), c);
+    segs = false;
+  }
   for (int i = tid; i < count; i += kSortThreads) {
     const KI k = s_keys[i];
     const uint32_t o = s_global[digit_of(k, shift)] + i;
