@@ -494,21 +494,25 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
     // then walks it from the nearest one, re-polling only unpublished entries.
     uint32_t excl = 0;
     if (bid != 0) {
-      int64_t look = (int64_t)bid - 1;
+      // a running pointer at predecessor `look`: the window's loads use
+      // immediate offsets (no 64-bit address arithmetic per load)
+      int look = (int)bid - 1;
+      const uint32_t* q = lb + (int64_t)look * kRadix + d;
       bool done = false;
       while (!done) {
         uint32_t v[kLookWindow];
 #pragma unroll
         for (int w = 0; w < kLookWindow; ++w)
-          v[w] = look - w >= 0 ? ld_acquire(lb + (look - w) * kRadix + d) : kFlagIncl;
+          v[w] = look - w >= 0 ? ld_acquire(q - w * kRadix) : kFlagIncl;
 #pragma unroll
         for (int w = 0; w < kLookWindow; ++w) {
           if (done) break;
-          while ((v[w] & ~kValueMask) == 0) v[w] = ld_acquire(lb + (look - w) * kRadix + d);
+          while ((v[w] & ~kValueMask) == 0) v[w] = ld_acquire(q - w * kRadix);
           excl += v[w] & kValueMask;
           done = (v[w] & ~kValueMask) == kFlagIncl;
         }
         look -= kLookWindow;
+        q -= kLookWindow * kRadix;
       }
       st_release(lb + (int64_t)bid * kRadix + d, kFlagIncl | (excl + total));
     }
