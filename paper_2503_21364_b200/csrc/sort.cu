@@ -504,12 +504,23 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
 #pragma unroll
         for (int w = 0; w < kLookWindow; ++w)
           v[w] = look - w >= 0 ? ld_acquire(q - w * kRadix) : kFlagIncl;
+        bool all_pub = true;
 #pragma unroll
-        for (int w = 0; w < kLookWindow; ++w) {
-          if (done) break;
-          while ((v[w] & ~kValueMask) == 0) v[w] = ld_acquire(q - w * kRadix);
-          excl += v[w] & kValueMask;
-          done = (v[w] & ~kValueMask) == kFlagIncl;
+        for (int w = 0; w < kLookWindow; ++w) all_pub &= (v[w] & ~kValueMask) != 0;
+        if (all_pub) {  // the common case: a predicated walk, no polling branches
+#pragma unroll
+          for (int w = 0; w < kLookWindow; ++w) {
+            excl += done ? 0u : (v[w] & kValueMask);
+            done = done || (v[w] & ~kValueMask) == kFlagIncl;
+          }
+        } else {
+#pragma unroll
+          for (int w = 0; w < kLookWindow; ++w) {
+            if (done) break;
+            while ((v[w] & ~kValueMask) == 0) v[w] = ld_acquire(q - w * kRadix);
+            excl += v[w] & kValueMask;
+            done = (v[w] & ~kValueMask) == kFlagIncl;
+          }
         }
         look -= kLookWindow;
         q -= kLookWindow * kRadix;
