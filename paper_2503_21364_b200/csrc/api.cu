@@ -176,6 +176,20 @@ int fail(lmgs_context* c, int code, const std::string& msg) {
     }                                                                                 \
   } while (0)
 
+#ifndef LMGS_SERIAL_K1
+#define LMGS_SERIAL_K1 0  // 1: 805.4 vs 807.4 frames/s (neutral, profiles/r10/k1_serial_variants.txt)
+#endif
+// one event per device ordering the K1 launches of concurrent renders
+cudaEvent_t k1_serial_event(int dev) {
+  static cudaEvent_t ev[kMaxDevices] = {};
+  if (dev < 0 || dev >= kMaxDevices) return nullptr;
+  if (!ev[dev] && cudaEventCreateWithFlags(&ev[dev], cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    ev[dev] = nullptr;
+  }
+  return ev[dev];
+}
+
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {
@@ -819,7 +833,20 @@ int lmgs_render_group(lmgs_context* const* ctxs, int32_t n_views, const lmgs_gau
     ctxs[v]->pre_share = n_views;
     if (vp[v].timed) LMGS_CUDA(ctxs[v], cudaEventRecord(ctxs[v]->ev[0], s0));
   }
+  // concurrent renders: the K1 launches of the batch run one after another
+  // (each waits for the previous group's K1, in host order), the other
+  // streams' sorts and blends filling the SMs around them
+  cudaEvent_t k1_done = nullptr;
+  if ((s->flags & LMGS_FLAG_CONCURRENT) && LMGS_SERIAL_K1) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s0, &cap);
+    if (cap == cudaStreamCaptureStatusNone) {
+      k1_done = k1_serial_event(ctxs[0]->device);
+      if (k1_done) LMGS_CUDA(ctxs[0], cudaStreamWaitEvent(s0, k1_done, 0));
+    }
+  }
   const int k1 = launch_preprocess_multi(m, s0);
+  if (k1_done) LMGS_CUDA(ctxs[0], cudaEventRecord(k1_done, s0));
   for (int v = 0; v < n_views; ++v) {
     lmgs_context* c = ctxs[v];
     cudaStream_t sv = static_cast<cudaStream_t>(streams[v]);

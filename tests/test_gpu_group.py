@@ -148,3 +148,22 @@ def test_group_mixed_image_sizes(scene):
         assert torch.equal(o["touched"], ref.touched)
         assert torch.equal(o["kept"], ref.kept)
         assert torch.equal(o["ranges"], ref.tile_ranges)
+
+
+def test_concurrent_batch_equals_lone_renders():
+    """A batch over several streams (LMGS_FLAG_CONCURRENT: persistent one-CTA-
+    per-SM sort grids, look-back after ranking, packed tile pass) equals one
+    render() per view with the one-CTA-per-tile grids, at 1080p where every
+    pass walks thousands of tiles per CTA."""
+    from paper_2503_21364_b200.raster import render
+
+    model = GaussianModel.from_host(scenes.synthetic_gaussians(200_000, seed=9), validate=False)
+    cams = scenes.orbit_cameras(6, 1920, 1080, seed=9)
+    got = _render_all(model, cams, 1920, 1080, 2, n_streams=4)
+    for i, cam in enumerate(cams):
+        o = render(cam, model, 16, sh_eval_degree=3)
+        torch.cuda.synchronize()
+        ref = {"rgb": o.rgb, "alpha": o.alpha, "depth": o.depth, "touched": o.touched,
+               "kept": o.kept, "ranges": o.tile_ranges, "nproc": o.n_processed}
+        for f in FIELDS:
+            assert torch.equal(ref[f].cpu(), got[f][i]), (i, f)
