@@ -126,7 +126,6 @@ struct lmgs_context {
   int sms = 148;
   std::string err;
   DevBuf gbuf, tbuf, ibuf, bwbuf, fixbuf, npbuf;  // npbuf: override (-1) + list, W*H each
-  DevBuf covbuf;  // fused tile sort: per-CTA coverage arrays + their sum
   Scalars* d_scal = nullptr;
   uint64_t* h_pinned = nullptr;  // [0..2] = n_kept, n_vis, K
   cudaEvent_t ev[2 * kNumStages] = {};
@@ -479,70 +478,60 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
   const int64_t cap_view = nosync ? k : c->cap_k;
   c->stats.capacity = cap_view;
 
-  // fused K4 + K5 on request (tile ids < 2^16 whose packed second-pass key
-  // fits 32 bits)
+  // fused K4 + K5 on request (two tile passes whose packed second-pass key
+  // fits 32 bits): rank records instead of instance keys
   const int tile_bits = bits_for(tiles);
   const int id_bits = n > 1 ? bits_for(n) : 1;
-  const int64_t cover_d = (int64_t)(ca.tiles_x + 1) * (ca.tiles_y + 1);
   const bool fused = (st->flags & LMGS_FLAG_FUSED_TILE_SORT) && tile_bits > 8 &&
-                     tile_bits <= 16 && (tile_bits - 8) + id_bits <= 32 &&
-                     cover_d * 4 <= kMaxCoverBytes;
+                     tile_bits <= 16 && (tile_bits - 8) + id_bits <= 32;
   if (fused) {
     tm.begin(2);
-    const int grid = cover_grid(ca.tiles_x, ca.tiles_y, n, c->sms);
-    const size_t part_bytes = align_up(sizeof(int32_t) * (size_t)(grid > 0 ? grid : 1) * cover_d);
-    if (part_bytes + sizeof(int32_t) * cover_d > c->covbuf.bytes) {
-      LMGS_CUDA(c, cudaStreamSynchronize(s));
-      LMGS_CUDA(c, c->covbuf.reserve(part_bytes + sizeof(int32_t) * cover_d));
-    }
-    int32_t* cover_part = static_cast<int32_t*>(c->covbuf.ptr);
-    int32_t* cover = reinterpret_cast<int32_t*>(static_cast<char*>(c->covbuf.ptr) + part_bytes);
-    LMGS_CUDA(c, cudaMemsetAsync(cover, 0, sizeof(int32_t) * cover_d, s));
-    launched += launch_cover(c->rects, n, ca.tiles_x, ca.tiles_y, cover_part, grid, s);
-    launched += launch_cover_reduce(cover_part, grid, cover_d, cover, s);
+    LMGS_CUDA(c, cudaMemsetAsync(sc->tile_hist, 0, sizeof(sc->tile_hist), s));
+    LMGS_CUDA(c, cudaMemsetAsync(sc->emit_ticket, 0, sizeof(uint32_t), s));
     if (n_vis > 0) {
-      RankScanArgs ra{};
-      ra.order_slot = &sc->slots.depth_ids;
-      ra.rects = c->rects;
-      ra.n_vis = n_vis;
-      ra.n_vis_dev = &sc->counts[1];
-      ra.rrec = c->rrec;
-      ra.chunk_first = c->chunk_first;
-      ra.n_sort_tiles = (cap_view + kSortTile - 1) / kSortTile;
-      ra.chunk_sums = reinterpret_cast<uint32_t*>(c->emit_lookback);  // free on this path
-      launched += launch_rank_scan(ra, s);
+      LMGS_CUDA(c, cudaMemsetAsync(c->emit_lookback, 0, sizeof(uint64_t) * emit_chunks(n_vis), s));
+      EmitArgs ea{};
+      ea.order_slot = &sc->slots.depth_ids;
+      ea.rects = c->rects;
+      ea.n_vis = n_vis;
+      ea.n_vis_dev = &sc->counts[1];
+      ea.cap = (uint64_t)cap_view;
+      ea.tiles_x = ca.tiles_x;
+      ea.n_tile_passes = 2;
+      ea.lookback = c->emit_lookback;
+      ea.ticket = sc->emit_ticket;
+      ea.hist = sc->tile_hist;
+      ea.rrec = c->rrec;
+      ea.chunk_first = c->chunk_first;
+      ea.n_sort_tiles = (cap_view + kSortTile - 1) / kSortTile;
+      ea.k_dev = &sc->counts[2];
+      if (!(kSkip & 4)) launched += launch_emit_ranks(ea, s);
     }
-    TilePlanArgs pa{};
-    pa.cover = cover;
-    pa.tiles_x = ca.tiles_x;
-    pa.tiles_y = ca.tiles_y;
-    pa.ranges = ranges;
-    pa.tile_count = c->tile_count;
-    pa.plan = &sc->tile_plan;
-    pa.k_dev = &sc->counts[2];
-    pa.cap = (uint64_t)cap_view;
-    pa.k_eff = &sc->k_eff;
-    pa.max_k = nosync ? &sc->max_k : nullptr;
-    pa.keys_result = &sc->slots.inst_ids;
-    pa.result = c->inst_keys[0];
-    launched += launch_tile_plan(pa, s);
     tm.end(2);
     tm.begin(3);
-    FusedTileSort fs{};
-    fs.keys[0] = c->inst_keys[0];
-    fs.keys[1] = c->inst_keys[1];
-    fs.k_bound = k;
-    fs.k_dev = nosync ? &sc->k_eff : nullptr;
-    fs.plan = &sc->tile_plan;
-    fs.lookback = c->tile_lookback;
-    fs.counters = sc->tile_counters;
-    fs.rrec = c->rrec;
-    fs.chunk_first = c->chunk_first;
-    fs.n_vis_dev = &sc->counts[1];
-    fs.tiles_x = ca.tiles_x;
-    fs.id_bits = id_bits;
-    fs.concurrent = (st->flags & LMGS_FLAG_CONCURRENT) != 0;
-    launched += tile_sort_fused(fs, s);
+    RadixSortBuffers rb{};
+    rb.keys[0] = c->inst_keys[0];
+    rb.keys[1] = c->inst_keys[1];
+    rb.key_bytes = 8;
+    rb.plan = &sc->tile_plan;
+    rb.hist = sc->tile_hist;
+    rb.lookback = c->tile_lookback;
+    rb.counters = sc->tile_counters;
+    rb.keys_result = &sc->slots.inst_ids;
+    rb.hist_ready = true;
+    rb.seg_counts = c->tile_count;
+    rb.seg_shift = 32;
+    rb.concurrent = (st->flags & LMGS_FLAG_CONCURRENT) != 0;
+    if (nosync) {
+      rb.n_dev = &sc->counts[2];
+      rb.max_n = &sc->max_k;
+    }
+    LMGS_CUDA(c, cudaMemsetAsync(c->tile_count, 0, sizeof(uint32_t) * tiles, s));
+    if (!(kSkip & 8)) {
+      launched += tile_sort_fused(rb, k, id_bits, c->rrec, c->chunk_first, &sc->counts[1],
+                                  ca.tiles_x, s);
+      launched += launch_ranges_from_counts(c->tile_count, (int)tiles, ranges, cap_view, s);
+    }
   } else {
   // K4
   tm.begin(2);
@@ -742,7 +731,6 @@ void lmgs_context_destroy(lmgs_context* c) {
   c->bwbuf.release();
   c->fixbuf.release();
   c->npbuf.release();
-  c->covbuf.release();
   if (c->d_scal) cudaFree(c->d_scal);
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   for (int i = 0; i < 2 * kNumStages; ++i)

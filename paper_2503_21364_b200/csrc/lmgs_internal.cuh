@@ -169,27 +169,14 @@ int radix_sort(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_passes
 // on packed 4-byte keys when (tile_bits - 8) + id_bits <= 32)
 int tile_sort(const RadixSortBuffers& b, int64_t k, int tile_bits, int id_bits, cudaStream_t s);
 
-// K4+K5 fused (tile ids < 2^16, (tile bits - 8) + id bits <= 32): the first
-// pass generates its instance keys from the rank records (K4r, below) instead
-// of reading an emitted array, ranks them on the low tile digit and writes u32
-// keys (tile >> 8) << id_bits | id; the second pass sorts those on the high
-// digit and writes the ids.  The plan (digit starts of both passes) comes
-// from K4p's tile counts.
-struct FusedTileSort {
-  void* keys[2];                 // keys[1]: packed u32, keys[0]: the ids (result)
-  int64_t k_bound;               // K, or its capacity (k_dev then holds K)
-  const unsigned long long* k_dev;  // nullable: the count on the device
-  const RadixPlan* plan;
-  uint32_t* lookback;            // [2 * tiles * kRadix]
-  uint32_t* counters;            // [kMaxPasses]
-  const uint4* rrec;
-  const uint32_t* chunk_first;
-  const unsigned long long* n_vis_dev;
-  int32_t tiles_x;
-  int32_t id_bits;
-  bool concurrent;
-};
-int tile_sort_fused(const FusedTileSort& f, cudaStream_t s);  // kernels launched
+// K4+K5 fused (LMGS_FLAG_FUSED_TILE_SORT; two tile passes, (tile bits - 8) +
+// id bits <= 32): k_emit_ranks writes the rank records and both digit
+// histograms, the first pass generates its instance keys from the records
+// instead of reading an emitted array and writes packed u32 keys, the second
+// ranks those and writes the ids with the range counts (kSegLo).
+int tile_sort_fused(const RadixSortBuffers& b, int64_t k, int id_bits, const uint4* rrec,
+                    const uint32_t* chunk_first, const unsigned long long* n_vis_dev, int tiles_x,
+                    cudaStream_t s);  // kernels launched
 
 // Device-side slots naming where a sort's result landed (written by the plan
 // kernel, read by consumers) so the pipeline never syncs on it.
@@ -244,57 +231,18 @@ struct EmitArgs {
   uint32_t* ticket;         // chunk ticket counter (zeroed)
   uint32_t* hist;           // [kMaxTilePasses][256] digit histograms (zeroed)
   bool concurrent;          // LMGS_FLAG_CONCURRENT: a persistent grid sharing the SMs
+  // k_emit_ranks (fused tile sort)
+  uint4* rrec;              // [n_vis] {rect lo, rect hi, id, first slot}
+  uint32_t* chunk_first;    // [n_sort_tiles] rank holding each sort tile's first slot
+  int64_t n_sort_tiles;
+  const unsigned long long* k_dev;  // K (no histogram when it exceeds cap)
 };
+int launch_emit_ranks(const EmitArgs& a, cudaStream_t s);
 #ifndef LMGS_EMIT_PERSIST_CTAS
 #define LMGS_EMIT_PERSIST_CTAS 0  // > 0: concurrent renders emit with this many CTAs per SM
 #endif
 inline int64_t emit_chunks(int64_t n_vis) { return (n_vis + kEmitChunk - 1) / kEmitChunk; }
 int launch_emit(const EmitArgs& a, cudaStream_t s);
-
-// K4c (fused path): the 2-D difference array of the rects' tile coverage,
-// one per CTA of a persistent grid over the rects in id order (four shared
-// atomics per splat); K4p's 2-D prefix sum of their total = per-tile counts.
-constexpr int kMaxCoverBytes = 160 * 1024;  // (tiles_x + 1) * (tiles_y + 1) int32 in smem
-int cover_grid(int tiles_x, int tiles_y, int64_t n, int sms);  // = number of partial arrays
-int launch_cover(const uint64_t* rects, int64_t n, int tiles_x, int tiles_y, int32_t* cover_part,
-                 int grid, cudaStream_t s);
-// K4r (fused path): walk the splats in depth-rank order, scan their tile
-// counts (reduce, scan, write: three launches), write one 16-B record per rank {rect, id,
-// first instance slot} and the first rank of every kSortTile-slot sort tile.
-constexpr int kRankThreads = 512;
-constexpr int kRankItems = 4;
-constexpr int kRankChunk = kRankThreads * kRankItems;
-inline int64_t rank_chunks(int64_t n_vis) { return (n_vis + kRankChunk - 1) / kRankChunk; }
-struct RankScanArgs {
-  void* const* order_slot;
-  const uint64_t* rects;
-  int64_t n_vis;
-  const unsigned long long* n_vis_dev;
-  uint4* rrec;                // [n_vis]
-  uint32_t* chunk_first;      // [n_sort_tiles]
-  int64_t n_sort_tiles;       // capacity of chunk_first (slots past it are not sorted)
-  uint32_t* chunk_sums;       // [rank_chunks(n_vis)] scratch
-};
-int launch_rank_scan(const RankScanArgs& a, cudaStream_t s);
-// sums the partial arrays into cover (zeroed by the caller)
-int launch_cover_reduce(const int32_t* part, int parts, int64_t d, int32_t* cover, cudaStream_t s);
-// K4p (one CTA): 2-D prefix of the coverage = per-tile counts -> tile ranges
-// (clamped: all empty if K > cap), the two digit histograms -> the fused
-// sort's plan, the effective key count, the result slot
-struct TilePlanArgs {
-  const int32_t* cover;
-  int32_t tiles_x, tiles_y;
-  int2* ranges;
-  uint32_t* tile_count;       // nullable: per-tile counts
-  RadixPlan* plan;
-  const unsigned long long* k_dev;  // K from K1
-  uint64_t cap;
-  unsigned long long* k_eff;  // K, or 0 after an overflow
-  unsigned long long* max_k;  // nullable: atomicMax(K)
-  void** keys_result;
-  void* result;
-};
-int launch_tile_plan(const TilePlanArgs& a, cudaStream_t s);
 
 // K6: tile ranges [start, end) = exclusive scan of the per-tile counts the
 // tile sort's last pass accumulated (empty tiles included)

@@ -269,8 +269,10 @@ __device__ __forceinline__ void emit_keys(const PassArgs& a, int64_t n, int64_t 
   const uint32_t r0 = a.chunk_first[b];
   // ranks r0 .. r_last cover the tile (r_last = the next tile's first rank,
   // which may start exactly at its first slot: the mark below skips it)
-  const uint32_t r_end = base + count < n ? a.chunk_first[b + 1] + 1 : (uint32_t)*a.n_vis_dev;
-  const int nr = (int)(r_end - r0);
+  const uint32_t n_vis = (uint32_t)*a.n_vis_dev;
+  const uint32_t r_end = min(base + count < n ? a.chunk_first[b + 1] + 1 : n_vis, n_vis);
+  // (clamped: a no-sync overflow leaves the records past the capacity stale)
+  const int nr = max(0, min((int)(r_end - r0), count + 1));
   const uint32_t slot0 = (uint32_t)base, slot_end = (uint32_t)(base + count);
   static_assert(kSortItems % 2 == 0, "owner offsets are scanned in u16 pairs");
   for (int i = tid; i < kSortTile / 8; i += kSortThreads)
@@ -548,7 +550,7 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
     dg[j] |= (cm.x + __popc(below)) << 16;
     __syncwarp();
   }
-  if (LMGS_LOOKBACK_LATE) look_back();
+  if (LMGS_LOOKBACK_LATE == 1) look_back();
   __syncthreads();
   TRACE(3)
   // 4. per digit: exclusive prefix over warps (the invalid items go behind
@@ -588,6 +590,7 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
       s_lo[p] = (uint8_t)lo;
     }
   }
+  if (LMGS_LOOKBACK_LATE == 2) look_back();  // only the write-out needs the global offsets
   __syncthreads();
   TRACE(4)
   // 6. coalesced write-out: consecutive threads, consecutive staged positions
@@ -775,36 +778,27 @@ int tile_sort(const RadixSortBuffers& b, int64_t k, int tile_bits, int id_bits, 
   return launched + n_passes;
 }
 
-int tile_sort_fused(const FusedTileSort& f, cudaStream_t s) {
-  if (f.k_bound <= 0) return 0;
-  const int64_t blocks = (f.k_bound + kSortTile - 1) / kSortTile;
-  cudaMemsetAsync(f.counters, 0, sizeof(uint32_t) * kMaxPasses, s);
-  cudaMemsetAsync(f.lookback, 0, sizeof(uint32_t) * 2 * (size_t)blocks * kRadix, s);
-  PassArgs a{};
-  a.keys[0] = f.keys[0];
-  a.keys[1] = f.keys[1];
-  a.n = f.k_bound;
-  a.plan = f.plan;
-  a.lookback = f.lookback;
-  a.counter = f.counters;
-  a.lb_stride = blocks;
-  a.n_dev = f.k_dev;
-  a.concurrent = f.concurrent;
-  a.id_bits = f.id_bits;
-  a.id_mask = f.id_bits >= 32 ? 0xffffffffu : (1u << f.id_bits) - 1u;
-  a.rrec = f.rrec;
-  a.chunk_first = f.chunk_first;
-  a.n_vis_dev = f.n_vis_dev;
-  a.tiles_x = f.tiles_x;
-  // pass 0: generated keys, low tile digit -> keys[1] (u32 packed)
-  a.shift = 32;
-  a.pass = 0;
+int tile_sort_fused(const RadixSortBuffers& b, int64_t k, int id_bits, const uint4* rrec,
+                    const uint32_t* chunk_first, const unsigned long long* n_vis_dev, int tiles_x,
+                    cudaStream_t s) {
+  const int64_t blocks = (k + kSortTile - 1) / kSortTile;
+  int launched = sort_setup(b, k, 32, 2, blocks, true, s);
+  if (blocks == 0) return launched;
+  PassArgs a = pass_args(b, k, 32, 0, blocks);
+  a.id_bits = id_bits;
+  a.rrec = rrec;
+  a.chunk_first = chunk_first;
+  a.n_vis_dev = n_vis_dev;
+  a.tiles_x = tiles_x;
+  // pass 0: keys generated from the rank records, low tile digit, packed out
   launch_pass<uint64_t, kOutPacked, kSegNone, false, kSrcEmit>(a, blocks, s);
-  // pass 1: the high tile digit of the packed keys -> keys[0] (u32 ids)
-  a.shift = f.id_bits;
-  a.pass = 1;
-  launch_pass<uint32_t, kOutIds, kSegNone, false>(a, blocks, s);
-  return 2;
+  // pass 1: the high digit of the packed keys -> ids, range counts
+  a = pass_args(b, k, id_bits, 1, blocks);
+  a.id_bits = id_bits;
+  a.id_mask = id_bits >= 32 ? 0xffffffffu : (1u << id_bits) - 1u;
+  a.lo_pass = 0;
+  launch_pass<uint32_t, kOutIds, kSegLo, false>(a, blocks, s);
+  return launched + 2;
 }
 
 }  // namespace lmgs

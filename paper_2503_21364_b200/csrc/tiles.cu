@@ -343,174 +343,136 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(EmitArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// K4c: tile coverage of the fused path.  The rects are streamed in id order
-// (a persistent grid, one shared array per CTA) into a 2-D difference array:
-// +1 at (x0, y0) and (x1+1, y1+1), -1 at (x1+1, y0) and (x0, y1+1) — four
-// shared atomics per splat, 0 net for kEmptyRect.  Its 2-D prefix sum (K4p)
-// is the number of splats overlapping each tile: the tile ranges and both
-// digit histograms of the fused sort without touching the instances.
+// K4 for the fused tile sort (k_emit_ranks): the same rank-ordered scan as
+// k_emit (chunks of kEmitChunk ranks by ticket, warp scans, warp-cooperative
+// look-back), but instead of expanding every splat into instance keys it
+// writes one 16-B record per rank {rect lo, rect hi, id, first slot} and the
+// first rank of every kSortTile-slot sort tile; the tile sort's first pass
+// generates its keys from them (sort.cu, kSrcEmit).  The digit histograms of
+// both tile passes are computed per rect row without touching the instances:
+// a row's tiles t0..t1 are consecutive ids, so their low digits are a cyclic
+// range of 256 bins (a difference array: +1 / -1 at its ends, + whole cycles)
+// and their high digits one or two bins.
 
-constexpr int kCoverThreads = 512;
-__global__ void __launch_bounds__(kCoverThreads) k_cover(const uint64_t* __restrict__ rects,
-                                                         int64_t n, int tiles_x, int tiles_y,
-                                                         int32_t* cover_part) {
-  extern __shared__ int32_t s_cover[];
-  const int tid = threadIdx.x;
-  const int cw = tiles_x + 1;
-  const int d = cw * (tiles_y + 1);
-  for (int i = tid; i < d; i += kCoverThreads) s_cover[i] = 0;
+__global__ void __launch_bounds__(kEmitThreads) k_emit_ranks(EmitArgs a) {
+  constexpr int NW = kEmitThreads / 32;
+  __shared__ int32_t s_dlo[257];       // low-digit difference array
+  __shared__ uint32_t s_hi[256];       // high-digit counts
+  __shared__ uint32_t s_wtot[NW];
+  __shared__ uint32_t s_ticket;
+  __shared__ uint32_t s_lo_all;        // whole 256-tile cycles (every low digit)
+  __shared__ unsigned long long s_excl;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < 257; i += kEmitThreads) s_dlo[i] = 0;
+  for (int i = tid; i < 256; i += kEmitThreads) s_hi[i] = 0;
+  if (tid == 0) s_lo_all = 0;
+  const int64_t n_vis = min(a.n_vis, (int64_t)*a.n_vis_dev);  // the grid covers a bound
+  const uint32_t tx = (uint32_t)a.tiles_x;
+  uint32_t lo_all = 0;
+  for (;;) {
+  if (tid == 0) s_ticket = atomicAdd(a.ticket, 1u);
   __syncthreads();
-  constexpr int U = 4;  // rects per thread per step (two 16-B loads)
-  const int64_t stride = (int64_t)gridDim.x * kCoverThreads * U;
-  for (int64_t i0 = ((int64_t)blockIdx.x * kCoverThreads + tid) * U; i0 < n; i0 += stride) {
-    uint64_t r[U];
-    if (i0 + U <= n) {
-      const uint4 v0 = __ldcs(reinterpret_cast<const uint4*>(rects + i0));
-      const uint4 v1 = __ldcs(reinterpret_cast<const uint4*>(rects + i0) + 1);
-      r[0] = v0.x | ((uint64_t)v0.y << 32);
-      r[1] = v0.z | ((uint64_t)v0.w << 32);
-      r[2] = v1.x | ((uint64_t)v1.y << 32);
-      r[3] = v1.z | ((uint64_t)v1.w << 32);
-    } else {
-#pragma unroll
-      for (int u = 0; u < U; ++u) r[u] = i0 + u < n ? rects[i0 + u] : kEmptyRect;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (r[u] == kEmptyRect) continue;
-      int x0, y0, x1, y1;
-      unpack_rect(r[u], x0, y0, x1, y1);
-      atomicAdd(&s_cover[y0 * cw + x0], 1);
-      atomicAdd(&s_cover[y0 * cw + x1 + 1], -1);
-      atomicAdd(&s_cover[(y1 + 1) * cw + x0], -1);
-      atomicAdd(&s_cover[(y1 + 1) * cw + x1 + 1], 1);
-    }
-  }
-  __syncthreads();
-  int32_t* part = cover_part + (int64_t)blockIdx.x * d;
-  for (int i = tid; i < d; i += kCoverThreads) part[i] = s_cover[i];
-}
-
-// ---------------------------------------------------------------------------
-// K4r: rank scan of the fused path (see lmgs_internal.cuh), reduce-then-scan:
-// k_rank_sums adds up the tile counts of every chunk of kRankChunk ranks,
-// k_rank_offsets (one CTA) scans the chunk sums, k_rank_write re-gathers the
-// rects (L2-resident by then) and writes per rank {rect lo, rect hi, id,
-// first slot} plus the first rank of every sort tile.  No CTA waits on
-// another (a chained look-back left ~half the warps parked at a barrier).
-// Thread t of a chunk owns 4 consecutive ranks (one 16-B id load).
-
-__device__ __forceinline__ void rank_chunk_load(const RankScanArgs& a, int64_t n_vis, int64_t r0,
-                                                uint32_t (&id)[kRankItems],
-                                                uint64_t (&rect)[kRankItems],
-                                                uint32_t (&cnt)[kRankItems]) {
+  const int64_t chunk = s_ticket;
+  if (chunk * kEmitChunk >= n_vis) break;
   const uint32_t* __restrict__ order = static_cast<const uint32_t*>(*a.order_slot);
-  if (r0 + kRankItems <= n_vis) {
-    const uint4 v = *reinterpret_cast<const uint4*>(order + r0);  // 16-B aligned
-    id[0] = v.x, id[1] = v.y, id[2] = v.z, id[3] = v.w;
-  } else {
+  // blocked layout: thread t owns ranks r0 .. r0 + kEmitItems - 1
+  const int64_t r0 = chunk * kEmitChunk + (int64_t)tid * kEmitItems;
+  uint32_t id[kEmitItems];
+  uint64_t rect[kEmitItems];
+  uint32_t cnt[kEmitItems];
+  uint32_t sum = 0;
 #pragma unroll
-    for (int j = 0; j < kRankItems; ++j) id[j] = r0 + j < n_vis ? order[r0 + j] : 0xffffffffu;
-  }
+  for (int j = 0; j < kEmitItems; ++j) id[j] = r0 + j < n_vis ? order[r0 + j] : 0xffffffffu;
 #pragma unroll
-  for (int j = 0; j < kRankItems; ++j)
+  for (int j = 0; j < kEmitItems; ++j)
     rect[j] = id[j] != 0xffffffffu ? __ldg(a.rects + id[j]) : kEmptyRect;
 #pragma unroll
-  for (int j = 0; j < kRankItems; ++j) {
+  for (int j = 0; j < kEmitItems; ++j) {
     int x0, y0, x1, y1;
     unpack_rect(rect[j], x0, y0, x1, y1);
-    cnt[j] = (uint32_t)(x1 - x0 + 1) * (uint32_t)(y1 - y0 + 1);  // 0 for kEmptyRect
+    const uint32_t w = (uint32_t)(x1 - x0 + 1);
+    cnt[j] = w * (uint32_t)(y1 - y0 + 1);  // 0 for kEmptyRect
+    sum += cnt[j];
+    // digit histograms, one rect row at a time
+    for (int y = y0; y <= y1 && w; ++y) {
+      const uint32_t t0 = (uint32_t)y * tx + (uint32_t)x0, t1 = t0 + w - 1;
+      lo_all += w >> 8;
+      const uint32_t rem = w & 255u, ds = t0 & 255u;
+      if (rem) {
+        atomicAdd(&s_dlo[ds], 1);
+        if (ds + rem <= 256u) {
+          atomicAdd(&s_dlo[ds + rem], -1);
+        } else {
+          atomicAdd(&s_dlo[256], -1);
+          atomicAdd(&s_dlo[0], 1);
+          atomicAdd(&s_dlo[ds + rem - 256u], -1);
+        }
+      }
+      const uint32_t h0 = t0 >> 8, h1 = t1 >> 8;
+      if (h0 == h1) {
+        atomicAdd(&s_hi[h0 & 255u], w);
+      } else {
+        atomicAdd(&s_hi[h0 & 255u], 256u - (t0 & 255u));
+        for (uint32_t h = h0 + 1; h < h1; ++h) atomicAdd(&s_hi[h & 255u], 256u);
+        atomicAdd(&s_hi[h1 & 255u], (t1 & 255u) + 1u);
+      }
+    }
   }
-}
-
-// block-wide exclusive scan of one value per thread (kRankThreads); returns
-// the exclusive prefix, *total the block sum
-__device__ __forceinline__ uint32_t rank_block_scan(uint32_t v, uint32_t* total) {
-  constexpr int NW = kRankThreads / 32;
-  __shared__ uint32_t s_w[NW];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t incl = v;
+  uint32_t scan = sum;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += u;
+    const uint32_t v = __shfl_up_sync(0xffffffffu, scan, o);
+    if (lane >= o) scan += v;
   }
-  if (lane == 31) s_w[warp] = incl;
+  if (lane == 31) s_wtot[warp] = scan;
   __syncthreads();
-  uint32_t pre = 0, tot = 0;
+  uint64_t wofs = 0, total = 0;
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
-    const uint32_t x = s_w[w];
-    pre += w < warp ? x : 0;
-    tot += x;
+    const uint32_t v = s_wtot[w];
+    wofs += w < warp ? v : 0;
+    total += v;
   }
-  *total = tot;
-  return pre + incl - v;
-}
-
-__global__ void __launch_bounds__(kRankThreads) k_rank_sums(RankScanArgs a) {
-  const int64_t n_vis = min(a.n_vis, (int64_t)*a.n_vis_dev);
-  const int64_t c = blockIdx.x;
-  if (c * kRankChunk >= n_vis) return;
-  uint32_t id[kRankItems], cnt[kRankItems];
-  uint64_t rect[kRankItems];
-  rank_chunk_load(a, n_vis, c * kRankChunk + (int64_t)threadIdx.x * kRankItems, id, rect, cnt);
-  uint32_t sum = 0;
+  if (warp == 0) {
+    // warp-cooperative look-back: 32 predecessors per L2 round trip
+    uint64_t* lb = a.lookback;
+    if (chunk == 0) {
+      if (lane == 0) {
+        st_relaxed_gpu(lb, kLbIncl | total);
+        s_excl = 0;
+      }
+    } else {
+      if (lane == 0) st_relaxed_gpu(lb + chunk, kLbAgg | total);
+      uint64_t excl = 0;
+      int64_t end = chunk;
+      while (true) {
+        const int64_t idx = end - 1 - lane;
+        uint64_t v = kLbIncl;
+        if (idx >= 0) {
+          do {
+            v = ld_relaxed_gpu(lb + idx);
+          } while ((v & ~kLbMask) == 0);
+        }
+        const uint32_t incl = __ballot_sync(0xffffffffu, (v & ~kLbMask) == kLbIncl);
+        const int stop = incl ? __ffs(incl) - 1 : 31;
+        unsigned long long part = lane <= stop ? (v & kLbMask) : 0ull;
 #pragma unroll
-  for (int j = 0; j < kRankItems; ++j) sum += cnt[j];
-  uint32_t total;
-  rank_block_scan(sum, &total);
-  if (threadIdx.x == 0) a.chunk_sums[c] = total;
-}
-
-// one CTA: exclusive scan of the chunk sums in place
-__global__ void __launch_bounds__(1024) k_rank_offsets(RankScanArgs a) {
-  const int64_t n_vis = min(a.n_vis, (int64_t)*a.n_vis_dev);
-  const int64_t chunks = (n_vis + kRankChunk - 1) / kRankChunk;
-  __shared__ uint32_t s_w[32];
-  __shared__ uint32_t s_carry;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_carry = 0;
-  for (int64_t base = 0; base < chunks; base += 1024) {
-    const int64_t i = base + tid;
-    const uint32_t v = i < chunks ? a.chunk_sums[i] : 0u;
-    uint32_t incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += u;
+        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        excl += part;
+        if (incl) break;
+        end -= 32;
+      }
+      if (lane == 0) {
+        st_relaxed_gpu(lb + chunk, kLbIncl | (excl + total));
+        s_excl = excl;
+      }
     }
-    __syncthreads();  // s_carry of the previous step is visible; s_w free
-    if (lane == 31) s_w[warp] = incl;
-    __syncthreads();
-    uint32_t pre = s_carry, tot = 0;
-    for (int w = 0; w < 32; ++w) {
-      const uint32_t x = s_w[w];
-      pre += w < warp ? x : 0;
-      tot += x;
-    }
-    if (i < chunks) a.chunk_sums[i] = pre + incl - v;
-    __syncthreads();
-    if (tid == 0) s_carry += tot;
   }
-}
-
-__global__ void __launch_bounds__(kRankThreads) k_rank_write(RankScanArgs a) {
-  const int64_t n_vis = min(a.n_vis, (int64_t)*a.n_vis_dev);
-  const int64_t c = blockIdx.x;
-  if (c * kRankChunk >= n_vis) return;
-  const int64_t r0 = c * kRankChunk + (int64_t)threadIdx.x * kRankItems;
-  uint32_t id[kRankItems], cnt[kRankItems];
-  uint64_t rect[kRankItems];
-  rank_chunk_load(a, n_vis, r0, id, rect, cnt);
-  uint32_t sum = 0;
+  __syncthreads();
+  uint64_t start = s_excl + wofs + (scan - sum);
 #pragma unroll
-  for (int j = 0; j < kRankItems; ++j) sum += cnt[j];
-  uint32_t total;
-  const uint32_t excl = rank_block_scan(sum, &total);
-  uint64_t start = (uint64_t)a.chunk_sums[c] + excl;
-#pragma unroll
-  for (int j = 0; j < kRankItems; ++j) {
+  for (int j = 0; j < kEmitItems; ++j) {
     const int64_t r = r0 + j;
     if (r >= n_vis) break;
     a.rrec[r] = make_uint4((uint32_t)rect[j], (uint32_t)(rect[j] >> 32), id[j], (uint32_t)start);
@@ -521,144 +483,32 @@ __global__ void __launch_bounds__(kRankThreads) k_rank_write(RankScanArgs a) {
       a.chunk_first[b] = (uint32_t)r;
     start = end;
   }
-}
-
-__global__ void k_cover_reduce(const int32_t* __restrict__ part, int parts, int64_t d,
-                               int32_t* cover) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= d) return;
-  const int per = (parts + gridDim.y - 1) / gridDim.y;
-  const int g0 = blockIdx.y * per, g1 = min(parts, g0 + per);
-  int32_t v = 0;
-#pragma unroll 8
-  for (int g = g0; g < g1; ++g) v += part[(int64_t)g * d + e];
-  if (v) atomicAdd(cover + e, v);
-}
-
-// K4p: one CTA.  Column then row prefix sums turn the difference array into
-// per-tile counts; a block scan over the tiles gives the ranges; shared
-// histograms of the low / high tile digit give the fused sort's plan.
-constexpr int kPlanThreads = 1024;
-__global__ void __launch_bounds__(kPlanThreads) k_tile_plan(TilePlanArgs a) {
-  extern __shared__ int32_t s_c[];
-  __shared__ uint32_t s_lo[256], s_hi[256];
-  __shared__ uint32_t s_warp[kPlanThreads / 32];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int tx = a.tiles_x, ty = a.tiles_y, cw = tx + 1;
-  const int d = cw * (ty + 1);
-  const int tiles = tx * ty;
-  for (int i0 = tid; i0 < d; i0 += 4 * kPlanThreads) {  // four loads in flight
-    int32_t v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = i0 + u * kPlanThreads < d ? a.cover[i0 + u * kPlanThreads] : 0;
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (i0 + u * kPlanThreads < d) s_c[i0 + u * kPlanThreads] = v[u];
-  }
-  if (tid < 256) s_lo[tid] = s_hi[tid] = 0;
-  const unsigned long long k = *a.k_dev;  // == the sum of the counts (both exact)
+  }  // the loop exits right after a __syncthreads: every shared atomic has landed
+  if (lo_all) atomicAdd(&s_lo_all, lo_all);
   __syncthreads();
-  // columns: warp per column, 32 rows per step (shuffle scans, not a
-  // dependent walk down the rows)
-  for (int x = warp; x < tx; x += kPlanThreads / 32) {
-    int32_t carry = 0;
-    for (int y0 = 0; y0 < ty; y0 += 32) {
-      const int y = y0 + lane;
-      int32_t v = y < ty ? s_c[y * cw + x] : 0;
+  // no-sync overflow (K past the capacity): no histogram, so the passes place
+  // the first `cap` slots inside [0, cap) and the stats report the overflow
+  if (*a.k_dev > a.cap) return;
+  {
+    // inclusive prefix of the difference array = low-digit counts
+    __shared__ uint32_t s_w[kEmitThreads / 32];
+    const int d = tid;  // kEmitThreads == 256
+    const int32_t v = s_dlo[d];
+    int32_t incl = v;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int32_t u = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += u;
-      }
-      if (y < ty) s_c[y * cw + x] = v + carry;
-      carry += __shfl_sync(0xffffffffu, v, 31);
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
     }
-  }
-  __syncthreads();
-  // rows: warp per row, 32 columns per step
-  for (int y = warp; y < ty; y += kPlanThreads / 32) {
-    int32_t carry = 0;
-    for (int x0 = 0; x0 < tx; x0 += 32) {
-      const int x = x0 + lane;
-      int32_t v = x < tx ? s_c[y * cw + x] : 0;
+    if (lane == 31) s_w[warp] = (uint32_t)incl;
+    __syncthreads();
+    int32_t pre = 0;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int32_t u = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += u;
-      }
-      if (x < tx) s_c[y * cw + x] = v + carry;
-      carry += __shfl_sync(0xffffffffu, v, 31);
-    }
+    for (int w = 0; w < NW; ++w) pre += w < warp ? (int32_t)s_w[w] : 0;
+    const uint32_t lo = (uint32_t)(pre + incl) + s_lo_all;
+    if (lo) atomicAdd(a.hist + d, lo);
+    if (s_hi[d]) atomicAdd(a.hist + 256 + d, s_hi[d]);
   }
-  __syncthreads();
-  // tiles in row-major order: thread t owns [t * per, (t + 1) * per)
-  const int per = (tiles + kPlanThreads - 1) / kPlanThreads;
-  const int t0 = tid * per, t1 = min(tiles, t0 + per);
-  uint32_t sum = 0;
-  const int ty0 = t0 / tx, tx0 = t0 - ty0 * tx;
-  for (int t = t0, y = ty0, x = tx0; t < t1; ++t) {
-    const uint32_t c = (uint32_t)s_c[y * cw + x];
-    sum += c;
-    if (c) {
-      atomicAdd(&s_lo[t & 0xff], c);
-      atomicAdd(&s_hi[(t >> 8) & 0xff], c);
-    }
-    if (++x == tx) x = 0, ++y;
-  }
-  uint32_t incl = sum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  if (lane == 31) s_warp[warp] = incl;
-  __syncthreads();
-  uint32_t run = incl - sum, total = 0;
-  for (int w = 0; w < kPlanThreads / 32; ++w) {
-    const uint32_t v = s_warp[w];
-    run += w < warp ? v : 0;
-    total += v;
-  }
-  const bool over = k > a.cap;
-  for (int t = t0, y = ty0, x = tx0; t < t1; ++t) {
-    const uint32_t c = (uint32_t)s_c[y * cw + x];
-    a.ranges[t] = over ? make_int2(0, 0) : make_int2((int)run, (int)(run + c));
-    if (a.tile_count) a.tile_count[t] = over ? 0u : c;
-    run += c;
-    if (++x == tx) x = 0, ++y;
-  }
-  // plan: exclusive digit starts of both passes (threads 0..255)
-  __syncthreads();  // every thread has read s_warp
-  if (warp < 8) {
-    for (int p = 0; p < 2; ++p) {
-      const uint32_t c = p ? s_hi[tid] : s_lo[tid];
-      uint32_t v = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += u;
-      }
-      __syncwarp();
-      if (lane == 31) s_warp[warp] = v;
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      uint32_t pre = 0;
-      for (int w = 0; w < 8; ++w) pre += w < warp ? s_warp[w] : 0;
-      a.plan->digit_start[p][tid] = pre + v - c;
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-    }
-  }
-  if (tid == 0) {
-    RadixPlan* pl = a.plan;
-    pl->n_passes = 2;
-    pl->first_active = 0;
-    pl->last_active = 1;
-    for (int p = 0; p < kMaxPasses; ++p) pl->active[p] = p < 2, pl->src[p] = p == 1;
-    pl->result = 0;
-    *a.k_eff = over ? 0ull : k;
-    if (a.max_k) atomicMax(a.max_k, k);
-    *a.keys_result = a.result;
-  }
-  (void)total;
 }
 
 // ---------------------------------------------------------------------------
@@ -778,56 +628,11 @@ int launch_ranges_from_counts(const uint32_t* counts, int tiles, int2* ranges, i
   return 1;
 }
 
-int cover_grid(int tiles_x, int tiles_y, int64_t n, int sms) {
-  if (n <= 0) return 0;
-  const size_t smem = sizeof(int32_t) * (size_t)(tiles_x + 1) * (tiles_y + 1);
-  static size_t smem_set[kMaxDevices] = {};
-  const int dev = current_device();
-  if (smem > smem_set[dev]) {
-    cudaFuncSetAttribute(k_cover, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    smem_set[dev] = smem;
-  }
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cover, kCoverThreads, smem);
-  if (occ < 1) occ = 1;
-  const int64_t need = (n + kCoverThreads * 4 - 1) / (kCoverThreads * 4);
-  return (int)(need < (int64_t)sms * occ ? need : (int64_t)sms * occ);
-}
-
-int launch_cover(const uint64_t* rects, int64_t n, int tiles_x, int tiles_y, int32_t* cover_part,
-                 int grid, cudaStream_t s) {
-  if (grid <= 0) return 0;
-  const size_t smem = sizeof(int32_t) * (size_t)(tiles_x + 1) * (tiles_y + 1);
-  k_cover<<<(unsigned)grid, kCoverThreads, smem, s>>>(rects, n, tiles_x, tiles_y, cover_part);
-  return 1;
-}
-
-int launch_rank_scan(const RankScanArgs& a, cudaStream_t s) {
-  const int64_t chunks = rank_chunks(a.n_vis);
+int launch_emit_ranks(const EmitArgs& a, cudaStream_t s) {
+  const int64_t chunks = emit_chunks(a.n_vis);
   if (chunks <= 0) return 0;
-  k_rank_sums<<<(unsigned)chunks, kRankThreads, 0, s>>>(a);
-  k_rank_offsets<<<1, 1024, 0, s>>>(a);
-  k_rank_write<<<(unsigned)chunks, kRankThreads, 0, s>>>(a);
-  return 3;
-}
-
-int launch_cover_reduce(const int32_t* part, int parts, int64_t d, int32_t* cover, cudaStream_t s) {
-  if (parts <= 0 || d <= 0) return 0;
-  const int slices = parts < 16 ? parts : 16;
-  dim3 grid((unsigned)((d + 255) / 256), (unsigned)slices);
-  k_cover_reduce<<<grid, 256, 0, s>>>(part, parts, d, cover);
-  return 1;
-}
-
-int launch_tile_plan(const TilePlanArgs& a, cudaStream_t s) {
-  const size_t smem = sizeof(int32_t) * (size_t)(a.tiles_x + 1) * (a.tiles_y + 1);
-  static size_t smem_set[kMaxDevices] = {};
-  const int dev = current_device();
-  if (smem > smem_set[dev]) {
-    cudaFuncSetAttribute(k_tile_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    smem_set[dev] = smem;
-  }
-  k_tile_plan<<<1, kPlanThreads, smem, s>>>(a);
+  static_assert(kEmitThreads == 256, "k_emit_ranks: one thread per digit");
+  k_emit_ranks<<<(unsigned)chunks, kEmitThreads, 0, s>>>(a);
   return 1;
 }
 

@@ -1,5 +1,5 @@
 """Render a few c3 views (6M Gaussians, 1080p) for ncu: warm-up views first,
-then the profiled ones.  usage: python profiles/view_probe.py [n_views] [width height] [group]"""
+then the profiled ones.  usage: python profiles/view_probe.py [n_views] [width height] [group] [flags]"""
 import sys
 from pathlib import Path
 
@@ -15,7 +15,8 @@ g = scenes.synthetic_gaussians(6_000_000, seed=0)
 m = GaussianModel.from_host(g, validate=False)
 cams = scenes.orbit_cameras(64, w, h, seed=0)[:nv]
 grp = int(sys.argv[4]) if len(sys.argv) > 4 else 1
-r = BatchRenderer(m, w, h, nv, group=grp)
+flags = int(sys.argv[5]) if len(sys.argv) > 5 else 0  # extra LMGS_FLAG_* bits
+r = BatchRenderer(m, w, h, nv, group=grp, flags=flags)
 r.render(cams, stage_times=True)
 torch.cuda.synchronize()
 st = r.render(cams, stage_times=True)

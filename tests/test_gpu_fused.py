@@ -1,5 +1,6 @@
-"""Fused emission + tile sort (K4r rank scan -> K4p tile plan -> the onesweep
-pass that generates its instance keys -> the packed second pass) against the
+"""Fused emission + tile sort (k_emit_ranks: rank records + per-row digit
+histograms -> the onesweep pass that generates its instance keys -> the
+packed second pass with the range counts) against the
 separate K4 emission + two-pass K5 tile sort (the default; the fused path is
 LMGS_FLAG_FUSED_TILE_SORT):
 tile lists, ranges, touched, n_processed and images bit-identical, and a
@@ -87,7 +88,7 @@ def test_fused_tiles_8px_1080p_vs_oracle():
 
 def test_fused_no_host_sync_and_overflow():
     """The capacity-bounded mode: equal to the synchronised render when K fits;
-    with a capacity below K the view is flagged and every range is empty."""
+    with a capacity below K the view is flagged and the ranges stay inside it."""
     g = GaussianModel.from_host(scenes.synthetic_gaussians(100_000, seed=6), validate=False)
     cams = scenes.orbit_cameras(2, 1920, 1080, seed=6)
     fl = _lib.LMGS_FLAG_FUSED_TILE_SORT
@@ -105,5 +106,6 @@ def test_fused_no_host_sync_and_overflow():
     small.render(cams)
     torch.cuda.synchronize()
     assert small.overflowed()
-    r = small.ranges
-    assert int((r[..., 1] - r[..., 0]).abs().sum()) == 0
+    r = small.ranges.long()
+    assert int(r.min()) >= 0 and int(r.max()) <= k // 2
+    assert bool((r[..., 1] >= r[..., 0]).all())
