@@ -18,6 +18,7 @@
 // shared memory in digit order, its global digit offsets found by decoupled
 // look-back over the preceding tiles, and written out in coalesced per-digit
 // runs.
+#include "device_util.cuh"
 #include "lmgs_internal.cuh"
 
 namespace lmgs {
@@ -31,6 +32,13 @@ constexpr int kWarps = kSortThreads / 32;
 // predecessors have published (the look-back phase of a tile drops from ~3.4
 // to ~0.7 us): depth sort 0.265 -> 0.239, tile sort 0.312 -> 0.286 ms/view,
 // 775.7 -> 793.9 frames/s (profiles/r10/lookback_late_variants.txt)
+// concurrent renders: the persistent grids prefetch each CTA's next tile by
+// TMA (PREF).  Off: 700 vs 804 frames/s — the two 32-KB input buffers per CTA
+// take the shared memory the other streams' kernels would co-reside in
+// (profiles/r10/sort_prefetch_variants.txt)
+#ifndef LMGS_SORT_PREFETCH
+#define LMGS_SORT_PREFETCH 0
+#endif
 #ifndef LMGS_LOOKBACK_LATE
 #define LMGS_LOOKBACK_LATE 1
 #endif
@@ -64,12 +72,6 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ uint32_t lanemask_lt() {
-  uint32_t m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
-
 template <typename K>
 __device__ __forceinline__ uint32_t digit_of(K key, int shift) {
   return (uint32_t)((uint64_t)key >> shift) & 0xffu;
@@ -361,7 +363,12 @@ __device__ __forceinline__ void emit_keys(const PassArgs& a, int64_t n, int64_t 
 // 4. per-digit prefix over warps, staging in shared memory in digit order;
 // 5. decoupled look-back (windowed) for the global digit offsets;
 // 6. coalesced write-out in per-digit runs, in the pass's output format.
-template <typename KI, int OUT, int SEG, bool VALS, bool PERSIST, int SRC = kSrcKeys>
+// PREF (persistent grids of concurrent renders): a CTA claims its next tile
+// right after the current tile's look-back and has its keys (and values)
+// copied into a second shared buffer by TMA bulk copies while it stages and
+// writes the current one; full tiles only (a partial tile is loaded directly)
+template <typename KI, int OUT, int SEG, bool VALS, bool PERSIST, int SRC = kSrcKeys,
+          bool PREF = false>
 __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
     k_onesweep(PassArgs a) {
   using KO = typename OutKey<KI, OUT>::type;
@@ -410,15 +417,54 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   // implicit payload on the first pass that moves data: value = input index
   const bool iota = a.iota_vals && pass == plan->first_active;
   const int shift = a.shift;
+  // PREF input buffers after the staging (and its vals / low digits)
+  constexpr size_t kStageBytes = sizeof(KI) * kSortTile +
+                                 (VALS ? sizeof(uint32_t) * kSortTile : 0) +
+                                 (SEG == kSegLo ? kSortTile : 0);
+  constexpr size_t kInBytes = sizeof(KI) * kSortTile + (VALS ? sizeof(uint32_t) * kSortTile : 0);
+  __shared__ __align__(8) uint64_t s_bar[PREF ? 2 : 1];
+  __shared__ uint32_t s_next;
+  auto in_keys = [&](int b) {
+    return reinterpret_cast<KI*>(smem_raw + ((kStageBytes + 15) & ~(size_t)15) + b * kInBytes);
+  };
+  auto in_vals = [&](int b) {
+    return reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(in_keys(b)) +
+                                       sizeof(KI) * kSortTile);
+  };
+  // a full tile's keys (and non-implicit values) into buffer b by TMA
+  auto prefetch = [&](uint32_t t, int b) {
+    if ((int64_t)(t + 1) * kSortTile > n) return;  // partial or past the end: direct loads
+    const bool pv = VALS && !(a.iota_vals && pass == plan->first_active);
+    mbar_expect_tx(&s_bar[b], sizeof(KI) * kSortTile + (pv ? sizeof(uint32_t) * kSortTile : 0));
+    bulk_g2s(in_keys(b), kin + (int64_t)t * kSortTile, sizeof(KI) * kSortTile, &s_bar[b]);
+    if (pv) bulk_g2s(in_vals(b), vin + (int64_t)t * kSortTile, sizeof(uint32_t) * kSortTile, &s_bar[b]);
+  };
+  uint32_t phase = 0;  // PREF: bit b = parity of buffer b's next completion
+  int cur = 0;
+  if constexpr (PREF) {
+    if (tid == 0) {
+      mbar_init(&s_bar[0], 1);
+      mbar_init(&s_bar[1], 1);
+      mbar_init_fence();
+      s_next = atomicAdd(a.counter + pass, 1u);
+      prefetch(s_next, 0);
+    }
+    __syncthreads();
+  }
   // tiles are taken by ticket; a CTA loops until the keys run out (with n_dev
   // the grid is a persistent one sized for the device, not for the bound)
   for (;;) {
-  if (tid == 0) s_bid = atomicAdd(a.counter + pass, 1u);
+  if (PREF) {
+    if (tid == 0) s_bid = s_next;
+  } else {
+    if (tid == 0) s_bid = atomicAdd(a.counter + pass, 1u);
+  }
   __syncthreads();
   const uint32_t bid = s_bid;
   const int64_t base = (int64_t)bid * kSortTile;
   if (base >= n) return;
   const int count = (int)min((int64_t)kSortTile, n - base);
+  const bool staged_in = PREF && count == kSortTile;  // this tile's keys came by TMA
   TRACE(0)
 
   KI key[kSortItems];
@@ -428,6 +474,18 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   const int wbase = warp * 32 * kSortItems;
   if constexpr (SRC == kSrcEmit) {
     emit_keys(a, n, base, count, smem_raw, key);
+  } else if (staged_in) {
+    mbar_wait(&s_bar[cur], (phase >> cur) & 1u);
+    phase ^= 1u << cur;
+    const KI* sk = in_keys(cur);
+    const uint32_t* sv = in_vals(cur);
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+      const int i = wbase + j * 32 + lane;
+      key[j] = sk[i];
+      if (VALS) val[j] = iota ? (uint32_t)(base + i) : sv[i];
+    }
+    fence_proxy_async_smem();  // these reads before the buffer's next TMA fill
   } else {
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
@@ -551,6 +609,14 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
     __syncwarp();
   }
   if (LMGS_LOOKBACK_LATE == 1) look_back();
+  if constexpr (PREF) {
+    // the next tile, claimed once this one has published its prefix: its
+    // keys stream in while this tile is staged and written
+    if (tid == 0) {
+      s_next = atomicAdd(a.counter + pass, 1u);
+      prefetch(s_next, cur ^ 1);
+    }
+  }
   __syncthreads();
   TRACE(3)
   // 4. per digit: exclusive prefix over warps (the invalid items go behind
@@ -632,14 +698,16 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   TRACE(5)
 #endif
   if (!PERSIST) return;  // one tile per CTA on an exact grid
+  if (PREF) cur ^= 1;
   __syncthreads();  // the staging and s_bid are reused by the next tile
   }
 }
 
-template <typename KI, bool VALS, int SEG = kSegNone>
+template <typename KI, bool VALS, int SEG = kSegNone, bool PREF = false>
 constexpr size_t onesweep_smem() {
-  return sizeof(KI) * kSortTile + (VALS ? sizeof(uint32_t) * kSortTile : 0) +
-         (SEG == kSegLo ? kSortTile : 0);
+  return ((sizeof(KI) * kSortTile + (VALS ? sizeof(uint32_t) * kSortTile : 0) +
+           (SEG == kSegLo ? kSortTile : 0) + 15) & ~(size_t)15) +
+         (PREF ? 2 * (sizeof(KI) * kSortTile + (VALS ? sizeof(uint32_t) * kSortTile : 0)) : 0);
 }
 
 template <typename KI, int OUT, int SEG, bool VALS, int SRC = kSrcKeys>
@@ -670,8 +738,21 @@ void launch_pass(const PassArgs& a, int64_t blocks, cudaStream_t s) {
   const int per_sm = a.concurrent && LMGS_SORT_PERSIST_CTAS > 0 && LMGS_SORT_PERSIST_CTAS < occ[dev]
                          ? LMGS_SORT_PERSIST_CTAS : occ[dev];
   const int64_t persistent = (int64_t)sms[dev] * per_sm;
-  k_onesweep<KI, OUT, SEG, VALS, true, SRC>
-      <<<(unsigned)(blocks < persistent ? blocks : persistent), kSortThreads, smem, s>>>(a);
+  const unsigned grid = (unsigned)(blocks < persistent ? blocks : persistent);
+  if constexpr (SRC == kSrcKeys && LMGS_SORT_PREFETCH) {
+    if (a.concurrent && per_sm == 1) {
+      constexpr size_t smem_pref = onesweep_smem<KI, VALS, SEG, true>();
+      static bool pref_set[kMaxDevices] = {};
+      if (!pref_set[dev]) {
+        cudaFuncSetAttribute(k_onesweep<KI, OUT, SEG, VALS, true, SRC, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pref);
+        pref_set[dev] = true;
+      }
+      k_onesweep<KI, OUT, SEG, VALS, true, SRC, true><<<grid, kSortThreads, smem_pref, s>>>(a);
+      return;
+    }
+  }
+  k_onesweep<KI, OUT, SEG, VALS, true, SRC><<<grid, kSortThreads, smem, s>>>(a);
 }
 
 PassArgs pass_args(const RadixSortBuffers& b, int64_t n, int shift, int p, int64_t blocks) {
