@@ -355,6 +355,9 @@ constexpr int kWarpsPerBlock16 = 8;
 #ifndef LMGS_BLEND_ID_AHEAD
 #define LMGS_BLEND_ID_AHEAD 1
 #endif
+#ifndef LMGS_BLEND_COMPACT
+#define LMGS_BLEND_COMPACT 0  // 1: 264 -> 295 M warp instructions, 807 -> 799 frames/s (profiles/r10/blend_compact_variants.txt)
+#endif
 #ifndef LMGS_BLEND_PAIRS
 #define LMGS_BLEND_PAIRS 0  // 1: two hits per trip, one break vote per pair (777.6 vs 777.3 frames/s: neutral, profiles/r10)
 #endif
@@ -368,7 +371,7 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
   __shared__ float4 s_rec[kWarpsPerBlock16][32][3];
   __shared__ double s_mx[kWarpsPerBlock16][32], s_my[kWarpsPerBlock16][32],
       s_r2[kWarpsPerBlock16][32];
-  __shared__ uint32_t s_id[kWarpsPerBlock16][32];
+  __shared__ uint8_t s_lane[kWarpsPerBlock16][32];  // LMGS_BLEND_COMPACT: slot -> list lane
   constexpr int kItemsPerTile = 8 / NP;
   constexpr int kRows = 4 * NP;  // block height
 
@@ -491,34 +494,40 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
         g0 = __ldg(rec4 + 4 * (size_t)id);
         g1 = __ldg(rec4 + 4 * (size_t)id + 1);
       }
-      bool hit = false;
-      if (have) {
-        const double mx = __hiloint2double(__float_as_int(c0.y), __float_as_int(c0.x));
-        const double my = __hiloint2double(__float_as_int(c0.w), __float_as_int(c0.z));
-        const double r2 = __hiloint2double(__float_as_int(c1.y), __float_as_int(c1.x));
-        const double mxl = mx - (double)x0, myl = my - (double)y0;
-        const float fx = (float)mxl, fy = (float)myl;
-        // exact circle-vs-box cull (the reference's support is the circle
-        // d.d <= r^2 around the mean) with a conservative radius margin
-        const float r = sqrtf((float)r2) * 1.0001f + 1e-3f;
-        const float ex = fx - fminf(fmaxf(fx, bx0), bx1);
-        const float ey = fy - fminf(fmaxf(fy, by0), by1);
-        hit = fmaf(ex, ex, ey * ey) <= r * r;
-        if (hit) {
-          const float4 g2 = __ldg(rec4 + 4 * (size_t)cid + 2);  // qc, log2a, r, g
-          const float4 g3 = __ldg(rec4 + 4 * (size_t)cid + 3);  // b, z
-          const double ax = fabs(mxl) + 16.0, ay = fabs(myl) + 16.0;
-          const double band =  // explicit rounding (touched_fix.cu)
-              __dmul_rn(__dadd_rn(__dadd_rn(r2, __dmul_rn(ax, ax)), __dmul_rn(ay, ay)), 0x1p-18);
-          s_rec[warp][lane][0] = make_float4(fx, fy, c1.z, c1.w);
-          s_rec[warp][lane][1] = make_float4(g2.x, g2.y, __double2float_rd(r2 - band),
-                                             __double2float_ru(r2 + band));
-          s_rec[warp][lane][2] = make_float4(g2.z, g2.w, g3.x, g3.y);
-          s_mx[warp][lane] = mx;
-          s_my[warp][lane] = my;
-          s_r2[warp][lane] = r2;
-          s_id[warp][lane] = cid;
-        }
+      // (computed on every lane; a lane past the list end has no hit)
+      const double mx = __hiloint2double(__float_as_int(c0.y), __float_as_int(c0.x));
+      const double my = __hiloint2double(__float_as_int(c0.w), __float_as_int(c0.z));
+      const double r2 = __hiloint2double(__float_as_int(c1.y), __float_as_int(c1.x));
+      const double mxl = mx - (double)x0, myl = my - (double)y0;
+      const float fx = (float)mxl, fy = (float)myl;
+      // exact circle-vs-box cull (the reference's support is the circle
+      // d.d <= r^2 around the mean) with a conservative radius margin
+      const float r = sqrtf((float)r2) * 1.0001f + 1e-3f;
+      const float ex = fx - fminf(fmaxf(fx, bx0), bx1);
+      const float ey = fy - fminf(fmaxf(fy, by0), by1);
+      const bool hit = have && fmaf(ex, ex, ey * ey) <= r * r;
+#if LMGS_BLEND_COMPACT
+      // hits staged in list order at consecutive slots: the hit loop walks
+      // slots 0.. with a counter (no find-first-set per hit)
+      const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+      const int slot = __popc(hm & lanemask_lt());
+      if (hit) s_lane[warp][slot] = (uint8_t)lane;
+#else
+      const int slot = lane;
+#endif
+      if (hit) {
+        const float4 g2 = __ldg(rec4 + 4 * (size_t)cid + 2);  // qc, log2a, r, g
+        const float4 g3 = __ldg(rec4 + 4 * (size_t)cid + 3);  // b, z
+        const double ax = fabs(mxl) + 16.0, ay = fabs(myl) + 16.0;
+        const double band =  // explicit rounding (touched_fix.cu)
+            __dmul_rn(__dadd_rn(__dadd_rn(r2, __dmul_rn(ax, ax)), __dmul_rn(ay, ay)), 0x1p-18);
+        s_rec[warp][slot][0] = make_float4(fx, fy, c1.z, c1.w);
+        s_rec[warp][slot][1] = make_float4(g2.x, g2.y, __double2float_rd(r2 - band),
+                                           __double2float_ru(r2 + band));
+        s_rec[warp][slot][2] = make_float4(g2.z, g2.w, g3.x, g3.y);
+        s_mx[warp][slot] = mx;
+        s_my[warp][slot] = my;
+        s_r2[warp][slot] = r2;
       }
       uint32_t m = __ballot_sync(0xffffffffu, hit);
       __syncwarp();
@@ -607,14 +616,25 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
         for (int q = 0; q < NP; ++q) active |= T[q] >= kTermEpsF;
         if (NP == 1) {  // the owner keeps its splat's ballot; counted after the batch
           const uint32_t bl = __ballot_sync(0xffffffffu, contrib1);
-          my_ballot = lane == k ? bl : my_ballot;
+          my_ballot = hit && slot == k ? bl : my_ballot;
         } else {
           const int wsum = __reduce_add_sync(0xffffffffu, contrib_bits);
-          if (lane == k) my_touch += wsum;
+          if (hit && slot == k) my_touch += wsum;
         }
         return active;
       };
-#if LMGS_BLEND_PAIRS
+#if LMGS_BLEND_COMPACT
+      const int nh = __popc(m);
+      for (int h = 0; h < nh; ++h) {
+        // pixels only go inactive on a splat they are inside: the warp's break
+        // index is the first splat after which none of its pixels is active
+        if (!__any_sync(0xffffffffu, blend_one(h))) {
+          last = b - range.x + s_lane[warp][h];
+          live = false;
+          break;
+        }
+      }
+#elif LMGS_BLEND_PAIRS
       // two hits per trip and one break vote per pair: a pixel that went
       // inactive takes nothing more (sigma 0, no w > 0), so blending the
       // second splat of a pair after the break changes nothing; when the pair
