@@ -38,7 +38,15 @@ constexpr float kSigmaMaxF = 0.9999f;
 // The band is BlendArgs.fix_band: 1e-4 by default (10x the measured fp32/fp64
 // T gap, < 1e-5 at the crossing), 1e-2 with LMGS_FLAG_WIDE_FIX_BAND (the
 // check that the default band misses no disagreement).
+//
+// The crossing splat's own fp32 error widens the band per pixel: sigma is
+// within ~1.5e-7 of the fp64 value (fp32 rounding + ex2.approx), so 1 - sigma
+// — the factor T took at that splat — is relatively off by up to 1.5e-7 /
+// (1 - sigma) = 1.5e-7 * Tc / T: negligible for translucent splats (c3: alpha
+// <= 0.88 -> < 2e-6), up to ~2e-3 for a near-opaque one (sigma -> 0.9999);
+// taken at 3e-7 * Tc / T (tests/test_gpu_parity.py::test_opaque_splats_*).
 __device__ __forceinline__ bool crossing_uncertain(float T, float Tc, float band) {
+  band += 3e-7f * __fdividef(Tc, fmaxf(T, 1e-30f));  // (2x margin covers the approximation)
   const float hi = kTermEpsF * (1.0f + band), lo = kTermEpsF * (1.0f - band);
   if (T < kTermEpsF) return Tc < hi || T >= lo;
   return T < hi;

@@ -303,3 +303,18 @@ def test_fix_band_misses_nothing(n, view):
     assert torch.equal(a.touched, b.touched)
     assert torch.equal(a.n_processed, b.n_processed)
     assert torch.equal(a.rgb, b.rgb)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+def test_opaque_splats_touched_exact(seed):
+    """Near-opaque splats (logits 3..12: alpha up to 0.99999, sigma clamped at
+    SIGMA_MAX): in fp32, 1 - sigma near 1e-4 carries a relative error up to
+    ~6e-4, far wider than the base K7b band — the blend must widen the band of
+    the pixels that took such a splat, or touched / n_processed drift."""
+    g = scenes.synthetic_gaussians(20_000, seed=seed)
+    rng = np.random.default_rng(100 + seed)
+    g.opacity_logits[:] = rng.uniform(3.0, 12.0, g.opacity_logits.shape).astype(np.float32)
+    cam = scenes.orbit_cameras(1, 320, 240, seed=seed)[0]
+    r = _full_frame_check(g, cam)
+    assert r["err"] <= IMG_TOL and r["aerr"] <= IMG_TOL
+    assert r["touched_mismatch"] == 0 and r["nproc_mismatch"] == 0
