@@ -318,3 +318,28 @@ def test_opaque_splats_touched_exact(seed):
     r = _full_frame_check(g, cam)
     assert r["err"] <= IMG_TOL and r["aerr"] <= IMG_TOL
     assert r["touched_mismatch"] == 0 and r["nproc_mismatch"] == 0
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("view", [0, 17])
+def test_fix_band_misses_nothing_opaque(view):
+    """The wide-band check on a near-opaque 1M-Gaussian scene (logits 3..12)
+    at 1080p: the default band, widened per pixel by the crossing splat's
+    fp32 error, replays every pixel whose touched / break index could differ."""
+    from paper_2503_21364_b200.raster import context
+
+    g = scenes.synthetic_gaussians(1_000_000, seed=7)
+    rng = np.random.default_rng(7)
+    g.opacity_logits[:] = rng.uniform(3.0, 12.0, g.opacity_logits.shape).astype(np.float32)
+    m = GaussianModel.from_host(g, validate=False)
+    cam = scenes.orbit_cameras(64, 1920, 1080, seed=0)[view]
+    ctx = context(0)
+    a = render(cam, m, 16, (0.0, 0.0, 0.0), 3, ctx=ctx)
+    qa = ctx.touched_fix_count()
+    b = render(cam, m, 16, (0.0, 0.0, 0.0), 3, ctx=ctx, wide_fix_band=True)
+    qb = ctx.touched_fix_count()
+    torch.cuda.synchronize()
+    assert qb > qa > 0
+    assert torch.equal(a.touched, b.touched)
+    assert torch.equal(a.n_processed, b.n_processed)
+    assert torch.equal(a.rgb, b.rgb)
