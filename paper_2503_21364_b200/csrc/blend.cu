@@ -45,7 +45,13 @@ constexpr float kSigmaMaxF = 0.9999f;
 // (1 - sigma) = 1.5e-7 * Tc / T: negligible for translucent splats (c3: alpha
 // <= 0.88 -> < 2e-6), up to ~2e-3 for a near-opaque one (sigma -> 0.9999);
 // taken at 3e-7 * Tc / T (tests/test_gpu_parity.py::test_opaque_splats_*).
+// (sigma <= SIGMA_MAX bounds Tc / T by ~1e4, so the widening stays below
+// 1e-2: pixels outside band + 1e-2 are rejected before the division)
 __device__ __forceinline__ bool crossing_uncertain(float T, float Tc, float band) {
+  {
+    const float hi = kTermEpsF * (1.01f + band), lo = kTermEpsF * (0.99f - band);
+    if (!(T < kTermEpsF ? (Tc < hi || T >= lo) : T < hi)) return false;
+  }
   band += 3e-7f * __fdividef(Tc, fmaxf(T, 1e-30f));  // (2x margin covers the approximation)
   const float hi = kTermEpsF * (1.0f + band), lo = kTermEpsF * (1.0f - band);
   if (T < kTermEpsF) return Tc < hi || T >= lo;
