@@ -5,8 +5,9 @@
 //       so equal keys stay in id order; runs of equal fp32 keys are then fixed
 //       up by the exact fp64 depth — _sort_order, gaussian_core.py:277-283);
 //   K5  the instance keys tile << 32 | id, sorted on the tile bits only
-//       (stable: the emitted array is already in depth-rank order).  The last
-//       pass writes the 32-bit ids alone, which is all the blend reads
+//       (stable: the emitted array is already in depth-rank order).  With two
+//       passes the first writes packed 4-byte keys (tile >> 8) << id_bits | id
+//       and the second the 32-bit ids alone, which is all the blend reads
 //       (tile_sort below).
 //
 // Per sort: one histogram kernel computes every digit's global histogram in a
@@ -14,7 +15,7 @@
 // scans them, marks digits all keys share as trivial (skipped on the device;
 // not for K5, whose passes change the key format) and routes the ping-pong
 // buffers; then one onesweep kernel per digit: a tile of kSortTile keys is
-// ranked in shared memory (warp match + per-warp counters, stable), staged in
+// ranked in shared memory ({count, match} words per warp, stable), staged in
 // shared memory in digit order, its global digit offsets found by decoupled
 // look-back over the preceding tiles, and written out in coalesced per-digit
 // runs.
@@ -360,9 +361,11 @@ __device__ __forceinline__ void emit_keys(const PassArgs& a, int64_t n, int64_t 
 //    lanes below), and the lowest of them stores {count + peers, 0} — no
 //    shuffle, no counter atomic (MATCH.ANY serialised; a separate match word +
 //    leader atomicAdd + shuffle cost ~39 SASS per key, this ~12);
-// 4. per-digit prefix over warps, staging in shared memory in digit order;
-// 5. decoupled look-back (windowed) for the global digit offsets;
-// 6. coalesced write-out in per-digit runs, in the pass's output format.
+// 4. decoupled look-back (windowed) for the global digit offsets — after the
+//    ranking (LMGS_LOOKBACK_LATE), when the predecessors have published;
+// 5. per-digit prefix over warps, staging in shared memory in digit order;
+// 6. coalesced write-out in per-digit runs, in the pass's output format (the
+//    last tile pass also counts the tile runs for the ranges).
 // PREF (persistent grids of concurrent renders): a CTA claims its next tile
 // right after the current tile's look-back and has its keys (and values)
 // copied into a second shared buffer by TMA bulk copies while it stages and
