@@ -208,6 +208,9 @@ def arm_config(args, world):
             "gaussians": N_GAUSS, "views_per_step": views, "views_per_gpu": my_views,
             "width": W, "height": H, "parallelism": f"camera-batch dp{world}",
             "views_per_k1_launch": args.group, "launch_mode": args.mode,
+            "streams": args.streams,
+            "sort_grids": "persistent, one CTA per SM (LMGS_FLAG_CONCURRENT)" if args.streams > 1
+            else "one CTA per tile",
             "l2": "no flush: scene 1.42 GB and per-view buffers > 126 MB L2",
             "geometry": "fp64 (bit-exact tile lists)", "blend": "fp32",
             "scene_replication": "rank 0 generates, NCCL broadcast" if world > 1
