@@ -71,7 +71,8 @@ def batch_config(name: str, n: int, w: int, h: int, views: int, steps: int) -> d
             "frames_per_s": views / (ms / 1e3), "ms_per_frame": ms / views,
             "stage_ms_per_frame": per, "instances_per_frame": st["per_frame"]["instances"],
             "processed_per_frame": st["per_frame"]["processed"],
-            "stage_gbs": {k: st["alg_bytes"][k] / (per[k] / 1e3) / 1e9 for k in per if per[k]},
+            "stage_gbs": {k: st["alg_bytes"][k] / (per[k] / 1e3) / 1e9 for k in per
+                          if per[k] and k in st["alg_bytes"]},
             "host_generate_s": gen_s}
 
 
