@@ -124,6 +124,9 @@ __device__ void fix_run(uint32_t* ids, int len, const uint64_t* __restrict__ key
 #define LMGS_FIXUP_PER 4
 #endif
 constexpr int kFixupPer = LMGS_FIXUP_PER;
+#ifndef LMGS_FIXUP_WARP
+#define LMGS_FIXUP_WARP 1  // run heads compacted per warp (k_depth_fixup_w)
+#endif
 __global__ void k_depth_fixup(void* const* keys_slot, void* const* ids_slot, int64_t n,
                               const uint64_t* __restrict__ key64,
                               const int64_t* __restrict__ pid) {
@@ -156,6 +159,71 @@ __global__ void k_depth_fixup(void* const* keys_slot, void* const* ids_slot, int
     }
     while (i + len < n && keys[i + len] == k[u]) ++len;
     fix_run(static_cast<uint32_t*>(*ids_slot) + i, (int)len, key64, pid);
+  }
+}
+
+// Warp-compacted variant: a warp finds the run heads among its 128 keys (4 per
+// lane, as above), compacts them in shared memory, and then resolves 32 heads
+// at a time with every lane busy — the per-thread loop above runs each of its
+// 4 head slots as a divergent path in nearly every warp (c3: ~20 % of the keys
+// head a run).
+__global__ void __launch_bounds__(256) k_depth_fixup_w(void* const* keys_slot, void* const* ids_slot,
+                                                       int64_t n, const uint64_t* __restrict__ key64,
+                                                       const int64_t* __restrict__ pid) {
+  static_assert(kFixupPer == 4, "128 keys per warp: 7-bit head offsets");
+  __shared__ uint8_t s_head[8][32 * kFixupPer];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t wbase = ((int64_t)blockIdx.x * 8 + warp) * 32 * kFixupPer;
+  if (wbase >= n) return;
+  const int64_t i0 = wbase + (int64_t)lane * kFixupPer;
+  const uint32_t* __restrict__ keys = static_cast<const uint32_t*>(*keys_slot);
+  uint32_t* __restrict__ ids = static_cast<uint32_t*>(*ids_slot);
+  uint32_t k[kFixupPer + 2];  // keys[i0 - 1 .. i0 + kFixupPer]
+#pragma unroll
+  for (int u = 0; u < kFixupPer + 2; ++u) {
+    const int64_t i = i0 - 1 + u;
+    k[u] = (i >= 0 && i < n) ? keys[i] : kDepthKeyNone + 1 + u;  // sentinels never equal
+  }
+  uint32_t heads = 0, twos = 0;  // bit u-1: key i0 + u - 1 heads a run (of length 2)
+#pragma unroll
+  for (int u = 1; u <= kFixupPer; ++u) {
+    const bool head = i0 - 1 + u < n && k[u] != kDepthKeyNone && k[u - 1] != k[u] &&
+                      k[u + 1] == k[u];
+    if (head) heads |= 1u << (u - 1);
+    if (head && u + 2 <= kFixupPer + 1 && k[u + 2] != k[u]) twos |= 1u << (u - 1);
+  }
+  const uint32_t cnt = __popc(heads);
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  uint32_t at = incl - cnt;
+#pragma unroll
+  for (int u = 0; u < kFixupPer; ++u)
+    if (heads >> u & 1u)
+      s_head[warp][at++] = (uint8_t)(lane * kFixupPer + u) | (uint8_t)((twos >> u & 1u) << 7);
+  __syncwarp();
+  for (uint32_t h = lane; h < total; h += 32) {
+    const uint8_t e = s_head[warp][h];
+    const int64_t i = wbase + (e & 0x7f);
+    uint32_t* run = ids + i;
+    if (e & 0x80) {  // a run of two: two independent gathers, maybe a swap
+      const uint32_t a0 = run[0], a1 = run[1];
+      const uint64_t d0 = key64[a0], d1 = key64[a1];
+      const int64_t p0 = pid ? pid[a0] : (int64_t)a0, p1 = pid ? pid[a1] : (int64_t)a1;
+      if (less64(d1, p1, d0, p0)) {
+        run[0] = a1;
+        run[1] = a0;
+      }
+    } else {
+      const uint32_t kv = keys[i];
+      int64_t len = 2;
+      while (i + len < n && keys[i + len] == kv) ++len;
+      fix_run(run, (int)len, key64, pid);
+    }
   }
 }
 
@@ -600,8 +668,12 @@ int launch_depth_fixup(void* const* keys_slot, void* const* ids_slot, int64_t n,
                        const uint64_t* key64, const int64_t* prim_ids, cudaStream_t s) {
   if (n <= 1) return 0;
   const int64_t threads = (n + kFixupPer - 1) / kFixupPer;
-  k_depth_fixup<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(keys_slot, ids_slot, n, key64,
-                                                                   prim_ids);
+  if (LMGS_FIXUP_WARP)
+    k_depth_fixup_w<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(keys_slot, ids_slot, n,
+                                                                       key64, prim_ids);
+  else
+    k_depth_fixup<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(keys_slot, ids_slot, n, key64,
+                                                                     prim_ids);
   return 1;
 }
 
