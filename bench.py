@@ -59,7 +59,7 @@ C5_PER_BLOCK = 6_250_000
 NCU_TRAFFIC_SOURCE = "profiles/r10/ncu_launch_table.txt"
 NCU_TRAFFIC = {
     "preprocess": 2783.8e6 / 2,  # one k_preprocess_tma<2> launch serves two views
-    "depth_sort": 48.1e6 + 3 * 41.4e6 + 105.2e6,  # keys, 3 passes (concurrent grids), fix-up
+    "depth_sort": 48.1e6 + 3 * 41.4e6 + 104.8e6,  # keys, 3 passes (concurrent grids), fix-up
     "emit": 257.5e6,
     "tile_sort": 222.8e6 + 123.4e6,  # u64 -> packed u32 pass, u32 -> ids pass
     "blend": 163.5e6,
