@@ -40,6 +40,9 @@ constexpr int kWarps = kSortThreads / 32;
 #ifndef LMGS_SORT_PREFETCH
 #define LMGS_SORT_PREFETCH 0
 #endif
+#ifndef LMGS_RANK_PAIRS
+#define LMGS_RANK_PAIRS 0  // 1: two items per round with {count, matchA, matchB} words: 692 vs 815 frames/s (profiles/r10/rank_pairs_variants.txt)
+#endif
 #ifndef LMGS_LOOKBACK_LATE
 #define LMGS_LOOKBACK_LATE 1
 #endif
@@ -403,7 +406,12 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   __shared__ uint32_t s_dstart[SEG == kSegLo ? kRadix : 1];
   // digit kRadix collects the invalid items of a partial tile, so neither the
   // counts nor the ranking need a validity predicate
-  __shared__ uint2 s_wm[kWarps][kRadix + 1];
+#if LMGS_RANK_PAIRS
+  using RankWord = uint4;  // {count, match of item j, match of item j + 1, -}
+#else
+  using RankWord = uint2;  // {count, match}
+#endif
+  __shared__ RankWord s_wm[kWarps][kRadix + 1];
   __shared__ uint32_t s_hist[kRadix + 1];
   __shared__ uint32_t s_local_start[kRadix];
   __shared__ uint32_t s_global[kRadix];
@@ -501,7 +509,7 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   uint32_t my_dstart = 0;  // kSegLo: start of bucket tid of the previous pass
   if constexpr (SEG == kSegLo) my_dstart = plan->digit_start[a.lo_pass][tid];
   for (int i = tid; i < kWarps * (kRadix + 1); i += kSortThreads)
-    (&s_wm[0][0])[i] = make_uint2(0u, 0u);
+    (&s_wm[0][0])[i] = RankWord{};
   s_hist[tid] = 0;  // kSortThreads == kRadix
   if (tid == 0) s_hist[kRadix] = 0;
 #pragma unroll
@@ -599,7 +607,28 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   TRACE(2)
 #endif
   const uint32_t lt = lanemask_lt();
-  uint2* my = s_wm[warp];
+  RankWord* my = s_wm[warp];
+#if LMGS_RANK_PAIRS
+  // two items per round, each with its own match half: item j + 1's rank
+  // counts every item j of its digit first; one store per digit (the lowest
+  // lane of item j holding it, else the lowest of item j + 1)
+  static_assert(kSortItems % 2 == 0, "");
+#pragma unroll
+  for (int j = 0; j < kSortItems; j += 2) {
+    const uint32_t da = dg[j], db = dg[j + 1];
+    atomicOr(&my[da].y, 1u << lane);
+    atomicOr(&my[db].z, 1u << lane);
+    __syncwarp();
+    const uint4 qa = my[da], qb = my[db];
+    __syncwarp();
+    const uint32_t below_a = qa.y & lt;
+    if (below_a == 0) my[da] = make_uint4(qa.x + __popc(qa.y) + __popc(qa.z), 0u, 0u, 0u);
+    if (qb.y == 0 && (qb.z & lt) == 0) my[db] = make_uint4(qb.x + __popc(qb.z), 0u, 0u, 0u);
+    dg[j] |= (qa.x + __popc(below_a)) << 16;
+    dg[j + 1] |= (qb.x + __popc(qb.y) + __popc(qb.z & lt)) << 16;
+    __syncwarp();
+  }
+#else
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     atomicOr(&my[dg[j]].y, 1u << lane);
@@ -611,6 +640,7 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
     dg[j] |= (cm.x + __popc(below)) << 16;
     __syncwarp();
   }
+#endif
   if (LMGS_LOOKBACK_LATE == 1) look_back();
   if constexpr (PREF) {
     // the next tile, claimed once this one has published its prefix: its
