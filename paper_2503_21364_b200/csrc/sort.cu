@@ -40,6 +40,9 @@ constexpr int kWarps = kSortThreads / 32;
 #ifndef LMGS_SORT_PREFETCH
 #define LMGS_SORT_PREFETCH 0
 #endif
+#ifndef LMGS_SORT_SMEM_PAD
+#define LMGS_SORT_SMEM_PAD 0  // extra dynamic shared bytes per onesweep CTA (co-residency experiments)
+#endif
 #ifndef LMGS_RANK_PAIRS
 #define LMGS_RANK_PAIRS 0  // 1: two items per round with {count, matchA, matchB} words: 692 vs 815 frames/s (profiles/r10/rank_pairs_variants.txt)
 #endif
@@ -400,6 +403,13 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   }
   extern __shared__ __align__(16) unsigned char smem_raw[];
   KI* s_keys = reinterpret_cast<KI*>(smem_raw);  // [kSortTile] staging
+  // kOutPacked stages the 4-byte output and the 1-byte digit only (5 B, not 8,
+  // per key: the sort CTAs' shared footprint sets how much the co-running
+  // streams' kernels keep, profiles/r10/sort_smem_pad_variants.txt)
+  constexpr bool kPackedStage = OUT == kOutPacked;
+  static_assert(!kPackedStage || (SEG == kSegNone && !VALS), "packed staging: keys only");
+  uint32_t* s_pk = reinterpret_cast<uint32_t*>(smem_raw);
+  uint8_t* s_dg8 = reinterpret_cast<uint8_t*>(smem_raw + sizeof(uint32_t) * kSortTile);
   uint32_t* s_vals = reinterpret_cast<uint32_t*>(smem_raw + sizeof(KI) * kSortTile);
   // kSegLo: the staged keys' low tile digits (the vals slot: kSegLo has none)
   uint8_t* s_lo = reinterpret_cast<uint8_t*>(smem_raw + sizeof(KI) * kSortTile);
@@ -429,7 +439,7 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   const bool iota = a.iota_vals && pass == plan->first_active;
   const int shift = a.shift;
   // PREF input buffers after the staging (and its vals / low digits)
-  constexpr size_t kStageBytes = sizeof(KI) * kSortTile +
+  constexpr size_t kStageBytes = (kPackedStage ? 5 * (size_t)kSortTile : sizeof(KI) * kSortTile) +
                                  (VALS ? sizeof(uint32_t) * kSortTile : 0) +
                                  (SEG == kSegLo ? kSortTile : 0);
   constexpr size_t kInBytes = sizeof(KI) * kSortTile + (VALS ? sizeof(uint32_t) * kSortTile : 0);
@@ -677,7 +687,12 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const uint32_t p = (dg[j] >> 16) + my[dg[j] & 0xffffu].x;
-    s_keys[p] = key[j];
+    if constexpr (kPackedStage) {
+      s_pk[p] = out_key<KI, OUT>(key[j], a);
+      s_dg8[p] = (uint8_t)dg[j];
+    } else {
+      s_keys[p] = key[j];
+    }
     if (VALS) s_vals[p] = val[j];
     if constexpr (SEG == kSegLo) {
       // the key's input position's bucket: the tile's first one plus the
@@ -701,6 +716,9 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
     if (c) atomicAdd(a.seg_counts + ((uint32_t)tid << 8 | (lo_info & 0xffffu)), c);
     segs = false;
   }
+  if constexpr (kPackedStage) {
+    for (int i = tid; i < count; i += kSortThreads) kout[s_global[s_dg8[i]] + i] = s_pk[i];
+  } else
   for (int i = tid; i < count; i += kSortThreads) {
     const KI k = s_keys[i];
     const uint32_t o = s_global[digit_of(k, shift)] + i;
@@ -736,16 +754,17 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   }
 }
 
-template <typename KI, bool VALS, int SEG = kSegNone, bool PREF = false>
+template <typename KI, bool VALS, int SEG = kSegNone, bool PREF = false, int OUT = kOutSame>
 constexpr size_t onesweep_smem() {
-  return ((sizeof(KI) * kSortTile + (VALS ? sizeof(uint32_t) * kSortTile : 0) +
-           (SEG == kSegLo ? kSortTile : 0) + 15) & ~(size_t)15) +
+  return (((OUT == kOutPacked ? 5 * (size_t)kSortTile : sizeof(KI) * kSortTile) +
+           (VALS ? sizeof(uint32_t) * kSortTile : 0) + (SEG == kSegLo ? kSortTile : 0) + 15) &
+          ~(size_t)15) +
          (PREF ? 2 * (sizeof(KI) * kSortTile + (VALS ? sizeof(uint32_t) * kSortTile : 0)) : 0);
 }
 
 template <typename KI, int OUT, int SEG, bool VALS, int SRC = kSrcKeys>
 void launch_pass(const PassArgs& a, int64_t blocks, cudaStream_t s) {
-  constexpr size_t smem = onesweep_smem<KI, VALS, SEG>();
+  constexpr size_t smem = onesweep_smem<KI, VALS, SEG, false, OUT>() + LMGS_SORT_SMEM_PAD;  // (pad: experiments)
   static_assert(SRC == kSrcKeys || smem >= 2 * kSortTile, "the owner map aliases the staging");
   static bool attr_set[kMaxDevices] = {};
   static int occ[kMaxDevices] = {}, sms[kMaxDevices] = {};
@@ -774,7 +793,7 @@ void launch_pass(const PassArgs& a, int64_t blocks, cudaStream_t s) {
   const unsigned grid = (unsigned)(blocks < persistent ? blocks : persistent);
   if constexpr (SRC == kSrcKeys && LMGS_SORT_PREFETCH) {
     if (a.concurrent && per_sm == 1) {
-      constexpr size_t smem_pref = onesweep_smem<KI, VALS, SEG, true>();
+      constexpr size_t smem_pref = onesweep_smem<KI, VALS, SEG, true, OUT>();
       static bool pref_set[kMaxDevices] = {};
       if (!pref_set[dev]) {
         cudaFuncSetAttribute(k_onesweep<KI, OUT, SEG, VALS, true, SRC, true>,
