@@ -745,6 +745,7 @@ int launch_blend(const BlendArgs& args, cudaStream_t s) {
     if (!bps_cache[dev]) {
       int bps = 0, sms = 0;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      set_carveout(k_blend16w<kBlendNP>);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_blend16w<kBlendNP>, 256, 0);
       sms_cache[dev] = sms > 0 ? sms : 148;
       bps_cache[dev] = bps > 0 ? bps : 1;

@@ -41,6 +41,20 @@ __host__ __device__ inline uint64_t pack_rect(uint32_t x0, uint32_t y0, uint32_t
 // area is 0 and its four coverage corners (K4c) cancel.
 constexpr uint64_t kEmptyRect = 1ull;  // pack_rect(1, 0, 0, 0)
 
+// Preferred shared-memory carveout (percent of the unified L1 / shared
+// storage) for the view pipeline's kernels; -1 keeps the driver's choice.
+// The streams' kernels co-reside on the SMs only when the SM's carveout fits
+// them all, so one consistent carveout can matter more than each kernel's own.
+#ifndef LMGS_CARVEOUT
+#define LMGS_CARVEOUT -1
+#endif
+template <typename F>
+inline void set_carveout(F* fn) {
+  if (LMGS_CARVEOUT >= 0)
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                         cudaFuncAttributePreferredSharedMemoryCarveout, LMGS_CARVEOUT);
+}
+
 // Per-device launch caches (function attributes are per device context).
 constexpr int kMaxDevices = 64;
 inline int current_device() {

@@ -433,6 +433,7 @@ int launch_preprocess_multi(const PreprocessMulti& m, cudaStream_t s) {
     const int slot = (m.nv - 1) * 2 + (loop && m.nv <= 4 ? 1 : 0);
     if (smem > set[slot][dev]) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      set_carveout(kern);
       set[slot][dev] = smem;
     }
     PreprocessMulti mm = m;

@@ -774,6 +774,8 @@ void launch_pass(const PassArgs& a, int64_t blocks, cudaStream_t s) {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_onesweep<KI, OUT, SEG, VALS, true, SRC>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_carveout(k_onesweep<KI, OUT, SEG, VALS, false, SRC>);
+    set_carveout(k_onesweep<KI, OUT, SEG, VALS, true, SRC>);
     cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &occ[dev], k_onesweep<KI, OUT, SEG, VALS, true, SRC>, kSortThreads, smem);

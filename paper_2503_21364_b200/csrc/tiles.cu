@@ -668,6 +668,8 @@ int launch_depth_fixup(void* const* keys_slot, void* const* ids_slot, int64_t n,
                        const uint64_t* key64, const int64_t* prim_ids, cudaStream_t s) {
   if (n <= 1) return 0;
   const int64_t threads = (n + kFixupPer - 1) / kFixupPer;
+  static bool once = false;
+  if (!once) set_carveout(k_depth_fixup_w), set_carveout(k_depth_keys), once = true;
   if (LMGS_FIXUP_WARP)
     k_depth_fixup_w<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(keys_slot, ids_slot, n,
                                                                        key64, prim_ids);
@@ -688,6 +690,8 @@ int launch_emit(const EmitArgs& a, cudaStream_t s) {
     const int64_t p = (int64_t)sms[dev] * LMGS_EMIT_PERSIST_CTAS;
     if (grid > p) grid = p;
   }
+  static bool once = false;
+  if (!once) set_carveout(k_emit), once = true;
   k_emit<<<(unsigned)grid, kEmitThreads, 0, s>>>(a);
   return 1;
 }

@@ -280,6 +280,8 @@ int launch_touched_fix(const TouchedFixArgs& a, cudaStream_t s) {
 #ifndef LMGS_FIX_CTAS_PER_SM
 #define LMGS_FIX_CTAS_PER_SM (2048 / kFixThreads)
 #endif
+  static bool once = false;
+  if (!once) set_carveout(k_touched_fix), once = true;
   k_touched_fix<<<148 * LMGS_FIX_CTAS_PER_SM, kFixThreads, 0, s>>>(a);
   return 1;
 }
