@@ -369,6 +369,9 @@ constexpr int kWarpsPerBlock16 = 8;
 #ifndef LMGS_BLEND_ID_AHEAD
 #define LMGS_BLEND_ID_AHEAD 1
 #endif
+#ifndef LMGS_BLEND_SMEM_FP64
+#define LMGS_BLEND_SMEM_FP64 0  // 1: hits' fp64 mean / r^2 staged in shared memory (6 KB per CTA)
+#endif
 #ifndef LMGS_BLEND_COMPACT
 #define LMGS_BLEND_COMPACT 0  // 1: 264 -> 295 M warp instructions, 807 -> 799 frames/s (profiles/r10/blend_compact_variants.txt)
 #endif
@@ -383,8 +386,10 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
   // per hit splat: {mx_local, my_local, qa, qb}, {qc, log2_alpha, r2_lo, r2_hi},
   // {r, g, b, z} side by side (one address per splat)
   __shared__ float4 s_rec[kWarpsPerBlock16][32][3];
+#if LMGS_BLEND_SMEM_FP64
   __shared__ double s_mx[kWarpsPerBlock16][32], s_my[kWarpsPerBlock16][32],
       s_r2[kWarpsPerBlock16][32];
+#endif
   __shared__ uint8_t s_lane[kWarpsPerBlock16][32];  // LMGS_BLEND_COMPACT: slot -> list lane
   constexpr int kItemsPerTile = 8 / NP;
   constexpr int kRows = 4 * NP;  // block height
@@ -539,9 +544,11 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
         s_rec[warp][slot][1] = make_float4(g2.x, g2.y, __double2float_rd(r2 - band),
                                            __double2float_ru(r2 + band));
         s_rec[warp][slot][2] = make_float4(g2.z, g2.w, g3.x, g3.y);
+#if LMGS_BLEND_SMEM_FP64
         s_mx[warp][slot] = mx;
         s_my[warp][slot] = my;
         s_r2[warp][slot] = r2;
+#endif
       }
       uint32_t m = __ballot_sync(0xffffffffu, hit);
       __syncwarp();
@@ -589,6 +596,9 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
           else contrib_bits += contrib;
         }
         if (__any_sync(0xffffffffu, any_rare)) {
+#if !LMGS_BLEND_SMEM_FP64
+          const uint32_t rare_id = __shfl_sync(0xffffffffu, cid, LMGS_BLEND_COMPACT ? s_lane[warp][k] : k);
+#endif
 #pragma unroll
           for (int q = 0; q < NP; ++q) {
             const float dy = ((float)ly[q] + 0.5f) - g.y;
@@ -608,9 +618,18 @@ __global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, 
               continue;
             }
             // guard band: the reference's fp64 circle test
-            const double ddx = ((double)(x0 + lx) + 0.5) - s_mx[warp][k];
-            const double ddy = ((double)(y0 + ly[q]) + 0.5) - s_my[warp][k];
-            if (!(__dadd_rn(__dmul_rn(ddx, ddx), __dmul_rn(ddy, ddy)) <= s_r2[warp][k])) continue;
+#if LMGS_BLEND_SMEM_FP64
+            const double gmx = s_mx[warp][k], gmy = s_my[warp][k], gr2 = s_r2[warp][k];
+#else
+            // (rare path: the splat's fp64 mean and r^2 come back from its
+            // record instead of 6 KB of shared staging per CTA)
+            const double2 gm = __ldg(reinterpret_cast<const double2*>(a.recs + rare_id));
+            const double gmx = gm.x, gmy = gm.y;
+            const double gr2 = __ldg(&a.recs[rare_id].r2);
+#endif
+            const double ddx = ((double)(x0 + lx) + 0.5) - gmx;
+            const double ddy = ((double)(y0 + ly[q]) + 0.5) - gmy;
+            if (!(__dadd_rn(__dmul_rn(ddx, ddx), __dmul_rn(ddy, ddy)) <= gr2)) continue;
             bool contrib = power > -1060.0f;
             if (!contrib && power >= -1080.0f)  // fp32 ex2 underflows first
               contrib = exp2((double)power) * (double)T[q] > 0.0;
