@@ -381,8 +381,13 @@ constexpr int kWarpsPerBlock16 = 8;
 #ifndef LMGS_BLEND_MINB
 #define LMGS_BLEND_MINB 4  // 4 x 256 threads per SM (64 registers): measured best
 #endif
+#ifdef LMGS_BLEND_MAXREG  // experiment: a register cap between the MINB steps
+#define LMGS_BLEND_BOUNDS __maxnreg__(LMGS_BLEND_MAXREG)
+#else
+#define LMGS_BLEND_BOUNDS __launch_bounds__(256, LMGS_BLEND_MINB)
+#endif
 template <int NP>
-__global__ void __launch_bounds__(256, LMGS_BLEND_MINB) k_blend16w(BlendArgs a, int n_items) {
+__global__ void LMGS_BLEND_BOUNDS k_blend16w(BlendArgs a, int n_items) {
   // per hit splat: {mx_local, my_local, qa, qb}, {qc, log2_alpha, r2_lo, r2_hi},
   // {r, g, b, z} side by side (one address per splat)
   __shared__ float4 s_rec[kWarpsPerBlock16][32][3];
