@@ -43,6 +43,9 @@ constexpr int kWarps = kSortThreads / 32;
 #ifndef LMGS_SORT_SMEM_PAD
 #define LMGS_SORT_SMEM_PAD 0  // extra dynamic shared bytes per onesweep CTA (co-residency experiments)
 #endif
+#ifndef LMGS_RANK_SPLIT
+#define LMGS_RANK_SPLIT 1  // separate match / 16-bit count arrays (smaller shared footprint)
+#endif
 #ifndef LMGS_RANK_PAIRS
 #define LMGS_RANK_PAIRS 0  // 1: two items per round with {count, matchA, matchB} words: 692 vs 815 frames/s (profiles/r10/rank_pairs_variants.txt)
 #endif
@@ -421,7 +424,15 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
 #else
   using RankWord = uint2;  // {count, match}
 #endif
+#if LMGS_RANK_SPLIT
+  // match words and 16-bit counts in separate arrays (12.3 KB, not 16.4)
+  __shared__ uint32_t s_mt[kWarps][kRadix + 1];
+  __shared__ uint16_t s_ct[kWarps][kRadix + 1];
+#define LMGS_WCOUNT(w, d) s_ct[w][d]
+#else
   __shared__ RankWord s_wm[kWarps][kRadix + 1];
+#define LMGS_WCOUNT(w, d) s_wm[w][d].x
+#endif
   __shared__ uint32_t s_hist[kRadix + 1];
   __shared__ uint32_t s_local_start[kRadix];
   __shared__ uint32_t s_global[kRadix];
@@ -519,7 +530,11 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   uint32_t my_dstart = 0;  // kSegLo: start of bucket tid of the previous pass
   if constexpr (SEG == kSegLo) my_dstart = plan->digit_start[a.lo_pass][tid];
   for (int i = tid; i < kWarps * (kRadix + 1); i += kSortThreads)
+#if LMGS_RANK_SPLIT
+    (&s_mt[0][0])[i] = 0u, (&s_ct[0][0])[i] = 0;
+#else
     (&s_wm[0][0])[i] = RankWord{};
+#endif
   s_hist[tid] = 0;  // kSortThreads == kRadix
   if (tid == 0) s_hist[kRadix] = 0;
 #pragma unroll
@@ -617,6 +632,25 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   TRACE(2)
 #endif
   const uint32_t lt = lanemask_lt();
+#if LMGS_RANK_SPLIT
+  uint32_t* my_mt = s_mt[warp];
+  uint16_t* my_ct = s_ct[warp];
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const uint32_t d = dg[j];
+    atomicOr(&my_mt[d], 1u << lane);
+    __syncwarp();
+    const uint32_t peers = my_mt[d], c = my_ct[d];
+    __syncwarp();
+    const uint32_t below = peers & lt;
+    if (below == 0) {
+      my_ct[d] = (uint16_t)(c + __popc(peers));
+      my_mt[d] = 0u;
+    }
+    dg[j] |= (c + __popc(below)) << 16;
+    __syncwarp();
+  }
+#else
   RankWord* my = s_wm[warp];
 #if LMGS_RANK_PAIRS
   // two items per round, each with its own match half: item j + 1's rank
@@ -651,6 +685,7 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
     __syncwarp();
   }
 #endif
+#endif
   if (LMGS_LOOKBACK_LATE == 1) look_back();
   if constexpr (PREF) {
     // the next tile, claimed once this one has published its prefix: its
@@ -669,16 +704,16 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
     uint32_t run = s_local_start[d];
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
-      const uint32_t c = s_wm[w][d].x;
-      s_wm[w][d].x = run;
+      const uint32_t c = LMGS_WCOUNT(w, d);
+      LMGS_WCOUNT(w, d) = run;
       run += c;
     }
     if (tid == 0) {
       run = (uint32_t)count;
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) {
-        const uint32_t c = s_wm[w][kRadix].x;
-        s_wm[w][kRadix].x = run;
+        const uint32_t c = LMGS_WCOUNT(w, kRadix);
+        LMGS_WCOUNT(w, kRadix) = run;
         run += c;
       }
     }
@@ -686,7 +721,7 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
-    const uint32_t p = (dg[j] >> 16) + my[dg[j] & 0xffffu].x;
+    const uint32_t p = (dg[j] >> 16) + LMGS_WCOUNT(warp, dg[j] & 0xffffu);
     if constexpr (kPackedStage) {
       s_pk[p] = out_key<KI, OUT>(key[j], a);
       s_dg8[p] = (uint8_t)dg[j];
