@@ -43,6 +43,9 @@ constexpr int kWarps = kSortThreads / 32;
 #ifndef LMGS_SORT_SMEM_PAD
 #define LMGS_SORT_SMEM_PAD 0  // extra dynamic shared bytes per onesweep CTA (co-residency experiments)
 #endif
+#ifndef LMGS_SORT_IOTA16
+#define LMGS_SORT_IOTA16 1  // the first pass stages implicit values as 16-bit positions
+#endif
 #ifndef LMGS_RANK_SPLIT
 #define LMGS_RANK_SPLIT 1  // separate match / 16-bit count arrays (smaller shared footprint)
 #endif
@@ -206,7 +209,10 @@ enum : int { kOutSame = 0, kOutIds = 1, kOutPacked = 2 };
 enum : int { kSegNone = 0, kSegKey = 1, kSegLo = 2 };
 // Where a pass's keys come from: the input buffer, or generated from the rank
 // records of the visible splats (fused emission, tile_sort_fused).
-enum : int { kSrcKeys = 0, kSrcEmit = 1 };
+// kSrcIota: keys from the input, values implicit (input index) and staged as
+// 16-bit tile positions (2 B, not 4, per key): the first pass of a sort with
+// iota_vals, whose pass 0 is the first active one whenever it moves data
+enum : int { kSrcKeys = 0, kSrcEmit = 1, kSrcIota = 2 };
 
 struct PassArgs {
   void* keys[2];  // ping-pong buffers, each large enough for n keys of the wider format
@@ -414,6 +420,9 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   uint32_t* s_pk = reinterpret_cast<uint32_t*>(smem_raw);
   uint8_t* s_dg8 = reinterpret_cast<uint8_t*>(smem_raw + sizeof(uint32_t) * kSortTile);
   uint32_t* s_vals = reinterpret_cast<uint32_t*>(smem_raw + sizeof(KI) * kSortTile);
+  constexpr bool kIota16 = SRC == kSrcIota;
+  static_assert(!kIota16 || (VALS && kSortTile <= 65536), "16-bit implicit values");
+  uint16_t* s_idx16 = reinterpret_cast<uint16_t*>(smem_raw + sizeof(KI) * kSortTile);
   // kSegLo: the staged keys' low tile digits (the vals slot: kSegLo has none)
   uint8_t* s_lo = reinterpret_cast<uint8_t*>(smem_raw + sizeof(KI) * kSortTile);
   __shared__ uint32_t s_dstart[SEG == kSegLo ? kRadix : 1];
@@ -426,7 +435,9 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
 #endif
 #if LMGS_RANK_SPLIT
   // match words and 16-bit counts in separate arrays (12.3 KB, not 16.4)
+#if LMGS_RANK_SPLIT == 1
   __shared__ uint32_t s_mt[kWarps][kRadix + 1];
+#endif
   __shared__ uint16_t s_ct[kWarps][kRadix + 1];
 #define LMGS_WCOUNT(w, d) s_ct[w][d]
 #else
@@ -451,7 +462,7 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   const int shift = a.shift;
   // PREF input buffers after the staging (and its vals / low digits)
   constexpr size_t kStageBytes = (kPackedStage ? 5 * (size_t)kSortTile : sizeof(KI) * kSortTile) +
-                                 (VALS ? sizeof(uint32_t) * kSortTile : 0) +
+                                 (VALS ? (kIota16 ? 2 : 4) * (size_t)kSortTile : 0) +
                                  (SEG == kSegLo ? kSortTile : 0);
   constexpr size_t kInBytes = sizeof(KI) * kSortTile + (VALS ? sizeof(uint32_t) * kSortTile : 0);
   __shared__ __align__(8) uint64_t s_bar[PREF ? 2 : 1];
@@ -500,7 +511,7 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   TRACE(0)
 
   KI key[kSortItems];
-  uint32_t val[VALS ? kSortItems : 1];
+  uint32_t val[VALS && !kIota16 ? kSortItems : 1];
   uint32_t dg[kSortItems];  // digit (kRadix: invalid), then | rank in the warp << 16
   uint32_t lo_info = 0;  // kSegLo: the tile's first low digit | inner bucket starts << 16
   const int wbase = warp * 32 * kSortItems;
@@ -515,7 +526,7 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
     for (int j = 0; j < kSortItems; ++j) {
       const int i = wbase + j * 32 + lane;
       key[j] = sk[i];
-      if (VALS) val[j] = iota ? (uint32_t)(base + i) : sv[i];
+      if (VALS && !kIota16) val[j] = iota ? (uint32_t)(base + i) : sv[i];
     }
     fence_proxy_async_smem();  // these reads before the buffer's next TMA fill
   } else {
@@ -523,7 +534,7 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
     for (int j = 0; j < kSortItems; ++j) {
       const int i = wbase + j * 32 + lane;
       key[j] = i < count ? kin[base + i] : (KI)~(KI)0;
-      if (VALS) val[j] = iota ? (uint32_t)(base + i) : (i < count ? vin[base + i] : 0u);
+      if (VALS && !kIota16) val[j] = iota ? (uint32_t)(base + i) : (i < count ? vin[base + i] : 0u);
     }
   }
   // the loads above are in flight while the ranking state is cleared
@@ -531,7 +542,12 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   if constexpr (SEG == kSegLo) my_dstart = plan->digit_start[a.lo_pass][tid];
   for (int i = tid; i < kWarps * (kRadix + 1); i += kSortThreads)
 #if LMGS_RANK_SPLIT
-    (&s_mt[0][0])[i] = 0u, (&s_ct[0][0])[i] = 0;
+  {
+#if LMGS_RANK_SPLIT == 1
+    (&s_mt[0][0])[i] = 0u;
+#endif
+    (&s_ct[0][0])[i] = 0;
+  }
 #else
     (&s_wm[0][0])[i] = RankWord{};
 #endif
@@ -633,19 +649,28 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
 #endif
   const uint32_t lt = lanemask_lt();
 #if LMGS_RANK_SPLIT
+#if LMGS_RANK_SPLIT == 1
   uint32_t* my_mt = s_mt[warp];
+#endif
   uint16_t* my_ct = s_ct[warp];
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const uint32_t d = dg[j];
+#if LMGS_RANK_SPLIT == 1
     atomicOr(&my_mt[d], 1u << lane);
     __syncwarp();
     const uint32_t peers = my_mt[d], c = my_ct[d];
+#else
+    // experiment: MATCH.ANY instead of the shared match words (8 KB less per CTA)
+    const uint32_t peers = __match_any_sync(~0u, d), c = my_ct[d];
+#endif
     __syncwarp();
     const uint32_t below = peers & lt;
     if (below == 0) {
       my_ct[d] = (uint16_t)(c + __popc(peers));
+#if LMGS_RANK_SPLIT == 1
       my_mt[d] = 0u;
+#endif
     }
     dg[j] |= (c + __popc(below)) << 16;
     __syncwarp();
@@ -728,7 +753,8 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
     } else {
       s_keys[p] = key[j];
     }
-    if (VALS) s_vals[p] = val[j];
+    if constexpr (kIota16) s_idx16[p] = (uint16_t)(wbase + j * 32 + lane);
+    else if (VALS) s_vals[p] = val[j];
     if constexpr (SEG == kSegLo) {
       // the key's input position's bucket: the tile's first one plus the
       // inner buckets (lo_first + 1 ..) starting at or before it
@@ -758,7 +784,8 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
     const KI k = s_keys[i];
     const uint32_t o = s_global[digit_of(k, shift)] + i;
     kout[o] = out_key<KI, OUT>(k, a);
-    if (VALS) vout[o] = s_vals[i];
+    if constexpr (kIota16) vout[o] = (uint32_t)base + s_idx16[i];
+    else if (VALS) vout[o] = s_vals[i];
     if (segs) {
       // the staged tile is sorted on every key bit sorted so far: runs of one
       // segment are contiguous; a run [i0, i1] adds (i1 + 1) - i0
@@ -789,18 +816,19 @@ __global__ void __launch_bounds__(kSortThreads, (sort_min_ctas<KI, VALS>()))
   }
 }
 
-template <typename KI, bool VALS, int SEG = kSegNone, bool PREF = false, int OUT = kOutSame>
+template <typename KI, bool VALS, int SEG = kSegNone, bool PREF = false, int OUT = kOutSame,
+          int SRC = kSrcKeys>
 constexpr size_t onesweep_smem() {
   return (((OUT == kOutPacked ? 5 * (size_t)kSortTile : sizeof(KI) * kSortTile) +
-           (VALS ? sizeof(uint32_t) * kSortTile : 0) + (SEG == kSegLo ? kSortTile : 0) + 15) &
+           (VALS ? (SRC == kSrcIota ? 2 : 4) * (size_t)kSortTile : 0) + (SEG == kSegLo ? kSortTile : 0) + 15) &
           ~(size_t)15) +
          (PREF ? 2 * (sizeof(KI) * kSortTile + (VALS ? sizeof(uint32_t) * kSortTile : 0)) : 0);
 }
 
 template <typename KI, int OUT, int SEG, bool VALS, int SRC = kSrcKeys>
 void launch_pass(const PassArgs& a, int64_t blocks, cudaStream_t s) {
-  constexpr size_t smem = onesweep_smem<KI, VALS, SEG, false, OUT>() + LMGS_SORT_SMEM_PAD;  // (pad: experiments)
-  static_assert(SRC == kSrcKeys || smem >= 2 * kSortTile, "the owner map aliases the staging");
+  constexpr size_t smem = onesweep_smem<KI, VALS, SEG, false, OUT, SRC>() + LMGS_SORT_SMEM_PAD;  // (pad: experiments)
+  static_assert(SRC != kSrcEmit || smem >= 2 * kSortTile, "the owner map aliases the staging");
   static bool attr_set[kMaxDevices] = {};
   static int occ[kMaxDevices] = {}, sms[kMaxDevices] = {};
   const int dev = current_device();
@@ -900,7 +928,9 @@ int radix_sort_impl(const RadixSortBuffers& b, int64_t n, int begin_bit, int n_p
   if (blocks == 0) return launched;
   for (int p = 0; p < n_passes; ++p) {
     const PassArgs a = pass_args(b, n, begin_bit + 8 * p, p, blocks);
-    if (b.vals[1]) launch_pass<K, kOutSame, kSegNone, true>(a, blocks, s);
+    if (b.vals[1] && b.iota_vals && p == 0 && LMGS_SORT_IOTA16)
+      launch_pass<K, kOutSame, kSegNone, true, kSrcIota>(a, blocks, s);
+    else if (b.vals[1]) launch_pass<K, kOutSame, kSegNone, true>(a, blocks, s);
     else if (b.seg_counts) launch_pass<K, kOutSame, kSegKey, false>(a, blocks, s);
     else launch_pass<K, kOutSame, kSegNone, false>(a, blocks, s);
   }
