@@ -253,7 +253,7 @@ struct EmitArgs {
 };
 int launch_emit_ranks(const EmitArgs& a, cudaStream_t s);
 #ifndef LMGS_EMIT_PERSIST_CTAS
-#define LMGS_EMIT_PERSIST_CTAS 0  // > 0: concurrent renders emit with this many CTAs per SM
+#define LMGS_EMIT_PERSIST_CTAS 4  // > 0: concurrent renders emit with this many CTAs per SM
 #endif
 inline int64_t emit_chunks(int64_t n_vis) { return (n_vis + kEmitChunk - 1) / kEmitChunk; }
 int launch_emit(const EmitArgs& a, cudaStream_t s);
