@@ -44,6 +44,9 @@ __device__ __forceinline__ void unpack_rect(uint64_t rect, int& x0, int& y0, int
 #ifndef LMGS_DEPTH_KEYS_U
 #define LMGS_DEPTH_KEYS_U 4
 #endif
+#ifndef LMGS_EMIT_HIST_LANE
+#define LMGS_EMIT_HIST_LANE 1  // K4's tile-digit histograms: per-lane increments for every digit
+#endif
 #ifndef LMGS_DEPTH_KEYS_CTAS_PER_SM
 #define LMGS_DEPTH_KEYS_CTAS_PER_SM 8
 #endif
@@ -382,10 +385,17 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(EmitArgs a) {
       else if ((dy + 1) * w <= q) ++dy;
       tile = (uint32_t)(y0 + (int)dy) * (uint32_t)a.tiles_x + (uint32_t)x0 + (q - dy * w);
       a.keys[out0 + p] = ((uint64_t)tile << 32) | id_i;
-      // the low digit differs across lanes (consecutive tiles of a row)
       atomicAdd(&s_hist[0][tile & 0xffu], 1u);
+#if LMGS_EMIT_HIST_LANE
+      // every digit by a per-lane increment: a window holds ~9 splats at
+      // random places (depth order), so even the high digits are warp-uniform
+      // in under 1% of windows (c3, ncu) and a vote-then-aggregate step costs
+      // more than it saves
+      for (int ps = 1; ps < passes; ++ps) atomicAdd(&s_hist[ps][(tile >> (8 * ps)) & 0xffu], 1u);
+#endif
     }
-    // higher digits are almost always warp-uniform: one aggregated add
+#if !LMGS_EMIT_HIST_LANE
+    // higher digits by one aggregated add when warp-uniform
     const uint32_t act = __ballot_sync(0xffffffffu, on);
     const int first = __ffs(act) - 1;
     for (int ps = 1; ps < passes; ++ps) {
@@ -397,6 +407,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(EmitArgs a) {
         atomicAdd(&s_hist[ps][dg], 1u);
       }
     }
+#endif
     // next window starts in the item holding slot p0 + 32
     const int idx31 = __shfl_sync(0xffffffffu, idx, 31);
     k0 += idx31 + (ends[k0 + idx31] == p0 + 32u ? 1 : 0);
