@@ -591,6 +591,7 @@ int view_finish(lmgs_context* c, const lmgs_gaussians* g, const lmgs_camera* cam
   // K7
   tm.begin(4);
   BlendArgs ba{};
+  ba.concurrent = (st->flags & LMGS_FLAG_CONCURRENT) != 0;
   ba.keys_slot = &sc->slots.inst_ids;
   ba.ranges = ranges;
   ba.recs = c->recs;

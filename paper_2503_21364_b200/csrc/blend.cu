@@ -378,6 +378,9 @@ constexpr int kWarpsPerBlock16 = 8;
 #ifndef LMGS_BLEND_PAIRS
 #define LMGS_BLEND_PAIRS 0  // 1: two hits per trip, one break vote per pair (777.6 vs 777.3 frames/s: neutral, profiles/r10)
 #endif
+#ifndef LMGS_BLEND_CONCURRENT_CTAS
+#define LMGS_BLEND_CONCURRENT_CTAS 2  // blend CTAs per SM under LMGS_FLAG_CONCURRENT (0: all)
+#endif
 #ifndef LMGS_BLEND_MINB
 #define LMGS_BLEND_MINB 4  // 4 x 256 threads per SM (64 registers): measured best
 #endif
@@ -777,7 +780,11 @@ int launch_blend(const BlendArgs& args, cudaStream_t s) {
 #ifdef LMGS_BLEND_CTAS_PER_SM  // experiment: leave room for other streams' kernels
     int grid = sms_cache[dev] * min(bps_cache[dev], LMGS_BLEND_CTAS_PER_SM);
 #else
-    int grid = sms_cache[dev] * bps_cache[dev];
+    // concurrent renders: fewer resident blend CTAs (each holds a quarter of
+    // the register file) so the other streams' kernels share the SMs
+    int grid = sms_cache[dev] *
+               (a.concurrent && LMGS_BLEND_CONCURRENT_CTAS > 0
+                    ? min(bps_cache[dev], LMGS_BLEND_CONCURRENT_CTAS) : bps_cache[dev]);
 #endif
     const int need = (items + kWarpsPerBlock16 - 1) / kWarpsPerBlock16;
     if (grid > need) grid = need;

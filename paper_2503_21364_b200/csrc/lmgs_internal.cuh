@@ -292,6 +292,7 @@ struct BlendArgs {
   int32_t* touched;
   int32_t* n_processed;
   int* work_counter;  // device scalar for the persistent 16x16 kernel (nullable)
+  bool concurrent;    // LMGS_FLAG_CONCURRENT: the persistent grid leaves room on each SM
   // strip targets (lmgs_render_strips): when n_strips > 0, pixel row y goes to
   // strip y / strip_rows at row y % strip_rows of srgb / strans / sdepth
   // (possibly peer-GPU pointers) instead of rgb / alpha / depth / trans
