@@ -58,12 +58,13 @@ C5_PER_BLOCK = 6_250_000
 # reported as `traffic` beside the algorithmic bytes.
 NCU_TRAFFIC_SOURCE = "profiles/r10/ncu_launch_table.txt"
 NCU_TRAFFIC = {
-    "preprocess": 2783.8e6 / 2,  # one k_preprocess_tma<2> launch serves two views
-    "depth_sort": 48.1e6 + 3 * 41.4e6 + 104.8e6,  # keys, 3 passes (concurrent grids), fix-up
-    "emit": 257.5e6,
-    "tile_sort": 222.8e6 + 123.4e6,  # u64 -> packed u32 pass, u32 -> ids pass
-    "blend": 163.5e6,
-    "touched_fix": 110.0e6,
+    "preprocess": 2784.0e6 / 2,  # one k_preprocess_tma<2> launch serves two views
+    # keys, 3 passes (concurrent grids; the first stages 16-bit implicit values), fix-up
+    "depth_sort": 48.1e6 + 24.5e6 + 2 * 50.2e6 + 104.9e6,
+    "emit": 258.4e6,
+    "tile_sort": 222.2e6 + 124.4e6,  # u64 -> packed u32 pass, u32 -> ids pass
+    "blend": 159.4e6,
+    "touched_fix": 110.3e6,
 }
 
 
