@@ -43,6 +43,9 @@ constexpr int kWarps = kSortThreads / 32;
 #ifndef LMGS_SORT_SMEM_PAD
 #define LMGS_SORT_SMEM_PAD 0  // extra dynamic shared bytes per onesweep CTA (co-residency experiments)
 #endif
+#ifndef LMGS_SORT_PERSIST_CTAS_VALS
+#define LMGS_SORT_PERSIST_CTAS_VALS LMGS_SORT_PERSIST_CTAS  // key-value (depth) sorts
+#endif
 #ifndef LMGS_SORT_IOTA16
 #define LMGS_SORT_IOTA16 1  // the first pass stages implicit values as 16-bit positions
 #endif
@@ -852,8 +855,8 @@ void launch_pass(const PassArgs& a, int64_t blocks, cudaStream_t s) {
   // the key count is on the device: a persistent grid takes tiles by ticket
   // (concurrent streams: always, with LMGS_SORT_PERSIST_CTAS CTAs per SM,
   // leaving room for the other streams' kernels)
-  const int per_sm = a.concurrent && LMGS_SORT_PERSIST_CTAS > 0 && LMGS_SORT_PERSIST_CTAS < occ[dev]
-                         ? LMGS_SORT_PERSIST_CTAS : occ[dev];
+  constexpr int kPersist = VALS ? LMGS_SORT_PERSIST_CTAS_VALS : LMGS_SORT_PERSIST_CTAS;
+  const int per_sm = a.concurrent && kPersist > 0 && kPersist < occ[dev] ? kPersist : occ[dev];
   const int64_t persistent = (int64_t)sms[dev] * per_sm;
   const unsigned grid = (unsigned)(blocks < persistent ? blocks : persistent);
   if constexpr (SRC == kSrcKeys && LMGS_SORT_PREFETCH) {
